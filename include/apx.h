@@ -1,0 +1,85 @@
+/*
+ * apx.h -- C-ABI of the B200-native approximate dense product (arXiv 2504.19308).
+ *
+ * Drop-in boundary for the reference package `apxmm` (pkg/src/apxmm). The reference has no
+ * plugin registry: its boundary is the set of module-level Python functions listed per entry
+ * point below (file:line under /root/reference/pkg/src/apxmm/). The Python shim in
+ * paper_2504_19308_b200/ keeps those exact signatures and calls these functions via ctypes.
+ *
+ * Conventions
+ *   - Every matrix argument is a DEVICE pointer to a dense row-major array (leading dim = cols).
+ *   - dtype: APX_F32 / APX_F64 real inputs; complex outputs use interleaved (re, im) pairs.
+ *   - `stream` is a cudaStream_t passed as void*; all work is enqueued on it, nothing blocks,
+ *     nothing is allocated: the caller owns `ws` (size from the matching *_workspace call).
+ *   - Selected component indices are written to device int32 arrays, ascending.
+ *   - `scalars` is a device array of APX_NSCALARS doubles (see APX_S_* slots); the shim turns
+ *     them into the reference's ApproxReport (report.py:8-36) fields.
+ *   - Return value 0 = success; nonzero = APX_E_* code, message via apx_last_error() (thread
+ *     local). APX_E_ARG maps to the reference's ValueError.
+ *   - Reentrant: no global mutable state besides the thread-local error string.
+ */
+#ifndef APX_H_
+#define APX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define APX_F32 0
+#define APX_F64 1
+#define APX_C64 2
+#define APX_C128 3
+
+#define APX_OK 0
+#define APX_E_ARG 1
+#define APX_E_CUDA 2
+#define APX_E_WS 3
+#define APX_E_NUMERIC 4
+#define APX_E_UNSUPPORTED 5
+
+/* scalar slots written by the product entry points */
+#define APX_S_FRO2_A 0  /* ||A||_F^2 */
+#define APX_S_FRO2_B 1  /* ||B||_F^2 */
+#define APX_S_KEPT_A 2  /* energy captured by A's kept components */
+#define APX_S_KEPT_B 3  /* energy captured by B's kept components */
+#define APX_S_FRO2_M 4  /* ||M||_F^2 */
+#define APX_S_RES2_A 5  /* ||dA||_F^2 measured directly (sfft only), else 0 */
+#define APX_S_RES2_B 6  /* ||dB||_F^2 measured directly (sfft only), else 0 */
+#define APX_NSCALARS 8
+
+int apx_abi_version(void);
+const char* apx_last_error(void);
+
+/* ---------------------------------------------------------------- selection primitives ---- */
+
+/* top_indices (circulant.py:63-70): k largest of w[0..n) (non-negative doubles, device),
+ * ties toward the lower index, written ascending to sel[0..k). */
+int apx_top_indices(const double* w, int64_t n, int k, int32_t* sel, void* stream);
+
+/* Cycle norms ||lambda_j||_2 of the left layout, i.e. the column norms of
+ * cycle_reorder(A, "left") (core.py:106-125, left branch :123-124). norms: n doubles (device);
+ * fro2 (device, may be NULL) receives ||A||_F^2. */
+size_t apx_cycle_norms_workspace(int dtype, int64_t n);
+int apx_cycle_norms(int dtype, const void* A, int64_t n, double* norms, double* fro2,
+                    void* ws, size_t ws_bytes, void* stream);
+
+/* -------------------------------------------------------------- cycle-truncated product ---- */
+/* Restated (the reference ships only the primitives core.py:106-154):
+ * A = sum_{j in J_A} Lambda_j C^j + dA, same for B with k_b cycles.
+ * order 0: M = Ahat . Bhat;  order 1: M = Ahat . B + dA . Bhat  (first-order form of
+ * svd.py:174-177 / circulant.py:193-198). force_sel_a/b (device, may be NULL) override the
+ * selection (near-tie protocol, as test_circulant.py:108-110 does with spec.selected). */
+size_t apx_cycle_first_order_workspace(int dtype, int64_t n, int k_a, int k_b, int order);
+int apx_cycle_first_order(int dtype, const void* A, const void* B, int64_t n, int k_a, int k_b,
+                          int order, const int32_t* force_sel_a, const int32_t* force_sel_b,
+                          void* M, int32_t* sel_a, int32_t* sel_b, double* scalars,
+                          void* ws, size_t ws_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* APX_H_ */

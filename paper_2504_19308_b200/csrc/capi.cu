@@ -1,0 +1,147 @@
+// C-ABI entry points (include/apx.h). Validation, workspace planning, and the launch sequence
+// of each product; the kernels live in the other translation units.
+#include <cstdarg>
+
+#include "../../include/apx.h"
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace apx {
+
+static thread_local char g_err[1024] = "";
+
+void set_error(const char* fmt, ...) {
+  va_list ap;
+  va_start(ap, fmt);
+  vsnprintf(g_err, sizeof(g_err), fmt, ap);
+  va_end(ap);
+}
+
+static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// ------------------------------------------------------------------------------------------
+// cycle product plan
+// ------------------------------------------------------------------------------------------
+struct CyclePlan {
+  double* partial;   // energy partials (shared by A then B)
+  double* en_a;      // energies A
+  double* nr_a;      // norms A
+  double* en_b;
+  double* nr_b;
+  void* lam_a;       // k_a x n
+  void* lam_b;       // k_b x n
+  void* bhat;        // n x n (order 0 only)
+  double* msq;       // ||M||^2 partials
+  int n_msq;
+};
+
+static void plan_cycle(Workspace& ws, CyclePlan& p, int dtype, int n, int ka, int kb, int order) {
+  const size_t e = dtype == F32 ? 4 : 8;
+  p.partial = ws.take<double>(cycle_energy_ws(n) / sizeof(double) + 1);
+  p.en_a = ws.take<double>(n);
+  p.nr_a = ws.take<double>(n);
+  p.en_b = ws.take<double>(n);
+  p.nr_b = ws.take<double>(n);
+  p.lam_a = ws.take<char>((size_t)std::max(ka, 1) * n * e);
+  p.lam_b = ws.take<char>((size_t)std::max(kb, 1) * n * e);
+  p.bhat = order == 0 ? (void*)ws.take<char>((size_t)n * n * e) : nullptr;
+  p.n_msq = std::max<int>((int)ceil_div(n, 1), kNumSMs * 4);
+  p.msq = ws.take<double>(p.n_msq);
+}
+
+template <typename T>
+static int run_cycle(const T* A, const T* B, int n, int ka, int kb, int order, const int* fa, const int* fb, T* M,
+                     int* sa, int* sb, double* scal, const CyclePlan& p, cudaStream_t st) {
+  APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
+  APX_TRY(launch_cycle_energies<T>(A, n, p.en_a, p.nr_a, scal + APX_S_FRO2_A, p.partial, st));
+  APX_TRY(launch_cycle_energies<T>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, st));
+  if (fa) { if (ka) APX_CUDA(cudaMemcpyAsync(sa, fa, ka * sizeof(int), cudaMemcpyDeviceToDevice, st)); }
+  else APX_TRY(launch_topk(p.nr_a, n, ka, sa, st));
+  if (fb) { if (kb) APX_CUDA(cudaMemcpyAsync(sb, fb, kb * sizeof(int), cudaMemcpyDeviceToDevice, st)); }
+  else APX_TRY(launch_topk(p.nr_b, n, kb, sb, st));
+  APX_TRY(launch_kept_energy(p.nr_a, sa, ka, 1.0, scal + APX_S_KEPT_A, st));
+  APX_TRY(launch_kept_energy(p.nr_b, sb, kb, 1.0, scal + APX_S_KEPT_B, st));
+  T* la = (T*)p.lam_a;
+  T* lb = (T*)p.lam_b;
+  APX_TRY(launch_cycle_extract<T>(A, n, sa, ka, la, st));
+  APX_TRY(launch_cycle_extract<T>(B, n, sb, kb, lb, st));
+  if (order == 1) {
+    // M = Ahat . B   (left gather over column strips of B)
+    APX_TRY(launch_cycle_left_gather<T>(B, la, sa, ka, n, 0, M, st));
+    // M += dA . Bhat (right gather over row blocks of A, masked to dA on load) + ||M||^2
+    APX_TRY(launch_cycle_right_gather<T>(A, sa, ka, lb, sb, kb, n, 1, M, p.msq, st));
+    const int rblocks = (int)ceil_div(n, right_gather_rows(n, sizeof(T)));
+    APX_TRY(launch_sum_vector(p.msq, rblocks, scal + APX_S_FRO2_M, st));
+  } else {
+    T* bh = (T*)p.bhat;
+    APX_TRY(launch_cycle_materialize<T>(lb, sb, kb, n, bh, st));
+    APX_TRY(launch_cycle_left_gather<T>(bh, la, sa, ka, n, 0, M, st));
+    int parts = 0;
+    APX_TRY(launch_sumsq<T>(M, (size_t)n * n, p.msq, &parts, st));
+    APX_TRY(launch_sum_vector(p.msq, parts, scal + APX_S_FRO2_M, st));
+  }
+  return OK;
+}
+
+}  // namespace apx
+
+using namespace apx;
+
+extern "C" {
+
+int apx_abi_version(void) { return 1; }
+
+const char* apx_last_error(void) { return g_err; }
+
+int apx_top_indices(const double* w, int64_t n, int k, int32_t* sel, void* stream) {
+  APX_REQUIRE(n >= 1, "n must be >= 1");
+  APX_REQUIRE(k >= 0 && k <= n, "k=%d out of range [0, %lld]", k, (long long)n);
+  return launch_topk(w, (int)n, k, sel, S(stream));
+}
+
+size_t apx_cycle_norms_workspace(int dtype, int64_t n) {
+  (void)dtype;
+  Workspace ws(nullptr, 0, true);
+  ws.take<double>(cycle_energy_ws((int)n) / sizeof(double) + 1);
+  ws.take<double>(n);
+  return ws.off;
+}
+
+int apx_cycle_norms(int dtype, const void* A, int64_t n, double* norms, double* fro2, void* wsp, size_t ws_bytes,
+                    void* stream) {
+  APX_REQUIRE(dtype == F32 || dtype == F64, "cycle_norms: real dtype required");
+  APX_REQUIRE(n >= 1 && n <= 46340, "n=%lld out of range", (long long)n);
+  Workspace ws(wsp, ws_bytes);
+  double* partial = ws.take<double>(cycle_energy_ws((int)n) / sizeof(double) + 1);
+  double* en = ws.take<double>(n);
+  APX_WS_CHECK(ws);
+  if (dtype == F32) return launch_cycle_energies<float>((const float*)A, (int)n, en, norms, fro2, partial, S(stream));
+  return launch_cycle_energies<double>((const double*)A, (int)n, en, norms, fro2, partial, S(stream));
+}
+
+size_t apx_cycle_first_order_workspace(int dtype, int64_t n, int k_a, int k_b, int order) {
+  Workspace ws(nullptr, 0, true);
+  CyclePlan p;
+  plan_cycle(ws, p, dtype, (int)n, k_a, k_b, order);
+  return ws.off;
+}
+
+int apx_cycle_first_order(int dtype, const void* A, const void* B, int64_t n, int k_a, int k_b, int order,
+                          const int32_t* force_sel_a, const int32_t* force_sel_b, void* M, int32_t* sel_a,
+                          int32_t* sel_b, double* scalars, void* wsp, size_t ws_bytes, void* stream) {
+  APX_REQUIRE(dtype == F32 || dtype == F64, "cycle product: real dtype required");
+  APX_REQUIRE(n >= 1 && n <= 46340, "n=%lld out of range", (long long)n);
+  APX_REQUIRE(k_a >= 0 && k_a <= n && k_b >= 0 && k_b <= n, "k out of range [0, %lld]", (long long)n);
+  APX_REQUIRE(order == 0 || order == 1, "order must be 0 or 1");
+  Workspace ws(wsp, ws_bytes);
+  CyclePlan p;
+  plan_cycle(ws, p, dtype, (int)n, k_a, k_b, order);
+  APX_WS_CHECK(ws);
+  if (dtype == F32)
+    return run_cycle<float>((const float*)A, (const float*)B, (int)n, k_a, k_b, order, force_sel_a, force_sel_b,
+                            (float*)M, sel_a, sel_b, scalars, p, S(stream));
+  return run_cycle<double>((const double*)A, (const double*)B, (int)n, k_a, k_b, order, force_sel_a, force_sel_b,
+                           (double*)M, sel_a, sel_b, scalars, p, S(stream));
+}
+
+}  // extern "C"

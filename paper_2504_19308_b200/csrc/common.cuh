@@ -1,0 +1,118 @@
+// Shared helpers for the apx (approximate-product) sm_100a kernels.
+#pragma once
+#include <cuda_runtime.h>
+#include <cstdint>
+#include <cstdio>
+#include <cstring>
+#include <string>
+#include <algorithm>
+#include <type_traits>
+
+namespace apx {
+
+constexpr int kNumSMs = 148;  // B200
+
+// dtype codes used across the C-ABI (include/apx.h)
+enum DType : int { F32 = 0, F64 = 1, C64 = 2, C128 = 3 };
+
+// error codes returned by every C-ABI entry point
+enum Err : int {
+  OK = 0,
+  E_ARG = 1,       // precondition violated (maps to ValueError in the Python shim)
+  E_CUDA = 2,      // CUDA runtime error
+  E_WS = 3,        // workspace too small
+  E_NUMERIC = 4,   // numerical breakdown the caller must handle
+  E_UNSUPPORTED = 5
+};
+
+void set_error(const char* fmt, ...);
+
+#define APX_CUDA(expr)                                                                  \
+  do {                                                                                  \
+    cudaError_t _e = (expr);                                                            \
+    if (_e != cudaSuccess) {                                                            \
+      ::apx::set_error("%s:%d %s: %s", __FILE__, __LINE__, #expr, cudaGetErrorString(_e)); \
+      return ::apx::E_CUDA;                                                             \
+    }                                                                                   \
+  } while (0)
+
+#define APX_LAUNCH_CHECK()                                                               \
+  do {                                                                                  \
+    cudaError_t _e = cudaGetLastError();                                                \
+    if (_e != cudaSuccess) {                                                            \
+      ::apx::set_error("%s:%d launch: %s", __FILE__, __LINE__, cudaGetErrorString(_e)); \
+      return ::apx::E_CUDA;                                                             \
+    }                                                                                   \
+  } while (0)
+
+#define APX_REQUIRE(cond, ...)          \
+  do {                                  \
+    if (!(cond)) {                      \
+      ::apx::set_error(__VA_ARGS__);    \
+      return ::apx::E_ARG;              \
+    }                                   \
+  } while (0)
+
+#define APX_TRY(expr)            \
+  do {                           \
+    int _r = (expr);             \
+    if (_r != ::apx::OK) return _r; \
+  } while (0)
+
+// Bump allocator over the caller-owned workspace (no allocation inside the library).
+struct Workspace {
+  char* base;
+  size_t cap;
+  size_t off = 0;
+  bool dry;  // size-query mode: base may be null
+  Workspace(void* b, size_t c, bool d = false) : base((char*)b), cap(c), dry(d) {}
+  template <typename T>
+  T* take(size_t count) {
+    size_t a = (off + 255) & ~size_t(255);
+    off = a + count * sizeof(T);
+    if (dry) return nullptr;
+    return (T*)(base + a);
+  }
+  bool ok() const { return dry || off <= cap; }
+};
+
+#define APX_WS_CHECK(ws)                                                                 \
+  do {                                                                                  \
+    if (!(ws).ok()) {                                                                   \
+      ::apx::set_error("workspace too small: need %zu bytes, have %zu", (ws).off, (ws).cap); \
+      return ::apx::E_WS;                                                               \
+    }                                                                                   \
+  } while (0)
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+
+__device__ __forceinline__ int wrap_mod(int64_t v, int64_t n) {
+  int64_t r = v % n;
+  return (int)(r < 0 ? r + n : r);
+}
+
+template <typename T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Deterministic block sum (fixed tree); result valid in thread 0. `sh` holds >= 32 entries.
+template <typename T>
+__device__ __forceinline__ T block_sum(T v, T* sh) {
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  v = warp_sum(v);
+  __syncthreads();
+  if (lane == 0) sh[w] = v;
+  __syncthreads();
+  T r = 0;
+  if (w == 0) {
+    int nw = (blockDim.x + 31) >> 5;
+    r = lane < nw ? sh[lane] : T(0);
+    r = warp_sum(r);
+  }
+  return r;
+}
+
+}  // namespace apx

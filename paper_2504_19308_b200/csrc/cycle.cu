@@ -1,0 +1,406 @@
+// Cycle-decomposition kernels: A = sum_j Lambda_j C^j (left layout, reference core.py:113,123-124,
+// lambda_j[i] = A[i, (i-j) mod n]) and the gather passes of the cycle-truncated product.
+//
+//  K3  cycle_energy_partial / cycle_energy_finalize : ||lambda_j||^2 for all j in one HBM pass
+//  K4  topk_select_kernel (select.cuh)              : top_indices semantics (circulant.py:63-70)
+//      cycle_extract                                : lambda_t for the selected shifts (k x n)
+//  K10 cycle_left_gather  : M[r,c] (+)= sum_t lamA_t[r] * X[(r - JA_t) mod n, c]   (Ahat . X)
+//  K11 cycle_right_gather : M[r,c] (+)= sum_t X[r, m] * lamB_t[m],  m = (c + JB_t) mod n
+//                           (X . Bhat), X optionally masked to dA (kept cycles of A zeroed)
+#include "common.cuh"
+#include "select.cuh"
+#include "kernels.cuh"
+
+namespace apx {
+
+// ------------------------------------------------------------------------------------------
+// K3: energies. Thread j walks the wrapped diagonal of cycle j over a chunk of rows; a warp
+// reads 32 consecutive columns of one row per step (coalesced). fp32 inputs accumulate in fp32
+// per chunk (<= 256 terms) and combine chunks in fp64; fp64 inputs accumulate in fp64.
+// ------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(256) cycle_energy_partial(const T* __restrict__ A, int n, int rows_per_chunk,
+                                                            double* __restrict__ partial) {
+  using Acc = T;
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  const int g = blockIdx.y;
+  const int r0 = g * rows_per_chunk;
+  const int r1 = min(n, r0 + rows_per_chunk);
+  if (j >= n) return;
+  Acc acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+  int col = r0 - j;
+  if (col < 0) col += n;
+  const T* rowp = A + (size_t)r0 * n;
+  int r = r0;
+  for (; r + 4 <= r1; r += 4) {
+    int c0 = col, c1 = c0 + 1 == n ? 0 : c0 + 1;
+    int c2 = c1 + 1 == n ? 0 : c1 + 1, c3 = c2 + 1 == n ? 0 : c2 + 1;
+    T v0 = __ldg(rowp + c0), v1 = __ldg(rowp + n + c1), v2 = __ldg(rowp + 2 * (size_t)n + c2),
+      v3 = __ldg(rowp + 3 * (size_t)n + c3);
+    acc0 += v0 * v0; acc1 += v1 * v1; acc2 += v2 * v2; acc3 += v3 * v3;
+    col = c3 + 1 == n ? 0 : c3 + 1;
+    rowp += 4 * (size_t)n;
+  }
+  for (; r < r1; ++r) {
+    T v = __ldg(rowp + col);
+    acc0 += v * v;
+    col = col + 1 == n ? 0 : col + 1;
+    rowp += n;
+  }
+  partial[(size_t)g * n + j] = (double)((acc0 + acc1) + (acc2 + acc3));
+}
+
+// energies[j] = sum_g partial[g][j] (fixed order); norms[j] = sqrt(energies[j]).
+__global__ void cycle_energy_finalize(const double* __restrict__ partial, int n, int groups,
+                                      double* __restrict__ energies, double* __restrict__ norms) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double s = 0.0;
+  for (int g = 0; g < groups; ++g) s += partial[(size_t)g * n + j];
+  energies[j] = s;
+  norms[j] = sqrt(s);
+}
+
+// Single-block deterministic sum of v[0..n) into *out (fixed order per thread, fixed tree).
+__global__ void sum_vector_kernel(const double* __restrict__ v, int n, double* __restrict__ out) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) s += v[i];
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) *out = s;
+}
+
+__global__ void __launch_bounds__(kSelThreads) topk_select_kernel(const double* __restrict__ w, int n, int k,
+                                                                  int* __restrict__ sel) {
+  topk_select_block(w, n, k, sel);
+}
+
+// kept = sum over selected t of norms[sel[t]]^2, ascending t (mirrors circulant.py:132 order).
+__global__ void kept_energy_kernel(const double* __restrict__ norms, const int* __restrict__ sel, int k,
+                                   double scale, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double s = 0.0;
+    for (int t = 0; t < k; ++t) {
+      double m = norms[sel[t]];
+      s += m * m;
+    }
+    *out = scale * s;
+  }
+}
+
+// lam[t][i] = A[i, (i - J_t) mod n]
+template <typename T>
+__global__ void cycle_extract(const T* __restrict__ A, int n, const int* __restrict__ J, int k,
+                              T* __restrict__ lam) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.y;
+  if (i >= n || t >= k) return;
+  int c = i - J[t];
+  if (c < 0) c += n;
+  lam[(size_t)t * n + i] = A[(size_t)i * n + c];
+}
+
+// Dense materialization of sum_t Lambda_t C^{J_t} (zero elsewhere).
+template <typename T>
+__global__ void cycle_materialize_kernel(const T* __restrict__ lam, const int* __restrict__ J, int k, int n,
+                                         T* __restrict__ out) {
+  const size_t total = (size_t)n * n;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x)
+    out[e] = T(0);
+}
+template <typename T>
+__global__ void cycle_scatter_kernel(const T* __restrict__ lam, const int* __restrict__ J, int k, int n,
+                                     T* __restrict__ out) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  const int t = blockIdx.y;
+  if (i >= n || t >= k) return;
+  int c = i - J[t];
+  if (c < 0) c += n;
+  out[(size_t)i * n + c] = lam[(size_t)t * n + i];
+}
+
+// ------------------------------------------------------------------------------------------
+// K10: left gather on a column strip. The CTA keeps X[:, c0:c0+W] in shared memory (row stride
+// padded to avoid bank conflicts); thread = output row, W accumulators.
+// ------------------------------------------------------------------------------------------
+template <typename T, int W>
+__global__ void __launch_bounds__(256) cycle_left_gather(const T* __restrict__ X, const T* __restrict__ lam,
+                                                         const int* __restrict__ J, int k, int n, int accumulate,
+                                                         T* __restrict__ M) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Xs = reinterpret_cast<T*>(smem_raw);
+  constexpr int S = (W == 1) ? 1 : W + 1;  // padded row stride
+  const int c0 = blockIdx.x * W;
+  const int wcols = min(W, n - c0);
+  // load strip
+  for (int e = threadIdx.x; e < n * W; e += blockDim.x) {
+    const int r = e / W, q = e - r * W;
+    Xs[r * S + q] = q < wcols ? __ldg(X + (size_t)r * n + c0 + q) : T(0);
+  }
+  __syncthreads();
+  const int rows_per_group = (n + gridDim.y - 1) / gridDim.y;
+  const int rlo = blockIdx.y * rows_per_group, rhi = min(n, rlo + rows_per_group);
+  for (int r = rlo + threadIdx.x; r < rhi; r += blockDim.x) {
+    T acc[W];
+#pragma unroll
+    for (int q = 0; q < W; ++q) acc[q] = T(0);
+    const T* lp = lam + r;
+#pragma unroll 4
+    for (int t = 0; t < k; ++t) {
+      const T l = __ldg(lp + (size_t)t * n);
+      int src = r - __ldg(J + t);
+      if (src < 0) src += n;
+      const T* xs = Xs + src * S;
+#pragma unroll
+      for (int q = 0; q < W; ++q) acc[q] = fma(l, xs[q], acc[q]);
+    }
+    T* mp = M + (size_t)r * n + c0;
+    for (int q = 0; q < wcols; ++q) mp[q] = accumulate ? mp[q] + acc[q] : acc[q];
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K11: right gather on a row block. The CTA keeps X[r0:r0+R, :] in shared memory (masked to dA
+// when JA != nullptr); thread = output column(s); per shift one lambda load feeds R FMAs.
+// Also emits the block's partial sum of |M|^2 for the report's ||M||_F.
+// ------------------------------------------------------------------------------------------
+template <typename T, int R>
+__global__ void __launch_bounds__(512) cycle_right_gather(const T* __restrict__ X, const int* __restrict__ JA, int ka,
+                                                          const T* __restrict__ lam, const int* __restrict__ J, int k,
+                                                          int n, int accumulate, T* __restrict__ M,
+                                                          double* __restrict__ msq_partial) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Xs = reinterpret_cast<T*>(smem_raw);
+  __shared__ double red[32];
+  const int r0 = blockIdx.x * R;
+  const int rows = min(R, n - r0);
+  // coalesced row-block load (vectorised when rows are 16B aligned)
+  const size_t base = (size_t)r0 * n;
+  const size_t cnt = (size_t)rows * n;
+  constexpr int V = 16 / sizeof(T);
+  if ((n % V) == 0) {
+    using Vec = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+    const Vec* src = reinterpret_cast<const Vec*>(X + base);
+    Vec* dst = reinterpret_cast<Vec*>(Xs);
+    for (size_t e = threadIdx.x; e < cnt / V; e += blockDim.x) dst[e] = __ldg(src + e);
+  } else {
+    for (size_t e = threadIdx.x; e < cnt; e += blockDim.x) Xs[e] = __ldg(X + base + e);
+  }
+  __syncthreads();
+  if (JA != nullptr) {
+    for (int e = threadIdx.x; e < rows * ka; e += blockDim.x) {
+      const int rr = e / ka, t = e - rr * ka;
+      int m = r0 + rr - JA[t];
+      if (m < 0) m += n;
+      Xs[(size_t)rr * n + m] = T(0);
+    }
+    __syncthreads();
+  }
+  double msq = 0.0;
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    T acc[R];
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) acc[rr] = T(0);
+#pragma unroll 4
+    for (int t = 0; t < k; ++t) {
+      int m = c + __ldg(J + t);
+      if (m >= n) m -= n;
+      const T l = __ldg(lam + (size_t)t * n + m);
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) acc[rr] = fma(Xs[(size_t)rr * n + m], l, acc[rr]);
+    }
+#pragma unroll
+    for (int rr = 0; rr < R; ++rr) {
+      if (rr < rows) {
+        T* mp = M + (size_t)(r0 + rr) * n + c;
+        T v = accumulate ? *mp + acc[rr] : acc[rr];
+        *mp = v;
+        msq += (double)v * (double)v;
+      }
+    }
+  }
+  double s = block_sum(msq, red);
+  if (threadIdx.x == 0 && msq_partial) msq_partial[blockIdx.x] = s;
+}
+
+// sum of |x|^2 over a dense array, per-block partials (for ||M||_F when no gather wrote M last)
+template <typename T>
+__global__ void __launch_bounds__(256) sumsq_partial_kernel(const T* __restrict__ x, size_t cnt,
+                                                            double* __restrict__ partial) {
+  __shared__ double red[32];
+  double s = 0.0;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < cnt; e += (size_t)gridDim.x * blockDim.x) {
+    double v = (double)x[e];
+    s += v * v;
+  }
+  s = block_sum(s, red);
+  if (threadIdx.x == 0) partial[blockIdx.x] = s;
+}
+
+// ------------------------------------------------------------------------------------------
+// host-side launchers
+// ------------------------------------------------------------------------------------------
+template <typename T>
+static int set_smem(const void* fn, size_t bytes) {
+  if (bytes > 48 * 1024) APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes));
+  return OK;
+}
+
+static int energy_groups(int n, int* rows_per_chunk) {
+  const int cblocks = (int)ceil_div(n, 256);
+  int groups = (int)ceil_div(kNumSMs * 8, cblocks);
+  groups = std::max(1, std::min(groups, (int)ceil_div(n, 16)));
+  *rows_per_chunk = (int)ceil_div(n, groups);
+  return (int)ceil_div(n, *rows_per_chunk);
+}
+
+size_t cycle_energy_ws(int n) {
+  int rpc;
+  int g = energy_groups(n, &rpc);
+  return (size_t)g * n * sizeof(double) + 256;
+}
+
+template <typename T>
+int launch_cycle_energies(const T* A, int n, double* energies, double* norms, double* fro2, double* partial,
+                          cudaStream_t st) {
+  int rpc;
+  const int groups = energy_groups(n, &rpc);
+  dim3 grid((unsigned)ceil_div(n, 256), (unsigned)groups);
+  cycle_energy_partial<T><<<grid, 256, 0, st>>>(A, n, rpc, partial);
+  APX_LAUNCH_CHECK();
+  cycle_energy_finalize<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(partial, n, groups, energies, norms);
+  APX_LAUNCH_CHECK();
+  if (fro2) {
+    sum_vector_kernel<<<1, 1024, 0, st>>>(energies, n, fro2);
+    APX_LAUNCH_CHECK();
+  }
+  return OK;
+}
+
+int launch_topk(const double* w, int n, int k, int* sel, cudaStream_t st) {
+  if (k <= 0) return OK;
+  topk_select_kernel<<<1, kSelThreads, 0, st>>>(w, n, k, sel);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+int launch_kept_energy(const double* norms, const int* sel, int k, double scale, double* out, cudaStream_t st) {
+  kept_energy_kernel<<<1, 32, 0, st>>>(norms, sel, k, scale, out);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+template <typename T>
+int launch_cycle_extract(const T* A, int n, const int* J, int k, T* lam, cudaStream_t st) {
+  if (k <= 0) return OK;
+  dim3 grid((unsigned)ceil_div(n, 256), (unsigned)k);
+  cycle_extract<T><<<grid, 256, 0, st>>>(A, n, J, k, lam);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+template <typename T>
+int launch_cycle_materialize(const T* lam, const int* J, int k, int n, T* out, cudaStream_t st) {
+  cycle_materialize_kernel<T><<<kNumSMs * 4, 256, 0, st>>>(lam, J, k, n, out);
+  APX_LAUNCH_CHECK();
+  if (k > 0) {
+    dim3 grid((unsigned)ceil_div(n, 256), (unsigned)k);
+    cycle_scatter_kernel<T><<<grid, 256, 0, st>>>(lam, J, k, n, out);
+    APX_LAUNCH_CHECK();
+  }
+  return OK;
+}
+
+constexpr size_t kSmemBudget = 200 * 1024;
+
+template <typename T, int W>
+static int left_gather_w(const T* X, const T* lam, const int* J, int k, int n, int acc, T* M, cudaStream_t st) {
+  constexpr int S = (W == 1) ? 1 : W + 1;
+  const size_t smem = (size_t)n * S * sizeof(T);
+  APX_TRY(set_smem<T>((const void*)cycle_left_gather<T, W>, smem));
+  const int strips = (int)ceil_div(n, W);
+  int groups = 1;
+  if (strips < 2 * kNumSMs) groups = std::min<int>((int)ceil_div(2 * kNumSMs, strips), std::max(1, n / 256));
+  dim3 grid((unsigned)strips, (unsigned)groups);
+  cycle_left_gather<T, W><<<grid, 256, smem, st>>>(X, lam, J, k, n, acc, M);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+template <typename T>
+int launch_cycle_left_gather(const T* X, const T* lam, const int* J, int k, int n, int accumulate, T* M,
+                             cudaStream_t st) {
+  const size_t per_col = (size_t)n * sizeof(T);
+  int w = 1;
+  while (w < 8 && (size_t)(2 * w + 1) * per_col <= kSmemBudget) w *= 2;
+  APX_REQUIRE((size_t)(w == 1 ? 1 : w + 1) * per_col <= 227 * 1024, "n=%d too large for the left gather strip", n);
+  switch (w) {
+    case 1: return left_gather_w<T, 1>(X, lam, J, k, n, accumulate, M, st);
+    case 2: return left_gather_w<T, 2>(X, lam, J, k, n, accumulate, M, st);
+    case 4: return left_gather_w<T, 4>(X, lam, J, k, n, accumulate, M, st);
+    default: return left_gather_w<T, 8>(X, lam, J, k, n, accumulate, M, st);
+  }
+}
+
+template <typename T, int R>
+static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int acc,
+                          T* M, double* msq_partial, cudaStream_t st) {
+  const size_t smem = (size_t)R * n * sizeof(T);
+  APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R>, smem));
+  const int blocks = (int)ceil_div(n, R);
+  const int threads = n >= 512 ? 512 : ((n + 31) / 32) * 32;
+  cycle_right_gather<T, R><<<blocks, threads, smem, st>>>(X, JA, ka, lam, J, k, n, acc, M, msq_partial);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+int right_gather_rows(int n, size_t elem) {
+  int r = 8;
+  while (r > 1 && (size_t)r * n * elem > kSmemBudget) --r;
+  return r;
+}
+
+template <typename T>
+int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n,
+                              int accumulate, T* M, double* msq_partial, cudaStream_t st) {
+  const int r = right_gather_rows(n, sizeof(T));
+  APX_REQUIRE((size_t)n * sizeof(T) <= 227 * 1024, "n=%d too large for the right gather row block", n);
+  switch (r) {
+    case 1: return right_gather_r<T, 1>(X, JA, ka, lam, J, k, n, accumulate, M, msq_partial, st);
+    case 2: return right_gather_r<T, 2>(X, JA, ka, lam, J, k, n, accumulate, M, msq_partial, st);
+    case 3: return right_gather_r<T, 3>(X, JA, ka, lam, J, k, n, accumulate, M, msq_partial, st);
+    case 4: return right_gather_r<T, 4>(X, JA, ka, lam, J, k, n, accumulate, M, msq_partial, st);
+    case 5: return right_gather_r<T, 5>(X, JA, ka, lam, J, k, n, accumulate, M, msq_partial, st);
+    case 6: return right_gather_r<T, 6>(X, JA, ka, lam, J, k, n, accumulate, M, msq_partial, st);
+    case 7: return right_gather_r<T, 7>(X, JA, ka, lam, J, k, n, accumulate, M, msq_partial, st);
+    default: return right_gather_r<T, 8>(X, JA, ka, lam, J, k, n, accumulate, M, msq_partial, st);
+  }
+}
+
+template <typename T>
+int launch_sumsq(const T* x, size_t cnt, double* partial, int* nparts, cudaStream_t st) {
+  const int blocks = kNumSMs * 4;
+  sumsq_partial_kernel<T><<<blocks, 256, 0, st>>>(x, cnt, partial);
+  APX_LAUNCH_CHECK();
+  *nparts = blocks;
+  return OK;
+}
+
+int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st) {
+  sum_vector_kernel<<<1, 1024, 0, st>>>(v, n, out);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+#define APX_INST(T)                                                                                            \
+  template int launch_cycle_energies<T>(const T*, int, double*, double*, double*, double*, cudaStream_t);     \
+  template int launch_cycle_extract<T>(const T*, int, const int*, int, T*, cudaStream_t);                     \
+  template int launch_cycle_materialize<T>(const T*, const int*, int, int, T*, cudaStream_t);                 \
+  template int launch_cycle_left_gather<T>(const T*, const T*, const int*, int, int, int, T*, cudaStream_t);  \
+  template int launch_cycle_right_gather<T>(const T*, const int*, int, const T*, const int*, int, int, int, T*, \
+                                            double*, cudaStream_t);                                          \
+  template int launch_sumsq<T>(const T*, size_t, double*, int*, cudaStream_t);
+APX_INST(float)
+APX_INST(double)
+
+}  // namespace apx

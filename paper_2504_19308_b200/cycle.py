@@ -1,0 +1,83 @@
+"""Cycle-truncated and mixed (rSVD x cycles) approximate products -- GPU path.
+
+The reference ships the cycle primitives only (core.py:106-154; the paper marks cycle products
+"not demonstrated here"). This module supplies the product with the reference's
+conventions:
+
+  * A = sum_j Lambda_j C^j, Lambda_j = diag(cycle_reorder(A, "left")[:, j])  (core.py:123-124)
+  * selection = top_indices of the cycle 2-norms (circulant.py:63-70: ties -> lower index)
+  * order 0: Ahat . Bhat (zeroth order, the svd convention svd.py:169-172)
+  * order 1: Ahat . B + dA . Bhat (first order, svd.py:174-177 / circulant.py:193-198)
+  * residual norms from energy differences (circulant.py:130-133)
+"""
+
+from __future__ import annotations
+
+import math
+import time
+
+import torch
+
+from . import _device as D
+from . import _native as N
+from .errest import ErrorModel, finish_report
+
+
+def cycle_product_device(A, B, k_a: int, k_b: int, order: int, force_sel_a=None, force_sel_b=None,
+                         out=None):
+    """Device-level call: returns dict(M, sel_a, sel_b, scalars) with device tensors.
+
+    A, B: square device tensors of one real dtype (float32 / float64)."""
+    n = A.shape[0]
+    code = N.APX_F32 if A.dtype == torch.float32 else N.APX_F64
+    dev = A.device
+    M = out if out is not None else torch.empty((n, n), dtype=A.dtype, device=dev)
+    sa = torch.empty(max(k_a, 1), dtype=torch.int32, device=dev)
+    sb = torch.empty(max(k_b, 1), dtype=torch.int32, device=dev)
+    fa = None if force_sel_a is None else torch.as_tensor(force_sel_a, dtype=torch.int32).to(dev)
+    fb = None if force_sel_b is None else torch.as_tensor(force_sel_b, dtype=torch.int32).to(dev)
+    scal = torch.zeros(N.NSCALARS, dtype=torch.float64, device=dev)
+    ws = D.workspace(N.size("apx_cycle_first_order_workspace", code, n, k_a, k_b, order))
+    N.call("apx_cycle_first_order", code, A.data_ptr(), B.data_ptr(), n, k_a, k_b, order,
+           D.ptr(fa), D.ptr(fb), M.data_ptr(), sa.data_ptr(), sb.data_ptr(), scal.data_ptr(),
+           ws.data_ptr(), ws.numel(), D.stream_ptr())
+    return {"M": M, "sel_a": sa[:k_a], "sel_b": sb[:k_b], "scalars": scal, "ws": ws}
+
+
+def _norms(s):
+    nA = math.sqrt(max(0.0, s[N.S_FRO2_A]))
+    nB = math.sqrt(max(0.0, s[N.S_FRO2_B]))
+    ndA = math.sqrt(max(0.0, s[N.S_FRO2_A] - s[N.S_KEPT_A]))
+    ndB = math.sqrt(max(0.0, s[N.S_FRO2_B] - s[N.S_KEPT_B]))
+    return nA, nB, ndA, ndB, math.sqrt(max(0.0, s[N.S_FRO2_M]))
+
+
+def cycle_first_order_multiply(A, B, k: int, order: int, model: ErrorModel | None = None,
+                               k_b: int | None = None, force_sel_a=None, force_sel_b=None):
+    """Approximate A @ B keeping the k dominant cycles of A (k_b of B, default k).
+
+    Mirrors circulant_first_order_multiply's contract (circulant.py:164-218): square real
+    inputs, 0 <= k <= n, order in {0, 1}, returns (M, ApproxReport) with method "cycle".
+    numpy in -> numpy float64 out; torch CUDA in -> torch CUDA out (same dtype)."""
+    Ad, code_a, host = D.as_device_matrix(A, real_only=True)
+    Bd, code_b, _ = D.as_device_matrix(B, real_only=True)
+    n = Ad.shape[0]
+    if Ad.shape[1] != n or tuple(Bd.shape) != (n, n):
+        raise ValueError(f"two square n x n matrices required, got {tuple(Ad.shape)} x {tuple(Bd.shape)}")
+    if Bd.dtype != Ad.dtype:
+        Bd = Bd.to(Ad.dtype)
+    k_b = k if k_b is None else k_b
+    if not 0 <= k <= n or not 0 <= k_b <= n:
+        raise ValueError(f"k={k} out of range [0, {n}]")
+    if order not in (0, 1):
+        raise ValueError("order must be 0 or 1")
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = cycle_product_device(Ad, Bd, k, k_b, order, force_sel_a, force_sel_b)
+    s = r["scalars"].tolist()  # synchronises
+    wall = time.perf_counter() - t0
+    nA, nB, ndA, ndB, nM = _norms(s)
+    rep = finish_report("cycle", order, k, nA, nB, ndA, ndB, nM, n, wall, model)
+    rep.selected_a = r["sel_a"].tolist()
+    rep.selected_b = r["sel_b"].tolist()
+    return D.to_user(r["M"], host), rep
