@@ -78,6 +78,19 @@ int apx_cycle_first_order(int dtype, const void* A, const void* B, int64_t n, in
                           void* M, int32_t* sel_a, int32_t* sel_b, double* scalars,
                           void* ws, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------- mixed rSVD x cycles ---- */
+/* Config C4 (restated): A by the randomized range finder of
+ * randomized_partial_svd (svd.py:83-119) with l = k_svd sketch columns, q power iterations and
+ * the caller's Gaussian sketch omega (n x l, device, drawn by the host exactly as svd.py:105-106
+ * does, from default_rng([seed, 0]) -- svd.py:161); B by its k_cyc dominant cycles.
+ * order 1: M = Ahat.B + dA.Bhat, evaluated as Q(Q^T A . dB) + A.Bhat; order 0: M = Ahat.Bhat.
+ * flags bit 0: fp32 GEMMs as 3xTF32 (default single-pass TF32). APX_S_KEPT_A = sum sigma^2. */
+size_t apx_mixed_first_order_workspace(int dtype, int64_t n, int k_svd, int k_cyc, int order);
+int apx_mixed_first_order(int dtype, const void* A, const void* B, int64_t n, int k_svd, int k_cyc,
+                          int order, int power_iterations, const void* omega,
+                          const int32_t* force_sel_b, int flags, void* M, int32_t* sel_b,
+                          double* scalars, void* ws, size_t ws_bytes, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -69,7 +69,7 @@ static int run_cycle(const T* A, const T* B, int n, int ka, int kb, int order, c
     // M = Ahat . B   (left gather over column strips of B)
     APX_TRY(launch_cycle_left_gather<T>(B, la, sa, ka, n, 0, M, st));
     // M += dA . Bhat (right gather over row blocks of A, masked to dA on load) + ||M||^2
-    APX_TRY(launch_cycle_right_gather<T>(A, sa, ka, lb, sb, kb, n, 1, M, p.msq, st));
+    APX_TRY(launch_cycle_right_gather<T>(A, sa, ka, lb, sb, kb, n, n, 1, M, p.msq, nullptr, st));
     const int rblocks = (int)ceil_div(n, right_gather_rows(n, sizeof(T)));
     APX_TRY(launch_sum_vector(p.msq, rblocks, scal + APX_S_FRO2_M, st));
   } else {
@@ -79,6 +79,99 @@ static int run_cycle(const T* A, const T* B, int n, int ka, int kb, int order, c
     int parts = 0;
     APX_TRY(launch_sumsq<T>(M, (size_t)n * n, p.msq, &parts, st));
     APX_TRY(launch_sum_vector(p.msq, parts, scal + APX_S_FRO2_M, st));
+  }
+  return OK;
+}
+
+// ------------------------------------------------------------------------------------------
+// mixed product plan: A by rSVD (l = k_svd columns, q power iterations), B by k_cyc cycles.
+//   order 1:  M = Q (Bm . dB) + A . Bhat      (== Ahat.B + dA.Bhat, Ahat = Q Q^T A = Q Bm)
+//   order 0:  M = Q (Bm . Bhat)               (== Ahat . Bhat)
+// Only the projector Q Q^T enters M when l = k, so no small SVD is needed;
+// sum sigma^2 = ||Bm||_F^2 gives the residual norm (svd.py:122-130).
+// ------------------------------------------------------------------------------------------
+struct MixedPlan {
+  double* partial;
+  double* en_b;
+  double* nr_b;
+  void* lam_b;
+  void *Y, *Q, *Qt, *Z, *Bm, *W, *part;
+  void* qr_ws;
+  size_t qr_bytes;
+  double* msq;
+  double* asq;
+  int n_part_rows;
+};
+
+static int mixed_gemm_splits(int n, int l) {
+  return std::max(gemm_splits(n, l, n, 128, 64), gemm_splits(l, n, n, 64, 128));
+}
+
+static void plan_mixed(Workspace& ws, MixedPlan& p, int dtype, int n, int l, int kc) {
+  const size_t e = dtype == F32 ? 4 : 8;
+  p.partial = ws.take<double>(cycle_energy_ws(n) / sizeof(double) + 1);
+  p.en_b = ws.take<double>(n);
+  p.nr_b = ws.take<double>(n);
+  p.lam_b = ws.take<char>((size_t)std::max(kc, 1) * n * e);
+  const size_t nl = (size_t)n * l * e;
+  p.Y = ws.take<char>(nl);
+  p.Q = ws.take<char>(nl);
+  p.Qt = ws.take<char>(nl);
+  p.Z = ws.take<char>(nl);
+  p.Bm = ws.take<char>(nl);
+  p.W = ws.take<char>(nl);
+  p.part = ws.take<char>(nl * (size_t)std::max(1, mixed_gemm_splits(n, l)));
+  p.qr_bytes = qr_ws_bytes(n, l);
+  p.qr_ws = ws.take<char>(p.qr_bytes);
+  p.n_part_rows = (int)ceil_div(n, 1);
+  p.msq = ws.take<double>(std::max<int>(n, kNumSMs * 4));
+  p.asq = ws.take<double>(std::max<int>(n, kNumSMs * 4));
+}
+
+template <typename T>
+static int run_mixed(const T* A, const T* B, int n, int l, int kc, int order, int q, const T* Omega, const int* fb,
+                     T* M, int* sb, double* scal, const MixedPlan& p, bool split3, cudaStream_t st) {
+  APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
+  // B: cycle norms, selection, kept diagonals
+  APX_TRY(launch_cycle_energies<T>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, st));
+  if (fb) { if (kc) APX_CUDA(cudaMemcpyAsync(sb, fb, kc * sizeof(int), cudaMemcpyDeviceToDevice, st)); }
+  else APX_TRY(launch_topk(p.nr_b, n, kc, sb, st));
+  APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, st));
+  T* lb = (T*)p.lam_b;
+  APX_TRY(launch_cycle_extract<T>(B, n, sb, kc, lb, st));
+  // A: randomized range finder (svd.py:105-111)
+  T *Y = (T*)p.Y, *Q = (T*)p.Q, *Qt = (T*)p.Qt, *Z = (T*)p.Z, *Bm = (T*)p.Bm, *W = (T*)p.W, *part = (T*)p.part;
+  const int s0 = gemm_splits(n, l, n, 128, 64);
+  const int s1 = gemm_splits(l, n, n, 64, 128);
+  APX_TRY(gemm_skinny<T>(0, A, n, Omega, l, Y, l, n, l, n, 0, nullptr, 0, 1, part, s0, split3, st));
+  APX_TRY((qr_orthonormalize<T, T>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, st)));
+  for (int it = 0; it < q; ++it) {
+    // Q <- qr(A^T Q) with A^T Q = (Q^T A)^T, then Q <- qr(A Q)
+    APX_TRY(gemm_skinny<T>(1, Qt, n, A, n, Z, n, l, n, n, 0, nullptr, 0, 1, part, s1, split3, st));
+    APX_TRY((qr_orthonormalize<T, T>(Z, 1, n, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, st)));
+    APX_TRY(gemm_skinny<T>(0, A, n, Q, l, Y, l, n, l, n, 0, nullptr, 0, 1, part, s0, split3, st));
+    APX_TRY((qr_orthonormalize<T, T>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, st)));
+  }
+  // Bm = Q^T A; ||Bm||_F^2 = sum sigma^2
+  APX_TRY(gemm_skinny<T>(1, Qt, n, A, n, Bm, n, l, n, n, 0, nullptr, 0, 1, part, s1, split3, st));
+  int parts = 0;
+  APX_TRY(launch_sumsq<T>(Bm, (size_t)l * n, p.msq, &parts, st));
+  APX_TRY(launch_sum_vector(p.msq, parts, scal + APX_S_KEPT_A, st));
+  if (order == 1) {
+    // W = Bm . dB (kept cycles of B masked on load), M = Q W, M += A . Bhat (+ ||M||^2, ||A||^2)
+    APX_TRY(gemm_skinny<T>(1, Bm, n, B, n, W, n, l, n, n, 0, sb, kc, n, part, s1, split3, st));
+    APX_TRY(gemm_skinny<T>(2, Q, l, W, n, M, n, n, n, l, 0, nullptr, 0, 1, nullptr, 1, split3, st));
+    APX_TRY(launch_cycle_right_gather<T>(A, nullptr, 0, lb, sb, kc, n, n, 1, M, p.msq, p.asq, st));
+    const int rblocks = (int)ceil_div(n, right_gather_rows(n, sizeof(T)));
+    APX_TRY(launch_sum_vector(p.msq, rblocks, scal + APX_S_FRO2_M, st));
+    APX_TRY(launch_sum_vector(p.asq, rblocks, scal + APX_S_FRO2_A, st));
+  } else {
+    APX_TRY(launch_cycle_right_gather<T>(Bm, nullptr, 0, lb, sb, kc, n, l, 0, W, p.msq, nullptr, st));
+    APX_TRY(gemm_skinny<T>(2, Q, l, W, n, M, n, n, n, l, 0, nullptr, 0, 1, nullptr, 1, split3, st));
+    APX_TRY(launch_sumsq<T>(M, (size_t)n * n, p.msq, &parts, st));
+    APX_TRY(launch_sum_vector(p.msq, parts, scal + APX_S_FRO2_M, st));
+    APX_TRY(launch_sumsq<T>(A, (size_t)n * n, p.asq, &parts, st));
+    APX_TRY(launch_sum_vector(p.asq, parts, scal + APX_S_FRO2_A, st));
   }
   return OK;
 }
@@ -142,6 +235,35 @@ int apx_cycle_first_order(int dtype, const void* A, const void* B, int64_t n, in
                             (float*)M, sel_a, sel_b, scalars, p, S(stream));
   return run_cycle<double>((const double*)A, (const double*)B, (int)n, k_a, k_b, order, force_sel_a, force_sel_b,
                            (double*)M, sel_a, sel_b, scalars, p, S(stream));
+}
+
+size_t apx_mixed_first_order_workspace(int dtype, int64_t n, int k_svd, int k_cyc, int order) {
+  (void)order;
+  Workspace ws(nullptr, 0, true);
+  MixedPlan p;
+  plan_mixed(ws, p, dtype, (int)n, k_svd, k_cyc);
+  return ws.off;
+}
+
+int apx_mixed_first_order(int dtype, const void* A, const void* B, int64_t n, int k_svd, int k_cyc, int order,
+                          int power_iterations, const void* omega, const int32_t* force_sel_b, int flags, void* M,
+                          int32_t* sel_b, double* scalars, void* wsp, size_t ws_bytes, void* stream) {
+  APX_REQUIRE(dtype == F32 || dtype == F64, "mixed product: real dtype required");
+  APX_REQUIRE(n >= 2 && n <= 46340, "n=%lld out of range", (long long)n);
+  APX_REQUIRE(k_svd >= 1 && k_svd <= 128 && k_svd <= n, "k_svd=%d out of range [1, min(n,128)]", k_svd);
+  APX_REQUIRE(k_cyc >= 0 && k_cyc <= n, "k_cyc=%d out of range [0, %lld]", k_cyc, (long long)n);
+  APX_REQUIRE(order == 0 || order == 1, "order must be 0 or 1");
+  APX_REQUIRE(power_iterations >= 0, "power_iterations must be >= 0");
+  Workspace ws(wsp, ws_bytes);
+  MixedPlan p;
+  plan_mixed(ws, p, dtype, (int)n, k_svd, k_cyc);
+  APX_WS_CHECK(ws);
+  const bool split3 = (flags & 1) != 0;
+  if (dtype == F32)
+    return run_mixed<float>((const float*)A, (const float*)B, (int)n, k_svd, k_cyc, order, power_iterations,
+                            (const float*)omega, force_sel_b, (float*)M, sel_b, scalars, p, split3, S(stream));
+  return run_mixed<double>((const double*)A, (const double*)B, (int)n, k_svd, k_cyc, order, power_iterations,
+                           (const double*)omega, force_sel_b, (double*)M, sel_b, scalars, p, split3, S(stream));
 }
 
 }  // extern "C"

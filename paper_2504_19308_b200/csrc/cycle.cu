@@ -167,13 +167,14 @@ __global__ void __launch_bounds__(256) cycle_left_gather(const T* __restrict__ X
 template <typename T, int R>
 __global__ void __launch_bounds__(512) cycle_right_gather(const T* __restrict__ X, const int* __restrict__ JA, int ka,
                                                           const T* __restrict__ lam, const int* __restrict__ J, int k,
-                                                          int n, int accumulate, T* __restrict__ M,
-                                                          double* __restrict__ msq_partial) {
+                                                          int n, int m_rows, int accumulate, T* __restrict__ M,
+                                                          double* __restrict__ msq_partial,
+                                                          double* __restrict__ xsq_partial) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Xs = reinterpret_cast<T*>(smem_raw);
   __shared__ double red[32];
   const int r0 = blockIdx.x * R;
-  const int rows = min(R, n - r0);
+  const int rows = min(R, m_rows - r0);
   // coalesced row-block load (vectorised when rows are 16B aligned)
   const size_t base = (size_t)r0 * n;
   const size_t cnt = (size_t)rows * n;
@@ -187,6 +188,15 @@ __global__ void __launch_bounds__(512) cycle_right_gather(const T* __restrict__ 
     for (size_t e = threadIdx.x; e < cnt; e += blockDim.x) Xs[e] = __ldg(X + base + e);
   }
   __syncthreads();
+  if (xsq_partial != nullptr) {  // ||X||^2 of the (unmasked) rows, for free from shared memory
+    double xs = 0.0;
+    for (size_t e = threadIdx.x; e < cnt; e += blockDim.x) {
+      const double v = (double)Xs[e];
+      xs = fma(v, v, xs);
+    }
+    xs = block_sum(xs, red);
+    if (threadIdx.x == 0) xsq_partial[blockIdx.x] = xs;
+  }
   if (JA != nullptr) {
     for (int e = threadIdx.x; e < rows * ka; e += blockDim.x) {
       const int rr = e / ka, t = e - rr * ka;
@@ -343,13 +353,14 @@ int launch_cycle_left_gather(const T* X, const T* lam, const int* J, int k, int 
 }
 
 template <typename T, int R>
-static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int acc,
-                          T* M, double* msq_partial, cudaStream_t st) {
+static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int m_rows,
+                          int acc, T* M, double* msq_partial, double* xsq_partial, cudaStream_t st) {
   const size_t smem = (size_t)R * n * sizeof(T);
   APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R>, smem));
-  const int blocks = (int)ceil_div(n, R);
+  const int blocks = (int)ceil_div(m_rows, R);
   const int threads = n >= 512 ? 512 : ((n + 31) / 32) * 32;
-  cycle_right_gather<T, R><<<blocks, threads, smem, st>>>(X, JA, ka, lam, J, k, n, acc, M, msq_partial);
+  cycle_right_gather<T, R><<<blocks, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M, msq_partial,
+                                                          xsq_partial);
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -362,19 +373,22 @@ int right_gather_rows(int n, size_t elem) {
 
 template <typename T>
 int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n,
-                              int accumulate, T* M, double* msq_partial, cudaStream_t st) {
+                              int m_rows, int accumulate, T* M, double* msq_partial, double* xsq_partial,
+                              cudaStream_t st) {
   const int r = right_gather_rows(n, sizeof(T));
   APX_REQUIRE((size_t)n * sizeof(T) <= 227 * 1024, "n=%d too large for the right gather row block", n);
+#define APX_RG(RV) return right_gather_r<T, RV>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, st)
   switch (r) {
-    case 1: return right_gather_r<T, 1>(X, JA, ka, lam, J, k, n, accumulate, M, msq_partial, st);
-    case 2: return right_gather_r<T, 2>(X, JA, ka, lam, J, k, n, accumulate, M, msq_partial, st);
-    case 3: return right_gather_r<T, 3>(X, JA, ka, lam, J, k, n, accumulate, M, msq_partial, st);
-    case 4: return right_gather_r<T, 4>(X, JA, ka, lam, J, k, n, accumulate, M, msq_partial, st);
-    case 5: return right_gather_r<T, 5>(X, JA, ka, lam, J, k, n, accumulate, M, msq_partial, st);
-    case 6: return right_gather_r<T, 6>(X, JA, ka, lam, J, k, n, accumulate, M, msq_partial, st);
-    case 7: return right_gather_r<T, 7>(X, JA, ka, lam, J, k, n, accumulate, M, msq_partial, st);
-    default: return right_gather_r<T, 8>(X, JA, ka, lam, J, k, n, accumulate, M, msq_partial, st);
+    case 1: APX_RG(1);
+    case 2: APX_RG(2);
+    case 3: APX_RG(3);
+    case 4: APX_RG(4);
+    case 5: APX_RG(5);
+    case 6: APX_RG(6);
+    case 7: APX_RG(7);
+    default: APX_RG(8);
   }
+#undef APX_RG
 }
 
 template <typename T>
@@ -397,8 +411,8 @@ int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st) {
   template int launch_cycle_extract<T>(const T*, int, const int*, int, T*, cudaStream_t);                     \
   template int launch_cycle_materialize<T>(const T*, const int*, int, int, T*, cudaStream_t);                 \
   template int launch_cycle_left_gather<T>(const T*, const T*, const int*, int, int, int, T*, cudaStream_t);  \
-  template int launch_cycle_right_gather<T>(const T*, const int*, int, const T*, const int*, int, int, int, T*, \
-                                            double*, cudaStream_t);                                          \
+  template int launch_cycle_right_gather<T>(const T*, const int*, int, const T*, const int*, int, int, int, int, T*, \
+                                            double*, double*, cudaStream_t);                                 \
   template int launch_sumsq<T>(const T*, size_t, double*, int*, cudaStream_t);
 APX_INST(float)
 APX_INST(double)

@@ -20,10 +20,23 @@ template <typename T>
 int launch_cycle_left_gather(const T* X, const T* lam, const int* J, int k, int n, int accumulate, T* M,
                              cudaStream_t st);
 template <typename T>
-int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n,
-                              int accumulate, T* M, double* msq_partial, cudaStream_t st);
+int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int m_rows,
+                              int accumulate, T* M, double* msq_partial, double* xsq_partial, cudaStream_t st);
 template <typename T>
 int launch_sumsq(const T* x, size_t cnt, double* partial, int* nparts, cudaStream_t st);
 int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st);
 
+}  // namespace apx
+
+namespace apx {
+// ---- gemm.cu ----
+int gemm_splits(int M, int N, int K, int BM, int BN);
+template <typename T>
+int gemm_skinny(int kind, const T* A, int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc, int M, int N, int K,
+                int accumulate, const int* mJ, int mk, int mod_n, T* part, int splits, bool split3, cudaStream_t st);
+// ---- linalg.cu ----
+size_t qr_ws_bytes(int m, int l);
+template <typename TI, typename TO>
+int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, int64_t qrs, int64_t qcs, TO* Q2,
+                      int64_t q2rs, int64_t q2cs, void* wsp, size_t ws_bytes, int method, cudaStream_t st);
 }  // namespace apx

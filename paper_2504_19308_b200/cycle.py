@@ -81,3 +81,59 @@ def cycle_first_order_multiply(A, B, k: int, order: int, model: ErrorModel | Non
     rep.selected_a = r["sel_a"].tolist()
     rep.selected_b = r["sel_b"].tolist()
     return D.to_user(r["M"], host), rep
+
+
+def draw_sketch(n: int, k: int, seed) -> "np.ndarray":
+    """The Gaussian test matrix of randomized_partial_svd for operand A: default_rng([seed, 0])
+    (svd.py:161) then rng.standard_normal((n, k)) (svd.py:105-106) -- drawn on the host with
+    numpy itself so it is bit-identical to the reference's sketch."""
+    import numpy as np
+
+    return np.random.default_rng([seed, 0]).standard_normal((n, k))
+
+
+def mixed_product_device(A, B, k_svd: int, k_cyc: int, order: int, omega, power_iterations: int = 0,
+                         force_sel_b=None, split3: bool = False, out=None):
+    """Device-level mixed product (config C4). omega: device tensor n x k_svd (A's dtype)."""
+    n = A.shape[0]
+    code = N.APX_F32 if A.dtype == torch.float32 else N.APX_F64
+    dev = A.device
+    M = out if out is not None else torch.empty((n, n), dtype=A.dtype, device=dev)
+    sb = torch.empty(max(k_cyc, 1), dtype=torch.int32, device=dev)
+    fb = None if force_sel_b is None else torch.as_tensor(force_sel_b, dtype=torch.int32).to(dev)
+    scal = torch.zeros(N.NSCALARS, dtype=torch.float64, device=dev)
+    ws = D.workspace(N.size("apx_mixed_first_order_workspace", code, n, k_svd, k_cyc, order))
+    N.call("apx_mixed_first_order", code, A.data_ptr(), B.data_ptr(), n, k_svd, k_cyc, order,
+           power_iterations, omega.data_ptr(), D.ptr(fb), 1 if split3 else 0, M.data_ptr(),
+           sb.data_ptr(), scal.data_ptr(), ws.data_ptr(), ws.numel(), D.stream_ptr())
+    return {"M": M, "sel_b": sb[:k_cyc], "scalars": scal, "ws": ws}
+
+
+def mixed_first_order_multiply(A, B, k_svd: int, k_cyc: int, order: int, seed,
+                               power_iterations: int = 0, model: ErrorModel | None = None,
+                               force_sel_b=None, split3: bool = False):
+    """Approximate A @ B with A truncated by randomized SVD (rank k_svd, svd.py:83-119) and B by
+    its k_cyc dominant cycles (config C4). Returns (M, ApproxReport(method="mixed"))."""
+    Ad, _, host = D.as_device_matrix(A, real_only=True)
+    Bd, _, _ = D.as_device_matrix(B, real_only=True)
+    n = Ad.shape[0]
+    if Ad.shape[1] != n or tuple(Bd.shape) != (n, n):
+        raise ValueError(f"two square n x n matrices required, got {tuple(Ad.shape)} x {tuple(Bd.shape)}")
+    if Bd.dtype != Ad.dtype:
+        Bd = Bd.to(Ad.dtype)
+    if order not in (0, 1):
+        raise ValueError("order must be 0 or 1")
+    if not 1 <= k_svd <= n or not 0 <= k_cyc <= n:
+        raise ValueError("component counts out of range")
+    if power_iterations < 0:
+        raise ValueError("power_iterations must be >= 0")
+    omega = torch.from_numpy(draw_sketch(n, k_svd, seed)).to(device=Ad.device, dtype=Ad.dtype)
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    r = mixed_product_device(Ad, Bd, k_svd, k_cyc, order, omega, power_iterations, force_sel_b, split3)
+    s = r["scalars"].tolist()
+    wall = time.perf_counter() - t0
+    nA, nB, ndA, ndB, nM = _norms(s)
+    rep = finish_report("mixed", order, k_svd, nA, nB, ndA, ndB, nM, n, wall, model)
+    rep.selected_b = r["sel_b"].tolist()
+    return D.to_user(r["M"], host), rep

@@ -1,0 +1,66 @@
+"""GPU parity: mixed rSVD x cycles product (config C4) vs the CPU oracle."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def P():
+    import paper_2504_19308_b200 as P
+    return P
+
+
+@pytest.mark.parametrize("order", [0, 1])
+def test_mixed_golden_fp64(P, golden, order):
+    g = golden("cycle")
+    n, ks, kc, seed = (int(v) for v in g["mx_par"])
+    M, rep = P.mixed_first_order_multiply(g["mx_A"], g["mx_B"], ks, kc, order, seed)
+    assert rep.selected_b == list(g["mx_Jb"])
+    assert rel(M, g[f"mx_M{order}"]) < 1e-10
+
+
+@pytest.mark.parametrize("n,ks,kc,q", [(96, 8, 5, 0), (256, 16, 12, 1), (500, 24, 7, 2)])
+@pytest.mark.parametrize("order", [0, 1])
+def test_mixed_fp64_vs_oracle(P, n, ks, kc, q, order):
+    A = O.gen_haar_spectrum(n, (np.arange(n) + 1.0) ** -1.5, 3 * n)
+    B = O.gen_cycle_operand(n, kc + 3, 3 * n + 1)
+    M, rep = P.mixed_first_order_multiply(A, B, ks, kc, order, seed=n, power_iterations=q)
+    Mo, ro = O.mixed_first_order_multiply(A, B, ks, kc, order, n, power_iterations=q)
+    assert rep.selected_b == ro["selected_b"]
+    assert rel(M, Mo) < 1e-10
+    assert rep.norm_da == pytest.approx(ro["norm_da"], rel=1e-6)
+    assert rep.norm_db == pytest.approx(ro["norm_db"], rel=1e-6)
+
+
+@pytest.mark.parametrize("split3", [False, True])
+def test_mixed_fp32_c4_shape(P, split3):
+    """C4 structure (sigma_i=(i+1)^-1.5 Haar A; 64-cycle B) at n=1024, fp32 tensors, tol 1e-4."""
+    n, k = 1024, 64
+    A = O.gen_haar_spectrum(n, (np.arange(n) + 1.0) ** -1.5, 8).astype(np.float32)
+    B = O.gen_cycle_operand(n, 64, 9).astype(np.float32)
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    M, rep = P.mixed_first_order_multiply(Ad, Bd, k, k, 1, seed=4, split3=split3)
+    assert M.dtype == torch.float32
+    Mo, ro = O.mixed_first_order_multiply(A.astype(np.float64), B.astype(np.float64), k, k, 1, 4)
+    assert rep.selected_b == ro["selected_b"]
+    err = rel(M.cpu().numpy(), Mo)
+    print(f"fp32 mixed n={n} split3={split3}: rel vs oracle {err:.3e}")
+    assert err < 1e-4
+
+
+def test_mixed_rank_deficient_sketch_fp64(P):
+    """Rank-1 A with a 6-column sketch: CholeskyQR2 breaks down and the device Householder
+    fallback must take over (svd.py tests feed such inputs, test_svd.py:56-64)."""
+    rng = np.random.default_rng(3)
+    n = 64
+    A = np.outer(rng.standard_normal(n), rng.standard_normal(n))
+    B = O.gen_cycle_operand(n, 4, 2)
+    for order in (0, 1):
+        M, rep = P.mixed_first_order_multiply(A, B, 6, 4, order, seed=5)
+        Mo, ro = O.mixed_first_order_multiply(A, B, 6, 4, order, 5)
+        assert rel(M, Mo) < 1e-9
