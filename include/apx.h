@@ -53,6 +53,12 @@ extern "C" {
 int apx_abi_version(void);
 const char* apx_last_error(void);
 
+/* diagnostics: number of kernels this library has launched since it was loaded, and
+ * thread-local stage-boundary events (cudaEvent_t*, recorded on the call's stream at each
+ * stage boundary of the product entry points; NULL disables). Used by bench.py. */
+long long apx_launch_count(void);
+int apx_set_stage_events(void** events, int count);
+
 /* ---------------------------------------------------------------- selection primitives ---- */
 
 /* top_indices (circulant.py:63-70): k largest of w[0..n) (non-negative doubles, device),

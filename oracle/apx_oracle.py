@@ -512,6 +512,7 @@ def mixed_first_order_multiply(A, B, k_svd: int, k_cyc: int, order: int, seed,
     t0 = time.perf_counter()
     U, s, V, fa = rsvd(A, k_svd, np.random.default_rng([seed, 0]), power_iterations)
     Jb, lb, nb_, nB, ndB = cycle_decompose(B, k_cyc, force_sel_b)
+    t_dec = time.perf_counter() - t0
     r = np.arange(n) if rows is None else np.asarray(rows)
     Us = U[r] * s
     if order == 0:
@@ -522,6 +523,7 @@ def mixed_first_order_multiply(A, B, k_svd: int, k_cyc: int, order: int, seed,
     wall = time.perf_counter() - t0
     rep = _report("mixed", order, s.size, math.sqrt(fa), nB, _svd_resid(s, fa), ndB, M, n, wall)
     rep["selected_b"], rep["norms_b"] = Jb, nb_
+    rep["t_decompose"] = t_dec
     return M, rep
 
 

@@ -57,6 +57,10 @@ def as_device_matrix(a, real_only: bool = False):
     """Return (device tensor, dtype code, came_from_host). Device tensors are validated for
     shape/dtype only (a finiteness scan would cost a full HBM pass)."""
     dev = require_cuda()
+    if isinstance(a, torch.Tensor) and not a.is_cuda:
+        # host torch tensor (pinned for the e2e path): async H2D, result goes back to the host
+        t, code, _ = as_device_matrix(a.to(dev, non_blocking=True), real_only)
+        return t, code, "torch"
     if is_device(a):
         t = a
         if t.dim() != 2:
@@ -94,7 +98,16 @@ def ptr(t) -> int | None:
     return None if t is None else t.data_ptr()
 
 
-def to_user(t: torch.Tensor, host: bool):
+def to_user(t: torch.Tensor, host, out=None):
+    """Return the result in the caller's container: numpy for numpy inputs (the reference
+    contract), a (pinned) host tensor for host torch inputs -- written into ``out`` when given --
+    and the device tensor otherwise."""
     if not host:
         return t
+    if host == "torch":
+        if out is None:
+            out = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)
+        out.copy_(t, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        return out
     return t.cpu().numpy()

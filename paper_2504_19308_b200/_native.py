@@ -25,6 +25,8 @@ _vp, _i64, _i32, _sz = C.c_void_p, C.c_int64, C.c_int, C.c_size_t
 SIGNATURES = {
     "apx_abi_version": (C.c_int, []),
     "apx_last_error": (C.c_char_p, []),
+    "apx_launch_count": (C.c_longlong, []),
+    "apx_set_stage_events": (C.c_int, [_vp, _i32]),
     "apx_top_indices": (C.c_int, [_vp, _i64, _i32, _vp, _vp]),
     "apx_cycle_norms_workspace": (_sz, [_i32, _i64]),
     "apx_cycle_norms": (C.c_int, [_i32, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),

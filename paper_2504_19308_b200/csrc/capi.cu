@@ -1,5 +1,6 @@
 // C-ABI entry points (include/apx.h). Validation, workspace planning, and the launch sequence
 // of each product; the kernels live in the other translation units.
+#include <atomic>
 #include <cstdarg>
 
 #include "../../include/apx.h"
@@ -9,12 +10,21 @@
 namespace apx {
 
 static thread_local char g_err[1024] = "";
+static std::atomic<long long> g_launches{0};
+static thread_local cudaEvent_t* g_stage_ev = nullptr;
+static thread_local int g_stage_n = 0;
 
 void set_error(const char* fmt, ...) {
   va_list ap;
   va_start(ap, fmt);
   vsnprintf(g_err, sizeof(g_err), fmt, ap);
   va_end(ap);
+}
+
+void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+void stage_mark(int i, cudaStream_t st) {
+  if (g_stage_ev != nullptr && i < g_stage_n) cudaEventRecord(g_stage_ev[i], st);
 }
 
 static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
@@ -52,6 +62,7 @@ static void plan_cycle(Workspace& ws, CyclePlan& p, int dtype, int n, int ka, in
 template <typename T>
 static int run_cycle(const T* A, const T* B, int n, int ka, int kb, int order, const int* fa, const int* fb, T* M,
                      int* sa, int* sb, double* scal, const CyclePlan& p, cudaStream_t st) {
+  stage_mark(0, st);
   APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
   APX_TRY(launch_cycle_energies<T>(A, n, p.en_a, p.nr_a, scal + APX_S_FRO2_A, p.partial, st));
   APX_TRY(launch_cycle_energies<T>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, st));
@@ -65,11 +76,14 @@ static int run_cycle(const T* A, const T* B, int n, int ka, int kb, int order, c
   T* lb = (T*)p.lam_b;
   APX_TRY(launch_cycle_extract<T>(A, n, sa, ka, la, st));
   APX_TRY(launch_cycle_extract<T>(B, n, sb, kb, lb, st));
+  stage_mark(1, st);
   if (order == 1) {
     // M = Ahat . B   (left gather over column strips of B)
     APX_TRY(launch_cycle_left_gather<T>(B, la, sa, ka, n, 0, M, st));
+    stage_mark(2, st);
     // M += dA . Bhat (right gather over row blocks of A, masked to dA on load) + ||M||^2
     APX_TRY(launch_cycle_right_gather<T>(A, sa, ka, lb, sb, kb, n, n, 1, M, p.msq, nullptr, st));
+    stage_mark(3, st);
     const int rblocks = (int)ceil_div(n, right_gather_rows(n, sizeof(T)));
     APX_TRY(launch_sum_vector(p.msq, rblocks, scal + APX_S_FRO2_M, st));
   } else {
@@ -80,6 +94,7 @@ static int run_cycle(const T* A, const T* B, int n, int ka, int kb, int order, c
     APX_TRY(launch_sumsq<T>(M, (size_t)n * n, p.msq, &parts, st));
     APX_TRY(launch_sum_vector(p.msq, parts, scal + APX_S_FRO2_M, st));
   }
+  stage_mark(4, st);
   return OK;
 }
 
@@ -131,6 +146,7 @@ static void plan_mixed(Workspace& ws, MixedPlan& p, int dtype, int n, int l, int
 template <typename T>
 static int run_mixed(const T* A, const T* B, int n, int l, int kc, int order, int q, const T* Omega, const int* fb,
                      T* M, int* sb, double* scal, const MixedPlan& p, bool split3, cudaStream_t st) {
+  stage_mark(0, st);
   APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
   // B: cycle norms, selection, kept diagonals
   APX_TRY(launch_cycle_energies<T>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, st));
@@ -139,11 +155,13 @@ static int run_mixed(const T* A, const T* B, int n, int l, int kc, int order, in
   APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, st));
   T* lb = (T*)p.lam_b;
   APX_TRY(launch_cycle_extract<T>(B, n, sb, kc, lb, st));
+  stage_mark(1, st);
   // A: randomized range finder (svd.py:105-111)
   T *Y = (T*)p.Y, *Q = (T*)p.Q, *Qt = (T*)p.Qt, *Z = (T*)p.Z, *Bm = (T*)p.Bm, *W = (T*)p.W, *part = (T*)p.part;
   const int s0 = gemm_splits(n, l, n, 128, 64);
   const int s1 = gemm_splits(l, n, n, 64, 128);
   APX_TRY(gemm_skinny<T>(0, A, n, Omega, l, Y, l, n, l, n, 0, nullptr, 0, 1, part, s0, split3, st));
+  stage_mark(2, st);
   APX_TRY((qr_orthonormalize<T, T>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, st)));
   for (int it = 0; it < q; ++it) {
     // Q <- qr(A^T Q) with A^T Q = (Q^T A)^T, then Q <- qr(A Q)
@@ -152,16 +170,21 @@ static int run_mixed(const T* A, const T* B, int n, int l, int kc, int order, in
     APX_TRY(gemm_skinny<T>(0, A, n, Q, l, Y, l, n, l, n, 0, nullptr, 0, 1, part, s0, split3, st));
     APX_TRY((qr_orthonormalize<T, T>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, st)));
   }
+  stage_mark(3, st);
   // Bm = Q^T A; ||Bm||_F^2 = sum sigma^2
   APX_TRY(gemm_skinny<T>(1, Qt, n, A, n, Bm, n, l, n, n, 0, nullptr, 0, 1, part, s1, split3, st));
   int parts = 0;
   APX_TRY(launch_sumsq<T>(Bm, (size_t)l * n, p.msq, &parts, st));
   APX_TRY(launch_sum_vector(p.msq, parts, scal + APX_S_KEPT_A, st));
+  stage_mark(4, st);
   if (order == 1) {
     // W = Bm . dB (kept cycles of B masked on load), M = Q W, M += A . Bhat (+ ||M||^2, ||A||^2)
     APX_TRY(gemm_skinny<T>(1, Bm, n, B, n, W, n, l, n, n, 0, sb, kc, n, part, s1, split3, st));
+    stage_mark(5, st);
     APX_TRY(gemm_skinny<T>(2, Q, l, W, n, M, n, n, n, l, 0, nullptr, 0, 1, nullptr, 1, split3, st));
+    stage_mark(6, st);
     APX_TRY(launch_cycle_right_gather<T>(A, nullptr, 0, lb, sb, kc, n, n, 1, M, p.msq, p.asq, st));
+    stage_mark(7, st);
     const int rblocks = (int)ceil_div(n, right_gather_rows(n, sizeof(T)));
     APX_TRY(launch_sum_vector(p.msq, rblocks, scal + APX_S_FRO2_M, st));
     APX_TRY(launch_sum_vector(p.asq, rblocks, scal + APX_S_FRO2_A, st));
@@ -173,6 +196,7 @@ static int run_mixed(const T* A, const T* B, int n, int l, int kc, int order, in
     APX_TRY(launch_sumsq<T>(A, (size_t)n * n, p.asq, &parts, st));
     APX_TRY(launch_sum_vector(p.asq, parts, scal + APX_S_FRO2_A, st));
   }
+  stage_mark(8, st);
   return OK;
 }
 
@@ -183,6 +207,14 @@ using namespace apx;
 extern "C" {
 
 int apx_abi_version(void) { return 1; }
+
+long long apx_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int apx_set_stage_events(void** events, int count) {
+  g_stage_ev = reinterpret_cast<cudaEvent_t*>(events);
+  g_stage_n = events ? count : 0;
+  return OK;
+}
 
 const char* apx_last_error(void) { return g_err; }
 

@@ -26,8 +26,11 @@ enum Err : int {
 };
 
 void set_error(const char* fmt, ...);
+void count_launch();
+// Records the i-th stage-boundary event on `st` when the caller armed them (apx_set_stage_events).
+void stage_mark(int i, cudaStream_t st);
 
-#define APX_CUDA(expr)                                                                  \
+#define APX_CUDA(expr)                                                                 \
   do {                                                                                  \
     cudaError_t _e = (expr);                                                            \
     if (_e != cudaSuccess) {                                                            \
@@ -38,6 +41,7 @@ void set_error(const char* fmt, ...);
 
 #define APX_LAUNCH_CHECK()                                                               \
   do {                                                                                  \
+    ::apx::count_launch();                                                              \
     cudaError_t _e = cudaGetLastError();                                                \
     if (_e != cudaSuccess) {                                                            \
       ::apx::set_error("%s:%d launch: %s", __FILE__, __LINE__, cudaGetErrorString(_e)); \

@@ -111,7 +111,7 @@ def mixed_product_device(A, B, k_svd: int, k_cyc: int, order: int, omega, power_
 
 def mixed_first_order_multiply(A, B, k_svd: int, k_cyc: int, order: int, seed,
                                power_iterations: int = 0, model: ErrorModel | None = None,
-                               force_sel_b=None, split3: bool = False):
+                               force_sel_b=None, split3: bool = False, out=None):
     """Approximate A @ B with A truncated by randomized SVD (rank k_svd, svd.py:83-119) and B by
     its k_cyc dominant cycles (config C4). Returns (M, ApproxReport(method="mixed"))."""
     Ad, _, host = D.as_device_matrix(A, real_only=True)
@@ -136,4 +136,4 @@ def mixed_first_order_multiply(A, B, k_svd: int, k_cyc: int, order: int, seed,
     nA, nB, ndA, ndB, nM = _norms(s)
     rep = finish_report("mixed", order, k_svd, nA, nB, ndA, ndB, nM, n, wall, model)
     rep.selected_b = r["sel_b"].tolist()
-    return D.to_user(r["M"], host), rep
+    return D.to_user(r["M"], host, out), rep
