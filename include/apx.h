@@ -97,6 +97,16 @@ int apx_mixed_first_order(int dtype, const void* A, const void* B, int64_t n, in
                           const int32_t* force_sel_b, int flags, void* M, int32_t* sel_b,
                           double* scalars, void* ws, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------------------- diagnostics ---- */
+/* The tcgen05 TF32 GEMM used by the fp32 rSVD stages, exposed for kernel-level tests:
+ * C (+)= opA . opB with layout bit 1 = A stored [k][m] (MN-major), bit 2 = B stored [k][n]
+ * (MN-major; else [n][k]), bit 4 = store C transposed; bn in {64,128,256}; splits > 1 writes
+ * `splits` partial slices of M*ldc floats. mask_j (optional) drops A-operand entries (m,k)
+ * with (k - m) mod mod_n in mask_j (MN-major A only). */
+int apx_debug_umma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb,
+                        float* C, int64_t ldc, int64_t M, int64_t N, int64_t K, int splits,
+                        int accumulate, const int32_t* mask_j, int mask_k, int mod_n, void* stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -29,6 +29,16 @@ void stage_mark(int i, cudaStream_t st) {
 
 static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
 
+// gather lambda tables are padded to a multiple of 8 rows (zeros) for the unguarded fast path
+static inline int pad8(int k) { return (int)ceil_div(std::max(k, 1), 8) * 8; }
+
+template <typename T>
+static int zero_pad_rows(T* lam, int k, int n, cudaStream_t st) {
+  const int kp = pad8(k);
+  if (kp > k) APX_CUDA(cudaMemsetAsync(lam + (size_t)k * n, 0, (size_t)(kp - k) * n * sizeof(T), st));
+  return OK;
+}
+
 // ------------------------------------------------------------------------------------------
 // cycle product plan
 // ------------------------------------------------------------------------------------------
@@ -53,7 +63,7 @@ static void plan_cycle(Workspace& ws, CyclePlan& p, int dtype, int n, int ka, in
   p.en_b = ws.take<double>(n);
   p.nr_b = ws.take<double>(n);
   p.lam_a = ws.take<char>((size_t)std::max(ka, 1) * n * e);
-  p.lam_b = ws.take<char>((size_t)std::max(kb, 1) * n * e);
+  p.lam_b = ws.take<char>((size_t)pad8(kb) * n * e);
   p.bhat = order == 0 ? (void*)ws.take<char>((size_t)n * n * e) : nullptr;
   p.n_msq = std::max<int>((int)ceil_div(n, 1), kNumSMs * 4);
   p.msq = ws.take<double>(p.n_msq);
@@ -76,15 +86,16 @@ static int run_cycle(const T* A, const T* B, int n, int ka, int kb, int order, c
   T* lb = (T*)p.lam_b;
   APX_TRY(launch_cycle_extract<T>(A, n, sa, ka, la, st));
   APX_TRY(launch_cycle_extract<T>(B, n, sb, kb, lb, st));
+  APX_TRY(zero_pad_rows<T>(lb, kb, n, st));
   stage_mark(1, st);
   if (order == 1) {
     // M = Ahat . B   (left gather over column strips of B)
     APX_TRY(launch_cycle_left_gather<T>(B, la, sa, ka, n, 0, M, st));
     stage_mark(2, st);
     // M += dA . Bhat (right gather over row blocks of A, masked to dA on load) + ||M||^2
-    APX_TRY(launch_cycle_right_gather<T>(A, sa, ka, lb, sb, kb, n, n, 1, M, p.msq, nullptr, st));
+    APX_TRY(launch_cycle_right_gather<T>(A, sa, ka, lb, sb, kb, n, n, 1, M, p.msq, nullptr, st, true));
     stage_mark(3, st);
-    const int rblocks = (int)ceil_div(n, right_gather_rows(n, sizeof(T)));
+    const int rblocks = (int)ceil_div(n, right_gather_rows(n, sizeof(T), kb));
     APX_TRY(launch_sum_vector(p.msq, rblocks, scal + APX_S_FRO2_M, st));
   } else {
     T* bh = (T*)p.bhat;
@@ -127,7 +138,7 @@ static void plan_mixed(Workspace& ws, MixedPlan& p, int dtype, int n, int l, int
   p.partial = ws.take<double>(cycle_energy_ws(n) / sizeof(double) + 1);
   p.en_b = ws.take<double>(n);
   p.nr_b = ws.take<double>(n);
-  p.lam_b = ws.take<char>((size_t)std::max(kc, 1) * n * e);
+  p.lam_b = ws.take<char>((size_t)pad8(kc) * n * e);
   const size_t nl = (size_t)n * l * e;
   p.Y = ws.take<char>(nl);
   p.Q = ws.take<char>(nl);
@@ -155,6 +166,7 @@ static int run_mixed(const T* A, const T* B, int n, int l, int kc, int order, in
   APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, st));
   T* lb = (T*)p.lam_b;
   APX_TRY(launch_cycle_extract<T>(B, n, sb, kc, lb, st));
+  APX_TRY(zero_pad_rows<T>(lb, kc, n, st));
   stage_mark(1, st);
   // A: randomized range finder (svd.py:105-111)
   T *Y = (T*)p.Y, *Q = (T*)p.Q, *Qt = (T*)p.Qt, *Z = (T*)p.Z, *Bm = (T*)p.Bm, *W = (T*)p.W, *part = (T*)p.part;
@@ -183,13 +195,13 @@ static int run_mixed(const T* A, const T* B, int n, int l, int kc, int order, in
     stage_mark(5, st);
     APX_TRY(gemm_skinny<T>(2, Q, l, W, n, M, n, n, n, l, 0, nullptr, 0, 1, nullptr, 1, split3, st));
     stage_mark(6, st);
-    APX_TRY(launch_cycle_right_gather<T>(A, nullptr, 0, lb, sb, kc, n, n, 1, M, p.msq, p.asq, st));
+    APX_TRY(launch_cycle_right_gather<T>(A, nullptr, 0, lb, sb, kc, n, n, 1, M, p.msq, p.asq, st, true));
     stage_mark(7, st);
-    const int rblocks = (int)ceil_div(n, right_gather_rows(n, sizeof(T)));
+    const int rblocks = (int)ceil_div(n, right_gather_rows(n, sizeof(T), kc));
     APX_TRY(launch_sum_vector(p.msq, rblocks, scal + APX_S_FRO2_M, st));
     APX_TRY(launch_sum_vector(p.asq, rblocks, scal + APX_S_FRO2_A, st));
   } else {
-    APX_TRY(launch_cycle_right_gather<T>(Bm, nullptr, 0, lb, sb, kc, n, l, 0, W, p.msq, nullptr, st));
+    APX_TRY(launch_cycle_right_gather<T>(Bm, nullptr, 0, lb, sb, kc, n, l, 0, W, p.msq, nullptr, st, true));
     APX_TRY(gemm_skinny<T>(2, Q, l, W, n, M, n, n, n, l, 0, nullptr, 0, 1, nullptr, 1, split3, st));
     APX_TRY(launch_sumsq<T>(M, (size_t)n * n, p.msq, &parts, st));
     APX_TRY(launch_sum_vector(p.msq, parts, scal + APX_S_FRO2_M, st));
@@ -267,6 +279,15 @@ int apx_cycle_first_order(int dtype, const void* A, const void* B, int64_t n, in
                             (float*)M, sel_a, sel_b, scalars, p, S(stream));
   return run_cycle<double>((const double*)A, (const double*)B, (int)n, k_a, k_b, order, force_sel_a, force_sel_b,
                            (double*)M, sel_a, sel_b, scalars, p, S(stream));
+}
+
+int apx_debug_umma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                        int64_t ldc, int64_t M, int64_t N, int64_t K, int splits, int accumulate, const int32_t* mask_j,
+                        int mask_k, int mod_n, void* stream) {
+  APX_REQUIRE(M >= 1 && N >= 1 && K >= 1 && splits >= 1, "bad GEMM shape");
+  if (layout >= 64) { APX_TRY(umma_set_variant(layout >> 6)); layout &= 63; }
+  return umma_gemm(layout, bn, A, lda, B, ldb, C, ldc, (int64_t)M * ldc, (int)M, (int)N, (int)K, splits, accumulate,
+                   mask_j, mask_k, mod_n, S(stream));
 }
 
 size_t apx_mixed_first_order_workspace(int dtype, int64_t n, int k_svd, int k_cyc, int order) {

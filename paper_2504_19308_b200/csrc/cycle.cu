@@ -160,40 +160,102 @@ __global__ void __launch_bounds__(256) cycle_left_gather(const T* __restrict__ X
 }
 
 // ------------------------------------------------------------------------------------------
-// K11: right gather on a row block. The CTA keeps X[r0:r0+R, :] in shared memory (masked to dA
-// when JA != nullptr); thread = output column(s); per shift one lambda load feeds R FMAs.
-// Also emits the block's partial sum of |M|^2 for the report's ||M||_F.
+// K11: right gather on a row block. The CTA keeps X[r0:r0+R, :] in shared memory, stored
+// row-INTERLEAVED (Xs[m*RP + rr]) so that the R values one output column needs at source column
+// m are contiguous: one address per (shift, column), then LDS.64 pairs feeding packed
+// fma.rn.f32x2 (fp32) or scalar DFMA (fp64). X is optionally masked to dA (kept cycles of A
+// zeroed on load). Thread = output column(s); each lambda value (an L2 load) feeds R FMAs.
+// Also emits the block's partial sums of |M|^2 (report's ||M||_F) and |X|^2 (||A||_F).
 // ------------------------------------------------------------------------------------------
-template <typename T, int R>
-__global__ void __launch_bounds__(512) cycle_right_gather(const T* __restrict__ X, const int* __restrict__ JA, int ka,
+__device__ __forceinline__ unsigned long long ffma2(unsigned long long a, unsigned long long b,
+                                                    unsigned long long c) {
+  unsigned long long d;
+  asm volatile("fma.rn.f32x2 %0, %1, %2, %3;" : "=l"(d) : "l"(a), "l"(b), "l"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned long long pack2(float x, float y) {
+  return ((unsigned long long)__float_as_uint(y) << 32) | __float_as_uint(x);
+}
+
+// Non-coherent load as volatile asm: volatile statements keep their relative order, so all U*CPT
+// lambda loads of a batch are issued before the first FMA consumes one (the scheduler otherwise
+// sinks each load next to its use and exposes the L2 latency every time).
+__device__ __forceinline__ float ldg_nc_ordered(const float* p) {
+  float v;
+  asm volatile("ld.global.nc.f32 %0, [%1];" : "=f"(v) : "l"(p));
+  return v;
+}
+__device__ __forceinline__ double ldg_nc_ordered(const double* p) {
+  double v;
+  asm volatile("ld.global.nc.f64 %0, [%1];" : "=d"(v) : "l"(p));
+  return v;
+}
+
+template <typename T, int R, bool FAST>
+__global__ void __launch_bounds__(512, 1) cycle_right_gather(const T* __restrict__ X, const int* __restrict__ JA, int ka,
                                                           const T* __restrict__ lam, const int* __restrict__ J, int k,
                                                           int n, int m_rows, int accumulate, T* __restrict__ M,
                                                           double* __restrict__ msq_partial,
                                                           double* __restrict__ xsq_partial) {
+  constexpr int RP = R + (R & 1);  // interleave pitch (even, so float pairs stay 8B aligned)
+  constexpr int CPT = 2, U = 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Xs = reinterpret_cast<T*>(smem_raw);
+  int* sJ = reinterpret_cast<int*>(Xs + (size_t)RP * n);
   __shared__ double red[32];
   const int r0 = blockIdx.x * R;
   const int rows = min(R, m_rows - r0);
-  // coalesced row-block load (vectorised when rows are 16B aligned)
-  const size_t base = (size_t)r0 * n;
-  const size_t cnt = (size_t)rows * n;
+  // coalesced row reads, interleaved shared-memory writes; rows past the end are zero.
+  // The row block is read in batches of 16-byte vectors with all RP rows' loads issued before
+  // any is stored, so a CTA pays ~one DRAM latency per batch instead of one per element.
+  double xs = 0.0;
   constexpr int V = 16 / sizeof(T);
-  if ((n % V) == 0) {
-    using Vec = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
-    const Vec* src = reinterpret_cast<const Vec*>(X + base);
-    Vec* dst = reinterpret_cast<Vec*>(Xs);
-    for (size_t e = threadIdx.x; e < cnt / V; e += blockDim.x) dst[e] = __ldg(src + e);
-  } else {
-    for (size_t e = threadIdx.x; e < cnt; e += blockDim.x) Xs[e] = __ldg(X + base + e);
-  }
-  __syncthreads();
-  if (xsq_partial != nullptr) {  // ||X||^2 of the (unmasked) rows, for free from shared memory
-    double xs = 0.0;
-    for (size_t e = threadIdx.x; e < cnt; e += blockDim.x) {
-      const double v = (double)Xs[e];
-      xs = fma(v, v, xs);
+  using Vec = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+  if (FAST && (n % V) == 0) {
+    const int nv = n / V;
+    for (int base = threadIdx.x; base < nv; base += blockDim.x * 2) {
+      Vec buf[RP][2];
+#pragma unroll
+      for (int rr = 0; rr < RP; ++rr)
+#pragma unroll
+        for (int h = 0; h < 2; ++h) {
+          const int iv = base + h * blockDim.x;
+          if (rr < rows && iv < nv)
+            buf[rr][h] = __ldg(reinterpret_cast<const Vec*>(X + (size_t)(r0 + rr) * n) + iv);
+          else
+            buf[rr][h] = Vec{};
+        }
+#pragma unroll
+      for (int h = 0; h < 2; ++h) {
+        const int iv = base + h * blockDim.x;
+        if (iv >= nv) continue;
+#pragma unroll
+        for (int rr = 0; rr < RP; ++rr) {
+          const T* e = reinterpret_cast<const T*>(&buf[rr][h]);
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            xs = fma((double)e[q], (double)e[q], xs);
+            Xs[(size_t)(iv * V + q) * RP + rr] = e[q];
+          }
+        }
+      }
     }
+  } else {
+    for (int rr = 0; rr < RP; ++rr) {
+      const T* src = X + (size_t)(r0 + rr) * n;
+      for (int m = threadIdx.x; m < n; m += blockDim.x) {
+        T v = T(0);
+        if (rr < rows) v = __ldg(src + m);
+        xs = fma((double)v, (double)v, xs);
+        Xs[(size_t)m * RP + rr] = v;
+      }
+    }
+  }
+  // shifts, padded with zeros to a multiple of U (FAST: the lambda rows are zero-padded too)
+  const int kp = FAST ? (int)ceil_div(k, U) * U : k;
+  for (int t = threadIdx.x; t < kp; t += blockDim.x) sJ[t] = t < k ? J[t] : 0;
+  __syncthreads();
+  if (xsq_partial != nullptr) {  // ||X||^2 of the (unmasked) rows
     xs = block_sum(xs, red);
     if (threadIdx.x == 0) xsq_partial[blockIdx.x] = xs;
   }
@@ -202,30 +264,113 @@ __global__ void __launch_bounds__(512) cycle_right_gather(const T* __restrict__ 
       const int rr = e / ka, t = e - rr * ka;
       int m = r0 + rr - JA[t];
       if (m < 0) m += n;
-      Xs[(size_t)rr * n + m] = T(0);
+      Xs[(size_t)m * RP + rr] = T(0);
     }
     __syncthreads();
   }
   double msq = 0.0;
-  for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    T acc[R];
+  // Each thread owns CPT columns (blockDim apart, so warps stay coalesced). U shifts' worth of
+  // lambda loads are issued before any is consumed (U*CPT L2 loads in flight per thread).
+  constexpr int NP = (sizeof(T) == 4) ? R / 2 : 0;    // packed float pairs
+  constexpr int NS = (sizeof(T) == 4) ? (R & 1) : R;  // scalar rows
+  const int stride = blockDim.x;
+  for (int cb = threadIdx.x; cb < n; cb += stride * CPT) {
+    unsigned long long acc2[CPT][NP > 0 ? NP : 1];
+    T accs[CPT][NS > 0 ? NS : 1];
 #pragma unroll
-    for (int rr = 0; rr < R; ++rr) acc[rr] = T(0);
-#pragma unroll 4
-    for (int t = 0; t < k; ++t) {
-      int m = c + __ldg(J + t);
-      if (m >= n) m -= n;
-      const T l = __ldg(lam + (size_t)t * n + m);
+    for (int q = 0; q < CPT; ++q) {
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr) acc[rr] = fma(Xs[(size_t)rr * n + m], l, acc[rr]);
+      for (int p = 0; p < (NP > 0 ? NP : 1); ++p) acc2[q][p] = 0ull;
+#pragma unroll
+      for (int s = 0; s < (NS > 0 ? NS : 1); ++s) accs[q][s] = T(0);
+    }
+    // software pipeline across shift batches: batch i+1's lambda loads are in flight while
+    // batch i is consumed (ping-pong register buffers A/B)
+    auto load_batch = [&](int t0, int (&mm)[U][CPT], T (&lv)[U][CPT]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u) {
+        const int t = t0 + u;
+        const int jt = sJ[t];  // broadcast
+        const T* lrow = lam + t * n;
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+          const int c = cb + q * stride;
+          int m = c + jt;
+          m = m >= n ? m - n : m;
+          if constexpr (FAST) {
+            mm[u][q] = m * RP;
+            lv[u][q] = ldg_nc_ordered(lrow + m);
+          } else {
+            const bool ok = t < k && c < n;
+            mm[u][q] = ok ? m * RP : 0;
+            lv[u][q] = ok ? __ldg(lrow + m) : T(0);
+          }
+        }
+      }
+    };
+    auto compute_batch = [&](const int (&mm)[U][CPT], const T (&lv)[U][CPT]) {
+#pragma unroll
+      for (int u = 0; u < U; ++u)
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+          const T* xp = Xs + mm[u][q];
+          if constexpr (NP > 0) {
+            const unsigned long long l2 = pack2((float)lv[u][q], (float)lv[u][q]);
+            const unsigned long long* xp2 = reinterpret_cast<const unsigned long long*>(xp);
+#pragma unroll
+            for (int p = 0; p < NP; ++p) acc2[q][p] = ffma2(xp2[p], l2, acc2[q][p]);
+          }
+          if constexpr (NS > 0) {
+#pragma unroll
+            for (int s2 = 0; s2 < NS; ++s2) accs[q][s2] = fma(xp[2 * NP + s2], lv[u][q], accs[q][s2]);
+          }
+        }
+    };
+    // the epilogue reads back M (written by the preceding low-rank GEMM, usually DRAM-resident):
+    // pull those lines toward L2 now so the read-modify-write does not stall on DRAM latency
+    if (accumulate) {
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+        const int c = cb + q * stride;
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr)
+          if ((FAST || c < n) && rr < rows)
+            asm volatile("prefetch.global.L2 [%0];" ::"l"(M + (size_t)(r0 + rr) * n + c));
+      }
+    }
+    int mmA[U][CPT], mmB[U][CPT];
+    T lvA[U][CPT], lvB[U][CPT];
+    load_batch(0, mmA, lvA);
+    for (int t0 = 0; t0 < kp; t0 += 2 * U) {
+      if (t0 + U < kp) load_batch(t0 + U, mmB, lvB);
+      compute_batch(mmA, lvA);
+      if (t0 + U >= kp) break;
+      if (t0 + 2 * U < kp) load_batch(t0 + 2 * U, mmA, lvA);
+      compute_batch(mmB, lvB);
     }
 #pragma unroll
-    for (int rr = 0; rr < R; ++rr) {
-      if (rr < rows) {
-        T* mp = M + (size_t)(r0 + rr) * n + c;
-        T v = accumulate ? *mp + acc[rr] : acc[rr];
-        *mp = v;
-        msq += (double)v * (double)v;
+    for (int q = 0; q < CPT; ++q) {
+      const int c = cb + q * stride;
+      if (!FAST && c >= n) continue;
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr) {
+        T a;
+        if constexpr (NP > 0) {
+          if (rr < 2 * NP) {
+            const unsigned long long v = acc2[q][rr >> 1];
+            a = (T)__uint_as_float((unsigned)(rr & 1 ? (v >> 32) : (v & 0xffffffffull)));
+          } else {
+            a = accs[q][rr - 2 * NP];
+          }
+        } else {
+          a = accs[q][rr];
+        }
+        if (rr < rows) {
+          T* mp = M + (size_t)(r0 + rr) * n + c;
+          T v = accumulate ? *mp + a : a;
+          *mp = v;
+          msq += (double)v * (double)v;
+        }
       }
     }
   }
@@ -354,30 +499,43 @@ int launch_cycle_left_gather(const T* X, const T* lam, const int* J, int k, int 
 
 template <typename T, int R>
 static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int m_rows,
-                          int acc, T* M, double* msq_partial, double* xsq_partial, cudaStream_t st) {
-  const size_t smem = (size_t)R * n * sizeof(T);
-  APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R>, smem));
+                          int acc, T* M, double* msq_partial, double* xsq_partial, bool lam_padded, cudaStream_t st) {
+  constexpr int U = 8, CPT = 2;
+  const int kp = (int)ceil_div(std::max(k, 1), U) * U;
+  const size_t smem = (size_t)(R + (R & 1)) * n * sizeof(T) + (size_t)kp * sizeof(int);
   const int blocks = (int)ceil_div(m_rows, R);
   const int threads = n >= 512 ? 512 : ((n + 31) / 32) * 32;
-  cycle_right_gather<T, R><<<blocks, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M, msq_partial,
-                                                          xsq_partial);
+  const bool fast = lam_padded && (n % (threads * CPT)) == 0;
+  if (fast) {
+    APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R, true>, smem));
+    cycle_right_gather<T, R, true><<<blocks, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
+                                                                  msq_partial, xsq_partial);
+  } else {
+    APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R, false>, smem));
+    cycle_right_gather<T, R, false><<<blocks, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
+                                                                   msq_partial, xsq_partial);
+  }
   APX_LAUNCH_CHECK();
   return OK;
 }
 
-int right_gather_rows(int n, size_t elem) {
-  int r = 8;
-  while (r > 1 && (size_t)r * n * elem > kSmemBudget) --r;
+int right_gather_rows(int n, size_t elem, int k) {
+  int r = 8;  // even row counts keep the fp32 pairs packed
+  while (r > 1 && (size_t)(r + (r & 1)) * n * elem + (size_t)(k + 8) * sizeof(int) > kSmemBudget)
+    r -= (r > 2 ? 2 : 1);
   return r;
 }
 
+// lam: k x n, or (lam_padded) ceil(k/8)*8 x n with zero rows past k -- enables the fast path.
 template <typename T>
 int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n,
                               int m_rows, int accumulate, T* M, double* msq_partial, double* xsq_partial,
-                              cudaStream_t st) {
-  const int r = right_gather_rows(n, sizeof(T));
-  APX_REQUIRE((size_t)n * sizeof(T) <= 227 * 1024, "n=%d too large for the right gather row block", n);
-#define APX_RG(RV) return right_gather_r<T, RV>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, st)
+                              cudaStream_t st, bool lam_padded) {
+  const int r = right_gather_rows(n, sizeof(T), k);
+  APX_REQUIRE((size_t)n * sizeof(T) + (size_t)(k + 8) * sizeof(int) <= 227 * 1024,
+              "n=%d too large for the right gather row block", n);
+#define APX_RG(RV) \
+  return right_gather_r<T, RV>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, lam_padded, st)
   switch (r) {
     case 1: APX_RG(1);
     case 2: APX_RG(2);
@@ -412,7 +570,7 @@ int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st) {
   template int launch_cycle_materialize<T>(const T*, const int*, int, int, T*, cudaStream_t);                 \
   template int launch_cycle_left_gather<T>(const T*, const T*, const int*, int, int, int, T*, cudaStream_t);  \
   template int launch_cycle_right_gather<T>(const T*, const int*, int, const T*, const int*, int, int, int, int, T*, \
-                                            double*, double*, cudaStream_t);                                 \
+                                            double*, double*, cudaStream_t, bool);                           \
   template int launch_sumsq<T>(const T*, size_t, double*, int*, cudaStream_t);
 APX_INST(float)
 APX_INST(double)

@@ -149,8 +149,7 @@ __global__ void __launch_bounds__(WM* WN * 32) gemm_kernel(const T* __restrict__
       const int k0 = kbeg + kt * BK;
       for (int e = tid; e < BK * mk; e += Cfg::kThreads) {
         const int r = e / mk, t = e - r * mk;
-        int c = k0 + r - mJ[t];
-        c %= mod_n;
+        int c = k0 + r - mJ[t];  // k0 + r < mod_n and 0 <= mJ[t] < mod_n
         if (c < 0) c += mod_n;
         if (c >= n0 && c < n0 + BN) b[r * Cfg::kSB + (c - n0)] = T(0);
       }

@@ -6,7 +6,7 @@ namespace apx {
 
 // ---- cycle.cu ----
 size_t cycle_energy_ws(int n);
-int right_gather_rows(int n, size_t elem);
+int right_gather_rows(int n, size_t elem, int k);
 template <typename T>
 int launch_cycle_energies(const T* A, int n, double* energies, double* norms, double* fro2, double* partial,
                           cudaStream_t st);
@@ -21,7 +21,8 @@ int launch_cycle_left_gather(const T* X, const T* lam, const int* J, int k, int 
                              cudaStream_t st);
 template <typename T>
 int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int m_rows,
-                              int accumulate, T* M, double* msq_partial, double* xsq_partial, cudaStream_t st);
+                              int accumulate, T* M, double* msq_partial, double* xsq_partial, cudaStream_t st,
+                              bool lam_padded = false);
 template <typename T>
 int launch_sumsq(const T* x, size_t cnt, double* partial, int* nparts, cudaStream_t st);
 int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st);
@@ -39,4 +40,12 @@ size_t qr_ws_bytes(int m, int l);
 template <typename TI, typename TO>
 int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, int64_t qrs, int64_t qcs, TO* Q2,
                       int64_t q2rs, int64_t q2cs, void* wsp, size_t ws_bytes, int method, cudaStream_t st);
+}  // namespace apx
+
+namespace apx {
+// ---- umma.cu (tcgen05 TF32) ----
+int umma_set_variant(int v);
+int umma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+              int64_t c_split_stride, int M, int N, int K, int splits, int accumulate, const int* mJ, int mk,
+              int mod_n, cudaStream_t st);
 }  // namespace apx

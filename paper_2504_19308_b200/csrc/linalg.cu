@@ -58,21 +58,23 @@ __global__ void gram_reduce_kernel(const double* __restrict__ part, int parts, i
 __global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict__ Gin, int l,
                                                         double* __restrict__ Rinv, int* __restrict__ flag) {
   if (*flag) return;
+  // One l x l buffer: the upper triangle holds G and is factored in place into R (G = R^T R);
+  // the strictly lower triangle then receives X = R^{-1} transposed (X[i][c] at (c, i)), with
+  // X's diagonal in a separate vector. 128 KB at l = 128.
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* G = reinterpret_cast<double*>(smem_raw);  // l x l, upper triangle used (mirrored)
-  double* R = G + l * l;
+  double* Gs = reinterpret_cast<double*>(smem_raw);
+  __shared__ double xdiag[kMaxL];
   __shared__ double s_maxd;
   __shared__ int s_bad;
   const int tid = threadIdx.x;
   for (int e = tid; e < l * l; e += blockDim.x) {
     const int i = e / l, j = e - i * l;
-    G[e] = i <= j ? Gin[e] : Gin[j * l + i];
-    R[e] = 0.0;
+    Gs[e] = i <= j ? Gin[e] : 0.0;
   }
   __syncthreads();
   if (tid == 0) {
     double md = 0.0;
-    for (int i = 0; i < l; ++i) md = fmax(md, G[i * l + i]);
+    for (int i = 0; i < l; ++i) md = fmax(md, Gs[i * l + i]);
     s_maxd = md;
     s_bad = 0;
   }
@@ -80,19 +82,19 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict
   const double tol = 4.0 * l * 2.220446049250313e-16 * s_maxd;
   for (int j = 0; j < l; ++j) {
     if (tid == 0) {
-      const double d2 = G[j * l + j];
+      const double d2 = Gs[j * l + j];
       if (!(d2 > tol)) s_bad = 1;
-      R[j * l + j] = sqrt(fmax(d2, 0.0));
+      Gs[j * l + j] = sqrt(fmax(d2, 0.0));
     }
     __syncthreads();
     if (s_bad) break;
-    const double d = R[j * l + j];
-    for (int c = j + 1 + tid; c < l; c += blockDim.x) R[j * l + c] = G[j * l + c] / d;
+    const double inv = 1.0 / Gs[j * l + j];
+    for (int c = j + 1 + tid; c < l; c += blockDim.x) Gs[j * l + c] *= inv;
     __syncthreads();
     const int rem = l - j - 1;
     for (int e = tid; e < rem * rem; e += blockDim.x) {
       const int r = j + 1 + e / rem, c = j + 1 + e % rem;
-      if (c >= r) G[r * l + c] -= R[j * l + r] * R[j * l + c];
+      if (c >= r) Gs[r * l + c] -= Gs[j * l + r] * Gs[j * l + c];
     }
     __syncthreads();
   }
@@ -100,13 +102,20 @@ __global__ void __launch_bounds__(1024) chol_inv_kernel(const double* __restrict
     if (tid == 0) *flag = 1;
     return;
   }
-  // X = R^{-1} (upper): column c by back substitution
+  // X = R^{-1} (upper), column c by back substitution; thread c owns row c of the lower part
   for (int c = tid; c < l; c += blockDim.x) {
-    for (int i = l - 1; i >= 0; --i) {
-      double s = (i == c) ? 1.0 : 0.0;
-      for (int j2 = i + 1; j2 <= c; ++j2) s -= R[i * l + j2] * Rinv[j2 * l + c];
-      Rinv[i * l + c] = i <= c ? s / R[i * l + i] : 0.0;
+    const double xc = 1.0 / Gs[c * l + c];
+    xdiag[c] = xc;
+    for (int i = c - 1; i >= 0; --i) {
+      double s = Gs[i * l + c] * xc;  // j = c term
+      for (int j2 = i + 1; j2 < c; ++j2) s = fma(Gs[i * l + j2], Gs[c * l + j2], s);
+      Gs[c * l + i] = -s / Gs[i * l + i];
     }
+  }
+  __syncthreads();
+  for (int e = tid; e < l * l; e += blockDim.x) {
+    const int i = e / l, c = e - i * l;
+    Rinv[e] = i < c ? Gs[c * l + i] : (i == c ? xdiag[c] : 0.0);
   }
 }
 
@@ -305,7 +314,7 @@ static int launch_gram(const TI* Y, int64_t rs, int64_t cs, int m, int l, const 
 }
 
 static int launch_chol(const double* G, int l, double* Rinv, int* flag, cudaStream_t st) {
-  const size_t smem = 2 * (size_t)l * l * sizeof(double);
+  const size_t smem = (size_t)l * l * sizeof(double);
   APX_CUDA(cudaFuncSetAttribute(chol_inv_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   chol_inv_kernel<<<1, 1024, smem, st>>>(G, l, Rinv, flag);
   APX_LAUNCH_CHECK();
