@@ -146,12 +146,108 @@ static void plan_mixed(Workspace& ws, MixedPlan& p, int dtype, int n, int l, int
   p.Z = ws.take<char>(nl);
   p.Bm = ws.take<char>(nl);
   p.W = ws.take<char>(nl);
-  p.part = ws.take<char>(nl * (size_t)std::max(1, mixed_gemm_splits(n, l)));
+  p.part = ws.take<char>(nl * (size_t)std::max(8, mixed_gemm_splits(n, l)));
   p.qr_bytes = qr_ws_bytes(n, l);
   p.qr_ws = ws.take<char>(p.qr_bytes);
   p.n_part_rows = (int)ceil_div(n, 1);
   p.msq = ws.take<double>(std::max<int>(n, kNumSMs * 4));
   p.asq = ws.take<double>(std::max<int>(n, kNumSMs * 4));
+}
+
+// fp32 GEMM stages of the mixed product on tcgen05 (umma.cu). Layout bits: 1 = A operand stored
+// [k][m] (MN-major), 2 = B operand stored [k][n] (MN-major), 4 = transposed store.
+struct UmmaStages {
+  static int splits(int n) { return std::max(1, std::min(8, (int)((2 * kNumSMs) / ceil_div(n, 128)))); }
+  static int umma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                       int64_t ldc, int64_t css, int M, int N, int K, int splits, int acc, const int* mJ, int mk,
+                       int mod_n, cudaStream_t st) {
+    return umma_tma_gemm(layout, bn, A, lda, B, ldb, C, ldc, css, M, N, K, splits, acc, mJ, mk, mod_n, st);
+  }
+  // Y[n x l] = A . X, X stored n x l (row-major)
+  static int a_times_x(const float* A, const float* X, float* Y, float* part, int n, int l, cudaStream_t st) {
+    const int s = splits(n);
+    APX_TRY(umma_gemm(2, 64, A, n, X, l, s > 1 ? part : Y, l, (int64_t)n * l, n, l, n, s, 0, nullptr, 0, 1, st));
+    if (s > 1) APX_TRY(launch_split_reduce_f32(part, s, (size_t)n * l, Y, st));
+    return OK;
+  }
+  // Z[n x l] = A^T . X   (= (X^T A)^T), X stored n x l
+  static int at_times_x(const float* A, const float* X, float* Z, float* part, int n, int l, cudaStream_t st) {
+    const int s = splits(n);
+    APX_TRY(umma_gemm(3, 64, A, n, X, l, s > 1 ? part : Z, l, (int64_t)n * l, n, l, n, s, 0, nullptr, 0, 1, st));
+    if (s > 1) APX_TRY(launch_split_reduce_f32(part, s, (size_t)n * l, Z, st));
+    return OK;
+  }
+  // Bm[l x n] = Q^T . A, computed as (A^T Q) stored transposed; Q stored n x l
+  static int qt_times_a(const float* A, const float* Q, float* Bm, float* part, int n, int l, cudaStream_t st) {
+    const int s = splits(n);
+    APX_TRY(umma_gemm(7, 64, A, n, Q, l, s > 1 ? part : Bm, n, (int64_t)l * n, n, l, n, s, 0, nullptr, 0, 1, st));
+    if (s > 1) APX_TRY(launch_split_reduce_f32(part, s, (size_t)n * l, Bm, st));
+    return OK;
+  }
+  // W[l x n] = Bm . dB, computed as (dB^T Bm^T) stored transposed; dB = B with kept cycles masked
+  static int bm_times_db(const float* B, const float* Bm, float* W, float* part, int n, int l, const int* J, int kc,
+                         cudaStream_t st) {
+    const int s = splits(n);
+    APX_TRY(umma_gemm(5, 64, B, n, Bm, n, s > 1 ? part : W, n, (int64_t)l * n, n, l, n, s, 0, J, kc, n, st));
+    if (s > 1) APX_TRY(launch_split_reduce_f32(part, s, (size_t)n * l, W, st));
+    return OK;
+  }
+  // M[n x n] = Q . W  (Q stored n x l, W stored l x n)
+  static int q_times_w(const float* Q, const float* W, float* M, int n, int l, cudaStream_t st) {
+    return umma_gemm(2, 256, Q, l, W, n, M, n, 0, n, n, l, 1, 0, nullptr, 0, 1, st);
+  }
+};
+
+static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int kc, int order, int q,
+                              const float* Omega, const int* fb, float* M, int* sb, double* scal,
+                              const MixedPlan& p, cudaStream_t st) {
+  stage_mark(0, st);
+  APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
+  APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, st));
+  if (fb) { if (kc) APX_CUDA(cudaMemcpyAsync(sb, fb, kc * sizeof(int), cudaMemcpyDeviceToDevice, st)); }
+  else APX_TRY(launch_topk(p.nr_b, n, kc, sb, st));
+  APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, st));
+  float* lb = (float*)p.lam_b;
+  APX_TRY(launch_cycle_extract<float>(B, n, sb, kc, lb, st));
+  APX_TRY(zero_pad_rows<float>(lb, kc, n, st));
+  stage_mark(1, st);
+  float *Y = (float*)p.Y, *Q = (float*)p.Q, *Qt = (float*)p.Qt, *Z = (float*)p.Z, *Bm = (float*)p.Bm,
+        *W = (float*)p.W, *part = (float*)p.part;
+  APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, st));
+  stage_mark(2, st);
+  APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, st)));
+  for (int it = 0; it < q; ++it) {
+    APX_TRY(UmmaStages::at_times_x(A, Q, Z, part, n, l, st));
+    APX_TRY((qr_orthonormalize<float, float>(Z, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, st)));
+    APX_TRY(UmmaStages::a_times_x(A, Q, Y, part, n, l, st));
+    APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, st)));
+  }
+  stage_mark(3, st);
+  APX_TRY(UmmaStages::qt_times_a(A, Q, Bm, part, n, l, st));
+  int parts = 0;
+  APX_TRY(launch_sumsq<float>(Bm, (size_t)l * n, p.msq, &parts, st));
+  APX_TRY(launch_sum_vector(p.msq, parts, scal + APX_S_KEPT_A, st));
+  stage_mark(4, st);
+  if (order == 1) {
+    APX_TRY(UmmaStages::bm_times_db(B, Bm, W, part, n, l, sb, kc, st));
+    stage_mark(5, st);
+    APX_TRY(UmmaStages::q_times_w(Q, W, M, n, l, st));
+    stage_mark(6, st);
+    APX_TRY(launch_cycle_right_gather<float>(A, nullptr, 0, lb, sb, kc, n, n, 1, M, p.msq, p.asq, st, true));
+    stage_mark(7, st);
+    const int rblocks = (int)ceil_div(n, right_gather_rows(n, sizeof(float), kc));
+    APX_TRY(launch_sum_vector(p.msq, rblocks, scal + APX_S_FRO2_M, st));
+    APX_TRY(launch_sum_vector(p.asq, rblocks, scal + APX_S_FRO2_A, st));
+  } else {
+    APX_TRY(launch_cycle_right_gather<float>(Bm, nullptr, 0, lb, sb, kc, n, l, 0, W, p.msq, nullptr, st, true));
+    APX_TRY(UmmaStages::q_times_w(Q, W, M, n, l, st));
+    APX_TRY(launch_sumsq<float>(M, (size_t)n * n, p.msq, &parts, st));
+    APX_TRY(launch_sum_vector(p.msq, parts, scal + APX_S_FRO2_M, st));
+    APX_TRY(launch_sumsq<float>(A, (size_t)n * n, p.asq, &parts, st));
+    APX_TRY(launch_sum_vector(p.asq, parts, scal + APX_S_FRO2_A, st));
+  }
+  stage_mark(8, st);
+  return OK;
 }
 
 template <typename T>
@@ -285,8 +381,11 @@ int apx_debug_umma_gemm(int layout, int bn, const float* A, int64_t lda, const f
                         int64_t ldc, int64_t M, int64_t N, int64_t K, int splits, int accumulate, const int32_t* mask_j,
                         int mask_k, int mod_n, void* stream) {
   APX_REQUIRE(M >= 1 && N >= 1 && K >= 1 && splits >= 1, "bad GEMM shape");
-  if (layout >= 64) { APX_TRY(umma_set_variant(layout >> 6)); layout &= 63; }
-  return umma_gemm(layout, bn, A, lda, B, ldb, C, ldc, (int64_t)M * ldc, (int)M, (int)N, (int)K, splits, accumulate,
+  const int64_t slice = (int64_t)((layout & 4) ? N : M) * ldc;
+  if (layout & 32)
+    return umma_tma_gemm(layout & 7, bn, A, lda, B, ldb, C, ldc, slice, (int)M, (int)N, (int)K, splits,
+                         accumulate, mask_j, mask_k, mod_n, S(stream));
+  return umma_gemm(layout, bn, A, lda, B, ldb, C, ldc, slice, (int)M, (int)N, (int)K, splits, accumulate,
                    mask_j, mask_k, mod_n, S(stream));
 }
 
@@ -312,6 +411,12 @@ int apx_mixed_first_order(int dtype, const void* A, const void* B, int64_t n, in
   plan_mixed(ws, p, dtype, (int)n, k_svd, k_cyc);
   APX_WS_CHECK(ws);
   const bool split3 = (flags & 1) != 0;
+  // tcgen05 path: fp32, l == 64 (one N=64 tile), n a multiple of 4 (16-byte rows), <= 128 masked
+  // cycles; 3xTF32 requests and other shapes use the mma.sync path
+  const bool umma_ok = dtype == F32 && !split3 && k_svd == 64 && (n % 4) == 0 && k_cyc <= 128 && !(flags & 2);
+  if (umma_ok)
+    return run_mixed_f32_umma((const float*)A, (const float*)B, (int)n, k_svd, k_cyc, order, power_iterations,
+                              (const float*)omega, force_sel_b, (float*)M, sel_b, scalars, p, S(stream));
   if (dtype == F32)
     return run_mixed<float>((const float*)A, (const float*)B, (int)n, k_svd, k_cyc, order, power_iterations,
                             (const float*)omega, force_sel_b, (float*)M, sel_b, scalars, p, split3, S(stream));

@@ -347,6 +347,13 @@ int gemm_skinny(int kind, const T* A, int64_t lda, const T* B, int64_t ldb, T* C
   return OK;
 }
 
+int launch_split_reduce_f32(const float* part, int splits, size_t count, float* out, cudaStream_t st) {
+  split_reduce_kernel<float, float><<<(unsigned)std::min<int64_t>(ceil_div(count, 256), kNumSMs * 8), 256, 0, st>>>(
+      part, splits, count, out);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
 template int gemm_skinny<float>(int, const float*, int64_t, const float*, int64_t, float*, int64_t, int, int, int,
                                 int, const int*, int, int, float*, int, bool, cudaStream_t);
 template int gemm_skinny<double>(int, const double*, int64_t, const double*, int64_t, double*, int64_t, int, int,

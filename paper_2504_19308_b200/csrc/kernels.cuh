@@ -32,6 +32,7 @@ int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st);
 namespace apx {
 // ---- gemm.cu ----
 int gemm_splits(int M, int N, int K, int BM, int BN);
+int launch_split_reduce_f32(const float* part, int splits, size_t count, float* out, cudaStream_t st);
 template <typename T>
 int gemm_skinny(int kind, const T* A, int64_t lda, const T* B, int64_t ldb, T* C, int64_t ldc, int M, int N, int K,
                 int accumulate, const int* mJ, int mk, int mod_n, T* part, int splits, bool split3, cudaStream_t st);
@@ -45,6 +46,9 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
 namespace apx {
 // ---- umma.cu (tcgen05 TF32) ----
 int umma_set_variant(int v);
+int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                  int64_t ldc, int64_t c_split_stride, int M, int N, int K, int splits, int accumulate,
+                  const int* mJ, int mk, int mod_n, cudaStream_t st);
 int umma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
               int64_t c_split_stride, int M, int N, int K, int splits, int accumulate, const int* mJ, int mk,
               int mod_n, cudaStream_t st);

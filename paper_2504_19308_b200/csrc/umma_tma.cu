@@ -1,0 +1,353 @@
+// Warp-specialized tcgen05 TF32 GEMM with TMA operand loads (the fp32 rSVD contractions).
+//
+//   C[M x N] (=|+=) opA[M x K] . opB[K x N]   (same operand conventions as umma.cu)
+//
+// 192 threads per CTA, one 128 x BN output tile (split-K slice):
+//   warp 0      TMA producer: one elected lane streams A/B K-tiles (BK = 32) into a STAGES-deep
+//               shared-memory ring, arming each stage's `full` mbarrier with the byte count.
+//   warp 1      TMEM allocator + MMA issuer: one lane issues tcgen05.mma.cta_group::1.kind::tf32
+//               (M=128, N=BN, K=8) x4 per stage and commits to the stage's `empty` mbarrier.
+//   warps 2..5  (MASK only) zero the kept-cycle entries of each landed A tile (dB^T), then
+//               epilogue: tcgen05.ld.32x32b.x32 from TMEM (warp%4 selects the lane quarter).
+// Layouts: K-major tiles use TMA SWIZZLE_128B <-> UMMA SWIZZLE_128B (rows of 128 B, 8-row atoms,
+// SBO = 1024 B, K advanced by 32 B per MMA); MN-major tiles (TF32 requires it) use TMA
+// SWIZZLE_128B_ATOM_32B <-> UMMA SWIZZLE_128B_BASE32B (boxes of 32 mn x 32 k = 4 KB; 4-row atoms,
+// SBO = 512 B between k-groups, LBO = 4 KB between 32-mn boxes).
+#include <cuda.h>
+
+#include <mutex>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace apx {
+namespace tma {
+
+constexpr int BM = 128, BK = 32, kThreads = 192;
+
+__device__ __forceinline__ uint32_t saddr(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(saddr(b)), "r"(c));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* b, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(saddr(b)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* b) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(saddr(b)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n}\n" ::"r"(saddr(b)),
+      "r"(phase)
+      : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
+          "r"(dst),
+      "l"(map), "r"(c0), "r"(c1), "r"(saddr(bar))
+      : "memory");
+}
+__device__ __forceinline__ uint64_t desc(uint32_t addr, uint32_t lbo, uint32_t sbo, uint32_t layout) {
+  return (uint64_t)((addr >> 4) & 0x3FFF) | ((uint64_t)((lbo >> 4) & 0x3FFF) << 16) |
+         ((uint64_t)((sbo >> 4) & 0x3FFF) << 32) | ((uint64_t)1 << 46) | ((uint64_t)(layout & 7) << 61);
+}
+__host__ __device__ constexpr uint32_t idesc(int M, int N, bool a_mn, bool b_mn) {
+  return (1u << 4) | (2u << 7) | (2u << 10) | ((a_mn ? 1u : 0u) << 15) | ((b_mn ? 1u : 0u) << 16) |
+         ((uint32_t)(N >> 3) << 17) | ((uint32_t)(M >> 4) << 24);
+}
+__device__ __forceinline__ void mma(uint32_t d, uint64_t a, uint64_t b, uint32_t id, uint32_t acc) {
+  asm volatile(
+      "{\n.reg .pred p;\nsetp.ne.b32 p, %4, 0;\n"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n}\n" ::"r"(d),
+      "l"(a), "l"(b), "r"(id), "r"(acc));
+}
+__device__ __forceinline__ void commit(uint64_t* b) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(saddr(b))
+               : "memory");
+}
+__device__ __forceinline__ void fence_after() { asm volatile("tcgen05.fence::after_thread_sync;" ::: "memory"); }
+__device__ __forceinline__ void fence_before() { asm volatile("tcgen05.fence::before_thread_sync;" ::: "memory"); }
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, float* v) {
+  uint32_t r[32];
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 {%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16,%17,%18,%"
+      "19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]),
+        "=r"(r[8]), "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]),
+        "=r"(r[16]), "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]),
+        "=r"(r[24]), "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+#pragma unroll
+  for (int i = 0; i < 32; ++i) v[i] = __uint_as_float(r[i]);
+}
+
+// byte offset of element (mn, k) in an MN-major tile built from 32x32 TMA boxes (ATOM_32B swizzle)
+__device__ __forceinline__ uint32_t mn_off(int mn, int k) {
+  const int e = mn & 31;
+  return (uint32_t)((mn >> 5) * 4096 + k * 128 + ((((e >> 3) ^ (k & 3)) & 3) << 5) + (e & 7) * 4);
+}
+
+template <int BN, int STAGES>
+struct Cfg {
+  static constexpr int kTileA = BM * BK * 4;
+  static constexpr int kTileB = BN * BK * 4;
+  static constexpr int kStage = kTileA + kTileB;
+  static constexpr size_t kSmem = (size_t)STAGES * kStage + 1024 /*align slack*/ + 256 /*barriers*/;
+  static constexpr int kTmemCols = BN;
+};
+
+template <int BN, int STAGES, bool A_MN, bool B_MN, bool TRANS_OUT, bool MASK>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                    float* __restrict__ C, int64_t ldc, int64_t c_split_stride, int M, int N, int K,
+                    int k_per_split, int accumulate, const int* __restrict__ mJ, int mk, int mod_n) {
+  using CF = Cfg<BN, STAGES>;
+  extern __shared__ unsigned char smem_raw[];
+  // 1024-byte alignment for the swizzled tiles
+  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * CF::kStage);
+  uint64_t* empty = full + STAGES;
+  uint64_t* masked = empty + STAGES;
+  uint64_t* done = masked + STAGES;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  __shared__ int sJ[128];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  const int kz = blockIdx.z;
+  const int kbeg = kz * k_per_split, kend = min(K, kbeg + k_per_split);
+  const int ktiles = (int)ceil_div(max(0, kend - kbeg), BK);
+
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < STAGES; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+      mbar_init(&masked[s], 128);
+    }
+    mbar_init(done, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(tmem_slot)),
+                 "r"(CF::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  for (int t = threadIdx.x; t < mk && t < 128; t += kThreads) sJ[t] = mJ[t];
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = saddr(smem);
+
+  if (warp == 0) {
+    // ---------------- TMA producer ----------------
+    if (lane == 0) {
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % STAGES;
+        if (kt >= STAGES) mbar_wait(&empty[s], (uint32_t)(((kt / STAGES) - 1) & 1));
+        mbar_expect_tx(&full[s], (uint32_t)CF::kStage);
+        const uint32_t a_s = sbase + s * CF::kStage, b_s = a_s + CF::kTileA;
+        const int k0 = kbeg + kt * BK;
+        if (!A_MN) {
+          tma_load_2d(a_s, &tmA, k0, m0, &full[s]);
+        } else {
+#pragma unroll
+          for (int a = 0; a < BM / 32; ++a) tma_load_2d(a_s + a * 4096, &tmA, m0 + 32 * a, k0, &full[s]);
+        }
+        if (!B_MN) {
+          tma_load_2d(b_s, &tmB, k0, n0, &full[s]);
+        } else {
+#pragma unroll
+          for (int a = 0; a < BN / 32; ++a) tma_load_2d(b_s + a * 4096, &tmB, n0 + 32 * a, k0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    // ---------------- MMA issuer ----------------
+    constexpr uint32_t id = idesc(BM, BN, A_MN, B_MN);
+    if (lane == 0) {
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % STAGES;
+        const uint32_t ph = (uint32_t)((kt / STAGES) & 1);
+        if (MASK) mbar_wait(&masked[s], ph);
+        else mbar_wait(&full[s], ph);
+        fence_after();
+        const uint32_t a_s = sbase + s * CF::kStage, b_s = a_s + CF::kTileA;
+#pragma unroll
+        for (int kk = 0; kk < BK / 8; ++kk) {
+          const uint64_t da = A_MN ? desc(a_s + kk * 1024, 4096, 512, 1) : desc(a_s + kk * 32, 16, 1024, 2);
+          const uint64_t db = B_MN ? desc(b_s + kk * 1024, 4096, 512, 1) : desc(b_s + kk * 32, 16, 1024, 2);
+          mma(tmem, da, db, id, (kt > 0 || kk > 0) ? 1u : 0u);
+        }
+        commit(&empty[s]);
+      }
+      if (ktiles > 0) commit(done);
+      else mbar_arrive(done);
+    }
+  } else {
+    // ---------------- mask fix-up (dB^T) + epilogue ----------------
+    const int et = threadIdx.x - 64;  // 0..127
+    if (MASK) {
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % STAGES;
+        mbar_wait(&full[s], (uint32_t)((kt / STAGES) & 1));
+        unsigned char* a_p = smem + (size_t)s * CF::kStage;
+        const int k0 = kbeg + kt * BK;
+        for (int e = et; e < BK * mk; e += 128) {
+          const int kk = e / mk, t = e - kk * mk;
+          int m = k0 + kk - sJ[t];
+          if (m < 0) m += mod_n;
+          if (m >= m0 && m < m0 + BM) *reinterpret_cast<float*>(a_p + mn_off(m - m0, kk)) = 0.f;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&masked[s]);
+      }
+    }
+    mbar_wait(done, 0);
+    fence_after();
+    const int quarter = warp & 3;
+    const int row = m0 + quarter * 32 + lane;
+    float* Cz = C + (size_t)kz * c_split_stride;
+#pragma unroll 1
+    for (int j0 = 0; j0 < BN; j0 += 32) {
+      float v[32];
+      if (ktiles > 0) {
+        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)j0, v);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 32; ++i) v[i] = 0.f;
+      }
+      if (row < M) {
+        if (!TRANS_OUT) {
+          float* p = Cz + (size_t)row * ldc + n0 + j0;
+          const bool fullrow = (n0 + j0 + 32 <= N) && ((((uintptr_t)p) & 15) == 0);
+          if (fullrow) {
+#pragma unroll
+            for (int i = 0; i < 32; i += 4) {
+              float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
+              if (accumulate) {
+                const float4 q = *reinterpret_cast<const float4*>(p + i);
+                o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
+              }
+              *reinterpret_cast<float4*>(p + i) = o;
+            }
+          } else {
+            for (int i = 0; i < 32; ++i)
+              if (n0 + j0 + i < N) p[i] = accumulate ? p[i] + v[i] : v[i];
+          }
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) {
+            const int col = n0 + j0 + i;
+            if (col < N) {
+              float* p = Cz + (size_t)col * ldc + row;
+              *p = accumulate ? *p + v[i] : v[i];
+            }
+          }
+        }
+      }
+    }
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CF::kTmemCols));
+  }
+}
+
+// ---- host: tensor maps through the driver entry point (no libcuda link dependency) ----------
+using EncodeFn = CUresult (*)(CUtensorMap*, CUtensorMapDataType, cuuint32_t, void*, const cuuint64_t*,
+                              const cuuint64_t*, const cuuint32_t*, const cuuint32_t*, CUtensorMapInterleave,
+                              CUtensorMapSwizzle, CUtensorMapL2promotion, CUtensorMapFloatOOBfill);
+
+static EncodeFn encode_fn() {
+  static EncodeFn fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<EncodeFn>(p);
+  });
+  return fn;
+}
+
+// 2-D fp32 tensor map over a row-major [rows][cols] array with leading dimension ld (elements).
+// kmajor: box = 32 cols x box_rows, 128B swizzle. mnmajor: box = 32 x 32, 128B/32B-atom swizzle.
+static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t cols, int64_t ld, int box_rows,
+                    bool mn_major) {
+  EncodeFn fn = encode_fn();
+  if (!fn) {
+    set_error("cuTensorMapEncodeTiled unavailable");
+    return E_CUDA;
+  }
+  cuuint64_t dims[2] = {(cuuint64_t)cols, (cuuint64_t)rows};
+  cuuint64_t strides[1] = {(cuuint64_t)(ld * 4)};
+  cuuint32_t box[2] = {32u, (cuuint32_t)(mn_major ? 32 : box_rows)};
+  cuuint32_t estr[2] = {1u, 1u};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, (void*)base, dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  if (r != CUDA_SUCCESS) {
+    set_error("cuTensorMapEncodeTiled failed (%d): rows=%lld cols=%lld ld=%lld", (int)r, (long long)rows,
+              (long long)cols, (long long)ld);
+    return E_CUDA;
+  }
+  return OK;
+}
+
+template <int BN, int STAGES, bool A_MN, bool B_MN, bool TRANS_OUT, bool MASK>
+static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
+                  int64_t c_split_stride, int M, int N, int K, int splits, int accumulate, const int* mJ, int mk,
+                  int mod_n, cudaStream_t st) {
+  using CF = Cfg<BN, STAGES>;
+  CUtensorMap ta, tb;
+  // A operand: K-major stored [M][K]; MN-major stored [K][M]
+  APX_TRY(make_map(&ta, A, A_MN ? K : M, A_MN ? M : K, lda, BM, A_MN));
+  APX_TRY(make_map(&tb, B, B_MN ? K : N, B_MN ? N : K, ldb, BN, B_MN));
+  const int kps = (int)(ceil_div(ceil_div(K, splits), BK) * BK);
+  dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)splits);
+  auto fn = gemm_tma_kernel<BN, STAGES, A_MN, B_MN, TRANS_OUT, MASK>;
+  APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem));
+  fn<<<grid, kThreads, CF::kSmem, st>>>(ta, tb, C, ldc, c_split_stride, M, N, K, kps, accumulate, mJ, mk, mod_n);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+}  // namespace tma
+
+// Same contract as umma_gemm (umma.cu); requires 16-byte aligned bases and leading dimensions,
+// M, N multiples of 32 for MN-major operands. layout bits: 1 A MN-major, 2 B MN-major, 4 C^T.
+int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
+                  int64_t ldc, int64_t c_split_stride, int M, int N, int K, int splits, int accumulate,
+                  const int* mJ, int mk, int mod_n, cudaStream_t st) {
+  APX_REQUIRE(mk <= 128, "umma_tma_gemm: at most 128 masked shifts");
+  APX_REQUIRE(((uintptr_t)A % 16) == 0 && ((uintptr_t)B % 16) == 0 && (lda % 4) == 0 && (ldb % 4) == 0,
+              "umma_tma_gemm: 16-byte aligned operands required");
+  const bool mask = mJ != nullptr && mk > 0;
+#define APX_TL(BNV, ST, L, MK)                                                                                \
+  if (bn == BNV && layout == L && mask == MK)                                                                 \
+    return tma::launch<BNV, ST, (L & 1) != 0, (L & 2) != 0, (L & 4) != 0, MK>(A, lda, B, ldb, C, ldc,          \
+                                                                              c_split_stride, M, N, K, splits, \
+                                                                              accumulate, mJ, mk, mod_n, st);
+  APX_TL(64, 4, 0, false) APX_TL(64, 4, 1, false) APX_TL(64, 4, 2, false) APX_TL(64, 4, 3, false)
+  APX_TL(64, 4, 4, false) APX_TL(64, 4, 5, false) APX_TL(64, 4, 6, false) APX_TL(64, 4, 7, false)
+  APX_TL(64, 4, 1, true) APX_TL(64, 4, 5, true)
+  APX_TL(128, 4, 0, false) APX_TL(128, 4, 2, false) APX_TL(256, 3, 0, false) APX_TL(256, 3, 2, false)
+#undef APX_TL
+  set_error("umma_tma_gemm: unsupported layout %d / BN %d / mask %d", layout, bn, (int)mask);
+  return E_ARG;
+}
+
+}  // namespace apx

@@ -19,12 +19,13 @@ def run(layout, bn, M, N, K, splits=1, accumulate=0, mask=None, mod_n=1, trans_o
     rng = np.random.default_rng(layout * 1000 + bn + M + N + K)
     a = tf32(rng.standard_normal((M, K)))
     b = tf32(rng.standard_normal((K, N)))
-    A_st = a.T.copy() if layout & 1 else a            # MN-major A is stored [k][m]
-    B_st = b.copy() if layout & 2 else b.T.copy()     # MN-major B stored [k][n], else [n][k]
+    L = layout & 7
+    A_st = a.T.copy() if L & 1 else a            # MN-major A is stored [k][m]
+    B_st = b.copy() if L & 2 else b.T.copy()     # MN-major B stored [k][n], else [n][k]
     dA = torch.from_numpy(A_st).cuda()
     dB = torch.from_numpy(B_st).cuda()
-    ldc = M if layout & 4 else N
-    rows_c = N if layout & 4 else M
+    ldc = M if L & 4 else N
+    rows_c = N if L & 4 else M
     C0 = rng.standard_normal((rows_c, ldc)).astype(np.float32) if accumulate else np.zeros((rows_c, ldc), np.float32)
     dC = torch.from_numpy(np.tile(C0, (splits, 1))).cuda()
     dm = None
@@ -42,10 +43,10 @@ def run(layout, bn, M, N, K, splits=1, accumulate=0, mask=None, mod_n=1, trans_o
         a64 = np.where(np.isin((k_idx - m_idx) % mod_n, mask), 0.0, a64)
     ref = a64 @ b.astype(np.float64)
     got = C.sum(axis=0) if splits > 1 else C[0]
-    if layout & 4:
+    if L & 4:
         got = got.T
     if accumulate:
-        ref = ref + (C0.T if layout & 4 else C0)
+        ref = ref + (C0.T if L & 4 else C0)
     return float(np.linalg.norm(got - ref) / np.linalg.norm(ref))
 
 
@@ -72,3 +73,22 @@ def test_umma_accumulate():
 def test_umma_masked_mn_a():
     # A operand = dB^T with cycles {0, 3, 17} of a 256-cycle pattern masked
     assert run(1, 64, 256, 64, 256, mask=[0, 3, 17], mod_n=256) < 1e-5
+
+
+# ---- TMA + warp-specialized variant (layout bit 32) ----
+@pytest.mark.parametrize("layout", range(8))
+def test_umma_tma_layouts_bn64(layout):
+    assert run(32 | layout, 64, 256, 64, 96) < 1e-5
+
+
+@pytest.mark.parametrize("layout", [0, 2])
+@pytest.mark.parametrize("bn", [128, 256])
+def test_umma_tma_wide(layout, bn):
+    assert run(32 | layout, bn, 384, 512, 64) < 1e-5
+
+
+def test_umma_tma_ragged_split_mask():
+    assert run(32 | 1, 64, 256, 64, 336, splits=3) < 1e-5
+    assert run(32 | 5, 64, 256, 64, 256, splits=2) < 1e-5
+    assert run(32 | 1, 64, 256, 64, 256, mask=[0, 3, 17], mod_n=256) < 1e-5
+    assert run(32 | 2, 256, 256, 512, 64, accumulate=1) < 1e-5
