@@ -98,6 +98,39 @@ int apx_mixed_first_order(int dtype, const void* A, const void* B, int64_t n, in
                           const int32_t* force_sel_b, int flags, void* M, int32_t* sel_b,
                           double* scalars, void* ws, size_t ws_bytes, void* stream);
 
+/* ------------------------------------------------------------------ randomized SVD path ---- */
+/* randomized_partial_svd (svd.py:83-119), fp64: sketch width l (= k in the reference; l > k is
+ * the oversampled variant of config C1), q power iterations, host-drawn Gaussian omega (n x l,
+ * rng.standard_normal((n, l)) as svd.py:105-106). Outputs U (m x k), sigma (k, descending),
+ * V (n x k); scalars: APX_S_FRO2_A = ||A||_F^2, APX_S_KEPT_A = sum sigma^2. */
+size_t apx_rsvd_workspace(int dtype, int64_t m, int64_t n, int l);
+int apx_rsvd(int dtype, const void* A, int64_t m, int64_t n, int l, int k, int power_iterations,
+             const void* omega, void* U, double* sigma, void* V, double* scalars,
+             void* ws, size_t ws_bytes, void* stream);
+
+/* svd_first_order_multiply (svd.py:138-200), fp64, A m x n, B n x p, sketches l_a/l_b kept
+ * k_a/k_b (k = l in the reference; k < l truncates an oversampled sketch), omega_a from
+ * default_rng([seed,0]), omega_b from default_rng([seed,1]) (svd.py:161-162).
+ * order 0: M = Ahat Bhat; order 1: M = Ahat B + dA Bhat. */
+size_t apx_svd_first_order_workspace(int dtype, int64_t m, int64_t n, int64_t p, int l_a, int l_b);
+int apx_svd_first_order(int dtype, const void* A, const void* B, int64_t m, int64_t n, int64_t p,
+                        int l_a, int k_a, int l_b, int k_b, int power_iterations, int order,
+                        const void* omega_a, const void* omega_b, void* M, double* scalars,
+                        void* ws, size_t ws_bytes, void* stream);
+
+/* qr_decompose (svd.py:63-69): thin QR of Y (m x k, m >= k), Householder with LAPACK's
+ * reflector signs; R exactly upper triangular. */
+size_t apx_qr_workspace(int dtype, int64_t m, int64_t k);
+int apx_qr(int dtype, const void* Y, int64_t m, int64_t k, void* Q, void* R, void* ws,
+           size_t ws_bytes, void* stream);
+
+/* Dense product C (+)= op(A) op(B) (matmul_naive core.py:48-61 / svd_reconstruct svd.py:133-135):
+ * fp64 DMMA, fp32 3xTF32. trans_a: A stored K x M; trans_b: B stored N x K. */
+size_t apx_gemm_workspace(int dtype, int64_t M, int64_t N, int64_t K, int trans_a, int trans_b);
+int apx_gemm(int dtype, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const void* A,
+             int64_t lda, const void* B, int64_t ldb, void* C, int64_t ldc, int accumulate,
+             void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------------- diagnostics ---- */
 /* The tcgen05 TF32 GEMM used by the fp32 rSVD stages, exposed for kernel-level tests:
  * C (+)= opA . opB with layout bit 1 = A stored [k][m] (MN-major), bit 2 = B stored [k][n]

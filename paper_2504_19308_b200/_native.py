@@ -35,6 +35,16 @@ SIGNATURES = {
                                         _vp, _vp, _sz, _vp]),
     "apx_debug_umma_gemm": (C.c_int, [_i32, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32,
                                       _vp, _i32, _i32, _vp]),
+    "apx_rsvd_workspace": (_sz, [_i32, _i64, _i64, _i32]),
+    "apx_rsvd": (C.c_int, [_i32, _vp, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
+    "apx_svd_first_order_workspace": (_sz, [_i32, _i64, _i64, _i64, _i32, _i32]),
+    "apx_svd_first_order": (C.c_int, [_i32, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32, _i32, _i32, _i32, _vp,
+                                      _vp, _vp, _vp, _vp, _sz, _vp]),
+    "apx_qr_workspace": (_sz, [_i32, _i64, _i64]),
+    "apx_qr": (C.c_int, [_i32, _vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "apx_gemm_workspace": (_sz, [_i32, _i64, _i64, _i64, _i32, _i32]),
+    "apx_gemm": (C.c_int, [_i32, _i32, _i32, _i64, _i64, _i64, _vp, _i64, _vp, _i64, _vp, _i64, _i32, _vp, _sz,
+                           _vp]),
     "apx_mixed_first_order_workspace": (_sz, [_i32, _i64, _i32, _i32, _i32]),
     "apx_mixed_first_order": (C.c_int, [_i32, _vp, _vp, _i64, _i32, _i32, _i32, _i32, _vp, _vp, _i32, _vp,
                                         _vp, _vp, _vp, _sz, _vp]),

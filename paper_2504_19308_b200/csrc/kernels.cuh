@@ -53,3 +53,11 @@ int umma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, i
               int64_t c_split_stride, int M, int N, int K, int splits, int accumulate, const int* mJ, int mk,
               int mod_n, cudaStream_t st);
 }  // namespace apx
+
+namespace apx {
+// ---- svd.cu ----
+int launch_small_svd(const double* W, int l, double* U, double* S, double* V, double* VT, cudaStream_t st);
+int launch_axpy2d(double* y, int64_t ldy, const double* x, int64_t ldx, int rows, int cols, double alpha,
+                  const double* rowscale, int overwrite, cudaStream_t st);
+int launch_sumsq_prefix(const double* s, int k, double* out, cudaStream_t st);
+}  // namespace apx

@@ -1,0 +1,184 @@
+// Small dense SVD for the randomized SVD (K14; reference svd.py:113 -> LAPACK gesdd).
+//
+// One CTA runs one-sided (Hestenes) Jacobi on a square l x l matrix W (l <= 128) held
+// column-major in shared memory: W V' = U' S. Rounds of the circle tournament rotate l/2
+// disjoint column pairs in parallel (one warp per pair, lanes over rows, fp64), sweeps repeat
+// until no pair is rotated. Singular values come out as column norms, sorted descending (stable
+// on ties); columns with zero norm are completed to an orthonormal basis by Gram-Schmidt on unit
+// vectors, so U' is orthonormal even for rank-deficient inputs (zero / rank-1 test matrices,
+// test_svd.py:56-77), where a Gram-matrix eigensolver would lose the tiny singular values.
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace apx {
+
+constexpr int kSvdMax = 128;
+
+__global__ void __launch_bounds__(512) hestenes_svd_kernel(const double* __restrict__ Win, int l,
+                                                           double* __restrict__ Uout, double* __restrict__ Sout,
+                                                           double* __restrict__ Vout, double* __restrict__ VoutT) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int le = l + (l & 1);  // even number of columns (pad with a zero column)
+  double* Wc = reinterpret_cast<double*>(smem_raw);  // le columns x l rows, column-major
+  double* Vc = Wc + (size_t)le * l;                  // le x le
+  __shared__ int s_rot;
+  __shared__ int perm[kSvdMax + 2];
+  __shared__ double norms[kSvdMax + 2];
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
+  for (int e = tid; e < le * l; e += blockDim.x) {
+    const int j = e / l, i = e - j * l;
+    Wc[e] = j < l ? Win[i * l + j] : 0.0;
+  }
+  for (int e = tid; e < le * le; e += blockDim.x) {
+    const int j = e / le, i = e - j * le;
+    Vc[e] = (i == j) ? 1.0 : 0.0;
+  }
+  __syncthreads();
+  const double eps = 2.220446049250313e-16;
+  for (int sweep = 0; sweep < 60; ++sweep) {
+    if (tid == 0) s_rot = 0;
+    __syncthreads();
+    for (int round = 0; round < le - 1; ++round) {
+      for (int pr = warp; pr < le / 2; pr += nw) {
+        // circle method: position 0 fixed, others rotate
+        int a = (pr == 0) ? 0 : 1 + (pr - 1 + round) % (le - 1);
+        int b = 1 + (le - 2 - pr + round) % (le - 1);
+        if (a > b) { const int t = a; a = b; b = t; }
+        double* wa = Wc + (size_t)a * l;
+        double* wb = Wc + (size_t)b * l;
+        double al = 0.0, be = 0.0, ga = 0.0;
+        for (int i = lane; i < l; i += 32) {
+          al = fma(wa[i], wa[i], al);
+          be = fma(wb[i], wb[i], be);
+          ga = fma(wa[i], wb[i], ga);
+        }
+        al = warp_sum(al);
+        be = warp_sum(be);
+        ga = warp_sum(ga);
+        if (ga != 0.0 && fabs(ga) > eps * l * sqrt(al * be)) {
+          const double zeta = (be - al) / (2.0 * ga);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
+          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
+          for (int i = lane; i < l; i += 32) {
+            const double x = wa[i], y = wb[i];
+            wa[i] = c * x - s * y;
+            wb[i] = s * x + c * y;
+          }
+          double* va = Vc + (size_t)a * le;
+          double* vb = Vc + (size_t)b * le;
+          for (int i = lane; i < le; i += 32) {
+            const double x = va[i], y = vb[i];
+            va[i] = c * x - s * y;
+            vb[i] = s * x + c * y;
+          }
+          if (lane == 0) s_rot = 1;
+        }
+      }
+      __syncthreads();
+    }
+    if (!s_rot) break;
+    __syncthreads();
+  }
+  // column norms, stable descending order
+  for (int j = tid; j < l; j += blockDim.x) {
+    double s = 0.0;
+    for (int i = 0; i < l; ++i) s = fma(Wc[(size_t)j * l + i], Wc[(size_t)j * l + i], s);
+    norms[j] = sqrt(s);
+  }
+  __syncthreads();
+  for (int j = tid; j < l; j += blockDim.x) {
+    int rank = 0;
+    for (int q = 0; q < l; ++q) rank += (norms[q] > norms[j]) || (norms[q] == norms[j] && q < j);
+    perm[rank] = j;
+  }
+  __syncthreads();
+  // U' columns = W columns / sigma (zero columns completed below); outputs row-major l x l
+  for (int e = tid; e < l * l; e += blockDim.x) {
+    const int i = e / l, r = e - i * l;  // row i, output column r
+    const int j = perm[r];
+    const double sg = norms[j];
+    Uout[e] = sg > 0.0 ? Wc[(size_t)j * l + i] / sg : 0.0;
+    Vout[e] = Vc[(size_t)j * le + i];
+  }
+  for (int r = tid; r < l; r += blockDim.x) Sout[r] = norms[perm[r]];
+  if (VoutT != nullptr)
+    for (int e = tid; e < l * l; e += blockDim.x) {
+      const int r = e / l, i = e - r * l;  // V'^T[r][i] = V'[i][r]
+      VoutT[e] = Vc[(size_t)perm[r] * le + i];
+    }
+  __threadfence_block();
+  __syncthreads();
+  if (tid == 0) {
+    // Gram-Schmidt completion of zero columns (rank-deficient input)
+    for (int r = 0; r < l; ++r) {
+      if (norms[perm[r]] > 0.0) continue;
+      for (int cand = 0; cand < l; ++cand) {
+        double v[kSvdMax];
+        for (int i = 0; i < l; ++i) v[i] = (i == cand) ? 1.0 : 0.0;
+        for (int pass = 0; pass < 2; ++pass)
+          for (int q = 0; q < l; ++q) {
+            if (q == r) continue;
+            double d = 0.0;
+            for (int i = 0; i < l; ++i) d += Uout[i * l + q] * v[i];
+            for (int i = 0; i < l; ++i) v[i] -= d * Uout[i * l + q];
+          }
+        double nv = 0.0;
+        for (int i = 0; i < l; ++i) nv += v[i] * v[i];
+        nv = sqrt(nv);
+        if (nv > 0.5) {
+          for (int i = 0; i < l; ++i) Uout[i * l + r] = v[i] / nv;
+          break;
+        }
+      }
+    }
+  }
+}
+
+int launch_small_svd(const double* W, int l, double* U, double* S, double* V, double* VT, cudaStream_t st) {
+  APX_REQUIRE(l >= 1 && l <= kSvdMax, "small SVD size %d outside [1, %d]", l, kSvdMax);
+  const int le = l + (l & 1);
+  const size_t smem = ((size_t)le * l + (size_t)le * le) * sizeof(double);
+  APX_CUDA(cudaFuncSetAttribute(hestenes_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  hestenes_svd_kernel<<<1, 512, smem, st>>>(W, l, U, S, V, VT);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+// y[i*ldy + j] (+)= alpha * x[i*ldx + j] * (rowscale ? rowscale[i] : 1), i < rows, j < cols
+__global__ void axpy2d_kernel(double* __restrict__ y, int64_t ldy, const double* __restrict__ x, int64_t ldx,
+                              int rows, int cols, double alpha, const double* __restrict__ rowscale, int overwrite) {
+  const size_t total = (size_t)rows * cols;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / cols), j = (int)(e % cols);
+    double v = alpha * x[(size_t)i * ldx + j];
+    if (rowscale) v *= rowscale[i];
+    double* py = y + (size_t)i * ldy + j;
+    *py = overwrite ? v : *py + v;
+  }
+}
+
+int launch_axpy2d(double* y, int64_t ldy, const double* x, int64_t ldx, int rows, int cols, double alpha,
+                  const double* rowscale, int overwrite, cudaStream_t st) {
+  if (rows <= 0 || cols <= 0) return OK;
+  const int blocks = (int)std::min<int64_t>(ceil_div((int64_t)rows * cols, 256), kNumSMs * 8);
+  axpy2d_kernel<<<blocks, 256, 0, st>>>(y, ldy, x, ldx, rows, cols, alpha, rowscale, overwrite);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+// out = sum_{i<k} s[i]^2 (single thread, fixed order)
+__global__ void sumsq_prefix_kernel(const double* __restrict__ s, int k, double* __restrict__ out) {
+  if (threadIdx.x == 0 && blockIdx.x == 0) {
+    double a = 0.0;
+    for (int i = 0; i < k; ++i) a += s[i] * s[i];
+    *out = a;
+  }
+}
+
+int launch_sumsq_prefix(const double* s, int k, double* out, cudaStream_t st) {
+  sumsq_prefix_kernel<<<1, 32, 0, st>>>(s, k, out);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+}  // namespace apx
