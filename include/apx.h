@@ -98,6 +98,56 @@ int apx_mixed_first_order(int dtype, const void* A, const void* B, int64_t n, in
                           const int32_t* force_sel_b, int flags, void* M, int32_t* sel_b,
                           double* scalars, void* ws, size_t ws_bytes, void* stream);
 
+/* ---------------------------------------------------------------------- circulant path ---- */
+/* circulant_first_order_multiply (circulant.py:164-218): A, B n x n fp64 or complex128 (dtype
+ * APX_F64 / APX_C128), k components each, order 0 (Ahat B) / 1 (Ahat B + dA Bhat); M is n x n
+ * complex128. Selections (ties -> lower index, ascending) land in sel_a / sel_b; force_sel_*
+ * override them (near-tie protocol). scalars: FRO2_A/B, KEPT_A/B (= n sum mag^2), FRO2_M. */
+size_t apx_circulant_first_order_workspace(int dtype, int64_t n, int k, int order);
+int apx_circulant_first_order(int dtype, const void* A, const void* B, int64_t n, int k, int order,
+                              const int32_t* force_sel_a, const int32_t* force_sel_b, void* M,
+                              int32_t* sel_a, int32_t* sel_b, double* scalars, void* ws,
+                              size_t ws_bytes, void* stream);
+
+/* circulant_decompose (circulant.py:73-91): columns (n x n complex128, row k = first column of
+ * R_k) and magnitudes (n doubles). */
+size_t apx_circulant_decompose_workspace(int dtype, int64_t n);
+int apx_circulant_decompose(int dtype, const void* A, int64_t n, void* columns, double* magnitudes,
+                            void* ws, size_t ws_bytes, void* stream);
+
+/* circulant_materialize (circulant.py:116-127) from the k selected first columns Ssel (k x n). */
+size_t apx_circulant_materialize_workspace(int64_t n);
+int apx_circulant_materialize(const void* Ssel, const int32_t* sel, int k, int64_t n, void* out,
+                              void* ws, size_t ws_bytes, void* stream);
+
+/* circulant_component (circulant.py:94-108): first column of R_kk by cycle averaging. Workspace:
+ * apx_circulant_materialize_workspace(n). */
+int apx_circulant_component(int dtype, const void* A, int64_t n, int kk, void* out, void* ws,
+                            size_t ws_bytes, void* stream);
+
+/* ------------------------------------------------------------------ core.py primitives ---- */
+/* unitary_dft (core.py:82-97) on `batch` complex128 vectors (element i of vector b at
+ * x[b*dist + i*stride]); inverse = 0 applies W, 1 applies W*. Any length (direct DFT for
+ * non-powers of two). */
+size_t apx_unitary_dft_workspace(int64_t n);
+int apx_unitary_dft(const void* x, void* y, int64_t n, int64_t batch, int64_t stride, int64_t dist,
+                    int inverse, void* ws, size_t ws_bytes, void* stream);
+
+/* cycle_reorder (mode 0 right / 1 left) and cycle_reorder_inverse (2 right / 3 left),
+ * core.py:106-137, elements of 8 (fp64) or 16 (complex128) bytes. */
+int apx_cycle_layout(int elem_bytes, const void* in, int64_t n, int mode, void* out, void* stream);
+
+/* apply_cycle_power (core.py:140-154): side 0 = C^k M (rows down), 1 = M C^k (columns left). */
+int apx_apply_cycle_power(int elem_bytes, const void* in, int64_t rows, int64_t cols, int64_t k,
+                          int side, void* out, void* stream);
+
+/* frobenius (core.py:64-79) / relative_error (core.py:157-166) reductions: mode 0 writes
+ * out[0..1] = <A,B>_F = sum conj(A) B (re, im); mode 1 writes (||B - A||_F^2, ||B||_F^2).
+ * dtype_a / dtype_b: APX_F64 or APX_C128. */
+size_t apx_pair_reduce_workspace(void);
+int apx_pair_reduce(int dtype_a, const void* A, int dtype_b, const void* B, int64_t count, int mode,
+                    double* out, void* ws, size_t ws_bytes, void* stream);
+
 /* ------------------------------------------------------------------ randomized SVD path ---- */
 /* randomized_partial_svd (svd.py:83-119), fp64: sketch width l (= k in the reference; l > k is
  * the oversampled variant of config C1), q power iterations, host-drawn Gaussian omega (n x l,

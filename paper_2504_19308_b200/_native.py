@@ -35,6 +35,20 @@ SIGNATURES = {
                                         _vp, _vp, _sz, _vp]),
     "apx_debug_umma_gemm": (C.c_int, [_i32, _i32, _vp, _i64, _vp, _i64, _vp, _i64, _i64, _i64, _i64, _i32, _i32,
                                       _vp, _i32, _i32, _vp]),
+    "apx_circulant_first_order_workspace": (_sz, [_i32, _i64, _i32, _i32]),
+    "apx_circulant_first_order": (C.c_int, [_i32, _vp, _vp, _i64, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _vp,
+                                            _sz, _vp]),
+    "apx_circulant_decompose_workspace": (_sz, [_i32, _i64]),
+    "apx_circulant_decompose": (C.c_int, [_i32, _vp, _i64, _vp, _vp, _vp, _sz, _vp]),
+    "apx_circulant_materialize_workspace": (_sz, [_i64]),
+    "apx_circulant_materialize": (C.c_int, [_vp, _vp, _i32, _i64, _vp, _vp, _sz, _vp]),
+    "apx_circulant_component": (C.c_int, [_i32, _vp, _i64, _i32, _vp, _vp, _sz, _vp]),
+    "apx_unitary_dft_workspace": (_sz, [_i64]),
+    "apx_unitary_dft": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i32, _vp, _sz, _vp]),
+    "apx_cycle_layout": (C.c_int, [_i32, _vp, _i64, _i32, _vp, _vp]),
+    "apx_apply_cycle_power": (C.c_int, [_i32, _vp, _i64, _i64, _i64, _i32, _vp, _vp]),
+    "apx_pair_reduce_workspace": (_sz, []),
+    "apx_pair_reduce": (C.c_int, [_i32, _vp, _i32, _vp, _i64, _i32, _vp, _vp, _sz, _vp]),
     "apx_rsvd_workspace": (_sz, [_i32, _i64, _i64, _i32]),
     "apx_rsvd": (C.c_int, [_i32, _vp, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "apx_svd_first_order_workspace": (_sz, [_i32, _i64, _i64, _i64, _i32, _i32]),

@@ -1,0 +1,513 @@
+// Circulant decomposition A = sum_k R_k D^k and its truncated first-order product
+// (reference circulant.py), plus the unitary DFT and cycle-layout primitives of core.py.
+//
+//   decompose   S[t][j] = (1/n) sum_i A[(i+j)%n][i] w^{-ti}   (circulant.py:73-91: W applied to
+//               the right cycle layout, / sqrt(n)); magnitudes[t] = ||S[t,:]||_2
+//   left        term1[:, c] = W* sum_t diag(L_t) C^t (W B[:, c]),  L_t = fft(S_A[t])  (:136-147)
+//   right       term2[r, :] = conj(W* sum_t C^{-t} diag(conj L_t) W conj(dA[r, :]))     (:150-161)
+//               with dA[r, c] = A[r, c] - sum_t S_A[t][(r-c)%n] w^{tc} formed on the fly (:116-127,197)
+// Every length-n transform runs in shared memory (fft.cuh); term1 is column-local and term2
+// row-local, so each CTA owns one column (left) or one row (right) end to end.
+#include "../../include/apx.h"
+#include "common.cuh"
+#include "fft.cuh"
+#include "kernels.cuh"
+
+namespace apx {
+
+__global__ void roots_kernel(double2* roots, int n) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < n; k += gridDim.x * blockDim.x) {
+    double s, c;
+    sincospi(2.0 * (double)k / (double)n, &s, &c);
+    roots[k] = make_double2(c, -s);  // exp(-2 pi i k / n)
+  }
+}
+
+void launch_roots(double2* roots, int n, cudaStream_t st) {
+  roots_kernel<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(n, 256), 1024)), 256, 0, st>>>(roots, n);
+}
+
+template <typename T>
+__device__ __forceinline__ double2 ld_c(const T* p, size_t i);
+template <>
+__device__ __forceinline__ double2 ld_c<double>(const double* p, size_t i) {
+  return make_double2(__ldg(p + i), 0.0);
+}
+template <>
+__device__ __forceinline__ double2 ld_c<double2>(const double2* p, size_t i) {
+  return __ldg(p + i);
+}
+
+static size_t fft_smem_bytes(int n, int buffers) {
+  return (size_t)(buffers + (is_pow2(n) ? 0 : 1)) * n * sizeof(double2);
+}
+
+// ---------------------------------------------------------------------------------------------
+// decompose: CTA handles cycles [j0, j0 + cpc); per cycle: gather, FFT, scale, store S column
+// and fold |S[t][j]|^2 into a per-CTA partial of the magnitudes.
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(512) circ_decompose_kernel(const T* __restrict__ A, int n, int cpc,
+                                                             const double2* __restrict__ roots,
+                                                             double2* __restrict__ S, double* __restrict__ mag2_part) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* x = reinterpret_cast<double2*>(smem_raw);
+  double2* scratch = x + n;
+  double* m2 = reinterpret_cast<double*>(scratch + (is_pow2(n) ? 0 : n));
+  for (int t = threadIdx.x; t < n; t += blockDim.x) m2[t] = 0.0;
+  const double inv_n = 1.0 / n;
+  const int j0 = blockIdx.x * cpc, j1 = min(n, j0 + cpc);
+  for (int j = j0; j < j1; ++j) {
+    for (int i = threadIdx.x; i < n; i += blockDim.x) {
+      int r = i + j;
+      if (r >= n) r -= n;
+      x[i] = ld_c<T>(A, (size_t)r * n + i);  // right layout: cycle j, entry i = A[(i+j)%n][i]
+    }
+    __syncthreads();
+    fft_block(x, scratch, n, roots, false);
+    for (int t = threadIdx.x; t < n; t += blockDim.x) {
+      const double2 v = cscale(x[t], inv_n);
+      if (S) S[(size_t)t * n + j] = v;
+      m2[t] = fma(v.x, v.x, fma(v.y, v.y, m2[t]));
+    }
+    __syncthreads();
+  }
+  for (int t = threadIdx.x; t < n; t += blockDim.x) mag2_part[(size_t)blockIdx.x * n + t] = m2[t];
+}
+
+__global__ void mag_finalize_kernel(const double* __restrict__ part, int parts, int n, double* __restrict__ mag) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t >= n) return;
+  double s = 0.0;
+  for (int p = 0; p < parts; ++p) s += part[(size_t)p * n + t];
+  mag[t] = sqrt(s);
+}
+
+// Selected spectrum rows: Ssel[q] = S[sel[q]], L[q] = fft(S[sel[q]]) (unnormalised, :145)
+__global__ void __launch_bounds__(512) circ_spectra_kernel(const double2* __restrict__ S, int n,
+                                                           const int* __restrict__ sel,
+                                                           const double2* __restrict__ roots,
+                                                           double2* __restrict__ Ssel, double2* __restrict__ L) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* x = reinterpret_cast<double2*>(smem_raw);
+  double2* scratch = x + n;
+  const int q = blockIdx.x;
+  const double2* row = S + (size_t)sel[q] * n;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double2 v = row[i];
+    x[i] = v;
+    if (Ssel) Ssel[(size_t)q * n + i] = v;
+  }
+  __syncthreads();
+  fft_block(x, scratch, n, roots, false);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) L[(size_t)q * n + i] = x[i];
+}
+
+// ---------------------------------------------------------------------------------------------
+// term1, one column per CTA: FB = W B[:,c]; acc[p] = sum_t L_t[p] FB[(p - t) % n]; M[:,c] = W* acc
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(512) circ_left_kernel(const T* __restrict__ B, int n, const double2* __restrict__ L,
+                                                        const int* __restrict__ sel, int k,
+                                                        const double2* __restrict__ roots, double2* __restrict__ M) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* x = reinterpret_cast<double2*>(smem_raw);
+  double2* y = x + n;
+  double2* scratch = y + n;
+  const int c = blockIdx.x;
+  const double rs = rsqrt((double)n);
+  for (int p = threadIdx.x; p < n; p += blockDim.x) x[p] = ld_c<T>(B, (size_t)p * n + c);
+  __syncthreads();
+  fft_block(x, scratch, n, roots, false);
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int q = 0; q < k; ++q) {
+      int src = p - sel[q];
+      if (src < 0) src += n;
+      acc = cadd(acc, cmul(__ldg(L + (size_t)q * n + p), cscale(x[src], rs)));
+    }
+    y[p] = acc;
+  }
+  __syncthreads();
+  fft_block(y, scratch, n, roots, true);
+  for (int p = threadIdx.x; p < n; p += blockDim.x) M[(size_t)p * n + c] = cscale(y[p], rs);
+}
+
+// ---------------------------------------------------------------------------------------------
+// term2, one row per CTA: x = W conj(dA[r,:]); a[p] = sum_t conj(L_t[(p+t)%n]) x[(p+t)%n];
+// M[r,:] += conj(W* a). dA's row is formed on the fly from the selected spectra of A.
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(512) circ_right_kernel(const T* __restrict__ A, int n,
+                                                         const double2* __restrict__ SselA,
+                                                         const int* __restrict__ selA, int ka,
+                                                         const double2* __restrict__ LB, const int* __restrict__ selB,
+                                                         int kb, const double2* __restrict__ roots,
+                                                         double2* __restrict__ M) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* x = reinterpret_cast<double2*>(smem_raw);
+  double2* y = x + n;
+  double2* scratch = y + n;
+  const int r = blockIdx.x;
+  const double rs = rsqrt((double)n);
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    // Ahat[r][c] = sum_t S_t[(r - c) % n] * w^{t c}, ascending t (circulant_materialize order)
+    double2 ah = make_double2(0.0, 0.0);
+    int d = r - c;
+    if (d < 0) d += n;
+    for (int q = 0; q < ka; ++q) {
+      const int t = selA[q];
+      const int e = (int)(((long long)t * c) % n);
+      const double2 w = cconj(__ldg(roots + e));  // exp(+2 pi i t c / n)
+      ah = cadd(ah, cmul(__ldg(SselA + (size_t)q * n + d), w));
+    }
+    const double2 a = ld_c<T>(A, (size_t)r * n + c);
+    x[c] = cconj(csub(a, ah));
+  }
+  __syncthreads();
+  fft_block(x, scratch, n, roots, false);
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    double2 acc = make_double2(0.0, 0.0);
+    for (int q = 0; q < kb; ++q) {
+      int src = p + selB[q];
+      if (src >= n) src -= n;
+      acc = cadd(acc, cmulc(cscale(x[src], rs), __ldg(LB + (size_t)q * n + src)));
+    }
+    y[p] = acc;
+  }
+  __syncthreads();
+  fft_block(y, scratch, n, roots, true);
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    const double2 v = cconj(cscale(y[c], rs));
+    double2* pm = M + (size_t)r * n + c;
+    *pm = cadd(*pm, v);
+  }
+}
+
+// out[r][c] = sum_q Ssel[q][(r-c)%n] * w^{sel[q] c}   (circulant_materialize, :116-127)
+__global__ void circ_materialize_kernel(const double2* __restrict__ Ssel, const int* __restrict__ sel, int k, int n,
+                                        const double2* __restrict__ roots, double2* __restrict__ out) {
+  const size_t total = (size_t)n * n;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int r = (int)(e / n), c = (int)(e % n);
+    int d = r - c;
+    if (d < 0) d += n;
+    double2 acc = make_double2(0.0, 0.0);
+    for (int q = 0; q < k; ++q) {
+      const int idx = (int)(((long long)sel[q] * c) % n);
+      acc = cadd(acc, cmul(Ssel[(size_t)q * n + d], cconj(roots[idx])));
+    }
+    out[e] = acc;
+  }
+}
+
+// circulant_component (:94-108): col[j] = (1/n) sum_i A[(i+j)%n][i] w^{-k i}
+template <typename T>
+__global__ void circ_component_kernel(const T* __restrict__ A, int n, int kk, const double2* __restrict__ roots,
+                                      double2* __restrict__ out) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double2 acc = make_double2(0.0, 0.0);
+  int idx = 0;
+  for (int i = 0; i < n; ++i) {
+    int r = i + j;
+    if (r >= n) r -= n;
+    acc = cadd(acc, cmul(ld_c<T>(A, (size_t)r * n + i), __ldg(roots + idx)));
+    idx += kk;
+    if (idx >= n) idx -= n;
+  }
+  out[j] = cscale(acc, 1.0 / n);
+}
+
+// unitary DFT of `batch` vectors of length n: element i of vector b at in[b*dist + i*stride]
+__global__ void __launch_bounds__(512) dft_batch_kernel(const double2* __restrict__ in, int64_t stride, int64_t dist,
+                                                        int n, int inverse, double scale,
+                                                        const double2* __restrict__ roots, double2* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* x = reinterpret_cast<double2*>(smem_raw);
+  double2* scratch = x + n;
+  const int64_t b = blockIdx.x;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = in[b * dist + (int64_t)i * stride];
+  __syncthreads();
+  fft_block(x, scratch, n, roots, inverse != 0);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[b * dist + (int64_t)i * stride] = cscale(x[i], scale);
+}
+
+// cycle layouts (core.py:106-137) and cycle powers (:140-154), element size es (8 or 16 bytes)
+template <typename E>
+__global__ void cycle_layout_kernel(const E* __restrict__ in, int n, int mode, E* __restrict__ out) {
+  const size_t total = (size_t)n * n;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / n), j = (int)(e % n);
+    size_t src;
+    switch (mode) {
+      case 0: src = (size_t)((i + j) % n) * n + i; break;        // reorder right: A[(i+j)%n, i]
+      case 1: src = (size_t)i * n + (i - j + n) % n; break;      // reorder left:  A[i, (i-j)%n]
+      case 2: src = (size_t)j * n + (i - j + n) % n; break;      // inverse right: At[c, (r-c)%n]
+      default: src = (size_t)i * n + (i - j + n) % n; break;     // inverse left:  At[r, (r-c)%n]
+    }
+    out[e] = in[src];
+  }
+}
+
+template <typename E>
+__global__ void cycle_power_kernel(const E* __restrict__ in, int rows, int cols, int k, int side, E* __restrict__ out) {
+  const size_t total = (size_t)rows * cols;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int i = (int)(e / cols), j = (int)(e % cols);
+    size_t src = side == 0 ? (size_t)((i - k + rows) % rows) * cols + j   // C^k M: rows down by k
+                           : (size_t)i * cols + (j + k) % cols;           // M C^k: cols left by k
+    out[e] = in[src];
+  }
+}
+
+// ---------------------------------------------------------------------------------------------
+// host side
+// ---------------------------------------------------------------------------------------------
+struct CircPlan {
+  double2 *roots, *S_a, *S_b, *Ssel_a, *L_a, *Ssel_b, *L_b;
+  double *part, *mag_a, *mag_b, *red;
+  int cpc, parts;
+};
+
+static void plan_circ(Workspace& ws, CircPlan& p, int n, int k, bool need_sa_full) {
+  p.cpc = std::max(1, (int)ceil_div(n, 2 * kNumSMs));
+  p.parts = (int)ceil_div(n, p.cpc);
+  p.roots = ws.take<double2>(n);
+  p.S_a = ws.take<double2>((size_t)n * n);
+  p.S_b = need_sa_full ? ws.take<double2>((size_t)n * n) : p.S_a;
+  p.Ssel_a = ws.take<double2>((size_t)std::max(k, 1) * n);
+  p.L_a = ws.take<double2>((size_t)std::max(k, 1) * n);
+  p.Ssel_b = ws.take<double2>((size_t)std::max(k, 1) * n);
+  p.L_b = ws.take<double2>((size_t)std::max(k, 1) * n);
+  p.part = ws.take<double>((size_t)p.parts * n);
+  p.mag_a = ws.take<double>(n);
+  p.mag_b = ws.take<double>(n);
+  p.red = ws.take<double>(4 * kNumSMs + 64);
+}
+
+template <typename T>
+static int circ_decompose_run(const T* A, int n, const CircPlan& p, double2* S, double* mag, cudaStream_t st) {
+  const size_t smem = fft_smem_bytes(n, 1) + (size_t)n * sizeof(double);
+  auto fn = circ_decompose_kernel<T>;
+  APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  fn<<<p.parts, 512, smem, st>>>(A, n, p.cpc, p.roots, S, p.part);
+  APX_LAUNCH_CHECK();
+  mag_finalize_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(p.part, p.parts, n, mag);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+static int circ_spectra_run(const double2* S, int n, const int* sel, int k, const double2* roots, double2* Ssel,
+                            double2* L, cudaStream_t st) {
+  if (k <= 0) return OK;
+  const size_t smem = fft_smem_bytes(n, 1);
+  APX_CUDA(cudaFuncSetAttribute(circ_spectra_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  circ_spectra_kernel<<<k, 512, smem, st>>>(S, n, sel, roots, Ssel, L);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+template <typename T>
+static int run_circulant(const T* A, const T* B, int n, int k, int order, const int* fa, const int* fb, double2* M,
+                         int* sa, int* sb, double* scal, const CircPlan& p, cudaStream_t st) {
+  stage_mark(0, st);
+  APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
+  launch_roots(p.roots, n, st);
+  APX_LAUNCH_CHECK();
+  APX_TRY(circ_decompose_run<T>(A, n, p, p.S_a, p.mag_a, st));
+  if (fa) { if (k) APX_CUDA(cudaMemcpyAsync(sa, fa, k * sizeof(int), cudaMemcpyDeviceToDevice, st)); }
+  else APX_TRY(launch_topk(p.mag_a, n, k, sa, st));
+  APX_TRY(launch_kept_energy(p.mag_a, sa, k, (double)n, scal + APX_S_KEPT_A, st));
+  APX_TRY(circ_spectra_run(p.S_a, n, sa, k, p.roots, p.Ssel_a, p.L_a, st));
+  // B's spectrum reuses S_a's storage (A's selected rows are already copied out)
+  APX_TRY(circ_decompose_run<T>(B, n, p, p.S_b, p.mag_b, st));
+  if (fb) { if (k) APX_CUDA(cudaMemcpyAsync(sb, fb, k * sizeof(int), cudaMemcpyDeviceToDevice, st)); }
+  else APX_TRY(launch_topk(p.mag_b, n, k, sb, st));
+  APX_TRY(launch_kept_energy(p.mag_b, sb, k, (double)n, scal + APX_S_KEPT_B, st));
+  APX_TRY(circ_spectra_run(p.S_b, n, sb, k, p.roots, p.Ssel_b, p.L_b, st));
+  stage_mark(1, st);
+  const size_t smem = fft_smem_bytes(n, 2);
+  {
+    auto fn = circ_left_kernel<T>;
+    APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fn<<<n, 512, smem, st>>>(B, n, p.L_a, sa, k, p.roots, M);
+    APX_LAUNCH_CHECK();
+  }
+  stage_mark(2, st);
+  if (order == 1) {
+    auto fn = circ_right_kernel<T>;
+    APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fn<<<n, 512, smem, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M);
+    APX_LAUNCH_CHECK();
+  }
+  stage_mark(3, st);
+  int parts = 0;
+  APX_TRY(launch_sumsq<double>(reinterpret_cast<const double*>(M), (size_t)2 * n * n, p.red, &parts, st));
+  APX_TRY(launch_sum_vector(p.red, parts, scal + APX_S_FRO2_M, st));
+  const size_t nel = (size_t)n * n * (sizeof(T) / sizeof(double));
+  APX_TRY(launch_sumsq<double>(reinterpret_cast<const double*>(A), nel, p.red, &parts, st));
+  APX_TRY(launch_sum_vector(p.red, parts, scal + APX_S_FRO2_A, st));
+  APX_TRY(launch_sumsq<double>(reinterpret_cast<const double*>(B), nel, p.red, &parts, st));
+  APX_TRY(launch_sum_vector(p.red, parts, scal + APX_S_FRO2_B, st));
+  stage_mark(4, st);
+  return OK;
+}
+
+}  // namespace apx
+
+using namespace apx;
+
+extern "C" {
+
+size_t apx_circulant_first_order_workspace(int dtype, int64_t n, int k, int order) {
+  (void)dtype;
+  (void)order;
+  Workspace ws(nullptr, 0, true);
+  CircPlan p;
+  plan_circ(ws, p, (int)n, k, false);
+  return ws.off;
+}
+
+int apx_circulant_first_order(int dtype, const void* A, const void* B, int64_t n, int k, int order,
+                              const int32_t* force_sel_a, const int32_t* force_sel_b, void* M, int32_t* sel_a,
+                              int32_t* sel_b, double* scalars, void* wsp, size_t ws_bytes, void* stream) {
+  APX_REQUIRE(dtype == F64 || dtype == C128, "circulant product: fp64 or complex128 inputs");
+  APX_REQUIRE(n >= 1 && fft_smem_bytes((int)n, 2) <= 227 * 1024, "n=%lld exceeds the shared-memory transforms",
+              (long long)n);
+  APX_REQUIRE(k >= 0 && k <= n, "k=%d out of range [0, %lld]", k, (long long)n);
+  APX_REQUIRE(order == 0 || order == 1, "order must be 0 or 1");
+  Workspace ws(wsp, ws_bytes);
+  CircPlan p;
+  plan_circ(ws, p, (int)n, k, false);
+  APX_WS_CHECK(ws);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (dtype == F64)
+    return run_circulant<double>((const double*)A, (const double*)B, (int)n, k, order, force_sel_a, force_sel_b,
+                                 (double2*)M, sel_a, sel_b, scalars, p, st);
+  return run_circulant<double2>((const double2*)A, (const double2*)B, (int)n, k, order, force_sel_a, force_sel_b,
+                                (double2*)M, sel_a, sel_b, scalars, p, st);
+}
+
+size_t apx_circulant_decompose_workspace(int dtype, int64_t n) {
+  (void)dtype;
+  Workspace ws(nullptr, 0, true);
+  ws.take<double2>(n);
+  ws.take<double>((size_t)ceil_div(n, std::max(1, (int)ceil_div(n, 2 * kNumSMs))) * n);
+  return ws.off;
+}
+
+int apx_circulant_decompose(int dtype, const void* A, int64_t n, void* columns, double* magnitudes, void* wsp,
+                            size_t ws_bytes, void* stream) {
+  APX_REQUIRE(dtype == F64 || dtype == C128, "circulant_decompose: fp64 or complex128 input");
+  APX_REQUIRE(n >= 1 && fft_smem_bytes((int)n, 1) + (size_t)n * 8 <= 227 * 1024,
+              "n=%lld exceeds the shared-memory transforms", (long long)n);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace ws(wsp, ws_bytes);
+  CircPlan p{};
+  p.cpc = std::max(1, (int)ceil_div(n, 2 * kNumSMs));
+  p.parts = (int)ceil_div(n, p.cpc);
+  p.roots = ws.take<double2>(n);
+  p.part = ws.take<double>((size_t)p.parts * n);
+  APX_WS_CHECK(ws);
+  launch_roots(p.roots, (int)n, st);
+  APX_LAUNCH_CHECK();
+  if (dtype == F64) return circ_decompose_run<double>((const double*)A, (int)n, p, (double2*)columns, magnitudes, st);
+  return circ_decompose_run<double2>((const double2*)A, (int)n, p, (double2*)columns, magnitudes, st);
+}
+
+size_t apx_circulant_materialize_workspace(int64_t n) {
+  Workspace ws(nullptr, 0, true);
+  ws.take<double2>(n);
+  return ws.off;
+}
+
+// out (n x n complex) = sum_q R_{sel[q]} D^{sel[q]} from the selected first columns Ssel (k x n)
+int apx_circulant_materialize(const void* Ssel, const int32_t* sel, int k, int64_t n, void* out, void* wsp,
+                              size_t ws_bytes, void* stream) {
+  APX_REQUIRE(n >= 1 && k >= 0 && k <= n, "bad materialize arguments");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace ws(wsp, ws_bytes);
+  double2* roots = ws.take<double2>(n);
+  APX_WS_CHECK(ws);
+  launch_roots(roots, (int)n, st);
+  APX_LAUNCH_CHECK();
+  circ_materialize_kernel<<<kNumSMs * 4, 256, 0, st>>>((const double2*)Ssel, sel, k, (int)n, roots, (double2*)out);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+int apx_circulant_component(int dtype, const void* A, int64_t n, int kk, void* out, void* wsp, size_t ws_bytes,
+                            void* stream) {
+  APX_REQUIRE(dtype == F64 || dtype == C128, "circulant_component: fp64 or complex128 input");
+  APX_REQUIRE(kk >= 0 && kk < n, "component index %d out of range [0, %lld)", kk, (long long)n);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace ws(wsp, ws_bytes);
+  double2* roots = ws.take<double2>(n);
+  APX_WS_CHECK(ws);
+  launch_roots(roots, (int)n, st);
+  APX_LAUNCH_CHECK();
+  const unsigned blocks = (unsigned)ceil_div(n, 128);
+  if (dtype == F64) circ_component_kernel<double><<<blocks, 128, 0, st>>>((const double*)A, (int)n, kk, roots, (double2*)out);
+  else circ_component_kernel<double2><<<blocks, 128, 0, st>>>((const double2*)A, (int)n, kk, roots, (double2*)out);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+size_t apx_unitary_dft_workspace(int64_t n) {
+  Workspace ws(nullptr, 0, true);
+  ws.take<double2>(n);
+  return ws.off;
+}
+
+// unitary_dft (core.py:82-97): `batch` complex128 vectors of length n, element i of vector b at
+// x[b*dist + i*stride]; forward applies W (e^{-2 pi i pq/n}/sqrt(n)), inverse W*.
+int apx_unitary_dft(const void* x, void* y, int64_t n, int64_t batch, int64_t stride, int64_t dist, int inverse,
+                    void* wsp, size_t ws_bytes, void* stream) {
+  APX_REQUIRE(n >= 1, "transform length must be >= 1");
+  APX_REQUIRE(fft_smem_bytes((int)n, 1) <= 227 * 1024, "transform length %lld exceeds the shared-memory DFT",
+              (long long)n);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace ws(wsp, ws_bytes);
+  double2* roots = ws.take<double2>(n);
+  APX_WS_CHECK(ws);
+  if (batch == 0) return OK;
+  launch_roots(roots, (int)n, st);
+  APX_LAUNCH_CHECK();
+  const size_t smem = fft_smem_bytes((int)n, 1);
+  APX_CUDA(cudaFuncSetAttribute(dft_batch_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  dft_batch_kernel<<<(unsigned)batch, 512, smem, st>>>((const double2*)x, stride, dist, (int)n, inverse,
+                                                       1.0 / sqrt((double)n), roots, (double2*)y);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+// cycle_reorder / cycle_reorder_inverse (core.py:106-137). mode: 0 reorder right, 1 reorder left,
+// 2 inverse right, 3 inverse left. elem_bytes 8 (fp64) or 16 (complex128).
+int apx_cycle_layout(int elem_bytes, const void* in, int64_t n, int mode, void* out, void* stream) {
+  APX_REQUIRE(n >= 1 && mode >= 0 && mode <= 3, "bad cycle layout arguments");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(n * n, 256), kNumSMs * 8);
+  if (elem_bytes == 8) cycle_layout_kernel<double><<<blocks, 256, 0, st>>>((const double*)in, (int)n, mode, (double*)out);
+  else cycle_layout_kernel<double2><<<blocks, 256, 0, st>>>((const double2*)in, (int)n, mode, (double2*)out);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+// apply_cycle_power (core.py:140-154): side 0 = C^k M (rows down by k), 1 = M C^k (cols left by k)
+int apx_apply_cycle_power(int elem_bytes, const void* in, int64_t rows, int64_t cols, int64_t k, int side, void* out,
+                          void* stream) {
+  const int64_t lim = side == 0 ? rows : cols;
+  APX_REQUIRE(k >= 0 && k < lim, "k=%lld out of range [0, %lld)", (long long)k, (long long)lim);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div(rows * cols, 256), kNumSMs * 8);
+  if (elem_bytes == 8)
+    cycle_power_kernel<double><<<blocks, 256, 0, st>>>((const double*)in, (int)rows, (int)cols, (int)k, side, (double*)out);
+  else
+    cycle_power_kernel<double2><<<blocks, 256, 0, st>>>((const double2*)in, (int)rows, (int)cols, (int)k, side,
+                                                        (double2*)out);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+}  // extern "C"

@@ -39,6 +39,14 @@ __device__ __forceinline__ int block_exclusive_scan_1024(int v, int* sh /*>=32*/
   return warp_excl + x - v;
 }
 
+// Order-preserving map of a double to an unsigned key (any sign); -0.0 is folded onto +0.0 so
+// that zeros tie like numpy's comparison of -w does.
+__device__ __forceinline__ unsigned long long dkey(double v) {
+  if (v == 0.0) v = 0.0;
+  const unsigned long long u = (unsigned long long)__double_as_longlong(v);
+  return (u >> 63) ? ~u : (u | 0x8000000000000000ull);
+}
+
 // Selects into sel[0..k) (ascending). w: n doubles (global). Must be launched with 1024 threads.
 __device__ void topk_select_block(const double* __restrict__ w, int n, int k, int* __restrict__ sel) {
   __shared__ unsigned int hist[256];
@@ -55,7 +63,7 @@ __device__ void topk_select_block(const double* __restrict__ w, int n, int k, in
     __syncthreads();
     const unsigned long long prefix = s_prefix, mask = s_mask;
     for (int i = tid; i < n; i += blockDim.x) {
-      unsigned long long key = (unsigned long long)__double_as_longlong(w[i]);
+      unsigned long long key = dkey(w[i]);
       if ((key & mask) == prefix) atomicAdd(&hist[(key >> shift) & 255u], 1u);
     }
     __syncthreads();
@@ -98,7 +106,7 @@ __device__ void topk_select_block(const double* __restrict__ w, int n, int k, in
   const int lo = min(n, tid * chunk), hi = min(n, lo + chunk);
   int eq = 0, gt = 0;
   for (int i = lo; i < hi; ++i) {
-    unsigned long long key = (unsigned long long)__double_as_longlong(w[i]);
+    unsigned long long key = dkey(w[i]);
     eq += key == T;
     gt += key > T;
   }
@@ -108,7 +116,7 @@ __device__ void topk_select_block(const double* __restrict__ w, int n, int k, in
   int pos = block_exclusive_scan_1024(gt + take_eq, scan_sh, &tot);
   int e = eq_before;
   for (int i = lo; i < hi; ++i) {
-    unsigned long long key = (unsigned long long)__double_as_longlong(w[i]);
+    unsigned long long key = dkey(w[i]);
     bool take = key > T;
     if (key == T) { take = e < krem; ++e; }
     if (take) sel[pos++] = i;
