@@ -125,6 +125,29 @@ int apx_circulant_materialize(const void* Ssel, const int32_t* sel, int k, int64
 int apx_circulant_component(int dtype, const void* A, int64_t n, int kk, void* out, void* ws,
                             size_t ws_bytes, void* stream);
 
+/* ----------------------------------------------------------- Fourier-sparsified path ---- */
+/* fft_sparse_first_order_multiply (fsparse.py:168-240): A m x n, B n x p (APX_F64 / APX_C128),
+ * At = A W*, Bt = W B, k largest |.| per row of At and per row (sparsify_cols = 0) or column
+ * (1) of Bt, ties toward the lower index. order 0: SA dense(SB); order 1: SA Bt + (At-SA) SB.
+ * M is m x p complex128. scalars: FRO2_A/B, RES2_A = ||At-SA||^2, RES2_B = ||Bt-SB||^2, FRO2_M.
+ * sel_a (m x min(k,n)) / sel_b (n or p rows x kept) receive the kept columns (optional). */
+size_t apx_sfft_first_order_workspace(int64_t m, int64_t n, int64_t p, int k);
+int apx_sfft_first_order(int dtype, const void* A, const void* B, int64_t m, int64_t n, int64_t p,
+                         int k, int order, int sparsify_cols, void* M, int32_t* sel_a,
+                         int32_t* sel_b, double* scalars, void* ws, size_t ws_bytes, void* stream);
+
+/* topk_sparsify (fsparse.py:121-139) on `rows` rows of complex128 M (rows x cols): budget[r]
+ * (or k when budget is NULL) largest |M[r,:]|, ties to the lower column; sel is rows x k
+ * (ascending, -1 padded), vals the kept entries. Workspace: rows*cols doubles. */
+size_t apx_topk_rows_workspace(int64_t rows, int64_t cols);
+int apx_topk_rows(const void* M, int64_t rows, int64_t cols, int k, const int32_t* budget,
+                  int32_t* sel, void* vals, void* ws, size_t ws_bytes, void* stream);
+
+/* sparse_dense_multiply (fsparse.py:142-165), S on the left: out (rows x p) = S X, S given as
+ * rows x k (sel, vals complex128; -1 = unused slot), X complex128 with p columns, k <= 256. */
+int apx_sparse_rows_multiply(const int32_t* sel, const void* vals, int k, int64_t rows,
+                             const void* X, int64_t p, void* out, void* stream);
+
 /* ------------------------------------------------------------------ core.py primitives ---- */
 /* unitary_dft (core.py:82-97) on `batch` complex128 vectors (element i of vector b at
  * x[b*dist + i*stride]); inverse = 0 applies W, 1 applies W*. Any length (direct DFT for

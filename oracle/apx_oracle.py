@@ -349,12 +349,18 @@ def circulant_first_order_multiply(A, B, k: int, order: int, force_sel_a=None, f
 # fsparse.py (secondary path)
 # ----------------------------------------------------------------------------------------------
 
-def topk_rows(M, k):
+def topk_rows(M, k, force=None):
     """fsparse.py:108-139 -- per-row k largest |.|, ties to the lower column; dense masked copy.
+    ``force`` (per-row column lists) replaces the selection (near-tie protocol).
 
     Returns (dense matrix holding only the kept entries, list of ascending column lists)."""
     M = as_matrix(M)
     rows, cols = M.shape
+    if force is not None:
+        out = np.zeros((rows, cols), dtype=np.complex128)
+        for i, keep in enumerate(force):
+            out[i, list(keep)] = M[i, list(keep)]
+        return out, [sorted(int(j) for j in keep) for keep in force]
     if np.isscalar(k):
         if k < 0:
             raise ValueError("k must be >= 0")
@@ -377,7 +383,8 @@ def topk_rows(M, k):
     return out, lists
 
 
-def fft_sparse_first_order_multiply(A, B, k: int, order: int, sparsify_b: str = "rows"):
+def fft_sparse_first_order_multiply(A, B, k: int, order: int, sparsify_b: str = "rows", force_a=None,
+                                    force_b=None):
     """fsparse.py:168-240 -- At = A W*, Bt = W B, per-row top-k of both, first-order product."""
     A = as_matrix(A)
     B = as_matrix(B)
@@ -393,11 +400,12 @@ def fft_sparse_first_order_multiply(A, B, k: int, order: int, sparsify_b: str = 
     t0 = time.perf_counter()
     At = unitary_dft(A, "inverse", axis=1)
     Bt = unitary_dft(B, "forward", axis=0)
-    SA, _ = topk_rows(At, k)
+    SA, la = topk_rows(At, k, force_a)
     if sparsify_b == "rows":
-        SB, _ = topk_rows(Bt, k)
+        SB, lb = topk_rows(Bt, k, force_b)
     else:
-        SB = topk_rows(Bt.T, k)[0].T
+        SBt, lb = topk_rows(Bt.T, k, force_b)
+        SB = SBt.T
     dAt = At - SA
     ndA, ndB = float(np.linalg.norm(dAt)), float(np.linalg.norm(Bt - SB))
     if order == 0:
@@ -407,6 +415,8 @@ def fft_sparse_first_order_multiply(A, B, k: int, order: int, sparsify_b: str = 
     wall = time.perf_counter() - t0
     rep = _report("sfft", order, k, float(np.linalg.norm(A)), float(np.linalg.norm(B)),
                   ndA, ndB, M, n, wall)
+    rep["selected_a"], rep["selected_b"] = la, lb
+    rep["At"], rep["Bt"] = At, Bt
     return M, rep
 
 

@@ -49,6 +49,12 @@ SIGNATURES = {
     "apx_apply_cycle_power": (C.c_int, [_i32, _vp, _i64, _i64, _i64, _i32, _vp, _vp]),
     "apx_pair_reduce_workspace": (_sz, []),
     "apx_pair_reduce": (C.c_int, [_i32, _vp, _i32, _vp, _i64, _i32, _vp, _vp, _sz, _vp]),
+    "apx_sfft_first_order_workspace": (_sz, [_i64, _i64, _i64, _i32]),
+    "apx_sfft_first_order": (C.c_int, [_i32, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp,
+                                       _vp, _sz, _vp]),
+    "apx_topk_rows_workspace": (_sz, [_i64, _i64]),
+    "apx_sparse_rows_multiply": (C.c_int, [_vp, _vp, _i32, _i64, _vp, _i64, _vp, _vp]),
+    "apx_topk_rows": (C.c_int, [_vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "apx_rsvd_workspace": (_sz, [_i32, _i64, _i64, _i32]),
     "apx_rsvd": (C.c_int, [_i32, _vp, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "apx_svd_first_order_workspace": (_sz, [_i32, _i64, _i64, _i64, _i32, _i32]),

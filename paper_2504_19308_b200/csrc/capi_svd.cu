@@ -126,6 +126,10 @@ __global__ void triu_kernel(double* R, int k) {
 
 }  // namespace
 
+int launch_transpose_f64(const double* in, int64_t ldi, int rows, int cols, double* out, int64_t ldo, cudaStream_t st) {
+  return launch_transpose<double>(in, ldi, rows, cols, out, ldo, st);
+}
+
 }  // namespace apx
 
 using namespace apx;

@@ -60,4 +60,5 @@ int launch_small_svd(const double* W, int l, double* U, double* S, double* V, do
 int launch_axpy2d(double* y, int64_t ldy, const double* x, int64_t ldx, int rows, int cols, double alpha,
                   const double* rowscale, int overwrite, cudaStream_t st);
 int launch_sumsq_prefix(const double* s, int k, double* out, cudaStream_t st);
+int launch_transpose_f64(const double* in, int64_t ldi, int rows, int cols, double* out, int64_t ldo, cudaStream_t st);
 }  // namespace apx

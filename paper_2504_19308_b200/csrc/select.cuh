@@ -48,7 +48,7 @@ __device__ __forceinline__ unsigned long long dkey(double v) {
 }
 
 // Selects into sel[0..k) (ascending). w: n doubles (global). Must be launched with 1024 threads.
-__device__ void topk_select_block(const double* __restrict__ w, int n, int k, int* __restrict__ sel) {
+__device__ inline void topk_select_block(const double* __restrict__ w, int n, int k, int* __restrict__ sel) {
   __shared__ unsigned int hist[256];
   __shared__ unsigned long long s_prefix, s_mask;
   __shared__ int s_krem;
