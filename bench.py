@@ -317,7 +317,7 @@ def run_ours(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": "C4 mixed rSVD(k=64) x cycles(k=64) first-order product, n=8192",
                        "n": n, "k_svd": K_SVD, "k_cyc": K_CYC, "order": 1, "power_iterations": 0,
-                       "gemm": "3xTF32" if split3 else "TF32 mma.sync",
+                       "gemm": "3xTF32 mma.sync" if split3 else "tcgen05 kind::tf32 (TMA, warp-specialized)",
                        "parallelism": f"replicas x{world} (one product per GPU per step)",
                        "l2": "inputs larger than L2 (2 x 256 MiB fp32); no flush"},
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(launches),
