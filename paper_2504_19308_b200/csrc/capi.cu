@@ -198,18 +198,42 @@ struct UmmaStages {
   }
 };
 
+// Per-thread side stream + fork/join events: B's cycle decomposition (HBM-bound energy pass,
+// latency-bound select) runs concurrently with A's range finder (GEMMs + the latency-bound QR).
+struct SideStream {
+  cudaStream_t s = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr;
+};
+static thread_local SideStream g_side;
+
+static int get_side(SideStream** out) {
+  if (!g_side.s) {
+    APX_CUDA(cudaStreamCreateWithFlags(&g_side.s, cudaStreamNonBlocking));
+    APX_CUDA(cudaEventCreateWithFlags(&g_side.fork, cudaEventDisableTiming));
+    APX_CUDA(cudaEventCreateWithFlags(&g_side.join, cudaEventDisableTiming));
+  }
+  *out = &g_side;
+  return OK;
+}
+
 static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int kc, int order, int q,
                               const float* Omega, const int* fb, float* M, int* sb, double* scal,
                               const MixedPlan& p, cudaStream_t st) {
   stage_mark(0, st);
   APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
-  APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, st));
-  if (fb) { if (kc) APX_CUDA(cudaMemcpyAsync(sb, fb, kc * sizeof(int), cudaMemcpyDeviceToDevice, st)); }
-  else APX_TRY(launch_topk(p.nr_b, n, kc, sb, st));
-  APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, st));
+  SideStream* ss = nullptr;
+  APX_TRY(get_side(&ss));
+  APX_CUDA(cudaEventRecord(ss->fork, st));
+  APX_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+  const cudaStream_t sb_st = ss->s;
+  APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, sb_st));
+  if (fb) { if (kc) APX_CUDA(cudaMemcpyAsync(sb, fb, kc * sizeof(int), cudaMemcpyDeviceToDevice, sb_st)); }
+  else APX_TRY(launch_topk(p.nr_b, n, kc, sb, sb_st));
+  APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, sb_st));
   float* lb = (float*)p.lam_b;
-  APX_TRY(launch_cycle_extract<float>(B, n, sb, kc, lb, st));
-  APX_TRY(zero_pad_rows<float>(lb, kc, n, st));
+  APX_TRY(launch_cycle_extract<float>(B, n, sb, kc, lb, sb_st));
+  APX_TRY(zero_pad_rows<float>(lb, kc, n, sb_st));
+  APX_CUDA(cudaEventRecord(ss->join, sb_st));
   stage_mark(1, st);
   float *Y = (float*)p.Y, *Q = (float*)p.Q, *Qt = (float*)p.Qt, *Z = (float*)p.Z, *Bm = (float*)p.Bm,
         *W = (float*)p.W, *part = (float*)p.part;
@@ -227,6 +251,7 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   int parts = 0;
   APX_TRY(launch_sumsq<float>(Bm, (size_t)l * n, p.msq, &parts, st));
   APX_TRY(launch_sum_vector(p.msq, parts, scal + APX_S_KEPT_A, st));
+  APX_CUDA(cudaStreamWaitEvent(st, ss->join, 0));  // B's selection and lambda table are ready
   stage_mark(4, st);
   if (order == 1) {
     APX_TRY(UmmaStages::bm_times_db(B, Bm, W, part, n, l, sb, kc, st));

@@ -201,11 +201,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         mbar_wait(&full[s], (uint32_t)((kt / STAGES) & 1));
         unsigned char* a_p = smem + (size_t)s * CF::kStage;
         const int k0 = kbeg + kt * BK;
-        for (int e = et; e < BK * mk; e += 128) {
-          const int kk = e / mk, t = e - kk * mk;
-          int m = k0 + kk - sJ[t];
-          if (m < 0) m += mod_n;
-          if (m >= m0 && m < m0 + BM) *reinterpret_cast<float*>(a_p + mn_off(m - m0, kk)) = 0.f;
+        // shift t masks the diagonal m = (k0 + kk - J_t) mod n of the tile: test the whole
+        // 32-row segment once, then zero the (rare) in-tile entries
+        for (int t = et; t < mk; t += 128) {
+          int off = k0 - sJ[t] - m0;  // m - m0 at kk = 0, taken mod n below
+          off %= mod_n;
+          if (off < 0) off += mod_n;
+          if (off < BM || off + BK - 1 >= mod_n) {
+#pragma unroll 4
+            for (int kk = 0; kk < BK; ++kk) {
+              int q = off + kk;
+              if (q >= mod_n) q -= mod_n;
+              if (q < BM) *reinterpret_cast<float*>(a_p + mn_off(q, kk)) = 0.f;
+            }
+          }
         }
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&masked[s]);
@@ -225,25 +234,26 @@ __global__ void __launch_bounds__(kThreads, 1)
 #pragma unroll
         for (int i = 0; i < 32; ++i) v[i] = 0.f;
       }
-      if (row < M) {
-        if (!TRANS_OUT) {
-          float* p = Cz + (size_t)row * ldc + n0 + j0;
-          const bool fullrow = (n0 + j0 + 32 <= N) && ((((uintptr_t)p) & 15) == 0);
-          if (fullrow) {
+      if (!TRANS_OUT) {
+        // transpose the warp's 32 x 32 chunk through shared memory (the drained stage ring) so
+        // every store instruction writes 128 contiguous bytes of one output row
+        float* tw = reinterpret_cast<float*>(smem) + (warp - 2) * (32 * 33);
+        __syncwarp();
 #pragma unroll
-            for (int i = 0; i < 32; i += 4) {
-              float4 o = make_float4(v[i], v[i + 1], v[i + 2], v[i + 3]);
-              if (accumulate) {
-                const float4 q = *reinterpret_cast<const float4*>(p + i);
-                o.x += q.x; o.y += q.y; o.z += q.z; o.w += q.w;
-              }
-              *reinterpret_cast<float4*>(p + i) = o;
-            }
-          } else {
-            for (int i = 0; i < 32; ++i)
-              if (n0 + j0 + i < N) p[i] = accumulate ? p[i] + v[i] : v[i];
+        for (int i = 0; i < 32; ++i) tw[lane * 33 + i] = v[i];
+        __syncwarp();
+        const int col = n0 + j0 + lane;
+#pragma unroll 4
+        for (int r = 0; r < 32; ++r) {
+          const int rr = m0 + quarter * 32 + r;
+          if (rr < M && col < N) {
+            float* p = Cz + (size_t)rr * ldc + col;
+            const float val = tw[r * 33 + lane];
+            *p = accumulate ? *p + val : val;
           }
-        } else {
+        }
+      } else if (row < M) {
+        {
 #pragma unroll
           for (int i = 0; i < 32; ++i) {
             const int col = n0 + j0 + i;
@@ -344,7 +354,7 @@ int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* 
   APX_TL(64, 4, 0, false) APX_TL(64, 4, 1, false) APX_TL(64, 4, 2, false) APX_TL(64, 4, 3, false)
   APX_TL(64, 4, 4, false) APX_TL(64, 4, 5, false) APX_TL(64, 4, 6, false) APX_TL(64, 4, 7, false)
   APX_TL(64, 4, 1, true) APX_TL(64, 4, 5, true)
-  APX_TL(128, 4, 0, false) APX_TL(128, 4, 2, false) APX_TL(256, 3, 0, false) APX_TL(256, 3, 2, false)
+  APX_TL(128, 4, 0, false) APX_TL(128, 4, 2, false) APX_TL(256, 2, 0, false) APX_TL(256, 2, 2, false)
 #undef APX_TL
   set_error("umma_tma_gemm: unsupported layout %d / BN %d / mask %d", layout, bn, (int)mask);
   return E_ARG;
