@@ -85,7 +85,7 @@ static int run_cycle(const T* A, const T* B, int n, int ka, int kb, int order, c
   T* la = (T*)p.lam_a;
   T* lb = (T*)p.lam_b;
   APX_TRY(launch_cycle_extract<T>(A, n, sa, ka, la, st));
-  APX_TRY(launch_cycle_extract<T>(B, n, sb, kb, lb, st));
+  APX_TRY(launch_cycle_extract<T>(B, n, sb, kb, lb, st, /*aligned=*/order == 1));  // order 0: materialize
   APX_TRY(zero_pad_rows<T>(lb, kb, n, st));
   stage_mark(1, st);
   if (order == 1) {
@@ -231,7 +231,7 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   else APX_TRY(launch_topk(p.nr_b, n, kc, sb, sb_st));
   APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, sb_st));
   float* lb = (float*)p.lam_b;
-  APX_TRY(launch_cycle_extract<float>(B, n, sb, kc, lb, sb_st));
+  APX_TRY(launch_cycle_extract<float>(B, n, sb, kc, lb, sb_st, /*aligned=*/true));
   APX_TRY(zero_pad_rows<float>(lb, kc, n, sb_st));
   APX_CUDA(cudaEventRecord(ss->join, sb_st));
   stage_mark(1, st);
@@ -286,7 +286,7 @@ static int run_mixed(const T* A, const T* B, int n, int l, int kc, int order, in
   else APX_TRY(launch_topk(p.nr_b, n, kc, sb, st));
   APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, st));
   T* lb = (T*)p.lam_b;
-  APX_TRY(launch_cycle_extract<T>(B, n, sb, kc, lb, st));
+  APX_TRY(launch_cycle_extract<T>(B, n, sb, kc, lb, st, /*aligned=*/true));
   APX_TRY(zero_pad_rows<T>(lb, kc, n, st));
   stage_mark(1, st);
   // A: randomized range finder (svd.py:105-111)

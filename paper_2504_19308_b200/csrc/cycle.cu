@@ -5,7 +5,8 @@
 //  K4  topk_select_kernel (select.cuh)              : top_indices semantics (circulant.py:63-70)
 //      cycle_extract                                : lambda_t for the selected shifts (k x n)
 //  K10 cycle_left_gather  : M[r,c] (+)= sum_t lamA_t[r] * X[(r - JA_t) mod n, c]   (Ahat . X)
-//  K11 cycle_right_gather : M[r,c] (+)= sum_t X[r, m] * lamB_t[m],  m = (c + JB_t) mod n
+//  K11 cycle_right_gather : M[r,c] (+)= sum_t X[r, m] * lamB'_t[c],  m = (c + JB_t) mod n,
+//                           lamB'_t[c] = B[m, c] (column-aligned table, read coalesced)
 //                           (X . Bhat), X optionally masked to dA (kept cycles of A zeroed)
 #include "common.cuh"
 #include "select.cuh"
@@ -88,16 +89,24 @@ __global__ void kept_energy_kernel(const double* __restrict__ norms, const int* 
   }
 }
 
-// lam[t][i] = A[i, (i - J_t) mod n]
-template <typename T>
+// left layout (row-indexed):       lam[t][i] = A[i, (i - J_t) mod n]
+// column-aligned layout (aligned): lam[t][c] = A[(c + J_t) mod n, c]  -- the coefficient that
+// output column c of X . Ahat takes from shift t, so the right gather reads it coalesced.
+template <typename T, bool ALIGNED>
 __global__ void cycle_extract(const T* __restrict__ A, int n, const int* __restrict__ J, int k,
                               T* __restrict__ lam) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int t = blockIdx.y;
   if (i >= n || t >= k) return;
-  int c = i - J[t];
-  if (c < 0) c += n;
-  lam[(size_t)t * n + i] = A[(size_t)i * n + c];
+  if (ALIGNED) {
+    int r = i + J[t];
+    if (r >= n) r -= n;
+    lam[(size_t)t * n + i] = A[(size_t)r * n + i];
+  } else {
+    int c = i - J[t];
+    if (c < 0) c += n;
+    lam[(size_t)t * n + i] = A[(size_t)i * n + c];
+  }
 }
 
 // Dense materialization of sum_t Lambda_t C^{J_t} (zero elsewhere).
@@ -191,8 +200,10 @@ __device__ __forceinline__ double ldg_nc_ordered(const double* p) {
   return v;
 }
 
+constexpr int kGatherThreads = 512;
+
 template <typename T, int R, bool FAST>
-__global__ void __launch_bounds__(512, 1) cycle_right_gather(const T* __restrict__ X, const int* __restrict__ JA, int ka,
+__global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T* __restrict__ X, const int* __restrict__ JA, int ka,
                                                           const T* __restrict__ lam, const int* __restrict__ J, int k,
                                                           int n, int m_rows, int accumulate, T* __restrict__ M,
                                                           double* __restrict__ msq_partial,
@@ -229,15 +240,23 @@ __global__ void __launch_bounds__(512, 1) cycle_right_gather(const T* __restrict
       for (int h = 0; h < 2; ++h) {
         const int iv = base + h * blockDim.x;
         if (iv >= nv) continue;
+        // the V columns of this vector times RP rows are one contiguous V*RP run of the
+        // interleaved layout: transpose in registers, then RP 16-byte stores
+        alignas(16) T tr[V * RP];
 #pragma unroll
         for (int rr = 0; rr < RP; ++rr) {
           const T* e = reinterpret_cast<const T*>(&buf[rr][h]);
+          T s = T(0);
 #pragma unroll
           for (int q = 0; q < V; ++q) {
-            xs = fma((double)e[q], (double)e[q], xs);
-            Xs[(size_t)(iv * V + q) * RP + rr] = e[q];
+            s = fma(e[q], e[q], s);
+            tr[q * RP + rr] = e[q];
           }
+          xs += (double)s;
         }
+        Vec* dst = reinterpret_cast<Vec*>(Xs + (size_t)iv * V * RP);
+#pragma unroll
+        for (int w = 0; w < RP; ++w) dst[w] = reinterpret_cast<const Vec*>(tr)[w];
       }
     }
   } else {
@@ -273,7 +292,7 @@ __global__ void __launch_bounds__(512, 1) cycle_right_gather(const T* __restrict
   // lambda loads are issued before any is consumed (U*CPT L2 loads in flight per thread).
   constexpr int NP = (sizeof(T) == 4) ? R / 2 : 0;    // packed float pairs
   constexpr int NS = (sizeof(T) == 4) ? (R & 1) : R;  // scalar rows
-  const int stride = blockDim.x;
+  const int stride = FAST ? kGatherThreads : (int)blockDim.x;  // FAST launches exactly kGatherThreads
   for (int cb = threadIdx.x; cb < n; cb += stride * CPT) {
     unsigned long long acc2[CPT][NP > 0 ? NP : 1];
     T accs[CPT][NS > 0 ? NS : 1];
@@ -291,19 +310,22 @@ __global__ void __launch_bounds__(512, 1) cycle_right_gather(const T* __restrict
       for (int u = 0; u < U; ++u) {
         const int t = t0 + u;
         const int jt = sJ[t];  // broadcast
-        const T* lrow = lam + t * n;
+        const T* lrow = lam + (size_t)t * n;
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
           const int c = cb + q * stride;
-          int m = c + jt;
-          m = m >= n ? m - n : m;
           if constexpr (FAST) {
-            mm[u][q] = m * RP;
-            lv[u][q] = ldg_nc_ordered(lrow + m);
+            // (c + jt) mod n as an unsigned min: c + jt - n wraps above c + jt unless c + jt >= n
+            unsigned m = (unsigned)(c + jt);
+            m = min(m, m - (unsigned)n);
+            mm[u][q] = (int)m;
+            lv[u][q] = ldg_nc_ordered(lrow + c);
           } else {
+            int m = c + jt;
+            m = m >= n ? m - n : m;
             const bool ok = t < k && c < n;
             mm[u][q] = ok ? m * RP : 0;
-            lv[u][q] = ok ? __ldg(lrow + m) : T(0);
+            lv[u][q] = ok ? __ldg(lrow + c) : T(0);
           }
         }
       }
@@ -313,7 +335,7 @@ __global__ void __launch_bounds__(512, 1) cycle_right_gather(const T* __restrict
       for (int u = 0; u < U; ++u)
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
-          const T* xp = Xs + mm[u][q];
+          const T* xp = Xs + (FAST ? (unsigned)mm[u][q] * RP : mm[u][q]);
           if constexpr (NP > 0) {
             const unsigned long long l2 = pack2((float)lv[u][q], (float)lv[u][q]);
             const unsigned long long* xp2 = reinterpret_cast<const unsigned long long*>(xp);
@@ -348,6 +370,17 @@ __global__ void __launch_bounds__(512, 1) cycle_right_gather(const T* __restrict
       if (t0 + 2 * U < kp) load_batch(t0 + 2 * U, mmA, lvA);
       compute_batch(mmB, lvB);
     }
+    // read-modify-write of M: all CPT*R old values are loaded before the first store, so the
+    // thread waits one L2 latency per column block rather than one per element (the compiler
+    // cannot hoist a load of M above a store to M on its own)
+    T mold[CPT][R];
+#pragma unroll
+    for (int q = 0; q < CPT; ++q) {
+      const int c = cb + q * stride;
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr)
+        mold[q][rr] = (accumulate && (FAST || c < n) && rr < rows) ? M[(size_t)(r0 + rr) * n + c] : T(0);
+    }
 #pragma unroll
     for (int q = 0; q < CPT; ++q) {
       const int c = cb + q * stride;
@@ -367,7 +400,7 @@ __global__ void __launch_bounds__(512, 1) cycle_right_gather(const T* __restrict
         }
         if (rr < rows) {
           T* mp = M + (size_t)(r0 + rr) * n + c;
-          T v = accumulate ? *mp + a : a;
+          T v = mold[q][rr] + a;
           *mp = v;
           msq += (double)v * (double)v;
         }
@@ -446,10 +479,13 @@ int launch_kept_energy(const double* norms, const int* sel, int k, double scale,
 }
 
 template <typename T>
-int launch_cycle_extract(const T* A, int n, const int* J, int k, T* lam, cudaStream_t st) {
+int launch_cycle_extract(const T* A, int n, const int* J, int k, T* lam, cudaStream_t st, bool aligned) {
   if (k <= 0) return OK;
   dim3 grid((unsigned)ceil_div(n, 256), (unsigned)k);
-  cycle_extract<T><<<grid, 256, 0, st>>>(A, n, J, k, lam);
+  if (aligned)
+    cycle_extract<T, true><<<grid, 256, 0, st>>>(A, n, J, k, lam);
+  else
+    cycle_extract<T, false><<<grid, 256, 0, st>>>(A, n, J, k, lam);
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -504,7 +540,7 @@ static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const
   const int kp = (int)ceil_div(std::max(k, 1), U) * U;
   const size_t smem = (size_t)(R + (R & 1)) * n * sizeof(T) + (size_t)kp * sizeof(int);
   const int blocks = (int)ceil_div(m_rows, R);
-  const int threads = n >= 512 ? 512 : ((n + 31) / 32) * 32;
+  const int threads = n >= kGatherThreads ? kGatherThreads : ((n + 31) / 32) * 32;
   const bool fast = lam_padded && (n % (threads * CPT)) == 0;
   if (fast) {
     APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R, true>, smem));
@@ -526,7 +562,8 @@ int right_gather_rows(int n, size_t elem, int k) {
   return r;
 }
 
-// lam: k x n, or (lam_padded) ceil(k/8)*8 x n with zero rows past k -- enables the fast path.
+// lam: the column-aligned table (cycle_extract<T, true>), k x n, or (lam_padded) ceil(k/8)*8 x n
+// with zero rows past k -- enables the fast path.
 template <typename T>
 int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n,
                               int m_rows, int accumulate, T* M, double* msq_partial, double* xsq_partial,
@@ -566,7 +603,7 @@ int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st) {
 
 #define APX_INST(T)                                                                                            \
   template int launch_cycle_energies<T>(const T*, int, double*, double*, double*, double*, cudaStream_t);     \
-  template int launch_cycle_extract<T>(const T*, int, const int*, int, T*, cudaStream_t);                     \
+  template int launch_cycle_extract<T>(const T*, int, const int*, int, T*, cudaStream_t, bool);                   \
   template int launch_cycle_materialize<T>(const T*, const int*, int, int, T*, cudaStream_t);                 \
   template int launch_cycle_left_gather<T>(const T*, const T*, const int*, int, int, int, T*, cudaStream_t);  \
   template int launch_cycle_right_gather<T>(const T*, const int*, int, const T*, const int*, int, int, int, int, T*, \

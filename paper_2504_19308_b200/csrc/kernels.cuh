@@ -13,7 +13,7 @@ int launch_cycle_energies(const T* A, int n, double* energies, double* norms, do
 int launch_topk(const double* w, int n, int k, int* sel, cudaStream_t st);
 int launch_kept_energy(const double* norms, const int* sel, int k, double scale, double* out, cudaStream_t st);
 template <typename T>
-int launch_cycle_extract(const T* A, int n, const int* J, int k, T* lam, cudaStream_t st);
+int launch_cycle_extract(const T* A, int n, const int* J, int k, T* lam, cudaStream_t st, bool aligned = false);
 template <typename T>
 int launch_cycle_materialize(const T* lam, const int* J, int k, int n, T* out, cudaStream_t st);
 template <typename T>
