@@ -126,6 +126,8 @@ struct MixedPlan {
   size_t qr_bytes;
   double* msq;
   double* asq;
+  double* bsq;
+  int* ticket;
   int n_part_rows;
 };
 
@@ -150,72 +152,109 @@ static void plan_mixed(Workspace& ws, MixedPlan& p, int dtype, int n, int l, int
   p.qr_bytes = qr_ws_bytes(n, l);
   p.qr_ws = ws.take<char>(p.qr_bytes);
   p.n_part_rows = (int)ceil_div(n, 1);
-  p.msq = ws.take<double>(std::max<int>(n, kNumSMs * 4));
+  const int64_t qw_ctas = ceil_div(n, 128) * ceil_div(n, 128);  // ||M||^2 partials of the Q.W GEMM
+  p.msq = ws.take<double>((size_t)std::max<int64_t>(std::max<int64_t>(n, kNumSMs * 4), qw_ctas));
   p.asq = ws.take<double>(std::max<int>(n, kNumSMs * 4));
+  p.bsq = ws.take<double>(std::max<int>(n, kNumSMs * 4));
+  p.ticket = ws.take<int>(4);
 }
 
 // fp32 GEMM stages of the mixed product on tcgen05 (umma.cu). Layout bits: 1 = A operand stored
 // [k][m] (MN-major), 2 = B operand stored [k][n] (MN-major), 4 = transposed store.
 struct UmmaStages {
-  static int splits(int n) { return std::max(1, std::min(8, (int)((2 * kNumSMs) / ceil_div(n, 128)))); }
+  // K splits for a skinny GEMM with ceil(n/128) row tiles on an SM budget (two CTAs per SM)
+  static int splits(int n, int sms = kNumSMs) {
+    return std::max(1, std::min(8, (int)((2 * sms) / ceil_div(n, 128))));
+  }
   static int umma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                        int64_t ldc, int64_t css, int M, int N, int K, int splits, int acc, const int* mJ, int mk,
                        int mod_n, cudaStream_t st) {
     return umma_tma_gemm(layout, bn, A, lda, B, ldb, C, ldc, css, M, N, K, splits, acc, mJ, mk, mod_n, st);
   }
   // Y[n x l] = A . X, X stored n x l (row-major)
-  static int a_times_x(const float* A, const float* X, float* Y, float* part, int n, int l, cudaStream_t st) {
-    const int s = splits(n);
+  static int a_times_x(const float* A, const float* X, float* Y, float* part, int n, int l, cudaStream_t st,
+                       int sms = kNumSMs) {
+    const int s = splits(n, sms);
     APX_TRY(umma_gemm(2, 64, A, n, X, l, s > 1 ? part : Y, l, (int64_t)n * l, n, l, n, s, 0, nullptr, 0, 1, st));
     if (s > 1) APX_TRY(launch_split_reduce_f32(part, s, (size_t)n * l, Y, st));
     return OK;
   }
   // Z[n x l] = A^T . X   (= (X^T A)^T), X stored n x l
-  static int at_times_x(const float* A, const float* X, float* Z, float* part, int n, int l, cudaStream_t st) {
-    const int s = splits(n);
+  static int at_times_x(const float* A, const float* X, float* Z, float* part, int n, int l, cudaStream_t st,
+                        int sms = kNumSMs) {
+    const int s = splits(n, sms);
     APX_TRY(umma_gemm(3, 64, A, n, X, l, s > 1 ? part : Z, l, (int64_t)n * l, n, l, n, s, 0, nullptr, 0, 1, st));
     if (s > 1) APX_TRY(launch_split_reduce_f32(part, s, (size_t)n * l, Z, st));
     return OK;
   }
   // Bm[l x n] = Q^T . A, computed as (A^T Q) stored transposed; Q stored n x l
-  static int qt_times_a(const float* A, const float* Q, float* Bm, float* part, int n, int l, cudaStream_t st) {
-    const int s = splits(n);
+  static int qt_times_a(const float* A, const float* Q, float* Bm, float* part, int n, int l, cudaStream_t st,
+                        int sms = kNumSMs) {
+    const int s = splits(n, sms);
     APX_TRY(umma_gemm(7, 64, A, n, Q, l, s > 1 ? part : Bm, n, (int64_t)l * n, n, l, n, s, 0, nullptr, 0, 1, st));
     if (s > 1) APX_TRY(launch_split_reduce_f32(part, s, (size_t)n * l, Bm, st));
     return OK;
   }
   // W[l x n] = Bm . dB, computed as (dB^T Bm^T) stored transposed; dB = B with kept cycles masked
   static int bm_times_db(const float* B, const float* Bm, float* W, float* part, int n, int l, const int* J, int kc,
-                         cudaStream_t st) {
-    const int s = splits(n);
+                         cudaStream_t st, int sms = kNumSMs) {
+    const int s = splits(n, sms);
     APX_TRY(umma_gemm(5, 64, B, n, Bm, n, s > 1 ? part : W, n, (int64_t)l * n, n, l, n, s, 0, J, kc, n, st));
     if (s > 1) APX_TRY(launch_split_reduce_f32(part, s, (size_t)n * l, W, st));
     return OK;
   }
-  // M[n x n] = Q . W  (Q stored n x l, W stored l x n)
-  static int q_times_w(const float* Q, const float* W, float* M, int n, int l, cudaStream_t st) {
-    return umma_gemm(2, 256, Q, l, W, n, M, n, 0, n, n, l, 1, 0, nullptr, 0, 1, st);
+  // M[n x n] (+)= Q . W  (Q stored n x l, W stored l x n); optional ||M||^2 partials per CTA
+  static int q_times_w(const float* Q, const float* W, float* M, int n, int l, cudaStream_t st, int acc = 0,
+                       double* sq = nullptr) {
+    // accumulate: BN 128 / 2 stages, whose drained ring holds the C tile for the staged epilogue
+    return umma_tma_gemm(2, acc ? 128 : 256, Q, l, W, n, M, n, 0, n, n, l, 1, acc, nullptr, 0, 1, st, sq);
   }
+  static int q_times_w_ctas(int n, int acc) { return (int)(ceil_div(n, acc ? 128 : 256) * ceil_div(n, 128)); }
 };
 
 // Per-thread side stream + fork/join events: B's cycle decomposition (HBM-bound energy pass,
 // latency-bound select) runs concurrently with A's range finder (GEMMs + the latency-bound QR).
+// Two internal streams per host thread: `hi` (greatest priority) carries the cycle side of the
+// product (B's decomposition, then the persistent row gather), `lo` (least priority) the
+// range finder. The gather's persistent CTAs leave a few SMs free; the range finder's
+// HBM-bound GEMMs and latency-bound QR run there concurrently, so they cost almost no gather
+// time. Priorities make freed SMs go to pending gather CTAs first.
 struct SideStream {
-  cudaStream_t s = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr;
+  cudaStream_t s = nullptr, hi = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, b_ready = nullptr, hi_done = nullptr;
 };
 static thread_local SideStream g_side;
 
 static int get_side(SideStream** out) {
   if (!g_side.s) {
-    APX_CUDA(cudaStreamCreateWithFlags(&g_side.s, cudaStreamNonBlocking));
+    int least = 0, greatest = 0;
+    APX_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
+    APX_CUDA(cudaStreamCreateWithPriority(&g_side.s, cudaStreamNonBlocking, least));
+    APX_CUDA(cudaStreamCreateWithPriority(&g_side.hi, cudaStreamNonBlocking, greatest));
     APX_CUDA(cudaEventCreateWithFlags(&g_side.fork, cudaEventDisableTiming));
     APX_CUDA(cudaEventCreateWithFlags(&g_side.join, cudaEventDisableTiming));
+    APX_CUDA(cudaEventCreateWithFlags(&g_side.b_ready, cudaEventDisableTiming));
+    APX_CUDA(cudaEventCreateWithFlags(&g_side.hi_done, cudaEventDisableTiming));
   }
   *out = &g_side;
   return OK;
 }
 
+// Persistent gather grid: the fewest rounds over the row blocks that still leaves at least
+// kMinFreeSMs SMs to the range finder (APX_GATHER_CTAS overrides, for tuning).
+static int gather_ctas(int nblk) {
+  constexpr int kMinFreeSMs = 8;
+  static const int env = [] {
+    const char* e = getenv("APX_GATHER_CTAS");
+    return e ? atoi(e) : 0;
+  }();
+  if (env > 0) return env;
+  const int rounds = (int)ceil_div(nblk, kNumSMs - kMinFreeSMs);
+  return (int)ceil_div(nblk, rounds);
+}
+
+// Stage markers (bench.py): 0 start | hi: 1 B decomposed, 2 gather done | lo: 3 Y, 4 QR, 5 Bm,
+// 6 W | main: 7 M += Q.W, 8 end.
 static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int kc, int order, int q,
                               const float* Omega, const int* fb, float* M, int* sb, double* scal,
                               const MixedPlan& p, cudaStream_t st) {
@@ -225,49 +264,66 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   APX_TRY(get_side(&ss));
   APX_CUDA(cudaEventRecord(ss->fork, st));
   APX_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
-  const cudaStream_t sb_st = ss->s;
-  APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, sb_st));
-  if (fb) { if (kc) APX_CUDA(cudaMemcpyAsync(sb, fb, kc * sizeof(int), cudaMemcpyDeviceToDevice, sb_st)); }
-  else APX_TRY(launch_topk(p.nr_b, n, kc, sb, sb_st));
-  APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, sb_st));
+  APX_CUDA(cudaStreamWaitEvent(ss->hi, ss->fork, 0));
+  const cudaStream_t hi = ss->hi, lo = ss->s;
+  const int rblocks = (int)ceil_div(n, right_gather_rows(n, sizeof(float), kc));
+  const int gctas = gather_ctas(rblocks);
+  const int free_sms = std::max(8, kNumSMs - gctas);
+  // ---- hi: B's cycle decomposition -> (order 1) the gather M = A . Bhat --------------------------
+  APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, hi));
+  if (fb) { if (kc) APX_CUDA(cudaMemcpyAsync(sb, fb, kc * sizeof(int), cudaMemcpyDeviceToDevice, hi)); }
+  else APX_TRY(launch_topk(p.nr_b, n, kc, sb, hi));
+  APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, hi));
   float* lb = (float*)p.lam_b;
-  APX_TRY(launch_cycle_extract<float>(B, n, sb, kc, lb, sb_st, /*aligned=*/true));
-  APX_TRY(zero_pad_rows<float>(lb, kc, n, sb_st));
-  APX_CUDA(cudaEventRecord(ss->join, sb_st));
-  stage_mark(1, st);
+  APX_TRY(launch_cycle_extract<float>(B, n, sb, kc, lb, hi, /*aligned=*/true));
+  APX_TRY(zero_pad_rows<float>(lb, kc, n, hi));
+  APX_CUDA(cudaEventRecord(ss->b_ready, hi));
+  stage_mark(1, hi);
+  if (order == 1) {
+    APX_TRY(launch_cycle_right_gather<float>(A, nullptr, 0, lb, sb, kc, n, n, 0, M, nullptr, p.asq, hi, true, gctas,
+                                             p.ticket));
+  }
+  stage_mark(2, hi);
+  APX_CUDA(cudaEventRecord(ss->hi_done, hi));
+  // ---- lo: randomized range finder on the SMs the gather leaves free ------------------------------
   float *Y = (float*)p.Y, *Q = (float*)p.Q, *Qt = (float*)p.Qt, *Z = (float*)p.Z, *Bm = (float*)p.Bm,
         *W = (float*)p.W, *part = (float*)p.part;
-  APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, st));
-  stage_mark(2, st);
-  APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, st)));
+  // Y starts once B is decomposed: both are HBM passes, and the B stage gates the gather
+  APX_CUDA(cudaStreamWaitEvent(lo, ss->b_ready, 0));
+  APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, lo, free_sms));
+  stage_mark(3, lo);
+  APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, lo)));
   for (int it = 0; it < q; ++it) {
-    APX_TRY(UmmaStages::at_times_x(A, Q, Z, part, n, l, st));
-    APX_TRY((qr_orthonormalize<float, float>(Z, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, st)));
-    APX_TRY(UmmaStages::a_times_x(A, Q, Y, part, n, l, st));
-    APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, st)));
+    APX_TRY(UmmaStages::at_times_x(A, Q, Z, part, n, l, lo, free_sms));
+    APX_TRY((qr_orthonormalize<float, float>(Z, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, lo)));
+    APX_TRY(UmmaStages::a_times_x(A, Q, Y, part, n, l, lo, free_sms));
+    APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, lo)));
   }
-  stage_mark(3, st);
-  APX_TRY(UmmaStages::qt_times_a(A, Q, Bm, part, n, l, st));
+  stage_mark(4, lo);
+  APX_TRY(UmmaStages::qt_times_a(A, Q, Bm, part, n, l, lo, free_sms));
   int parts = 0;
-  APX_TRY(launch_sumsq<float>(Bm, (size_t)l * n, p.msq, &parts, st));
-  APX_TRY(launch_sum_vector(p.msq, parts, scal + APX_S_KEPT_A, st));
-  APX_CUDA(cudaStreamWaitEvent(st, ss->join, 0));  // B's selection and lambda table are ready
-  stage_mark(4, st);
+  APX_TRY(launch_sumsq<float>(Bm, (size_t)l * n, p.bsq, &parts, lo));
+  APX_TRY(launch_sum_vector(p.bsq, parts, scal + APX_S_KEPT_A, lo));
+  stage_mark(5, lo);
+  // W = Bm . dB = Bm . B - Bm . Bhat (order 1) or Bm . Bhat (order 0): an unmasked TF32 GEMM plus a
+  // 64-row gather over column chunks (cheaper on a few SMs than masking every GEMM stage). The
+  // subtracted gather uses the same TF32-truncated operands as the tensor core, so the large kept
+  // part cancels exactly and W keeps TF32 accuracy relative to Bm . dB, not to Bm . B.
+  const int wchunks = std::max(1, free_sms / (int)ceil_div(l, right_gather_rows(n, sizeof(float), kc)));
+  if (order == 1) APX_TRY(UmmaStages::bm_times_db(B, Bm, W, part, n, l, nullptr, 0, lo, free_sms));
+  APX_TRY(launch_cycle_right_gather<float>(Bm, nullptr, 0, lb, sb, kc, n, l, order == 1 ? -1 : 0, W, nullptr, nullptr,
+                                           lo, true, 0, nullptr, wchunks, /*tf32_operands=*/order == 1));
+  stage_mark(6, lo);
+  APX_CUDA(cudaEventRecord(ss->join, lo));
+  // ---- main: M (+)= Q . W with ||M||^2 fused into the epilogue ---------------------------------
+  APX_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
+  APX_CUDA(cudaStreamWaitEvent(st, ss->hi_done, 0));
+  APX_TRY(UmmaStages::q_times_w(Q, W, M, n, l, st, order == 1 ? 1 : 0, p.msq));
+  stage_mark(7, st);
+  APX_TRY(launch_sum_vector(p.msq, UmmaStages::q_times_w_ctas(n, order == 1), scal + APX_S_FRO2_M, st));
   if (order == 1) {
-    APX_TRY(UmmaStages::bm_times_db(B, Bm, W, part, n, l, sb, kc, st));
-    stage_mark(5, st);
-    APX_TRY(UmmaStages::q_times_w(Q, W, M, n, l, st));
-    stage_mark(6, st);
-    APX_TRY(launch_cycle_right_gather<float>(A, nullptr, 0, lb, sb, kc, n, n, 1, M, p.msq, p.asq, st, true));
-    stage_mark(7, st);
-    const int rblocks = (int)ceil_div(n, right_gather_rows(n, sizeof(float), kc));
-    APX_TRY(launch_sum_vector(p.msq, rblocks, scal + APX_S_FRO2_M, st));
     APX_TRY(launch_sum_vector(p.asq, rblocks, scal + APX_S_FRO2_A, st));
   } else {
-    APX_TRY(launch_cycle_right_gather<float>(Bm, nullptr, 0, lb, sb, kc, n, l, 0, W, p.msq, nullptr, st, true));
-    APX_TRY(UmmaStages::q_times_w(Q, W, M, n, l, st));
-    APX_TRY(launch_sumsq<float>(M, (size_t)n * n, p.msq, &parts, st));
-    APX_TRY(launch_sum_vector(p.msq, parts, scal + APX_S_FRO2_M, st));
     APX_TRY(launch_sumsq<float>(A, (size_t)n * n, p.asq, &parts, st));
     APX_TRY(launch_sum_vector(p.asq, parts, scal + APX_S_FRO2_A, st));
   }

@@ -202,213 +202,241 @@ __device__ __forceinline__ double ldg_nc_ordered(const double* p) {
 
 constexpr int kGatherThreads = 512;
 
-template <typename T, int R, bool FAST>
+// TRUNC (fp32 only): operands truncated to TF32 (low 13 mantissa bits cleared) exactly as the
+// tcgen05 kind::tf32 datapath reads them, so subtracting this gather from a TF32 GEMM over the
+// same operands cancels the kept part exactly (up to fp32 summation order).
+__device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
+__device__ __forceinline__ double tf32_trunc(double x) { return x; }
+
+template <typename T, int R, bool FAST, bool TRUNC = false>
 __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T* __restrict__ X, const int* __restrict__ JA, int ka,
                                                           const T* __restrict__ lam, const int* __restrict__ J, int k,
                                                           int n, int m_rows, int accumulate, T* __restrict__ M,
                                                           double* __restrict__ msq_partial,
-                                                          double* __restrict__ xsq_partial) {
+                                                          double* __restrict__ xsq_partial, int* __restrict__ ticket) {
   constexpr int RP = R + (R & 1);  // interleave pitch (even, so float pairs stay 8B aligned)
   constexpr int CPT = 2, U = 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Xs = reinterpret_cast<T*>(smem_raw);
   int* sJ = reinterpret_cast<int*>(Xs + (size_t)RP * n);
   __shared__ double red[32];
-  const int r0 = blockIdx.x * R;
-  const int rows = min(R, m_rows - r0);
-  // coalesced row reads, interleaved shared-memory writes; rows past the end are zero.
-  // The row block is read in batches of 16-byte vectors with all RP rows' loads issued before
-  // any is stored, so a CTA pays ~one DRAM latency per batch instead of one per element.
-  double xs = 0.0;
-  constexpr int V = 16 / sizeof(T);
-  using Vec = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
-  if (FAST && (n % V) == 0) {
-    const int nv = n / V;
-    for (int base = threadIdx.x; base < nv; base += blockDim.x * 2) {
-      Vec buf[RP][2];
+  __shared__ int s_blk;
+  const int nblk = (int)ceil_div(m_rows, R);
+  // ticket == nullptr: one row block per CTA (blockIdx.x). Otherwise a persistent grid smaller
+  // than the SM count pulls row blocks from an atomic ticket, leaving the remaining SMs to a
+  // concurrent stream (the mixed product's range finder).
+  for (int it = 0;; ++it) {
+    int blk;
+    if (ticket) {
+      if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1);
+      __syncthreads();
+      blk = s_blk;
+    } else {
+      if (it > 0) break;
+      blk = blockIdx.x;
+    }
+    if (blk >= nblk) break;
+    const int r0 = blk * R;
+    const int rows = min(R, m_rows - r0);
+    // coalesced row reads, interleaved shared-memory writes; rows past the end are zero.
+    // The row block is read in batches of 16-byte vectors with all RP rows' loads issued before
+    // any is stored, so a CTA pays ~one DRAM latency per batch instead of one per element.
+    double xs = 0.0;
+    constexpr int V = 16 / sizeof(T);
+    using Vec = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+    if (FAST && (n % V) == 0) {
+      const int nv = n / V;
+      for (int base = threadIdx.x; base < nv; base += blockDim.x * 2) {
+        Vec buf[RP][2];
 #pragma unroll
-      for (int rr = 0; rr < RP; ++rr)
+        for (int rr = 0; rr < RP; ++rr)
+#pragma unroll
+          for (int h = 0; h < 2; ++h) {
+            const int iv = base + h * blockDim.x;
+            if (rr < rows && iv < nv)
+              buf[rr][h] = __ldg(reinterpret_cast<const Vec*>(X + (size_t)(r0 + rr) * n) + iv);
+            else
+              buf[rr][h] = Vec{};
+          }
 #pragma unroll
         for (int h = 0; h < 2; ++h) {
           const int iv = base + h * blockDim.x;
-          if (rr < rows && iv < nv)
-            buf[rr][h] = __ldg(reinterpret_cast<const Vec*>(X + (size_t)(r0 + rr) * n) + iv);
-          else
-            buf[rr][h] = Vec{};
-        }
+          if (iv >= nv) continue;
+          // the V columns of this vector times RP rows are one contiguous V*RP run of the
+          // interleaved layout: transpose in registers, then RP 16-byte stores
+          alignas(16) T tr[V * RP];
 #pragma unroll
-      for (int h = 0; h < 2; ++h) {
-        const int iv = base + h * blockDim.x;
-        if (iv >= nv) continue;
-        // the V columns of this vector times RP rows are one contiguous V*RP run of the
-        // interleaved layout: transpose in registers, then RP 16-byte stores
-        alignas(16) T tr[V * RP];
+          for (int rr = 0; rr < RP; ++rr) {
+            const T* e = reinterpret_cast<const T*>(&buf[rr][h]);
+            T s = T(0);
 #pragma unroll
-        for (int rr = 0; rr < RP; ++rr) {
-          const T* e = reinterpret_cast<const T*>(&buf[rr][h]);
-          T s = T(0);
-#pragma unroll
-          for (int q = 0; q < V; ++q) {
-            s = fma(e[q], e[q], s);
-            tr[q * RP + rr] = e[q];
+            for (int q = 0; q < V; ++q) {
+              s = fma(e[q], e[q], s);
+              tr[q * RP + rr] = TRUNC ? tf32_trunc(e[q]) : e[q];
+            }
+            xs += (double)s;
           }
-          xs += (double)s;
+          Vec* dst = reinterpret_cast<Vec*>(Xs + (size_t)iv * V * RP);
+#pragma unroll
+          for (int w = 0; w < RP; ++w) dst[w] = reinterpret_cast<const Vec*>(tr)[w];
         }
-        Vec* dst = reinterpret_cast<Vec*>(Xs + (size_t)iv * V * RP);
-#pragma unroll
-        for (int w = 0; w < RP; ++w) dst[w] = reinterpret_cast<const Vec*>(tr)[w];
+      }
+    } else {
+      for (int rr = 0; rr < RP; ++rr) {
+        const T* src = X + (size_t)(r0 + rr) * n;
+        for (int m = threadIdx.x; m < n; m += blockDim.x) {
+          T v = T(0);
+          if (rr < rows) v = __ldg(src + m);
+          xs = fma((double)v, (double)v, xs);
+          Xs[(size_t)m * RP + rr] = v;
+        }
       }
     }
-  } else {
-    for (int rr = 0; rr < RP; ++rr) {
-      const T* src = X + (size_t)(r0 + rr) * n;
-      for (int m = threadIdx.x; m < n; m += blockDim.x) {
-        T v = T(0);
-        if (rr < rows) v = __ldg(src + m);
-        xs = fma((double)v, (double)v, xs);
-        Xs[(size_t)m * RP + rr] = v;
-      }
-    }
-  }
-  // shifts, padded with zeros to a multiple of U (FAST: the lambda rows are zero-padded too)
-  const int kp = FAST ? (int)ceil_div(k, U) * U : k;
-  for (int t = threadIdx.x; t < kp; t += blockDim.x) sJ[t] = t < k ? J[t] : 0;
-  __syncthreads();
-  if (xsq_partial != nullptr) {  // ||X||^2 of the (unmasked) rows
-    xs = block_sum(xs, red);
-    if (threadIdx.x == 0) xsq_partial[blockIdx.x] = xs;
-  }
-  if (JA != nullptr) {
-    for (int e = threadIdx.x; e < rows * ka; e += blockDim.x) {
-      const int rr = e / ka, t = e - rr * ka;
-      int m = r0 + rr - JA[t];
-      if (m < 0) m += n;
-      Xs[(size_t)m * RP + rr] = T(0);
-    }
+    // shifts, padded with zeros to a multiple of U (FAST: the lambda rows are zero-padded too)
+    const int kp = FAST ? (int)ceil_div(k, U) * U : k;
+    for (int t = threadIdx.x; t < kp; t += blockDim.x) sJ[t] = t < k ? J[t] : 0;
     __syncthreads();
-  }
-  double msq = 0.0;
-  // Each thread owns CPT columns (blockDim apart, so warps stay coalesced). U shifts' worth of
-  // lambda loads are issued before any is consumed (U*CPT L2 loads in flight per thread).
-  constexpr int NP = (sizeof(T) == 4) ? R / 2 : 0;    // packed float pairs
-  constexpr int NS = (sizeof(T) == 4) ? (R & 1) : R;  // scalar rows
-  const int stride = FAST ? kGatherThreads : (int)blockDim.x;  // FAST launches exactly kGatherThreads
-  for (int cb = threadIdx.x; cb < n; cb += stride * CPT) {
-    unsigned long long acc2[CPT][NP > 0 ? NP : 1];
-    T accs[CPT][NS > 0 ? NS : 1];
-#pragma unroll
-    for (int q = 0; q < CPT; ++q) {
-#pragma unroll
-      for (int p = 0; p < (NP > 0 ? NP : 1); ++p) acc2[q][p] = 0ull;
-#pragma unroll
-      for (int s = 0; s < (NS > 0 ? NS : 1); ++s) accs[q][s] = T(0);
+    if (xsq_partial != nullptr) {  // ||X||^2 of the (unmasked) rows
+      xs = block_sum(xs, red);
+      if (threadIdx.x == 0) xsq_partial[blk] = xs;
     }
-    // software pipeline across shift batches: batch i+1's lambda loads are in flight while
-    // batch i is consumed (ping-pong register buffers A/B)
-    auto load_batch = [&](int t0, int (&mm)[U][CPT], T (&lv)[U][CPT]) {
+    if (JA != nullptr) {
+      for (int e = threadIdx.x; e < rows * ka; e += blockDim.x) {
+        const int rr = e / ka, t = e - rr * ka;
+        int m = r0 + rr - JA[t];
+        if (m < 0) m += n;
+        Xs[(size_t)m * RP + rr] = T(0);
+      }
+      __syncthreads();
+    }
+    double msq = 0.0;
+    // Each thread owns CPT columns (blockDim apart, so warps stay coalesced). U shifts' worth of
+    // lambda loads are issued before any is consumed (U*CPT L2 loads in flight per thread).
+    constexpr int NP = (sizeof(T) == 4) ? R / 2 : 0;    // packed float pairs
+    constexpr int NS = (sizeof(T) == 4) ? (R & 1) : R;  // scalar rows
+    const int stride = FAST ? kGatherThreads : (int)blockDim.x;  // FAST launches exactly kGatherThreads
+    // column chunk of this CTA (grid.y > 1 only in FAST mode: chunk widths are multiples of stride*CPT)
+    const int cw = (int)ceil_div(ceil_div(n, stride * CPT), gridDim.y) * stride * CPT;
+    const int c_lo = blockIdx.y * cw, c_hi = min(n, c_lo + cw);
+    for (int cb = c_lo + threadIdx.x; cb < c_hi; cb += stride * CPT) {
+      unsigned long long acc2[CPT][NP > 0 ? NP : 1];
+      T accs[CPT][NS > 0 ? NS : 1];
 #pragma unroll
-      for (int u = 0; u < U; ++u) {
-        const int t = t0 + u;
-        const int jt = sJ[t];  // broadcast
-        const T* lrow = lam + (size_t)t * n;
+      for (int q = 0; q < CPT; ++q) {
+#pragma unroll
+        for (int p = 0; p < (NP > 0 ? NP : 1); ++p) acc2[q][p] = 0ull;
+#pragma unroll
+        for (int s = 0; s < (NS > 0 ? NS : 1); ++s) accs[q][s] = T(0);
+      }
+      // software pipeline across shift batches: batch i+1's lambda loads are in flight while
+      // batch i is consumed (ping-pong register buffers A/B)
+      auto load_batch = [&](int t0, int (&mm)[U][CPT], T (&lv)[U][CPT]) {
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+          const int t = t0 + u;
+          const int jt = sJ[t];  // broadcast
+          const T* lrow = lam + (size_t)t * n;
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) {
+            const int c = cb + q * stride;
+            if constexpr (FAST) {
+              // (c + jt) mod n as an unsigned min: c + jt - n wraps above c + jt unless c + jt >= n
+              unsigned m = (unsigned)(c + jt);
+              m = min(m, m - (unsigned)n);
+              mm[u][q] = (int)m;
+              lv[u][q] = ldg_nc_ordered(lrow + c);
+              if constexpr (TRUNC) lv[u][q] = tf32_trunc(lv[u][q]);
+            } else {
+              int m = c + jt;
+              m = m >= n ? m - n : m;
+              const bool ok = t < k && c < n;
+              mm[u][q] = ok ? m * RP : 0;
+              lv[u][q] = ok ? __ldg(lrow + c) : T(0);
+            }
+          }
+        }
+      };
+      auto compute_batch = [&](const int (&mm)[U][CPT], const T (&lv)[U][CPT]) {
+#pragma unroll
+        for (int u = 0; u < U; ++u)
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) {
+            const T* xp = Xs + (FAST ? (unsigned)mm[u][q] * RP : mm[u][q]);
+            if constexpr (NP > 0) {
+              const unsigned long long l2 = pack2((float)lv[u][q], (float)lv[u][q]);
+              const unsigned long long* xp2 = reinterpret_cast<const unsigned long long*>(xp);
+#pragma unroll
+              for (int p = 0; p < NP; ++p) acc2[q][p] = ffma2(xp2[p], l2, acc2[q][p]);
+            }
+            if constexpr (NS > 0) {
+#pragma unroll
+              for (int s2 = 0; s2 < NS; ++s2) accs[q][s2] = fma(xp[2 * NP + s2], lv[u][q], accs[q][s2]);
+            }
+          }
+      };
+      // the epilogue reads back M (written by the preceding low-rank GEMM, usually DRAM-resident):
+      // pull those lines toward L2 now so the read-modify-write does not stall on DRAM latency
+      if (accumulate) {
 #pragma unroll
         for (int q = 0; q < CPT; ++q) {
           const int c = cb + q * stride;
-          if constexpr (FAST) {
-            // (c + jt) mod n as an unsigned min: c + jt - n wraps above c + jt unless c + jt >= n
-            unsigned m = (unsigned)(c + jt);
-            m = min(m, m - (unsigned)n);
-            mm[u][q] = (int)m;
-            lv[u][q] = ldg_nc_ordered(lrow + c);
-          } else {
-            int m = c + jt;
-            m = m >= n ? m - n : m;
-            const bool ok = t < k && c < n;
-            mm[u][q] = ok ? m * RP : 0;
-            lv[u][q] = ok ? __ldg(lrow + c) : T(0);
-          }
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr)
+            if ((FAST || c < n) && rr < rows)
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(M + (size_t)(r0 + rr) * n + c));
         }
       }
-    };
-    auto compute_batch = [&](const int (&mm)[U][CPT], const T (&lv)[U][CPT]) {
-#pragma unroll
-      for (int u = 0; u < U; ++u)
-#pragma unroll
-        for (int q = 0; q < CPT; ++q) {
-          const T* xp = Xs + (FAST ? (unsigned)mm[u][q] * RP : mm[u][q]);
-          if constexpr (NP > 0) {
-            const unsigned long long l2 = pack2((float)lv[u][q], (float)lv[u][q]);
-            const unsigned long long* xp2 = reinterpret_cast<const unsigned long long*>(xp);
-#pragma unroll
-            for (int p = 0; p < NP; ++p) acc2[q][p] = ffma2(xp2[p], l2, acc2[q][p]);
-          }
-          if constexpr (NS > 0) {
-#pragma unroll
-            for (int s2 = 0; s2 < NS; ++s2) accs[q][s2] = fma(xp[2 * NP + s2], lv[u][q], accs[q][s2]);
-          }
-        }
-    };
-    // the epilogue reads back M (written by the preceding low-rank GEMM, usually DRAM-resident):
-    // pull those lines toward L2 now so the read-modify-write does not stall on DRAM latency
-    if (accumulate) {
+      int mmA[U][CPT], mmB[U][CPT];
+      T lvA[U][CPT], lvB[U][CPT];
+      load_batch(0, mmA, lvA);
+      for (int t0 = 0; t0 < kp; t0 += 2 * U) {
+        if (t0 + U < kp) load_batch(t0 + U, mmB, lvB);
+        compute_batch(mmA, lvA);
+        if (t0 + U >= kp) break;
+        if (t0 + 2 * U < kp) load_batch(t0 + 2 * U, mmA, lvA);
+        compute_batch(mmB, lvB);
+      }
+      // read-modify-write of M: all CPT*R old values are loaded before the first store, so the
+      // thread waits one L2 latency per column block rather than one per element (the compiler
+      // cannot hoist a load of M above a store to M on its own)
+      T mold[CPT][R];
 #pragma unroll
       for (int q = 0; q < CPT; ++q) {
         const int c = cb + q * stride;
 #pragma unroll
         for (int rr = 0; rr < R; ++rr)
-          if ((FAST || c < n) && rr < rows)
-            asm volatile("prefetch.global.L2 [%0];" ::"l"(M + (size_t)(r0 + rr) * n + c));
+          mold[q][rr] = (accumulate && (FAST || c < n) && rr < rows) ? M[(size_t)(r0 + rr) * n + c] : T(0);
       }
-    }
-    int mmA[U][CPT], mmB[U][CPT];
-    T lvA[U][CPT], lvB[U][CPT];
-    load_batch(0, mmA, lvA);
-    for (int t0 = 0; t0 < kp; t0 += 2 * U) {
-      if (t0 + U < kp) load_batch(t0 + U, mmB, lvB);
-      compute_batch(mmA, lvA);
-      if (t0 + U >= kp) break;
-      if (t0 + 2 * U < kp) load_batch(t0 + 2 * U, mmA, lvA);
-      compute_batch(mmB, lvB);
-    }
-    // read-modify-write of M: all CPT*R old values are loaded before the first store, so the
-    // thread waits one L2 latency per column block rather than one per element (the compiler
-    // cannot hoist a load of M above a store to M on its own)
-    T mold[CPT][R];
 #pragma unroll
-    for (int q = 0; q < CPT; ++q) {
-      const int c = cb + q * stride;
+      for (int q = 0; q < CPT; ++q) {
+        const int c = cb + q * stride;
+        if (!FAST && c >= n) continue;
 #pragma unroll
-      for (int rr = 0; rr < R; ++rr)
-        mold[q][rr] = (accumulate && (FAST || c < n) && rr < rows) ? M[(size_t)(r0 + rr) * n + c] : T(0);
-    }
-#pragma unroll
-    for (int q = 0; q < CPT; ++q) {
-      const int c = cb + q * stride;
-      if (!FAST && c >= n) continue;
-#pragma unroll
-      for (int rr = 0; rr < R; ++rr) {
-        T a;
-        if constexpr (NP > 0) {
-          if (rr < 2 * NP) {
-            const unsigned long long v = acc2[q][rr >> 1];
-            a = (T)__uint_as_float((unsigned)(rr & 1 ? (v >> 32) : (v & 0xffffffffull)));
+        for (int rr = 0; rr < R; ++rr) {
+          T a;
+          if constexpr (NP > 0) {
+            if (rr < 2 * NP) {
+              const unsigned long long v = acc2[q][rr >> 1];
+              a = (T)__uint_as_float((unsigned)(rr & 1 ? (v >> 32) : (v & 0xffffffffull)));
+            } else {
+              a = accs[q][rr - 2 * NP];
+            }
           } else {
-            a = accs[q][rr - 2 * NP];
+            a = accs[q][rr];
           }
-        } else {
-          a = accs[q][rr];
-        }
-        if (rr < rows) {
-          T* mp = M + (size_t)(r0 + rr) * n + c;
-          T v = mold[q][rr] + a;
-          *mp = v;
-          msq += (double)v * (double)v;
+          if (rr < rows) {
+            T* mp = M + (size_t)(r0 + rr) * n + c;
+            T v = accumulate < 0 ? mold[q][rr] - a : mold[q][rr] + a;
+            *mp = v;
+            msq += (double)v * (double)v;
+          }
         }
       }
     }
+    double s = block_sum(msq, red);
+    if (threadIdx.x == 0 && msq_partial) msq_partial[blk] = s;
+    __syncthreads();  // Xs / sJ / red are refilled by the next row block
   }
-  double s = block_sum(msq, red);
-  if (threadIdx.x == 0 && msq_partial) msq_partial[blockIdx.x] = s;
 }
 
 // sum of |x|^2 over a dense array, per-block partials (for ||M||_F when no gather wrote M last)
@@ -535,21 +563,40 @@ int launch_cycle_left_gather(const T* X, const T* lam, const int* J, int k, int 
 
 template <typename T, int R>
 static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int m_rows,
-                          int acc, T* M, double* msq_partial, double* xsq_partial, bool lam_padded, cudaStream_t st) {
+                          int acc, T* M, double* msq_partial, double* xsq_partial, bool lam_padded, int max_ctas,
+                          int* ticket, int col_chunks, bool trunc, cudaStream_t st) {
   constexpr int U = 8, CPT = 2;
   const int kp = (int)ceil_div(std::max(k, 1), U) * U;
   const size_t smem = (size_t)(R + (R & 1)) * n * sizeof(T) + (size_t)kp * sizeof(int);
-  const int blocks = (int)ceil_div(m_rows, R);
+  int blocks = (int)ceil_div(m_rows, R);
+  if (max_ctas > 0 && ticket) {
+    APX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
+    blocks = std::min(blocks, max_ctas);
+  } else {
+    ticket = nullptr;
+  }
   const int threads = n >= kGatherThreads ? kGatherThreads : ((n + 31) / 32) * 32;
   const bool fast = lam_padded && (n % (threads * CPT)) == 0;
+  // column chunks: more CTAs for short inputs (few row blocks); partial sums are per row block
+  int chunks = 1;
+  if (fast && !ticket && col_chunks > 1 && msq_partial == nullptr && xsq_partial == nullptr)
+    chunks = std::min(col_chunks, n / (threads * CPT));
+  const dim3 grid((unsigned)blocks, (unsigned)chunks);
   if (fast) {
+    if (trunc && sizeof(T) == 4) {
+      APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R, true, true>, smem));
+      cycle_right_gather<T, R, true, true><<<grid, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
+                                                                        msq_partial, xsq_partial, ticket);
+      APX_LAUNCH_CHECK();
+      return OK;
+    }
     APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R, true>, smem));
-    cycle_right_gather<T, R, true><<<blocks, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
-                                                                  msq_partial, xsq_partial);
+    cycle_right_gather<T, R, true><<<grid, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
+                                                                  msq_partial, xsq_partial, ticket);
   } else {
     APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R, false>, smem));
     cycle_right_gather<T, R, false><<<blocks, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
-                                                                   msq_partial, xsq_partial);
+                                                                   msq_partial, xsq_partial, ticket);
   }
   APX_LAUNCH_CHECK();
   return OK;
@@ -563,16 +610,20 @@ int right_gather_rows(int n, size_t elem, int k) {
 }
 
 // lam: the column-aligned table (cycle_extract<T, true>), k x n, or (lam_padded) ceil(k/8)*8 x n
-// with zero rows past k -- enables the fast path.
+// with zero rows past k -- enables the fast path. accumulate: 0 M = X.Bhat, 1 M += X.Bhat,
+// -1 M -= X.Bhat. max_ctas + ticket: persistent grid; col_chunks: split the columns over CTAs;
+// tf32_operands (fp32 fast path): X and lambda truncated to TF32 (see cycle_right_gather).
 template <typename T>
 int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n,
                               int m_rows, int accumulate, T* M, double* msq_partial, double* xsq_partial,
-                              cudaStream_t st, bool lam_padded) {
+                              cudaStream_t st, bool lam_padded, int max_ctas, int* ticket, int col_chunks,
+                              bool tf32_operands) {
   const int r = right_gather_rows(n, sizeof(T), k);
   APX_REQUIRE((size_t)n * sizeof(T) + (size_t)(k + 8) * sizeof(int) <= 227 * 1024,
               "n=%d too large for the right gather row block", n);
 #define APX_RG(RV) \
-  return right_gather_r<T, RV>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, lam_padded, st)
+  return right_gather_r<T, RV>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, lam_padded, \
+                               max_ctas, ticket, col_chunks, tf32_operands, st)
   switch (r) {
     case 1: APX_RG(1);
     case 2: APX_RG(2);
@@ -607,7 +658,7 @@ int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st) {
   template int launch_cycle_materialize<T>(const T*, const int*, int, int, T*, cudaStream_t);                 \
   template int launch_cycle_left_gather<T>(const T*, const T*, const int*, int, int, int, T*, cudaStream_t);  \
   template int launch_cycle_right_gather<T>(const T*, const int*, int, const T*, const int*, int, int, int, int, T*, \
-                                            double*, double*, cudaStream_t, bool);                           \
+                                            double*, double*, cudaStream_t, bool, int, int*, int, bool);     \
   template int launch_sumsq<T>(const T*, size_t, double*, int*, cudaStream_t);
 APX_INST(float)
 APX_INST(double)

@@ -17,11 +17,80 @@ namespace apx {
 
 constexpr int kMaxL = 128;
 
-// ---- Gram partials: G_p = Y[rows_p]^T Y[rows_p] -------------------------------------------
+// ---- 64-row tile of a strided n x l matrix (l <= 64) into shared memory as fp64 -------------
+// Each of the 256 threads owns 16 elements; all 16 loads are issued before the first store, so a
+// CTA waits for one memory latency instead of sixteen. Elements past m rows / l columns are 0.
+// The element order follows the contiguous dimension (cs == 1: columns, else rows) so the loads
+// coalesce; T_[i][r] (TRANSPOSED) or T_[r][i] layout, row pitch 66 (16-byte aligned rows).
+constexpr int kTP = 66;
+constexpr size_t kApplySmem = 2 * 64 * kTP * sizeof(double);
+template <bool TRANSPOSED, typename T>
+__device__ __forceinline__ void load_tile64(const T* __restrict__ Y, int64_t rs, int64_t cs, int m, int l, int r0,
+                                            double (*Ts)[kTP]) {
+  const int tid = threadIdx.x;
+  const bool col_fast = cs == 1;
+  T v[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int e = tid + 256 * u;
+    const int r = col_fast ? (e >> 6) : (e & 63), i = col_fast ? (e & 63) : (e >> 6);
+    v[u] = (r0 + r < m && i < l) ? Y[(size_t)(r0 + r) * rs + (size_t)i * cs] : T(0);
+  }
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int e = tid + 256 * u;
+    const int r = col_fast ? (e >> 6) : (e & 63), i = col_fast ? (e & 63) : (e >> 6);
+    if (TRANSPOSED)
+      Ts[i][r] = (double)v[u];
+    else
+      Ts[r][i] = (double)v[u];
+  }
+}
+
+// ---- Gram partials: G_p = Y[rows_p]^T Y[rows_p] over 64-row tiles (fp64) ---------------------
+// 256 threads on a 16 x 16 grid of 4 x 4 blocks of the (padded) 64 x 64 Gram matrix; each row
+// of the tile costs two 16-byte loads per operand and 16 FMAs. The full l x l block is written.
+template <typename T>
+__global__ void __launch_bounds__(256) gram_partial_kernel(const T* __restrict__ Y, int64_t rs, int64_t cs, int m,
+                                                           int l, const int* __restrict__ skip,
+                                                           double* __restrict__ part) {
+  if (skip && *skip) return;
+  __shared__ __align__(16) double Ys[64][kTP];  // [r][i]
+  load_tile64<false>(Y, rs, cs, m, l, blockIdx.x * 64, Ys);
+  __syncthreads();
+  const int bi = (threadIdx.x >> 4) * 4, bj = (threadIdx.x & 15) * 4;
+  double acc[4][4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+#pragma unroll 8
+  for (int r = 0; r < 64; ++r) {
+    const double2 a01 = *reinterpret_cast<const double2*>(&Ys[r][bi]);
+    const double2 a23 = *reinterpret_cast<const double2*>(&Ys[r][bi + 2]);
+    const double2 b01 = *reinterpret_cast<const double2*>(&Ys[r][bj]);
+    const double2 b23 = *reinterpret_cast<const double2*>(&Ys[r][bj + 2]);
+    const double av[4] = {a01.x, a01.y, a23.x, a23.y}, bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
+  }
+  double* out = part + (size_t)blockIdx.x * l * l;
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int i = bi + x, j = bj + y;
+      if (i < l && j < l) out[i * l + j] = acc[x][y];
+    }
+}
+
+// ---- Gram partials for 64 < l <= 128: G_p = Y[rows_p]^T Y[rows_p] ----------------------------
 // 64 rows per CTA staged as fp64 in shared memory; thread t owns a 4x4 block (bi, bj) of G
 // (upper block triangle only), so each pair of 4-wide row loads feeds 16 FMAs.
 template <typename T>
-__global__ void __launch_bounds__(256) gram_partial_kernel(const T* __restrict__ Y, int64_t rs, int64_t cs, int m,
+__global__ void __launch_bounds__(256) gram_partial_wide_kernel(const T* __restrict__ Y, int64_t rs, int64_t cs, int m,
                                                            int l, int rows_per, const int* __restrict__ skip,
                                                            double* __restrict__ part) {
   if (skip && *skip) return;
@@ -221,167 +290,170 @@ __global__ void __launch_bounds__(64) chol64_kernel(const double* __restrict__ G
 }
 
 // ---- fast path (l <= 64): Cholesky + triangular inverse + conditioning test, one CTA --------
-// 128 threads: thread (c = tid & 63, h = tid >> 6) keeps rows [32h, 32h+32) of column c of G in
-// registers; each of the l pivot steps costs three 128-thread barriers and <= 32 predicated FMAs
-// per thread. Then X = R^{-1} is formed column-parallel in shared memory (reciprocal diagonal,
-// no divisions), and kappa_F = ||R||_F ||X||_F >= cond_2(Y) decides whether CholeskyQR's second
-// pass can be skipped: with fp32 outputs one fp64 pass already leaves ||Q^T Q - I|| <~
-// u64 * kappa^2, so kappa_F <= skip_kappa skips pass 2 (flag_skip = 1).
-__global__ void __launch_bounds__(128) cholinv64_kernel(const double* __restrict__ Gin, int l, double* __restrict__ Xout,
+// Elimination on the augmented pair [G | I] (rows/columns l..63 padded with the identity): the
+// row operations of the Cholesky factorisation turn G into R and I into R^{-T}, so X = R^{-1} is
+// read off transposed -- no separate back substitution. Both live in one 64 x 64 work matrix:
+// the upper triangle (c >= r) holds G -> R, the strict lower triangle holds R^{-T}; its diagonal
+// (1 / R[j][j]) is kept in rinv[]. 256 threads; thread t owns 16 consecutive entries of row
+// t / 4 in registers. Step j: the four owners of row j publish it (double-buffered), one barrier,
+// then every row r > j subtracts (A[j][r] / p) * row j on its active entries and row j scales
+// itself by 1 / sqrt(p). The loop is NOT unrolled over j: fully unrolled elimination code does
+// not fit the instruction cache (measured: ~75% of the time stalled on instruction fetch).
+// kappa_F = ||R||_F ||X||_F >= cond_2(Y) decides whether CholeskyQR's second pass can be
+// skipped: with fp32 outputs one fp64 pass already leaves ||Q^T Q - I|| <~ u64 * kappa^2, so
+// kappa_F <= skip_kappa skips pass 2 (skip_out = 1). A pivot below 4*l*eps*max(diag G) raises
+// the breakdown flag (Householder fallback).
+__global__ void __launch_bounds__(256) cholinv64_kernel(const double* __restrict__ Gin, int l, double* __restrict__ Xout,
                                                         const int* __restrict__ gate, int* __restrict__ breakdown,
                                                         int* __restrict__ skip_out, double skip_kappa) {
   if (*gate) return;
-  extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* Rs = reinterpret_cast<double*>(smem_raw);  // 64 x 65
-  double* Xs = Rs + 64 * 65;                          // 64 x 65
-  __shared__ double rowj[64];
+  __shared__ __align__(16) double rowbuf[2][64];
   __shared__ double rinv[64];
-  __shared__ double red[32];
-  __shared__ double s_inv;
-  __shared__ int s_bad;
-  const int tid = threadIdx.x, c = tid & 63, h = tid >> 6;
-  double g[32];
+  __shared__ double red[8][2];
+  const int t = threadIdx.x, r = t >> 2, c0 = (t & 3) * 16;
+  const int lane = t & 31, warp = t >> 5;
+  double w[16];
 #pragma unroll
-  for (int rr = 0; rr < 32; ++rr) {
-    const int r = 32 * h + rr;
-    g[rr] = (c < l && r <= c) ? Gin[r * l + c] : 0.0;
+  for (int u = 0; u < 16; ++u) {
+    const int c = c0 + u;
+    w[u] = (r < l && c < l) ? (c >= r ? Gin[r * l + c] : 0.0) : (c == r ? 1.0 : 0.0);
   }
-  // max diagonal -> breakdown tolerance
-  double dg = 0.0;
+  double md = ((t & 3) == 0 && r < l) ? Gin[r * l + r] : 0.0;
 #pragma unroll
-  for (int rr = 0; rr < 32; ++rr)
-    if (32 * h + rr == c) dg = g[rr];
-  rowj[c] = 0.0;
+  for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
+  if (lane == 0) red[warp][0] = md;
   __syncthreads();
-  if (c < l && (c >> 5) == h) rowj[c] = dg;
-  if (tid == 0) s_bad = 0;
-  __syncthreads();
-  double md = 0.0;
-  for (int i = 0; i < l; ++i) md = fmax(md, rowj[i]);
+#pragma unroll
+  for (int i = 0; i < 8; ++i) md = fmax(md, red[i][0]);
   const double tol = 4.0 * l * 2.220446049250313e-16 * md;
-  __syncthreads();
+  bool bad = false;
 #pragma unroll 1
-  for (int j = 0; j < l; ++j) {
-    const int hj = j >> 5, jj = j & 31;
-    if (c == j && h == hj) {
-      double d2 = 0.0;
+  for (int j = 0; j < 64; ++j) {
+    double* b = rowbuf[j & 1];
+    if (r == j) {
 #pragma unroll
-      for (int rr = 0; rr < 32; ++rr)
-        if (rr == jj) d2 = g[rr];
-      if (!(d2 > tol)) s_bad = 1;
-      const double inv = rsqrt(fmax(d2, 1e-300));
-      s_inv = inv;
-      rinv[j] = inv;
-#pragma unroll
-      for (int rr = 0; rr < 32; ++rr)
-        if (rr == jj) g[rr] = d2 * inv;
+      for (int u = 0; u < 16; u += 2) *reinterpret_cast<double2*>(&b[c0 + u]) = make_double2(w[u], w[u + 1]);
     }
     __syncthreads();
-    if (s_bad) break;
-    if (c > j && c < l && h == hj) {
-      const double inv = s_inv;
-      double rjc = 0.0;
+    double p = b[j];
+    if (j < l && !(p > tol)) bad = true;  // uniform: every thread reads the same pivot
+    if (!(p > 0.0)) p = 1.0;              // keep the (discarded) arithmetic finite after a breakdown
+    const double rsq = rsqrt(p);
+    if (r > j) {
+      const double f = b[r] * (rsq * rsq);  // A[r][j] / p, with A[r][j] = A[j][r]
+      // active entries: c >= r (trailing G) and c <= j (R^{-T} part; its row-j diagonal is 1)
+      const unsigned lo = (unsigned)min(max(r - c0, 0), 16);       // u >= lo: c >= r
+      const unsigned hi = (unsigned)min(max(j - c0 + 1, 0), 16);   // u <  hi: c <= j
+      const unsigned act = (0xffffu << lo) | ((1u << hi) - 1u);
 #pragma unroll
-      for (int rr = 0; rr < 32; ++rr)
-        if (rr == jj) { g[rr] *= inv; rjc = g[rr]; }
-      rowj[c] = rjc;
-    }
-    __syncthreads();
-    if (c > j && c < l) {
-      const double rjc = rowj[c];
-#pragma unroll
-      for (int rr = 0; rr < 32; ++rr) {
-        const int r = 32 * h + rr;
-        if (r > j && r <= c) g[rr] = fma(-rowj[r], rjc, g[rr]);
+      for (int u = 0; u < 16; u += 2) {
+        const double2 bv = *reinterpret_cast<const double2*>(&b[c0 + u]);
+        const double b0 = (c0 + u == j) ? 1.0 : bv.x, b1 = (c0 + u + 1 == j) ? 1.0 : bv.y;
+        if (act & (1u << u)) w[u] = fma(-f, b0, w[u]);
+        if (act & (2u << u)) w[u + 1] = fma(-f, b1, w[u + 1]);
       }
+    } else if (r == j) {
+#pragma unroll
+      for (int u = 0; u < 16; ++u) w[u] *= rsq;
+      if ((t & 3) == 0) rinv[j] = rsq;
     }
-    __syncthreads();
   }
-  if (s_bad) {
-    if (tid == 0) {
+  if (bad) {
+    if (t == 0) {
       *breakdown = 1;
       if (skip_out) *skip_out = 1;
     }
     return;
   }
-  // R (upper) to shared memory
-#pragma unroll
-  for (int rr = 0; rr < 32; ++rr) {
-    const int r = 32 * h + rr;
-    if (r < 64) Rs[r * 65 + c] = (c < l && r <= c) ? g[rr] : 0.0;
-  }
   __syncthreads();
-  // X = R^{-1}: thread c < l solves R x = e_c by back substitution (column c of X)
-  if (tid < l) {
-    for (int i = l - 1; i >= 0; --i) {
-      double sacc = (i == c) ? 1.0 : 0.0;
-      if (i <= c) {
-        for (int k = i + 1; k <= c; ++k) sacc = fma(-Rs[i * 65 + k], Xs[k * 65 + c], sacc);
-      } else {
-        sacc = 0.0;
-      }
-      Xs[i * 65 + c] = (i <= c) ? sacc * rinv[i] : 0.0;
+  double r2 = 0.0, x2 = 0.0;
+  if (r < l) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int c = c0 + u;
+      if (c >= l) continue;
+      // work[r][c]: c >= r -> R[r][c]; c < r -> (R^{-T})[r][c] = X[c][r]
+      if (c >= r) r2 = fma(w[u], w[u], r2);
+      else x2 = fma(w[u], w[u], x2);
+      const double xv = c < r ? w[u] : (c == r ? rinv[r] : 0.0);
+      Xout[c * l + r] = xv;
+      if (c == r) x2 = fma(xv, xv, x2);
     }
   }
-  __syncthreads();
-  // kappa_F = ||R||_F ||X||_F
-  double r2 = 0.0, x2 = 0.0;
-  for (int e = tid; e < l * l; e += blockDim.x) {
-    const int i = e / l, k = e - i * l;
-    const double rv = Rs[i * 65 + k], xv = Xs[i * 65 + k];
-    r2 = fma(rv, rv, r2);
-    x2 = fma(xv, xv, x2);
-    Xout[e] = xv;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+    x2 += __shfl_xor_sync(0xffffffffu, x2, o);
   }
-  r2 = block_sum(r2, red);
+  if (lane == 0) {
+    red[warp][0] = r2;
+    red[warp][1] = x2;
+  }
   __syncthreads();
-  x2 = block_sum(x2, red);
-  if (tid == 0 && skip_out) *skip_out = (sqrt(r2) * sqrt(x2) <= skip_kappa) ? 1 : 0;
+  if (t == 0 && skip_out) {
+    double sr = 0.0, sx = 0.0;
+    for (int i = 0; i < 8; ++i) {
+      sr += red[i][0];
+      sx += red[i][1];
+    }
+    *skip_out = (sqrt(sr) * sqrt(sx) <= skip_kappa) ? 1 : 0;
+  }
 }
 
-// ---- Q = Y X (X = R^{-1} upper), one warp per row; X staged in shared memory ----------------
-// Writes the fp64 copy Q1 (input of CholeskyQR's second pass) and/or the typed outputs Q, Q2.
-template <typename TI, typename TO, int LW>
+// ---- Q = Y X (X = R^{-1} upper, l <= 64) over 64-row tiles ---------------------------------
+// CTA = 64 rows x 64 columns of Q, 256 threads on a 16 x 16 grid of 4 x 4 blocks. The Y tile is
+// staged transposed (Ys[i][r], fp64) with all loads in flight at once, X zero-padded to 64 x 64.
+// Writes the fp64 copy Q1 (input of CholeskyQR's second pass, unless *q1_skip says it will not
+// run) and/or the typed outputs Q, Q2.
+template <typename TI, typename TO>
 __global__ void __launch_bounds__(256) apply_x_kernel(const TI* __restrict__ Y, int64_t rs, int64_t cs, int m, int l,
                                                       const double* __restrict__ X, const int* __restrict__ skip,
-                                                      double* __restrict__ Q1, TO* __restrict__ Q, int64_t qrs,
+                                                      const int* __restrict__ q1_skip, double* __restrict__ Q1,
+                                                      TO* __restrict__ Q, int64_t qrs,
                                                       int64_t qcs, TO* __restrict__ Q2, int64_t q2rs, int64_t q2cs) {
   if (*skip) return;
+  if (q1_skip && *q1_skip) Q1 = nullptr;  // CholeskyQR's second pass will not run
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  double* Xs = reinterpret_cast<double*>(smem_raw);
-  for (int e = threadIdx.x; e < l * l; e += blockDim.x) Xs[e] = X[e];
+  double(*Ys)[kTP] = reinterpret_cast<double(*)[kTP]>(smem_raw);  // [i][r]
+  double(*Xs)[kTP] = Ys + 64;                                      // [i][c]
+  const int tid = threadIdx.x;
+  const int r0 = blockIdx.x * 64;
+#pragma unroll 4
+  for (int e = tid; e < 64 * 64; e += 256) {
+    const int i = e >> 6, c = e & 63;
+    Xs[i][c] = (i < l && c < l) ? X[i * l + c] : 0.0;
+  }
+  load_tile64<true>(Y, rs, cs, m, l, r0, Ys);
   __syncthreads();
-  const int lane = threadIdx.x & 31;
-  const int warps = blockDim.x >> 5;
-  for (int r = blockIdx.x * warps + (threadIdx.x >> 5); r < m; r += gridDim.x * warps) {
-    double y[LW], acc[LW];
+  const int tr = (tid >> 4) * 4, tc = (tid & 15) * 4;
+  double acc[4][4];
 #pragma unroll
-    for (int q = 0; q < LW; ++q) {
-      const int c = lane + 32 * q;
-      y[q] = c < l ? (double)Y[(size_t)r * rs + (size_t)c * cs] : 0.0;
-      acc[q] = 0.0;
-    }
+  for (int x = 0; x < 4; ++x)
 #pragma unroll
-    for (int q = 0; q < LW; ++q) {
+    for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
 #pragma unroll 8
-      for (int i = 0; i < 32; ++i) {
-        const int ii = 32 * q + i;
-        const double yi = __shfl_sync(0xffffffffu, y[q], i);
+  for (int i = 0; i < 64; ++i) {
+    const double2 a01 = *reinterpret_cast<const double2*>(&Ys[i][tr]);
+    const double2 a23 = *reinterpret_cast<const double2*>(&Ys[i][tr + 2]);
+    const double2 b01 = *reinterpret_cast<const double2*>(&Xs[i][tc]);
+    const double2 b23 = *reinterpret_cast<const double2*>(&Xs[i][tc + 2]);
+    const double av[4] = {a01.x, a01.y, a23.x, a23.y}, bv[4] = {b01.x, b01.y, b23.x, b23.y};
 #pragma unroll
-        for (int p = 0; p < LW; ++p) {
-          const int c = lane + 32 * p;
-          if (ii < l && c < l) acc[p] = fma(yi, Xs[ii * l + c], acc[p]);
-        }
-      }
-    }
+    for (int x = 0; x < 4; ++x)
 #pragma unroll
-    for (int q = 0; q < LW; ++q) {
-      const int c = lane + 32 * q;
-      if (c < l) {
-        if (Q1) Q1[(size_t)r * l + c] = acc[q];
-        if (Q) Q[(size_t)r * qrs + (size_t)c * qcs] = (TO)acc[q];
-        if (Q2) Q2[(size_t)r * q2rs + (size_t)c * q2cs] = (TO)acc[q];
-      }
+      for (int y = 0; y < 4; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x) {
+    const int r = r0 + tr + x;
+    if (r >= m) continue;
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int c = tc + y;
+      if (c >= l) continue;
+      if (Q1) Q1[(size_t)r * l + c] = acc[x][y];
+      if (Q) Q[(size_t)r * qrs + (size_t)c * qcs] = (TO)acc[x][y];
+      if (Q2) Q2[(size_t)r * q2rs + (size_t)c * q2cs] = (TO)acc[x][y];
     }
   }
 }
@@ -580,13 +652,17 @@ static int launch_apply(const TI* Y, int64_t rs, int64_t cs, int m, int l, const
 template <typename TI>
 static int launch_gram(const TI* Y, int64_t rs, int64_t cs, int m, int l, const int* skip, double* part, double* G,
                        cudaStream_t st) {
-  const int rows_per = 64;
-  const int parts = (int)ceil_div(m, rows_per);
-  const size_t smem = (size_t)rows_per * (ceil_div(l, 4) * 4 + 4) * sizeof(double);
-  auto fn = gram_partial_kernel<TI>;
-  APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  fn<<<parts, 256, smem, st>>>(Y, rs, cs, m, l, rows_per, skip, part);
-  APX_LAUNCH_CHECK();
+  const int parts = (int)ceil_div(m, 64);
+  if (l <= 64) {
+    gram_partial_kernel<TI><<<parts, 256, 0, st>>>(Y, rs, cs, m, l, skip, part);
+    APX_LAUNCH_CHECK();
+  } else {
+    const size_t smem = (size_t)64 * (ceil_div(l, 4) * 4 + 4) * sizeof(double);
+    auto fn = gram_partial_wide_kernel<TI>;
+    APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fn<<<parts, 256, smem, st>>>(Y, rs, cs, m, l, 64, skip, part);
+    APX_LAUNCH_CHECK();
+  }
   gram_reduce_kernel<<<(unsigned)ceil_div(l * l, 32), 256, 0, st>>>(part, parts, l, skip, G);
   APX_LAUNCH_CHECK();
   return OK;
@@ -630,29 +706,20 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
     // fast path: CholeskyQR with R^{-1}; second pass only when the conditioning requires it
     int* skip2 = flag + 1;
     const double skip_kappa = sizeof(TO) == 4 ? 3.0e4 : 0.0;
-    const size_t smem = (size_t)l * l * sizeof(double);
-    const int blocks = (int)std::min<int64_t>(ceil_div(m, 8), kNumSMs);
-    const int lw = (int)ceil_div(l, 32);
-    const size_t csmem = 2 * 64 * 65 * sizeof(double);
-    APX_CUDA(cudaFuncSetAttribute(cholinv64_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)csmem));
+    const int tiles = (int)ceil_div(m, 64);
     APX_TRY(launch_gram<TI>(Y, rs, cs, m, l, flag, part, G, st));
-    cholinv64_kernel<<<1, 128, csmem, st>>>(G, l, Rinv, flag, flag, skip2, skip_kappa);
+    cholinv64_kernel<<<1, 256, 0, st>>>(G, l, Rinv, flag, flag, skip2, skip_kappa);
     APX_LAUNCH_CHECK();
-    {
-      auto fn = lw == 1 ? apply_x_kernel<TI, TO, 1> : apply_x_kernel<TI, TO, 2>;
-      APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      fn<<<blocks, 256, smem, st>>>(Y, rs, cs, m, l, Rinv, flag, Q1, Q, qrs, qcs, Q2, q2rs, q2cs);
-      APX_LAUNCH_CHECK();
-    }
+    APX_CUDA(cudaFuncSetAttribute(apply_x_kernel<TI, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem));
+    APX_CUDA(cudaFuncSetAttribute(apply_x_kernel<double, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem));
+    apply_x_kernel<TI, TO><<<tiles, 256, kApplySmem, st>>>(Y, rs, cs, m, l, Rinv, flag, skip2, Q1, Q, qrs, qcs, Q2, q2rs, q2cs);
+    APX_LAUNCH_CHECK();
     APX_TRY(launch_gram<double>(Q1, l, 1, m, l, skip2, part, G, st));
-    cholinv64_kernel<<<1, 128, csmem, st>>>(G, l, Rinv, skip2, flag, (int*)nullptr, 0.0);
+    cholinv64_kernel<<<1, 256, 0, st>>>(G, l, Rinv, skip2, flag, (int*)nullptr, 0.0);
     APX_LAUNCH_CHECK();
-    {
-      auto fn = lw == 1 ? apply_x_kernel<double, TO, 1> : apply_x_kernel<double, TO, 2>;
-      APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      fn<<<blocks, 256, smem, st>>>(Q1, l, 1, m, l, Rinv, skip2, (double*)nullptr, Q, qrs, qcs, Q2, q2rs, q2cs);
-      APX_LAUNCH_CHECK();
-    }
+    apply_x_kernel<double, TO><<<tiles, 256, kApplySmem, st>>>(Q1, l, 1, m, l, Rinv, skip2, (const int*)nullptr,
+                                                      (double*)nullptr, Q, qrs, qcs, Q2, q2rs, q2cs);
+    APX_LAUNCH_CHECK();
   } else if (!householder_only) {
     // pass 1: Q1 = Y R1^{-1} (fp64)
     APX_TRY(launch_gram<TI>(Y, rs, cs, m, l, flag, part, G, st));

@@ -106,7 +106,8 @@ template <int BN, int STAGES, bool A_MN, bool B_MN, bool TRANS_OUT, bool MASK>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     float* __restrict__ C, int64_t ldc, int64_t c_split_stride, int M, int N, int K,
-                    int k_per_split, int accumulate, const int* __restrict__ mJ, int mk, int mod_n) {
+                    int k_per_split, int accumulate, const int* __restrict__ mJ, int mk, int mod_n,
+                    double* __restrict__ sq_partial, int c_async) {
   using CF = Cfg<BN, STAGES>;
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte alignment for the swizzled tiles
@@ -117,6 +118,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint64_t* done = masked + STAGES;
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
   __shared__ int sJ[128];
+  __shared__ double sq_red[4];
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
@@ -128,7 +130,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     for (int s = 0; s < STAGES; ++s) {
       mbar_init(&full[s], 1);
       mbar_init(&empty[s], 1);
-      mbar_init(&masked[s], 128);
+      mbar_init(&masked[s], 4);  // one arrival per mask warp
     }
     mbar_init(done, 1);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
@@ -203,11 +205,13 @@ __global__ void __launch_bounds__(kThreads, 1)
         const int k0 = kbeg + kt * BK;
         // shift t masks the diagonal m = (k0 + kk - J_t) mod n of the tile: test the whole
         // 32-row segment once, then zero the (rare) in-tile entries
+        bool wrote = false;
         for (int t = et; t < mk; t += 128) {
           int off = k0 - sJ[t] - m0;  // m - m0 at kk = 0, taken mod n below
           off %= mod_n;
           if (off < 0) off += mod_n;
           if (off < BM || off + BK - 1 >= mod_n) {
+            wrote = true;
 #pragma unroll 4
             for (int kk = 0; kk < BK; ++kk) {
               int q = off + kk;
@@ -216,8 +220,24 @@ __global__ void __launch_bounds__(kThreads, 1)
             }
           }
         }
-        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-        mbar_arrive(&masked[s]);
+        // generic-proxy writes must be made visible to the tensor core (async proxy) before the
+        // MMA issuer is released; warps that wrote nothing skip the proxy fence
+        if (__any_sync(0xffffffffu, wrote)) asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&masked[s]);
+      }
+    }
+    // C tile staged through the (drained) operand ring for a read-modify-write epilogue
+    constexpr bool kStageC = !TRANS_OUT && (size_t)STAGES * CF::kStage >= (size_t)BM * BN * 4;
+    const bool stage_c = kStageC && accumulate && c_async;
+    if (accumulate && !TRANS_OUT && !stage_c) {
+      // the read-modify-write epilogue reads this CTA's C tile: start pulling it toward L2 now
+      // (overlaps the main loop); 128 threads x BN/32 lines per row group
+      for (int rr = et; rr < BM; rr += 128) {
+        const int r = m0 + rr;
+        if (r < M)
+          for (int cc = 0; cc < BN; cc += 32)
+            if (n0 + cc < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(C + (size_t)kz * c_split_stride + (size_t)r * ldc + n0 + cc));
       }
     }
     mbar_wait(done, 0);
@@ -225,8 +245,67 @@ __global__ void __launch_bounds__(kThreads, 1)
     const int quarter = warp & 3;
     const int row = m0 + quarter * 32 + lane;
     float* Cz = C + (size_t)kz * c_split_stride;
+    double sq = 0.0;  // sum of squares of the values this thread stores (sq_partial)
+    if (stage_c) {
+      // Each warp copies its 32 x BN slab of C into the ring with cp.async (every 16-byte granule
+      // in flight at once), adds the accumulator in place, then streams the rows back out.
+      // Granule gc of row r sits at (gc ^ (r & 7)): row-wise float4 access (lane = row) and
+      // column-wise reads (lane = column) are both bank-conflict free.
+      constexpr int GPR = BN / 4;
+      float* creg = reinterpret_cast<float*>(smem) + (size_t)quarter * 32 * BN;
+      const int rbase = m0 + quarter * 32;
+#pragma unroll 4
+      for (int g = lane; g < 32 * GPR; g += 32) {
+        const int r = g / GPR, gc = g - r * GPR;
+        const int rg = rbase + r, cg = n0 + gc * 4;
+        const bool ok = rg < M && cg < N;
+        const float* src = ok ? Cz + (size_t)rg * ldc + cg : Cz;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr(creg + r * BN + ((gc ^ (r & 7)) << 2))),
+                     "l"(src), "r"(ok ? 16 : 0)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
 #pragma unroll 1
-    for (int j0 = 0; j0 < BN; j0 += 32) {
+      for (int j0 = 0; j0 < BN; j0 += 32) {
+        float v[32];
+        if (ktiles > 0) {
+          tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)j0, v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        float* rowp = creg + lane * BN;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float4* p4 = reinterpret_cast<float4*>(rowp + ((((j0 >> 2) + i) ^ (lane & 7)) << 2));
+          float4 o = *p4;
+          o.x += v[4 * i];
+          o.y += v[4 * i + 1];
+          o.z += v[4 * i + 2];
+          o.w += v[4 * i + 3];
+          *p4 = o;
+        }
+      }
+      __syncwarp();
+#pragma unroll 1
+      for (int r = 0; r < 32; ++r) {
+        const int rg = rbase + r;
+        if (rg >= M) break;
+        const float* rowp = creg + r * BN;
+#pragma unroll
+        for (int j0 = 0; j0 < BN; j0 += 32) {
+          const int c = j0 + lane;
+          const float val = rowp[((((c >> 2) ^ (r & 7))) << 2) | (c & 3)];
+          if (n0 + c < N) {
+            Cz[(size_t)rg * ldc + n0 + c] = val;
+            sq = fma((double)val, (double)val, sq);
+          }
+        }
+      }
+    }
+#pragma unroll 1
+    for (int j0 = 0; j0 < BN && !stage_c; j0 += 32) {
       float v[32];
       if (ktiles > 0) {
         tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)j0, v);
@@ -243,13 +322,23 @@ __global__ void __launch_bounds__(kThreads, 1)
         for (int i = 0; i < 32; ++i) tw[lane * 33 + i] = v[i];
         __syncwarp();
         const int col = n0 + j0 + lane;
-#pragma unroll 4
-        for (int r = 0; r < 32; ++r) {
-          const int rr = m0 + quarter * 32 + r;
-          if (rr < M && col < N) {
-            float* p = Cz + (size_t)rr * ldc + col;
-            const float val = tw[r * 33 + lane];
-            *p = accumulate ? *p + val : val;
+#pragma unroll 1
+        for (int r8 = 0; r8 < 32; r8 += 16) {
+          // accumulate: the 16 old values are loaded before the first store (one latency, not 16)
+          float old[16];
+#pragma unroll
+          for (int r = 0; r < 16; ++r) {
+            const int rr = m0 + quarter * 32 + r8 + r;
+            old[r] = (accumulate && rr < M && col < N) ? Cz[(size_t)rr * ldc + col] : 0.f;
+          }
+#pragma unroll
+          for (int r = 0; r < 16; ++r) {
+            const int rr = m0 + quarter * 32 + r8 + r;
+            if (rr < M && col < N) {
+              const float val = old[r] + tw[(r8 + r) * 33 + lane];
+              Cz[(size_t)rr * ldc + col] = val;
+              sq = fma((double)val, (double)val, sq);
+            }
           }
         }
       } else if (row < M) {
@@ -259,11 +348,22 @@ __global__ void __launch_bounds__(kThreads, 1)
             const int col = n0 + j0 + i;
             if (col < N) {
               float* p = Cz + (size_t)col * ldc + row;
-              *p = accumulate ? *p + v[i] : v[i];
+              const float val = accumulate ? *p + v[i] : v[i];
+              *p = val;
+              sq = fma((double)val, (double)val, sq);
             }
           }
         }
       }
+    }
+    if (sq_partial) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+      if (lane == 0) sq_red[quarter] = sq;
+      asm volatile("bar.sync 1, 128;" ::: "memory");  // the four epilogue warps only
+      if (et == 0)
+        sq_partial[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] =
+            (sq_red[0] + sq_red[1]) + (sq_red[2] + sq_red[3]);
     }
   }
   fence_before();
@@ -320,7 +420,7 @@ static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t c
 template <int BN, int STAGES, bool A_MN, bool B_MN, bool TRANS_OUT, bool MASK>
 static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                   int64_t c_split_stride, int M, int N, int K, int splits, int accumulate, const int* mJ, int mk,
-                  int mod_n, cudaStream_t st) {
+                  int mod_n, double* sq_partial, cudaStream_t st) {
   using CF = Cfg<BN, STAGES>;
   CUtensorMap ta, tb;
   // A operand: K-major stored [M][K]; MN-major stored [K][M]
@@ -330,7 +430,9 @@ static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, floa
   dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)splits);
   auto fn = gemm_tma_kernel<BN, STAGES, A_MN, B_MN, TRANS_OUT, MASK>;
   APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem));
-  fn<<<grid, kThreads, CF::kSmem, st>>>(ta, tb, C, ldc, c_split_stride, M, N, K, kps, accumulate, mJ, mk, mod_n);
+  const int c_async = ((uintptr_t)C % 16) == 0 && (ldc % 4) == 0 && (N % 4) == 0 && (c_split_stride % 4) == 0;
+  fn<<<grid, kThreads, CF::kSmem, st>>>(ta, tb, C, ldc, c_split_stride, M, N, K, kps, accumulate, mJ, mk, mod_n,
+                                        sq_partial, c_async);
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -339,22 +441,28 @@ static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, floa
 
 // Same contract as umma_gemm (umma.cu); requires 16-byte aligned bases and leading dimensions,
 // M, N multiples of 32 for MN-major operands. layout bits: 1 A MN-major, 2 B MN-major, 4 C^T.
+// sq_partial (optional): one fp64 sum of squares of the stored values per CTA, indexed
+// (z * grid.y + y) * grid.x + x -- ||C||_F^2 partials for a split-free launch.
 int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                   int64_t ldc, int64_t c_split_stride, int M, int N, int K, int splits, int accumulate,
-                  const int* mJ, int mk, int mod_n, cudaStream_t st) {
+                  const int* mJ, int mk, int mod_n, cudaStream_t st, double* sq_partial) {
   APX_REQUIRE(mk <= 128, "umma_tma_gemm: at most 128 masked shifts");
   APX_REQUIRE(((uintptr_t)A % 16) == 0 && ((uintptr_t)B % 16) == 0 && (lda % 4) == 0 && (ldb % 4) == 0,
               "umma_tma_gemm: 16-byte aligned operands required");
   const bool mask = mJ != nullptr && mk > 0;
+  // ring depth: BN 128 with K <= 2 K-tiles needs only 2 stages (and then fits a staged C tile)
+  const int stages = bn == 256 ? 2 : (bn == 128 && K <= 2 * tma::BK) ? 2 : 4;
 #define APX_TL(BNV, ST, L, MK)                                                                                \
-  if (bn == BNV && layout == L && mask == MK)                                                                 \
+  if (bn == BNV && stages == ST && layout == L && mask == MK)                                                 \
     return tma::launch<BNV, ST, (L & 1) != 0, (L & 2) != 0, (L & 4) != 0, MK>(A, lda, B, ldb, C, ldc,          \
                                                                               c_split_stride, M, N, K, splits, \
-                                                                              accumulate, mJ, mk, mod_n, st);
+                                                                              accumulate, mJ, mk, mod_n,       \
+                                                                              sq_partial, st);
   APX_TL(64, 4, 0, false) APX_TL(64, 4, 1, false) APX_TL(64, 4, 2, false) APX_TL(64, 4, 3, false)
   APX_TL(64, 4, 4, false) APX_TL(64, 4, 5, false) APX_TL(64, 4, 6, false) APX_TL(64, 4, 7, false)
   APX_TL(64, 4, 1, true) APX_TL(64, 4, 5, true)
   APX_TL(128, 4, 0, false) APX_TL(128, 4, 2, false) APX_TL(256, 2, 0, false) APX_TL(256, 2, 2, false)
+  APX_TL(128, 2, 0, false) APX_TL(128, 2, 2, false)
 #undef APX_TL
   set_error("umma_tma_gemm: unsupported layout %d / BN %d / mask %d", layout, bn, (int)mask);
   return E_ARG;

@@ -92,3 +92,12 @@ def test_umma_tma_ragged_split_mask():
     assert run(32 | 5, 64, 256, 64, 256, splits=2) < 1e-5
     assert run(32 | 1, 64, 256, 64, 256, mask=[0, 3, 17], mod_n=256) < 1e-5
     assert run(32 | 2, 256, 256, 512, 64, accumulate=1) < 1e-5
+
+
+@pytest.mark.parametrize("layout", [0, 2])
+def test_umma_tma_staged_c_accumulate(layout):
+    """BN 128 with K <= 64 runs a 2-stage ring and stages the C tile through it (cp.async) for the
+    read-modify-write epilogue; ragged M/N exercise the zero-fill and the store guards."""
+    assert run(32 | layout, 128, 384, 512, 64, accumulate=1) < 1e-5
+    assert run(32 | layout, 128, 200, 260, 40, accumulate=1) < 1e-5
+    assert run(32 | layout, 128, 256, 256, 128, accumulate=1) < 1e-5  # 4-stage ring: L2-prefetch path
