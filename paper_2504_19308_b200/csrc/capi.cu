@@ -240,17 +240,16 @@ static int get_side(SideStream** out) {
   return OK;
 }
 
-// Persistent gather grid: the fewest rounds over the row blocks that still leaves at least
-// kMinFreeSMs SMs to the range finder (APX_GATHER_CTAS overrides, for tuning).
+// Persistent gather grid: all but kMinFreeSMs SMs (the row blocks are pulled from a ticket, so
+// the count need not divide them); APX_GATHER_CTAS overrides, for tuning.
 static int gather_ctas(int nblk) {
-  constexpr int kMinFreeSMs = 8;
+  constexpr int kMinFreeSMs = 18;  // measured at n = 8192 (bench sweep): 130 gather CTAs balance the two streams
   static const int env = [] {
     const char* e = getenv("APX_GATHER_CTAS");
     return e ? atoi(e) : 0;
   }();
   if (env > 0) return env;
-  const int rounds = (int)ceil_div(nblk, kNumSMs - kMinFreeSMs);
-  return (int)ceil_div(nblk, rounds);
+  return std::min(nblk, kNumSMs - kMinFreeSMs);
 }
 
 // Stage markers (bench.py): 0 start | hi: 1 B decomposed, 2 gather done | lo: 3 Y, 4 QR, 5 Bm,
@@ -270,10 +269,14 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   const int gctas = gather_ctas(rblocks);
   const int free_sms = std::max(8, kNumSMs - gctas);
   // ---- hi: B's cycle decomposition -> (order 1) the gather M = A . Bhat --------------------------
-  APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, hi));
-  if (fb) { if (kc) APX_CUDA(cudaMemcpyAsync(sb, fb, kc * sizeof(int), cudaMemcpyDeviceToDevice, hi)); }
-  else APX_TRY(launch_topk(p.nr_b, n, kc, sb, hi));
-  APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, hi));
+  if (fb) {
+    APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, hi));
+    if (kc) APX_CUDA(cudaMemcpyAsync(sb, fb, kc * sizeof(int), cudaMemcpyDeviceToDevice, hi));
+    APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, hi));
+  } else {  // selection with ||B||^2 and the kept energy fused into the select kernel
+    APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, nullptr, p.partial, hi));
+    APX_TRY(launch_topk(p.nr_b, n, kc, sb, hi, p.nr_b, 1.0, scal + APX_S_KEPT_B, p.en_b, scal + APX_S_FRO2_B));
+  }
   float* lb = (float*)p.lam_b;
   APX_TRY(launch_cycle_extract<float>(B, n, sb, kc, lb, hi, /*aligned=*/true));
   APX_TRY(zero_pad_rows<float>(lb, kc, n, hi));
@@ -288,9 +291,9 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   // ---- lo: randomized range finder on the SMs the gather leaves free ------------------------------
   float *Y = (float*)p.Y, *Q = (float*)p.Q, *Qt = (float*)p.Qt, *Z = (float*)p.Z, *Bm = (float*)p.Bm,
         *W = (float*)p.W, *part = (float*)p.part;
-  // Y starts once B is decomposed: both are HBM passes, and the B stage gates the gather
-  APX_CUDA(cudaStreamWaitEvent(lo, ss->b_ready, 0));
-  APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, lo, free_sms));
+  // Y runs on the whole GPU alongside B's decomposition (before the gather claims its SMs); the
+  // rest of the range finder then fits on the SMs the persistent gather leaves free
+  APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, lo, 32));  // 64 CTAs: SMs left for B's kernels
   stage_mark(3, lo);
   APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, lo)));
   for (int it = 0; it < q; ++it) {

@@ -1,7 +1,7 @@
 // Cycle-decomposition kernels: A = sum_j Lambda_j C^j (left layout, reference core.py:113,123-124,
 // lambda_j[i] = A[i, (i-j) mod n]) and the gather passes of the cycle-truncated product.
 //
-//  K3  cycle_energy_partial / cycle_energy_finalize : ||lambda_j||^2 for all j in one HBM pass
+//  K3  cycle_energy_partial (finalize fused)        : ||lambda_j||^2 for all j in one HBM pass
 //  K4  topk_select_kernel (select.cuh)              : top_indices semantics (circulant.py:63-70)
 //      cycle_extract                                : lambda_t for the selected shifts (k x n)
 //  K10 cycle_left_gather  : M[r,c] (+)= sum_t lamA_t[r] * X[(r - JA_t) mod n, c]   (Ahat . X)
@@ -19,47 +19,68 @@ namespace apx {
 // reads 32 consecutive columns of one row per step (coalesced). fp32 inputs accumulate in fp32
 // per chunk (<= 256 terms) and combine chunks in fp64; fp64 inputs accumulate in fp64.
 // ------------------------------------------------------------------------------------------
+// With `counters` (one per 256-column block, zero on entry, left zero on exit) the last CTA of
+// each column block to finish also reduces that block's partials in fixed group order
+// (energies, norms) -- the finalize pass without its own launch.
 template <typename T>
 __global__ void __launch_bounds__(256) cycle_energy_partial(const T* __restrict__ A, int n, int rows_per_chunk,
-                                                            double* __restrict__ partial) {
+                                                            double* __restrict__ partial,
+                                                            unsigned* __restrict__ counters,
+                                                            double* __restrict__ energies,
+                                                            double* __restrict__ norms) {
   using Acc = T;
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int g = blockIdx.y;
   const int r0 = g * rows_per_chunk;
   const int r1 = min(n, r0 + rows_per_chunk);
-  if (j >= n) return;
-  Acc acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
-  int col = r0 - j;
-  if (col < 0) col += n;
-  const T* rowp = A + (size_t)r0 * n;
-  int r = r0;
-  for (; r + 4 <= r1; r += 4) {
-    int c0 = col, c1 = c0 + 1 == n ? 0 : c0 + 1;
-    int c2 = c1 + 1 == n ? 0 : c1 + 1, c3 = c2 + 1 == n ? 0 : c2 + 1;
-    T v0 = __ldg(rowp + c0), v1 = __ldg(rowp + n + c1), v2 = __ldg(rowp + 2 * (size_t)n + c2),
-      v3 = __ldg(rowp + 3 * (size_t)n + c3);
-    acc0 += v0 * v0; acc1 += v1 * v1; acc2 += v2 * v2; acc3 += v3 * v3;
-    col = c3 + 1 == n ? 0 : c3 + 1;
-    rowp += 4 * (size_t)n;
+  const bool valid = j < n;  // ragged last column block: idle threads still join the barriers
+  if (valid) {
+    Acc acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
+    int col = r0 - j;
+    if (col < 0) col += n;
+    const T* rowp = A + (size_t)r0 * n;
+    int r = r0;
+    for (; r + 4 <= r1; r += 4) {
+      int c0 = col, c1 = c0 + 1 == n ? 0 : c0 + 1;
+      int c2 = c1 + 1 == n ? 0 : c1 + 1, c3 = c2 + 1 == n ? 0 : c2 + 1;
+      T v0 = __ldg(rowp + c0), v1 = __ldg(rowp + n + c1), v2 = __ldg(rowp + 2 * (size_t)n + c2),
+        v3 = __ldg(rowp + 3 * (size_t)n + c3);
+      acc0 += v0 * v0; acc1 += v1 * v1; acc2 += v2 * v2; acc3 += v3 * v3;
+      col = c3 + 1 == n ? 0 : c3 + 1;
+      rowp += 4 * (size_t)n;
+    }
+    for (; r < r1; ++r) {
+      T v = __ldg(rowp + col);
+      acc0 += v * v;
+      col = col + 1 == n ? 0 : col + 1;
+      rowp += n;
+    }
+    partial[(size_t)g * n + j] = (double)((acc0 + acc1) + (acc2 + acc3));
   }
-  for (; r < r1; ++r) {
-    T v = __ldg(rowp + col);
-    acc0 += v * v;
-    col = col + 1 == n ? 0 : col + 1;
-    rowp += n;
+  if (counters == nullptr) return;
+  __shared__ unsigned s_last;
+  __threadfence();
+  __syncthreads();
+  if (threadIdx.x == 0) s_last = atomicAdd(&counters[blockIdx.x], 1u) == gridDim.y - 1;
+  __syncthreads();
+  if (!s_last) return;
+  __threadfence();
+  if (valid) {
+    // fixed group order; 8 loads in flight at a time (the sum itself stays sequential)
+    const int groups = (int)gridDim.y;
+    double e = 0.0;
+    for (int g0 = 0; g0 < groups; g0 += 8) {
+      double v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) v[u] = g0 + u < groups ? __ldcg(&partial[(size_t)(g0 + u) * n + j]) : 0.0;
+#pragma unroll
+      for (int u = 0; u < 8; ++u)
+        if (g0 + u < groups) e += v[u];
+    }
+    energies[j] = e;
+    norms[j] = sqrt(e);
   }
-  partial[(size_t)g * n + j] = (double)((acc0 + acc1) + (acc2 + acc3));
-}
-
-// energies[j] = sum_g partial[g][j] (fixed order); norms[j] = sqrt(energies[j]).
-__global__ void cycle_energy_finalize(const double* __restrict__ partial, int n, int groups,
-                                      double* __restrict__ energies, double* __restrict__ norms) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  double s = 0.0;
-  for (int g = 0; g < groups; ++g) s += partial[(size_t)g * n + j];
-  energies[j] = s;
-  norms[j] = sqrt(s);
+  if (threadIdx.x == 0) counters[blockIdx.x] = 0u;
 }
 
 // Single-block deterministic sum of v[0..n) into *out (fixed order per thread, fixed tree).
@@ -72,8 +93,10 @@ __global__ void sum_vector_kernel(const double* __restrict__ v, int n, double* _
 }
 
 __global__ void __launch_bounds__(kSelThreads) topk_select_kernel(const double* __restrict__ w, int n, int k,
-                                                                  int* __restrict__ sel) {
-  topk_select_block(w, n, k, sel);
+                                                                  int* __restrict__ sel, const double* kept_w,
+                                                                  double kept_scale, double* kept,
+                                                                  const double* tot_w, double* total) {
+  topk_select_block(w, n, k, sel, kept_w, kept_scale, kept, tot_w, total);
 }
 
 // kept = sum over selected t of norms[sel[t]]^2, ascending t (mirrors circulant.py:132 order).
@@ -92,21 +115,32 @@ __global__ void kept_energy_kernel(const double* __restrict__ norms, const int* 
 // left layout (row-indexed):       lam[t][i] = A[i, (i - J_t) mod n]
 // column-aligned layout (aligned): lam[t][c] = A[(c + J_t) mod n, c]  -- the coefficient that
 // output column c of X . Ahat takes from shift t, so the right gather reads it coalesced.
+// Each thread gathers kExtractT shifts of one index (all loads in flight before the stores).
+constexpr int kExtractT = 8;
 template <typename T, bool ALIGNED>
 __global__ void cycle_extract(const T* __restrict__ A, int n, const int* __restrict__ J, int k,
                               T* __restrict__ lam) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
-  const int t = blockIdx.y;
-  if (i >= n || t >= k) return;
-  if (ALIGNED) {
-    int r = i + J[t];
-    if (r >= n) r -= n;
-    lam[(size_t)t * n + i] = A[(size_t)r * n + i];
-  } else {
-    int c = i - J[t];
-    if (c < 0) c += n;
-    lam[(size_t)t * n + i] = A[(size_t)i * n + c];
+  const int t0 = blockIdx.y * kExtractT;
+  if (i >= n) return;
+  T v[kExtractT];
+#pragma unroll
+  for (int u = 0; u < kExtractT; ++u) {
+    const int t = t0 + u;
+    if (t >= k) break;
+    if (ALIGNED) {
+      int r = i + __ldg(J + t);
+      if (r >= n) r -= n;
+      v[u] = A[(size_t)r * n + i];
+    } else {
+      int c = i - __ldg(J + t);
+      if (c < 0) c += n;
+      v[u] = A[(size_t)i * n + c];
+    }
   }
+#pragma unroll
+  for (int u = 0; u < kExtractT; ++u)
+    if (t0 + u < k) lam[(size_t)(t0 + u) * n + i] = v[u];
 }
 
 // Dense materialization of sum_t Lambda_t C^{J_t} (zero elsewhere).
@@ -473,7 +507,7 @@ static int energy_groups(int n, int* rows_per_chunk) {
 size_t cycle_energy_ws(int n) {
   int rpc;
   int g = energy_groups(n, &rpc);
-  return (size_t)g * n * sizeof(double) + 256;
+  return (size_t)g * n * sizeof(double) + ceil_div(n, 256) * sizeof(unsigned) + 256;
 }
 
 template <typename T>
@@ -481,10 +515,12 @@ int launch_cycle_energies(const T* A, int n, double* energies, double* norms, do
                           cudaStream_t st) {
   int rpc;
   const int groups = energy_groups(n, &rpc);
-  dim3 grid((unsigned)ceil_div(n, 256), (unsigned)groups);
-  cycle_energy_partial<T><<<grid, 256, 0, st>>>(A, n, rpc, partial);
-  APX_LAUNCH_CHECK();
-  cycle_energy_finalize<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(partial, n, groups, energies, norms);
+  const unsigned cb = (unsigned)ceil_div(n, 256);
+  dim3 grid(cb, (unsigned)groups);
+  // finalize fused through per-column-block arrival counters kept after the partials
+  unsigned* counters = reinterpret_cast<unsigned*>(partial + (size_t)groups * n);
+  APX_CUDA(cudaMemsetAsync(counters, 0, cb * sizeof(unsigned), st));
+  cycle_energy_partial<T><<<grid, 256, 0, st>>>(A, n, rpc, partial, counters, energies, norms);
   APX_LAUNCH_CHECK();
   if (fro2) {
     sum_vector_kernel<<<1, 1024, 0, st>>>(energies, n, fro2);
@@ -493,9 +529,10 @@ int launch_cycle_energies(const T* A, int n, double* energies, double* norms, do
   return OK;
 }
 
-int launch_topk(const double* w, int n, int k, int* sel, cudaStream_t st) {
-  if (k <= 0) return OK;
-  topk_select_kernel<<<1, kSelThreads, 0, st>>>(w, n, k, sel);
+int launch_topk(const double* w, int n, int k, int* sel, cudaStream_t st, const double* kept_w, double kept_scale,
+                double* kept, const double* tot_w, double* total) {
+  if (k <= 0 && !kept && !total) return OK;
+  topk_select_kernel<<<1, kSelThreads, 0, st>>>(w, n, k, sel, kept_w, kept_scale, kept, tot_w, total);
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -509,7 +546,7 @@ int launch_kept_energy(const double* norms, const int* sel, int k, double scale,
 template <typename T>
 int launch_cycle_extract(const T* A, int n, const int* J, int k, T* lam, cudaStream_t st, bool aligned) {
   if (k <= 0) return OK;
-  dim3 grid((unsigned)ceil_div(n, 256), (unsigned)k);
+  dim3 grid((unsigned)ceil_div(n, 256), (unsigned)ceil_div(k, kExtractT));
   if (aligned)
     cycle_extract<T, true><<<grid, 256, 0, st>>>(A, n, J, k, lam);
   else

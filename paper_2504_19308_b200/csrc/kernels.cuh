@@ -10,7 +10,11 @@ int right_gather_rows(int n, size_t elem, int k);
 template <typename T>
 int launch_cycle_energies(const T* A, int n, double* energies, double* norms, double* fro2, double* partial,
                           cudaStream_t st);
-int launch_topk(const double* w, int n, int k, int* sel, cudaStream_t st);
+// top-k selection (select.cuh); optionally fused: *kept = kept_scale * sum_t kept_w[sel[t]]^2 and
+// *total = sum_i tot_w[i]
+int launch_topk(const double* w, int n, int k, int* sel, cudaStream_t st, const double* kept_w = nullptr,
+                double kept_scale = 1.0, double* kept = nullptr, const double* tot_w = nullptr,
+                double* total = nullptr);
 int launch_kept_energy(const double* norms, const int* sel, int k, double scale, double* out, cudaStream_t st);
 template <typename T>
 int launch_cycle_extract(const T* A, int n, const int* J, int k, T* lam, cudaStream_t st, bool aligned = false);

@@ -310,7 +310,9 @@ __global__ void __launch_bounds__(256) cholinv64_kernel(const double* __restrict
   __shared__ __align__(16) double rowbuf[2][64];
   __shared__ double rinv[64];
   __shared__ double red[8][2];
-  const int t = threadIdx.x, r = t >> 2, c0 = (t & 3) * 16;
+  // thread t: row t % 64, columns [16 (t / 64), +16): the lanes of a warp share their columns,
+  // so the row-j reads are shared-memory broadcasts
+  const int t = threadIdx.x, r = t & 63, c0 = (t >> 6) * 16;
   const int lane = t & 31, warp = t >> 5;
   double w[16];
 #pragma unroll
@@ -318,7 +320,7 @@ __global__ void __launch_bounds__(256) cholinv64_kernel(const double* __restrict
     const int c = c0 + u;
     w[u] = (r < l && c < l) ? (c >= r ? Gin[r * l + c] : 0.0) : (c == r ? 1.0 : 0.0);
   }
-  double md = ((t & 3) == 0 && r < l) ? Gin[r * l + r] : 0.0;
+  double md = (t < 64 && r < l) ? Gin[r * l + r] : 0.0;
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
   if (lane == 0) red[warp][0] = md;
@@ -349,13 +351,16 @@ __global__ void __launch_bounds__(256) cholinv64_kernel(const double* __restrict
       for (int u = 0; u < 16; u += 2) {
         const double2 bv = *reinterpret_cast<const double2*>(&b[c0 + u]);
         const double b0 = (c0 + u == j) ? 1.0 : bv.x, b1 = (c0 + u + 1 == j) ? 1.0 : bv.y;
-        if (act & (1u << u)) w[u] = fma(-f, b0, w[u]);
-        if (act & (2u << u)) w[u + 1] = fma(-f, b1, w[u + 1]);
+        // branch-free: inactive entries fold in a zero multiple (divergent per-entry branches
+        // cost ~4x the whole step)
+        const double f0 = (act & (1u << u)) ? f : 0.0, f1 = (act & (2u << u)) ? f : 0.0;
+        w[u] = fma(-f0, b0, w[u]);
+        w[u + 1] = fma(-f1, b1, w[u + 1]);
       }
     } else if (r == j) {
 #pragma unroll
       for (int u = 0; u < 16; ++u) w[u] *= rsq;
-      if ((t & 3) == 0) rinv[j] = rsq;
+      if (c0 == 0) rinv[j] = rsq;
     }
   }
   if (bad) {
