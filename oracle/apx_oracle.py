@@ -25,7 +25,7 @@ __all__ = [
     "frobenius", "relative_error", "top_indices", "component_count", "apriori_relative_error",
     "posterior_relative_error", "rsvd", "svd_first_order_multiply", "circulant_decompose",
     "circulant_materialize", "circulant_left_product", "circulant_right_product",
-    "circulant_first_order_multiply", "topk_rows", "fft_sparse_first_order_multiply",
+    "circulant_first_order_multiply", "topk_rows", "fft_sparse_first_order_multiply", "cycle_product_rows",
     "cycle_norms", "cycle_decompose", "cycle_materialize", "cycle_first_order_multiply",
     "mixed_first_order_multiply", "gen_haar_spectrum", "gen_cycle_operand",
     "gen_circulant_operand", "gen_c5_operand", "Report",
@@ -479,6 +479,26 @@ def _cycle_right_apply(X, J, lam) -> np.ndarray:
     for t, j in enumerate(J):
         out += np.roll(X * lam[t][None, :], -j, axis=1)
     return out
+
+
+def cycle_product_rows(rows, A_rows, JA, B_shifted_rows, JB, lamB):
+    """Rows R of the order-1 cycle product from row data only (config C5: n too large for the
+    full oracle): M[R,:] = sum_t lamA_t[R] B[(R-JA_t)%n, :] + dA[R,:] . Bhat.
+
+    A_rows: A[R, :]; B_shifted_rows[t]: B[(R - JA[t]) % n, :]; lamB: kb x n left-layout lambdas of
+    B (core.py:123-124).  term1 follows _cycle_left_apply, term2 _cycle_right_apply on dA[R, :],
+    dA = A with the kept cycles zeroed (_cycle_residual)."""
+    R = np.asarray(rows)
+    A_rows = np.asarray(A_rows, dtype=np.float64)
+    n = A_rows.shape[1]
+    ri = np.arange(R.size)
+    term1 = np.zeros(A_rows.shape)
+    dA = A_rows.copy()
+    for t, j in enumerate(JA):
+        cols = (R - j) % n
+        term1 += A_rows[ri, cols][:, None] * np.asarray(B_shifted_rows[t], dtype=np.float64)
+        dA[ri, cols] = 0.0
+    return term1 + _cycle_right_apply(dA, JB, np.asarray(lamB, dtype=np.float64))
 
 
 def cycle_first_order_multiply(A, B, k: int, order: int, kb: int | None = None,

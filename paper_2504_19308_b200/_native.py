@@ -12,7 +12,7 @@ import os
 import threading
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "_apx.so")
+LIB_PATH = os.environ.get("APX_LIB") or os.path.join(HERE, "_apx.so")  # APX_LIB: A/B builds
 
 APX_F32, APX_F64, APX_C64, APX_C128 = 0, 1, 2, 3
 E_ARG, E_CUDA, E_WS, E_NUMERIC, E_UNSUPPORTED = 1, 2, 3, 4, 5

@@ -234,7 +234,14 @@ __device__ __forceinline__ double ldg_nc_ordered(const double* p) {
   return v;
 }
 
-constexpr int kGatherThreads = 512;
+// Row-interleave pitch of the right gather's shared-memory block: even (8-byte aligned fp32 pairs)
+// except for a single row, which the largest n (32768 fp32, 16384 fp64) can only afford unpadded.
+__host__ __device__ constexpr int gather_pitch(int r) { return r == 1 ? 1 : r + (r & 1); }
+
+#ifndef APX_GATHER_THREADS
+#define APX_GATHER_THREADS 512
+#endif
+constexpr int kGatherThreads = APX_GATHER_THREADS;
 
 // TRUNC (fp32 only): operands truncated to TF32 (low 13 mantissa bits cleared) exactly as the
 // tcgen05 kind::tf32 datapath reads them, so subtracting this gather from a TF32 GEMM over the
@@ -248,7 +255,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
                                                           int n, int m_rows, int accumulate, T* __restrict__ M,
                                                           double* __restrict__ msq_partial,
                                                           double* __restrict__ xsq_partial, int* __restrict__ ticket) {
-  constexpr int RP = R + (R & 1);  // interleave pitch (even, so float pairs stay 8B aligned)
+  constexpr int RP = gather_pitch(R);  // interleave pitch (even, so float pairs stay 8B aligned)
   constexpr int CPT = 2, U = 8;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Xs = reinterpret_cast<T*>(smem_raw);
@@ -604,7 +611,7 @@ static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const
                           int* ticket, int col_chunks, bool trunc, cudaStream_t st) {
   constexpr int U = 8, CPT = 2;
   const int kp = (int)ceil_div(std::max(k, 1), U) * U;
-  const size_t smem = (size_t)(R + (R & 1)) * n * sizeof(T) + (size_t)kp * sizeof(int);
+  const size_t smem = (size_t)gather_pitch(R) * n * sizeof(T) + (size_t)kp * sizeof(int);
   int blocks = (int)ceil_div(m_rows, R);
   if (max_ctas > 0 && ticket) {
     APX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
@@ -641,7 +648,7 @@ static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const
 
 int right_gather_rows(int n, size_t elem, int k) {
   int r = 8;  // even row counts keep the fp32 pairs packed
-  while (r > 1 && (size_t)(r + (r & 1)) * n * elem + (size_t)(k + 8) * sizeof(int) > kSmemBudget)
+  while (r > 1 && (size_t)gather_pitch(r) * n * elem + (size_t)(k + 8) * sizeof(int) > kSmemBudget)
     r -= (r > 2 ? 2 : 1);
   return r;
 }
