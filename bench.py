@@ -50,6 +50,30 @@ SPANS = {  # name -> (start marker, end marker); "join" = the later of markers 2
 GATHER_SPAN = "M = A.Bhat (persistent row gather) [hi]"
 
 
+def gather_capture():
+    """DRAM traffic and L1 data-pipe load of the dominant kernel from the newest committed
+    `ncu --set full` capture (profiles/r*_gather_ncu.txt), or None."""
+    import glob
+    import re
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_gather_ncu.txt")))
+    if not files:
+        return None
+    vals = {}
+    for line in open(files[-1]):
+        m = re.match(r"(\S+)\s+([0-9.]+)\s*(\S*)", line)
+        if m:
+            scale = {"Gbyte": 1e9, "Mbyte": 1e6, "Kbyte": 1e3, "byte": 1.0}.get(m.group(3), 1.0)
+            vals[m.group(1)] = float(m.group(2)) * scale
+    try:
+        traffic = vals["dram__bytes_read.sum"] + vals["dram__bytes_write.sum"]
+        pipe = vals["l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"] / 100.0
+        grid = vals["launch__grid_size"]
+    except KeyError:
+        return None
+    return {"file": os.path.relpath(files[-1], ROOT), "traffic": traffic,
+            "l1_datapath_frac_active_sms": pipe * 148.0 / min(148.0, grid)}
+
+
 def hbm_peak():
     try:
         with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
@@ -107,6 +131,29 @@ class ClockSampler:
                     "samples": 0}
         return {"sm_mhz": float(statistics.median(self.samples)), "sm_max_mhz": self.max,
                 "reasons": sorted(self.reasons), "samples": len(self.samples)}
+
+
+# ------------------------------------------------------------------------------------------
+# multi-rank plumbing (replicas: every rank runs its own products; no data-path collective)
+# ------------------------------------------------------------------------------------------
+def replica_seed(rank: int) -> int:
+    """Operand seed of rank `rank`'s replica: independent inputs per GPU."""
+    return 1234 + 17 * rank
+
+
+def max_over_ranks(x: float, world: int, device) -> float:
+    """Max of a per-rank scalar over the job: the slowest rank sets the job's time."""
+    import torch
+    import torch.distributed as dist
+    t = torch.tensor([float(x)], device=device, dtype=torch.float64)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def job_throughput(units_per_rank: int, world: int, seconds_max: float) -> float:
+    """Whole-job rate: the units all ranks processed over the max-over-ranks time."""
+    return world * units_per_rank / seconds_max
 
 
 # ------------------------------------------------------------------------------------------
@@ -229,7 +276,7 @@ def run_ours(args, rank, world, local_rank):
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
     n = args.n
-    A, B = gen_c4(n, 1234 + 17 * rank, dev)
+    A, B = gen_c4(n, replica_seed(rank), dev)
     seed = 7
     omega = torch.from_numpy(P.cycle.draw_sketch(n, K_SVD, seed)).to(dev, torch.float32)
     M = torch.empty(n, n, device=dev, dtype=torch.float32)
@@ -268,11 +315,7 @@ def run_ours(args, rank, world, local_rank):
     launches = lib.apx_launch_count() - l0
     if world > 1:
         dist.barrier()
-    ms = start.elapsed_time(end)
-    t = torch.tensor([ms], device=dev, dtype=torch.float64)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    ms_max = float(t.item())
+    ms_max = max_over_ranks(start.elapsed_time(end), world, dev)
     def span_ms(row, a, b):
         t = [0.0] + [row[0].elapsed_time(row[i]) for i in range(1, nst)]
         ta = max(t[2], t[6]) if a == "join" else t[a]
@@ -299,12 +342,8 @@ def run_ours(args, rank, world, local_rank):
         for _ in range(e2e_steps):
             P.mixed_first_order_multiply(Ah, Bh, K_SVD, K_CYC, 1, seed, split3=split3, out=Mh)
         torch.cuda.synchronize()
-        te = time.perf_counter() - t0
-        tt = torch.tensor([te], device=dev, dtype=torch.float64)
-        if world > 1:
-            dist.all_reduce(tt, op=dist.ReduceOp.MAX)
-        te = float(tt.item())
-        e2e = {"value": world * e2e_steps / te, "unit": "products/s",
+        te = max_over_ranks(time.perf_counter() - t0, world, dev)
+        e2e = {"value": job_throughput(e2e_steps, world, te), "unit": "products/s",
                "h2d_bytes_per_step": 2 * n * n * 4 + n * K_SVD * 4,
                "d2h_bytes_per_step": n * n * 4 + N.NSCALARS * 8 + K_CYC * 4,
                "steps": e2e_steps, "ms_per_step": 1e3 * te / e2e_steps,
@@ -323,11 +362,12 @@ def run_ours(args, rank, world, local_rank):
     if rank == 0:
         peak, peak_kind = hbm_peak()
         gather_ms = stage_ms[GATHER_SPAN]
+        cap = gather_capture()
         alg_bytes = 8.0 * n * n  # A read + M write (fp32); Q.W accumulates onto it afterwards
         achieved = alg_bytes / (gather_ms * 1e-3) / 1e9
         total_alg_bytes = 24.0 * n * n  # SURVEY §8(d) C4 algorithmic bytes per product
         line = {
-            "metric": METRIC, "value": world * args.steps / (ms_max * 1e-3), "unit": "products/s",
+            "metric": METRIC, "value": job_throughput(args.steps, world, ms_max * 1e-3), "unit": "products/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
@@ -339,9 +379,13 @@ def run_ours(args, rank, world, local_rank):
             "clocks": clk.summary(), "e2e": e2e, "gpu_launches": int(launches),
             "roofline": {"bound": "hbm", "kernel": "cycle_right_gather (M = A.Bhat, persistent)",
                          "achieved": achieved, "peak": peak, "unit": "GB/s",
-                         "frac": achieved / peak, "traffic": None, "peak_kind": peak_kind,
+                         "frac": achieved / peak,
+                         "traffic": cap["traffic"] if cap else None, "peak_kind": peak_kind,
                          "alg_bytes_per_launch": alg_bytes,
-                         "note": "kernel is shared-memory-datapath bound: k*n^2 operand loads"},
+                         "datapath": ({"l1_wavefront_frac_active_sms": cap["l1_datapath_frac_active_sms"],
+                                       "source": cap["file"]} if cap else None),
+                         "note": ("the gather is bound by the SM load datapath (k*n^2 fp32 operands at "
+                                  "128 B/clk/SM), not HBM: see datapath and DESIGN.md section 4")},
             "whole_product_hbm_frac": (total_alg_bytes / (ms_max / args.steps * 1e-3) / 1e9) / peak,
             "stages_ms": stage_ms,
             "rel_err_vs_exact": rel_exact,
