@@ -35,15 +35,16 @@ sys.path.insert(0, ROOT)
 METRIC = "approx n×n products/sec at n=8192 (rel err vs exact AB); % of HBM/FP64-TC roofline"
 N_DEFAULT, K_SVD, K_CYC = 8192, 64, 64
 # Stage markers recorded by the C4 plan (capi.cu run_mixed_f32_umma): 0 start | hi stream: 1 B
-# decomposed, 2 gather done | lo stream: 3 Y, 4 QR, 5 Bm, 6 W | main: 7 M += Q.W, 8 end.
-N_MARKS = 9
+# decomposed, 2 gather done | lo stream: 3 Y, 4 QR, 5 Bm, 9 W GEMM, 6 W | main: 7 M += Q.W, 8 end.
+N_MARKS = 10
 SPANS = {  # name -> (start marker, end marker); "join" = the later of markers 2 and 6
     "B: cycle norms+select+extract [hi]": (0, 1),
     "M = A.Bhat (persistent row gather) [hi]": (1, 2),
     "Y = A.Omega (tcgen05 TF32) [lo]": (0, 3),
     "QR (CholeskyQR) [lo]": (3, 4),
     "Bm = Q^T A (+||Bm||^2) [lo]": (4, 5),
-    "W = Bm.dB (masked) [lo]": (5, 6),
+    "W0 = Bm.B (tcgen05 TF32) [lo]": (5, 9),
+    "W = W0 - Bm.Bhat (TF32-exact gather) [lo]": (9, 6),
     "M += Q.W (+||M||^2) [after join]": ("join", 7),
     "reductions": (7, 8),
 }

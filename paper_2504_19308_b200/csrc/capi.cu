@@ -221,7 +221,7 @@ struct UmmaStages {
 // time. Priorities make freed SMs go to pending gather CTAs first.
 struct SideStream {
   cudaStream_t s = nullptr, hi = nullptr;
-  cudaEvent_t fork = nullptr, join = nullptr, b_ready = nullptr, hi_done = nullptr;
+  cudaEvent_t fork = nullptr, join = nullptr, b_ready = nullptr, hi_done = nullptr, b_read = nullptr;
 };
 static thread_local SideStream g_side;
 
@@ -235,6 +235,7 @@ static int get_side(SideStream** out) {
     APX_CUDA(cudaEventCreateWithFlags(&g_side.join, cudaEventDisableTiming));
     APX_CUDA(cudaEventCreateWithFlags(&g_side.b_ready, cudaEventDisableTiming));
     APX_CUDA(cudaEventCreateWithFlags(&g_side.hi_done, cudaEventDisableTiming));
+    APX_CUDA(cudaEventCreateWithFlags(&g_side.b_read, cudaEventDisableTiming));
   }
   *out = &g_side;
   return OK;
@@ -253,7 +254,7 @@ static int gather_ctas(int nblk) {
 }
 
 // Stage markers (bench.py): 0 start | hi: 1 B decomposed, 2 gather done | lo: 3 Y, 4 QR, 5 Bm,
-// 6 W | main: 7 M += Q.W, 8 end.
+// 9 W GEMM, 6 W correction | main: 7 M += Q.W, 8 end.
 static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int kc, int order, int q,
                               const float* Omega, const int* fb, float* M, int* sb, double* scal,
                               const MixedPlan& p, cudaStream_t st) {
@@ -275,8 +276,10 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
     APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, hi));
   } else {  // selection with ||B||^2 and the kept energy fused into the select kernel
     APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, nullptr, p.partial, hi));
+    APX_CUDA(cudaEventRecord(ss->b_read, hi));
     APX_TRY(launch_topk(p.nr_b, n, kc, sb, hi, p.nr_b, 1.0, scal + APX_S_KEPT_B, p.en_b, scal + APX_S_FRO2_B));
   }
+  if (fb) APX_CUDA(cudaEventRecord(ss->b_read, hi));
   float* lb = (float*)p.lam_b;
   APX_TRY(launch_cycle_extract<float>(B, n, sb, kc, lb, hi, /*aligned=*/true));
   APX_TRY(zero_pad_rows<float>(lb, kc, n, hi));
@@ -291,9 +294,11 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   // ---- lo: randomized range finder on the SMs the gather leaves free ------------------------------
   float *Y = (float*)p.Y, *Q = (float*)p.Q, *Qt = (float*)p.Qt, *Z = (float*)p.Z, *Bm = (float*)p.Bm,
         *W = (float*)p.W, *part = (float*)p.part;
-  // Y runs on the whole GPU alongside B's decomposition (before the gather claims its SMs); the
-  // rest of the range finder then fits on the SMs the persistent gather leaves free
-  APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, lo, 32));  // 64 CTAs: SMs left for B's kernels
+  // Y starts when B's energy pass (the HBM-bound, critical part of B's decomposition) is done and
+  // overlaps the latency-bound select/extract and the gather's start; the rest of the range
+  // finder then fits on the SMs the persistent gather leaves free
+  APX_CUDA(cudaStreamWaitEvent(lo, ss->b_read, 0));
+  APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, lo, 32));  // 64 CTAs
   stage_mark(3, lo);
   APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, lo)));
   for (int it = 0; it < q; ++it) {
@@ -312,8 +317,11 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   // 64-row gather over column chunks (cheaper on a few SMs than masking every GEMM stage). The
   // subtracted gather uses the same TF32-truncated operands as the tensor core, so the large kept
   // part cancels exactly and W keeps TF32 accuracy relative to Bm . dB, not to Bm . B.
-  const int wchunks = std::max(1, free_sms / (int)ceil_div(l, right_gather_rows(n, sizeof(float), kc)));
+  // ~5 CTA waves over the free SMs: each of the l/R row blocks split into column chunks
+  const int wblocks = (int)ceil_div(l, right_gather_rows(n, sizeof(float), kc));
+  const int wchunks = std::max(1, std::min(8, (int)ceil_div(5 * free_sms, wblocks)));
   if (order == 1) APX_TRY(UmmaStages::bm_times_db(B, Bm, W, part, n, l, nullptr, 0, lo, free_sms));
+  stage_mark(9, lo);
   APX_TRY(launch_cycle_right_gather<float>(Bm, nullptr, 0, lb, sb, kc, n, l, order == 1 ? -1 : 0, W, nullptr, nullptr,
                                            lo, true, 0, nullptr, wchunks, /*tf32_operands=*/order == 1));
   stage_mark(6, lo);

@@ -1,7 +1,7 @@
 // Cycle-decomposition kernels: A = sum_j Lambda_j C^j (left layout, reference core.py:113,123-124,
 // lambda_j[i] = A[i, (i-j) mod n]) and the gather passes of the cycle-truncated product.
 //
-//  K3  cycle_energy_partial (finalize fused)        : ||lambda_j||^2 for all j in one HBM pass
+//  K3  cycle_energy_partial / cycle_energy_finalize : ||lambda_j||^2 for all j in one HBM pass
 //  K4  topk_select_kernel (select.cuh)              : top_indices semantics (circulant.py:63-70)
 //      cycle_extract                                : lambda_t for the selected shifts (k x n)
 //  K10 cycle_left_gather  : M[r,c] (+)= sum_t lamA_t[r] * X[(r - JA_t) mod n, c]   (Ahat . X)
@@ -81,6 +81,24 @@ __global__ void __launch_bounds__(256) cycle_energy_partial(const T* __restrict_
     norms[j] = sqrt(e);
   }
   if (threadIdx.x == 0) counters[blockIdx.x] = 0u;
+}
+
+// energies[j] = sum_g partial[g][j] (fixed order, 8 loads in flight); norms[j] = sqrt(energies[j]).
+__global__ void cycle_energy_finalize(const double* __restrict__ partial, int n, int groups,
+                                      double* __restrict__ energies, double* __restrict__ norms) {
+  const int j = blockIdx.x * blockDim.x + threadIdx.x;
+  if (j >= n) return;
+  double s = 0.0;
+  for (int g0 = 0; g0 < groups; g0 += 8) {
+    double v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) v[u] = g0 + u < groups ? partial[(size_t)(g0 + u) * n + j] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (g0 + u < groups) s += v[u];
+  }
+  energies[j] = s;
+  norms[j] = sqrt(s);
 }
 
 // Single-block deterministic sum of v[0..n) into *out (fixed order per thread, fixed tree).
@@ -524,10 +542,10 @@ int launch_cycle_energies(const T* A, int n, double* energies, double* norms, do
   const int groups = energy_groups(n, &rpc);
   const unsigned cb = (unsigned)ceil_div(n, 256);
   dim3 grid(cb, (unsigned)groups);
-  // finalize fused through per-column-block arrival counters kept after the partials
-  unsigned* counters = reinterpret_cast<unsigned*>(partial + (size_t)groups * n);
-  APX_CUDA(cudaMemsetAsync(counters, 0, cb * sizeof(unsigned), st));
-  cycle_energy_partial<T><<<grid, 256, 0, st>>>(A, n, rpc, partial, counters, energies, norms);
+  // separate finalize: the fused last-CTA reduce (counters != nullptr) measured 63 us vs 44 + 7
+  cycle_energy_partial<T><<<grid, 256, 0, st>>>(A, n, rpc, partial, nullptr, energies, norms);
+  APX_LAUNCH_CHECK();
+  cycle_energy_finalize<<<cb, 256, 0, st>>>(partial, n, groups, energies, norms);
   APX_LAUNCH_CHECK();
   if (fro2) {
     sum_vector_kernel<<<1, 1024, 0, st>>>(energies, n, fro2);

@@ -1,6 +1,6 @@
 set -e
 python -m pytest tests/ -m gpu -q -x 2>&1 | tail -2
-for g in 0 130 125; do
+for g in 0 134; do
   if [ $g -gt 0 ]; then export APX_GATHER_CTAS=$g; fi
   python bench.py --steps 5 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/b_$g.json 2> gpurun_out/b_$g.err
   python -c "
