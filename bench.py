@@ -326,29 +326,34 @@ def run_ours(args, rank, world, local_rank):
                 for name, (a, b) in SPANS.items()}
 
     # ---- e2e: public API with pinned host buffers (H2D inputs, D2H result, every step) ----
+    # MixedPipeline (the host-to-host serving API): each product copies its full A, B in and its
+    # full M out; product i's D2H overlaps product i+1's H2D (PCIe is full duplex) and its compute.
     e2e = None
     if not args.no_e2e:
         Ah = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
         Bh = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
-        Mh = torch.empty((n, n), dtype=torch.float32, pin_memory=True)
+        Mh = [torch.empty((n, n), dtype=torch.float32, pin_memory=True) for _ in range(3)]
         Ah.copy_(A)
         Bh.copy_(B)
-        for _ in range(max(1, min(args.warmup, 2))):
-            P.mixed_first_order_multiply(Ah, Bh, K_SVD, K_CYC, 1, seed, split3=split3, out=Mh)
-        e2e_steps = max(3, min(args.steps, 10))
+        pipe = P.MixedPipeline(n, K_SVD, K_CYC, 1, depth=3, split3=split3)
+        for i in range(2):
+            pipe.result(pipe.submit(Ah, Bh, seed, out=Mh[i % 3]))
+        e2e_steps = max(4, min(args.steps, 24))
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()
         t0 = time.perf_counter()
-        for _ in range(e2e_steps):
-            P.mixed_first_order_multiply(Ah, Bh, K_SVD, K_CYC, 1, seed, split3=split3, out=Mh)
+        tickets = [pipe.submit(Ah, Bh, seed, out=Mh[i % 3]) for i in range(e2e_steps)]
+        reps = [pipe.result(t)[1] for t in tickets]
         torch.cuda.synchronize()
         te = max_over_ranks(time.perf_counter() - t0, world, dev)
+        assert all(r.selected_b == reps[0].selected_b for r in reps)
         e2e = {"value": job_throughput(e2e_steps, world, te), "unit": "products/s",
                "h2d_bytes_per_step": 2 * n * n * 4 + n * K_SVD * 4,
                "d2h_bytes_per_step": n * n * 4 + N.NSCALARS * 8 + K_CYC * 4,
                "steps": e2e_steps, "ms_per_step": 1e3 * te / e2e_steps,
-               "path": "paper_2504_19308_b200.mixed_first_order_multiply(pinned host tensors)"}
+               "path": "paper_2504_19308_b200.MixedPipeline.submit/result (pinned host tensors, depth 3)"}
+        del pipe
 
     # ---- correctness side-channel (outside every timed region) ----
     r = step()

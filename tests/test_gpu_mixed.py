@@ -64,3 +64,21 @@ def test_mixed_rank_deficient_sketch_fp64(P):
         M, rep = P.mixed_first_order_multiply(A, B, 6, 4, order, seed=5)
         Mo, ro = O.mixed_first_order_multiply(A, B, 6, 4, order, 5)
         assert rel(M, Mo) < 1e-9
+
+
+def test_mixed_pipeline_matches_single_calls(P):
+    """MixedPipeline (overlapped H2D / compute / D2H) returns exactly the single-call results."""
+    n, k = 512, 32
+    A = O.gen_haar_spectrum(n, (np.arange(n) + 1.0) ** -1.5, 21).astype(np.float32)
+    Bs = [O.gen_cycle_operand(n, 48, 30 + i).astype(np.float32) for i in range(3)]
+    Ah = torch.from_numpy(A).pin_memory()
+    pipe = P.MixedPipeline(n, k, k, 1, depth=2)
+    outs = [torch.empty((n, n), dtype=torch.float32).pin_memory() for _ in Bs]
+    tickets = [pipe.submit(Ah, torch.from_numpy(B).pin_memory(), 5 + i, out=o)
+               for i, (B, o) in enumerate(zip(Bs, outs))]
+    for i, (B, t) in enumerate(zip(Bs, tickets)):
+        M, rep = pipe.result(t)
+        M1, rep1 = P.mixed_first_order_multiply(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), k, k, 1, 5 + i)
+        assert torch.equal(M, M1.cpu())
+        assert rep.selected_b == rep1.selected_b
+        assert rep.norm_da == rep1.norm_da and rep.norm_db == rep1.norm_db
