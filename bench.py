@@ -290,16 +290,17 @@ def run_ours(args, rank, world, local_rank):
         step()
     torch.cuda.synchronize()
 
-    # ---- timed region: K products on resident inputs ----
-    nst = N_MARKS
-    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nst)] for _ in range(args.steps)]
+    # ---- timed region: K products on resident inputs; only the gather's two stage events
+    # (markers 1, 2, recorded on the gather's stream) are live here ----
     import ctypes
     lib = N.lib()
-    for row in evs:  # torch creates the underlying cudaEvent_t lazily, on first record
+    gev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
+    for row in gev:
         for e in row:
             e.record()
     torch.cuda.synchronize()
-    ev_ptrs = [(ctypes.c_void_p * nst)(*[e.cuda_event for e in row]) for row in evs]
+    gptr = [(ctypes.c_void_p * N_MARKS)(*([None, row[0].cuda_event, row[1].cuda_event] + [None] * (N_MARKS - 3)))
+            for row in gev]
     start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
     if world > 1:
         dist.barrier()
@@ -308,12 +309,27 @@ def run_ours(args, rank, world, local_rank):
     with ClockSampler(local_rank) as clk:
         start.record()
         for s in range(args.steps):
-            lib.apx_set_stage_events(ev_ptrs[s], nst)
+            lib.apx_set_stage_events(gptr[s], N_MARKS)
             step()
         lib.apx_set_stage_events(None, 0)
         end.record()
         torch.cuda.synchronize()
     launches = lib.apx_launch_count() - l0
+    gather_ms_timed = statistics.mean(row[0].elapsed_time(row[1]) for row in gev)
+
+    # ---- full stage breakdown: the same K products again, all stage events (outside the timing) ----
+    nst = N_MARKS
+    evs = [[torch.cuda.Event(enable_timing=True) for _ in range(nst)] for _ in range(args.steps)]
+    for row in evs:  # torch creates the underlying cudaEvent_t lazily, on first record
+        for e in row:
+            e.record()
+    torch.cuda.synchronize()
+    ev_ptrs = [(ctypes.c_void_p * nst)(*[e.cuda_event for e in row]) for row in evs]
+    for s in range(args.steps):
+        lib.apx_set_stage_events(ev_ptrs[s], nst)
+        step()
+    lib.apx_set_stage_events(None, 0)
+    torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
     ms_max = max_over_ranks(start.elapsed_time(end), world, dev)
@@ -367,7 +383,7 @@ def run_ours(args, rank, world, local_rank):
     line = None
     if rank == 0:
         peak, peak_kind = hbm_peak()
-        gather_ms = stage_ms[GATHER_SPAN]
+        gather_ms = gather_ms_timed  # mean gather span inside the timed region
         cap = gather_capture()
         alg_bytes = 8.0 * n * n  # A read + M write (fp32); Q.W accumulates onto it afterwards
         achieved = alg_bytes / (gather_ms * 1e-3) / 1e9

@@ -24,7 +24,7 @@ void set_error(const char* fmt, ...) {
 void count_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
 
 void stage_mark(int i, cudaStream_t st) {
-  if (g_stage_ev != nullptr && i < g_stage_n) cudaEventRecord(g_stage_ev[i], st);
+  if (g_stage_ev != nullptr && i < g_stage_n && g_stage_ev[i] != nullptr) cudaEventRecord(g_stage_ev[i], st);
 }
 
 static inline cudaStream_t S(void* s) { return reinterpret_cast<cudaStream_t>(s); }
