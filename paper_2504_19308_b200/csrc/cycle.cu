@@ -256,6 +256,13 @@ __device__ __forceinline__ double ldg_nc_ordered(const double* p) {
 // except for a single row, which the largest n (32768 fp32, 16384 fp64) can only afford unpadded.
 __host__ __device__ constexpr int gather_pitch(int r) { return r == 1 ? 1 : r + (r & 1); }
 
+// shifts per lambda batch (U) and columns per thread (CPT) of the right gather (tuning knobs)
+#ifndef APX_GATHER_U
+#define APX_GATHER_U 4
+#endif
+#ifndef APX_GATHER_CPT
+#define APX_GATHER_CPT 4
+#endif
 #ifndef APX_GATHER_THREADS
 #define APX_GATHER_THREADS 512
 #endif
@@ -274,7 +281,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
                                                           double* __restrict__ msq_partial,
                                                           double* __restrict__ xsq_partial, int* __restrict__ ticket) {
   constexpr int RP = gather_pitch(R);  // interleave pitch (even, so float pairs stay 8B aligned)
-  constexpr int CPT = 2, U = 8;
+  constexpr int CPT = APX_GATHER_CPT, U = APX_GATHER_U;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Xs = reinterpret_cast<T*>(smem_raw);
   int* sJ = reinterpret_cast<int*>(Xs + (size_t)RP * n);
@@ -347,7 +354,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
           T v = T(0);
           if (rr < rows) v = __ldg(src + m);
           xs = fma((double)v, (double)v, xs);
-          Xs[(size_t)m * RP + rr] = v;
+          Xs[(size_t)m * RP + rr] = TRUNC ? tf32_trunc(v) : v;
         }
       }
     }
@@ -411,6 +418,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
               const bool ok = t < k && c < n;
               mm[u][q] = ok ? m * RP : 0;
               lv[u][q] = ok ? __ldg(lrow + c) : T(0);
+              if constexpr (TRUNC) lv[u][q] = tf32_trunc(lv[u][q]);
             }
           }
         }
@@ -627,7 +635,7 @@ template <typename T, int R>
 static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int m_rows,
                           int acc, T* M, double* msq_partial, double* xsq_partial, bool lam_padded, int max_ctas,
                           int* ticket, int col_chunks, bool trunc, cudaStream_t st) {
-  constexpr int U = 8, CPT = 2;
+  constexpr int U = APX_GATHER_U, CPT = APX_GATHER_CPT;
   const int kp = (int)ceil_div(std::max(k, 1), U) * U;
   const size_t smem = (size_t)gather_pitch(R) * n * sizeof(T) + (size_t)kp * sizeof(int);
   int blocks = (int)ceil_div(m_rows, R);
@@ -656,6 +664,13 @@ static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const
     cycle_right_gather<T, R, true><<<grid, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
                                                                   msq_partial, xsq_partial, ticket);
   } else {
+    if (trunc && sizeof(T) == 4) {
+      APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R, false, true>, smem));
+      cycle_right_gather<T, R, false, true><<<blocks, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
+                                                                         msq_partial, xsq_partial, ticket);
+      APX_LAUNCH_CHECK();
+      return OK;
+    }
     APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R, false>, smem));
     cycle_right_gather<T, R, false><<<blocks, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
                                                                    msq_partial, xsq_partial, ticket);
