@@ -1,0 +1,58 @@
+"""Config C4 at the headline size (n = 8192, fp32, rSVD rank 64 x 64 cycles, order 1) on the
+bench's synthetic operands (bench.gen_c4): oracle parity on a row sample (the full oracle
+product would take minutes) and the first-order identity on a random probe.
+
+  * selection of B's cycles: bit-exact vs the oracle;
+  * 16 output rows vs oracle.mixed_first_order_multiply(rows=...): rel. Frobenius <= 1e-4;
+  * (AB - M) x = dA (dB x) with the oracle's factors (fp64 matvecs), relative to ||ABx|| <= 1e-4.
+"""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+
+N, K, SEED = 8192, 64, 7
+
+
+@pytest.fixture(scope="module")
+def c4():
+    import bench
+    import paper_2504_19308_b200 as P
+    A, B = bench.gen_c4(N, 1234, torch.device("cuda", 0))
+    M, rep = P.mixed_first_order_multiply(A, B, K, K, 1, SEED)
+    torch.cuda.synchronize()
+    A64, B64 = A.double().cpu().numpy(), B.double().cpu().numpy()
+    yield A, B, M, rep, A64, B64
+    del A, B, M
+    torch.cuda.empty_cache()
+
+
+def test_c4_rows_and_selection(c4):
+    A, B, M, rep, A64, B64 = c4
+    rows = np.linspace(0, N - 1, 16).astype(int)
+    Mo, ro = O.mixed_first_order_multiply(A64, B64, K, K, 1, SEED, rows=rows)
+    assert rep.selected_b == ro["selected_b"]
+    err = rel(M[torch.from_numpy(rows).cuda()].double().cpu().numpy(), Mo)
+    print(f"C4 n={N}: 16 rows rel vs oracle {err:.3e}")
+    assert err < 1e-4
+    assert rep.norm_db == pytest.approx(ro["norm_db"], rel=1e-5)
+
+
+def test_c4_first_order_identity(c4):
+    A, B, M, rep, A64, B64 = c4
+    U, s, V, _ = O.rsvd(A64, K, np.random.default_rng([SEED, 0]), 0)
+    Jb, lamB, _, _, _ = O.cycle_decompose(B64, K, force_sel=rep.selected_b)
+    x = np.random.default_rng(11).standard_normal(N)
+    i = np.arange(N)
+    Bx = B64 @ x
+    Bhat_x = sum(lamB[t] * x[(i - j) % N] for t, j in enumerate(Jb))
+    dBx = Bx - Bhat_x
+    dA_dBx = A64 @ dBx - U @ (s * (V.T @ dBx))
+    lhs = A64 @ Bx - (M.double() @ torch.from_numpy(x).cuda()).cpu().numpy()
+    err = float(np.linalg.norm(lhs - dA_dBx) / np.linalg.norm(A64 @ Bx))
+    print(f"C4 first-order identity on a probe: {err:.3e}")
+    assert err < 1e-4
