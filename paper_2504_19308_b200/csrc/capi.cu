@@ -51,6 +51,10 @@ struct CyclePlan {
   void* lam_a;       // k_a x n
   void* lam_b;       // k_b x n
   void* bhat;        // n x n (order 0 only)
+  void* xt;          // n x n: X^T for the transposed left product (large n only)
+  void* tt;          // n x n: (A_hat . X)^T
+  int* jneg;         // (n - J_A) mod n
+  bool left_t;       // A_hat . X evaluated as (X^T A_hat^T)^T with the right gather
   double* msq;       // ||M||^2 partials
   int n_msq;
 };
@@ -62,9 +66,13 @@ static void plan_cycle(Workspace& ws, CyclePlan& p, int dtype, int n, int ka, in
   p.nr_a = ws.take<double>(n);
   p.en_b = ws.take<double>(n);
   p.nr_b = ws.take<double>(n);
-  p.lam_a = ws.take<char>((size_t)std::max(ka, 1) * n * e);
+  p.lam_a = ws.take<char>((size_t)pad8(ka) * n * e);
   p.lam_b = ws.take<char>((size_t)pad8(kb) * n * e);
   p.bhat = order == 0 ? (void*)ws.take<char>((size_t)n * n * e) : nullptr;
+  p.left_t = left_via_transpose(n, e, ka);
+  p.xt = p.left_t ? (void*)ws.take<char>((size_t)n * n * e) : nullptr;
+  p.tt = p.left_t ? (void*)ws.take<char>((size_t)n * n * e) : nullptr;
+  p.jneg = ws.take<int>((size_t)pad8(ka));
   p.n_msq = std::max<int>((int)ceil_div(n, 1), kNumSMs * 4);
   p.msq = ws.take<double>(p.n_msq);
 }
@@ -85,12 +93,25 @@ static int run_cycle(const T* A, const T* B, int n, int ka, int kb, int order, c
   T* la = (T*)p.lam_a;
   T* lb = (T*)p.lam_b;
   APX_TRY(launch_cycle_extract<T>(A, n, sa, ka, la, st));
+  APX_TRY(zero_pad_rows<T>(la, ka, n, st));
   APX_TRY(launch_cycle_extract<T>(B, n, sb, kb, lb, st, /*aligned=*/order == 1));  // order 0: materialize
   APX_TRY(zero_pad_rows<T>(lb, kb, n, st));
   stage_mark(1, st);
+  // Ahat . X: column strips of X in shared memory (left gather), or for large n -- where a strip
+  // is one or two columns and every lambda would be re-read per column -- as (X^T Ahat^T)^T:
+  // Ahat^T has shifts n - J_t and, aligned to its output index, the left-layout table itself, so
+  // the row-block right gather runs on X^T (R rows resident, each lambda feeding R FMAs)
+  auto left_product = [&](const T* X, T* out) -> int {
+    if (!p.left_t) return launch_cycle_left_gather<T>(X, la, sa, ka, n, 0, out, st);
+    T *xt = (T*)p.xt, *tt = (T*)p.tt;
+    APX_TRY(launch_transpose_any(X, n, n, n, xt, n, st));
+    APX_TRY(launch_negate_shifts(sa, ka, n, p.jneg, st));
+    APX_TRY(launch_cycle_right_gather<T>(xt, nullptr, 0, la, p.jneg, ka, n, n, 0, tt, nullptr, nullptr, st, true));
+    return launch_transpose_any(tt, n, n, n, out, n, st);
+  };
   if (order == 1) {
-    // M = Ahat . B   (left gather over column strips of B)
-    APX_TRY(launch_cycle_left_gather<T>(B, la, sa, ka, n, 0, M, st));
+    // M = Ahat . B
+    APX_TRY(left_product(B, M));
     stage_mark(2, st);
     // M += dA . Bhat (right gather over row blocks of A, masked to dA on load) + ||M||^2
     APX_TRY(launch_cycle_right_gather<T>(A, sa, ka, lb, sb, kb, n, n, 1, M, p.msq, nullptr, st, true));
@@ -100,7 +121,7 @@ static int run_cycle(const T* A, const T* B, int n, int ka, int kb, int order, c
   } else {
     T* bh = (T*)p.bhat;
     APX_TRY(launch_cycle_materialize<T>(lb, sb, kb, n, bh, st));
-    APX_TRY(launch_cycle_left_gather<T>(bh, la, sa, ka, n, 0, M, st));
+    APX_TRY(left_product(bh, M));
     int parts = 0;
     APX_TRY(launch_sumsq<T>(M, (size_t)n * n, p.msq, &parts, st));
     APX_TRY(launch_sum_vector(p.msq, parts, scal + APX_S_FRO2_M, st));

@@ -129,6 +129,9 @@ __global__ void triu_kernel(double* R, int k) {
 int launch_transpose_f64(const double* in, int64_t ldi, int rows, int cols, double* out, int64_t ldo, cudaStream_t st) {
   return launch_transpose<double>(in, ldi, rows, cols, out, ldo, st);
 }
+int launch_transpose_f32(const float* in, int64_t ldi, int rows, int cols, float* out, int64_t ldo, cudaStream_t st) {
+  return launch_transpose<float>(in, ldi, rows, cols, out, ldo, st);
+}
 
 }  // namespace apx
 

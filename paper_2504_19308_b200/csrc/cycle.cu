@@ -616,6 +616,29 @@ static int left_gather_w(const T* X, const T* lam, const int* J, int k, int n, i
   return OK;
 }
 
+__global__ void negate_shifts_kernel(const int* __restrict__ J, int k, int n, int* __restrict__ out) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  if (t < k) out[t] = J[t] == 0 ? 0 : n - J[t];
+}
+
+int launch_negate_shifts(const int* J, int k, int n, int* out, cudaStream_t st) {
+  if (k <= 0) return OK;
+  negate_shifts_kernel<<<(unsigned)ceil_div(k, 256), 256, 0, st>>>(J, k, n, out);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+static int left_strip_width(int n, size_t elem) {
+  const size_t per_col = (size_t)n * elem;
+  int w = 1;
+  while (w < 8 && (size_t)(2 * w + 1) * per_col <= kSmemBudget) w *= 2;
+  return w;
+}
+
+bool left_via_transpose(int n, size_t elem, int k) {
+  return left_strip_width(n, elem) <= 2 && (n % (kGatherThreads * APX_GATHER_CPT)) == 0 && k > 0;
+}
+
 template <typename T>
 int launch_cycle_left_gather(const T* X, const T* lam, const int* J, int k, int n, int accumulate, T* M,
                              cudaStream_t st) {

@@ -66,4 +66,18 @@ int launch_axpy2d(double* y, int64_t ldy, const double* x, int64_t ldx, int rows
                   const double* rowscale, int overwrite, cudaStream_t st);
 int launch_sumsq_prefix(const double* s, int k, double* out, cudaStream_t st);
 int launch_transpose_f64(const double* in, int64_t ldi, int rows, int cols, double* out, int64_t ldo, cudaStream_t st);
+int launch_transpose_f32(const float* in, int64_t ldi, int rows, int cols, float* out, int64_t ldo, cudaStream_t st);
+inline int launch_transpose_any(const float* in, int64_t ldi, int rows, int cols, float* out, int64_t ldo,
+                                cudaStream_t st) {
+  return launch_transpose_f32(in, ldi, rows, cols, out, ldo, st);
+}
+inline int launch_transpose_any(const double* in, int64_t ldi, int rows, int cols, double* out, int64_t ldo,
+                                cudaStream_t st) {
+  return launch_transpose_f64(in, ldi, rows, cols, out, ldo, st);
+}
+// out[t] = (n - J[t]) mod n
+int launch_negate_shifts(const int* J, int k, int n, int* out, cudaStream_t st);
+// true when the left gather (column strips of width <= 2) is better replaced by the transposed
+// right gather (A.X = (X^T A^T)^T) -- large n, where a column strip barely fits shared memory
+bool left_via_transpose(int n, size_t elem, int k);
 }  // namespace apx

@@ -120,3 +120,22 @@ def test_validation_errors(P):
         P.cycle_first_order_multiply(np.ones((4, 4)), np.ones((4, 4)), 1, 2)
     with pytest.raises(ValueError):
         P.cycle_first_order_multiply([[np.nan, 1.0], [1.0, 1.0]], np.ones((2, 2)), 1, 1)
+
+
+@pytest.mark.parametrize("order", [0, 1])
+def test_cycle_transposed_left_fp64(P, order):
+    """n = 4096 fp64: Ahat . X runs as (X^T Ahat^T)^T through the row-block gather (the column
+    strip of the left gather would be 2 columns wide); full oracle comparison at 1e-10."""
+    n, k = 4096, 12
+    A = O.gen_cycle_operand(n, 2 * k, 71)
+    B = O.gen_cycle_operand(n, 2 * k, 72)
+    M, rep = P.cycle_first_order_multiply(A, B, k, order)
+    rows = np.array([0, 1, 100, 2047, 4095])
+    Ja, la_, _, _, _ = O.cycle_decompose(A, k)
+    Jb, lb_, _, _, _ = O.cycle_decompose(B, k)
+    assert rep.selected_a == Ja and rep.selected_b == Jb
+    if order == 1:
+        Mo = O.cycle_product_rows(rows, A[rows], Ja, [B[(rows - j) % n] for j in Ja], Jb, lb_)
+    else:
+        Mo = O.apx_oracle._cycle_left_apply(Ja, la_, O.cycle_materialize(Jb, lb_, n), rows=rows)
+    assert rel(M[rows], Mo) < 1e-10
