@@ -102,7 +102,7 @@ __global__ void transpose_kernel(const T* __restrict__ in, int64_t ldi, int rows
   const int bx = blockIdx.x * 32, by = blockIdx.y * 32;
   for (int y = threadIdx.y; y < 32; y += blockDim.y) {
     const int r = by + y, c = bx + threadIdx.x;
-    tile[y][threadIdx.x] = (r < rows && c < cols) ? in[(size_t)r * ldi + c] : T(0);
+    tile[y][threadIdx.x] = (r < rows && c < cols) ? in[(size_t)r * ldi + c] : T{};
   }
   __syncthreads();
   for (int y = threadIdx.y; y < 32; y += blockDim.y) {
@@ -131,6 +131,10 @@ int launch_transpose_f64(const double* in, int64_t ldi, int rows, int cols, doub
 }
 int launch_transpose_f32(const float* in, int64_t ldi, int rows, int cols, float* out, int64_t ldo, cudaStream_t st) {
   return launch_transpose<float>(in, ldi, rows, cols, out, ldo, st);
+}
+int launch_transpose_c128(const double2* in, int64_t ldi, int rows, int cols, double2* out, int64_t ldo,
+                          cudaStream_t st) {
+  return launch_transpose<double2>(in, ldi, rows, cols, out, ldo, st);
 }
 
 }  // namespace apx

@@ -38,18 +38,51 @@ __device__ __forceinline__ double2 ld_c<double2>(const double2* p, size_t i) {
   return __ldg(p + i);
 }
 
+// (t * c) mod n for 0 <= t, c < n: a mask for power-of-two n, 32-bit arithmetic while n^2 < 2^32
+__device__ __forceinline__ int mulmod_n(int t, int c, int n) {
+  if ((n & (n - 1)) == 0) return (t * c) & (n - 1);
+  if (n < 65536) return (int)(((unsigned)t * (unsigned)c) % (unsigned)n);
+  return (int)(((long long)t * c) % n);
+}
+
 static size_t fft_smem_bytes(int n, int buffers) {
   return (size_t)(buffers + (is_pow2(n) ? 0 : 1)) * n * sizeof(double2);
 }
 
 // ---------------------------------------------------------------------------------------------
-// decompose: CTA handles cycles [j0, j0 + cpc); per cycle: gather, FFT, scale, store S column
-// and fold |S[t][j]|^2 into a per-CTA partial of the magnitudes.
+// skew: X[j][i] = A[(i+j)%n][i] (row j = cycle j in the right layout, core.py:113). The diagonal
+// read of the cycle layout touches one element per row of A -- one DRAM sector per element -- so
+// it is done once, tile by tile: a 32 x 32 tile of X needs a 63-row parallelogram of A whose
+// rows are contiguous column segments (coalesced reads), staged in shared memory and written
+// back as contiguous rows of X.
 // ---------------------------------------------------------------------------------------------
 template <typename T>
-__global__ void __launch_bounds__(512) circ_decompose_kernel(const T* __restrict__ A, int n, int cpc,
-                                                             const double2* __restrict__ roots,
-                                                             double2* __restrict__ S, double* __restrict__ mag2_part) {
+__global__ void __launch_bounds__(256) circ_skew_kernel(const T* __restrict__ A, int n, T* __restrict__ X) {
+  __shared__ T tile[32][33];
+  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+  for (int d = warp; d < 63; d += 8) {  // source row r = i0 + j0 + d, column i0 + lane, j = d - lane
+    const int jj = d - lane;
+    if (jj < 0 || jj >= 32 || i0 + lane >= n || j0 + jj >= n) continue;
+    int r = i0 + j0 + d;
+    r %= n;
+    tile[jj][lane] = A[(size_t)r * n + i0 + lane];
+  }
+  __syncthreads();
+  for (int jj = warp; jj < 32; jj += 8)
+    if (j0 + jj < n && i0 + lane < n) X[(size_t)(j0 + jj) * n + i0 + lane] = tile[jj][lane];
+}
+
+// ---------------------------------------------------------------------------------------------
+// decompose: CTA handles cycles [j0, j0 + cpc); per cycle: the (contiguous) row j of the skewed
+// copy, FFT, scale, store row j of S^T, and fold |S[t][j]|^2 into a per-CTA partial of the
+// magnitudes.
+// ---------------------------------------------------------------------------------------------
+template <typename T>
+__global__ void __launch_bounds__(512) circ_decompose_rows_kernel(const T* __restrict__ X, int n, int cpc,
+                                                                  const double2* __restrict__ roots,
+                                                                  double2* __restrict__ St,
+                                                                  double* __restrict__ mag2_part) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* x = reinterpret_cast<double2*>(smem_raw);
   double2* scratch = x + n;
@@ -58,16 +91,12 @@ __global__ void __launch_bounds__(512) circ_decompose_kernel(const T* __restrict
   const double inv_n = 1.0 / n;
   const int j0 = blockIdx.x * cpc, j1 = min(n, j0 + cpc);
   for (int j = j0; j < j1; ++j) {
-    for (int i = threadIdx.x; i < n; i += blockDim.x) {
-      int r = i + j;
-      if (r >= n) r -= n;
-      x[i] = ld_c<T>(A, (size_t)r * n + i);  // right layout: cycle j, entry i = A[(i+j)%n][i]
-    }
+    for (int i = threadIdx.x; i < n; i += blockDim.x) x[fsw(i, n)] = ld_c<T>(X, (size_t)j * n + i);
     __syncthreads();
     fft_block(x, scratch, n, roots, false);
     for (int t = threadIdx.x; t < n; t += blockDim.x) {
-      const double2 v = cscale(x[t], inv_n);
-      if (S) S[(size_t)t * n + j] = v;
+      const double2 v = cscale(x[fsw(t, n)], inv_n);
+      St[(size_t)j * n + t] = v;
       m2[t] = fma(v.x, v.x, fma(v.y, v.y, m2[t]));
     }
     __syncthreads();
@@ -83,7 +112,7 @@ __global__ void mag_finalize_kernel(const double* __restrict__ part, int parts, 
   mag[t] = sqrt(s);
 }
 
-// Selected spectrum rows: Ssel[q] = S[sel[q]], L[q] = fft(S[sel[q]]) (unnormalised, :145)
+// Selected spectrum rows from S^T: Ssel[q] = S[sel[q]], L[q] = fft(S[sel[q]]) (unnormalised, :145)
 __global__ void __launch_bounds__(512) circ_spectra_kernel(const double2* __restrict__ S, int n,
                                                            const int* __restrict__ sel,
                                                            const double2* __restrict__ roots,
@@ -92,15 +121,27 @@ __global__ void __launch_bounds__(512) circ_spectra_kernel(const double2* __rest
   double2* x = reinterpret_cast<double2*>(smem_raw);
   double2* scratch = x + n;
   const int q = blockIdx.x;
-  const double2* row = S + (size_t)sel[q] * n;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) {
-    const double2 v = row[i];
-    x[i] = v;
-    if (Ssel) Ssel[(size_t)q * n + i] = v;
+  const int t = sel[q];
+  // row t of S = column t of S^T (strided; 8 loads per thread in flight)
+  for (int i0 = threadIdx.x; i0 < n; i0 += 8 * blockDim.x) {
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * blockDim.x;
+      v[u] = i < n ? __ldg(S + (size_t)i * n + t) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int i = i0 + u * blockDim.x;
+      if (i < n) {
+        x[fsw(i, n)] = v[u];
+        if (Ssel) Ssel[(size_t)q * n + i] = v[u];
+      }
+    }
   }
   __syncthreads();
   fft_block(x, scratch, n, roots, false);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) L[(size_t)q * n + i] = x[i];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) L[(size_t)q * n + i] = x[fsw(i, n)];
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -116,7 +157,18 @@ __global__ void __launch_bounds__(512) circ_left_kernel(const T* __restrict__ B,
   double2* scratch = y + n;
   const int c = blockIdx.x;
   const double rs = rsqrt((double)n);
-  for (int p = threadIdx.x; p < n; p += blockDim.x) x[p] = ld_c<T>(B, (size_t)p * n + c);
+  // column c of B: strided, so 8 loads per thread are issued before the first store
+  for (int p0 = threadIdx.x; p0 < n; p0 += 8 * blockDim.x) {
+    double2 v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int p = p0 + u * blockDim.x;
+      v[u] = p < n ? ld_c<T>(B, (size_t)p * n + c) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u)
+      if (p0 + u * blockDim.x < n) x[fsw(p0 + u * blockDim.x, n)] = v[u];
+  }
   __syncthreads();
   fft_block(x, scratch, n, roots, false);
   for (int p = threadIdx.x; p < n; p += blockDim.x) {
@@ -124,13 +176,13 @@ __global__ void __launch_bounds__(512) circ_left_kernel(const T* __restrict__ B,
     for (int q = 0; q < k; ++q) {
       int src = p - sel[q];
       if (src < 0) src += n;
-      acc = cadd(acc, cmul(__ldg(L + (size_t)q * n + p), cscale(x[src], rs)));
+      acc = cadd(acc, cmul(__ldg(L + (size_t)q * n + p), cscale(x[fsw(src, n)], rs)));
     }
-    y[p] = acc;
+    y[fsw(p, n)] = acc;
   }
   __syncthreads();
   fft_block(y, scratch, n, roots, true);
-  for (int p = threadIdx.x; p < n; p += blockDim.x) M[(size_t)p * n + c] = cscale(y[p], rs);
+  for (int p = threadIdx.x; p < n; p += blockDim.x) M[(size_t)p * n + c] = cscale(y[fsw(p, n)], rs);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -157,12 +209,11 @@ __global__ void __launch_bounds__(512) circ_right_kernel(const T* __restrict__ A
     if (d < 0) d += n;
     for (int q = 0; q < ka; ++q) {
       const int t = selA[q];
-      const int e = (int)(((long long)t * c) % n);
-      const double2 w = cconj(__ldg(roots + e));  // exp(+2 pi i t c / n)
+      const double2 w = cconj(__ldg(roots + mulmod_n(t, c, n)));  // exp(+2 pi i t c / n)
       ah = cadd(ah, cmul(__ldg(SselA + (size_t)q * n + d), w));
     }
     const double2 a = ld_c<T>(A, (size_t)r * n + c);
-    x[c] = cconj(csub(a, ah));
+    x[fsw(c, n)] = cconj(csub(a, ah));
   }
   __syncthreads();
   fft_block(x, scratch, n, roots, false);
@@ -171,14 +222,14 @@ __global__ void __launch_bounds__(512) circ_right_kernel(const T* __restrict__ A
     for (int q = 0; q < kb; ++q) {
       int src = p + selB[q];
       if (src >= n) src -= n;
-      acc = cadd(acc, cmulc(cscale(x[src], rs), __ldg(LB + (size_t)q * n + src)));
+      acc = cadd(acc, cmulc(cscale(x[fsw(src, n)], rs), __ldg(LB + (size_t)q * n + src)));
     }
-    y[p] = acc;
+    y[fsw(p, n)] = acc;
   }
   __syncthreads();
   fft_block(y, scratch, n, roots, true);
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    const double2 v = cconj(cscale(y[c], rs));
+    const double2 v = cconj(cscale(y[fsw(c, n)], rs));
     double2* pm = M + (size_t)r * n + c;
     *pm = cadd(*pm, v);
   }
@@ -193,10 +244,7 @@ __global__ void circ_materialize_kernel(const double2* __restrict__ Ssel, const 
     int d = r - c;
     if (d < 0) d += n;
     double2 acc = make_double2(0.0, 0.0);
-    for (int q = 0; q < k; ++q) {
-      const int idx = (int)(((long long)sel[q] * c) % n);
-      acc = cadd(acc, cmul(Ssel[(size_t)q * n + d], cconj(roots[idx])));
-    }
+    for (int q = 0; q < k; ++q) acc = cadd(acc, cmul(Ssel[(size_t)q * n + d], cconj(roots[mulmod_n(sel[q], c, n)])));
     out[e] = acc;
   }
 }
@@ -227,10 +275,10 @@ __global__ void __launch_bounds__(512) dft_batch_kernel(const double2* __restric
   double2* x = reinterpret_cast<double2*>(smem_raw);
   double2* scratch = x + n;
   const int64_t b = blockIdx.x;
-  for (int i = threadIdx.x; i < n; i += blockDim.x) x[i] = in[b * dist + (int64_t)i * stride];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) x[fsw(i, n)] = in[b * dist + (int64_t)i * stride];
   __syncthreads();
   fft_block(x, scratch, n, roots, inverse != 0);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) out[b * dist + (int64_t)i * stride] = cscale(x[i], scale);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) out[b * dist + (int64_t)i * stride] = cscale(x[fsw(i, n)], scale);
 }
 
 // cycle layouts (core.py:106-137) and cycle powers (:140-154), element size es (8 or 16 bytes)
@@ -286,12 +334,16 @@ static void plan_circ(Workspace& ws, CircPlan& p, int n, int k, bool need_sa_ful
   p.red = ws.take<double>(4 * kNumSMs + 64);
 }
 
+// S^T (St[j][t] = S[t][j]) and the magnitudes; `skew` is n x n scratch of T
 template <typename T>
-static int circ_decompose_run(const T* A, int n, const CircPlan& p, double2* S, double* mag, cudaStream_t st) {
+static int circ_decompose_run(const T* A, int n, const CircPlan& p, double2* St, double* mag, T* skew,
+                              cudaStream_t st) {
   const size_t smem = fft_smem_bytes(n, 1) + (size_t)n * sizeof(double);
-  auto fn = circ_decompose_kernel<T>;
+  circ_skew_kernel<T><<<dim3((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32)), 256, 0, st>>>(A, n, skew);
+  APX_LAUNCH_CHECK();
+  auto fn = circ_decompose_rows_kernel<T>;
   APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  fn<<<p.parts, 512, smem, st>>>(A, n, p.cpc, p.roots, S, p.part);
+  fn<<<p.parts, 512, smem, st>>>(skew, n, p.cpc, p.roots, St, p.part);
   APX_LAUNCH_CHECK();
   mag_finalize_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(p.part, p.parts, n, mag);
   APX_LAUNCH_CHECK();
@@ -315,13 +367,14 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
   APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
   launch_roots(p.roots, n, st);
   APX_LAUNCH_CHECK();
-  APX_TRY(circ_decompose_run<T>(A, n, p, p.S_a, p.mag_a, st));
+  T* skew = reinterpret_cast<T*>(M);  // M (n x n complex) is scratch until the left product
+  APX_TRY(circ_decompose_run<T>(A, n, p, p.S_a, p.mag_a, skew, st));
   if (fa) { if (k) APX_CUDA(cudaMemcpyAsync(sa, fa, k * sizeof(int), cudaMemcpyDeviceToDevice, st)); }
   else APX_TRY(launch_topk(p.mag_a, n, k, sa, st));
   APX_TRY(launch_kept_energy(p.mag_a, sa, k, (double)n, scal + APX_S_KEPT_A, st));
   APX_TRY(circ_spectra_run(p.S_a, n, sa, k, p.roots, p.Ssel_a, p.L_a, st));
   // B's spectrum reuses S_a's storage (A's selected rows are already copied out)
-  APX_TRY(circ_decompose_run<T>(B, n, p, p.S_b, p.mag_b, st));
+  APX_TRY(circ_decompose_run<T>(B, n, p, p.S_b, p.mag_b, skew, st));
   if (fb) { if (k) APX_CUDA(cudaMemcpyAsync(sb, fb, k * sizeof(int), cudaMemcpyDeviceToDevice, st)); }
   else APX_TRY(launch_topk(p.mag_b, n, k, sb, st));
   APX_TRY(launch_kept_energy(p.mag_b, sb, k, (double)n, scal + APX_S_KEPT_B, st));
@@ -390,10 +443,11 @@ int apx_circulant_first_order(int dtype, const void* A, const void* B, int64_t n
 }
 
 size_t apx_circulant_decompose_workspace(int dtype, int64_t n) {
-  (void)dtype;
   Workspace ws(nullptr, 0, true);
   ws.take<double2>(n);
   ws.take<double>((size_t)ceil_div(n, std::max(1, (int)ceil_div(n, 2 * kNumSMs))) * n);
+  ws.take<double2>((size_t)n * n);                                  // S^T
+  ws.take<char>((size_t)n * n * (dtype == C128 ? 16 : 8));           // skewed copy of A
   return ws.off;
 }
 
@@ -409,11 +463,16 @@ int apx_circulant_decompose(int dtype, const void* A, int64_t n, void* columns, 
   p.parts = (int)ceil_div(n, p.cpc);
   p.roots = ws.take<double2>(n);
   p.part = ws.take<double>((size_t)p.parts * n);
+  double2* St = ws.take<double2>((size_t)n * n);
+  void* skew = ws.take<char>((size_t)n * n * (dtype == C128 ? 16 : 8));
   APX_WS_CHECK(ws);
   launch_roots(p.roots, (int)n, st);
   APX_LAUNCH_CHECK();
-  if (dtype == F64) return circ_decompose_run<double>((const double*)A, (int)n, p, (double2*)columns, magnitudes, st);
-  return circ_decompose_run<double2>((const double2*)A, (int)n, p, (double2*)columns, magnitudes, st);
+  if (dtype == F64)
+    APX_TRY(circ_decompose_run<double>((const double*)A, (int)n, p, St, magnitudes, (double*)skew, st));
+  else
+    APX_TRY(circ_decompose_run<double2>((const double2*)A, (int)n, p, St, magnitudes, (double2*)skew, st));
+  return launch_transpose_c128(St, n, (int)n, (int)n, (double2*)columns, n, st);
 }
 
 size_t apx_circulant_materialize_workspace(int64_t n) {

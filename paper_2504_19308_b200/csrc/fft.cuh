@@ -28,6 +28,13 @@ __host__ __device__ inline int ilog2(int n) {
   return l;
 }
 
+// Shared-memory slot of element i of a transform buffer of length n. Power-of-two buffers are
+// XOR-swizzled inside each group of 8 complex values (slot = i ^ ((i >> 3) & 7)), which makes
+// every radix-8 pass below -- stride-8 groups in the first pass, stride-1 in the later ones --
+// hit all eight 16-byte bank groups evenly. Every access to a buffer passed to fft_block must go
+// through fsw().
+__device__ __forceinline__ int fsw(int i, int n) { return (n & (n - 1)) == 0 ? (i ^ ((i >> 3) & 7)) : i; }
+
 // roots[k] = exp(-2 pi i k / n) for k < n (full table; pow2 transforms use the first n/2)
 void launch_roots(double2* roots, int n, cudaStream_t st);
 
@@ -42,13 +49,45 @@ __device__ inline void fft_block(double2* x, double2* scratch, int n, const doub
     for (int i = tid; i < n; i += nt) {
       const int j = (int)(__brev((unsigned)i) >> (32 - logn));
       if (i < j) {
-        const double2 t = x[i];
-        x[i] = x[j];
-        x[j] = t;
+        const double2 t = x[fsw(i, n)];
+        x[fsw(i, n)] = x[fsw(j, n)];
+        x[fsw(j, n)] = t;
       }
     }
     __syncthreads();
-    for (int s = 1; s <= logn; ++s) {
+    // radix-8 passes: three consecutive radix-2 DIT stages s, s+1, s+2 on the 8 elements
+    // base + pos + m*h (h = 2^(s-1)) held in registers -- one shared-memory round trip and one
+    // barrier per three stages; the same twiddles and butterfly order as the radix-2 stages below
+    int s = 1;
+    for (; s + 2 <= logn; s += 3) {
+      const int h = 1 << (s - 1);
+      for (int g = tid; g < (n >> 3); g += nt) {
+        const int pos = g & (h - 1);
+        const int base = (g >> (s - 1)) << (s + 2);
+        double2 v[8];
+#pragma unroll
+        for (int m = 0; m < 8; ++m) v[m] = x[fsw(base + pos + m * h, n)];
+#pragma unroll
+        for (int st = 0; st < 3; ++st) {
+          const int hs = 1 << st;  // pair distance in units of h
+#pragma unroll
+          for (int m = 0; m < 8; ++m) {
+            if (m & hs) continue;
+            const int q = pos + (m & (hs - 1)) * h;  // offset inside the stage's butterfly block
+            double2 w = __ldg(roots + (q << (logn - s - st)));
+            if (inverse) w.y = -w.y;
+            const double2 t = cmul(w, v[m + hs]);
+            const double2 u = v[m];
+            v[m] = cadd(u, t);
+            v[m + hs] = csub(u, t);
+          }
+        }
+#pragma unroll
+        for (int m = 0; m < 8; ++m) x[fsw(base + pos + m * h, n)] = v[m];
+      }
+      __syncthreads();
+    }
+    for (; s <= logn; ++s) {
       const int half = 1 << (s - 1);
       for (int b = tid; b < (n >> 1); b += nt) {
         const int pos = b & (half - 1);
@@ -56,10 +95,10 @@ __device__ inline void fft_block(double2* x, double2* scratch, int n, const doub
         const int j = i + half;
         double2 w = __ldg(roots + (pos << (logn - s)));
         if (inverse) w.y = -w.y;
-        const double2 t = cmul(w, x[j]);
-        const double2 u = x[i];
-        x[i] = cadd(u, t);
-        x[j] = csub(u, t);
+        const double2 t = cmul(w, x[fsw(j, n)]);
+        const double2 u = x[fsw(i, n)];
+        x[fsw(i, n)] = cadd(u, t);
+        x[fsw(j, n)] = csub(u, t);
       }
       __syncthreads();
     }

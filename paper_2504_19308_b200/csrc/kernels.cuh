@@ -67,6 +67,8 @@ int launch_axpy2d(double* y, int64_t ldy, const double* x, int64_t ldx, int rows
 int launch_sumsq_prefix(const double* s, int k, double* out, cudaStream_t st);
 int launch_transpose_f64(const double* in, int64_t ldi, int rows, int cols, double* out, int64_t ldo, cudaStream_t st);
 int launch_transpose_f32(const float* in, int64_t ldi, int rows, int cols, float* out, int64_t ldo, cudaStream_t st);
+int launch_transpose_c128(const double2* in, int64_t ldi, int rows, int cols, double2* out, int64_t ldo,
+                          cudaStream_t st);
 inline int launch_transpose_any(const float* in, int64_t ldi, int rows, int cols, float* out, int64_t ldo,
                                 cudaStream_t st) {
   return launch_transpose_f32(in, ldi, rows, cols, out, ldo, st);
