@@ -111,7 +111,9 @@ __global__ void __launch_bounds__(kThreads, 1)
   using CF = Cfg<BN, STAGES>;
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte alignment for the swizzled tiles
-  unsigned char* smem = (unsigned char*)(((uintptr_t)smem_raw + 1023) & ~(uintptr_t)1023);
+  // 1024-byte alignment by pointer arithmetic on the shared array (an integer round trip would
+  // lose the address space and turn every epilogue shared access into a generic one)
+  unsigned char* smem = smem_raw + ((1024u - (saddr(smem_raw) & 1023u)) & 1023u);
   uint64_t* full = reinterpret_cast<uint64_t*>(smem + (size_t)STAGES * CF::kStage);
   uint64_t* empty = full + STAGES;
   uint64_t* masked = empty + STAGES;
@@ -288,7 +290,8 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       __syncwarp();
-#pragma unroll 1
+      float sq32[2] = {0.f, 0.f};  // short fp32 partial sums, folded into the fp64 total
+#pragma unroll 4
       for (int r = 0; r < 32; ++r) {
         const int rg = rbase + r;
         if (rg >= M) break;
@@ -299,10 +302,11 @@ __global__ void __launch_bounds__(kThreads, 1)
           const float val = rowp[((((c >> 2) ^ (r & 7))) << 2) | (c & 3)];
           if (n0 + c < N) {
             Cz[(size_t)rg * ldc + n0 + c] = val;
-            sq = fma((double)val, (double)val, sq);
+            sq32[r & 1] = fmaf(val, val, sq32[r & 1]);
           }
         }
       }
+      sq += (double)sq32[0] + (double)sq32[1];
     }
 #pragma unroll 1
     for (int j0 = 0; j0 < BN && !stage_c; j0 += 32) {

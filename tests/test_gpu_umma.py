@@ -101,3 +101,4 @@ def test_umma_tma_staged_c_accumulate(layout):
     assert run(32 | layout, 128, 384, 512, 64, accumulate=1) < 1e-5
     assert run(32 | layout, 128, 200, 260, 40, accumulate=1) < 1e-5
     assert run(32 | layout, 128, 256, 256, 128, accumulate=1) < 1e-5  # 4-stage ring: L2-prefetch path
+
