@@ -2,7 +2,7 @@
 //
 // One CTA runs one-sided (Hestenes) Jacobi on a square l x l matrix W (l <= 128) held
 // column-major in shared memory: W V' = U' S. Rounds of the circle tournament rotate l/2
-// disjoint column pairs in parallel (one warp per pair, lanes over rows, fp64), sweeps repeat
+// disjoint column pairs in parallel (one half-warp per pair, lanes over rows, fp64), sweeps repeat
 // until no pair is rotated. Singular values come out as column norms, sorted descending (stable
 // on ties); columns with zero norm are completed to an orthonormal basis by Gram-Schmidt on unit
 // vectors, so U' is orthonormal even for rank-deficient inputs (zero / rank-1 test matrices,
@@ -39,39 +39,52 @@ __global__ void __launch_bounds__(512) hestenes_svd_kernel(const double* __restr
     if (tid == 0) s_rot = 0;
     __syncthreads();
     for (int round = 0; round < le - 1; ++round) {
-      for (int pr = warp; pr < le / 2; pr += nw) {
+      // half-warp per column pair (16 lanes over the rows): up to 2 * nw pairs per pass, and the
+      // three dot products reduce together (4 interleaved xor-shuffle levels)
+      const int half = lane >> 4, hl = lane & 15;
+      for (int p0 = 2 * warp; p0 < le / 2; p0 += 2 * nw) {
+        const int pr = p0 + half;
+        const bool active = pr < le / 2;
         // circle method: position 0 fixed, others rotate
-        int a = (pr == 0) ? 0 : 1 + (pr - 1 + round) % (le - 1);
-        int b = 1 + (le - 2 - pr + round) % (le - 1);
-        if (a > b) { const int t = a; a = b; b = t; }
+        int a = 0, b = 1;
+        if (active) {
+          a = (pr == 0) ? 0 : 1 + (pr - 1 + round) % (le - 1);
+          b = 1 + (le - 2 - pr + round) % (le - 1);
+          if (a > b) { const int t = a; a = b; b = t; }
+        }
         double* wa = Wc + (size_t)a * l;
         double* wb = Wc + (size_t)b * l;
         double al = 0.0, be = 0.0, ga = 0.0;
-        for (int i = lane; i < l; i += 32) {
-          al = fma(wa[i], wa[i], al);
-          be = fma(wb[i], wb[i], be);
-          ga = fma(wa[i], wb[i], ga);
+        if (active)
+          for (int i = hl; i < l; i += 16) {
+            const double x = wa[i], y = wb[i];
+            al = fma(x, x, al);
+            be = fma(y, y, be);
+            ga = fma(x, y, ga);
+          }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {
+          al += __shfl_xor_sync(0xffffffffu, al, o);
+          be += __shfl_xor_sync(0xffffffffu, be, o);
+          ga += __shfl_xor_sync(0xffffffffu, ga, o);
         }
-        al = warp_sum(al);
-        be = warp_sum(be);
-        ga = warp_sum(ga);
-        if (ga != 0.0 && fabs(ga) > eps * l * sqrt(al * be)) {
+        if (active && ga != 0.0 && fabs(ga) > eps * l * sqrt(al * be)) {
           const double zeta = (be - al) / (2.0 * ga);
           const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
           const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-          for (int i = lane; i < l; i += 32) {
+          for (int i = hl; i < l; i += 16) {
             const double x = wa[i], y = wb[i];
             wa[i] = c * x - s * y;
             wb[i] = s * x + c * y;
           }
           double* va = Vc + (size_t)a * le;
           double* vb = Vc + (size_t)b * le;
-          for (int i = lane; i < le; i += 32) {
+          for (int i = hl; i < le; i += 16) {
             const double x = va[i], y = vb[i];
             va[i] = c * x - s * y;
             vb[i] = s * x + c * y;
           }
-          if (lane == 0) s_rot = 1;
+          if (hl == 0) s_rot = 1;
         }
       }
       __syncthreads();
