@@ -286,7 +286,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
   T* Xs = reinterpret_cast<T*>(smem_raw);
   int* sJ = reinterpret_cast<int*>(Xs + (size_t)RP * n);
   __shared__ double red[32];
-  __shared__ int s_blk;
+  __shared__ int s_blk, s_nxt;
   const int nblk = (int)ceil_div(m_rows, R);
   // ticket == nullptr: one row block per CTA (blockIdx.x). Otherwise a persistent grid smaller
   // than the SM count pulls row blocks from an atomic ticket, leaving the remaining SMs to a
@@ -294,7 +294,13 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
   for (int it = 0;; ++it) {
     int blk;
     if (ticket) {
-      if (threadIdx.x == 0) s_blk = atomicAdd(ticket, 1);
+      // the next block is claimed (and its rows prefetched into L2) during the last column pass
+      // of the current one; the first block, or a block that ended without claiming, takes a
+      // ticket here
+      if (threadIdx.x == 0) {
+        s_blk = (it == 0 || s_nxt < 0) ? atomicAdd(ticket, 1) : s_nxt;
+        s_nxt = -1;
+      }
       __syncthreads();
       blk = s_blk;
     } else {
@@ -385,6 +391,17 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
     const int cw = (int)ceil_div(ceil_div(n, stride * CPT), gridDim.y) * stride * CPT;
     const int c_lo = blockIdx.y * cw, c_hi = min(n, c_lo + cw);
     for (int cb = c_lo + threadIdx.x; cb < c_hi; cb += stride * CPT) {
+      if (FAST && ticket && threadIdx.x == 0 && cb + stride * CPT >= c_hi) {
+        const int nx = atomicAdd(ticket, 1);
+        s_nxt = nx;
+        if (nx < nblk && ((uintptr_t)X & 15) == 0) {  // bulk prefetch: 16-byte granules
+          const int nrows = min(R, m_rows - nx * R);
+          for (int rr = 0; rr < nrows; ++rr)
+            asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(X + (size_t)(nx * R + rr) * n),
+                         "r"((unsigned)(n * sizeof(T)))
+                         : "memory");
+        }
+      }
       unsigned long long acc2[CPT][NP > 0 ? NP : 1];
       T accs[CPT][NS > 0 ? NS : 1];
 #pragma unroll
