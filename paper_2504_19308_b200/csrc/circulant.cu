@@ -155,6 +155,9 @@ __global__ void __launch_bounds__(512) circ_left_kernel(const T* __restrict__ B,
   double2* x = reinterpret_cast<double2*>(smem_raw);
   double2* y = x + n;
   double2* scratch = y + n;
+  int* s_sel = reinterpret_cast<int*>(scratch + (is_pow2(n) ? 0 : n));
+  for (int q = threadIdx.x; q < k; q += blockDim.x) s_sel[q] = sel[q];
+  sel = s_sel;
   const int c = blockIdx.x;
   const double rs = rsqrt((double)n);
   // column c of B: strided, so 8 loads per thread are issued before the first store
@@ -172,17 +175,183 @@ __global__ void __launch_bounds__(512) circ_left_kernel(const T* __restrict__ B,
   __syncthreads();
   fft_block(x, scratch, n, roots, false);
   for (int p = threadIdx.x; p < n; p += blockDim.x) {
-    double2 acc = make_double2(0.0, 0.0);
-    for (int q = 0; q < k; ++q) {
+    double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
+    int q = 0;
+    for (; q + 4 <= k; q += 4) {
+      double2 lv[4], xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int src = p - sel[q + u];
+        if (src < 0) src += n;
+        lv[u] = __ldg(L + (size_t)(q + u) * n + p);
+        xv[u] = x[fsw(src, n)];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u += 2) {
+        acc = cadd(acc, cmul(lv[u], cscale(xv[u], rs)));
+        acc2 = cadd(acc2, cmul(lv[u + 1], cscale(xv[u + 1], rs)));
+      }
+    }
+    for (; q < k; ++q) {
       int src = p - sel[q];
       if (src < 0) src += n;
       acc = cadd(acc, cmul(__ldg(L + (size_t)q * n + p), cscale(x[fsw(src, n)], rs)));
     }
-    y[fsw(p, n)] = acc;
+    y[fsw(p, n)] = cadd(acc, acc2);
   }
   __syncthreads();
   fft_block(y, scratch, n, roots, true);
   for (int p = threadIdx.x; p < n; p += blockDim.x) M[(size_t)p * n + c] = cscale(y[fsw(p, n)], rs);
+}
+
+// ---------------------------------------------------------------------------------------------
+// Two columns (left) / two rows (right) per CTA, n <= kPP * 512: every L_t load of the weighted
+// gather-sum serves both transforms, neighbouring B columns share DRAM sectors, and the two
+// rows' Ahat terms read adjacent S_t entries. The gather-sum results stay in registers (kPP
+// complex per thread per transform) until every thread has read its inputs; the input buffers
+// are then reused for the inverse transforms, so two transforms fit the shared memory of one.
+// ---------------------------------------------------------------------------------------------
+constexpr int kPP = 8;
+
+template <typename T>
+__global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B, int n, const double2* __restrict__ L,
+                                                         const int* __restrict__ sel, int k,
+                                                         const double2* __restrict__ roots, double2* __restrict__ M) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* x0 = reinterpret_cast<double2*>(smem_raw);
+  double2* x1 = x0 + n;
+  double2* scratch = x1 + n;
+  int* s_sel = reinterpret_cast<int*>(scratch + (is_pow2(n) ? 0 : n));
+  for (int q = threadIdx.x; q < k; q += blockDim.x) s_sel[q] = sel[q];
+  const int c0 = 2 * blockIdx.x;
+  const bool two = c0 + 1 < n;
+  const double rs = rsqrt((double)n);
+  for (int p0 = threadIdx.x; p0 < n; p0 += 4 * blockDim.x) {
+    double2 v0[4], v1[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int p = p0 + u * blockDim.x;
+      v0[u] = p < n ? ld_c<T>(B, (size_t)p * n + c0) : make_double2(0.0, 0.0);
+      v1[u] = (p < n && two) ? ld_c<T>(B, (size_t)p * n + c0 + 1) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int p = p0 + u * blockDim.x;
+      if (p < n) {
+        x0[fsw(p, n)] = v0[u];
+        x1[fsw(p, n)] = v1[u];
+      }
+    }
+  }
+  __syncthreads();
+  fft_block(x0, scratch, n, roots, false);
+  fft_block(x1, scratch, n, roots, false);
+  double2 y0[kPP], y1[kPP];
+#pragma unroll
+  for (int i = 0; i < kPP; ++i) {
+    const int p = threadIdx.x + i * blockDim.x;
+    double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+    if (p < n) {
+      for (int q = 0; q < k; ++q) {
+        int src = p - s_sel[q];
+        if (src < 0) src += n;
+        const double2 l = __ldg(L + (size_t)q * n + p);
+        a0 = cadd(a0, cmul(l, cscale(x0[fsw(src, n)], rs)));
+        a1 = cadd(a1, cmul(l, cscale(x1[fsw(src, n)], rs)));
+      }
+    }
+    y0[i] = a0;
+    y1[i] = a1;
+  }
+  __syncthreads();  // every gather read of x0 / x1 is done: reuse them for the inverse transforms
+#pragma unroll
+  for (int i = 0; i < kPP; ++i) {
+    const int p = threadIdx.x + i * blockDim.x;
+    if (p < n) {
+      x0[fsw(p, n)] = y0[i];
+      x1[fsw(p, n)] = y1[i];
+    }
+  }
+  __syncthreads();
+  fft_block(x0, scratch, n, roots, true);
+  fft_block(x1, scratch, n, roots, true);
+  for (int p = threadIdx.x; p < n; p += blockDim.x) {
+    M[(size_t)p * n + c0] = cscale(x0[fsw(p, n)], rs);
+    if (two) M[(size_t)p * n + c0 + 1] = cscale(x1[fsw(p, n)], rs);
+  }
+}
+
+template <typename T>
+__global__ void __launch_bounds__(512) circ_right2_kernel(const T* __restrict__ A, int n,
+                                                          const double2* __restrict__ SselA,
+                                                          const int* __restrict__ selA, int ka,
+                                                          const double2* __restrict__ LB, const int* __restrict__ selB,
+                                                          int kb, const double2* __restrict__ roots,
+                                                          double2* __restrict__ M) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* x0 = reinterpret_cast<double2*>(smem_raw);
+  double2* x1 = x0 + n;
+  double2* scratch = x1 + n;
+  int* sA = reinterpret_cast<int*>(scratch + (is_pow2(n) ? 0 : n));
+  int* sB = sA + ka;
+  for (int q = threadIdx.x; q < ka; q += blockDim.x) sA[q] = selA[q];
+  for (int q = threadIdx.x; q < kb; q += blockDim.x) sB[q] = selB[q];
+  __syncthreads();
+  const int r0 = 2 * blockIdx.x;
+  const bool two = r0 + 1 < n;
+  const double rs = rsqrt((double)n);
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    // Ahat[r][c] = sum_t S_t[(r - c) % n] * w^{t c}: rows r0, r0+1 read S_t[d], S_t[d+1]
+    double2 h0 = make_double2(0.0, 0.0), h1 = make_double2(0.0, 0.0);
+    int d = r0 - c;
+    if (d < 0) d += n;
+    const int d1 = d + 1 == n ? 0 : d + 1;
+    for (int q = 0; q < ka; ++q) {
+      const double2 w = cconj(__ldg(roots + mulmod_n(sA[q], c, n)));  // exp(+2 pi i t c / n)
+      const double2* Sq = SselA + (size_t)q * n;
+      h0 = cadd(h0, cmul(__ldg(Sq + d), w));
+      h1 = cadd(h1, cmul(__ldg(Sq + d1), w));
+    }
+    x0[fsw(c, n)] = cconj(csub(ld_c<T>(A, (size_t)r0 * n + c), h0));
+    x1[fsw(c, n)] = two ? cconj(csub(ld_c<T>(A, (size_t)(r0 + 1) * n + c), h1)) : make_double2(0.0, 0.0);
+  }
+  __syncthreads();
+  fft_block(x0, scratch, n, roots, false);
+  fft_block(x1, scratch, n, roots, false);
+  double2 y0[kPP], y1[kPP];
+#pragma unroll
+  for (int i = 0; i < kPP; ++i) {
+    const int p = threadIdx.x + i * blockDim.x;
+    double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
+    if (p < n) {
+      for (int q = 0; q < kb; ++q) {
+        int src = p + sB[q];
+        if (src >= n) src -= n;
+        const double2 l = __ldg(LB + (size_t)q * n + src);
+        a0 = cadd(a0, cmulc(cscale(x0[fsw(src, n)], rs), l));
+        a1 = cadd(a1, cmulc(cscale(x1[fsw(src, n)], rs), l));
+      }
+    }
+    y0[i] = a0;
+    y1[i] = a1;
+  }
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < kPP; ++i) {
+    const int p = threadIdx.x + i * blockDim.x;
+    if (p < n) {
+      x0[fsw(p, n)] = y0[i];
+      x1[fsw(p, n)] = y1[i];
+    }
+  }
+  __syncthreads();
+  fft_block(x0, scratch, n, roots, true);
+  fft_block(x1, scratch, n, roots, true);
+  for (int c = threadIdx.x; c < n; c += blockDim.x) {
+    double2* pm = M + (size_t)r0 * n + c;
+    *pm = cadd(*pm, cconj(cscale(x0[fsw(c, n)], rs)));
+    if (two) pm[n] = cadd(pm[n], cconj(cscale(x1[fsw(c, n)], rs)));
+  }
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -200,31 +369,69 @@ __global__ void __launch_bounds__(512) circ_right_kernel(const T* __restrict__ A
   double2* x = reinterpret_cast<double2*>(smem_raw);
   double2* y = x + n;
   double2* scratch = y + n;
+  // the selections, staged once: every term's index math needs them (a global load each time
+  // put two dependent loads on every term's critical path)
+  int* sA = reinterpret_cast<int*>(scratch + (is_pow2(n) ? 0 : n));
+  int* sB = sA + ka;
+  for (int q = threadIdx.x; q < ka; q += blockDim.x) sA[q] = selA[q];
+  for (int q = threadIdx.x; q < kb; q += blockDim.x) sB[q] = selB[q];
+  selA = sA;
+  selB = sB;
+  __syncthreads();
   const int r = blockIdx.x;
   const double rs = rsqrt((double)n);
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
     // Ahat[r][c] = sum_t S_t[(r - c) % n] * w^{t c}, ascending t (circulant_materialize order)
-    double2 ah = make_double2(0.0, 0.0);
+    double2 ah = make_double2(0.0, 0.0), ah2 = make_double2(0.0, 0.0);
     int d = r - c;
     if (d < 0) d += n;
-    for (int q = 0; q < ka; ++q) {
-      const int t = selA[q];
-      const double2 w = cconj(__ldg(roots + mulmod_n(t, c, n)));  // exp(+2 pi i t c / n)
-      ah = cadd(ah, cmul(__ldg(SselA + (size_t)q * n + d), w));
+    // four terms' loads in flight at a time, two accumulators (even / odd q)
+    int q = 0;
+    for (; q + 4 <= ka; q += 4) {
+      double2 w[4], sv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        w[u] = __ldg(roots + mulmod_n(selA[q + u], c, n));
+        sv[u] = __ldg(SselA + (size_t)(q + u) * n + d);
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u += 2) {
+        ah = cadd(ah, cmul(sv[u], cconj(w[u])));  // exp(+2 pi i t c / n)
+        ah2 = cadd(ah2, cmul(sv[u + 1], cconj(w[u + 1])));
+      }
     }
+    for (; q < ka; ++q)
+      ah = cadd(ah, cmul(__ldg(SselA + (size_t)q * n + d), cconj(__ldg(roots + mulmod_n(selA[q], c, n)))));
+    ah = cadd(ah, ah2);
     const double2 a = ld_c<T>(A, (size_t)r * n + c);
     x[fsw(c, n)] = cconj(csub(a, ah));
   }
   __syncthreads();
   fft_block(x, scratch, n, roots, false);
   for (int p = threadIdx.x; p < n; p += blockDim.x) {
-    double2 acc = make_double2(0.0, 0.0);
-    for (int q = 0; q < kb; ++q) {
+    double2 acc = make_double2(0.0, 0.0), acc2 = make_double2(0.0, 0.0);
+    int q = 0;
+    for (; q + 4 <= kb; q += 4) {
+      double2 lv[4], xv[4];
+#pragma unroll
+      for (int u = 0; u < 4; ++u) {
+        int src = p + selB[q + u];
+        if (src >= n) src -= n;
+        lv[u] = __ldg(LB + (size_t)(q + u) * n + src);
+        xv[u] = x[fsw(src, n)];
+      }
+#pragma unroll
+      for (int u = 0; u < 4; u += 2) {
+        acc = cadd(acc, cmulc(cscale(xv[u], rs), lv[u]));
+        acc2 = cadd(acc2, cmulc(cscale(xv[u + 1], rs), lv[u + 1]));
+      }
+    }
+    for (; q < kb; ++q) {
       int src = p + selB[q];
       if (src >= n) src -= n;
       acc = cadd(acc, cmulc(cscale(x[fsw(src, n)], rs), __ldg(LB + (size_t)q * n + src)));
     }
-    y[fsw(p, n)] = acc;
+    y[fsw(p, n)] = cadd(acc, acc2);
   }
   __syncthreads();
   fft_block(y, scratch, n, roots, true);
@@ -380,8 +587,14 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
   APX_TRY(launch_kept_energy(p.mag_b, sb, k, (double)n, scal + APX_S_KEPT_B, st));
   APX_TRY(circ_spectra_run(p.S_b, n, sb, k, p.roots, p.Ssel_b, p.L_b, st));
   stage_mark(1, st);
-  const size_t smem = fft_smem_bytes(n, 2);
-  {
+  const size_t smem = fft_smem_bytes(n, 2) + (size_t)2 * k * sizeof(int);  // + staged selections
+  const bool pairs = n >= 2 && n <= kPP * 512;  // two columns / rows per CTA (same smem footprint)
+  if (pairs) {
+    auto fn = circ_left2_kernel<T>;
+    APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    fn<<<(unsigned)ceil_div(n, 2), 512, smem, st>>>(B, n, p.L_a, sa, k, p.roots, M);
+    APX_LAUNCH_CHECK();
+  } else {
     auto fn = circ_left_kernel<T>;
     APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     fn<<<n, 512, smem, st>>>(B, n, p.L_a, sa, k, p.roots, M);
@@ -389,9 +602,15 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
   }
   stage_mark(2, st);
   if (order == 1) {
-    auto fn = circ_right_kernel<T>;
-    APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<n, 512, smem, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M);
+    if (pairs) {
+      auto fn = circ_right2_kernel<T>;
+      APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      fn<<<(unsigned)ceil_div(n, 2), 512, smem, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M);
+    } else {
+      auto fn = circ_right_kernel<T>;
+      APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      fn<<<n, 512, smem, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M);
+    }
     APX_LAUNCH_CHECK();
   }
   stage_mark(3, st);
@@ -426,7 +645,8 @@ int apx_circulant_first_order(int dtype, const void* A, const void* B, int64_t n
                               const int32_t* force_sel_a, const int32_t* force_sel_b, void* M, int32_t* sel_a,
                               int32_t* sel_b, double* scalars, void* wsp, size_t ws_bytes, void* stream) {
   APX_REQUIRE(dtype == F64 || dtype == C128, "circulant product: fp64 or complex128 inputs");
-  APX_REQUIRE(n >= 1 && fft_smem_bytes((int)n, 2) <= 227 * 1024, "n=%lld exceeds the shared-memory transforms",
+  APX_REQUIRE(n >= 1 && fft_smem_bytes((int)n, 2) + (size_t)2 * std::max(k, 0) * sizeof(int) <= 227 * 1024,
+              "n=%lld exceeds the shared-memory transforms",
               (long long)n);
   APX_REQUIRE(k >= 0 && k <= n, "k=%d out of range [0, %lld]", k, (long long)n);
   APX_REQUIRE(order == 0 || order == 1, "order must be 0 or 1");
