@@ -549,7 +549,9 @@ static int set_smem(const void* fn, size_t bytes) {
 static int energy_groups(int n, int* rows_per_chunk) {
   const int cblocks = (int)ceil_div(n, 256);
   int groups = (int)ceil_div(kNumSMs * 8, cblocks);
-  groups = std::max(1, std::min(groups, (int)ceil_div(n, 16)));
+  // at most 40 row groups: the finalize sums one column's groups per thread (n threads), so a
+  // small n with many groups made it the slow part (53 us at n = 2048 with 128 groups)
+  groups = std::max(1, std::min({groups, (int)ceil_div(n, 16), 40}));
   *rows_per_chunk = (int)ceil_div(n, groups);
   return (int)ceil_div(n, *rows_per_chunk);
 }
