@@ -191,13 +191,24 @@ __global__ void __launch_bounds__(256) cycle_left_gather(const T* __restrict__ X
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Xs = reinterpret_cast<T*>(smem_raw);
   constexpr int S = (W == 1) ? 1 : W + 1;  // padded row stride
+  int* sJ = reinterpret_cast<int*>(Xs + (size_t)n * S);
   const int c0 = blockIdx.x * W;
   const int wcols = min(W, n - c0);
-  // load strip
-  for (int e = threadIdx.x; e < n * W; e += blockDim.x) {
-    const int r = e / W, q = e - r * W;
-    Xs[r * S + q] = q < wcols ? __ldg(X + (size_t)r * n + c0 + q) : T(0);
+  // load strip (8 loads per thread in flight) and the shifts
+  for (int e0 = threadIdx.x; e0 < n * W; e0 += 8 * blockDim.x) {
+    T v[8];
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x, r = e / W, q = e - r * W;
+      v[u] = (e < n * W && q < wcols) ? __ldg(X + (size_t)r * n + c0 + q) : T(0);
+    }
+#pragma unroll
+    for (int u = 0; u < 8; ++u) {
+      const int e = e0 + u * blockDim.x, r = e / W, q = e - r * W;
+      if (e < n * W) Xs[r * S + q] = v[u];
+    }
   }
+  for (int t = threadIdx.x; t < k; t += blockDim.x) sJ[t] = J[t];
   __syncthreads();
   const int rows_per_group = (n + gridDim.y - 1) / gridDim.y;
   const int rlo = blockIdx.y * rows_per_group, rhi = min(n, rlo + rows_per_group);
@@ -206,14 +217,23 @@ __global__ void __launch_bounds__(256) cycle_left_gather(const T* __restrict__ X
 #pragma unroll
     for (int q = 0; q < W; ++q) acc[q] = T(0);
     const T* lp = lam + r;
-#pragma unroll 4
-    for (int t = 0; t < k; ++t) {
-      const T l = __ldg(lp + (size_t)t * n);
-      int src = r - __ldg(J + t);
-      if (src < 0) src += n;
-      const T* xs = Xs + src * S;
+    // 8 shifts' lambda loads in flight before their FMAs
+    for (int t0 = 0; t0 < k; t0 += 8) {
+      T l[8];
+      int src[8];
 #pragma unroll
-      for (int q = 0; q < W; ++q) acc[q] = fma(l, xs[q], acc[q]);
+      for (int u = 0; u < 8; ++u) {
+        const int t = t0 + u;
+        l[u] = t < k ? __ldg(lp + (size_t)t * n) : T(0);
+        int sr = r - (t < k ? sJ[t] : 0);
+        src[u] = sr < 0 ? sr + n : sr;
+      }
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        const T* xs = Xs + src[u] * S;
+#pragma unroll
+        for (int q = 0; q < W; ++q) acc[q] = fma(l[u], xs[q], acc[q]);
+      }
     }
     T* mp = M + (size_t)r * n + c0;
     for (int q = 0; q < wcols; ++q) mp[q] = accumulate ? mp[q] + acc[q] : acc[q];
@@ -254,7 +274,12 @@ __device__ __forceinline__ double ldg_nc_ordered(const double* p) {
 
 // Row-interleave pitch of the right gather's shared-memory block: even (8-byte aligned fp32 pairs)
 // except for a single row, which the largest n (32768 fp32, 16384 fp64) can only afford unpadded.
-__host__ __device__ constexpr int gather_pitch(int r) { return r == 1 ? 1 : r + (r & 1); }
+// fp32: even (LDS.64 pairs, pitch 24 B for R = 6 spreads a warp over all banks); fp64: odd, so a
+// warp's 32 consecutive m (8-byte loads at stride 8 * pitch) cover all 16 bank pairs (an even
+// fp64 pitch of 8 put 16 lanes on each bank pair).
+__host__ __device__ constexpr int gather_pitch(int r, size_t elem = 4) {
+  return r == 1 ? 1 : (elem == 8 ? (r | 1) : r + (r & 1));
+}
 
 // shifts per lambda batch (U) and columns per thread (CPT) of the right gather (tuning knobs)
 #ifndef APX_GATHER_U
@@ -280,7 +305,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
                                                           int n, int m_rows, int accumulate, T* __restrict__ M,
                                                           double* __restrict__ msq_partial,
                                                           double* __restrict__ xsq_partial, int* __restrict__ ticket) {
-  constexpr int RP = gather_pitch(R);  // interleave pitch (even, so float pairs stay 8B aligned)
+  constexpr int RP = gather_pitch(R, sizeof(T));  // interleave pitch (see gather_pitch)
   constexpr int CPT = APX_GATHER_CPT, U = APX_GATHER_U;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Xs = reinterpret_cast<T*>(smem_raw);
@@ -624,7 +649,7 @@ constexpr size_t kSmemBudget = 200 * 1024;
 template <typename T, int W>
 static int left_gather_w(const T* X, const T* lam, const int* J, int k, int n, int acc, T* M, cudaStream_t st) {
   constexpr int S = (W == 1) ? 1 : W + 1;
-  const size_t smem = (size_t)n * S * sizeof(T);
+  const size_t smem = (size_t)n * S * sizeof(T) + (size_t)std::max(k, 1) * sizeof(int);
   APX_TRY(set_smem<T>((const void*)cycle_left_gather<T, W>, smem));
   const int strips = (int)ceil_div(n, W);
   int groups = 1;
@@ -679,7 +704,7 @@ static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const
                           int* ticket, int col_chunks, bool trunc, cudaStream_t st) {
   constexpr int U = APX_GATHER_U, CPT = APX_GATHER_CPT;
   const int kp = (int)ceil_div(std::max(k, 1), U) * U;
-  const size_t smem = (size_t)gather_pitch(R) * n * sizeof(T) + (size_t)kp * sizeof(int);
+  const size_t smem = (size_t)gather_pitch(R, sizeof(T)) * n * sizeof(T) + (size_t)kp * sizeof(int);
   int blocks = (int)ceil_div(m_rows, R);
   if (max_ctas > 0 && ticket) {
     APX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
@@ -723,7 +748,7 @@ static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const
 
 int right_gather_rows(int n, size_t elem, int k) {
   int r = 8;  // even row counts keep the fp32 pairs packed
-  while (r > 1 && (size_t)gather_pitch(r) * n * elem + (size_t)(k + 8) * sizeof(int) > kSmemBudget)
+  while (r > 1 && (size_t)gather_pitch(r, elem) * n * elem + (size_t)(k + 8) * sizeof(int) > kSmemBudget)
     r -= (r > 2 ? 2 : 1);
   return r;
 }
