@@ -84,21 +84,27 @@ __global__ void __launch_bounds__(256) cycle_energy_partial(const T* __restrict_
 }
 
 // energies[j] = sum_g partial[g][j] (fixed order, 8 loads in flight); norms[j] = sqrt(energies[j]).
-__global__ void cycle_energy_finalize(const double* __restrict__ partial, int n, int groups,
-                                      double* __restrict__ energies, double* __restrict__ norms) {
-  const int j = blockIdx.x * blockDim.x + threadIdx.x;
-  if (j >= n) return;
-  double s = 0.0;
-  for (int g0 = 0; g0 < groups; g0 += 8) {
-    double v[8];
+// energies[j] = sum_g partial[g][j]; norms[j] = sqrt(energies[j]). A CTA covers 32 columns with
+// 8 slices of the groups (slice s: groups s, s+8, ...), combined in slice order -- a fixed order,
+// and 8x the threads of a column-per-thread pass (which ran on only n/256 SMs, latency-bound).
+__global__ void __launch_bounds__(256) cycle_energy_finalize(const double* __restrict__ partial, int n, int groups,
+                                                             double* __restrict__ energies,
+                                                             double* __restrict__ norms) {
+  __shared__ double part[8][33];
+  const int jx = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  const int j = blockIdx.x * 32 + jx;
+  double acc = 0.0;
+  if (j < n)
+    for (int g = sl; g < groups; g += 8) acc += partial[(size_t)g * n + j];
+  part[sl][jx] = acc;
+  __syncthreads();
+  if (sl == 0 && j < n) {
+    double e = 0.0;
 #pragma unroll
-    for (int u = 0; u < 8; ++u) v[u] = g0 + u < groups ? partial[(size_t)(g0 + u) * n + j] : 0.0;
-#pragma unroll
-    for (int u = 0; u < 8; ++u)
-      if (g0 + u < groups) s += v[u];
+    for (int q = 0; q < 8; ++q) e += part[q][jx];
+    energies[j] = e;
+    norms[j] = sqrt(e);
   }
-  energies[j] = s;
-  norms[j] = sqrt(s);
 }
 
 // Single-block deterministic sum of v[0..n) into *out (fixed order per thread, fixed tree).
@@ -597,7 +603,7 @@ int launch_cycle_energies(const T* A, int n, double* energies, double* norms, do
   // separate finalize: the fused last-CTA reduce (counters != nullptr) measured 63 us vs 44 + 7
   cycle_energy_partial<T><<<grid, 256, 0, st>>>(A, n, rpc, partial, nullptr, energies, norms);
   APX_LAUNCH_CHECK();
-  cycle_energy_finalize<<<cb, 256, 0, st>>>(partial, n, groups, energies, norms);
+  cycle_energy_finalize<<<(unsigned)ceil_div(n, 32), 256, 0, st>>>(partial, n, groups, energies, norms);
   APX_LAUNCH_CHECK();
   if (fro2) {
     sum_vector_kernel<<<1, 1024, 0, st>>>(energies, n, fro2);
