@@ -40,14 +40,20 @@ __global__ void __launch_bounds__(256) cycle_energy_partial(const T* __restrict_
     if (col < 0) col += n;
     const T* rowp = A + (size_t)r0 * n;
     int r = r0;
-    for (; r + 4 <= r1; r += 4) {
-      int c0 = col, c1 = c0 + 1 == n ? 0 : c0 + 1;
-      int c2 = c1 + 1 == n ? 0 : c1 + 1, c3 = c2 + 1 == n ? 0 : c2 + 1;
-      T v0 = __ldg(rowp + c0), v1 = __ldg(rowp + n + c1), v2 = __ldg(rowp + 2 * (size_t)n + c2),
-        v3 = __ldg(rowp + 3 * (size_t)n + c3);
-      acc0 += v0 * v0; acc1 += v1 * v1; acc2 += v2 * v2; acc3 += v3 * v3;
-      col = c3 + 1 == n ? 0 : c3 + 1;
-      rowp += 4 * (size_t)n;
+    // 8 rows per step: 8 independent loads in flight per thread (row r, column (r - j) mod n)
+    for (; r + 8 <= r1; r += 8) {
+      T v[8];
+#pragma unroll
+      for (int u = 0; u < 8; ++u) {
+        int cu = col + u;
+        if (cu >= n) cu -= n;
+        v[u] = __ldg(rowp + (size_t)u * n + cu);
+      }
+      acc0 += v[0] * v[0]; acc1 += v[1] * v[1]; acc2 += v[2] * v[2]; acc3 += v[3] * v[3];
+      acc0 += v[4] * v[4]; acc1 += v[5] * v[5]; acc2 += v[6] * v[6]; acc3 += v[7] * v[7];
+      col += 8;
+      if (col >= n) col -= n;
+      rowp += 8 * (size_t)n;
     }
     for (; r < r1; ++r) {
       T v = __ldg(rowp + col);
