@@ -37,7 +37,7 @@ N_DEFAULT, K_SVD, K_CYC = 8192, 64, 64
 # Stage markers recorded by the C4 plan (capi.cu run_mixed_f32_umma): 0 start | hi stream: 1 B
 # decomposed, 2 gather done | lo stream: 3 Y, 4 QR, 5 Bm, 9 W GEMM, 6 W | main: 7 M += Q.W, 8 end.
 N_MARKS = 10
-SPANS = {  # name -> (start marker, end marker); "join" = the later of markers 2 and 6
+SPANS = {  # name -> (start marker, end marker); "join" = the later of markers 2 and 7
     "B: cycle norms+select+extract [hi]": (0, 1),
     "M = A.Bhat (persistent row gather) [hi]": (1, 2),
     "Y = A.Omega (tcgen05 TF32) [lo]": (0, 3),
@@ -45,8 +45,8 @@ SPANS = {  # name -> (start marker, end marker); "join" = the later of markers 2
     "Bm = Q^T A (+||Bm||^2) [lo]": (4, 5),
     "W0 = Bm.B (tcgen05 TF32) [lo]": (5, 9),
     "W = W0 - Bm.Bhat (TF32-exact gather) [lo]": (9, 6),
-    "M += Q.W (+||M||^2) [after join]": ("join", 7),
-    "reductions": (7, 8),
+    "M += Q.W (+||M||^2; each tile waits for its gather rows) [lo]": (6, 7),
+    "after the join (fixed-order sums)": ("join", 8),
 }
 GATHER_SPAN = "M = A.Bhat (persistent row gather) [hi]"
 
@@ -335,7 +335,7 @@ def run_ours(args, rank, world, local_rank):
     ms_max = max_over_ranks(start.elapsed_time(end), world, dev)
     def span_ms(row, a, b):
         t = [0.0] + [row[0].elapsed_time(row[i]) for i in range(1, nst)]
-        ta = max(t[2], t[6]) if a == "join" else t[a]
+        ta = max(t[2], t[7]) if a == "join" else t[a]
         return t[b] - ta
 
     stage_ms = {name: statistics.mean(span_ms(evs[s], a, b) for s in range(args.steps))

@@ -197,6 +197,13 @@ size_t apx_qr_workspace(int dtype, int64_t m, int64_t k);
 int apx_qr(int dtype, const void* Y, int64_t m, int64_t k, void* Q, void* R, void* ws,
            size_t ws_bytes, void* stream);
 
+/* sketch_norm_estimate (errest.py:139-154): out[0] = ||A (B G)||_F^2 with A m x n, B n x p, G p x k
+ * (all fp64 row-major; G drawn on the host with numpy exactly as the reference draws it). The
+ * caller divides by k. Complex operands are passed as their real embeddings (see errest.py). */
+size_t apx_sketch_norm_workspace(int64_t m, int64_t n, int64_t p, int k);
+int apx_sketch_norm(const double* A, const double* B, int64_t m, int64_t n, int64_t p, const double* G, int k,
+                    double* out, void* ws, size_t ws_bytes, void* stream);
+
 /* Dense product C (+)= op(A) op(B) (matmul_naive core.py:48-61 / svd_reconstruct svd.py:133-135):
  * fp64 DMMA, fp32 3xTF32. trans_a: A stored K x M; trans_b: B stored N x K. */
 size_t apx_gemm_workspace(int dtype, int64_t M, int64_t N, int64_t K, int trans_a, int trans_b);

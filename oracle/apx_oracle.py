@@ -23,7 +23,7 @@ import numpy as np
 __all__ = [
     "as_matrix", "unitary_dft", "cycle_reorder", "cycle_reorder_inverse", "apply_cycle_power",
     "frobenius", "relative_error", "top_indices", "component_count", "apriori_relative_error",
-    "posterior_relative_error", "rsvd", "svd_first_order_multiply", "circulant_decompose",
+    "posterior_relative_error", "sketch_norm_estimate", "rsvd", "svd_first_order_multiply", "circulant_decompose",
     "circulant_materialize", "circulant_left_product", "circulant_right_product",
     "circulant_first_order_multiply", "topk_rows", "fft_sparse_first_order_multiply", "cycle_product_rows",
     "cycle_norms", "cycle_decompose", "cycle_materialize", "cycle_first_order_multiply",
@@ -171,6 +171,19 @@ def apriori_relative_error(normA, normB, ndA, ndB, n, case="mean-zero", c=None) 
 def posterior_relative_error(ndA, ndB, normM, n) -> float:
     """errest.py:127-136."""
     return ndA * ndB / (math.sqrt(n) * normM)
+
+
+def sketch_norm_estimate(A, B, k: int, seed) -> float:
+    """errest.py:139-154 -- ||A (B G)||_F^2 / k, G = default_rng(seed).standard_normal((cols(B), k))."""
+    A = as_matrix(A)
+    B = as_matrix(B)
+    if A.shape[1] != B.shape[0]:
+        raise ValueError("dimension mismatch")
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    G = np.random.default_rng(seed).standard_normal((B.shape[1], k))
+    T = A @ (B @ G)
+    return float(np.sum(np.abs(T) ** 2) / k)
 
 
 class Report(dict):

@@ -19,11 +19,14 @@ import os
 import sys
 import types
 
-from . import circulant, core, fsparse, report, svd
+from . import circulant, core, errest, fsparse, report, svd
 
 # reference module -> ours (the hot path); everything else is loaded from the reference tree
 GPU_MODULES = {"core": core, "svd": svd, "circulant": circulant, "fsparse": fsparse, "report": report}
 REFERENCE_MODULES = ("errest", "genmat", "baseline", "cli")
+# device implementations that replace single functions of a reference-loaded module (bound before
+# the modules after it execute their imports)
+GPU_FUNCTIONS = {"errest": {"sketch_norm_estimate": errest.sketch_norm_estimate}}
 
 
 def install(reference_src: str, name: str = "apxmm") -> types.ModuleType:
@@ -46,6 +49,8 @@ def install(reference_src: str, name: str = "apxmm") -> types.ModuleType:
         mod.__package__ = name
         sys.modules[f"{name}.{sub}"] = mod
         spec.loader.exec_module(mod)
+        for fname, fn in GPU_FUNCTIONS.get(sub, {}).items():
+            setattr(mod, fname, fn)
         setattr(pkg, sub, mod)
     # the package-level names of the reference __init__ (its re-exports), resolved to the above
     init = os.path.join(src, "__init__.py")

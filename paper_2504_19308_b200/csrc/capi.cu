@@ -149,6 +149,7 @@ struct MixedPlan {
   double* asq;
   double* bsq;
   int* ticket;
+  int* ready;  // per gather row block: 1 once its M rows are final (consumed by M += Q.W on lo)
   int n_part_rows;
 };
 
@@ -178,6 +179,7 @@ static void plan_mixed(Workspace& ws, MixedPlan& p, int dtype, int n, int l, int
   p.asq = ws.take<double>(std::max<int>(n, kNumSMs * 4));
   p.bsq = ws.take<double>(std::max<int>(n, kNumSMs * 4));
   p.ticket = ws.take<int>(4);
+  p.ready = ws.take<int>(n);
 }
 
 // fp32 GEMM stages of the mixed product on tcgen05 (umma.cu). Layout bits: 1 = A operand stored
@@ -226,10 +228,11 @@ struct UmmaStages {
   }
   // M[n x n] (+)= Q . W  (Q stored n x l, W stored l x n); optional ||M||^2 partials per CTA
   static int q_times_w(const float* Q, const float* W, float* M, int n, int l, cudaStream_t st, int acc = 0,
-                       double* sq = nullptr) {
+                       double* sq = nullptr, const int* ready = nullptr, int ready_rows = 0) {
     // accumulate: BN 128 / 2 stages, whose drained ring holds the C tile for the staged epilogue
     // (measured faster than a persistent double-buffered variant: 3 CTAs per SM = 12 epilogue warps)
-    return umma_tma_gemm(2, acc ? 128 : 256, Q, l, W, n, M, n, 0, n, n, l, 1, acc, nullptr, 0, 1, st, sq);
+    return umma_tma_gemm(2, acc ? 128 : 256, Q, l, W, n, M, n, 0, n, n, l, 1, acc, nullptr, 0, 1, st, sq, ready,
+                         ready_rows);
   }
   static int q_times_w_ctas(int n, int l, int acc) {
     return (int)(ceil_div(n, acc ? 128 : 256) * ceil_div(n, 128));
@@ -268,7 +271,9 @@ static int get_side(SideStream** out) {
 // Persistent gather grid: all but kMinFreeSMs SMs (the row blocks are pulled from a ticket, so
 // the count need not divide them); APX_GATHER_CTAS overrides, for tuning.
 static int gather_ctas(int nblk) {
-  constexpr int kMinFreeSMs = 18;  // measured at n = 8192 (bench sweep): 130 gather CTAs balance the two streams
+  // measured at n = 8192 (bench sweep): 16 free SMs = 32 slots for the range finder's 64-CTA GEMMs
+  // (exactly two waves); 14 free SMs need a third wave, 18 slow the gather
+  constexpr int kMinFreeSMs = 16;
   static const int env = [] {
     const char* e = getenv("APX_GATHER_CTAS");
     return e ? atoi(e) : 0;
@@ -278,19 +283,22 @@ static int gather_ctas(int nblk) {
 }
 
 // Stage markers (bench.py): 0 start | hi: 1 B decomposed, 2 gather done | lo: 3 Y, 4 QR, 5 Bm,
-// 9 W GEMM, 6 W correction | main: 7 M += Q.W, 8 end.
+// 9 W GEMM, 6 W correction, 7 M += Q.W (order 1; on the main stream after the join for order 0)
+// | main: 8 end.
 static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int kc, int order, int q,
                               const float* Omega, const int* fb, float* M, int* sb, double* scal,
                               const MixedPlan& p, cudaStream_t st) {
   stage_mark(0, st);
   APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
+  const int grows = right_gather_rows(n, sizeof(float), kc);
+  const int rblocks = (int)ceil_div(n, grows);
+  if (order == 1) APX_CUDA(cudaMemsetAsync(p.ready, 0, rblocks * sizeof(int), st));
   SideStream* ss = nullptr;
   APX_TRY(get_side(&ss));
   APX_CUDA(cudaEventRecord(ss->fork, st));
   APX_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
   APX_CUDA(cudaStreamWaitEvent(ss->hi, ss->fork, 0));
   const cudaStream_t hi = ss->hi, lo = ss->s;
-  const int rblocks = (int)ceil_div(n, right_gather_rows(n, sizeof(float), kc));
   const int gctas = gather_ctas(rblocks);
   const int free_sms = std::max(8, kNumSMs - gctas);
   // ---- hi: B's cycle decomposition -> (order 1) the gather M = A . Bhat --------------------------
@@ -311,9 +319,10 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   stage_mark(1, hi);
   if (order == 1) {
     APX_TRY(launch_cycle_right_gather<float>(A, nullptr, 0, lb, sb, kc, n, n, 0, M, nullptr, p.asq, hi, true, gctas,
-                                             p.ticket));
+                                             p.ticket, 1, false, p.ready));
   }
   stage_mark(2, hi);
+  if (order == 1) APX_TRY(launch_sum_vector(p.asq, rblocks, scal + APX_S_FRO2_A, hi));  // ||A||^2 (gather partials)
   APX_CUDA(cudaEventRecord(ss->hi_done, hi));
   // ---- lo: randomized range finder on the SMs the gather leaves free ------------------------------
   float *Y = (float*)p.Y, *Q = (float*)p.Q, *Qt = (float*)p.Qt, *Z = (float*)p.Z, *Bm = (float*)p.Bm,
@@ -349,16 +358,25 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   APX_TRY(launch_cycle_right_gather<float>(Bm, nullptr, 0, lb, sb, kc, n, l, order == 1 ? -1 : 0, W, nullptr, nullptr,
                                            lo, true, 0, nullptr, wchunks, /*tf32_operands=*/order == 1));
   stage_mark(6, lo);
+  // M += Q . W (order 1) with ||M||^2 fused into the epilogue, on lo while the gather is still
+  // running: each tile's operand pipeline and MMA run at once, and its epilogue waits (acquire)
+  // only for the gather row blocks under it, so the HBM-bound read-modify-write of the finished
+  // rows overlaps the shared-memory-bound gather on the SMs it leaves free, and the rest follows
+  // the gather's frontier onto the SMs it releases. The gather's CTAs are all resident before this
+  // launch (it is enqueued on hi well before the range finder ends), so the waits always progress.
+  if (order == 1) {
+    APX_TRY(UmmaStages::q_times_w(Q, W, M, n, l, lo, 1, p.msq, p.ready, grows));
+    stage_mark(7, lo);
+    APX_TRY(launch_sum_vector(p.msq, UmmaStages::q_times_w_ctas(n, l, 1), scal + APX_S_FRO2_M, lo));
+  }
   APX_CUDA(cudaEventRecord(ss->join, lo));
-  // ---- main: M (+)= Q . W with ||M||^2 fused into the epilogue ---------------------------------
+  // ---- main: join; (order 0) M = Q . W; the fixed-order sums ----------------------------------
   APX_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
   APX_CUDA(cudaStreamWaitEvent(st, ss->hi_done, 0));
-  APX_TRY(UmmaStages::q_times_w(Q, W, M, n, l, st, order == 1 ? 1 : 0, p.msq));
-  stage_mark(7, st);
-  APX_TRY(launch_sum_vector(p.msq, UmmaStages::q_times_w_ctas(n, l, order == 1), scal + APX_S_FRO2_M, st));
-  if (order == 1) {
-    APX_TRY(launch_sum_vector(p.asq, rblocks, scal + APX_S_FRO2_A, st));
-  } else {
+  if (order != 1) {
+    APX_TRY(UmmaStages::q_times_w(Q, W, M, n, l, st, 0, p.msq));
+    stage_mark(7, st);
+    APX_TRY(launch_sum_vector(p.msq, UmmaStages::q_times_w_ctas(n, l, 0), scal + APX_S_FRO2_M, st));
     APX_TRY(launch_sumsq<float>(A, (size_t)n * n, p.asq, &parts, st));
     APX_TRY(launch_sum_vector(p.asq, parts, scal + APX_S_FRO2_A, st));
   }

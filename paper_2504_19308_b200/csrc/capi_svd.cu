@@ -212,6 +212,37 @@ int apx_qr(int dtype, const void* Y_, int64_t m, int64_t k, void* Q_, void* R_, 
   return OK;
 }
 
+// ||A (B G)||_F^2 (errest.py:139-154 before its division by k): X = B G (n x k), T = A X
+// (m x k), both fp64 DMMA GEMMs, then a fixed-order sum of squares. O(k n^2) instead of O(n^3).
+size_t apx_sketch_norm_workspace(int64_t m, int64_t n, int64_t p, int k) {
+  Workspace ws(nullptr, 0, true);
+  ws.take<double>((size_t)n * k);
+  ws.take<double>((size_t)m * k);
+  ws.take<double>((size_t)8 * std::max(m, n) * k);
+  ws.take<double>(4096);
+  return ws.off;
+}
+
+int apx_sketch_norm(const double* A, const double* B, int64_t m, int64_t n, int64_t p, const double* G, int k,
+                    double* out, void* wsp, size_t ws_bytes, void* stream) {
+  APX_REQUIRE(m >= 1 && n >= 1 && p >= 1, "sketch_norm: empty operand");
+  APX_REQUIRE(k >= 1, "k must be >= 1");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace ws(wsp, ws_bytes);
+  double* X = ws.take<double>((size_t)n * k);
+  double* T = ws.take<double>((size_t)m * k);
+  double* part = ws.take<double>((size_t)8 * std::max(m, n) * k);
+  double* red = ws.take<double>(4096);
+  APX_WS_CHECK(ws);
+  Dgemm g{part, (size_t)8 * std::max(m, n) * k};
+  APX_TRY(g(B, p, G, k, X, k, (int)n, k, (int)p, 0, st));
+  APX_TRY(g(A, n, X, k, T, k, (int)m, k, (int)n, 0, st));
+  int parts = 0;
+  APX_TRY(launch_sumsq<double>(T, (size_t)m * k, red, &parts, st));
+  APX_REQUIRE(parts <= 4096, "sketch_norm: reduction workspace");
+  return launch_sum_vector(red, parts, out, st);
+}
+
 size_t apx_gemm_workspace(int dtype, int64_t M, int64_t N, int64_t K, int trans_a, int trans_b) {
   const size_t e = dtype == F32 ? 4 : 8;
   Workspace ws(nullptr, 0, true);

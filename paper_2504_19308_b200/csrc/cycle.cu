@@ -316,7 +316,8 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
                                                           const T* __restrict__ lam, const int* __restrict__ J, int k,
                                                           int n, int m_rows, int accumulate, T* __restrict__ M,
                                                           double* __restrict__ msq_partial,
-                                                          double* __restrict__ xsq_partial, int* __restrict__ ticket) {
+                                                          double* __restrict__ xsq_partial, int* __restrict__ ticket,
+                                                          int* __restrict__ ready) {
   constexpr int RP = gather_pitch(R, sizeof(T));  // interleave pitch (see gather_pitch)
   constexpr int CPT = APX_GATHER_CPT, U = APX_GATHER_U;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -554,8 +555,13 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
         }
       }
     }
-    double s = block_sum(msq, red);
+    double s = block_sum(msq, red);  // (its barriers also order every thread's M stores before the flag)
     if (threadIdx.x == 0 && msq_partial) msq_partial[blk] = s;
+    if (threadIdx.x == 0 && ready) {
+      // publish the finished row block to a concurrent consumer (the mixed product's M += Q.W)
+      __threadfence();
+      atomicExch(ready + blk, 1);
+    }
     __syncthreads();  // Xs / sJ / red are refilled by the next row block
   }
 }
@@ -713,7 +719,7 @@ int launch_cycle_left_gather(const T* X, const T* lam, const int* J, int k, int 
 template <typename T, int R>
 static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int m_rows,
                           int acc, T* M, double* msq_partial, double* xsq_partial, bool lam_padded, int max_ctas,
-                          int* ticket, int col_chunks, bool trunc, cudaStream_t st) {
+                          int* ticket, int col_chunks, bool trunc, int* ready, cudaStream_t st) {
   constexpr int U = APX_GATHER_U, CPT = APX_GATHER_CPT;
   const int kp = (int)ceil_div(std::max(k, 1), U) * U;
   const size_t smem = (size_t)gather_pitch(R, sizeof(T)) * n * sizeof(T) + (size_t)kp * sizeof(int);
@@ -730,29 +736,30 @@ static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const
   int chunks = 1;
   if (fast && !ticket && col_chunks > 1 && msq_partial == nullptr && xsq_partial == nullptr)
     chunks = std::min(col_chunks, n / (threads * CPT));
+  APX_REQUIRE(ready == nullptr || chunks == 1, "right gather: ready flags need whole-row blocks");
   const dim3 grid((unsigned)blocks, (unsigned)chunks);
   if (fast) {
     if (trunc && sizeof(T) == 4) {
       APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R, true, true>, smem));
       cycle_right_gather<T, R, true, true><<<grid, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
-                                                                        msq_partial, xsq_partial, ticket);
+                                                                        msq_partial, xsq_partial, ticket, ready);
       APX_LAUNCH_CHECK();
       return OK;
     }
     APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R, true>, smem));
     cycle_right_gather<T, R, true><<<grid, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
-                                                                  msq_partial, xsq_partial, ticket);
+                                                                  msq_partial, xsq_partial, ticket, ready);
   } else {
     if (trunc && sizeof(T) == 4) {
       APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R, false, true>, smem));
       cycle_right_gather<T, R, false, true><<<blocks, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
-                                                                         msq_partial, xsq_partial, ticket);
+                                                                         msq_partial, xsq_partial, ticket, ready);
       APX_LAUNCH_CHECK();
       return OK;
     }
     APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R, false>, smem));
     cycle_right_gather<T, R, false><<<blocks, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
-                                                                   msq_partial, xsq_partial, ticket);
+                                                                   msq_partial, xsq_partial, ticket, ready);
   }
   APX_LAUNCH_CHECK();
   return OK;
@@ -773,13 +780,13 @@ template <typename T>
 int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n,
                               int m_rows, int accumulate, T* M, double* msq_partial, double* xsq_partial,
                               cudaStream_t st, bool lam_padded, int max_ctas, int* ticket, int col_chunks,
-                              bool tf32_operands) {
+                              bool tf32_operands, int* ready) {
   const int r = right_gather_rows(n, sizeof(T), k);
   APX_REQUIRE((size_t)n * sizeof(T) + (size_t)(k + 8) * sizeof(int) <= 227 * 1024,
               "n=%d too large for the right gather row block", n);
 #define APX_RG(RV) \
   return right_gather_r<T, RV>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, lam_padded, \
-                               max_ctas, ticket, col_chunks, tf32_operands, st)
+                               max_ctas, ticket, col_chunks, tf32_operands, ready, st)
   switch (r) {
     case 1: APX_RG(1);
     case 2: APX_RG(2);
@@ -814,7 +821,7 @@ int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st) {
   template int launch_cycle_materialize<T>(const T*, const int*, int, int, T*, cudaStream_t);                 \
   template int launch_cycle_left_gather<T>(const T*, const T*, const int*, int, int, int, T*, cudaStream_t);  \
   template int launch_cycle_right_gather<T>(const T*, const int*, int, const T*, const int*, int, int, int, int, T*, \
-                                            double*, double*, cudaStream_t, bool, int, int*, int, bool);     \
+                                            double*, double*, cudaStream_t, bool, int, int*, int, bool, int*); \
   template int launch_sumsq<T>(const T*, size_t, double*, int*, cudaStream_t);
 APX_INST(float)
 APX_INST(double)

@@ -27,7 +27,7 @@ template <typename T>
 int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int m_rows,
                               int accumulate, T* M, double* msq_partial, double* xsq_partial, cudaStream_t st,
                               bool lam_padded = false, int max_ctas = 0, int* ticket = nullptr, int col_chunks = 1,
-                              bool tf32_operands = false);
+                              bool tf32_operands = false, int* ready = nullptr);
 template <typename T>
 int launch_sumsq(const T* x, size_t cnt, double* partial, int* nparts, cudaStream_t st);
 int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st);
@@ -53,7 +53,8 @@ namespace apx {
 int umma_set_variant(int v);
 int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                   int64_t ldc, int64_t c_split_stride, int M, int N, int K, int splits, int accumulate,
-                  const int* mJ, int mk, int mod_n, cudaStream_t st, double* sq_partial = nullptr);
+                  const int* mJ, int mk, int mod_n, cudaStream_t st, double* sq_partial = nullptr,
+                  const int* ready = nullptr, int ready_rows = 0);
 int umma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
               int64_t c_split_stride, int M, int N, int K, int splits, int accumulate, const int* mJ, int mk,
               int mod_n, cudaStream_t st);

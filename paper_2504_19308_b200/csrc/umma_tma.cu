@@ -44,6 +44,11 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
       "r"(phase)
       : "memory");
 }
+__device__ __forceinline__ int ld_relaxed_gpu(const int* p) {
+  int v;
+  asm volatile("ld.relaxed.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
 __device__ __forceinline__ void tma_load_2d(uint32_t dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
   asm volatile(
       "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::
@@ -107,7 +112,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     float* __restrict__ C, int64_t ldc, int64_t c_split_stride, int M, int N, int K,
                     int k_per_split, int accumulate, const int* __restrict__ mJ, int mk, int mod_n,
-                    double* __restrict__ sq_partial, int c_async) {
+                    double* __restrict__ sq_partial, int c_async, const int* __restrict__ ready, int ready_rows) {
   using CF = Cfg<BN, STAGES>;
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte alignment for the swizzled tiles
@@ -244,6 +249,22 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_wait(done, 0);
     fence_after();
+    if (ready != nullptr && accumulate) {
+      // C rows are produced by a concurrent kernel (the persistent gather) that publishes one flag
+      // per block of ready_rows rows: wait (acquire) for the blocks under this tile before reading
+      // C. The operand pipeline above has already run, so only the read-modify-write waits.
+      // The first epilogue warp polls one flag per lane (relaxed loads, all in flight at once),
+      // then one fence turns the observed flags into an acquire for the whole CTA.
+      if (warp == 2) {
+        const int b0 = m0 / ready_rows, b1 = (min(M, m0 + BM) - 1) / ready_rows;
+        for (int bb = b0; bb <= b1; bb += 32) {
+          const int b = bb + lane;
+          while (!__all_sync(0xffffffffu, b > b1 || ld_relaxed_gpu(ready + b) != 0)) __nanosleep(128);
+        }
+        __threadfence();
+      }
+      asm volatile("bar.sync 2, 128;" ::: "memory");  // the four epilogue warps only
+    }
     const int quarter = warp & 3;
     const int row = m0 + quarter * 32 + lane;
     float* Cz = C + (size_t)kz * c_split_stride;
@@ -424,7 +445,7 @@ static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t c
 template <int BN, int STAGES, bool A_MN, bool B_MN, bool TRANS_OUT, bool MASK>
 static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                   int64_t c_split_stride, int M, int N, int K, int splits, int accumulate, const int* mJ, int mk,
-                  int mod_n, double* sq_partial, cudaStream_t st) {
+                  int mod_n, double* sq_partial, const int* ready, int ready_rows, cudaStream_t st) {
   using CF = Cfg<BN, STAGES>;
   CUtensorMap ta, tb;
   // A operand: K-major stored [M][K]; MN-major stored [K][M]
@@ -436,7 +457,7 @@ static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, floa
   APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem));
   const int c_async = ((uintptr_t)C % 16) == 0 && (ldc % 4) == 0 && (N % 4) == 0 && (c_split_stride % 4) == 0;
   fn<<<grid, kThreads, CF::kSmem, st>>>(ta, tb, C, ldc, c_split_stride, M, N, K, kps, accumulate, mJ, mk, mod_n,
-                                        sq_partial, c_async);
+                                        sq_partial, c_async, ready, ready_rows);
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -449,7 +470,10 @@ static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, floa
 // (z * grid.y + y) * grid.x + x -- ||C||_F^2 partials for a split-free launch.
 int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                   int64_t ldc, int64_t c_split_stride, int M, int N, int K, int splits, int accumulate,
-                  const int* mJ, int mk, int mod_n, cudaStream_t st, double* sq_partial) {
+                  const int* mJ, int mk, int mod_n, cudaStream_t st, double* sq_partial, const int* ready,
+                  int ready_rows) {
+  APX_REQUIRE(ready == nullptr || (accumulate && ready_rows > 0 && splits == 1 && !(layout & 4)),
+              "umma_tma_gemm: ready flags need an accumulating, split-free, row-major C");
   APX_REQUIRE(mk <= 128, "umma_tma_gemm: at most 128 masked shifts");
   APX_REQUIRE(((uintptr_t)A % 16) == 0 && ((uintptr_t)B % 16) == 0 && (lda % 4) == 0 && (ldb % 4) == 0,
               "umma_tma_gemm: 16-byte aligned operands required");
@@ -461,7 +485,7 @@ int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* 
     return tma::launch<BNV, ST, (L & 1) != 0, (L & 2) != 0, (L & 4) != 0, MK>(A, lda, B, ldb, C, ldc,          \
                                                                               c_split_stride, M, N, K, splits, \
                                                                               accumulate, mJ, mk, mod_n,       \
-                                                                              sq_partial, st);
+                                                                              sq_partial, ready, ready_rows, st);
   APX_TL(64, 4, 0, false) APX_TL(64, 4, 1, false) APX_TL(64, 4, 2, false) APX_TL(64, 4, 3, false)
   APX_TL(64, 4, 4, false) APX_TL(64, 4, 5, false) APX_TL(64, 4, 6, false) APX_TL(64, 4, 7, false)
   APX_TL(64, 4, 1, true) APX_TL(64, 4, 5, true)

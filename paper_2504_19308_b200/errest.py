@@ -1,6 +1,8 @@
-"""Host-side scalar error estimates that end every multiply (reference errest.py:35-136).
+"""Error estimates (reference errest.py:35-154).
 
-These are O(1) host arithmetic on norms the device already reduced; they stay in Python.
+The a-priori / posterior formulas are O(1) host arithmetic on norms the device already reduced;
+they stay in Python. ``sketch_norm_estimate`` runs its two thin GEMMs and the reduction on the
+device through the C-ABI (apx_sketch_norm).
 """
 
 from __future__ import annotations
@@ -72,3 +74,41 @@ def finish_report(method: str, order: int, k: int, normA: float, normB: float, n
     posterior = posterior_relative_error(norm_da, norm_db, norm_m, n) if norm_m > 0 else None
     return ApproxReport(method=method, order=order, k=k, norm_da=norm_da, norm_db=norm_db,
                         apriori_estimate=apriori, posterior_estimate=posterior, wall_time=wall)
+
+
+def sketch_norm_estimate(A, B, k: int, seed) -> float:
+    """errest.py:139-154 -- ||A (B G)||_F^2 / k with G ~ N(0,1) of shape (cols(B), k) drawn by
+    ``np.random.default_rng(seed)`` exactly as the reference draws it; the two fp64 GEMMs and the
+    sum of squares run on the device (apx_sketch_norm). Complex operands go through their real
+    embeddings A' = [[Ar, -Ai], [Ai, Ar]], B' = [[Br], [Bi]], for which ||A'(B'G)|| = ||A(BG)||."""
+    import numpy as np
+    import torch
+
+    from . import _device as D
+    from . import _native as N
+    from .core import as_matrix
+
+    A = as_matrix(A)
+    B = as_matrix(B)
+    if A.shape[1] != B.shape[0]:
+        raise ValueError(f"dimension mismatch: {A.shape} x {B.shape}")
+    if k < 1:
+        raise ValueError("k must be >= 1")
+    rng = np.random.default_rng(seed)
+    G = rng.standard_normal((B.shape[1], k))
+    if np.iscomplexobj(A) or np.iscomplexobj(B):
+        Ar, Ai = A.real, (A.imag if np.iscomplexobj(A) else np.zeros_like(A.real))
+        Br, Bi = B.real, (B.imag if np.iscomplexobj(B) else np.zeros_like(B.real))
+        A = np.block([[Ar, -Ai], [Ai, Ar]])
+        B = np.concatenate([Br, Bi], axis=0)
+    m, n = A.shape
+    p = B.shape[1]
+    dev = D.require_cuda()
+    Ad = torch.from_numpy(np.ascontiguousarray(A, dtype=np.float64)).to(dev)
+    Bd = torch.from_numpy(np.ascontiguousarray(B, dtype=np.float64)).to(dev)
+    Gd = torch.from_numpy(np.ascontiguousarray(G)).to(dev)
+    out = torch.zeros(1, dtype=torch.float64, device=dev)
+    ws = D.workspace(N.size("apx_sketch_norm_workspace", m, n, p, k))
+    N.call("apx_sketch_norm", Ad.data_ptr(), Bd.data_ptr(), m, n, p, Gd.data_ptr(), k, out.data_ptr(),
+           ws.data_ptr(), ws.numel(), D.stream_ptr())
+    return float(out.item() / k)

@@ -207,12 +207,33 @@ def cycle_cases():
     np.savez_compressed(os.path.join(OUT, "cycle.npz"), **d)
 
 
+def errest_cases():
+    from apxmm import errest as re_
+    d = {}
+    rng = np.random.default_rng(300)
+    cases = [
+        ("sq", rng.standard_normal((32, 32)), rng.standard_normal((32, 32)), 4, 7),
+        ("rect", rng.standard_normal((17, 40)), rng.standard_normal((40, 23)), 5, 11),
+        ("cplx", rng.standard_normal((12, 9)) + 1j * rng.standard_normal((12, 9)),
+         rng.standard_normal((9, 14)) - 0.5j * rng.standard_normal((9, 14)), 3, 2),
+        ("half", rng.standard_normal((10, 10)), rng.standard_normal((10, 10)) + 1j * rng.standard_normal((10, 10)),
+         6, 5),
+        ("zero", np.zeros((4, 4)), np.eye(4), 3, 0),
+        ("wide", rng.standard_normal((3, 300)), rng.standard_normal((300, 2)), 64, 99),
+    ]
+    for name, A, B, k, seed in cases:
+        d[f"sk_{name}_A"], d[f"sk_{name}_B"] = A, B
+        d[f"sk_{name}_par"] = np.array([k, seed])
+        d[f"sk_{name}_out"] = np.array(re_.sketch_norm_estimate(A, B, k, seed))
+    d["sk_names"] = np.array([c[0] for c in cases])
+    np.savez_compressed(os.path.join(OUT, "errest.npz"), **d)
+
+
 if __name__ == "__main__":
-    core_cases()
-    circulant_cases()
-    svd_cases()
-    fsparse_cases()
-    cycle_cases()
+    only = sys.argv[1:]
+    for fn in (core_cases, circulant_cases, svd_cases, fsparse_cases, cycle_cases, errest_cases):
+        if not only or fn.__name__ in only:
+            fn()
     for f in sorted(os.listdir(OUT)):
         if f.endswith(".npz"):
             print(f, os.path.getsize(os.path.join(OUT, f)))

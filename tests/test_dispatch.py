@@ -32,6 +32,7 @@ def test_apxmm_shim_binds_the_gpu_path():
         assert apxmm.cli.matmul_naive is P.matmul_naive
         assert apxmm.ApproxReport is P.ApproxReport
         assert apxmm.svd_first_order_multiply is P.svd_first_order_multiply
+        assert apxmm.sketch_norm_estimate is P.sketch_norm_estimate
         # out-of-scope modules stay the reference's (CPU): the lowrank baseline still runs
         rng = np.random.default_rng(0)
         A, B = rng.standard_normal((8, 8)), rng.standard_normal((8, 8))
@@ -72,3 +73,12 @@ def test_dispatch_matches_oracle(method):
     assert rel(np.asarray(M), Mo) < 1e-10
     assert rep.method == {"naive": "naive", "svd": "svd", "cd": "cd", "sfft": "sfft", "cycle": "cycle",
                           "mixed": "mixed"}[method]
+
+
+def test_sketch_validation_before_device():
+    """errest.py:147-150: shape and k errors are raised before any device work."""
+    from paper_2504_19308_b200 import sketch_norm_estimate
+    with pytest.raises(ValueError):
+        sketch_norm_estimate(np.eye(3), np.eye(4), 2, 0)
+    with pytest.raises(ValueError):
+        sketch_norm_estimate(np.eye(3), np.eye(3), 0, 0)

@@ -163,3 +163,12 @@ def test_generators_deterministic():
     assert np.array_equal(a, O.gen_cycle_operand(32, 4, 3))
     c = O.gen_circulant_operand(32, 3, 1)
     assert np.isrealobj(c) and np.array_equal(c, O.gen_circulant_operand(32, 3, 1))
+
+
+def test_sketch_norm_golden(golden):
+    g = golden("errest")
+    for name in g["sk_names"]:
+        k, seed = (int(v) for v in g[f"sk_{name}_par"])
+        got = O.sketch_norm_estimate(g[f"sk_{name}_A"], g[f"sk_{name}_B"], k, seed)
+        ref = float(g[f"sk_{name}_out"])
+        assert abs(got - ref) <= 1e-12 * max(1.0, abs(ref)), name
