@@ -292,7 +292,10 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
   const int grows = right_gather_rows(n, sizeof(float), kc);
   const int rblocks = (int)ceil_div(n, grows);
-  if (order == 1) APX_CUDA(cudaMemsetAsync(p.ready, 0, rblocks * sizeof(int), st));
+  if (order == 1) {
+    APX_CUDA(cudaMemsetAsync(p.ready, 0, rblocks * sizeof(int), st));
+    APX_CUDA(cudaMemsetAsync(p.ticket, 0, sizeof(int), st));  // the gather's (x_early launch)
+  }
   SideStream* ss = nullptr;
   APX_TRY(get_side(&ss));
   APX_CUDA(cudaEventRecord(ss->fork, st));
@@ -319,7 +322,7 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   stage_mark(1, hi);
   if (order == 1) {
     APX_TRY(launch_cycle_right_gather<float>(A, nullptr, 0, lb, sb, kc, n, n, 0, M, nullptr, p.asq, hi, true, gctas,
-                                             p.ticket, 1, false, p.ready));
+                                             p.ticket, 1, false, p.ready, /*x_early=*/true));
   }
   stage_mark(2, hi);
   if (order == 1) APX_TRY(launch_sum_vector(p.asq, rblocks, scal + APX_S_FRO2_A, hi));  // ||A||^2 (gather partials)
@@ -330,7 +333,8 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   // Y starts when B's energy pass (the HBM-bound, critical part of B's decomposition) is done and
   // overlaps the latency-bound select/extract and the gather's start; the rest of the range
   // finder then fits on the SMs the persistent gather leaves free
-  APX_CUDA(cudaStreamWaitEvent(lo, ss->b_read, 0));
+  static const int y_wait = getenv("APX_Y_WAIT") ? atoi(getenv("APX_Y_WAIT")) : 0;
+  APX_CUDA(cudaStreamWaitEvent(lo, y_wait ? ss->b_ready : ss->b_read, 0));
   APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, lo, 32));  // 64 CTAs
   stage_mark(3, lo);
   APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, lo)));
@@ -355,6 +359,7 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   const int wchunks = std::max(1, std::min(8, (int)ceil_div(5 * free_sms, wblocks)));
   if (order == 1) APX_TRY(UmmaStages::bm_times_db(B, Bm, W, part, n, l, nullptr, 0, lo, free_sms));
   stage_mark(9, lo);
+  APX_CUDA(cudaStreamWaitEvent(lo, ss->b_ready, 0));  // B's selection and lambda' (long done by now)
   APX_TRY(launch_cycle_right_gather<float>(Bm, nullptr, 0, lb, sb, kc, n, l, order == 1 ? -1 : 0, W, nullptr, nullptr,
                                            lo, true, 0, nullptr, wchunks, /*tf32_operands=*/order == 1));
   stage_mark(6, lo);

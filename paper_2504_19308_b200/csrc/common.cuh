@@ -2,6 +2,8 @@
 #pragma once
 #include <cuda_runtime.h>
 #include <cstdint>
+#include <cstdlib>
+#include <utility>
 #include <cstdio>
 #include <cstring>
 #include <string>
@@ -48,6 +50,38 @@ void stage_mark(int i, cudaStream_t st);
       return ::apx::E_CUDA;                                                             \
     }                                                                                   \
   } while (0)
+
+// Programmatic dependent launch: a kernel launched with launch_pdl may start while the previous
+// kernel of its stream is still running; it must call pdl_wait() before touching anything that
+// kernel writes (griddepcontrol.wait returns once the previous grid has completed and its memory
+// is visible; it is a no-op for a normal launch). pdl_trigger() in the previous kernel lets the
+// dependent grid launch early. APX_NO_PDL=1 falls back to ordinary launches (A/B measurements).
+__device__ __forceinline__ void pdl_wait() { asm volatile("griddepcontrol.wait;" ::: "memory"); }
+__device__ __forceinline__ void pdl_trigger() { asm volatile("griddepcontrol.launch_dependents;" ::: "memory"); }
+
+inline bool pdl_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("APX_NO_PDL");
+    return !(e && atoi(e) != 0);
+  }();
+  return on;
+}
+
+template <typename... KArgs, typename... Args>
+inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t st,
+                              Args&&... args) {
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = st;
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
+}
 
 #define APX_REQUIRE(cond, ...)          \
   do {                                  \

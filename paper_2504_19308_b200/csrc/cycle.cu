@@ -23,12 +23,13 @@ namespace apx {
 // each column block to finish also reduces that block's partials in fixed group order
 // (energies, norms) -- the finalize pass without its own launch.
 template <typename T>
-__global__ void __launch_bounds__(256) cycle_energy_partial(const T* __restrict__ A, int n, int rows_per_chunk,
+__global__ void __launch_bounds__(256, 8) cycle_energy_partial(const T* __restrict__ A, int n, int rows_per_chunk,
                                                             double* __restrict__ partial,
                                                             unsigned* __restrict__ counters,
                                                             double* __restrict__ energies,
                                                             double* __restrict__ norms) {
   using Acc = T;
+  pdl_trigger();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int g = blockIdx.y;
   const int r0 = g * rows_per_chunk;
@@ -97,6 +98,8 @@ __global__ void __launch_bounds__(256) cycle_energy_finalize(const double* __res
                                                              double* __restrict__ energies,
                                                              double* __restrict__ norms) {
   __shared__ double part[8][33];
+  pdl_trigger();
+  pdl_wait();
   const int jx = threadIdx.x & 31, sl = threadIdx.x >> 5;
   const int j = blockIdx.x * 32 + jx;
   double acc = 0.0;
@@ -126,6 +129,8 @@ __global__ void __launch_bounds__(kSelThreads) topk_select_kernel(const double* 
                                                                   int* __restrict__ sel, const double* kept_w,
                                                                   double kept_scale, double* kept,
                                                                   const double* tot_w, double* total) {
+  pdl_trigger();
+  pdl_wait();
   topk_select_block(w, n, k, sel, kept_w, kept_scale, kept, tot_w, total);
 }
 
@@ -150,6 +155,8 @@ constexpr int kExtractT = 8;
 template <typename T, bool ALIGNED>
 __global__ void cycle_extract(const T* __restrict__ A, int n, const int* __restrict__ J, int k,
                               T* __restrict__ lam) {
+  pdl_trigger();
+  pdl_wait();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int t0 = blockIdx.y * kExtractT;
   if (i >= n) return;
@@ -317,8 +324,12 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
                                                           int n, int m_rows, int accumulate, T* __restrict__ M,
                                                           double* __restrict__ msq_partial,
                                                           double* __restrict__ xsq_partial, int* __restrict__ ticket,
-                                                          int* __restrict__ ready) {
-  constexpr int RP = gather_pitch(R, sizeof(T));  // interleave pitch (see gather_pitch)
+                                                          int* __restrict__ ready, int x_early) {
+  constexpr int RP = gather_pitch(R, sizeof(T));
+  // x_early: X (and the ticket / ready flags) predate the previous kernel of the stream, so under
+  // a programmatic dependent launch the first row block is staged before waiting for that
+  // kernel (the cycle selection / lambda extraction this gather consumes)
+  if (!x_early) pdl_wait();  // interleave pitch (see gather_pitch)
   constexpr int CPT = APX_GATHER_CPT, U = APX_GATHER_U;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Xs = reinterpret_cast<T*>(smem_raw);
@@ -402,6 +413,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
         }
       }
     }
+    if (x_early && it == 0) pdl_wait();
     // shifts, padded with zeros to a multiple of U (FAST: the lambda rows are zero-padded too)
     const int kp = FAST ? (int)ceil_div(k, U) * U : k;
     for (int t = threadIdx.x; t < kp; t += blockDim.x) sJ[t] = t < k ? J[t] : 0;
@@ -591,7 +603,8 @@ static int set_smem(const void* fn, size_t bytes) {
 
 static int energy_groups(int n, int* rows_per_chunk) {
   const int cblocks = (int)ceil_div(n, 256);
-  int groups = (int)ceil_div(kNumSMs * 8, cblocks);
+  // one full wave of 8 CTAs per SM (launch bounds (256, 8)): rounding up left a 0.33-wave tail
+  int groups = std::max(1, (kNumSMs * 8) / cblocks);
   // at most 40 row groups: the finalize sums one column's groups per thread (n threads), so a
   // small n with many groups made it the slow part (53 us at n = 2048 with 128 groups)
   groups = std::max(1, std::min({groups, (int)ceil_div(n, 16), 40}));
@@ -615,7 +628,8 @@ int launch_cycle_energies(const T* A, int n, double* energies, double* norms, do
   // separate finalize: the fused last-CTA reduce (counters != nullptr) measured 63 us vs 44 + 7
   cycle_energy_partial<T><<<grid, 256, 0, st>>>(A, n, rpc, partial, nullptr, energies, norms);
   APX_LAUNCH_CHECK();
-  cycle_energy_finalize<<<(unsigned)ceil_div(n, 32), 256, 0, st>>>(partial, n, groups, energies, norms);
+  APX_CUDA(launch_pdl(cycle_energy_finalize, dim3((unsigned)ceil_div(n, 32)), dim3(256), 0, st, partial, n, groups,
+                      energies, norms));
   APX_LAUNCH_CHECK();
   if (fro2) {
     sum_vector_kernel<<<1, 1024, 0, st>>>(energies, n, fro2);
@@ -627,7 +641,8 @@ int launch_cycle_energies(const T* A, int n, double* energies, double* norms, do
 int launch_topk(const double* w, int n, int k, int* sel, cudaStream_t st, const double* kept_w, double kept_scale,
                 double* kept, const double* tot_w, double* total) {
   if (k <= 0 && !kept && !total) return OK;
-  topk_select_kernel<<<1, kSelThreads, 0, st>>>(w, n, k, sel, kept_w, kept_scale, kept, tot_w, total);
+  APX_CUDA(launch_pdl(topk_select_kernel, dim3(1), dim3(kSelThreads), 0, st, w, n, k, sel, kept_w, kept_scale, kept,
+                      tot_w, total));
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -643,9 +658,9 @@ int launch_cycle_extract(const T* A, int n, const int* J, int k, T* lam, cudaStr
   if (k <= 0) return OK;
   dim3 grid((unsigned)ceil_div(n, 256), (unsigned)ceil_div(k, kExtractT));
   if (aligned)
-    cycle_extract<T, true><<<grid, 256, 0, st>>>(A, n, J, k, lam);
+    APX_CUDA(launch_pdl(cycle_extract<T, true>, grid, dim3(256), 0, st, A, n, J, k, lam));
   else
-    cycle_extract<T, false><<<grid, 256, 0, st>>>(A, n, J, k, lam);
+    APX_CUDA(launch_pdl(cycle_extract<T, false>, grid, dim3(256), 0, st, A, n, J, k, lam));
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -719,13 +734,15 @@ int launch_cycle_left_gather(const T* X, const T* lam, const int* J, int k, int 
 template <typename T, int R>
 static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int m_rows,
                           int acc, T* M, double* msq_partial, double* xsq_partial, bool lam_padded, int max_ctas,
-                          int* ticket, int col_chunks, bool trunc, int* ready, cudaStream_t st) {
+                          int* ticket, int col_chunks, bool trunc, int* ready, bool x_early, cudaStream_t st) {
   constexpr int U = APX_GATHER_U, CPT = APX_GATHER_CPT;
   const int kp = (int)ceil_div(std::max(k, 1), U) * U;
   const size_t smem = (size_t)gather_pitch(R, sizeof(T)) * n * sizeof(T) + (size_t)kp * sizeof(int);
   int blocks = (int)ceil_div(m_rows, R);
   if (max_ctas > 0 && ticket) {
-    APX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
+    // x_early: the caller zeroed the ticket before the previous kernel (a memset here would sit
+    // between that kernel and this programmatic dependent launch)
+    if (!x_early) APX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
     blocks = std::min(blocks, max_ctas);
   } else {
     ticket = nullptr;
@@ -738,31 +755,24 @@ static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const
     chunks = std::min(col_chunks, n / (threads * CPT));
   APX_REQUIRE(ready == nullptr || chunks == 1, "right gather: ready flags need whole-row blocks");
   const dim3 grid((unsigned)blocks, (unsigned)chunks);
+  auto go = [&](auto kern) -> int {
+    APX_TRY(set_smem<T>((const void*)kern, smem));
+    if (x_early) {
+      APX_CUDA(launch_pdl(kern, grid, dim3(threads), smem, st, X, JA, ka, lam, J, k, n, m_rows, acc, M, msq_partial,
+                          xsq_partial, ticket, ready, 1));
+    } else {
+      kern<<<grid, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M, msq_partial, xsq_partial, ticket,
+                                        ready, 0);
+    }
+    APX_LAUNCH_CHECK();
+    return OK;
+  };
   if (fast) {
-    if (trunc && sizeof(T) == 4) {
-      APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R, true, true>, smem));
-      cycle_right_gather<T, R, true, true><<<grid, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
-                                                                        msq_partial, xsq_partial, ticket, ready);
-      APX_LAUNCH_CHECK();
-      return OK;
-    }
-    APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R, true>, smem));
-    cycle_right_gather<T, R, true><<<grid, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
-                                                                  msq_partial, xsq_partial, ticket, ready);
-  } else {
-    if (trunc && sizeof(T) == 4) {
-      APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R, false, true>, smem));
-      cycle_right_gather<T, R, false, true><<<blocks, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
-                                                                         msq_partial, xsq_partial, ticket, ready);
-      APX_LAUNCH_CHECK();
-      return OK;
-    }
-    APX_TRY(set_smem<T>((const void*)cycle_right_gather<T, R, false>, smem));
-    cycle_right_gather<T, R, false><<<blocks, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M,
-                                                                   msq_partial, xsq_partial, ticket, ready);
+    if (trunc && sizeof(T) == 4) return go(cycle_right_gather<T, R, true, true>);
+    return go(cycle_right_gather<T, R, true>);
   }
-  APX_LAUNCH_CHECK();
-  return OK;
+  if (trunc && sizeof(T) == 4) return go(cycle_right_gather<T, R, false, true>);
+  return go(cycle_right_gather<T, R, false>);
 }
 
 int right_gather_rows(int n, size_t elem, int k) {
@@ -780,13 +790,13 @@ template <typename T>
 int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n,
                               int m_rows, int accumulate, T* M, double* msq_partial, double* xsq_partial,
                               cudaStream_t st, bool lam_padded, int max_ctas, int* ticket, int col_chunks,
-                              bool tf32_operands, int* ready) {
+                              bool tf32_operands, int* ready, bool x_early) {
   const int r = right_gather_rows(n, sizeof(T), k);
   APX_REQUIRE((size_t)n * sizeof(T) + (size_t)(k + 8) * sizeof(int) <= 227 * 1024,
               "n=%d too large for the right gather row block", n);
 #define APX_RG(RV) \
   return right_gather_r<T, RV>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, lam_padded, \
-                               max_ctas, ticket, col_chunks, tf32_operands, ready, st)
+                               max_ctas, ticket, col_chunks, tf32_operands, ready, x_early, st)
   switch (r) {
     case 1: APX_RG(1);
     case 2: APX_RG(2);
@@ -821,7 +831,7 @@ int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st) {
   template int launch_cycle_materialize<T>(const T*, const int*, int, int, T*, cudaStream_t);                 \
   template int launch_cycle_left_gather<T>(const T*, const T*, const int*, int, int, int, T*, cudaStream_t);  \
   template int launch_cycle_right_gather<T>(const T*, const int*, int, const T*, const int*, int, int, int, int, T*, \
-                                            double*, double*, cudaStream_t, bool, int, int*, int, bool, int*); \
+                                            double*, double*, cudaStream_t, bool, int, int*, int, bool, int*, bool); \
   template int launch_sumsq<T>(const T*, size_t, double*, int*, cudaStream_t);
 APX_INST(float)
 APX_INST(double)

@@ -27,7 +27,7 @@ template <typename T>
 int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int m_rows,
                               int accumulate, T* M, double* msq_partial, double* xsq_partial, cudaStream_t st,
                               bool lam_padded = false, int max_ctas = 0, int* ticket = nullptr, int col_chunks = 1,
-                              bool tf32_operands = false, int* ready = nullptr);
+                              bool tf32_operands = false, int* ready = nullptr, bool x_early = false);
 template <typename T>
 int launch_sumsq(const T* x, size_t cnt, double* partial, int* nparts, cudaStream_t st);
 int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st);
