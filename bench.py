@@ -434,6 +434,83 @@ def run_ours(args, rank, world, local_rank):
         print(json.dumps(line), flush=True)
 
 
+def run_sharded(args, rank, world, local_rank):
+    """--shard rows: ONE C4 product per step for the whole job, its rows of A and M split over the
+    ranks (sharded.mixed_product_rows; NCCL all-reduces of the Gram matrices, Q^T A and two norms).
+    Strong scaling: value = products/s of the job (max-over-ranks time)."""
+    import torch
+    import torch.distributed as dist
+    import paper_2504_19308_b200 as P
+    from paper_2504_19308_b200 import _native as N
+    from paper_2504_19308_b200 import sharded as S
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    n = args.n
+    A, B = gen_c4(n, 1234, dev)  # the same operands on every rank; each keeps its rows of A
+    r0, r1 = S.row_range(n, world, rank)
+    A_rows = A[r0:r1].contiguous()
+    omega = torch.from_numpy(P.cycle.draw_sketch(n, K_SVD, 7)).to(dev, torch.float32)
+    M_rows = torch.empty(r1 - r0, n, device=dev, dtype=torch.float32)
+
+    def reduce(t):
+        if world > 1:
+            dist.all_reduce(t)
+
+    def step():
+        return S._drive(S.mixed_rows_steps(A_rows, B, K_SVD, K_CYC, 1, omega, out=M_rows), reduce)
+
+    for _ in range(args.warmup):
+        step()
+    torch.cuda.synchronize()
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    l0 = N.lib().apx_launch_count()
+    with ClockSampler(local_rank) as clk:
+        start.record()
+        for _ in range(args.steps):
+            r = step()
+        end.record()
+        torch.cuda.synchronize()
+    launches = N.lib().apx_launch_count() - l0
+    S.check_breakdown(r)
+    if world > 1:
+        dist.barrier()
+    ms_max = max_over_ranks(start.elapsed_time(end), world, dev)
+    # correctness side-channel: these rows against the exact product's rows, selections equal
+    exact = A_rows.double() @ B.double()
+    err2 = torch.tensor([float(torch.linalg.norm(M_rows.double() - exact) ** 2),
+                         float(torch.linalg.norm(exact) ** 2)], device=dev, dtype=torch.float64)
+    del exact
+    sel = r["sel_b"].to(torch.int64)
+    if world > 1:
+        dist.all_reduce(err2)
+        sels = [torch.empty_like(sel) for _ in range(world)]
+        dist.all_gather(sels, sel)
+        same = all(torch.equal(x, sels[0]) for x in sels)
+    else:
+        same = True
+    if rank == 0:
+        s = r["scalars"].tolist()
+        line = {
+            "metric": METRIC, "value": args.steps / (ms_max * 1e-3), "unit": "products/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "strong",
+            "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "C4 mixed rSVD(k=64) x cycles(k=64) first-order product, n=8192",
+                       "n": n, "k_svd": K_SVD, "k_cyc": K_CYC, "order": 1, "power_iterations": 0,
+                       "parallelism": f"rows x{world} (one product per step, row blocks of A and M per rank)",
+                       "l2": "inputs larger than L2 (256 MiB B per rank); no flush"},
+            "clocks": clk.summary(), "gpu_launches": int(launches),
+            "rel_err_vs_exact": math.sqrt(err2[0].item() / err2[1].item()),
+            "selection_equal_across_ranks": same,
+            "norms": {"norm_da": math.sqrt(max(0, s[0] - s[2])), "norm_db": math.sqrt(max(0, s[1] - s[3]))},
+        }
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -445,6 +522,9 @@ def main():
     ap.add_argument("--split3", type=int, default=0)
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--shard", default="replicas", choices=["replicas", "rows"],
+                    help="replicas: one product per GPU (weak scaling, default); rows: one product per "
+                         "step split by rows over the GPUs (strong scaling)")
     args = ap.parse_args()
     rank = int(os.environ.get("RANK", 0))
     world = int(os.environ.get("WORLD_SIZE", 1))
@@ -458,7 +538,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_ours(args, rank, world, local_rank)
+        if args.shard == "rows":
+            run_sharded(args, rank, world, local_rank)
+        else:
+            run_ours(args, rank, world, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

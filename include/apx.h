@@ -197,6 +197,26 @@ size_t apx_qr_workspace(int dtype, int64_t m, int64_t k);
 int apx_qr(int dtype, const void* Y, int64_t m, int64_t k, void* Q, void* R, void* ws,
            size_t ws_bytes, void* stream);
 
+/* The C4 mixed product sharded by rows of A and M over ranks (the same math as
+ * apx_mixed_first_order with kind::tf32 GEMMs, fp32, k_svd = 64). Rank g passes its row block A_rows
+ * (m_rows x n), the whole B and the common sketch Omega (n x 64), and receives its rows of M. The call
+ * is made four times, phase = 1..4, on the same workspace and stream; after each phase the caller
+ * sums red_out over the ranks in place (NCCL all-reduce on `stream`) and passes it as the next
+ * phase's red_in:
+ *   phase 1: red_out = Gram(Y_g), 64 x 64 fp64          (red_in unused)
+ *   phase 2: red_in = sum Gram; red_out = pass-2 Gram, 64 x 64 fp64
+ *   phase 3: red_in = sum pass-2 Gram; red_out = Bm_g = Q_g^T A_g, 64 x n fp32
+ *   phase 4: red_in = sum Bm; red_out = [||A_g||_F^2, ||M_g||_F^2, Cholesky breakdown (0/1)] fp64
+ * flags bit 0: start M_g += Q_g W only after the whole gather (several shards driven on one device).
+ * scalars (APX_NSCALARS) receive the rank-independent values (||B||^2, kept energies); the caller
+ * fills FRO2_A / FRO2_M from the summed red_out of phase 4. Replaces nothing in the reference
+ * (which has no multi-device path); the per-rank product is svd.py:174-177 restricted to rows. */
+size_t apx_mixed_rows_workspace(int64_t n, int64_t m_rows, int k_svd, int k_cyc);
+int apx_mixed_rows_phase(int phase, const float* A_rows, int64_t m_rows, const float* B, int64_t n, int k_svd,
+                         int k_cyc, int order, int flags, const float* omega, float* M_rows, int32_t* sel_b,
+                         const void* red_in, void* red_out, double* scalars, void* ws, size_t ws_bytes,
+                         void* stream);
+
 /* sketch_norm_estimate (errest.py:139-154): out[0] = ||A (B G)||_F^2 with A m x n, B n x p, G p x k
  * (all fp64 row-major; G drawn on the host with numpy exactly as the reference draws it). The
  * caller divides by k. Complex operands are passed as their real embeddings (see errest.py). */

@@ -389,6 +389,118 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   return OK;
 }
 
+// ---- the C4 product sharded by rows of A and M -------------------------------------
+// Rank g holds the row block A_g (m x n) and the whole B; it computes M_g = Q_g W + A_g Bhat. The
+// plan of run_mixed_f32_umma is cut at the four points where the rows must be combined; between
+// phases the caller sums `red_out` over the ranks in place (an NCCL all-reduce on `stream`):
+//   1: B's cycle decomposition and the gather M_g = A_g Bhat start on hi (the gather runs through
+//      the later phases); Y_g = A_g Omega and its Gram matrix (out: l x l fp64)
+//   2: R1^{-1} from the summed Gram, Q_g = Y_g R1^{-1}, the pass-2 Gram (out: l x l fp64, zero
+//      when the conditioning lets pass 2 be skipped -- the same decision on every rank)
+//   3: pass 2 when needed; Bm_g = Q_g^T A_g (out: l x n fp32)
+//   4: W = Bm dB from the summed Bm (B is whole on every rank), M_g += Q_g W as the gather
+//      releases row blocks (out: [||A_g||^2, ||M_g||^2, Cholesky breakdown])
+struct RowsPlan {
+  MixedPlan mp;
+  void* qr;
+  size_t qr_bytes;
+  double* asum;  // ||A_g||^2 (hi, phase 1) until phase 4 reports it
+};
+
+static void plan_rows(Workspace& ws, RowsPlan& r, int n, int m, int l, int kc) {
+  plan_mixed(ws, r.mp, F32, n, l, kc);
+  r.qr_bytes = cholqr_rows_ws(m, l);
+  r.qr = ws.take<char>(r.qr_bytes);
+  r.asum = ws.take<double>(1);
+}
+
+static int run_mixed_rows_phase(int phase, const float* A, int m, const float* B, int n, int l, int kc, int order,
+                                int flags, const float* Omega, float* M, int* sb, const void* red_in, void* red_out,
+                                double* scal, const RowsPlan& r, cudaStream_t st) {
+  const MixedPlan& p = r.mp;
+  SideStream* ss = nullptr;
+  APX_TRY(get_side(&ss));
+  const cudaStream_t hi = ss->hi, lo = ss->s;
+  const int grows = right_gather_rows(n, sizeof(float), kc);
+  const int rblocks = (int)ceil_div(m, grows);
+  const int gctas = gather_ctas(rblocks);
+  const int free_sms = std::max(8, kNumSMs - gctas);
+  float *Y = (float*)p.Y, *Q = (float*)p.Q, *W = (float*)p.W, *part = (float*)p.part;
+  float* lb = (float*)p.lam_b;
+  if (phase == 1) {
+    APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
+    APX_CUDA(cudaMemsetAsync(p.ready, 0, rblocks * sizeof(int), st));
+    APX_CUDA(cudaMemsetAsync(p.ticket, 0, sizeof(int), st));
+    APX_CUDA(cudaEventRecord(ss->fork, st));
+    APX_CUDA(cudaStreamWaitEvent(lo, ss->fork, 0));
+    APX_CUDA(cudaStreamWaitEvent(hi, ss->fork, 0));
+    APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, nullptr, p.partial, hi));
+    APX_CUDA(cudaEventRecord(ss->b_read, hi));
+    APX_TRY(launch_topk(p.nr_b, n, kc, sb, hi, p.nr_b, 1.0, scal + APX_S_KEPT_B, p.en_b, scal + APX_S_FRO2_B));
+    APX_TRY(launch_cycle_extract<float>(B, n, sb, kc, lb, hi, /*aligned=*/true));
+    APX_TRY(zero_pad_rows<float>(lb, kc, n, hi));
+    APX_CUDA(cudaEventRecord(ss->b_ready, hi));
+    if (order == 1) {
+      APX_TRY(launch_cycle_right_gather<float>(A, nullptr, 0, lb, sb, kc, n, m, 0, M, nullptr, p.asq, hi, true, gctas,
+                                               p.ticket, 1, false, p.ready, /*x_early=*/true));
+      APX_TRY(launch_sum_vector(p.asq, rblocks, r.asum, hi));  // ||A_g||^2 (gather partials)
+    } else {
+      int parts = 0;
+      APX_TRY(launch_sumsq<float>(A, (size_t)m * n, p.asq, &parts, hi));
+      APX_TRY(launch_sum_vector(p.asq, parts, r.asum, hi));
+    }
+    APX_CUDA(cudaEventRecord(ss->hi_done, hi));
+    APX_CUDA(cudaStreamWaitEvent(lo, ss->b_read, 0));
+    const int s = std::max(1, std::min(8, (int)((2 * 32) / ceil_div(m, 128))));
+    APX_TRY(umma_tma_gemm(2, 64, A, n, Omega, l, s > 1 ? part : Y, l, (int64_t)m * l, m, l, n, s, 0, nullptr, 0, 1,
+                          lo));
+    if (s > 1) APX_TRY(launch_split_reduce_f32(part, s, (size_t)m * l, Y, lo));
+    APX_TRY(cholqr_rows_gram(Y, m, l, (double*)red_out, r.qr, r.qr_bytes, lo));
+  } else {
+    APX_CUDA(cudaEventRecord(ss->fork, st));  // the caller's all-reduce of the previous phase's output
+    APX_CUDA(cudaStreamWaitEvent(lo, ss->fork, 0));
+  }
+  if (phase == 2)
+    APX_TRY(cholqr_rows_pass1(Y, m, l, (const double*)red_in, Q, (double*)red_out, r.qr, r.qr_bytes, lo));
+  if (phase == 3) {
+    APX_TRY(cholqr_rows_pass2(m, l, (const double*)red_in, Q, r.qr, r.qr_bytes, lo));
+    // Bm_g = Q_g^T A_g, computed as (A_g^T Q_g) stored transposed
+    const int s = UmmaStages::splits(n, free_sms);
+    APX_TRY(umma_tma_gemm(7, 64, A, n, Q, l, s > 1 ? part : (float*)red_out, n, (int64_t)l * n, n, l, m, s, 0,
+                          nullptr, 0, 1, lo));
+    if (s > 1) APX_TRY(launch_split_reduce_f32(part, s, (size_t)n * l, (float*)red_out, lo));
+  }
+  if (phase == 4) {
+    const float* Bm = (const float*)red_in;
+    double* fin = (double*)red_out;  // [||A_g||^2, ||M_g||^2, breakdown]
+    int parts = 0;
+    APX_TRY(launch_sumsq<float>(Bm, (size_t)l * n, p.bsq, &parts, lo));
+    APX_TRY(launch_sum_vector(p.bsq, parts, scal + APX_S_KEPT_A, lo));
+    const int wblocks = (int)ceil_div(l, grows);
+    const int wchunks = std::max(1, std::min(8, (int)ceil_div(5 * free_sms, wblocks)));
+    if (order == 1) APX_TRY(UmmaStages::bm_times_db(B, Bm, W, part, n, l, nullptr, 0, lo, free_sms));
+    APX_CUDA(cudaStreamWaitEvent(lo, ss->b_ready, 0));
+    APX_TRY(launch_cycle_right_gather<float>(Bm, nullptr, 0, lb, sb, kc, n, l, order == 1 ? -1 : 0, W, nullptr,
+                                             nullptr, lo, true, 0, nullptr, wchunks, /*tf32_operands=*/order == 1));
+    // flags & 1: M += Q.W only after the whole gather (several shards on one device, whose gathers
+    // are queued behind each other on hi: a waiting Q.W grid could hold the SMs a later gather needs)
+    if (flags & 1) APX_CUDA(cudaStreamWaitEvent(lo, ss->hi_done, 0));
+    const int qw_ctas = (int)(ceil_div(n, order == 1 ? 128 : 256) * ceil_div(m, 128));
+    APX_TRY(umma_tma_gemm(2, order == 1 ? 128 : 256, Q, l, W, n, M, n, 0, m, n, l, 1, order == 1 ? 1 : 0, nullptr, 0,
+                          1, lo, p.msq, order == 1 ? p.ready : nullptr, grows));
+    APX_TRY(launch_sum_vector(p.msq, qw_ctas, fin + 1, lo));
+    APX_CUDA(cudaStreamWaitEvent(lo, ss->hi_done, 0));
+    APX_CUDA(cudaMemcpyAsync(fin, r.asum, sizeof(double), cudaMemcpyDeviceToDevice, lo));
+    APX_TRY(launch_flag_to_double(cholqr_rows_flags(r.qr, r.qr_bytes, m, l), fin + 2, lo));
+    APX_CUDA(cudaEventRecord(ss->join, lo));
+    APX_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
+    return OK;
+  }
+  APX_CUDA(cudaEventRecord(ss->join, lo));
+  APX_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
+  return OK;
+}
+
 template <typename T>
 static int run_mixed(const T* A, const T* B, int n, int l, int kc, int order, int q, const T* Omega, const int* fb,
                      T* M, int* sb, double* scal, const MixedPlan& p, bool split3, cudaStream_t st) {
@@ -534,6 +646,33 @@ size_t apx_mixed_first_order_workspace(int dtype, int64_t n, int k_svd, int k_cy
   MixedPlan p;
   plan_mixed(ws, p, dtype, (int)n, k_svd, k_cyc);
   return ws.off;
+}
+
+size_t apx_mixed_rows_workspace(int64_t n, int64_t m_rows, int k_svd, int k_cyc) {
+  Workspace ws(nullptr, 0, true);
+  RowsPlan r;
+  plan_rows(ws, r, (int)n, (int)m_rows, k_svd, k_cyc);
+  return ws.off;
+}
+
+int apx_mixed_rows_phase(int phase, const float* A_rows, int64_t m_rows, const float* B, int64_t n, int k_svd,
+                         int k_cyc, int order, int flags, const float* omega, float* M_rows, int32_t* sel_b,
+                         const void* red_in, void* red_out, double* scalars, void* wsp, size_t ws_bytes,
+                         void* stream) {
+  APX_REQUIRE(phase >= 1 && phase <= 4, "phase must be 1..4");
+  APX_REQUIRE(n >= 128 && n <= 46340 && (n % 32) == 0, "n=%lld: the sharded product needs n %% 32 == 0, n >= 128",
+              (long long)n);
+  APX_REQUIRE(m_rows >= 64 && m_rows <= n, "m_rows=%lld out of range [64, n]", (long long)m_rows);
+  APX_REQUIRE(k_svd == 64, "the sharded product is planned for k_svd = 64");
+  APX_REQUIRE(k_cyc >= 0 && k_cyc <= 128 && k_cyc <= n, "k_cyc=%d out of range [0, 128]", k_cyc);
+  APX_REQUIRE(order == 0 || order == 1, "order must be 0 or 1");
+  APX_REQUIRE(phase == 1 || red_in != nullptr, "phase %d needs the all-reduced output of phase %d", phase, phase - 1);
+  Workspace ws(wsp, ws_bytes);
+  RowsPlan r;
+  plan_rows(ws, r, (int)n, (int)m_rows, k_svd, k_cyc);
+  APX_WS_CHECK(ws);
+  return run_mixed_rows_phase(phase, A_rows, (int)m_rows, B, (int)n, k_svd, k_cyc, order, flags, omega, M_rows, sel_b,
+                              red_in, red_out, scalars, r, S(stream));
 }
 
 int apx_mixed_first_order(int dtype, const void* A, const void* B, int64_t n, int k_svd, int k_cyc, int order,

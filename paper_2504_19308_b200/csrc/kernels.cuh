@@ -43,6 +43,13 @@ int gemm_skinny(int kind, const T* A, int64_t lda, const T* B, int64_t ldb, T* C
                 int accumulate, const int* mJ, int mk, int mod_n, T* part, int splits, bool split3, cudaStream_t st);
 // ---- linalg.cu ----
 size_t qr_ws_bytes(int m, int l);
+size_t cholqr_rows_ws(int m, int l);
+int cholqr_rows_gram(const float* Y, int m, int l, double* G, void* ws, size_t bytes, cudaStream_t st);
+int cholqr_rows_pass1(const float* Y, int m, int l, const double* G, float* Q, double* G2, void* ws, size_t bytes,
+                      cudaStream_t st);
+int cholqr_rows_pass2(int m, int l, const double* G2, float* Q, void* ws, size_t bytes, cudaStream_t st);
+const int* cholqr_rows_flags(void* ws, size_t bytes, int m, int l);
+int launch_flag_to_double(const int* flag, double* out, cudaStream_t st);
 template <typename TI, typename TO>
 int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, int64_t qrs, int64_t qcs, TO* Q2,
                       int64_t q2rs, int64_t q2cs, void* wsp, size_t ws_bytes, int method, cudaStream_t st);

@@ -618,6 +618,13 @@ __global__ void __launch_bounds__(1024) householder_qr_kernel(const TI* __restri
 }
 
 __global__ void reset_flag_kernel(int* flag, int v) { *flag = v; }
+__global__ void flag_to_double_kernel(const int* flag, double* out) { *out = (double)*flag; }
+
+int launch_flag_to_double(const int* flag, double* out, cudaStream_t st) {
+  flag_to_double_kernel<<<1, 1, 0, st>>>(flag, out);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
 
 // ------------------------------------------------------------------------------------------
 size_t qr_ws_bytes(int m, int l) {
@@ -738,6 +745,77 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
   householder_qr_kernel<TI, TO><<<1, 1024, 0, st>>>(Y, rs, cs, m, l, flag, 0, W, V, Q, qrs, qcs, Q2, q2rs, q2cs);
   APX_LAUNCH_CHECK();
   return OK;
+}
+
+// ---- row-sharded CholeskyQR (fp32 sketch, l <= 64): the caller all-reduces the Gram matrices ----
+// between the steps, so every rank factors the same G and Q_g = Y_g R^{-1} is the row block g of
+// the orthonormal Q of the stacked Y. Same kernels and the same pass-2 rule as the fast path of
+// qr_orthonormalize; a Cholesky breakdown is reported through flags[0] (no Householder fallback:
+// it would need the whole Y on one device).
+namespace {
+struct RowsQR {
+  double *part, *Rinv, *Q1;
+  int* flag;  // [0] breakdown, [1] skip pass 2
+};
+RowsQR plan_rows_qr(Workspace& ws, int m, int l) {
+  RowsQR r;
+  r.part = ws.take<double>((size_t)ceil_div(m, 64) * l * l);
+  r.Rinv = ws.take<double>((size_t)l * l);
+  r.Q1 = ws.take<double>((size_t)m * l);
+  r.flag = ws.take<int>(4);
+  return r;
+}
+}  // namespace
+
+size_t cholqr_rows_ws(int m, int l) {
+  Workspace ws(nullptr, 0, true);
+  plan_rows_qr(ws, m, l);
+  return ws.off;
+}
+
+int cholqr_rows_gram(const float* Y, int m, int l, double* G, void* wsp, size_t bytes, cudaStream_t st) {
+  APX_REQUIRE(l >= 1 && l <= 64 && m >= 1, "row-sharded CholeskyQR: l=%d m=%d", l, m);
+  Workspace ws(wsp, bytes);
+  RowsQR r = plan_rows_qr(ws, m, l);
+  APX_WS_CHECK(ws);
+  return launch_gram<float>(Y, l, 1, m, l, nullptr, r.part, G, st);
+}
+
+int cholqr_rows_pass1(const float* Y, int m, int l, const double* G, float* Q, double* G2, void* wsp, size_t bytes,
+                      cudaStream_t st) {
+  Workspace ws(wsp, bytes);
+  RowsQR r = plan_rows_qr(ws, m, l);
+  APX_WS_CHECK(ws);
+  APX_CUDA(cudaMemsetAsync(r.flag, 0, 4 * sizeof(int), st));
+  APX_CUDA(cudaMemsetAsync(G2, 0, (size_t)l * l * sizeof(double), st));  // stays zero if pass 2 is skipped
+  cholinv64_kernel<<<1, 256, 0, st>>>(G, l, r.Rinv, r.flag, r.flag, r.flag + 1, 3.0e4);
+  APX_LAUNCH_CHECK();
+  APX_CUDA(cudaFuncSetAttribute(apply_x_kernel<float, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kApplySmem));
+  apply_x_kernel<float, float><<<(unsigned)ceil_div(m, 64), 256, kApplySmem, st>>>(
+      Y, l, 1, m, l, r.Rinv, r.flag, r.flag + 1, r.Q1, Q, l, 1, (float*)nullptr, 0, 0);
+  APX_LAUNCH_CHECK();
+  return launch_gram<double>(r.Q1, l, 1, m, l, r.flag + 1, r.part, G2, st);
+}
+
+int cholqr_rows_pass2(int m, int l, const double* G2, float* Q, void* wsp, size_t bytes, cudaStream_t st) {
+  Workspace ws(wsp, bytes);
+  RowsQR r = plan_rows_qr(ws, m, l);
+  APX_WS_CHECK(ws);
+  cholinv64_kernel<<<1, 256, 0, st>>>(G2, l, r.Rinv, r.flag + 1, r.flag, (int*)nullptr, 0.0);
+  APX_LAUNCH_CHECK();
+  APX_CUDA(cudaFuncSetAttribute(apply_x_kernel<double, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)kApplySmem));
+  apply_x_kernel<double, float><<<(unsigned)ceil_div(m, 64), 256, kApplySmem, st>>>(
+      r.Q1, l, 1, m, l, r.Rinv, r.flag + 1, (const int*)nullptr, (double*)nullptr, Q, l, 1, (float*)nullptr, 0, 0);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+const int* cholqr_rows_flags(void* wsp, size_t bytes, int m, int l) {
+  Workspace ws(wsp, bytes);
+  RowsQR r = plan_rows_qr(ws, m, l);
+  return r.flag;
 }
 
 template int qr_orthonormalize<float, float>(const float*, int64_t, int64_t, int, int, float*, int64_t, int64_t,

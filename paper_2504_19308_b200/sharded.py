@@ -1,0 +1,149 @@
+"""The C4 mixed product sharded by rows of A and M over ranks (BASELINE config 4).
+
+Rank g holds the row block A_g = A[r0:r1] and the whole B; it produces M[r0:r1]. The per-rank plan
+is the single-device plan of apx_mixed_first_order (B's cycle decomposition and the persistent row
+gather on one internal stream, the range finder on another) cut at the four points where rows
+must be combined (apx_mixed_rows_phase, include/apx.h):
+
+    Gram(Y_g) -> sum -> pass-1 Q_g, pass-2 Gram -> sum -> Bm_g = Q_g^T A_g -> sum -> W, M_g
+              -> sum of [||A_g||^2, ||M_g||^2]
+
+Only small factors cross ranks: two 64 x 64 fp64 Gram matrices, the 64 x n fp32 Bm (2 MiB at
+n = 8192) and two scalars -- the "all-gather of the small truncated factors" of the north star,
+as all-reduces. Every rank factors the same summed Gram, so the pass-2 decision and the
+orthonormal basis agree across ranks; B's cycle selection is computed on every rank from the same
+B (no exchange), so the selected indices are identical by construction.
+
+``mixed_rows_steps`` is the rank-local generator (yields the tensor to sum at each exchange
+point); ``mixed_product_rows`` drives it with torch.distributed (NCCL); ``lockstep`` drives
+several shards inside one process, summing on the device in rank order (tests, single-GPU
+simulation of the sharded math).
+"""
+
+from __future__ import annotations
+
+import math
+
+import torch
+
+from . import _device as D
+from . import _native as N
+
+
+def row_range(n: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous row block [r0, r1) of rank `rank`: boundaries are r * n / world rounded to a
+    multiple of 64 (the row-tile height of M += Q W), so every block is within 64 rows of n / world."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+
+    def cut(r):
+        return n if r == world else min(n, 64 * round(r * n / (64 * world)))
+
+    return cut(rank), cut(rank + 1)
+
+
+def mixed_rows_steps(A_rows, B, k_svd: int, k_cyc: int, order: int, omega, out=None, serialize: bool = False):
+    """One rank's share of the C4 product. A_rows (m x n), B (n x n), omega (n x k_svd): fp32 device
+    tensors. Yields the tensor to be summed over ranks (in place) at each of the four exchange
+    points; returns dict(M=rows of M, sel_b, scalars) with the scalars of apx_mixed_first_order.
+    serialize: start M_g += Q_g W only after this shard's whole gather (required when several shards
+    share one device, see apx_mixed_rows_phase)."""
+    if A_rows.dtype != torch.float32 or B.dtype != torch.float32:
+        raise ValueError("the sharded product is fp32")
+    m, n = A_rows.shape
+    if tuple(B.shape) != (n, n):
+        raise ValueError(f"B must be {n} x {n}, got {tuple(B.shape)}")
+    if order not in (0, 1):
+        raise ValueError("order must be 0 or 1")
+    dev = A_rows.device
+    l = k_svd
+    M = out if out is not None else torch.empty((m, n), dtype=torch.float32, device=dev)
+    sb = torch.empty(max(k_cyc, 1), dtype=torch.int32, device=dev)
+    scal = torch.zeros(N.NSCALARS, dtype=torch.float64, device=dev)
+    ws = D.workspace(N.size("apx_mixed_rows_workspace", n, m, k_svd, k_cyc))
+    g1 = torch.empty(l * l, dtype=torch.float64, device=dev)
+    g2 = torch.empty(l * l, dtype=torch.float64, device=dev)
+    bm = torch.empty(l * n, dtype=torch.float32, device=dev)
+    fin = torch.zeros(3, dtype=torch.float64, device=dev)
+
+    def phase(i, red_in, red_out):
+        N.call("apx_mixed_rows_phase", i, A_rows.data_ptr(), m, B.data_ptr(), n, k_svd, k_cyc, order,
+               1 if serialize else 0, omega.data_ptr(), M.data_ptr(), sb.data_ptr(), D.ptr(red_in),
+               red_out.data_ptr(), scal.data_ptr(), ws.data_ptr(), ws.numel(), D.stream_ptr())
+
+    phase(1, None, g1)
+    yield g1
+    phase(2, g1, g2)
+    yield g2
+    phase(3, g2, bm)
+    yield bm
+    phase(4, bm, fin)
+    yield fin[:2]
+    scal[N.S_FRO2_A] = fin[0]  # device-side copies: no host synchronisation inside the product
+    scal[N.S_FRO2_M] = fin[1]
+    return {"M": M, "sel_b": sb[:k_cyc], "scalars": scal, "breakdown": fin[2], "ws": ws}
+
+
+def check_breakdown(result):
+    """Raise if the row-sharded CholeskyQR broke down (reads one device scalar)."""
+    if float(result["breakdown"].item()) != 0.0:
+        raise RuntimeError("row-sharded CholeskyQR broke down (numerically rank-deficient sketch); "
+                           "use the single-device product, whose Householder fallback handles it")
+    return result
+
+
+def _drive(gen, reduce):
+    try:
+        t = next(gen)
+        while True:
+            reduce(t)
+            t = gen.send(None)
+    except StopIteration as e:
+        return e.value
+
+
+def mixed_product_rows(A_rows, B, k_svd: int, k_cyc: int, order: int, omega, group=None, out=None,
+                       check: bool = True):
+    """This rank's rows of the C4 product; the exchanges are torch.distributed all-reduces (NCCL on
+    the current stream for CUDA tensors). check=False skips the (synchronising) breakdown check --
+    call check_breakdown(result) later."""
+    import torch.distributed as dist
+
+    r = _drive(mixed_rows_steps(A_rows, B, k_svd, k_cyc, order, omega, out),
+               lambda t: dist.all_reduce(t, group=group))
+    return check_breakdown(r) if check else r
+
+
+def lockstep(gens):
+    """Run the generators of several shards in one process: at every exchange point the yielded
+    tensors are summed in rank order on the device and the sum is written back into each (what
+    an all-reduce does across processes). Returns the list of results. The shards must have been
+    created with serialize=True when they share a device."""
+    pending = [next(g) for g in gens]
+    results = [None] * len(gens)
+    while True:
+        total = pending[0].clone()
+        for t in pending[1:]:
+            total += t
+        nxt = []
+        for i, (g, t) in enumerate(zip(gens, pending)):
+            t.copy_(total)
+            try:
+                nxt.append(g.send(None))
+            except StopIteration as e:
+                results[i] = e.value
+                nxt.append(None)
+        if all(r is not None for r in results):
+            return results
+        if any(x is None for x in nxt):
+            raise RuntimeError("shards disagree on the number of exchange points")
+        pending = nxt
+
+
+def norms_from_scalars(s):
+    """(||A||, ||B||, ||dA||, ||dB||, ||M||) from the scalar vector (cycle._norms)."""
+    nA = math.sqrt(max(0.0, s[N.S_FRO2_A]))
+    nB = math.sqrt(max(0.0, s[N.S_FRO2_B]))
+    ndA = math.sqrt(max(0.0, s[N.S_FRO2_A] - s[N.S_KEPT_A]))
+    ndB = math.sqrt(max(0.0, s[N.S_FRO2_B] - s[N.S_KEPT_B]))
+    return nA, nB, ndA, ndB, math.sqrt(max(0.0, s[N.S_FRO2_M]))

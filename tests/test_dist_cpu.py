@@ -51,3 +51,71 @@ def test_single_rank_no_collective():
     import bench
     assert bench.max_over_ranks(3.5, 1, torch.device("cpu")) == 3.5
     assert bench.job_throughput(4, 1, 2.0) == 2.0
+
+
+# ---- the row-sharded product's exchange protocol (paper_2504_19308_b200.sharded) over gloo ----
+# The device phases are replaced by their fp64 algebra on CPU tensors (test-only stand-ins); what
+# is checked is the host protocol the GPU path uses -- one in-place all-reduce per exchange point,
+# in order -- and that the row-block algebra reproduces the unsharded projection Q Q^T A.
+
+def _toy_rows_steps(A_rows, Omega):
+    Y = A_rows @ Omega
+    G = Y.T @ Y
+    yield G                                   # Gram partial -> sum over ranks
+    R = torch.linalg.cholesky(G).T            # upper factor, identical on every rank
+    Q = torch.linalg.solve_triangular(R, Y, upper=True, left=False)
+    Bm = Q.T @ A_rows
+    yield Bm                                  # Q_g^T A_g -> sum over ranks
+    return Q @ Bm                             # rows of Q Q^T A
+
+
+def _sharded_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2504_19308_b200.sharded import _drive, row_range
+        g = torch.Generator().manual_seed(7)
+        n, l = 320, 8
+        A = torch.randn(n, n, generator=g, dtype=torch.float64)
+        Omega = torch.randn(n, l, generator=g, dtype=torch.float64)
+        r0, r1 = row_range(n, world, rank)
+        P_rows = _drive(_toy_rows_steps(A[r0:r1], Omega), lambda t: dist.all_reduce(t))
+        q.put((rank, r0, r1, P_rows.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_sharded_protocol_gloo():
+    import numpy as np
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted(q.get(timeout=120) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    g = torch.Generator().manual_seed(7)
+    n, l = 320, 8
+    A = torch.randn(n, n, generator=g, dtype=torch.float64)
+    Omega = torch.randn(n, l, generator=g, dtype=torch.float64)
+    Qf, _ = torch.linalg.qr(A @ Omega)
+    P = (Qf @ (Qf.T @ A)).numpy()
+    got = np.concatenate([o[3] for o in out], axis=0)
+    assert [o[1:3] for o in out] == [(0, 128), (128, 320)]
+    assert np.linalg.norm(got - P) <= 1e-10 * np.linalg.norm(P)
+
+
+def test_row_range_partition():
+    from paper_2504_19308_b200.sharded import row_range
+    for n in (128, 1000, 8192, 32768):
+        for world in (1, 2, 3, 4, 8):
+            blocks = [row_range(n, world, r) for r in range(world)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == n
+            assert all(a[1] == b[0] for a, b in zip(blocks, blocks[1:]))
+            sizes = [b - a for a, b in blocks]
+            assert all(abs(z - n / world) <= 64 for z in sizes)
+    with pytest.raises(ValueError):
+        row_range(128, 2, 2)
