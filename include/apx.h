@@ -150,9 +150,10 @@ int apx_sparse_rows_multiply(const int32_t* sel, const void* vals, int k, int64_
 
 /* ------------------------------------------------------------------ core.py primitives ---- */
 /* unitary_dft (core.py:82-97) on `batch` complex128 vectors (element i of vector b at
- * x[b*dist + i*stride]); inverse = 0 applies W, 1 applies W*. Any length (direct DFT for
- * non-powers of two). */
-size_t apx_unitary_dft_workspace(int64_t n);
+ * x[b*dist + i*stride]); inverse = 0 applies W, 1 applies W*. Lengths whose transform fits one
+ * CTA's shared memory run there (a direct DFT for non-powers of two, up to ~7200); longer powers of
+ * two (up to 2^18) use a four-step transform through global memory. */
+size_t apx_unitary_dft_workspace(int64_t n, int64_t batch);
 int apx_unitary_dft(const void* x, void* y, int64_t n, int64_t batch, int64_t stride, int64_t dist,
                     int inverse, void* ws, size_t ws_bytes, void* stream);
 

@@ -43,7 +43,7 @@ SIGNATURES = {
     "apx_circulant_materialize_workspace": (_sz, [_i64]),
     "apx_circulant_materialize": (C.c_int, [_vp, _vp, _i32, _i64, _vp, _vp, _sz, _vp]),
     "apx_circulant_component": (C.c_int, [_i32, _vp, _i64, _i32, _vp, _vp, _sz, _vp]),
-    "apx_unitary_dft_workspace": (_sz, [_i64]),
+    "apx_unitary_dft_workspace": (_sz, [_i64, _i64]),
     "apx_unitary_dft": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _i64, _i32, _vp, _sz, _vp]),
     "apx_cycle_layout": (C.c_int, [_i32, _vp, _i64, _i32, _vp, _vp]),
     "apx_apply_cycle_power": (C.c_int, [_i32, _vp, _i64, _i64, _i64, _i32, _vp, _vp]),

@@ -98,7 +98,7 @@ def unitary_dft(x, direction: str = "forward", axis: int = -1) -> np.ndarray:
     dev = D.require_cuda()
     xd = torch.from_numpy(flat).to(dev)
     yd = torch.empty_like(xd)
-    ws = D.workspace(N.size("apx_unitary_dft_workspace", n))
+    ws = D.workspace(N.size("apx_unitary_dft_workspace", n, flat.shape[0]))
     N.call("apx_unitary_dft", xd.data_ptr(), yd.data_ptr(), n, flat.shape[0], 1, n,
            1 if direction == "inverse" else 0, ws.data_ptr(), ws.numel(), D.stream_ptr())
     return np.moveaxis(yd.cpu().numpy().reshape(shape), -1, axis)

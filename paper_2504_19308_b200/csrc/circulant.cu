@@ -517,6 +517,247 @@ __global__ void cycle_power_kernel(const E* __restrict__ in, int rows, int cols,
 }
 
 // ---------------------------------------------------------------------------------------------
+// Transforms longer than one CTA's shared memory (power-of-two n >= 8192 for the products, whose
+// fused kernels above keep two length-n buffers in shared memory). Four-step FFT, n = n1 * n2,
+// element i = i1 * n2 + i2 of a row, output k = k1 + n1 * k2:
+//   pass 1: for every i2, the length-n1 DFT over i1, times the twiddle w_n^{i2 k1}  (in place)
+//   pass 2: for every k1, the length-n2 DFT over i2, stored at k1 + n1 k2            (to `out`)
+// Each CTA keeps a tile of TC columns (pass 1) or TR rows (pass 2) of one sequence in shared
+// memory, so every global access is a run of TC (TR) consecutive complex values. The products
+// then run unfused: skew / transpose -> batched FFT -> gather in frequency space -> inverse FFT.
+// ---------------------------------------------------------------------------------------------
+
+// `count` independent power-of-two transforms of length len, transform t at x + t * len (each
+// XOR-swizzled by fsw), all threads of the CTA cooperating; same butterflies as fft_block.
+__device__ inline void fft_multi(double2* x, int count, int len, const double2* __restrict__ roots, bool inverse) {
+  const int tid = threadIdx.x, nt = blockDim.x;
+  if (len == 1) return;
+  const int logn = ilog2(len);
+  for (int e = tid; e < count * len; e += nt) {
+    const int t = e >> logn, i = e & (len - 1);
+    const int j = (int)(__brev((unsigned)i) >> (32 - logn));
+    if (i < j) {
+      double2* b = x + (size_t)t * len;
+      const double2 v = b[fsw(i, len)];
+      b[fsw(i, len)] = b[fsw(j, len)];
+      b[fsw(j, len)] = v;
+    }
+  }
+  __syncthreads();
+  int s = 1;
+  const int g8 = len >> 3;
+  for (; s + 2 <= logn; s += 3) {
+    const int h = 1 << (s - 1);
+    for (int gg = tid; gg < count * g8; gg += nt) {
+      const int t = gg / g8, g = gg - t * g8;
+      double2* b = x + (size_t)t * len;
+      const int pos = g & (h - 1);
+      const int base = (g >> (s - 1)) << (s + 2);
+      double2 v[8];
+#pragma unroll
+      for (int m = 0; m < 8; ++m) v[m] = b[fsw(base + pos + m * h, len)];
+#pragma unroll
+      for (int st = 0; st < 3; ++st) {
+        const int hs = 1 << st;
+#pragma unroll
+        for (int m = 0; m < 8; ++m) {
+          if (m & hs) continue;
+          const int q = pos + (m & (hs - 1)) * h;
+          double2 w = __ldg(roots + (q << (logn - s - st)));
+          if (inverse) w.y = -w.y;
+          const double2 tt = cmul(w, v[m + hs]);
+          const double2 u = v[m];
+          v[m] = cadd(u, tt);
+          v[m + hs] = csub(u, tt);
+        }
+      }
+#pragma unroll
+      for (int m = 0; m < 8; ++m) b[fsw(base + pos + m * h, len)] = v[m];
+    }
+    __syncthreads();
+  }
+  const int g2 = len >> 1;
+  for (; s <= logn; ++s) {
+    const int half = 1 << (s - 1);
+    for (int gg = tid; gg < count * g2; gg += nt) {
+      const int t = gg / g2, bb = gg - t * g2;
+      double2* b = x + (size_t)t * len;
+      const int pos = bb & (half - 1);
+      const int i = ((bb >> (s - 1)) << s) + pos;
+      const int j = i + half;
+      double2 w = __ldg(roots + (pos << (logn - s)));
+      if (inverse) w.y = -w.y;
+      const double2 tt = cmul(w, b[fsw(j, len)]);
+      const double2 u = b[fsw(i, len)];
+      b[fsw(i, len)] = cadd(u, tt);
+      b[fsw(j, len)] = csub(u, tt);
+    }
+    __syncthreads();
+  }
+}
+
+constexpr int kBigTile = 16;  // columns (pass 1) / rows (pass 2) per CTA: 256-byte global runs
+
+// pass 1 of the four-step transform of `rows` sequences of length n = n1 * n2: in (TI) -> data
+// (complex; may alias `in` when TI is complex). grid (n2 / kBigTile, rows).
+template <typename TI>
+__global__ void __launch_bounds__(512) fft4_pass1_kernel(const TI* in, int n1, int n2, int inverse,
+                                                         const double2* __restrict__ roots_n,
+                                                         const double2* __restrict__ roots_n1, double2* data) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* x = reinterpret_cast<double2*>(smem_raw);
+  const size_t n = (size_t)n1 * n2;
+  const size_t row = blockIdx.y;
+  const int i20 = blockIdx.x * kBigTile;
+  for (int e = threadIdx.x; e < kBigTile * n1; e += blockDim.x) {
+    const int i1 = e / kBigTile, c = e - i1 * kBigTile;
+    x[(size_t)c * n1 + fsw(i1, n1)] = ld_c<TI>(in, row * n + (size_t)i1 * n2 + i20 + c);
+  }
+  __syncthreads();
+  fft_multi(x, kBigTile, n1, roots_n1, inverse != 0);
+  for (int e = threadIdx.x; e < kBigTile * n1; e += blockDim.x) {
+    const int k1 = e / kBigTile, c = e - k1 * kBigTile;
+    const int i2 = i20 + c;
+    double2 w = __ldg(roots_n + (((size_t)i2 * k1) & (n - 1)));
+    if (inverse) w.y = -w.y;
+    data[row * n + (size_t)k1 * n2 + i2] = cmul(x[(size_t)c * n1 + fsw(k1, n1)], w);
+  }
+}
+
+// pass 2: data -> out (must not alias). grid (n1 / kBigTile, rows).
+__global__ void __launch_bounds__(512) fft4_pass2_kernel(const double2* __restrict__ data, int n1, int n2,
+                                                         int inverse, const double2* __restrict__ roots_n2,
+                                                         double scale, double2* __restrict__ out) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* x = reinterpret_cast<double2*>(smem_raw);
+  const size_t n = (size_t)n1 * n2;
+  const size_t row = blockIdx.y;
+  const int k10 = blockIdx.x * kBigTile;
+  for (int e = threadIdx.x; e < kBigTile * n2; e += blockDim.x) {
+    const int r = e / n2, i2 = e - r * n2;
+    x[(size_t)r * n2 + fsw(i2, n2)] = __ldg(data + row * n + (size_t)(k10 + r) * n2 + i2);
+  }
+  __syncthreads();
+  fft_multi(x, kBigTile, n2, roots_n2, inverse != 0);
+  for (int e = threadIdx.x; e < kBigTile * n2; e += blockDim.x) {
+    const int k2 = e / kBigTile, r = e - k2 * kBigTile;
+    out[row * n + (size_t)(k10 + r) + (size_t)n1 * k2] = cscale(x[(size_t)r * n2 + fsw(k2, n2)], scale);
+  }
+}
+
+// big-path helpers (all grid-stride over n x n, or tiled where a transpose is involved)
+// out[c][p] = in[p][c] (real or complex in, complex out), 32 x 32 tiles
+template <typename TI>
+__global__ void __launch_bounds__(256) transpose_to_c_kernel(const TI* __restrict__ in, int n, double2* __restrict__ out) {
+  __shared__ double2 tile[32][33];
+  const int c0 = blockIdx.x * 32, p0 = blockIdx.y * 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int r = w; r < 32; r += 8) tile[r][lane] = ld_c<TI>(in, (size_t)(p0 + r) * n + c0 + lane);
+  __syncthreads();
+  for (int r = w; r < 32; r += 8) out[(size_t)(c0 + r) * n + p0 + lane] = tile[lane][r];
+}
+
+// M[p][c] = scale * Y[c][p]
+__global__ void __launch_bounds__(256) transpose_scale_c_kernel(const double2* __restrict__ Y, int n, double scale,
+                                                                double2* __restrict__ M) {
+  __shared__ double2 tile[32][33];
+  const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  for (int r = w; r < 32; r += 8) tile[r][lane] = Y[(size_t)(c0 + r) * n + p0 + lane];
+  __syncthreads();
+  for (int r = w; r < 32; r += 8) M[(size_t)(p0 + r) * n + c0 + lane] = cscale(tile[lane][r], scale);
+}
+
+// magnitudes: partial[g][t] = sum over rows j of chunk g of |St[j][t]|^2 * s2; then mag[t] = sqrt(sum_g)
+__global__ void __launch_bounds__(256) colsum_abs2_kernel(const double2* __restrict__ St, int n, int rpc, double s2,
+                                                          double* __restrict__ partial) {
+  const int t = blockIdx.x * blockDim.x + threadIdx.x;
+  const int j0 = blockIdx.y * rpc, j1 = min(n, j0 + rpc);
+  if (t >= n) return;
+  double a = 0.0;
+  for (int j = j0; j < j1; ++j) {
+    const double2 v = __ldg(St + (size_t)j * n + t);
+    a = fma(v.x, v.x, fma(v.y, v.y, a));
+  }
+  partial[(size_t)blockIdx.y * n + t] = a * s2;
+}
+
+// Ssel[q][i] = scale * St[i][sel[q]]
+__global__ void __launch_bounds__(256) gather_cols_kernel(const double2* __restrict__ St, int n, const int* __restrict__ sel,
+                                                          double scale, double2* __restrict__ Ssel) {
+  const int q = blockIdx.y;
+  const int t = sel[q];
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x)
+    Ssel[(size_t)q * n + i] = cscale(__ldg(St + (size_t)i * n + t), scale);
+}
+
+// term1 gather in frequency space: Y[c][p] = sum_q L_q[p] * rs * FB[c][(p - t_q) % n]
+__global__ void __launch_bounds__(256) big_left_gather_kernel(const double2* __restrict__ FB, int n,
+                                                              const double2* __restrict__ L, const int* __restrict__ sel,
+                                                              int k, double rs, double2* __restrict__ Y) {
+  __shared__ int s_buf[512];
+  for (int q = threadIdx.x; q < k && q < 512; q += blockDim.x) s_buf[q] = sel[q];
+  __syncthreads();
+  const int* s_sel = k <= 512 ? s_buf : sel;
+  const size_t c = blockIdx.y;
+  const double2* fb = FB + c * n;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    double2 a = make_double2(0.0, 0.0);
+    for (int q = 0; q < k; ++q) {
+      const int src = (p - s_sel[q]) & (n - 1);
+      a = cadd(a, cmul(__ldg(L + (size_t)q * n + p), cscale(__ldg(fb + src), rs)));
+    }
+    Y[c * n + p] = a;
+  }
+}
+
+// X[r][c] = conj(A[r][c] - Ahat[r][c]), Ahat[r][c] = sum_q Ssel[q][(r - c) % n] exp(+2 pi i t_q c / n)
+template <typename T>
+__global__ void __launch_bounds__(256) big_dA_kernel(const T* __restrict__ A, int n, const double2* __restrict__ Ssel,
+                                                     const int* __restrict__ sel, int k,
+                                                     const double2* __restrict__ roots, double2* __restrict__ X) {
+  __shared__ int s_buf[512];
+  for (int q = threadIdx.x; q < k && q < 512; q += blockDim.x) s_buf[q] = sel[q];
+  __syncthreads();
+  const int* s_sel = k <= 512 ? s_buf : sel;
+  const size_t r = blockIdx.y;
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
+    const int d = ((int)r - c) & (n - 1);
+    double2 ah = make_double2(0.0, 0.0);
+    for (int q = 0; q < k; ++q)
+      ah = cadd(ah, cmul(__ldg(Ssel + (size_t)q * n + d), cconj(__ldg(roots + mulmod_n(s_sel[q], c, n)))));
+    X[r * n + c] = cconj(csub(ld_c<T>(A, r * n + c), ah));
+  }
+}
+
+// term2 gather: Y[r][p] = sum_q (rs * X[r][(p + s_q) % n]) * conj(L_q[(p + s_q) % n])
+__global__ void __launch_bounds__(256) big_right_gather_kernel(const double2* __restrict__ X, int n,
+                                                               const double2* __restrict__ L, const int* __restrict__ sel,
+                                                               int k, double rs, double2* __restrict__ Y) {
+  __shared__ int s_buf[512];
+  for (int q = threadIdx.x; q < k && q < 512; q += blockDim.x) s_buf[q] = sel[q];
+  __syncthreads();
+  const int* s_sel = k <= 512 ? s_buf : sel;
+  const size_t r = blockIdx.y;
+  const double2* xr = X + r * n;
+  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
+    double2 a = make_double2(0.0, 0.0);
+    for (int q = 0; q < k; ++q) {
+      const int src = (p + s_sel[q]) & (n - 1);
+      a = cadd(a, cmulc(cscale(__ldg(xr + src), rs), __ldg(L + (size_t)q * n + src)));
+    }
+    Y[r * n + p] = a;
+  }
+}
+
+// M += conj(rs * Y)
+__global__ void __launch_bounds__(256) acc_conj_kernel(const double2* __restrict__ Y, size_t count, double rs,
+                                                       double2* __restrict__ M) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < count; e += (size_t)gridDim.x * blockDim.x)
+    M[e] = cadd(M[e], cconj(cscale(Y[e], rs)));
+}
+
+// ---------------------------------------------------------------------------------------------
 // host side
 // ---------------------------------------------------------------------------------------------
 struct CircPlan {
@@ -626,6 +867,164 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
   return OK;
 }
 
+
+// ---- big path (power-of-two n whose two-buffer transforms exceed shared memory) ----------------
+static bool big_fft_ok(int64_t n) { return n >= 256 && is_pow2((int)n) && n <= (1 << 18); }
+// APX_FFT_BIG=1 routes every eligible length through the four-step path (tests compare the two)
+static bool force_big(int64_t n) {
+  static const bool on = [] {
+    const char* e = getenv("APX_FFT_BIG");
+    return e && atoi(e) != 0;
+  }();
+  return on && big_fft_ok(n);
+}
+static bool circ_fused_fits(int n, int k) {
+  return !force_big(n) && fft_smem_bytes(n, 2) + (size_t)2 * std::max(k, 0) * sizeof(int) <= 227 * 1024;
+}
+
+struct BigFFT {
+  int n, n1, n2;
+  double2 *roots, *roots1, *roots2;
+};
+
+static void plan_big_fft(Workspace& ws, BigFFT& f, int n) {
+  const int l = ilog2(n);
+  f.n = n;
+  f.n1 = 1 << (l / 2);
+  f.n2 = 1 << (l - l / 2);
+  f.roots = ws.take<double2>(n);
+  f.roots1 = ws.take<double2>(f.n1);
+  f.roots2 = ws.take<double2>(f.n2);
+}
+
+static int big_fft_init(const BigFFT& f, cudaStream_t st) {
+  launch_roots(f.roots, f.n, st);
+  launch_roots(f.roots1, f.n1, st);
+  launch_roots(f.roots2, f.n2, st);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+// rows x n: in (TI) -> out (complex) via `data` (complex, may alias `in` but not `out`)
+template <typename TI>
+static int big_fft_rows(const BigFFT& f, const TI* in, double2* data, double2* out, int rows, bool inverse,
+                        double scale, cudaStream_t st) {
+  if (rows <= 0) return OK;
+  APX_REQUIRE(rows <= 65535, "big FFT: %d rows per launch", rows);
+  const size_t s1 = (size_t)kBigTile * f.n1 * sizeof(double2), s2 = (size_t)kBigTile * f.n2 * sizeof(double2);
+  APX_CUDA(cudaFuncSetAttribute(fft4_pass1_kernel<TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
+  APX_CUDA(cudaFuncSetAttribute(fft4_pass2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
+  fft4_pass1_kernel<TI><<<dim3((unsigned)(f.n2 / kBigTile), (unsigned)rows), 512, s1, st>>>(
+      in, f.n1, f.n2, inverse ? 1 : 0, f.roots, f.roots1, data);
+  APX_LAUNCH_CHECK();
+  fft4_pass2_kernel<<<dim3((unsigned)(f.n1 / kBigTile), (unsigned)rows), 512, s2, st>>>(
+      data, f.n1, f.n2, inverse ? 1 : 0, f.roots2, scale, out);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+struct BigCircPlan {
+  BigFFT f;
+  double2 *W1, *W2, *Ssel_a, *L_a, *Ssel_b, *L_b;
+  double *part, *mag_a, *mag_b, *red;
+  int groups;
+};
+
+static void plan_circ_big(Workspace& ws, BigCircPlan& p, int n, int k) {
+  plan_big_fft(ws, p.f, n);
+  p.W1 = ws.take<double2>((size_t)n * n);
+  p.W2 = ws.take<double2>((size_t)n * n);
+  const size_t kn = (size_t)std::max(k, 1) * n;
+  p.Ssel_a = ws.take<double2>(kn);
+  p.L_a = ws.take<double2>(kn);
+  p.Ssel_b = ws.take<double2>(kn);
+  p.L_b = ws.take<double2>(kn);
+  p.groups = 64;
+  p.part = ws.take<double>((size_t)p.groups * n);
+  p.mag_a = ws.take<double>(n);
+  p.mag_b = ws.take<double>(n);
+  p.red = ws.take<double>(4 * kNumSMs + 64);
+}
+
+// S^T (unnormalised, in W2) and the magnitudes of X's circulant spectrum
+template <typename T>
+static int big_decompose(const T* X, int n, const BigCircPlan& p, double* mag, cudaStream_t st) {
+  T* skew = reinterpret_cast<T*>(p.W2);  // scratch until pass 2 overwrites it
+  circ_skew_kernel<T><<<dim3((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32)), 256, 0, st>>>(X, n, skew);
+  APX_LAUNCH_CHECK();
+  APX_TRY(big_fft_rows<T>(p.f, skew, p.W1, p.W2, n, false, 1.0, st));
+  const int rpc = (int)ceil_div(n, p.groups);
+  colsum_abs2_kernel<<<dim3((unsigned)ceil_div(n, 256), (unsigned)ceil_div(n, rpc)), 256, 0, st>>>(
+      p.W2, n, rpc, 1.0 / ((double)n * n), p.part);
+  APX_LAUNCH_CHECK();
+  mag_finalize_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(p.part, (int)ceil_div(n, rpc), n, mag);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+// Ssel = selected rows of S (= columns of S^T / n), L = fft(Ssel)
+static int big_spectra(int n, const BigCircPlan& p, const int* sel, int k, double2* Ssel, double2* L, cudaStream_t st) {
+  if (k <= 0) return OK;
+  gather_cols_kernel<<<dim3((unsigned)std::min<int64_t>(ceil_div(n, 256), 64), (unsigned)k), 256, 0, st>>>(
+      p.W2, n, sel, 1.0 / n, Ssel);
+  APX_LAUNCH_CHECK();
+  return big_fft_rows<double2>(p.f, Ssel, p.W1, L, k, false, 1.0, st);
+}
+
+template <typename T>
+static int run_circulant_big(const T* A, const T* B, int n, int k, int order, const int* fa, const int* fb, double2* M,
+                             int* sa, int* sb, double* scal, const BigCircPlan& p, cudaStream_t st) {
+  stage_mark(0, st);
+  APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
+  APX_TRY(big_fft_init(p.f, st));
+  const double rs = 1.0 / sqrt((double)n);
+  const dim3 rows_grid((unsigned)std::min<int64_t>(ceil_div(n, 256), 16), (unsigned)n);
+  APX_TRY(big_decompose<T>(A, n, p, p.mag_a, st));
+  if (fa) { if (k) APX_CUDA(cudaMemcpyAsync(sa, fa, k * sizeof(int), cudaMemcpyDeviceToDevice, st)); }
+  else APX_TRY(launch_topk(p.mag_a, n, k, sa, st));
+  APX_TRY(launch_kept_energy(p.mag_a, sa, k, (double)n, scal + APX_S_KEPT_A, st));
+  APX_TRY(big_spectra(n, p, sa, k, p.Ssel_a, p.L_a, st));
+  APX_TRY(big_decompose<T>(B, n, p, p.mag_b, st));
+  if (fb) { if (k) APX_CUDA(cudaMemcpyAsync(sb, fb, k * sizeof(int), cudaMemcpyDeviceToDevice, st)); }
+  else APX_TRY(launch_topk(p.mag_b, n, k, sb, st));
+  APX_TRY(launch_kept_energy(p.mag_b, sb, k, (double)n, scal + APX_S_KEPT_B, st));
+  APX_TRY(big_spectra(n, p, sb, k, p.Ssel_b, p.L_b, st));
+  stage_mark(1, st);
+  // term1 = Ahat . B, column-local: columns of B as rows of W1, FFT, gather with L_A, inverse FFT
+  const dim3 tgrid((unsigned)(n / 32), (unsigned)(n / 32));
+  transpose_to_c_kernel<T><<<tgrid, 256, 0, st>>>(B, n, p.W1);
+  APX_LAUNCH_CHECK();
+  APX_TRY(big_fft_rows<double2>(p.f, p.W1, p.W1, p.W2, n, false, 1.0, st));
+  big_left_gather_kernel<<<rows_grid, 256, 0, st>>>(p.W2, n, p.L_a, sa, k, rs, p.W1);
+  APX_LAUNCH_CHECK();
+  APX_TRY(big_fft_rows<double2>(p.f, p.W1, p.W1, p.W2, n, true, 1.0, st));
+  transpose_scale_c_kernel<<<tgrid, 256, 0, st>>>(p.W2, n, rs, M);
+  APX_LAUNCH_CHECK();
+  stage_mark(2, st);
+  if (order == 1) {
+    // term2 = dA . Bhat, row-local: conj(dA) rows, FFT, gather with conj(L_B), inverse FFT, conj
+    big_dA_kernel<T><<<rows_grid, 256, 0, st>>>(A, n, p.Ssel_a, sa, k, p.f.roots, p.W1);
+    APX_LAUNCH_CHECK();
+    APX_TRY(big_fft_rows<double2>(p.f, p.W1, p.W1, p.W2, n, false, 1.0, st));
+    big_right_gather_kernel<<<rows_grid, 256, 0, st>>>(p.W2, n, p.L_b, sb, k, rs, p.W1);
+    APX_LAUNCH_CHECK();
+    APX_TRY(big_fft_rows<double2>(p.f, p.W1, p.W1, p.W2, n, true, 1.0, st));
+    acc_conj_kernel<<<kNumSMs * 8, 256, 0, st>>>(p.W2, (size_t)n * n, rs, M);
+    APX_LAUNCH_CHECK();
+  }
+  stage_mark(3, st);
+  int parts = 0;
+  APX_TRY(launch_sumsq<double>(reinterpret_cast<const double*>(M), (size_t)2 * n * n, p.red, &parts, st));
+  APX_TRY(launch_sum_vector(p.red, parts, scal + APX_S_FRO2_M, st));
+  const size_t nel = (size_t)n * n * (sizeof(T) / sizeof(double));
+  APX_TRY(launch_sumsq<double>(reinterpret_cast<const double*>(A), nel, p.red, &parts, st));
+  APX_TRY(launch_sum_vector(p.red, parts, scal + APX_S_FRO2_A, st));
+  APX_TRY(launch_sumsq<double>(reinterpret_cast<const double*>(B), nel, p.red, &parts, st));
+  APX_TRY(launch_sum_vector(p.red, parts, scal + APX_S_FRO2_B, st));
+  stage_mark(4, st);
+  return OK;
+}
+
 }  // namespace apx
 
 using namespace apx;
@@ -636,6 +1035,11 @@ size_t apx_circulant_first_order_workspace(int dtype, int64_t n, int k, int orde
   (void)dtype;
   (void)order;
   Workspace ws(nullptr, 0, true);
+  if (!circ_fused_fits((int)n, k) && big_fft_ok(n)) {
+    BigCircPlan b;
+    plan_circ_big(ws, b, (int)n, k);
+    return ws.off;
+  }
   CircPlan p;
   plan_circ(ws, p, (int)n, k, false);
   return ws.off;
@@ -645,12 +1049,23 @@ int apx_circulant_first_order(int dtype, const void* A, const void* B, int64_t n
                               const int32_t* force_sel_a, const int32_t* force_sel_b, void* M, int32_t* sel_a,
                               int32_t* sel_b, double* scalars, void* wsp, size_t ws_bytes, void* stream) {
   APX_REQUIRE(dtype == F64 || dtype == C128, "circulant product: fp64 or complex128 inputs");
-  APX_REQUIRE(n >= 1 && fft_smem_bytes((int)n, 2) + (size_t)2 * std::max(k, 0) * sizeof(int) <= 227 * 1024,
-              "n=%lld exceeds the shared-memory transforms",
-              (long long)n);
   APX_REQUIRE(k >= 0 && k <= n, "k=%d out of range [0, %lld]", k, (long long)n);
   APX_REQUIRE(order == 0 || order == 1, "order must be 0 or 1");
+  APX_REQUIRE(n >= 1 && (circ_fused_fits((int)n, k) || big_fft_ok(n)),
+              "n=%lld: beyond the shared-memory transforms only powers of two up to 2^18 are supported",
+              (long long)n);
   Workspace ws(wsp, ws_bytes);
+  if (!circ_fused_fits((int)n, k)) {
+    BigCircPlan b;
+    plan_circ_big(ws, b, (int)n, k);
+    APX_WS_CHECK(ws);
+    cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+    if (dtype == F64)
+      return run_circulant_big<double>((const double*)A, (const double*)B, (int)n, k, order, force_sel_a, force_sel_b,
+                                       (double2*)M, sel_a, sel_b, scalars, b, st);
+    return run_circulant_big<double2>((const double2*)A, (const double2*)B, (int)n, k, order, force_sel_a,
+                                      force_sel_b, (double2*)M, sel_a, sel_b, scalars, b, st);
+  }
   CircPlan p;
   plan_circ(ws, p, (int)n, k, false);
   APX_WS_CHECK(ws);
@@ -662,8 +1077,17 @@ int apx_circulant_first_order(int dtype, const void* A, const void* B, int64_t n
                                 (double2*)M, sel_a, sel_b, scalars, p, st);
 }
 
+static bool decompose_fits(int64_t n) {
+  return !force_big(n) && fft_smem_bytes((int)n, 1) + (size_t)n * 8 <= 227 * 1024;
+}
+
 size_t apx_circulant_decompose_workspace(int dtype, int64_t n) {
   Workspace ws(nullptr, 0, true);
+  if (!decompose_fits(n) && big_fft_ok(n)) {
+    BigCircPlan b;
+    plan_circ_big(ws, b, (int)n, 0);
+    return ws.off;
+  }
   ws.take<double2>(n);
   ws.take<double>((size_t)ceil_div(n, std::max(1, (int)ceil_div(n, 2 * kNumSMs))) * n);
   ws.take<double2>((size_t)n * n);                                  // S^T
@@ -674,10 +1098,23 @@ size_t apx_circulant_decompose_workspace(int dtype, int64_t n) {
 int apx_circulant_decompose(int dtype, const void* A, int64_t n, void* columns, double* magnitudes, void* wsp,
                             size_t ws_bytes, void* stream) {
   APX_REQUIRE(dtype == F64 || dtype == C128, "circulant_decompose: fp64 or complex128 input");
-  APX_REQUIRE(n >= 1 && fft_smem_bytes((int)n, 1) + (size_t)n * 8 <= 227 * 1024,
-              "n=%lld exceeds the shared-memory transforms", (long long)n);
+  APX_REQUIRE(n >= 1 && (decompose_fits(n) || big_fft_ok(n)),
+              "n=%lld: beyond the shared-memory transforms only powers of two up to 2^18 are supported",
+              (long long)n);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Workspace ws(wsp, ws_bytes);
+  if (!decompose_fits(n)) {
+    BigCircPlan b;
+    plan_circ_big(ws, b, (int)n, 0);
+    APX_WS_CHECK(ws);
+    APX_TRY(big_fft_init(b.f, st));
+    if (dtype == F64) APX_TRY(big_decompose<double>((const double*)A, (int)n, b, magnitudes, st));
+    else APX_TRY(big_decompose<double2>((const double2*)A, (int)n, b, magnitudes, st));
+    transpose_scale_c_kernel<<<dim3((unsigned)(n / 32), (unsigned)(n / 32)), 256, 0, st>>>(b.W2, (int)n, 1.0 / n,
+                                                                                           (double2*)columns);
+    APX_LAUNCH_CHECK();
+    return OK;
+  }
   CircPlan p{};
   p.cpc = std::max(1, (int)ceil_div(n, 2 * kNumSMs));
   p.parts = (int)ceil_div(n, p.cpc);
@@ -733,8 +1170,32 @@ int apx_circulant_component(int dtype, const void* A, int64_t n, int kk, void* o
   return OK;
 }
 
-size_t apx_unitary_dft_workspace(int64_t n) {
+static bool dft_fits(int64_t n) { return !force_big(n) && fft_smem_bytes((int)n, 1) <= 227 * 1024; }
+
+__global__ void strided_to_rows_kernel(const double2* __restrict__ x, int64_t stride, int64_t dist, int n,
+                                       size_t count, double2* __restrict__ rows) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < count; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = e / n, i = e - b * n;
+    rows[e] = x[b * dist + i * stride];
+  }
+}
+__global__ void rows_to_strided_kernel(const double2* __restrict__ rows, int64_t stride, int64_t dist, int n,
+                                       size_t count, double2* __restrict__ y) {
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < count; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t b = e / n, i = e - b * n;
+    y[b * dist + i * stride] = rows[e];
+  }
+}
+
+size_t apx_unitary_dft_workspace(int64_t n, int64_t batch) {
   Workspace ws(nullptr, 0, true);
+  if (!dft_fits(n) && big_fft_ok(n)) {
+    BigFFT f;
+    plan_big_fft(ws, f, (int)n);
+    ws.take<double2>((size_t)std::max<int64_t>(batch, 1) * n);
+    ws.take<double2>((size_t)std::max<int64_t>(batch, 1) * n);
+    return ws.off;
+  }
   ws.take<double2>(n);
   return ws.off;
 }
@@ -744,10 +1205,40 @@ size_t apx_unitary_dft_workspace(int64_t n) {
 int apx_unitary_dft(const void* x, void* y, int64_t n, int64_t batch, int64_t stride, int64_t dist, int inverse,
                     void* wsp, size_t ws_bytes, void* stream) {
   APX_REQUIRE(n >= 1, "transform length must be >= 1");
-  APX_REQUIRE(fft_smem_bytes((int)n, 1) <= 227 * 1024, "transform length %lld exceeds the shared-memory DFT",
+  APX_REQUIRE(dft_fits(n) || big_fft_ok(n),
+              "transform length %lld: beyond shared memory only powers of two up to 2^18 are supported",
               (long long)n);
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Workspace ws(wsp, ws_bytes);
+  if (!dft_fits(n)) {
+    BigFFT f;
+    plan_big_fft(ws, f, (int)n);
+    double2* t1 = ws.take<double2>((size_t)std::max<int64_t>(batch, 1) * n);
+    double2* t2 = ws.take<double2>((size_t)std::max<int64_t>(batch, 1) * n);
+    APX_WS_CHECK(ws);
+    if (batch == 0) return OK;
+    APX_TRY(big_fft_init(f, st));
+    const size_t count = (size_t)batch * n;
+    const unsigned blocks = (unsigned)std::min<int64_t>(ceil_div((int64_t)count, 256), kNumSMs * 16);
+    const double2* src = (const double2*)x;
+    const bool contiguous = stride == 1 && dist == n;
+    if (!contiguous) {
+      strided_to_rows_kernel<<<blocks, 256, 0, st>>>(src, stride, dist, (int)n, count, t2);
+      APX_LAUNCH_CHECK();
+      src = t2;
+    }
+    for (int64_t b0 = 0; b0 < batch; b0 += 65535) {
+      const int rows = (int)std::min<int64_t>(65535, batch - b0);
+      double2* outp = contiguous ? (double2*)y + b0 * n : t2 + b0 * n;
+      APX_TRY(big_fft_rows<double2>(f, src + b0 * n, t1 + b0 * n, outp, rows, inverse != 0, 1.0 / sqrt((double)n),
+                                    st));
+    }
+    if (!contiguous) {
+      rows_to_strided_kernel<<<blocks, 256, 0, st>>>(t2, stride, dist, (int)n, count, (double2*)y);
+      APX_LAUNCH_CHECK();
+    }
+    return OK;
+  }
   double2* roots = ws.take<double2>(n);
   APX_WS_CHECK(ws);
   if (batch == 0) return OK;

@@ -107,7 +107,7 @@ static unsigned grid_for(size_t cnt) { return (unsigned)std::min<int64_t>(ceil_d
 
 using namespace apx;
 
-extern "C" size_t apx_unitary_dft_workspace(int64_t n);
+extern "C" size_t apx_unitary_dft_workspace(int64_t n, int64_t batch);
 extern "C" int apx_unitary_dft(const void* x, void* y, int64_t n, int64_t batch, int64_t stride, int64_t dist,
                                int inverse, void* wsp, size_t ws_bytes, void* stream);
 
@@ -141,7 +141,7 @@ static void plan_sfft(Workspace& ws, SfftPlan& p, int m, int n, int q, int k) {
   p.mim = ws.take<double>(mq);
   p.sa = ws.take<int>((size_t)m * std::max(k, 1));
   p.sb = ws.take<int>((size_t)std::max(n, q) * std::max(k, 1));
-  p.dft_bytes = apx_unitary_dft_workspace(std::max(n, 1));
+  p.dft_bytes = apx_unitary_dft_workspace(std::max(n, 1), std::max(m, q));
   p.dft_ws = ws.take<char>(p.dft_bytes);
   p.gcap = 8 * std::max(mq, (size_t)1);
   p.gpart = ws.take<double>(p.gcap);

@@ -1,0 +1,101 @@
+"""Transforms longer than one CTA's shared memory: the four-step path of circulant.cu (batched
+FFT through global memory, unfused circulant stages) for power-of-two n up to 2^18.
+
+  * unitary_dft at n = 16384 / 65536 (contiguous and strided batches) against numpy's FFT;
+  * with APX_FFT_BIG=1 (a child process: the switch is read once) the four-step path runs at
+    small n and must reproduce the fused shared-memory path and the CPU oracle;
+  * the C3-style circulant product at n = 8192 (too large for the fused kernels) against the
+    CPU oracle, with the near-tie protocol of SURVEY §8(c).
+Tolerance: 1e-10 relative Frobenius (fp64), as everywhere on the circulant path.
+"""
+import os
+import subprocess
+import sys
+
+import numpy as np
+import pytest
+
+import oracle as O
+from conftest import rel
+
+pytestmark = pytest.mark.gpu
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+
+
+@pytest.mark.parametrize("n", [16384, 65536])
+def test_unitary_dft_long(n):
+    from paper_2504_19308_b200 import core as K
+    rng = np.random.default_rng(n)
+    x = rng.standard_normal((3, n)) + 1j * rng.standard_normal((3, n))
+    for direction, f in (("forward", np.fft.fft), ("inverse", np.fft.ifft)):
+        y = K.unitary_dft(x, direction, axis=-1)
+        assert rel(y, f(x, axis=-1, norm="ortho")) < 1e-12
+    xt = np.ascontiguousarray(x.T)  # strided: transform along axis 0
+    assert rel(K.unitary_dft(xt, "forward", axis=0), np.fft.fft(xt, axis=0, norm="ortho")) < 1e-12
+
+
+_CHILD = r"""
+import sys, numpy as np
+sys.path.insert(0, sys.argv[1])
+import oracle as O
+import paper_2504_19308_b200 as P
+from paper_2504_19308_b200 import circulant as C
+out = {}
+for n, k in ((256, 5), (1024, 5)):
+    A = O.gen_circulant_operand(n, 6, 11 + n)
+    B = O.gen_circulant_operand(n, 6, 12 + n)
+    for order in (0, 1):
+        M, rep = C.circulant_first_order_multiply(A, B, k, order)
+        out[f"M{n}_{order}"] = M
+        out[f"sel{n}_{order}"] = np.array(rep.selected_a + rep.selected_b)
+    spec = C.circulant_decompose(A)
+    out[f"cols{n}"] = spec.columns
+    out[f"mags{n}"] = spec.magnitudes
+    x = np.random.default_rng(n).standard_normal((4, n)) + 0j
+    out[f"dft{n}"] = P.unitary_dft(x, "forward", axis=-1)
+np.savez(sys.argv[2], **out)
+"""
+
+
+def _run_child(tmp_path, big):
+    path = str(tmp_path / f"child_{int(big)}.npz")
+    env = dict(os.environ)
+    env["APX_FFT_BIG"] = "1" if big else "0"
+    r = subprocess.run([sys.executable, "-c", _CHILD, ROOT, path], env=env, capture_output=True, text=True,
+                       timeout=600)
+    assert r.returncode == 0, r.stderr[-2000:]
+    with np.load(path) as z:
+        return {k: z[k] for k in z.files}
+
+
+def test_four_step_path_matches_fused_and_oracle(tmp_path):
+    big = _run_child(tmp_path, True)
+    fused = _run_child(tmp_path, False)
+    for key in big:
+        if key.startswith("sel"):
+            assert np.array_equal(big[key], fused[key]), key
+        else:
+            assert rel(big[key], fused[key]) < 1e-12, key
+    for n, k in ((256, 5), (1024, 5)):  # k below the 6 planted components: no near ties
+        A = O.gen_circulant_operand(n, 6, 11 + n)
+        B = O.gen_circulant_operand(n, 6, 12 + n)
+        for order in (0, 1):
+            Mo, ro = O.circulant_first_order_multiply(A, B, k, order)
+            assert list(big[f"sel{n}_{order}"]) == list(ro["selected_a"]) + list(ro["selected_b"])
+            assert rel(big[f"M{n}_{order}"], Mo) < 1e-10
+        S, mags = O.circulant_decompose(A)
+        assert rel(big[f"cols{n}"], S) < 1e-12
+        assert rel(big[f"mags{n}"], mags) < 1e-12
+
+
+def test_circulant_n8192_vs_oracle():
+    from paper_2504_19308_b200 import circulant as C
+    n, k = 8192, 16
+    A = O.gen_circulant_operand(n, 16, 5)
+    B = O.gen_circulant_operand(n, 16, 6)
+    M, rep = C.circulant_first_order_multiply(A, B, k, 1)
+    Mo, ro = O.circulant_first_order_multiply(A, B, k, 1)
+    assert rep.selected_a == list(ro["selected_a"]) and rep.selected_b == list(ro["selected_b"])
+    err = rel(M, Mo)
+    print(f"circulant n=8192 (four-step path): rel vs oracle {err:.3e}")
+    assert err < 1e-10
