@@ -652,9 +652,11 @@ __global__ void __launch_bounds__(256) transpose_to_c_kernel(const TI* __restric
   __shared__ double2 tile[32][33];
   const int c0 = blockIdx.x * 32, p0 = blockIdx.y * 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int r = w; r < 32; r += 8) tile[r][lane] = ld_c<TI>(in, (size_t)(p0 + r) * n + c0 + lane);
+  for (int r = w; r < 32; r += 8)
+    if (p0 + r < n && c0 + lane < n) tile[r][lane] = ld_c<TI>(in, (size_t)(p0 + r) * n + c0 + lane);
   __syncthreads();
-  for (int r = w; r < 32; r += 8) out[(size_t)(c0 + r) * n + p0 + lane] = tile[lane][r];
+  for (int r = w; r < 32; r += 8)
+    if (c0 + r < n && p0 + lane < n) out[(size_t)(c0 + r) * n + p0 + lane] = tile[lane][r];
 }
 
 // M[p][c] = scale * Y[c][p]
@@ -663,9 +665,11 @@ __global__ void __launch_bounds__(256) transpose_scale_c_kernel(const double2* _
   __shared__ double2 tile[32][33];
   const int p0 = blockIdx.x * 32, c0 = blockIdx.y * 32;
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  for (int r = w; r < 32; r += 8) tile[r][lane] = Y[(size_t)(c0 + r) * n + p0 + lane];
+  for (int r = w; r < 32; r += 8)
+    if (c0 + r < n && p0 + lane < n) tile[r][lane] = Y[(size_t)(c0 + r) * n + p0 + lane];
   __syncthreads();
-  for (int r = w; r < 32; r += 8) M[(size_t)(p0 + r) * n + c0 + lane] = cscale(tile[lane][r], scale);
+  for (int r = w; r < 32; r += 8)
+    if (p0 + r < n && c0 + lane < n) M[(size_t)(p0 + r) * n + c0 + lane] = cscale(tile[lane][r], scale);
 }
 
 // magnitudes: partial[g][t] = sum over rows j of chunk g of |St[j][t]|^2 * s2; then mag[t] = sqrt(sum_g)
@@ -704,7 +708,8 @@ __global__ void __launch_bounds__(256) big_left_gather_kernel(const double2* __r
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
     double2 a = make_double2(0.0, 0.0);
     for (int q = 0; q < k; ++q) {
-      const int src = (p - s_sel[q]) & (n - 1);
+      int src = p - s_sel[q];
+      if (src < 0) src += n;
       a = cadd(a, cmul(__ldg(L + (size_t)q * n + p), cscale(__ldg(fb + src), rs)));
     }
     Y[c * n + p] = a;
@@ -722,7 +727,8 @@ __global__ void __launch_bounds__(256) big_dA_kernel(const T* __restrict__ A, in
   const int* s_sel = k <= 512 ? s_buf : sel;
   const size_t r = blockIdx.y;
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
-    const int d = ((int)r - c) & (n - 1);
+    int d = (int)r - c;
+    if (d < 0) d += n;
     double2 ah = make_double2(0.0, 0.0);
     for (int q = 0; q < k; ++q)
       ah = cadd(ah, cmul(__ldg(Ssel + (size_t)q * n + d), cconj(__ldg(roots + mulmod_n(s_sel[q], c, n)))));
@@ -743,7 +749,8 @@ __global__ void __launch_bounds__(256) big_right_gather_kernel(const double2* __
   for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
     double2 a = make_double2(0.0, 0.0);
     for (int q = 0; q < k; ++q) {
-      const int src = (p + s_sel[q]) & (n - 1);
+      int src = p + s_sel[q];
+      if (src >= n) src -= n;
       a = cadd(a, cmulc(cscale(__ldg(xr + src), rs), __ldg(L + (size_t)q * n + src)));
     }
     Y[r * n + p] = a;
@@ -868,9 +875,19 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
 }
 
 
-// ---- big path (power-of-two n whose two-buffer transforms exceed shared memory) ----------------
-static bool big_fft_ok(int64_t n) { return n >= 256 && is_pow2((int)n) && n <= (1 << 18); }
-// APX_FFT_BIG=1 routes every eligible length through the four-step path (tests compare the two)
+// ---- big path: transforms whose buffers exceed shared memory ---------------------------------------
+// Powers of two run the four-step transform directly; other lengths go through Bluestein's
+// identity jk = (j^2 + k^2 - (k-j)^2) / 2: X[k] = w[k] sum_j (x[j] w[j]) conj(w[k-j]),
+// w[m] = exp(-pi i m^2 / n), a cyclic convolution of length L = 2^ceil(log2(2n-1)) evaluated with
+// two four-step transforms of length L and the precomputed transform of the conjugate chirp.
+static int next_pow2(int64_t v) {
+  int64_t p = 1;
+  while (p < v) p <<= 1;
+  return (int)p;
+}
+static int big_len(int64_t n) { return is_pow2((int)n) ? (int)n : next_pow2(2 * n - 1); }
+static bool big_fft_ok(int64_t n) { return n >= 256 && n <= 46340 * 2 && big_len(n) <= (1 << 18); }
+// APX_FFT_BIG=1 routes every eligible length through this path (tests compare it with the fused one)
 static bool force_big(int64_t n) {
   static const bool on = [] {
     const char* e = getenv("APX_FFT_BIG");
@@ -883,55 +900,160 @@ static bool circ_fused_fits(int n, int k) {
 }
 
 struct BigFFT {
-  int n, n1, n2;
-  double2 *roots, *roots1, *roots2;
+  int n, L, n1, n2;  // transform length; four-step length L = n1 * n2 (n itself for powers of two)
+  bool blue;
+  int chunk;         // Bluestein: rows per pass through t1 / t2
+  double2 *roots, *roots1, *roots2, *chirp, *bf, *t1, *t2;
 };
 
-static void plan_big_fft(Workspace& ws, BigFFT& f, int n) {
-  const int l = ilog2(n);
+static void plan_big_fft(Workspace& ws, BigFFT& f, int n, int max_rows) {
   f.n = n;
+  f.blue = !is_pow2(n);
+  f.L = big_len(n);
+  const int l = ilog2(f.L);
   f.n1 = 1 << (l / 2);
   f.n2 = 1 << (l - l / 2);
-  f.roots = ws.take<double2>(n);
+  f.roots = ws.take<double2>(f.L);
   f.roots1 = ws.take<double2>(f.n1);
   f.roots2 = ws.take<double2>(f.n2);
+  f.chunk = 0;
+  f.chirp = f.bf = f.t1 = f.t2 = nullptr;
+  if (f.blue) {
+    f.chunk = (int)std::max<int64_t>(1, std::min<int64_t>(std::max(max_rows, 1), (int64_t)(1 << 26) / f.L));
+    f.chirp = ws.take<double2>(n);
+    f.bf = ws.take<double2>(f.L);
+    f.t1 = ws.take<double2>((size_t)f.chunk * f.L);
+    f.t2 = ws.take<double2>((size_t)f.chunk * f.L);
+  }
 }
 
-static int big_fft_init(const BigFFT& f, cudaStream_t st) {
-  launch_roots(f.roots, f.n, st);
-  launch_roots(f.roots1, f.n1, st);
-  launch_roots(f.roots2, f.n2, st);
-  APX_LAUNCH_CHECK();
+__global__ void chirp_kernel(double2* w, int n) {
+  for (int m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x) {
+    const long long q = ((long long)m * m) % (2LL * n);  // exact: the angle pi m^2 / n mod 2 pi
+    double sn, cs;
+    sincospi((double)q / (double)n, &sn, &cs);
+    w[m] = make_double2(cs, -sn);  // exp(-pi i m^2 / n)
+  }
+}
+
+// b[m] = conj(w[|m|]) on the cyclic index set of length L (zero between n and L - n)
+__global__ void chirp_conv_kernel(const double2* __restrict__ w, int n, int L, double2* __restrict__ b) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < L; i += gridDim.x * blockDim.x) {
+    double2 v = make_double2(0.0, 0.0);
+    if (i < n) v = cconj(w[i]);
+    else if (i > L - n) v = cconj(w[L - i]);
+    b[i] = v;
+  }
+}
+
+// a[r][j] = (conj if inverse)(x[r][j]) * w[j] for j < n, 0 up to L
+template <typename TI>
+__global__ void chirp_pre_kernel(const TI* __restrict__ x, int n, int L, int rows, const double2* __restrict__ w,
+                                 int inverse, double2* __restrict__ a) {
+  const size_t total = (size_t)rows * L;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = e / L;
+    const int j = (int)(e - r * L);
+    double2 v = make_double2(0.0, 0.0);
+    if (j < n) {
+      double2 xv = ld_c<TI>(x, r * n + j);
+      if (inverse) xv = cconj(xv);
+      v = cmul(xv, w[j]);
+    }
+    a[e] = v;
+  }
+}
+
+__global__ void rows_mul_kernel(double2* __restrict__ a, int L, int rows, const double2* __restrict__ bf) {
+  const size_t total = (size_t)rows * L;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x)
+    a[e] = cmul(a[e], __ldg(bf + (e % L)));
+}
+
+// out[r][k] = scale * (conj if inverse)(w[k] * c[r][k]), k < n
+__global__ void chirp_post_kernel(const double2* __restrict__ c, int n, int L, int rows,
+                                  const double2* __restrict__ w, int inverse, double scale,
+                                  double2* __restrict__ out) {
+  const size_t total = (size_t)rows * n;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = e / n;
+    const int k = (int)(e - r * n);
+    double2 v = cmul(w[k], c[r * L + k]);
+    if (inverse) v = cconj(v);
+    out[e] = cscale(v, scale);
+  }
+}
+
+// the four-step transform of `rows` power-of-two sequences of length f.L
+template <typename TI>
+static int four_step_rows(const BigFFT& f, const TI* in, double2* data, double2* out, int rows, bool inverse,
+                          double scale, cudaStream_t st) {
+  const size_t s1 = (size_t)kBigTile * f.n1 * sizeof(double2), s2 = (size_t)kBigTile * f.n2 * sizeof(double2);
+  APX_CUDA(cudaFuncSetAttribute(fft4_pass1_kernel<TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
+  APX_CUDA(cudaFuncSetAttribute(fft4_pass2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
+  const size_t L = (size_t)f.L;
+  for (int r0 = 0; r0 < rows; r0 += 65535) {
+    const int rr = std::min(65535, rows - r0);
+    fft4_pass1_kernel<TI><<<dim3((unsigned)(f.n2 / kBigTile), (unsigned)rr), 512, s1, st>>>(
+        in + r0 * L, f.n1, f.n2, inverse ? 1 : 0, f.roots, f.roots1, data + r0 * L);
+    APX_LAUNCH_CHECK();
+    fft4_pass2_kernel<<<dim3((unsigned)(f.n1 / kBigTile), (unsigned)rr), 512, s2, st>>>(
+        data + r0 * L, f.n1, f.n2, inverse ? 1 : 0, f.roots2, scale, out + r0 * L);
+    APX_LAUNCH_CHECK();
+  }
   return OK;
 }
 
-// rows x n: in (TI) -> out (complex) via `data` (complex, may alias `in` but not `out`)
+static int big_fft_init(const BigFFT& f, cudaStream_t st) {
+  launch_roots(f.roots, f.L, st);
+  launch_roots(f.roots1, f.n1, st);
+  launch_roots(f.roots2, f.n2, st);
+  APX_LAUNCH_CHECK();
+  if (f.blue) {
+    const unsigned g = (unsigned)std::min<int64_t>(ceil_div(f.L, 256), 1024);
+    chirp_kernel<<<g, 256, 0, st>>>(f.chirp, f.n);
+    APX_LAUNCH_CHECK();
+    chirp_conv_kernel<<<g, 256, 0, st>>>(f.chirp, f.n, f.L, f.t1);
+    APX_LAUNCH_CHECK();
+    APX_TRY(four_step_rows<double2>(f, f.t1, f.t1, f.bf, 1, false, 1.0, st));
+  }
+  return OK;
+}
+
+// rows x n: in (TI) -> out (complex) via `data` (complex, may alias `in` but not `out`); scale
+// multiplies the result
 template <typename TI>
 static int big_fft_rows(const BigFFT& f, const TI* in, double2* data, double2* out, int rows, bool inverse,
                         double scale, cudaStream_t st) {
   if (rows <= 0) return OK;
-  APX_REQUIRE(rows <= 65535, "big FFT: %d rows per launch", rows);
-  const size_t s1 = (size_t)kBigTile * f.n1 * sizeof(double2), s2 = (size_t)kBigTile * f.n2 * sizeof(double2);
-  APX_CUDA(cudaFuncSetAttribute(fft4_pass1_kernel<TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
-  APX_CUDA(cudaFuncSetAttribute(fft4_pass2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
-  fft4_pass1_kernel<TI><<<dim3((unsigned)(f.n2 / kBigTile), (unsigned)rows), 512, s1, st>>>(
-      in, f.n1, f.n2, inverse ? 1 : 0, f.roots, f.roots1, data);
-  APX_LAUNCH_CHECK();
-  fft4_pass2_kernel<<<dim3((unsigned)(f.n1 / kBigTile), (unsigned)rows), 512, s2, st>>>(
-      data, f.n1, f.n2, inverse ? 1 : 0, f.roots2, scale, out);
-  APX_LAUNCH_CHECK();
+  if (!f.blue) return four_step_rows<TI>(f, in, data, out, rows, inverse, scale, st);
+  const size_t n = (size_t)f.n;
+  for (int r0 = 0; r0 < rows; r0 += f.chunk) {
+    const int rr = std::min(f.chunk, rows - r0);
+    const unsigned g = (unsigned)std::min<int64_t>(ceil_div((int64_t)rr * f.L, 256), kNumSMs * 16);
+    chirp_pre_kernel<TI><<<g, 256, 0, st>>>(in + r0 * n, f.n, f.L, rr, f.chirp, inverse ? 1 : 0, f.t1);
+    APX_LAUNCH_CHECK();
+    APX_TRY(four_step_rows<double2>(f, f.t1, f.t1, f.t2, rr, false, 1.0, st));
+    rows_mul_kernel<<<g, 256, 0, st>>>(f.t2, f.L, rr, f.bf);
+    APX_LAUNCH_CHECK();
+    APX_TRY(four_step_rows<double2>(f, f.t2, f.t2, f.t1, rr, true, 1.0 / f.L, st));
+    chirp_post_kernel<<<g, 256, 0, st>>>(f.t1, f.n, f.L, rr, f.chirp, inverse ? 1 : 0, scale, out + r0 * n);
+    APX_LAUNCH_CHECK();
+  }
   return OK;
 }
 
 struct BigCircPlan {
   BigFFT f;
+  double2* rootsn;  // exp(-2 pi i k / n): the on-the-fly Ahat (f.roots is for the length-L transforms)
   double2 *W1, *W2, *Ssel_a, *L_a, *Ssel_b, *L_b;
   double *part, *mag_a, *mag_b, *red;
   int groups;
 };
 
 static void plan_circ_big(Workspace& ws, BigCircPlan& p, int n, int k) {
-  plan_big_fft(ws, p.f, n);
+  plan_big_fft(ws, p.f, n, n);
+  p.rootsn = ws.take<double2>(n);
   p.W1 = ws.take<double2>((size_t)n * n);
   p.W2 = ws.take<double2>((size_t)n * n);
   const size_t kn = (size_t)std::max(k, 1) * n;
@@ -949,7 +1071,9 @@ static void plan_circ_big(Workspace& ws, BigCircPlan& p, int n, int k) {
 // S^T (unnormalised, in W2) and the magnitudes of X's circulant spectrum
 template <typename T>
 static int big_decompose(const T* X, int n, const BigCircPlan& p, double* mag, cudaStream_t st) {
-  T* skew = reinterpret_cast<T*>(p.W2);  // scratch until pass 2 overwrites it
+  // the skewed copy: in W2 for the four-step path (pass 1 consumes it before pass 2 writes W2);
+  // in W1 for Bluestein, which writes its output rows chunk by chunk while later rows are unread
+  T* skew = reinterpret_cast<T*>(p.f.blue ? p.W1 : p.W2);
   circ_skew_kernel<T><<<dim3((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32)), 256, 0, st>>>(X, n, skew);
   APX_LAUNCH_CHECK();
   APX_TRY(big_fft_rows<T>(p.f, skew, p.W1, p.W2, n, false, 1.0, st));
@@ -977,6 +1101,8 @@ static int run_circulant_big(const T* A, const T* B, int n, int k, int order, co
   stage_mark(0, st);
   APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
   APX_TRY(big_fft_init(p.f, st));
+  launch_roots(p.rootsn, n, st);
+  APX_LAUNCH_CHECK();
   const double rs = 1.0 / sqrt((double)n);
   const dim3 rows_grid((unsigned)std::min<int64_t>(ceil_div(n, 256), 16), (unsigned)n);
   APX_TRY(big_decompose<T>(A, n, p, p.mag_a, st));
@@ -991,7 +1117,7 @@ static int run_circulant_big(const T* A, const T* B, int n, int k, int order, co
   APX_TRY(big_spectra(n, p, sb, k, p.Ssel_b, p.L_b, st));
   stage_mark(1, st);
   // term1 = Ahat . B, column-local: columns of B as rows of W1, FFT, gather with L_A, inverse FFT
-  const dim3 tgrid((unsigned)(n / 32), (unsigned)(n / 32));
+  const dim3 tgrid((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32));
   transpose_to_c_kernel<T><<<tgrid, 256, 0, st>>>(B, n, p.W1);
   APX_LAUNCH_CHECK();
   APX_TRY(big_fft_rows<double2>(p.f, p.W1, p.W1, p.W2, n, false, 1.0, st));
@@ -1003,7 +1129,7 @@ static int run_circulant_big(const T* A, const T* B, int n, int k, int order, co
   stage_mark(2, st);
   if (order == 1) {
     // term2 = dA . Bhat, row-local: conj(dA) rows, FFT, gather with conj(L_B), inverse FFT, conj
-    big_dA_kernel<T><<<rows_grid, 256, 0, st>>>(A, n, p.Ssel_a, sa, k, p.f.roots, p.W1);
+    big_dA_kernel<T><<<rows_grid, 256, 0, st>>>(A, n, p.Ssel_a, sa, k, p.rootsn, p.W1);
     APX_LAUNCH_CHECK();
     APX_TRY(big_fft_rows<double2>(p.f, p.W1, p.W1, p.W2, n, false, 1.0, st));
     big_right_gather_kernel<<<rows_grid, 256, 0, st>>>(p.W2, n, p.L_b, sb, k, rs, p.W1);
@@ -1110,7 +1236,7 @@ int apx_circulant_decompose(int dtype, const void* A, int64_t n, void* columns, 
     APX_TRY(big_fft_init(b.f, st));
     if (dtype == F64) APX_TRY(big_decompose<double>((const double*)A, (int)n, b, magnitudes, st));
     else APX_TRY(big_decompose<double2>((const double2*)A, (int)n, b, magnitudes, st));
-    transpose_scale_c_kernel<<<dim3((unsigned)(n / 32), (unsigned)(n / 32)), 256, 0, st>>>(b.W2, (int)n, 1.0 / n,
+    transpose_scale_c_kernel<<<dim3((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32)), 256, 0, st>>>(b.W2, (int)n, 1.0 / n,
                                                                                            (double2*)columns);
     APX_LAUNCH_CHECK();
     return OK;
@@ -1191,7 +1317,7 @@ size_t apx_unitary_dft_workspace(int64_t n, int64_t batch) {
   Workspace ws(nullptr, 0, true);
   if (!dft_fits(n) && big_fft_ok(n)) {
     BigFFT f;
-    plan_big_fft(ws, f, (int)n);
+    plan_big_fft(ws, f, (int)n, (int)std::min<int64_t>(batch, 1 << 30));
     ws.take<double2>((size_t)std::max<int64_t>(batch, 1) * n);
     ws.take<double2>((size_t)std::max<int64_t>(batch, 1) * n);
     return ws.off;
@@ -1212,7 +1338,7 @@ int apx_unitary_dft(const void* x, void* y, int64_t n, int64_t batch, int64_t st
   Workspace ws(wsp, ws_bytes);
   if (!dft_fits(n)) {
     BigFFT f;
-    plan_big_fft(ws, f, (int)n);
+    plan_big_fft(ws, f, (int)n, (int)std::min<int64_t>(batch, 1 << 30));
     double2* t1 = ws.take<double2>((size_t)std::max<int64_t>(batch, 1) * n);
     double2* t2 = ws.take<double2>((size_t)std::max<int64_t>(batch, 1) * n);
     APX_WS_CHECK(ws);

@@ -22,7 +22,7 @@ pytestmark = pytest.mark.gpu
 ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
 
 
-@pytest.mark.parametrize("n", [16384, 65536])
+@pytest.mark.parametrize("n", [16384, 65536, 10007, 12000])
 def test_unitary_dft_long(n):
     from paper_2504_19308_b200 import core as K
     rng = np.random.default_rng(n)
@@ -34,6 +34,20 @@ def test_unitary_dft_long(n):
     assert rel(K.unitary_dft(xt, "forward", axis=0), np.fft.fft(xt, axis=0, norm="ortho")) < 1e-12
 
 
+def _oracle_with_protocol(A, B, k, order, sel_a, sel_b):
+    """SURVEY §8(c) near-tie protocol: real operands have conjugate-symmetric spectra, so the
+    magnitudes of t and n - t tie up to rounding; every differing pick must be such a near tie,
+    and the oracle is then re-run with the GPU's selections (as test_circulant.py:108-110 does)."""
+    from test_gpu_circulant import near_tie_ok
+    _, ma = O.circulant_decompose(A)
+    _, mb = O.circulant_decompose(B)
+    Mo, ro = O.circulant_first_order_multiply(A, B, k, order)
+    subs = near_tie_ok(sel_a, list(ro["selected_a"]), ma) + near_tie_ok(sel_b, list(ro["selected_b"]), mb)
+    if subs:
+        Mo, ro = O.circulant_first_order_multiply(A, B, k, order, force_sel_a=sel_a, force_sel_b=sel_b)
+    return Mo, subs
+
+
 _CHILD = r"""
 import sys, numpy as np
 sys.path.insert(0, sys.argv[1])
@@ -41,7 +55,7 @@ import oracle as O
 import paper_2504_19308_b200 as P
 from paper_2504_19308_b200 import circulant as C
 out = {}
-for n, k in ((256, 5), (1024, 5)):
+for n, k in ((256, 5), (1024, 5), (300, 5), (997, 4)):
     A = O.gen_circulant_operand(n, 6, 11 + n)
     B = O.gen_circulant_operand(n, 6, 12 + n)
     for order in (0, 1):
@@ -76,12 +90,12 @@ def test_four_step_path_matches_fused_and_oracle(tmp_path):
             assert np.array_equal(big[key], fused[key]), key
         else:
             assert rel(big[key], fused[key]) < 1e-12, key
-    for n, k in ((256, 5), (1024, 5)):  # k below the 6 planted components: no near ties
+    for n, k in ((256, 5), (1024, 5), (300, 5), (997, 4)):
         A = O.gen_circulant_operand(n, 6, 11 + n)
         B = O.gen_circulant_operand(n, 6, 12 + n)
         for order in (0, 1):
-            Mo, ro = O.circulant_first_order_multiply(A, B, k, order)
-            assert list(big[f"sel{n}_{order}"]) == list(ro["selected_a"]) + list(ro["selected_b"])
+            sel = [int(v) for v in big[f"sel{n}_{order}"]]
+            Mo, _ = _oracle_with_protocol(A, B, k, order, sel[:k], sel[k:])
             assert rel(big[f"M{n}_{order}"], Mo) < 1e-10
         S, mags = O.circulant_decompose(A)
         assert rel(big[f"cols{n}"], S) < 1e-12
@@ -94,8 +108,21 @@ def test_circulant_n8192_vs_oracle():
     A = O.gen_circulant_operand(n, 16, 5)
     B = O.gen_circulant_operand(n, 16, 6)
     M, rep = C.circulant_first_order_multiply(A, B, k, 1)
-    Mo, ro = O.circulant_first_order_multiply(A, B, k, 1)
-    assert rep.selected_a == list(ro["selected_a"]) and rep.selected_b == list(ro["selected_b"])
+    Mo, subs = _oracle_with_protocol(A, B, k, 1, rep.selected_a, rep.selected_b)
     err = rel(M, Mo)
-    print(f"circulant n=8192 (four-step path): rel vs oracle {err:.3e}")
+    print(f"circulant n=8192 (four-step path): rel vs oracle {err:.3e}, near-tie substitutions {subs}")
+    assert err < 1e-10
+
+
+def test_circulant_n5000_bluestein_vs_oracle():
+    """n = 5000: too long for the fused kernels' buffers and not a power of two -- Bluestein
+    transforms of length 16384 through the four-step path."""
+    from paper_2504_19308_b200 import circulant as C
+    n, k = 5000, 6
+    A = O.gen_circulant_operand(n, 8, 7)
+    B = O.gen_circulant_operand(n, 8, 8)
+    M, rep = C.circulant_first_order_multiply(A, B, k, 1)
+    Mo, subs = _oracle_with_protocol(A, B, k, 1, rep.selected_a, rep.selected_b)
+    err = rel(M, Mo)
+    print(f"circulant n=5000 (Bluestein): rel vs oracle {err:.3e}, near-tie substitutions {subs}")
     assert err < 1e-10
