@@ -556,21 +556,7 @@ __device__ inline void fft_multi(double2* x, int count, int len, const double2* 
       double2 v[8];
 #pragma unroll
       for (int m = 0; m < 8; ++m) v[m] = b[fsw(base + pos + m * h, len)];
-#pragma unroll
-      for (int st = 0; st < 3; ++st) {
-        const int hs = 1 << st;
-#pragma unroll
-        for (int m = 0; m < 8; ++m) {
-          if (m & hs) continue;
-          const int q = pos + (m & (hs - 1)) * h;
-          double2 w = __ldg(roots + (q << (logn - s - st)));
-          if (inverse) w.y = -w.y;
-          const double2 tt = cmul(w, v[m + hs]);
-          const double2 u = v[m];
-          v[m] = cadd(u, tt);
-          v[m + hs] = csub(u, tt);
-        }
-      }
+      radix8_apply(v, radix8_twiddles(roots, pos << (logn - s - 2), inverse));
 #pragma unroll
       for (int m = 0; m < 8; ++m) b[fsw(base + pos + m * h, len)] = v[m];
     }

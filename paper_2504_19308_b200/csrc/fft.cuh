@@ -22,6 +22,57 @@ __device__ __forceinline__ double2 cconj(double2 a) { return make_double2(a.x, -
 __device__ __forceinline__ double2 cscale(double2 a, double s) { return make_double2(a.x * s, a.y * s); }
 
 __host__ __device__ inline bool is_pow2(int n) { return n > 0 && (n & (n - 1)) == 0; }
+
+// The eight twiddles of one radix-8 group (three radix-2 DIT stages s, s+1, s+2 at offset pos):
+// stage s+2 uses u2 * e^{-+i pi m/4} (m = 0..3), stage s+1 uses u1 = u2^2 and u1 * (-+i), stage s
+// uses w0 = u2^4, with u2 = roots[pos << (logn - s - 2)]. One table load per group instead of
+// twelve (the table reads were most of the transform's L1 traffic); the squarings cost a few
+// ulp, far inside the 1e-10 parity bar.
+struct Radix8Tw {
+  double2 w0, u1, u1r, u2[4];
+};
+__device__ __forceinline__ Radix8Tw radix8_twiddles(const double2* __restrict__ roots, int idx, bool inverse) {
+  constexpr double r = 0.70710678118654752440;
+  double2 u = __ldg(roots + idx);
+  if (inverse) u.y = -u.y;
+  Radix8Tw t;
+  t.u1 = cmul(u, u);
+  t.w0 = cmul(t.u1, t.u1);
+  // times -i (forward) / +i (inverse)
+  t.u1r = inverse ? make_double2(-t.u1.y, t.u1.x) : make_double2(t.u1.y, -t.u1.x);
+  const double sg = inverse ? 1.0 : -1.0;
+  t.u2[0] = u;
+  t.u2[1] = cmul(u, make_double2(r, sg * r));
+  t.u2[2] = inverse ? make_double2(-u.y, u.x) : make_double2(u.y, -u.x);
+  t.u2[3] = cmul(u, make_double2(-r, sg * r));
+  return t;
+}
+
+// radix-8 butterflies on v[0..8) (same order as three radix-2 DIT stages)
+__device__ __forceinline__ void radix8_apply(double2 (&v)[8], const Radix8Tw& t) {
+#pragma unroll
+  for (int m = 0; m < 8; m += 2) {
+    const double2 tt = cmul(t.w0, v[m + 1]);
+    const double2 u = v[m];
+    v[m] = cadd(u, tt);
+    v[m + 1] = csub(u, tt);
+  }
+#pragma unroll
+  for (int m = 0; m < 8; ++m) {
+    if (m & 2) continue;
+    const double2 tt = cmul((m & 1) ? t.u1r : t.u1, v[m + 2]);
+    const double2 u = v[m];
+    v[m] = cadd(u, tt);
+    v[m + 2] = csub(u, tt);
+  }
+#pragma unroll
+  for (int m = 0; m < 4; ++m) {
+    const double2 tt = cmul(t.u2[m], v[m + 4]);
+    const double2 u = v[m];
+    v[m] = cadd(u, tt);
+    v[m + 4] = csub(u, tt);
+  }
+}
 __host__ __device__ inline int ilog2(int n) {
   int l = 0;
   while ((1 << l) < n) ++l;
@@ -67,21 +118,7 @@ __device__ inline void fft_block(double2* x, double2* scratch, int n, const doub
         double2 v[8];
 #pragma unroll
         for (int m = 0; m < 8; ++m) v[m] = x[fsw(base + pos + m * h, n)];
-#pragma unroll
-        for (int st = 0; st < 3; ++st) {
-          const int hs = 1 << st;  // pair distance in units of h
-#pragma unroll
-          for (int m = 0; m < 8; ++m) {
-            if (m & hs) continue;
-            const int q = pos + (m & (hs - 1)) * h;  // offset inside the stage's butterfly block
-            double2 w = __ldg(roots + (q << (logn - s - st)));
-            if (inverse) w.y = -w.y;
-            const double2 t = cmul(w, v[m + hs]);
-            const double2 u = v[m];
-            v[m] = cadd(u, t);
-            v[m + hs] = csub(u, t);
-          }
-        }
+        radix8_apply(v, radix8_twiddles(roots, pos << (logn - s - 2), inverse));
 #pragma unroll
         for (int m = 0; m < 8; ++m) x[fsw(base + pos + m * h, n)] = v[m];
       }
