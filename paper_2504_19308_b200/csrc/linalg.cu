@@ -292,13 +292,15 @@ __global__ void __launch_bounds__(64) chol64_kernel(const double* __restrict__ G
 // ---- fast path (l <= 64): Cholesky + triangular inverse + conditioning test, one CTA --------
 // Elimination on the augmented pair [G | I] (rows/columns l..63 padded with the identity): the
 // row operations of the Cholesky factorisation turn G into R and I into R^{-T}, so X = R^{-1} is
-// read off transposed -- no separate back substitution. Both live in one 64 x 64 work matrix:
-// the upper triangle (c >= r) holds G -> R, the strict lower triangle holds R^{-T}; its diagonal
-// (1 / R[j][j]) is kept in rinv[]. 256 threads; thread t owns 16 consecutive entries of row
-// t / 4 in registers. Step j: the four owners of row j publish it (double-buffered), one barrier,
-// then every row r > j subtracts (A[j][r] / p) * row j on its active entries and row j scales
-// itself by 1 / sqrt(p). The loop is NOT unrolled over j: fully unrolled elimination code does
-// not fit the instruction cache (measured: ~75% of the time stalled on instruction fetch).
+// read off transposed -- no separate back substitution. 256 threads; thread t owns row t % 64,
+// columns [16 (t / 64), +16) of both blocks in registers (the lanes of a warp share their
+// columns, so the row-j reads are shared-memory broadcasts). Step j: the four owners of row j
+// publish it (double-buffered), one barrier, then every row r > j subtracts (A[j][r] / p) * row j
+// and row j scales itself by 1 / sqrt(p). The two blocks are kept apart, so the update needs no
+// per-entry masks (a combined 64 x 64 work matrix with R^{-T} in its lower triangle needed ~4x
+// the instructions per step), and a warp skips a block whose 16 columns cannot change at step j
+// (left: all columns < j; right: all columns > j -- row j's right part is zero there). Only the
+// l real pivots run. The loop over j is not unrolled (the instruction cache; measured).
 // kappa_F = ||R||_F ||X||_F >= cond_2(Y) decides whether CholeskyQR's second pass can be
 // skipped: with fp32 outputs one fp64 pass already leaves ||Q^T Q - I|| <~ u64 * kappa^2, so
 // kappa_F <= skip_kappa skips pass 2 (skip_out = 1). A pivot below 4*l*eps*max(diag G) raises
@@ -307,18 +309,17 @@ __global__ void __launch_bounds__(256) cholinv64_kernel(const double* __restrict
                                                         const int* __restrict__ gate, int* __restrict__ breakdown,
                                                         int* __restrict__ skip_out, double skip_kappa) {
   if (*gate) return;
-  __shared__ __align__(16) double rowbuf[2][64];
-  __shared__ double rinv[64];
+  __shared__ __align__(16) double rowL[2][64];
+  __shared__ __align__(16) double rowR[2][64];
   __shared__ double red[8][2];
-  // thread t: row t % 64, columns [16 (t / 64), +16): the lanes of a warp share their columns,
-  // so the row-j reads are shared-memory broadcasts
   const int t = threadIdx.x, r = t & 63, c0 = (t >> 6) * 16;
   const int lane = t & 31, warp = t >> 5;
-  double w[16];
+  double wl[16], wr[16];
 #pragma unroll
   for (int u = 0; u < 16; ++u) {
     const int c = c0 + u;
-    w[u] = (r < l && c < l) ? (c >= r ? Gin[r * l + c] : 0.0) : (c == r ? 1.0 : 0.0);
+    wl[u] = (r < l && c < l) ? (c >= r ? Gin[r * l + c] : 0.0) : (c == r ? 1.0 : 0.0);
+    wr[u] = c == r ? 1.0 : 0.0;
   }
   double md = (t < 64 && r < l) ? Gin[r * l + r] : 0.0;
 #pragma unroll
@@ -330,37 +331,45 @@ __global__ void __launch_bounds__(256) cholinv64_kernel(const double* __restrict
   const double tol = 4.0 * l * 2.220446049250313e-16 * md;
   bool bad = false;
 #pragma unroll 1
-  for (int j = 0; j < 64; ++j) {
-    double* b = rowbuf[j & 1];
+  for (int j = 0; j < l; ++j) {
+    double* bl = rowL[j & 1];
+    double* br = rowR[j & 1];
     if (r == j) {
 #pragma unroll
-      for (int u = 0; u < 16; u += 2) *reinterpret_cast<double2*>(&b[c0 + u]) = make_double2(w[u], w[u + 1]);
+      for (int u = 0; u < 16; u += 2) {
+        *reinterpret_cast<double2*>(&bl[c0 + u]) = make_double2(wl[u], wl[u + 1]);
+        *reinterpret_cast<double2*>(&br[c0 + u]) = make_double2(wr[u], wr[u + 1]);
+      }
     }
     __syncthreads();
-    double p = b[j];
-    if (j < l && !(p > tol)) bad = true;  // uniform: every thread reads the same pivot
-    if (!(p > 0.0)) p = 1.0;              // keep the (discarded) arithmetic finite after a breakdown
+    double p = bl[j];
+    if (!(p > tol)) bad = true;  // uniform: every thread reads the same pivot
+    if (!(p > 0.0)) p = 1.0;     // keep the (discarded) arithmetic finite after a breakdown
     const double rsq = rsqrt(p);
     if (r > j) {
-      const double f = b[r] * (rsq * rsq);  // A[r][j] / p, with A[r][j] = A[j][r]
-      // active entries: c >= r (trailing G) and c <= j (R^{-T} part; its row-j diagonal is 1)
-      const unsigned lo = (unsigned)min(max(r - c0, 0), 16);       // u >= lo: c >= r
-      const unsigned hi = (unsigned)min(max(j - c0 + 1, 0), 16);   // u <  hi: c <= j
-      const unsigned act = (0xffffu << lo) | ((1u << hi) - 1u);
+      const double f = bl[r] * (rsq * rsq);  // A[r][j] / p, with A[r][j] = A[j][r]
+      if (c0 + 15 > j) {
 #pragma unroll
-      for (int u = 0; u < 16; u += 2) {
-        const double2 bv = *reinterpret_cast<const double2*>(&b[c0 + u]);
-        const double b0 = (c0 + u == j) ? 1.0 : bv.x, b1 = (c0 + u + 1 == j) ? 1.0 : bv.y;
-        // branch-free: inactive entries fold in a zero multiple (divergent per-entry branches
-        // cost ~4x the whole step)
-        const double f0 = (act & (1u << u)) ? f : 0.0, f1 = (act & (2u << u)) ? f : 0.0;
-        w[u] = fma(-f0, b0, w[u]);
-        w[u + 1] = fma(-f1, b1, w[u + 1]);
+        for (int u = 0; u < 16; u += 2) {
+          const double2 bv = *reinterpret_cast<const double2*>(&bl[c0 + u]);
+          wl[u] = fma(-f, bv.x, wl[u]);
+          wl[u + 1] = fma(-f, bv.y, wl[u + 1]);
+        }
+      }
+      if (c0 <= j) {
+#pragma unroll
+        for (int u = 0; u < 16; u += 2) {
+          const double2 bv = *reinterpret_cast<const double2*>(&br[c0 + u]);
+          wr[u] = fma(-f, bv.x, wr[u]);
+          wr[u + 1] = fma(-f, bv.y, wr[u + 1]);
+        }
       }
     } else if (r == j) {
 #pragma unroll
-      for (int u = 0; u < 16; ++u) w[u] *= rsq;
-      if (c0 == 0) rinv[j] = rsq;
+      for (int u = 0; u < 16; ++u) {
+        wl[u] *= rsq;
+        wr[u] *= rsq;
+      }
     }
   }
   if (bad) {
@@ -370,19 +379,16 @@ __global__ void __launch_bounds__(256) cholinv64_kernel(const double* __restrict
     }
     return;
   }
-  __syncthreads();
   double r2 = 0.0, x2 = 0.0;
   if (r < l) {
 #pragma unroll
     for (int u = 0; u < 16; ++u) {
       const int c = c0 + u;
       if (c >= l) continue;
-      // work[r][c]: c >= r -> R[r][c]; c < r -> (R^{-T})[r][c] = X[c][r]
-      if (c >= r) r2 = fma(w[u], w[u], r2);
-      else x2 = fma(w[u], w[u], x2);
-      const double xv = c < r ? w[u] : (c == r ? rinv[r] : 0.0);
+      if (c >= r) r2 = fma(wl[u], wl[u], r2);  // R[r][c]
+      const double xv = c <= r ? wr[u] : 0.0;  // (R^{-T})[r][c] = X[c][r]
+      x2 = fma(xv, xv, x2);
       Xout[c * l + r] = xv;
-      if (c == r) x2 = fma(xv, xv, x2);
     }
   }
 #pragma unroll
@@ -390,6 +396,7 @@ __global__ void __launch_bounds__(256) cholinv64_kernel(const double* __restrict
     r2 += __shfl_xor_sync(0xffffffffu, r2, o);
     x2 += __shfl_xor_sync(0xffffffffu, x2, o);
   }
+  __syncthreads();  // red[] is reused
   if (lane == 0) {
     red[warp][0] = r2;
     red[warp][1] = x2;
