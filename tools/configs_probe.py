@@ -55,4 +55,9 @@ from devgen import c5_operand  # noqa: E402
 A, _ = c5_operand(32768, 128, 32, seed=5, operand=0)
 B, _ = c5_operand(32768, 128, 32, seed=5, operand=1)
 out["C5_cycle_ms"] = timed(lambda: P.cycle_product_device(A, B, 128, 128, 1), reps=2, warm=1)
+# C5 secondary: circulant k=32 on the same operands (fp64 on the device, four-step transforms)
+from paper_2504_19308_b200 import _native as NT  # noqa: E402
+A, B = A.double(), B.double()
+torch.cuda.empty_cache()
+out["C5_circ_ms"] = timed(lambda: PC.circulant_product_device(A, B, NT.APX_F64, 32, 1), reps=2, warm=1)
 print(json.dumps(out))
