@@ -333,8 +333,8 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   // Y starts when B's energy pass (the HBM-bound, critical part of B's decomposition) is done and
   // overlaps the latency-bound select/extract and the gather's start; the rest of the range
   // finder then fits on the SMs the persistent gather leaves free
-  static const int y_wait = getenv("APX_Y_WAIT") ? atoi(getenv("APX_Y_WAIT")) : 0;
-  APX_CUDA(cudaStreamWaitEvent(lo, y_wait ? ss->b_ready : ss->b_read, 0));
+  // (waiting for the extraction instead -- Y entirely after B's stage -- measured the same)
+  APX_CUDA(cudaStreamWaitEvent(lo, ss->b_read, 0));
   APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, lo, 32));  // 64 CTAs
   stage_mark(3, lo);
   APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, lo)));
