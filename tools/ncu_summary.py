@@ -17,6 +17,9 @@ METRICS = [
     "l1tex__data_bank_conflicts_pipe_lsu_mem_shared.sum", "l1tex__t_sectors_pipe_lsu_mem_global_op_ld.sum",
     "smsp__issue_active.avg.pct_of_peak_sustained_active",
     "sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active", "lts__t_sector_hit_rate.pct",
+    "sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active",
+    "sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active",
+    "gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed", "sm__warps_active.avg.pct_of_peak_sustained_active",
 ]
 
 
@@ -29,7 +32,8 @@ def ncu_csv(rep, *extra):
 
 def main():
     rep, header = sys.argv[1], sys.argv[2]
-    h, units, vals = ncu_csv(rep)
+    extra = ["-k", "regex:" + sys.argv[3]] if len(sys.argv) > 3 else []
+    h, units, vals = ncu_csv(rep, *extra)
     d, u = dict(zip(h, vals)), dict(zip(h, units))
     print(f"# {header}")
     print(f"Kernel Name{' ' * 66}{d['Kernel Name']} ")
@@ -42,7 +46,8 @@ def main():
     print("\n# warp stall sampling (all samples)")
     for k, v in sorted(stalls.items(), key=lambda kv: -kv[1])[:8]:
         print(f"  {100 * v / tot:5.1f}%  {k}")
-    h2, _, v2 = ncu_csv(rep, "--print-metric-instances", "details", "--metrics", "sass__inst_executed_per_opcode")
+    h2, _, v2 = ncu_csv(rep, *extra, "--print-metric-instances", "details", "--metrics",
+                        "sass__inst_executed_per_opcode")
     txt = dict(zip(h2, v2)).get("sass__inst_executed_per_opcode", "")
     m = re.match(r"\s*(\d+)\s*\((.*)\)", txt)
     if m:
