@@ -116,7 +116,7 @@ static int run_cycle(const T* A, const T* B, int n, int ka, int kb, int order, c
     // M += dA . Bhat (right gather over row blocks of A, masked to dA on load) + ||M||^2
     APX_TRY(launch_cycle_right_gather<T>(A, sa, ka, lb, sb, kb, n, n, 1, M, p.msq, nullptr, st, true));
     stage_mark(3, st);
-    const int rblocks = (int)ceil_div(n, right_gather_rows(n, sizeof(T), kb));
+    const int rblocks = (int)ceil_div(n, right_gather_rows_plain(n, sizeof(T), kb));
     APX_TRY(launch_sum_vector(p.msq, rblocks, scal + APX_S_FRO2_M, st));
   } else {
     T* bh = (T*)p.bhat;
@@ -544,7 +544,7 @@ static int run_mixed(const T* A, const T* B, int n, int l, int kc, int order, in
     stage_mark(6, st);
     APX_TRY(launch_cycle_right_gather<T>(A, nullptr, 0, lb, sb, kc, n, n, 1, M, p.msq, p.asq, st, true));
     stage_mark(7, st);
-    const int rblocks = (int)ceil_div(n, right_gather_rows(n, sizeof(T), kc));
+    const int rblocks = (int)ceil_div(n, right_gather_rows_plain(n, sizeof(T), kc));
     APX_TRY(launch_sum_vector(p.msq, rblocks, scal + APX_S_FRO2_M, st));
     APX_TRY(launch_sum_vector(p.asq, rblocks, scal + APX_S_FRO2_A, st));
   } else {

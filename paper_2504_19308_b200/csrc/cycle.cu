@@ -578,6 +578,299 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
   }
 }
 
+// ------------------------------------------------------------------------------------------
+// K11s: segmented right gather for large n, where a whole row no longer fits shared memory R>2
+// times (fp32 n = 32768: one 128 KB row per CTA, so each lambda' value -- an L2 load -- fed a
+// single FMA and the kernel was L2-bound). The CTA keeps R rows but only a column SEGMENT of
+// them, [s0, s0 + sw), in shared memory, and sweeps the segments: for output column c only the
+// shifts whose source column m = (c + J_t) mod n falls in the segment contribute. With J sorted
+// once per CTA, those shifts are one cyclic run of the sorted list, found by binary search per
+// (warp, segment) -- so every (c, t) pair is visited exactly once over the sweep, each lambda'
+// load again feeds R FMAs, and M is read-modified-written once per segment (from L2).
+// ------------------------------------------------------------------------------------------
+constexpr int kSegThreads = 512;
+constexpr int kSegU = 4;    // shifts per batch (kSegU * kSegCPT lambda loads in flight per thread)
+// columns per thread (lane + 32 q of the warp's column chunk): 4 fp32, 2 fp64 (register budget)
+template <typename T>
+__host__ __device__ constexpr int seg_cpt() { return sizeof(T) == 4 ? 4 : 2; }
+
+// L2 eviction policies: lambda' (re-read for every row block) is kept, the streamed operand rows
+// and the M read-modify-write traffic go first
+__device__ __forceinline__ unsigned long long l2_policy_evict_last() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ unsigned long long l2_policy_evict_first() {
+  unsigned long long p;
+  asm volatile("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(p));
+  return p;
+}
+__device__ __forceinline__ float ldg_nc_hint(const float* a, unsigned long long pol) {
+  float v;
+  asm volatile("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ldg_nc_hint(const double* a, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.nc.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ float ldg_hint(const float* a, unsigned long long pol) {
+  float v;
+  asm volatile("ld.global.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ double ldg_hint(const double* a, unsigned long long pol) {
+  double v;
+  asm volatile("ld.global.L2::cache_hint.f64 %0, [%1], %2;" : "=d"(v) : "l"(a), "l"(pol));
+  return v;
+}
+__device__ __forceinline__ void stg_hint(float* a, float v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.f32 [%0], %1, %2;" ::"l"(a), "f"(v), "l"(pol) : "memory");
+}
+__device__ __forceinline__ void stg_hint(double* a, double v, unsigned long long pol) {
+  asm volatile("st.global.L2::cache_hint.f64 [%0], %1, %2;" ::"l"(a), "d"(v), "l"(pol) : "memory");
+}
+
+// first index i >= from with tab[i].x >= v (tab ascending in .x)
+__device__ __forceinline__ int lower_index(const int2* tab, int k, int v, int from) {
+  int a = from, b = k;
+  while (a < b) {
+    const int h = (a + b) >> 1;
+    if (tab[h].x < v) a = h + 1; else b = h;
+  }
+  return a;
+}
+
+template <typename T, int R>
+__global__ void __launch_bounds__(kSegThreads, 1)
+    cycle_right_gather_seg(const T* __restrict__ X, const int* __restrict__ JA, int ka, const T* __restrict__ lam,
+                           const int* __restrict__ J, int k, int n, int m_rows, int accumulate, T* __restrict__ M,
+                           double* __restrict__ msq_partial, double* __restrict__ xsq_partial, int SW) {
+  constexpr int RP = gather_pitch(R, sizeof(T));
+  constexpr int CPT = seg_cpt<T>();
+  constexpr int NP = (sizeof(T) == 4) ? R / 2 : 0;
+  constexpr int NS = (sizeof(T) == 4) ? (R & 1) : R;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  T* Xs = reinterpret_cast<T*>(smem_raw);
+  int2* sJT = reinterpret_cast<int2*>(Xs + (size_t)RP * SW);  // (shift, lambda row), ascending shift
+  __shared__ double red[32];
+  const unsigned long long pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
+  // rank sort of the (distinct) shifts
+  for (int t = threadIdx.x; t < k; t += blockDim.x) {
+    const int j = J[t];
+    int rank = 0;
+    for (int u = 0; u < k; ++u) rank += J[u] < j;
+    sJT[rank] = make_int2(j, t);
+  }
+  const int r0 = blockIdx.x * R;
+  const int rows = min(R, m_rows - r0);
+  const int nseg = (int)ceil_div(n, SW);
+  double xs = 0.0, msq = 0.0;
+  for (int s = 0; s < nseg; ++s) {
+    const int s0 = s * SW, sw = min(SW, n - s0);
+    __syncthreads();  // the previous segment's readers are done (and the sort is visible)
+    // fill: coalesced 16-byte row reads, transposed in registers to the interleaved layout
+    {
+      constexpr int V = 16 / sizeof(T);
+      using Vec = typename std::conditional<sizeof(T) == 4, float4, double2>::type;
+      const int nv = sw / V;
+      for (int iv = threadIdx.x; iv < nv; iv += blockDim.x) {
+        Vec buf[RP];
+#pragma unroll
+        for (int rr = 0; rr < RP; ++rr)
+          buf[rr] = rr < rows ? __ldg(reinterpret_cast<const Vec*>(X + (size_t)(r0 + rr) * n + s0) + iv) : Vec{};
+        alignas(16) T tr[V * RP];
+#pragma unroll
+        for (int rr = 0; rr < RP; ++rr) {
+          const T* e = reinterpret_cast<const T*>(&buf[rr]);
+#pragma unroll
+          for (int q = 0; q < V; ++q) {
+            xs = fma((double)e[q], (double)e[q], xs);
+            tr[q * RP + rr] = e[q];
+          }
+        }
+        Vec* dst = reinterpret_cast<Vec*>(Xs + (size_t)iv * V * RP);
+#pragma unroll
+        for (int w = 0; w < RP; ++w) dst[w] = reinterpret_cast<const Vec*>(tr)[w];
+      }
+    }
+    if (JA != nullptr) {
+      __syncthreads();
+      for (int e = threadIdx.x; e < rows * ka; e += blockDim.x) {
+        const int rr = e / ka, t = e - rr * ka;
+        int m = r0 + rr - JA[t];
+        if (m < 0) m += n;
+        if (m >= s0 && m < s0 + sw) Xs[(size_t)(m - s0) * RP + rr] = T(0);
+      }
+    }
+    __syncthreads();
+    const bool last = s == nseg - 1;
+    if (threadIdx.x == 0 && s + 1 < nseg) {  // next segment's rows toward L2 while this one runs
+      const int n1 = min(SW, n - (s0 + SW));
+      for (int rr = 0; rr < rows; ++rr)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(X + (size_t)(r0 + rr) * n + s0 + SW),
+                     "r"((unsigned)(n1 * sizeof(T)))
+                     : "memory");
+    }
+    const int lane = threadIdx.x & 31;
+    constexpr int CW = 32 * CPT;  // a warp's column chunk: lane + 32 q, q < CPT
+    const T* xlane = Xs + (size_t)lane * RP;
+    for (int cw = (threadIdx.x >> 5) * CW; cw < n; cw += (blockDim.x >> 5) * CW) {
+      // The chunk's source window under shift J is [m0, m0 + CW), m0 = (cw + J) mod n.
+      //  interior: the window lies inside the segment (m0 in [s0, s0 + sw - CW]): one warp-uniform
+      //            offset, no per-lane checks;
+      //  boundary: the window straddles a segment end (m0 in [s0 - CW + 1, s0) or
+      //            (s0 + sw - CW, s0 + sw)): per-lane checks, ~2 such shifts per chunk over the sweep.
+      // Each is a cyclic interval of J values, i.e. a cyclic run of the sorted table.
+      auto run = [&](int v, int len, int& first) -> int {  // J in [v, v + len) mod n, len < n
+        v %= n;
+        if (v < 0) v += n;
+        first = lower_index(sJT, k, v, 0);
+        int cnt;
+        if (v + len <= n) {
+          cnt = lower_index(sJT, k, v + len, first) - first;
+        } else {
+          cnt = (k - first) + min(lower_index(sJT, k, v + len - n, 0), first);
+        }
+        if (first >= k) first -= k;  // every shift is below v: the run starts at index 0
+        return cnt;
+      };
+      int f_int, f_lo, f_hi;
+      const int c_int = run(s0 - cw, sw - CW + 1, f_int);
+      const int c_lo = run(s0 - CW + 1 - cw, CW - 1, f_lo);
+      const int c_hi = nseg > 1 ? run(s0 + sw - CW + 1 - cw, CW - 1, f_hi) : 0;
+      // the chunk's M lines toward L2 (read back by the epilogue)
+      if (s > 0 || accumulate != 0) {
+#pragma unroll
+        for (int q = 0; q < CPT; ++q)
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr)
+            if (rr < rows) asm volatile("prefetch.global.L2 [%0];" ::"l"(M + (size_t)(r0 + rr) * n + cw + 32 * q + lane));
+      }
+      unsigned long long acc2[CPT][NP > 0 ? NP : 1];
+      T accs[CPT][NS > 0 ? NS : 1];
+#pragma unroll
+      for (int q = 0; q < CPT; ++q) {
+#pragma unroll
+        for (int p = 0; p < (NP > 0 ? NP : 1); ++p) acc2[q][p] = 0ull;
+#pragma unroll
+        for (int p = 0; p < (NS > 0 ? NS : 1); ++p) accs[q][p] = T(0);
+      }
+      auto fma_rows = [&](int q, const T* xp, T l) {
+        if constexpr (NP > 0) {
+          const unsigned long long l2 = pack2((float)l, (float)l);
+          const unsigned long long* xp2 = reinterpret_cast<const unsigned long long*>(xp);
+#pragma unroll
+          for (int p = 0; p < NP; ++p) acc2[q][p] = ffma2(xp2[p], l2, acc2[q][p]);
+        }
+        if constexpr (NS > 0) {
+#pragma unroll
+          for (int p = 0; p < NS; ++p) accs[q][p] = fma(xp[2 * NP + p], l, accs[q][p]);
+        }
+      };
+      // interior shifts, kSegU per batch, batch i+1's lambda loads in flight while batch i is
+      // consumed. off[u]: the warp-uniform source offset (m0 - s0) * RP of shift u.
+      auto load_batch = [&](int i0, int (&off)[kSegU], T (&lv)[kSegU][CPT]) {
+#pragma unroll
+        for (int u = 0; u < kSegU; ++u) {
+          int i = f_int + i0 + u;
+          i = i >= k ? i - k : i;
+          const bool in = i0 + u < c_int;
+          const int2 jt = sJT[in ? i : f_int];  // broadcast
+          unsigned m = (unsigned)(cw + jt.x);
+          m = min(m, m - (unsigned)n);  // (cw + J) mod n
+          off[u] = in ? (int)(m - (unsigned)s0) * RP : 0;
+          const T* lrow = lam + (size_t)jt.y * n + cw + lane;
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) lv[u][q] = in ? ldg_nc_hint(lrow + 32 * q, pol_keep) : T(0);
+        }
+      };
+      auto compute_batch = [&](const int (&off)[kSegU], const T (&lv)[kSegU][CPT]) {
+#pragma unroll
+        for (int u = 0; u < kSegU; ++u)
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) fma_rows(q, xlane + off[u] + 32 * q * RP, lv[u][q]);
+      };
+      {
+        int oA[kSegU], oB[kSegU];
+        T lvA[kSegU][CPT], lvB[kSegU][CPT];
+        if (c_int > 0) load_batch(0, oA, lvA);
+        for (int i0 = 0; i0 < c_int; i0 += 2 * kSegU) {
+          if (i0 + kSegU < c_int) load_batch(i0 + kSegU, oB, lvB);
+          compute_batch(oA, lvA);
+          if (i0 + kSegU >= c_int) break;
+          if (i0 + 2 * kSegU < c_int) load_batch(i0 + 2 * kSegU, oA, lvA);
+          compute_batch(oB, lvB);
+        }
+      }
+      // boundary shifts: per-lane segment test; lanes outside read offset 0 with a zero lambda
+      auto boundary = [&](int first, int cnt) {
+        for (int e = 0; e < cnt; ++e) {
+          int i = first + e;
+          i = i >= k ? i - k : i;
+          const int2 jt = sJT[i];
+          const T* lrow = lam + (size_t)jt.y * n;
+          T lv[CPT];
+          unsigned l[CPT];
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) {
+            const int c = cw + 32 * q + lane;
+            unsigned m = (unsigned)(c + jt.x);
+            m = min(m, m - (unsigned)n);
+            const unsigned d = m - (unsigned)s0;
+            const bool ok = d < (unsigned)sw;
+            l[q] = ok ? d : 0u;
+            lv[q] = ok ? __ldg(lrow + c) : T(0);
+          }
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) fma_rows(q, Xs + (size_t)l[q] * RP, lv[q]);
+        }
+      };
+      boundary(f_lo, c_lo);
+      boundary(f_hi, c_hi);
+      // M (+)= the segment's partial sums: the first segment applies `accumulate`, later ones
+      // add (subtract for accumulate < 0); all old values are loaded before the first store
+      T old[CPT][R];
+#pragma unroll
+      for (int q = 0; q < CPT; ++q)
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr)
+          old[q][rr] = (rr < rows && (s > 0 || accumulate != 0)) ? ldg_hint(M + (size_t)(r0 + rr) * n + cw + 32 * q + lane, pol_stream) : T(0);
+#pragma unroll
+      for (int q = 0; q < CPT; ++q)
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) {
+          T a;
+          if constexpr (NP > 0) {
+            if (rr < 2 * NP) {
+              const unsigned long long v = acc2[q][rr >> 1];
+              a = (T)__uint_as_float((unsigned)(rr & 1 ? (v >> 32) : (v & 0xffffffffull)));
+            } else {
+              a = accs[q][rr - 2 * NP];
+            }
+          } else {
+            a = accs[q][rr];
+          }
+          if (rr < rows) {
+            const T v = accumulate < 0 ? old[q][rr] - a : old[q][rr] + a;
+            stg_hint(M + (size_t)(r0 + rr) * n + cw + 32 * q + lane, v, pol_stream);
+            if (last) msq += (double)v * (double)v;
+          }
+        }
+    }
+  }
+  if (xsq_partial != nullptr) {
+    const double t = block_sum(xs, red);
+    if (threadIdx.x == 0) xsq_partial[blockIdx.x] = t;
+  }
+  if (msq_partial != nullptr) {
+    const double t = block_sum(msq, red);
+    if (threadIdx.x == 0) msq_partial[blockIdx.x] = t;
+  }
+}
+
 // sum of |x|^2 over a dense array, per-block partials (for ||M||_F when no gather wrote M last)
 template <typename T>
 __global__ void __launch_bounds__(256) sumsq_partial_kernel(const T* __restrict__ x, size_t cnt,
@@ -784,6 +1077,44 @@ int right_gather_rows(int n, size_t elem, int k) {
   return r;
 }
 
+// Segmented gather (K11s) for the plain (non-persistent, non-TF32) call when a whole row fits at
+// most twice: R rows over column segments of width SW. APX_SEG_R overrides R (tuning).
+static int seg_rows(size_t elem) {
+  static const int env = [] {
+    const char* e = getenv("APX_SEG_R");
+    return e ? atoi(e) : 0;
+  }();
+  if (env == 2 || env == 4 || env == 6 || env == 8) return env;
+  return elem == 8 ? 4 : 6;
+}
+static int seg_width(int n, size_t elem, int k, int R) {
+  const size_t budget = kSmemBudget - (size_t)2 * std::max(k, 1) * sizeof(int);
+  const int64_t maxw = (int64_t)(budget / ((size_t)gather_pitch(R, elem) * elem)) & ~int64_t(31);
+  const int64_t nseg = ceil_div(n, maxw);
+  return (int)(ceil_div(ceil_div(n, nseg), 32) * 32);
+}
+int right_gather_seg_rows(int n, size_t elem, int k) {
+  if (right_gather_rows(n, elem, k) > 2 || n % kSegThreads != 0 || k <= 0) return 0;
+  return seg_rows(elem);
+}
+int right_gather_rows_plain(int n, size_t elem, int k) {
+  const int r = right_gather_seg_rows(n, elem, k);
+  return r > 0 ? r : right_gather_rows(n, elem, k);
+}
+
+template <typename T, int R>
+static int right_gather_seg_r(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n,
+                              int m_rows, int acc, T* M, double* msq_partial, double* xsq_partial, cudaStream_t st) {
+  const int SW = seg_width(n, sizeof(T), k, R);
+  const size_t smem = (size_t)gather_pitch(R, sizeof(T)) * SW * sizeof(T) + (size_t)2 * k * sizeof(int);
+  auto kern = cycle_right_gather_seg<T, R>;
+  APX_TRY(set_smem<T>((const void*)kern, smem));
+  kern<<<(unsigned)ceil_div(m_rows, R), kSegThreads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M, msq_partial,
+                                                                 xsq_partial, SW);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
 // lam: the column-aligned table (cycle_extract<T, true>), k x n, or (lam_padded) ceil(k/8)*8 x n
 // with zero rows past k -- enables the fast path. accumulate: 0 M = X.Bhat, 1 M += X.Bhat,
 // -1 M -= X.Bhat. max_ctas + ticket: persistent grid; col_chunks: split the columns over CTAs;
@@ -793,6 +1124,15 @@ int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, c
                               int m_rows, int accumulate, T* M, double* msq_partial, double* xsq_partial,
                               cudaStream_t st, bool lam_padded, int max_ctas, int* ticket, int col_chunks,
                               bool tf32_operands, int* ready, bool x_early) {
+  const int rs = right_gather_seg_rows(n, sizeof(T), k);
+  if (rs > 0 && !(max_ctas > 0 && ticket) && ready == nullptr && !(tf32_operands && sizeof(T) == 4)) {
+    switch (rs) {
+      case 2: return right_gather_seg_r<T, 2>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, st);
+      case 4: return right_gather_seg_r<T, 4>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, st);
+      case 6: return right_gather_seg_r<T, 6>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, st);
+      default: return right_gather_seg_r<T, 8>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, st);
+    }
+  }
   const int r = right_gather_rows(n, sizeof(T), k);
   APX_REQUIRE((size_t)n * sizeof(T) + (size_t)(k + 8) * sizeof(int) <= 227 * 1024,
               "n=%d too large for the right gather row block", n);

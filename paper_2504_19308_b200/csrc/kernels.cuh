@@ -7,6 +7,10 @@ namespace apx {
 // ---- cycle.cu ----
 size_t cycle_energy_ws(int n);
 int right_gather_rows(int n, size_t elem, int k);
+// rows per block of a plain right gather (no ticket / ready flags / TF32 operands): the segmented
+// kernel's R at large n, else right_gather_rows
+int right_gather_rows_plain(int n, size_t elem, int k);
+int right_gather_seg_rows(int n, size_t elem, int k);
 template <typename T>
 int launch_cycle_energies(const T* A, int n, double* energies, double* norms, double* fro2, double* partial,
                           cudaStream_t st);
