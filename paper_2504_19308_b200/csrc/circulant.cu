@@ -300,20 +300,40 @@ __global__ void __launch_bounds__(512) circ_right2_kernel(const T* __restrict__ 
   const int r0 = 2 * blockIdx.x;
   const bool two = r0 + 1 < n;
   const double rs = rsqrt((double)n);
-  for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    // Ahat[r][c] = sum_t S_t[(r - c) % n] * w^{t c}: rows r0, r0+1 read S_t[d], S_t[d+1]
-    double2 h0 = make_double2(0.0, 0.0), h1 = make_double2(0.0, 0.0);
-    int d = r0 - c;
-    if (d < 0) d += n;
-    const int d1 = d + 1 == n ? 0 : d + 1;
+  {
+    // Ahat[r][c] = sum_t S_t[(r - c) % n] * w^{t c} at the thread's columns c_i = tid + i * nt:
+    // rows r0, r0+1 read S_t[d], S_t[d+1]; the twiddle of c_{i+1} is the one of c_i times
+    // w^{t nt}, so each term takes two table loads per thread instead of one per column (the
+    // table index t c mod n scatters the lanes over the table: one sector per lane)
+    const int nt = blockDim.x;
+    double2 h0[kPP], h1[kPP];
+#pragma unroll
+    for (int i = 0; i < kPP; ++i) h0[i] = h1[i] = make_double2(0.0, 0.0);
     for (int q = 0; q < ka; ++q) {
-      const double2 w = cconj(__ldg(roots + mulmod_n(sA[q], c, n)));  // exp(+2 pi i t c / n)
+      double2 w = cconj(__ldg(roots + mulmod_n(sA[q], threadIdx.x, n)));  // exp(+2 pi i t c / n)
+      const double2 stp = cconj(__ldg(roots + mulmod_n(sA[q], nt % n, n)));
       const double2* Sq = SselA + (size_t)q * n;
-      h0 = cadd(h0, cmul(__ldg(Sq + d), w));
-      h1 = cadd(h1, cmul(__ldg(Sq + d1), w));
+#pragma unroll
+      for (int i = 0; i < kPP; ++i) {
+        const int c = threadIdx.x + i * nt;
+        if (c < n) {
+          int d = r0 - c;
+          if (d < 0) d += n;
+          const int d1 = d + 1 == n ? 0 : d + 1;
+          h0[i] = cadd(h0[i], cmul(__ldg(Sq + d), w));
+          h1[i] = cadd(h1[i], cmul(__ldg(Sq + d1), w));
+          w = cmul(w, stp);
+        }
+      }
     }
-    x0[fsw(c, n)] = cconj(csub(ld_c<T>(A, (size_t)r0 * n + c), h0));
-    x1[fsw(c, n)] = two ? cconj(csub(ld_c<T>(A, (size_t)(r0 + 1) * n + c), h1)) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int i = 0; i < kPP; ++i) {
+      const int c = threadIdx.x + i * nt;
+      if (c < n) {
+        x0[fsw(c, n)] = cconj(csub(ld_c<T>(A, (size_t)r0 * n + c), h0[i]));
+        x1[fsw(c, n)] = two ? cconj(csub(ld_c<T>(A, (size_t)(r0 + 1) * n + c), h1[i])) : make_double2(0.0, 0.0);
+      }
+    }
   }
   __syncthreads();
   fft_block(x0, scratch, n, roots, false);
@@ -527,17 +547,18 @@ __global__ void cycle_power_kernel(const E* __restrict__ in, int rows, int cols,
 // then run unfused: skew / transpose -> batched FFT -> gather in frequency space -> inverse FFT.
 // ---------------------------------------------------------------------------------------------
 
-// `count` independent power-of-two transforms of length len, transform t at x + t * len (each
+// `count` independent power-of-two transforms of length len, transform t at x + t * stride (each
 // XOR-swizzled by fsw), all threads of the CTA cooperating; same butterflies as fft_block.
-__device__ inline void fft_multi(double2* x, int count, int len, const double2* __restrict__ roots, bool inverse) {
+__device__ inline void fft_multi(double2* x, int count, int len, int stride, const double2* __restrict__ roots,
+                                 bool inverse) {
   const int tid = threadIdx.x, nt = blockDim.x;
   if (len == 1) return;
   const int logn = ilog2(len);
   for (int e = tid; e < count * len; e += nt) {
-    const int t = e >> logn, i = e & (len - 1);
+    const int t = e >> logn, i = bitrev_order(e & (len - 1), logn);
     const int j = (int)(__brev((unsigned)i) >> (32 - logn));
     if (i < j) {
-      double2* b = x + (size_t)t * len;
+      double2* b = x + (size_t)t * stride;
       const double2 v = b[fsw(i, len)];
       b[fsw(i, len)] = b[fsw(j, len)];
       b[fsw(j, len)] = v;
@@ -545,12 +566,12 @@ __device__ inline void fft_multi(double2* x, int count, int len, const double2* 
   }
   __syncthreads();
   int s = 1;
-  const int g8 = len >> 3;
+  const int lg8 = logn - 3;
   for (; s + 2 <= logn; s += 3) {
     const int h = 1 << (s - 1);
-    for (int gg = tid; gg < count * g8; gg += nt) {
-      const int t = gg / g8, g = gg - t * g8;
-      double2* b = x + (size_t)t * len;
+    for (int gg = tid; gg < (count << lg8); gg += nt) {
+      const int t = gg >> lg8, g = gg & ((1 << lg8) - 1);
+      double2* b = x + (size_t)t * stride;
       const int pos = g & (h - 1);
       const int base = (g >> (s - 1)) << (s + 2);
       double2 v[8];
@@ -562,12 +583,12 @@ __device__ inline void fft_multi(double2* x, int count, int len, const double2* 
     }
     __syncthreads();
   }
-  const int g2 = len >> 1;
+  const int lg2 = logn - 1;
   for (; s <= logn; ++s) {
     const int half = 1 << (s - 1);
-    for (int gg = tid; gg < count * g2; gg += nt) {
-      const int t = gg / g2, bb = gg - t * g2;
-      double2* b = x + (size_t)t * len;
+    for (int gg = tid; gg < (count << lg2); gg += nt) {
+      const int t = gg >> lg2, bb = gg & ((1 << lg2) - 1);
+      double2* b = x + (size_t)t * stride;
       const int pos = bb & (half - 1);
       const int i = ((bb >> (s - 1)) << s) + pos;
       const int j = i + half;
@@ -582,52 +603,98 @@ __device__ inline void fft_multi(double2* x, int count, int len, const double2* 
   }
 }
 
+// Tiles of kBigTile sequences per CTA; tile t sits at x + t * (len + 1) in shared memory: the pad
+// puts element i of the kBigTile sequences in different 16-byte bank groups, so the transposing
+// tile loads / stores (consecutive threads = consecutive sequences) are conflict-free.
 constexpr int kBigTile = 16;  // columns (pass 1) / rows (pass 2) per CTA: 256-byte global runs
+constexpr int kBigThreads = 512;
+constexpr int kBigMaxE = 16;  // tile elements per thread (kBigTile * len / kBigThreads, len <= 512)
 
 // pass 1 of the four-step transform of `rows` sequences of length n = n1 * n2: in (TI) -> data
 // (complex; may alias `in` when TI is complex). grid (n2 / kBigTile, rows).
 template <typename TI>
-__global__ void __launch_bounds__(512) fft4_pass1_kernel(const TI* in, int n1, int n2, int inverse,
-                                                         const double2* __restrict__ roots_n,
-                                                         const double2* __restrict__ roots_n1, double2* data) {
+__global__ void __launch_bounds__(kBigThreads) fft4_pass1_kernel(const TI* in, int n1, int n2, int inverse,
+                                                                 const double2* __restrict__ roots_n,
+                                                                 const double2* __restrict__ roots_n1, double2* data) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* x = reinterpret_cast<double2*>(smem_raw);
+  const int P = n1 + 1;
   const size_t n = (size_t)n1 * n2;
   const size_t row = blockIdx.y;
   const int i20 = blockIdx.x * kBigTile;
-  for (int e = threadIdx.x; e < kBigTile * n1; e += blockDim.x) {
-    const int i1 = e / kBigTile, c = e - i1 * kBigTile;
-    x[(size_t)c * n1 + fsw(i1, n1)] = ld_c<TI>(in, row * n + (size_t)i1 * n2 + i20 + c);
+  const int c = threadIdx.x & (kBigTile - 1), e0 = threadIdx.x / kBigTile;  // column, first i1 / k1
+  constexpr int kStep = kBigThreads / kBigTile;                              // i1 / k1 step per element
+  // every load of the tile in flight before the first shared-memory store
+  double2 v[kBigMaxE];
+  const TI* src = in + row * n + i20 + c;
+#pragma unroll
+  for (int j = 0; j < kBigMaxE; ++j) {
+    const int i1 = e0 + kStep * j;
+    if (i1 < n1) v[j] = ld_c<TI>(src, (size_t)i1 * n2);
+  }
+#pragma unroll
+  for (int j = 0; j < kBigMaxE; ++j) {
+    const int i1 = e0 + kStep * j;
+    if (i1 < n1) x[c * P + fsw(i1, n1)] = v[j];
   }
   __syncthreads();
-  fft_multi(x, kBigTile, n1, roots_n1, inverse != 0);
-  for (int e = threadIdx.x; e < kBigTile * n1; e += blockDim.x) {
-    const int k1 = e / kBigTile, c = e - k1 * kBigTile;
-    const int i2 = i20 + c;
-    double2 w = __ldg(roots_n + (((size_t)i2 * k1) & (n - 1)));
-    if (inverse) w.y = -w.y;
-    data[row * n + (size_t)k1 * n2 + i2] = cmul(x[(size_t)c * n1 + fsw(k1, n1)], w);
+  fft_multi(x, kBigTile, n1, P, roots_n1, inverse != 0);
+  // twiddle w_n^{i2 k1} for k1 = e0 + kStep j: the first from the table, the rest by repeated
+  // multiplication with w_n^{i2 kStep} (<= 15 products: a few ulp)
+  const size_t i2 = (size_t)(i20 + c);
+  double2 w = __ldg(roots_n + ((i2 * e0) & (n - 1)));
+  double2 stp = __ldg(roots_n + ((i2 * kStep) & (n - 1)));
+  if (inverse) {
+    w.y = -w.y;
+    stp.y = -stp.y;
+  }
+  double2* dst = data + row * n + i2;
+#pragma unroll
+  for (int j = 0; j < kBigMaxE; ++j) {
+    const int k1 = e0 + kStep * j;
+    if (k1 < n1) {
+      dst[(size_t)k1 * n2] = cmul(x[c * P + fsw(k1, n1)], w);
+      w = cmul(w, stp);
+    }
   }
 }
 
 // pass 2: data -> out (must not alias). grid (n1 / kBigTile, rows).
-__global__ void __launch_bounds__(512) fft4_pass2_kernel(const double2* __restrict__ data, int n1, int n2,
-                                                         int inverse, const double2* __restrict__ roots_n2,
-                                                         double scale, double2* __restrict__ out) {
+__global__ void __launch_bounds__(kBigThreads) fft4_pass2_kernel(const double2* __restrict__ data, int n1, int n2,
+                                                                 int inverse, const double2* __restrict__ roots_n2,
+                                                                 double scale, double2* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* x = reinterpret_cast<double2*>(smem_raw);
+  const int P = n2 + 1;
   const size_t n = (size_t)n1 * n2;
   const size_t row = blockIdx.y;
   const int k10 = blockIdx.x * kBigTile;
-  for (int e = threadIdx.x; e < kBigTile * n2; e += blockDim.x) {
-    const int r = e / n2, i2 = e - r * n2;
-    x[(size_t)r * n2 + fsw(i2, n2)] = __ldg(data + row * n + (size_t)(k10 + r) * n2 + i2);
+  // rows k10 .. k10 + kBigTile of the n1 x n2 matrix are one contiguous run of the sequence
+  const double2* src = data + row * n + (size_t)k10 * n2;
+  const int tot = kBigTile * n2;
+  double2 v[kBigMaxE];
+#pragma unroll
+  for (int j = 0; j < kBigMaxE; ++j) {
+    const int e = threadIdx.x + kBigThreads * j;
+    if (e < tot) v[j] = __ldg(src + e);
+  }
+#pragma unroll
+  for (int j = 0; j < kBigMaxE; ++j) {
+    const int e = threadIdx.x + kBigThreads * j;
+    if (e < tot) {
+      const int r = e / n2, i2 = e - r * n2;
+      x[r * P + fsw(i2, n2)] = v[j];
+    }
   }
   __syncthreads();
-  fft_multi(x, kBigTile, n2, roots_n2, inverse != 0);
-  for (int e = threadIdx.x; e < kBigTile * n2; e += blockDim.x) {
-    const int k2 = e / kBigTile, r = e - k2 * kBigTile;
-    out[row * n + (size_t)(k10 + r) + (size_t)n1 * k2] = cscale(x[(size_t)r * n2 + fsw(k2, n2)], scale);
+  fft_multi(x, kBigTile, n2, P, roots_n2, inverse != 0);
+  const int r = threadIdx.x & (kBigTile - 1), e0 = threadIdx.x / kBigTile;
+  constexpr int kStep = kBigThreads / kBigTile;
+  double2* dst = out + row * n + k10 + r;
+#pragma unroll
+  for (int j = 0; j < kBigMaxE; ++j) {
+    const int k2 = e0 + kStep * j;
+    if (k2 < n2) dst[(size_t)n1 * k2] = cscale(x[r * P + fsw(k2, n2)], scale);
   }
 }
 
@@ -702,7 +769,10 @@ __global__ void __launch_bounds__(256) big_left_gather_kernel(const double2* __r
   }
 }
 
-// X[r][c] = conj(A[r][c] - Ahat[r][c]), Ahat[r][c] = sum_q Ssel[q][(r - c) % n] exp(+2 pi i t_q c / n)
+// X[r][c] = conj(A[r][c] - Ahat[r][c]), Ahat[r][c] = sum_q Ssel[q][(r - c) % n] exp(+2 pi i t_q c / n).
+// Thread = column c of a block of kDaRows rows: the twiddle of (q, c) -- a scattered table load --
+// is shared by the block's rows, and for a fixed row the lanes read consecutive S_q entries.
+constexpr int kDaRows = 16;
 template <typename T>
 __global__ void __launch_bounds__(256) big_dA_kernel(const T* __restrict__ A, int n, const double2* __restrict__ Ssel,
                                                      const int* __restrict__ sel, int k,
@@ -711,14 +781,28 @@ __global__ void __launch_bounds__(256) big_dA_kernel(const T* __restrict__ A, in
   for (int q = threadIdx.x; q < k && q < 512; q += blockDim.x) s_buf[q] = sel[q];
   __syncthreads();
   const int* s_sel = k <= 512 ? s_buf : sel;
-  const size_t r = blockIdx.y;
-  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < n; c += gridDim.x * blockDim.x) {
-    int d = (int)r - c;
-    if (d < 0) d += n;
-    double2 ah = make_double2(0.0, 0.0);
-    for (int q = 0; q < k; ++q)
-      ah = cadd(ah, cmul(__ldg(Ssel + (size_t)q * n + d), cconj(__ldg(roots + mulmod_n(s_sel[q], c, n)))));
-    X[r * n + c] = cconj(csub(ld_c<T>(A, r * n + c), ah));
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  const int r0 = blockIdx.y * kDaRows;
+  if (c >= n) return;
+  double2 ah[kDaRows];
+#pragma unroll
+  for (int rr = 0; rr < kDaRows; ++rr) ah[rr] = make_double2(0.0, 0.0);
+  int d0 = r0 - c;
+  if (d0 < 0) d0 += n;
+  for (int q = 0; q < k; ++q) {
+    const double2 w = cconj(__ldg(roots + mulmod_n(s_sel[q], c, n)));
+    const double2* Sq = Ssel + (size_t)q * n;
+#pragma unroll
+    for (int rr = 0; rr < kDaRows; ++rr) {
+      int d = d0 + rr;
+      if (d >= n) d -= n;
+      ah[rr] = cadd(ah[rr], cmul(__ldg(Sq + d), w));
+    }
+  }
+#pragma unroll
+  for (int rr = 0; rr < kDaRows; ++rr) {
+    const size_t r = (size_t)r0 + rr;
+    if (r < (size_t)n) X[r * n + c] = cconj(csub(ld_c<T>(A, r * n + c), ah[rr]));
   }
 }
 
@@ -974,16 +1058,16 @@ __global__ void chirp_post_kernel(const double2* __restrict__ c, int n, int L, i
 template <typename TI>
 static int four_step_rows(const BigFFT& f, const TI* in, double2* data, double2* out, int rows, bool inverse,
                           double scale, cudaStream_t st) {
-  const size_t s1 = (size_t)kBigTile * f.n1 * sizeof(double2), s2 = (size_t)kBigTile * f.n2 * sizeof(double2);
+  const size_t s1 = (size_t)kBigTile * (f.n1 + 1) * sizeof(double2), s2 = (size_t)kBigTile * (f.n2 + 1) * sizeof(double2);
   APX_CUDA(cudaFuncSetAttribute(fft4_pass1_kernel<TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
   APX_CUDA(cudaFuncSetAttribute(fft4_pass2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));
   const size_t L = (size_t)f.L;
   for (int r0 = 0; r0 < rows; r0 += 65535) {
     const int rr = std::min(65535, rows - r0);
-    fft4_pass1_kernel<TI><<<dim3((unsigned)(f.n2 / kBigTile), (unsigned)rr), 512, s1, st>>>(
+    fft4_pass1_kernel<TI><<<dim3((unsigned)(f.n2 / kBigTile), (unsigned)rr), kBigThreads, s1, st>>>(
         in + r0 * L, f.n1, f.n2, inverse ? 1 : 0, f.roots, f.roots1, data + r0 * L);
     APX_LAUNCH_CHECK();
-    fft4_pass2_kernel<<<dim3((unsigned)(f.n1 / kBigTile), (unsigned)rr), 512, s2, st>>>(
+    fft4_pass2_kernel<<<dim3((unsigned)(f.n1 / kBigTile), (unsigned)rr), kBigThreads, s2, st>>>(
         data + r0 * L, f.n1, f.n2, inverse ? 1 : 0, f.roots2, scale, out + r0 * L);
     APX_LAUNCH_CHECK();
   }
@@ -1115,7 +1199,8 @@ static int run_circulant_big(const T* A, const T* B, int n, int k, int order, co
   stage_mark(2, st);
   if (order == 1) {
     // term2 = dA . Bhat, row-local: conj(dA) rows, FFT, gather with conj(L_B), inverse FFT, conj
-    big_dA_kernel<T><<<rows_grid, 256, 0, st>>>(A, n, p.Ssel_a, sa, k, p.rootsn, p.W1);
+    big_dA_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)ceil_div(n, kDaRows)), 256, 0, st>>>(
+        A, n, p.Ssel_a, sa, k, p.rootsn, p.W1);
     APX_LAUNCH_CHECK();
     APX_TRY(big_fft_rows<double2>(p.f, p.W1, p.W1, p.W2, n, false, 1.0, st));
     big_right_gather_kernel<<<rows_grid, 256, 0, st>>>(p.W2, n, p.L_b, sb, k, rs, p.W1);

@@ -86,6 +86,17 @@ __host__ __device__ inline int ilog2(int n) {
 // through fsw().
 __device__ __forceinline__ int fsw(int i, int n) { return (n & (n - 1)) == 0 ? (i ^ ((i >> 3) & 7)) : i; }
 
+// Visiting order of the bit-reversal swap: the e-th index swapped (a bijection of [0, 2^logn)).
+// An 8-lane phase gets indices with distinct low three bits (distinct bank groups on the i side)
+// and distinct top three bits (the partners j = brev(i) then differ in their low three bits),
+// all other bits shared, so both sides of the swap are conflict-free under fsw(). In plain
+// order the j side was an 8-way conflict: half of the transforms' excess shared wavefronts.
+__device__ __forceinline__ int bitrev_order(int e, int logn) {
+  if (logn < 6) return e;
+  const int lam = e & 7, rho = (e >> 3) & 7, mid = e >> 6;
+  return (((lam + rho) & 7) << (logn - 3)) | (mid << 3) | lam;
+}
+
 // roots[k] = exp(-2 pi i k / n) for k < n (full table; pow2 transforms use the first n/2)
 void launch_roots(double2* roots, int n, cudaStream_t st);
 
@@ -97,7 +108,8 @@ __device__ inline void fft_block(double2* x, double2* scratch, int n, const doub
   if (n == 1) return;
   if (is_pow2(n)) {
     const int logn = ilog2(n);
-    for (int i = tid; i < n; i += nt) {
+    for (int e = tid; e < n; e += nt) {
+      const int i = bitrev_order(e, logn);
       const int j = (int)(__brev((unsigned)i) >> (32 - logn));
       if (i < j) {
         const double2 t = x[fsw(i, n)];
