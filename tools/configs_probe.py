@@ -38,6 +38,22 @@ B = torch.from_numpy(O.gen_haar_spectrum(n, 0.9 ** np.arange(n), 2)).to(dev)
 oa = np.random.default_rng([0, 0]).standard_normal((n, 40))
 ob = np.random.default_rng([0, 1]).standard_normal((n, 40))
 out["C1_ms"] = timed(lambda: PS.svd_product_device(A, B, 40, 32, 40, 32, 2, 0, oa, ob))
+# C1 batched: NB independent products per CUDA-graph replay, concurrent on S streams (batch.py)
+NB = int(os.environ.get("C1_BATCH", 128))
+sig = 0.9 ** np.arange(n)
+Ab = torch.from_numpy(np.stack([O.gen_haar_spectrum(n, sig, 2 * t) for t in range(NB)])).to(dev)
+Bb = torch.from_numpy(np.stack([O.gen_haar_spectrum(n, sig, 2 * t + 1) for t in range(NB)])).to(dev)
+oab = torch.from_numpy(np.stack([np.random.default_rng([t, 0]).standard_normal((n, 40)) for t in range(NB)]))
+obb = torch.from_numpy(np.stack([np.random.default_rng([t, 1]).standard_normal((n, 40)) for t in range(NB)]))
+best = None
+for S in (16, 32, 64):
+    bt = P.SvdProductBatch(Ab, Bb, 40, 32, 40, 32, 2, 0, oab, obb, streams=S)
+    ms = timed(bt.run, reps=5, warm=2)
+    out[f"C1_batch{NB}_s{S}_ms"] = ms
+    best = ms if best is None else min(best, ms)
+    del bt
+out["C1_batch_products_per_s"] = NB / (best * 1e-3)
+del Ab, Bb
 # C2: cycle fp64 n=2048, k=32, order 1
 n = 2048
 A = torch.from_numpy(O.gen_cycle_operand(n, 32, 3)).to(dev)
