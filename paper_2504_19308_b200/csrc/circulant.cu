@@ -609,11 +609,12 @@ __device__ inline void fft_multi(double2* x, int count, int len, int stride, con
 constexpr int kBigTile = 16;  // columns (pass 1) / rows (pass 2) per CTA: 256-byte global runs
 constexpr int kBigThreads = 512;
 constexpr int kBigMaxE = 16;  // tile elements per thread (kBigTile * len / kBigThreads, len <= 512)
+constexpr int kBigRound = 8;  // loads in flight per thread (two CTAs per SM: <= 64 registers)
 
 // pass 1 of the four-step transform of `rows` sequences of length n = n1 * n2: in (TI) -> data
 // (complex; may alias `in` when TI is complex). grid (n2 / kBigTile, rows).
 template <typename TI>
-__global__ void __launch_bounds__(kBigThreads) fft4_pass1_kernel(const TI* in, int n1, int n2, int inverse,
+__global__ void __launch_bounds__(kBigThreads, 2) fft4_pass1_kernel(const TI* in, int n1, int n2, int inverse,
                                                                  const double2* __restrict__ roots_n,
                                                                  const double2* __restrict__ roots_n1, double2* data) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -624,18 +625,21 @@ __global__ void __launch_bounds__(kBigThreads) fft4_pass1_kernel(const TI* in, i
   const int i20 = blockIdx.x * kBigTile;
   const int c = threadIdx.x & (kBigTile - 1), e0 = threadIdx.x / kBigTile;  // column, first i1 / k1
   constexpr int kStep = kBigThreads / kBigTile;                              // i1 / k1 step per element
-  // every load of the tile in flight before the first shared-memory store
-  double2 v[kBigMaxE];
+  // the tile's loads in rounds of kBigRound, all of a round in flight before its stores
   const TI* src = in + row * n + i20 + c;
 #pragma unroll
-  for (int j = 0; j < kBigMaxE; ++j) {
-    const int i1 = e0 + kStep * j;
-    if (i1 < n1) v[j] = ld_c<TI>(src, (size_t)i1 * n2);
-  }
+  for (int j0 = 0; j0 < kBigMaxE; j0 += kBigRound) {
+    double2 v[kBigRound];
 #pragma unroll
-  for (int j = 0; j < kBigMaxE; ++j) {
-    const int i1 = e0 + kStep * j;
-    if (i1 < n1) x[c * P + fsw(i1, n1)] = v[j];
+    for (int j = 0; j < kBigRound; ++j) {
+      const int i1 = e0 + kStep * (j0 + j);
+      if (i1 < n1) v[j] = ld_c<TI>(src, (size_t)i1 * n2);
+    }
+#pragma unroll
+    for (int j = 0; j < kBigRound; ++j) {
+      const int i1 = e0 + kStep * (j0 + j);
+      if (i1 < n1) x[c * P + fsw(i1, n1)] = v[j];
+    }
   }
   __syncthreads();
   fft_multi(x, kBigTile, n1, P, roots_n1, inverse != 0);
@@ -660,7 +664,7 @@ __global__ void __launch_bounds__(kBigThreads) fft4_pass1_kernel(const TI* in, i
 }
 
 // pass 2: data -> out (must not alias). grid (n1 / kBigTile, rows).
-__global__ void __launch_bounds__(kBigThreads) fft4_pass2_kernel(const double2* __restrict__ data, int n1, int n2,
+__global__ void __launch_bounds__(kBigThreads, 2) fft4_pass2_kernel(const double2* __restrict__ data, int n1, int n2,
                                                                  int inverse, const double2* __restrict__ roots_n2,
                                                                  double scale, double2* __restrict__ out) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -672,18 +676,21 @@ __global__ void __launch_bounds__(kBigThreads) fft4_pass2_kernel(const double2* 
   // rows k10 .. k10 + kBigTile of the n1 x n2 matrix are one contiguous run of the sequence
   const double2* src = data + row * n + (size_t)k10 * n2;
   const int tot = kBigTile * n2;
-  double2 v[kBigMaxE];
 #pragma unroll
-  for (int j = 0; j < kBigMaxE; ++j) {
-    const int e = threadIdx.x + kBigThreads * j;
-    if (e < tot) v[j] = __ldg(src + e);
-  }
+  for (int j0 = 0; j0 < kBigMaxE; j0 += kBigRound) {
+    double2 v[kBigRound];
 #pragma unroll
-  for (int j = 0; j < kBigMaxE; ++j) {
-    const int e = threadIdx.x + kBigThreads * j;
-    if (e < tot) {
-      const int r = e / n2, i2 = e - r * n2;
-      x[r * P + fsw(i2, n2)] = v[j];
+    for (int j = 0; j < kBigRound; ++j) {
+      const int e = threadIdx.x + kBigThreads * (j0 + j);
+      if (e < tot) v[j] = __ldg(src + e);
+    }
+#pragma unroll
+    for (int j = 0; j < kBigRound; ++j) {
+      const int e = threadIdx.x + kBigThreads * (j0 + j);
+      if (e < tot) {
+        const int r = e / n2, i2 = e - r * n2;
+        x[r * P + fsw(i2, n2)] = v[j];
+      }
     }
   }
   __syncthreads();
@@ -748,7 +755,13 @@ __global__ void __launch_bounds__(256) gather_cols_kernel(const double2* __restr
     Ssel[(size_t)q * n + i] = cscale(__ldg(St + (size_t)i * n + t), scale);
 }
 
-// term1 gather in frequency space: Y[c][p] = sum_q L_q[p] * rs * FB[c][(p - t_q) % n]
+// Frequency-space gathers of the unfused path, kGatherRows rows per thread: the coefficient of
+// a term (L_q[p], or conj(L_q[src]) on the right) does not depend on the row, so one load of it
+// serves all the thread's rows (the rows' X reads are the only per-row traffic; a whole row is
+// 16n bytes, beyond shared memory at these n, so they stream from L2).
+constexpr int kGatherRows = 4;
+
+// term1: Y[c][p] = sum_q L_q[p] * rs * FB[c][(p - t_q) % n]
 __global__ void __launch_bounds__(256) big_left_gather_kernel(const double2* __restrict__ FB, int n,
                                                               const double2* __restrict__ L, const int* __restrict__ sel,
                                                               int k, double rs, double2* __restrict__ Y) {
@@ -756,17 +769,26 @@ __global__ void __launch_bounds__(256) big_left_gather_kernel(const double2* __r
   for (int q = threadIdx.x; q < k && q < 512; q += blockDim.x) s_buf[q] = sel[q];
   __syncthreads();
   const int* s_sel = k <= 512 ? s_buf : sel;
-  const size_t c = blockIdx.y;
-  const double2* fb = FB + c * n;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-    double2 a = make_double2(0.0, 0.0);
-    for (int q = 0; q < k; ++q) {
-      int src = p - s_sel[q];
-      if (src < 0) src += n;
-      a = cadd(a, cmul(__ldg(L + (size_t)q * n + p), cscale(__ldg(fb + src), rs)));
-    }
-    Y[c * n + p] = a;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t c0 = (size_t)blockIdx.y * kGatherRows;
+  if (p >= n) return;
+  double2 a[kGatherRows];
+#pragma unroll
+  for (int rr = 0; rr < kGatherRows; ++rr) a[rr] = make_double2(0.0, 0.0);
+  for (int q = 0; q < k; ++q) {
+    int src = p - s_sel[q];
+    if (src < 0) src += n;
+    const double2 l = __ldg(L + (size_t)q * n + p);
+    double2 x[kGatherRows];
+#pragma unroll
+    for (int rr = 0; rr < kGatherRows; ++rr)
+      x[rr] = c0 + rr < (size_t)n ? __ldg(FB + (c0 + rr) * n + src) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int rr = 0; rr < kGatherRows; ++rr) a[rr] = cadd(a[rr], cmul(l, x[rr]));
   }
+#pragma unroll
+  for (int rr = 0; rr < kGatherRows; ++rr)
+    if (c0 + rr < (size_t)n) Y[(c0 + rr) * n + p] = cscale(a[rr], rs);
 }
 
 // X[r][c] = conj(A[r][c] - Ahat[r][c]), Ahat[r][c] = sum_q Ssel[q][(r - c) % n] exp(+2 pi i t_q c / n).
@@ -806,7 +828,7 @@ __global__ void __launch_bounds__(256) big_dA_kernel(const T* __restrict__ A, in
   }
 }
 
-// term2 gather: Y[r][p] = sum_q (rs * X[r][(p + s_q) % n]) * conj(L_q[(p + s_q) % n])
+// term2: Y[r][p] = sum_q (rs * X[r][(p + s_q) % n]) * conj(L_q[(p + s_q) % n])
 __global__ void __launch_bounds__(256) big_right_gather_kernel(const double2* __restrict__ X, int n,
                                                                const double2* __restrict__ L, const int* __restrict__ sel,
                                                                int k, double rs, double2* __restrict__ Y) {
@@ -814,17 +836,26 @@ __global__ void __launch_bounds__(256) big_right_gather_kernel(const double2* __
   for (int q = threadIdx.x; q < k && q < 512; q += blockDim.x) s_buf[q] = sel[q];
   __syncthreads();
   const int* s_sel = k <= 512 ? s_buf : sel;
-  const size_t r = blockIdx.y;
-  const double2* xr = X + r * n;
-  for (int p = blockIdx.x * blockDim.x + threadIdx.x; p < n; p += gridDim.x * blockDim.x) {
-    double2 a = make_double2(0.0, 0.0);
-    for (int q = 0; q < k; ++q) {
-      int src = p + s_sel[q];
-      if (src >= n) src -= n;
-      a = cadd(a, cmulc(cscale(__ldg(xr + src), rs), __ldg(L + (size_t)q * n + src)));
-    }
-    Y[r * n + p] = a;
+  const int p = blockIdx.x * blockDim.x + threadIdx.x;
+  const size_t r0 = (size_t)blockIdx.y * kGatherRows;
+  if (p >= n) return;
+  double2 a[kGatherRows];
+#pragma unroll
+  for (int rr = 0; rr < kGatherRows; ++rr) a[rr] = make_double2(0.0, 0.0);
+  for (int q = 0; q < k; ++q) {
+    int src = p + s_sel[q];
+    if (src >= n) src -= n;
+    const double2 l = __ldg(L + (size_t)q * n + src);
+    double2 x[kGatherRows];
+#pragma unroll
+    for (int rr = 0; rr < kGatherRows; ++rr)
+      x[rr] = r0 + rr < (size_t)n ? __ldg(X + (r0 + rr) * n + src) : make_double2(0.0, 0.0);
+#pragma unroll
+    for (int rr = 0; rr < kGatherRows; ++rr) a[rr] = cadd(a[rr], cmulc(x[rr], l));
   }
+#pragma unroll
+  for (int rr = 0; rr < kGatherRows; ++rr)
+    if (r0 + rr < (size_t)n) Y[(r0 + rr) * n + p] = cscale(a[rr], rs);
 }
 
 // M += conj(rs * Y)
@@ -1174,7 +1205,7 @@ static int run_circulant_big(const T* A, const T* B, int n, int k, int order, co
   launch_roots(p.rootsn, n, st);
   APX_LAUNCH_CHECK();
   const double rs = 1.0 / sqrt((double)n);
-  const dim3 rows_grid((unsigned)std::min<int64_t>(ceil_div(n, 256), 16), (unsigned)n);
+  const dim3 gather_grid((unsigned)ceil_div(n, 256), (unsigned)ceil_div(n, kGatherRows));
   APX_TRY(big_decompose<T>(A, n, p, p.mag_a, st));
   if (fa) { if (k) APX_CUDA(cudaMemcpyAsync(sa, fa, k * sizeof(int), cudaMemcpyDeviceToDevice, st)); }
   else APX_TRY(launch_topk(p.mag_a, n, k, sa, st));
@@ -1191,7 +1222,7 @@ static int run_circulant_big(const T* A, const T* B, int n, int k, int order, co
   transpose_to_c_kernel<T><<<tgrid, 256, 0, st>>>(B, n, p.W1);
   APX_LAUNCH_CHECK();
   APX_TRY(big_fft_rows<double2>(p.f, p.W1, p.W1, p.W2, n, false, 1.0, st));
-  big_left_gather_kernel<<<rows_grid, 256, 0, st>>>(p.W2, n, p.L_a, sa, k, rs, p.W1);
+  big_left_gather_kernel<<<gather_grid, 256, 0, st>>>(p.W2, n, p.L_a, sa, k, rs, p.W1);
   APX_LAUNCH_CHECK();
   APX_TRY(big_fft_rows<double2>(p.f, p.W1, p.W1, p.W2, n, true, 1.0, st));
   transpose_scale_c_kernel<<<tgrid, 256, 0, st>>>(p.W2, n, rs, M);
@@ -1203,7 +1234,7 @@ static int run_circulant_big(const T* A, const T* B, int n, int k, int order, co
         A, n, p.Ssel_a, sa, k, p.rootsn, p.W1);
     APX_LAUNCH_CHECK();
     APX_TRY(big_fft_rows<double2>(p.f, p.W1, p.W1, p.W2, n, false, 1.0, st));
-    big_right_gather_kernel<<<rows_grid, 256, 0, st>>>(p.W2, n, p.L_b, sb, k, rs, p.W1);
+    big_right_gather_kernel<<<gather_grid, 256, 0, st>>>(p.W2, n, p.L_b, sb, k, rs, p.W1);
     APX_LAUNCH_CHECK();
     APX_TRY(big_fft_rows<double2>(p.f, p.W1, p.W1, p.W2, n, true, 1.0, st));
     acc_conj_kernel<<<kNumSMs * 8, 256, 0, st>>>(p.W2, (size_t)n * n, rs, M);

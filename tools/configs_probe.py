@@ -59,6 +59,16 @@ n = 2048
 A = torch.from_numpy(O.gen_cycle_operand(n, 32, 3)).to(dev)
 B = torch.from_numpy(O.gen_cycle_operand(n, 32, 4)).to(dev)
 out["C2_ms"] = timed(lambda: P.cycle_product_device(A, B, 32, 32, 1))
+# C2 batched: NB2 independent products per CUDA-graph replay on 8 streams (batch.py)
+NB2 = 16
+A2 = [torch.from_numpy(O.gen_cycle_operand(n, 32, 100 + 2 * t)).to(dev) for t in range(NB2)]
+B2 = [torch.from_numpy(O.gen_cycle_operand(n, 32, 101 + 2 * t)).to(dev) for t in range(NB2)]
+bt = P.GraphBatch([(lambda a, b: (lambda: P.cycle_product_device(a, b, 32, 32, 1)))(a, b) for a, b in zip(A2, B2)],
+                  streams=8)
+ms = timed(bt.replay, reps=5, warm=2)
+out[f"C2_batch{NB2}_ms"] = ms
+out["C2_batch_products_per_s"] = NB2 / (ms * 1e-3)
+del bt, A2, B2
 # C3: circulant fp64 n=4096, k=16, order 1
 n = 4096
 A = torch.from_numpy(O.gen_circulant_operand(n, 16, 5)).to(dev)
