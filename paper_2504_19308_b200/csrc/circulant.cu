@@ -104,12 +104,25 @@ __global__ void __launch_bounds__(512) circ_decompose_rows_kernel(const T* __res
   for (int t = threadIdx.x; t < n; t += blockDim.x) mag2_part[(size_t)blockIdx.x * n + t] = m2[t];
 }
 
-__global__ void mag_finalize_kernel(const double* __restrict__ part, int parts, int n, double* __restrict__ mag) {
-  const int t = blockIdx.x * blockDim.x + threadIdx.x;
-  if (t >= n) return;
-  double s = 0.0;
-  for (int p = 0; p < parts; ++p) s += part[(size_t)p * n + t];
-  mag[t] = sqrt(s);
+// mag[t] = sqrt(sum_p part[p][t]): a CTA covers 32 columns with 8 slices of the parts (slice s:
+// parts s, s+8, ...), combined in slice order -- a fixed order, 8x the loads in flight of a
+// column-per-thread loop over all parts (which was latency-bound: 33 us at n = 4096)
+__global__ void __launch_bounds__(256) mag_finalize_kernel(const double* __restrict__ part, int parts, int n,
+                                                           double* __restrict__ mag) {
+  __shared__ double acc_s[8][33];
+  const int jx = threadIdx.x & 31, sl = threadIdx.x >> 5;
+  const int t = blockIdx.x * 32 + jx;
+  double a = 0.0;
+  if (t < n)
+    for (int q = sl; q < parts; q += 8) a += part[(size_t)q * n + t];
+  acc_s[sl][jx] = a;
+  __syncthreads();
+  if (sl == 0 && t < n) {
+    double e = 0.0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) e += acc_s[q][jx];
+    mag[t] = sqrt(e);
+  }
 }
 
 // Selected spectrum rows from S^T: Ssel[q] = S[sel[q]], L[q] = fft(S[sel[q]]) (unnormalised, :145)
@@ -901,7 +914,7 @@ static int circ_decompose_run(const T* A, int n, const CircPlan& p, double2* St,
   APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
   fn<<<p.parts, 512, smem, st>>>(skew, n, p.cpc, p.roots, St, p.part);
   APX_LAUNCH_CHECK();
-  mag_finalize_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(p.part, p.parts, n, mag);
+  mag_finalize_kernel<<<(unsigned)ceil_div(n, 32), 256, 0, st>>>(p.part, p.parts, n, mag);
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -1182,7 +1195,7 @@ static int big_decompose(const T* X, int n, const BigCircPlan& p, double* mag, c
   colsum_abs2_kernel<<<dim3((unsigned)ceil_div(n, 256), (unsigned)ceil_div(n, rpc)), 256, 0, st>>>(
       p.W2, n, rpc, 1.0 / ((double)n * n), p.part);
   APX_LAUNCH_CHECK();
-  mag_finalize_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, st>>>(p.part, (int)ceil_div(n, rpc), n, mag);
+  mag_finalize_kernel<<<(unsigned)ceil_div(n, 32), 256, 0, st>>>(p.part, (int)ceil_div(n, rpc), n, mag);
   APX_LAUNCH_CHECK();
   return OK;
 }

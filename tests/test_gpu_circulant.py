@@ -38,10 +38,14 @@ def test_circulant_golden(C, golden, n):
     assert rel(spec.magnitudes, g[f"cd{n}_mags"]) < 1e-12
     sel = C.circulant_select(spec, k).selected
     near_tie_ok(sel, list(g[f"cd{n}_sel"]), g[f"cd{n}_mags"])
+    # B's selection (the golden file pins A's): the oracle's, under the same near-tie protocol
+    mags_b = O.circulant_decompose(B)[1]
+    sel_b = O.top_indices(mags_b, k)
     for order in (0, 1):
         M, rep = C.circulant_first_order_multiply(A, B, k, order)
         ref = g[f"cd{n}_M{order}"]
-        if rep.selected_a == list(g[f"cd{n}_sel"]):
+        near_tie_ok(rep.selected_b, sel_b, mags_b)
+        if rep.selected_a == list(g[f"cd{n}_sel"]) and rep.selected_b == sel_b:
             assert rel(M, ref) < 1e-10
         else:  # re-run the oracle with the GPU's selections forced
             Mo, _ = O.circulant_first_order_multiply(A, B, k, order, rep.selected_a, rep.selected_b)
