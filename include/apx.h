@@ -218,6 +218,23 @@ int apx_mixed_rows_phase(int phase, const float* A_rows, int64_t m_rows, const f
                          const void* red_in, void* red_out, double* scalars, void* ws, size_t ws_bytes,
                          void* stream);
 
+/* The cycle product (restated C2 / C5 path, apx_cycle_first_order) sharded by rows of A and M over
+ * ranks. Rank g passes its row block A_rows = A[row0 : row0 + m_rows] and the whole
+ * B, and receives M[row0 : row0 + m_rows]. Two calls on the same workspace and stream:
+ *   phase 1: red_out = the energies of A's cycles over the rank's rows, n fp64 (red_in unused);
+ *            the caller sums red_out over the ranks in place (NCCL all-reduce on `stream`);
+ *   phase 2: red_in = the summed energies; selections, lambdas and the product rows; red_out[0] =
+ *            ||M_g||_F^2, to be summed by the caller into scalars[APX_S_FRO2_M].
+ * Every rank selects from the same summed energies, so sel_a agrees across ranks; B is replicated.
+ * For the large-n left product (fp32 n > 5688, fp64 n > 2844) n must be a multiple of 512 and the
+ * row block aligned to 128 (fp32) / 64 (fp64) rows. Replaces nothing in the reference (which has no
+ * multi-device path); the per-rank product is the cycle product restricted to rows. */
+size_t apx_cycle_rows_workspace(int dtype, int64_t n, int64_t m_rows, int k_a, int k_b, int order);
+int apx_cycle_rows_phase(int phase, int dtype, const void* A_rows, int64_t m_rows, int64_t row0, const void* B,
+                         int64_t n, int k_a, int k_b, int order, void* M_rows, int32_t* sel_a, int32_t* sel_b,
+                         const double* red_in, double* red_out, double* scalars, void* ws, size_t ws_bytes,
+                         void* stream);
+
 /* sketch_norm_estimate (errest.py:139-154): out[0] = ||A (B G)||_F^2 with A m x n, B n x p, G p x k
  * (all fp64 row-major; G drawn on the host with numpy exactly as the reference draws it). The
  * caller divides by k. Complex operands are passed as their real embeddings (see errest.py). */

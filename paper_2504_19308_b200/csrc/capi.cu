@@ -131,6 +131,89 @@ static int run_cycle(const T* A, const T* B, int n, int ka, int kb, int order, c
 }
 
 // ------------------------------------------------------------------------------------------
+// row-sharded cycle product (C2 / C5 rows over ranks): rank g holds the row
+// block A_rows = A[r0:r0+m] and the whole B, and produces M[r0:r0+m]. A's cycle energies are
+// row-separable, so the only exchange before the product is the sum of the rank's energy
+// partials (n fp64); the selection is then made from identical sums on every rank, B's selection
+// from the (replicated) B. After the product, ||M_g||^2 is summed.
+// ------------------------------------------------------------------------------------------
+struct CycleRowsPlan {
+  double *partial, *nr_a, *en_b, *nr_b, *msq;
+  void *lam_a, *lam_b, *bhat, *xt, *tt;
+  int *jneg;
+  bool left_t;
+};
+
+static void plan_cycle_rows(Workspace& ws, CycleRowsPlan& p, int dtype, int n, int m, int ka, int kb, int order) {
+  const size_t e = dtype == F32 ? 4 : 8;
+  p.partial = ws.take<double>(cycle_energy_ws(n) / sizeof(double) + 1);
+  p.nr_a = ws.take<double>(n);
+  p.en_b = ws.take<double>(n);
+  p.nr_b = ws.take<double>(n);
+  p.msq = ws.take<double>(std::max<int>(m, kNumSMs * 4));
+  p.lam_a = ws.take<char>((size_t)std::max(ka, 1) * m * e);
+  p.lam_b = ws.take<char>((size_t)pad8(kb) * n * e);
+  p.bhat = order == 0 ? (void*)ws.take<char>((size_t)n * n * e) : nullptr;
+  p.left_t = left_via_transpose(n, e, ka);
+  p.xt = p.left_t ? (void*)ws.take<char>((size_t)n * n * e) : nullptr;
+  p.tt = p.left_t ? (void*)ws.take<char>((size_t)n * m * e) : nullptr;
+  p.jneg = ws.take<int>((size_t)pad8(ka));
+}
+
+__global__ void sqrt_vector_kernel(const double* __restrict__ e, int n, double* __restrict__ out) {
+  for (int j = blockIdx.x * blockDim.x + threadIdx.x; j < n; j += gridDim.x * blockDim.x) out[j] = sqrt(e[j]);
+}
+
+template <typename T>
+static int run_cycle_rows(int phase, const T* A, int m, int r0, const T* B, int n, int ka, int kb, int order, T* M,
+                          int* sa, int* sb, const double* red_in, double* red_out, double* scal,
+                          const CycleRowsPlan& p, cudaStream_t st) {
+  if (phase == 1) return launch_cycle_energies_rows<T>(A, m, r0, n, red_out, p.partial, st);
+  // phase 2: red_in = A's energies summed over the ranks
+  APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
+  sqrt_vector_kernel<<<(unsigned)std::min<int64_t>(ceil_div(n, 256), 1024), 256, 0, st>>>(red_in, n, p.nr_a);
+  APX_LAUNCH_CHECK();
+  APX_TRY(launch_topk(p.nr_a, n, ka, sa, st, p.nr_a, 1.0, scal + APX_S_KEPT_A, red_in, scal + APX_S_FRO2_A));
+  APX_TRY(launch_cycle_energies<T>(B, n, p.en_b, p.nr_b, nullptr, p.partial, st));
+  APX_TRY(launch_topk(p.nr_b, n, kb, sb, st, p.nr_b, 1.0, scal + APX_S_KEPT_B, p.en_b, scal + APX_S_FRO2_B));
+  T* la = (T*)p.lam_a;
+  T* lb = (T*)p.lam_b;
+  APX_TRY(launch_cycle_extract_rows<T>(A, m, r0, n, sa, ka, la, st));
+  APX_TRY(launch_cycle_extract<T>(B, n, sb, kb, lb, st, /*aligned=*/order == 1));
+  APX_TRY(zero_pad_rows<T>(lb, kb, n, st));
+  const T* X = B;
+  if (order == 0) {
+    APX_TRY(launch_cycle_materialize<T>(lb, sb, kb, n, (T*)p.bhat, st));
+    X = (const T*)p.bhat;
+  }
+  // term1 rows: Ahat[r0:r0+m] . X
+  if (ka == 0) {
+    APX_CUDA(cudaMemsetAsync(M, 0, (size_t)m * n * sizeof(T), st));
+  } else if (!p.left_t) {
+    APX_TRY(launch_cycle_left_gather_rows<T>(X, la, sa, ka, n, r0, r0 + m, M, st));
+  } else {
+    // (X^T Ahat^T)^T restricted to the output columns r0..r0+m of X^T Ahat^T
+    T *xt = (T*)p.xt, *tt = (T*)p.tt;
+    APX_TRY(launch_transpose_any(X, n, n, n, xt, n, st));
+    APX_TRY(launch_negate_shifts(sa, ka, n, p.jneg, st));
+    APX_TRY(launch_cycle_right_gather_cols<T>(xt, la, p.jneg, ka, n, n, r0, r0 + m, tt, st));
+    APX_TRY(launch_transpose_any(tt, m, n, m, M, n, st));
+  }
+  if (order == 1) {
+    // M_rows += dA_rows . Bhat (A's kept cycles masked on load, global row r0 + r) + ||M_g||^2
+    APX_TRY(launch_cycle_right_gather<T>(A, sa, ka, lb, sb, kb, n, m, 1, M, p.msq, nullptr, st, true, 0, nullptr, 1,
+                                         false, nullptr, false, r0));
+    const int rblocks = (int)ceil_div(m, right_gather_rows_plain(n, sizeof(T), kb));
+    APX_TRY(launch_sum_vector(p.msq, rblocks, red_out, st));
+  } else {
+    int parts = 0;
+    APX_TRY(launch_sumsq<T>(M, (size_t)m * n, p.msq, &parts, st));
+    APX_TRY(launch_sum_vector(p.msq, parts, red_out, st));
+  }
+  return OK;
+}
+
+// ------------------------------------------------------------------------------------------
 // mixed product plan: A by rSVD (l = k_svd columns, q power iterations), B by k_cyc cycles.
 //   order 1:  M = Q (Bm . dB) + A . Bhat      (== Ahat.B + dA.Bhat, Ahat = Q Q^T A = Q Bm)
 //   order 0:  M = Q (Bm . Bhat)               (== Ahat . Bhat)
@@ -626,6 +709,36 @@ int apx_cycle_first_order(int dtype, const void* A, const void* B, int64_t n, in
                             (float*)M, sel_a, sel_b, scalars, p, S(stream));
   return run_cycle<double>((const double*)A, (const double*)B, (int)n, k_a, k_b, order, force_sel_a, force_sel_b,
                            (double*)M, sel_a, sel_b, scalars, p, S(stream));
+}
+
+size_t apx_cycle_rows_workspace(int dtype, int64_t n, int64_t m_rows, int k_a, int k_b, int order) {
+  Workspace ws(nullptr, 0, true);
+  CycleRowsPlan p;
+  plan_cycle_rows(ws, p, dtype, (int)n, (int)m_rows, k_a, k_b, order);
+  return ws.off;
+}
+
+int apx_cycle_rows_phase(int phase, int dtype, const void* A_rows, int64_t m_rows, int64_t row0, const void* B,
+                         int64_t n, int k_a, int k_b, int order, void* M_rows, int32_t* sel_a, int32_t* sel_b,
+                         const double* red_in, double* red_out, double* scalars, void* wsp, size_t ws_bytes,
+                         void* stream) {
+  APX_REQUIRE(phase == 1 || phase == 2, "phase must be 1 or 2");
+  APX_REQUIRE(dtype == F32 || dtype == F64, "cycle product: real dtype required");
+  APX_REQUIRE(n >= 1 && n <= 46340, "n=%lld out of range", (long long)n);
+  APX_REQUIRE(m_rows >= 1 && row0 >= 0 && row0 + m_rows <= n, "row block [%lld, %lld) outside [0, %lld)",
+              (long long)row0, (long long)(row0 + m_rows), (long long)n);
+  APX_REQUIRE(k_a >= 0 && k_a <= n && k_b >= 0 && k_b <= n, "k out of range [0, %lld]", (long long)n);
+  APX_REQUIRE(order == 0 || order == 1, "order must be 0 or 1");
+  APX_REQUIRE(phase == 1 || red_in != nullptr, "phase 2 needs the summed energies");
+  Workspace ws(wsp, ws_bytes);
+  CycleRowsPlan p;
+  plan_cycle_rows(ws, p, dtype, (int)n, (int)m_rows, k_a, k_b, order);
+  APX_WS_CHECK(ws);
+  if (dtype == F32)
+    return run_cycle_rows<float>(phase, (const float*)A_rows, (int)m_rows, (int)row0, (const float*)B, (int)n, k_a,
+                                 k_b, order, (float*)M_rows, sel_a, sel_b, red_in, red_out, scalars, p, S(stream));
+  return run_cycle_rows<double>(phase, (const double*)A_rows, (int)m_rows, (int)row0, (const double*)B, (int)n, k_a,
+                                k_b, order, (double*)M_rows, sel_a, sel_b, red_in, red_out, scalars, p, S(stream));
 }
 
 int apx_debug_umma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,

@@ -27,17 +27,18 @@ __global__ void __launch_bounds__(256, 8) cycle_energy_partial(const T* __restri
                                                             double* __restrict__ partial,
                                                             unsigned* __restrict__ counters,
                                                             double* __restrict__ energies,
-                                                            double* __restrict__ norms) {
+                                                            double* __restrict__ norms, int m_rows, int row_off) {
   using Acc = T;
   pdl_trigger();
   const int j = blockIdx.x * blockDim.x + threadIdx.x;
   const int g = blockIdx.y;
   const int r0 = g * rows_per_chunk;
-  const int r1 = min(n, r0 + rows_per_chunk);
+  const int r1 = min(m_rows, r0 + rows_per_chunk);
   const bool valid = j < n;  // ragged last column block: idle threads still join the barriers
   if (valid) {
     Acc acc0 = 0, acc1 = 0, acc2 = 0, acc3 = 0;
-    int col = r0 - j;
+    // local rows [0, m_rows) are global rows row_off + r (a row block of a sharded operand)
+    int col = (r0 + row_off - j) % n;
     if (col < 0) col += n;
     const T* rowp = A + (size_t)r0 * n;
     int r = r0;
@@ -112,7 +113,7 @@ __global__ void __launch_bounds__(256) cycle_energy_finalize(const double* __res
 #pragma unroll
     for (int q = 0; q < 8; ++q) e += part[q][jx];
     energies[j] = e;
-    norms[j] = sqrt(e);
+    if (norms) norms[j] = sqrt(e);
   }
 }
 
@@ -154,12 +155,14 @@ __global__ void kept_energy_kernel(const double* __restrict__ norms, const int* 
 constexpr int kExtractT = 8;
 template <typename T, bool ALIGNED>
 __global__ void cycle_extract(const T* __restrict__ A, int n, const int* __restrict__ J, int k,
-                              T* __restrict__ lam) {
+                              T* __restrict__ lam, int m_rows, int row_off) {
   pdl_trigger();
   pdl_wait();
+  // left layout over local rows i < m_rows (global row row_off + i), table row stride m_rows;
+  // the aligned layout is always over all n columns (m_rows == n, row_off == 0)
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   const int t0 = blockIdx.y * kExtractT;
-  if (i >= n) return;
+  if (i >= m_rows) return;
   T v[kExtractT];
 #pragma unroll
   for (int u = 0; u < kExtractT; ++u) {
@@ -170,14 +173,14 @@ __global__ void cycle_extract(const T* __restrict__ A, int n, const int* __restr
       if (r >= n) r -= n;
       v[u] = A[(size_t)r * n + i];
     } else {
-      int c = i - __ldg(J + t);
+      int c = (i + row_off - __ldg(J + t)) % n;
       if (c < 0) c += n;
       v[u] = A[(size_t)i * n + c];
     }
   }
 #pragma unroll
   for (int u = 0; u < kExtractT; ++u)
-    if (t0 + u < k) lam[(size_t)(t0 + u) * n + i] = v[u];
+    if (t0 + u < k) lam[(size_t)(t0 + u) * m_rows + i] = v[u];
 }
 
 // Dense materialization of sum_t Lambda_t C^{J_t} (zero elsewhere).
@@ -206,7 +209,7 @@ __global__ void cycle_scatter_kernel(const T* __restrict__ lam, const int* __res
 template <typename T, int W>
 __global__ void __launch_bounds__(256) cycle_left_gather(const T* __restrict__ X, const T* __restrict__ lam,
                                                          const int* __restrict__ J, int k, int n, int accumulate,
-                                                         T* __restrict__ M) {
+                                                         T* __restrict__ M, int r_lo, int r_hi, int lam_ld) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   T* Xs = reinterpret_cast<T*>(smem_raw);
   constexpr int S = (W == 1) ? 1 : W + 1;  // padded row stride
@@ -229,13 +232,15 @@ __global__ void __launch_bounds__(256) cycle_left_gather(const T* __restrict__ X
   }
   for (int t = threadIdx.x; t < k; t += blockDim.x) sJ[t] = J[t];
   __syncthreads();
-  const int rows_per_group = (n + gridDim.y - 1) / gridDim.y;
-  const int rlo = blockIdx.y * rows_per_group, rhi = min(n, rlo + rows_per_group);
+  // output rows [r_lo, r_hi) (a sharded row block: lam holds those rows, stride lam_ld, and M
+  // row r - r_lo); the whole matrix is r_lo = 0, r_hi = n, lam_ld = n
+  const int rows_per_group = (r_hi - r_lo + gridDim.y - 1) / gridDim.y;
+  const int rlo = r_lo + blockIdx.y * rows_per_group, rhi = min(r_hi, rlo + rows_per_group);
   for (int r = rlo + threadIdx.x; r < rhi; r += blockDim.x) {
     T acc[W];
 #pragma unroll
     for (int q = 0; q < W; ++q) acc[q] = T(0);
-    const T* lp = lam + r;
+    const T* lp = lam + (r - r_lo);
     // 8 shifts' lambda loads in flight before their FMAs
     for (int t0 = 0; t0 < k; t0 += 8) {
       T l[8];
@@ -243,7 +248,7 @@ __global__ void __launch_bounds__(256) cycle_left_gather(const T* __restrict__ X
 #pragma unroll
       for (int u = 0; u < 8; ++u) {
         const int t = t0 + u;
-        l[u] = t < k ? __ldg(lp + (size_t)t * n) : T(0);
+        l[u] = t < k ? __ldg(lp + (size_t)t * lam_ld) : T(0);
         int sr = r - (t < k ? sJ[t] : 0);
         src[u] = sr < 0 ? sr + n : sr;
       }
@@ -254,7 +259,7 @@ __global__ void __launch_bounds__(256) cycle_left_gather(const T* __restrict__ X
         for (int q = 0; q < W; ++q) acc[q] = fma(l[u], xs[q], acc[q]);
       }
     }
-    T* mp = M + (size_t)r * n + c0;
+    T* mp = M + (size_t)(r - r_lo) * n + c0;
     for (int q = 0; q < wcols; ++q) mp[q] = accumulate ? mp[q] + acc[q] : acc[q];
   }
 }
@@ -324,7 +329,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
                                                           int n, int m_rows, int accumulate, T* __restrict__ M,
                                                           double* __restrict__ msq_partial,
                                                           double* __restrict__ xsq_partial, int* __restrict__ ticket,
-                                                          int* __restrict__ ready, int x_early) {
+                                                          int* __restrict__ ready, int x_early, int row_off) {
   constexpr int RP = gather_pitch(R, sizeof(T));
   // x_early: X (and the ticket / ready flags) predate the previous kernel of the stream, so under
   // a programmatic dependent launch the first row block is staged before waiting for that
@@ -425,7 +430,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
     if (JA != nullptr) {
       for (int e = threadIdx.x; e < rows * ka; e += blockDim.x) {
         const int rr = e / ka, t = e - rr * ka;
-        int m = r0 + rr - JA[t];
+        int m = (r0 + rr + row_off - JA[t]) % n;  // global row of local row r0 + rr
         if (m < 0) m += n;
         Xs[(size_t)m * RP + rr] = T(0);
       }
@@ -647,7 +652,8 @@ template <typename T, int R>
 __global__ void __launch_bounds__(kSegThreads, 1)
     cycle_right_gather_seg(const T* __restrict__ X, const int* __restrict__ JA, int ka, const T* __restrict__ lam,
                            const int* __restrict__ J, int k, int n, int m_rows, int accumulate, T* __restrict__ M,
-                           double* __restrict__ msq_partial, double* __restrict__ xsq_partial, int SW) {
+                           double* __restrict__ msq_partial, double* __restrict__ xsq_partial, int SW, int row_off,
+                           int c_lo, int c_hi, int lam_ld, int out_ld) {
   constexpr int RP = gather_pitch(R, sizeof(T));
   constexpr int CPT = seg_cpt<T>();
   constexpr int NP = (sizeof(T) == 4) ? R / 2 : 0;
@@ -700,7 +706,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
       __syncthreads();
       for (int e = threadIdx.x; e < rows * ka; e += blockDim.x) {
         const int rr = e / ka, t = e - rr * ka;
-        int m = r0 + rr - JA[t];
+        int m = (r0 + rr + row_off - JA[t]) % n;
         if (m < 0) m += n;
         if (m >= s0 && m < s0 + sw) Xs[(size_t)(m - s0) * RP + rr] = T(0);
       }
@@ -717,7 +723,9 @@ __global__ void __launch_bounds__(kSegThreads, 1)
     const int lane = threadIdx.x & 31;
     constexpr int CW = 32 * CPT;  // a warp's column chunk: lane + 32 q, q < CPT
     const T* xlane = Xs + (size_t)lane * RP;
-    for (int cw = (threadIdx.x >> 5) * CW; cw < n; cw += (blockDim.x >> 5) * CW) {
+    // output columns [c_lo, c_hi) (all n, or a sharded block); lambda' column c at lam_c[c - c_lo]
+    // in rows of stride lam_ld; M column c at M_c[c - c_lo] in rows of stride out_ld
+    for (int cw = c_lo + (threadIdx.x >> 5) * CW; cw < c_hi; cw += (blockDim.x >> 5) * CW) {
       // The chunk's source window under shift J is [m0, m0 + CW), m0 = (cw + J) mod n.
       //  interior: the window lies inside the segment (m0 in [s0, s0 + sw - CW]): one warp-uniform
       //            offset, no per-lane checks;
@@ -739,15 +747,16 @@ __global__ void __launch_bounds__(kSegThreads, 1)
       };
       int f_int, f_lo, f_hi;
       const int c_int = run(s0 - cw, sw - CW + 1, f_int);
-      const int c_lo = run(s0 - CW + 1 - cw, CW - 1, f_lo);
-      const int c_hi = nseg > 1 ? run(s0 + sw - CW + 1 - cw, CW - 1, f_hi) : 0;
+      const int n_blo = run(s0 - CW + 1 - cw, CW - 1, f_lo);
+      const int n_bhi = nseg > 1 ? run(s0 + sw - CW + 1 - cw, CW - 1, f_hi) : 0;
       // the chunk's M lines toward L2 (read back by the epilogue)
       if (s > 0 || accumulate != 0) {
 #pragma unroll
         for (int q = 0; q < CPT; ++q)
 #pragma unroll
           for (int rr = 0; rr < R; ++rr)
-            if (rr < rows) asm volatile("prefetch.global.L2 [%0];" ::"l"(M + (size_t)(r0 + rr) * n + cw + 32 * q + lane));
+            if (rr < rows)
+              asm volatile("prefetch.global.L2 [%0];" ::"l"(M + (size_t)(r0 + rr) * out_ld + (cw - c_lo) + 32 * q + lane));
       }
       unsigned long long acc2[CPT][NP > 0 ? NP : 1];
       T accs[CPT][NS > 0 ? NS : 1];
@@ -782,7 +791,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
           unsigned m = (unsigned)(cw + jt.x);
           m = min(m, m - (unsigned)n);  // (cw + J) mod n
           off[u] = in ? (int)(m - (unsigned)s0) * RP : 0;
-          const T* lrow = lam + (size_t)jt.y * n + cw + lane;
+          const T* lrow = lam + (size_t)jt.y * lam_ld + (cw - c_lo) + lane;
 #pragma unroll
           for (int q = 0; q < CPT; ++q) lv[u][q] = in ? ldg_nc_hint(lrow + 32 * q, pol_keep) : T(0);
         }
@@ -811,7 +820,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
           int i = first + e;
           i = i >= k ? i - k : i;
           const int2 jt = sJT[i];
-          const T* lrow = lam + (size_t)jt.y * n;
+          const T* lrow = lam + (size_t)jt.y * lam_ld;
           T lv[CPT];
           unsigned l[CPT];
 #pragma unroll
@@ -822,14 +831,14 @@ __global__ void __launch_bounds__(kSegThreads, 1)
             const unsigned d = m - (unsigned)s0;
             const bool ok = d < (unsigned)sw;
             l[q] = ok ? d : 0u;
-            lv[q] = ok ? __ldg(lrow + c) : T(0);
+            lv[q] = ok ? __ldg(lrow + (c - c_lo)) : T(0);
           }
 #pragma unroll
           for (int q = 0; q < CPT; ++q) fma_rows(q, Xs + (size_t)l[q] * RP, lv[q]);
         }
       };
-      boundary(f_lo, c_lo);
-      boundary(f_hi, c_hi);
+      boundary(f_lo, n_blo);
+      boundary(f_hi, n_bhi);
       // M (+)= the segment's partial sums: the first segment applies `accumulate`, later ones
       // add (subtract for accumulate < 0); all old values are loaded before the first store
       T old[CPT][R];
@@ -837,7 +846,9 @@ __global__ void __launch_bounds__(kSegThreads, 1)
       for (int q = 0; q < CPT; ++q)
 #pragma unroll
         for (int rr = 0; rr < R; ++rr)
-          old[q][rr] = (rr < rows && (s > 0 || accumulate != 0)) ? ldg_hint(M + (size_t)(r0 + rr) * n + cw + 32 * q + lane, pol_stream) : T(0);
+          old[q][rr] = (rr < rows && (s > 0 || accumulate != 0))
+                           ? ldg_hint(M + (size_t)(r0 + rr) * out_ld + (cw - c_lo) + 32 * q + lane, pol_stream)
+                           : T(0);
 #pragma unroll
       for (int q = 0; q < CPT; ++q)
 #pragma unroll
@@ -855,7 +866,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
           }
           if (rr < rows) {
             const T v = accumulate < 0 ? old[q][rr] - a : old[q][rr] + a;
-            stg_hint(M + (size_t)(r0 + rr) * n + cw + 32 * q + lane, v, pol_stream);
+            stg_hint(M + (size_t)(r0 + rr) * out_ld + (cw - c_lo) + 32 * q + lane, v, pol_stream);
             if (last) msq += (double)v * (double)v;
           }
         }
@@ -947,7 +958,7 @@ int launch_cycle_energies(const T* A, int n, double* energies, double* norms, do
   const unsigned cb = (unsigned)ceil_div(n, 256);
   dim3 grid(cb, (unsigned)groups);
   // separate finalize: the fused last-CTA reduce (counters != nullptr) measured 63 us vs 44 + 7
-  cycle_energy_partial<T><<<grid, 256, 0, st>>>(A, n, rpc, partial, nullptr, energies, norms);
+  cycle_energy_partial<T><<<grid, 256, 0, st>>>(A, n, rpc, partial, nullptr, energies, norms, n, 0);
   APX_LAUNCH_CHECK();
   APX_CUDA(launch_pdl(cycle_energy_finalize, dim3((unsigned)ceil_div(n, 32)), dim3(256), 0, st, partial, n, groups,
                       energies, norms));
@@ -956,6 +967,24 @@ int launch_cycle_energies(const T* A, int n, double* energies, double* norms, do
     sum_vector_kernel<<<1, 1024, 0, st>>>(energies, n, fro2);
     APX_LAUNCH_CHECK();
   }
+  return OK;
+}
+
+// energies over a row block (local rows [0, m), global rows row_off + r) of an n x n operand:
+// the partial vector a row-sharded product sums over ranks (no norms)
+template <typename T>
+int launch_cycle_energies_rows(const T* A, int m, int row_off, int n, double* energies, double* partial,
+                               cudaStream_t st) {
+  const unsigned cb = (unsigned)ceil_div(n, 256);
+  const int groups = std::max(1, std::min({(kNumSMs * 8) / (int)cb, (int)ceil_div(m, 16), 40}));
+  const int rpc = (int)ceil_div(m, groups);
+  const int g = (int)ceil_div(m, rpc);
+  cycle_energy_partial<T><<<dim3(cb, (unsigned)g), 256, 0, st>>>(A, n, rpc, partial, nullptr, energies, nullptr, m,
+                                                                 row_off);
+  APX_LAUNCH_CHECK();
+  APX_CUDA(launch_pdl(cycle_energy_finalize, dim3((unsigned)ceil_div(n, 32)), dim3(256), 0, st, partial, n, g, energies,
+                      (double*)nullptr));
+  APX_LAUNCH_CHECK();
   return OK;
 }
 
@@ -979,9 +1008,19 @@ int launch_cycle_extract(const T* A, int n, const int* J, int k, T* lam, cudaStr
   if (k <= 0) return OK;
   dim3 grid((unsigned)ceil_div(n, 256), (unsigned)ceil_div(k, kExtractT));
   if (aligned)
-    APX_CUDA(launch_pdl(cycle_extract<T, true>, grid, dim3(256), 0, st, A, n, J, k, lam));
+    APX_CUDA(launch_pdl(cycle_extract<T, true>, grid, dim3(256), 0, st, A, n, J, k, lam, n, 0));
   else
-    APX_CUDA(launch_pdl(cycle_extract<T, false>, grid, dim3(256), 0, st, A, n, J, k, lam));
+    APX_CUDA(launch_pdl(cycle_extract<T, false>, grid, dim3(256), 0, st, A, n, J, k, lam, n, 0));
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+// left-layout lambdas of a row block (local rows [0, m), global row_off + i): k x m table
+template <typename T>
+int launch_cycle_extract_rows(const T* A, int m, int row_off, int n, const int* J, int k, T* lam, cudaStream_t st) {
+  if (k <= 0) return OK;
+  dim3 grid((unsigned)ceil_div(m, 256), (unsigned)ceil_div(k, kExtractT));
+  cycle_extract<T, false><<<grid, 256, 0, st>>>(A, n, J, k, lam, m, row_off);
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -1001,15 +1040,19 @@ int launch_cycle_materialize(const T* lam, const int* J, int k, int n, T* out, c
 constexpr size_t kSmemBudget = 200 * 1024;
 
 template <typename T, int W>
-static int left_gather_w(const T* X, const T* lam, const int* J, int k, int n, int acc, T* M, cudaStream_t st) {
+static int left_gather_w(const T* X, const T* lam, const int* J, int k, int n, int acc, T* M, cudaStream_t st,
+                         int r_lo = 0, int r_hi = -1, int lam_ld = -1) {
+  if (r_hi < 0) r_hi = n;
+  if (lam_ld < 0) lam_ld = n;
   constexpr int S = (W == 1) ? 1 : W + 1;
   const size_t smem = (size_t)n * S * sizeof(T) + (size_t)std::max(k, 1) * sizeof(int);
   APX_TRY(set_smem<T>((const void*)cycle_left_gather<T, W>, smem));
   const int strips = (int)ceil_div(n, W);
   int groups = 1;
-  if (strips < 2 * kNumSMs) groups = std::min<int>((int)ceil_div(2 * kNumSMs, strips), std::max(1, n / 256));
+  const int rows = r_hi - r_lo;
+  if (strips < 2 * kNumSMs) groups = std::min<int>((int)ceil_div(2 * kNumSMs, strips), std::max(1, rows / 256));
   dim3 grid((unsigned)strips, (unsigned)groups);
-  cycle_left_gather<T, W><<<grid, 256, smem, st>>>(X, lam, J, k, n, acc, M);
+  cycle_left_gather<T, W><<<grid, 256, smem, st>>>(X, lam, J, k, n, acc, M, r_lo, r_hi, lam_ld);
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -1052,10 +1095,29 @@ int launch_cycle_left_gather(const T* X, const T* lam, const int* J, int k, int 
   }
 }
 
+// output rows [r_lo, r_hi) of Ahat . X into M_rows ((r_hi - r_lo) x n); lam: k x (r_hi - r_lo)
+// left-layout table of those rows. Strip path only (left_via_transpose false).
+template <typename T>
+int launch_cycle_left_gather_rows(const T* X, const T* lam, const int* J, int k, int n, int r_lo, int r_hi, T* M_rows,
+                                  cudaStream_t st) {
+  const size_t per_col = (size_t)n * sizeof(T);
+  int w = 1;
+  while (w < 8 && (size_t)(2 * w + 1) * per_col <= kSmemBudget) w *= 2;
+  APX_REQUIRE((size_t)(w == 1 ? 1 : w + 1) * per_col <= 227 * 1024, "n=%d too large for the left gather strip", n);
+  const int ld = r_hi - r_lo;
+  switch (w) {
+    case 1: return left_gather_w<T, 1>(X, lam, J, k, n, 0, M_rows, st, r_lo, r_hi, ld);
+    case 2: return left_gather_w<T, 2>(X, lam, J, k, n, 0, M_rows, st, r_lo, r_hi, ld);
+    case 4: return left_gather_w<T, 4>(X, lam, J, k, n, 0, M_rows, st, r_lo, r_hi, ld);
+    default: return left_gather_w<T, 8>(X, lam, J, k, n, 0, M_rows, st, r_lo, r_hi, ld);
+  }
+}
+
 template <typename T, int R>
 static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int m_rows,
                           int acc, T* M, double* msq_partial, double* xsq_partial, bool lam_padded, int max_ctas,
-                          int* ticket, int col_chunks, bool trunc, int* ready, bool x_early, cudaStream_t st) {
+                          int* ticket, int col_chunks, bool trunc, int* ready, bool x_early, int row_off,
+                          cudaStream_t st) {
   constexpr int U = APX_GATHER_U, CPT = APX_GATHER_CPT;
   const int kp = (int)ceil_div(std::max(k, 1), U) * U;
   const size_t smem = (size_t)gather_pitch(R, sizeof(T)) * n * sizeof(T) + (size_t)kp * sizeof(int);
@@ -1080,10 +1142,10 @@ static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const
     APX_TRY(set_smem<T>((const void*)kern, smem));
     if (x_early) {
       APX_CUDA(launch_pdl(kern, grid, dim3(threads), smem, st, X, JA, ka, lam, J, k, n, m_rows, acc, M, msq_partial,
-                          xsq_partial, ticket, ready, 1));
+                          xsq_partial, ticket, ready, 1, row_off));
     } else {
       kern<<<grid, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M, msq_partial, xsq_partial, ticket,
-                                        ready, 0);
+                                        ready, 0, row_off);
     }
     APX_LAUNCH_CHECK();
     return OK;
@@ -1132,13 +1194,17 @@ int right_gather_rows_plain(int n, size_t elem, int k) {
 
 template <typename T, int R>
 static int right_gather_seg_r(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n,
-                              int m_rows, int acc, T* M, double* msq_partial, double* xsq_partial, cudaStream_t st) {
+                              int m_rows, int acc, T* M, double* msq_partial, double* xsq_partial, cudaStream_t st,
+                              int row_off = 0, int c_lo = 0, int c_hi = -1, int lam_ld = -1, int out_ld = -1) {
+  if (c_hi < 0) c_hi = n;
+  if (lam_ld < 0) lam_ld = n;
+  if (out_ld < 0) out_ld = n;
   const int SW = seg_width(n, sizeof(T), k, R);
   const size_t smem = (size_t)gather_pitch(R, sizeof(T)) * SW * sizeof(T) + (size_t)2 * k * sizeof(int);
   auto kern = cycle_right_gather_seg<T, R>;
   APX_TRY(set_smem<T>((const void*)kern, smem));
   kern<<<(unsigned)ceil_div(m_rows, R), kSegThreads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M, msq_partial,
-                                                                 xsq_partial, SW);
+                                                                 xsq_partial, SW, row_off, c_lo, c_hi, lam_ld, out_ld);
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -1151,14 +1217,18 @@ template <typename T>
 int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n,
                               int m_rows, int accumulate, T* M, double* msq_partial, double* xsq_partial,
                               cudaStream_t st, bool lam_padded, int max_ctas, int* ticket, int col_chunks,
-                              bool tf32_operands, int* ready, bool x_early) {
+                              bool tf32_operands, int* ready, bool x_early, int row_off) {
   const int rs = right_gather_seg_rows(n, sizeof(T), k);
   if (rs > 0 && !(max_ctas > 0 && ticket) && ready == nullptr && !(tf32_operands && sizeof(T) == 4)) {
     switch (rs) {
-      case 2: return right_gather_seg_r<T, 2>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, st);
-      case 4: return right_gather_seg_r<T, 4>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, st);
-      case 6: return right_gather_seg_r<T, 6>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, st);
-      default: return right_gather_seg_r<T, 8>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, st);
+      case 2: return right_gather_seg_r<T, 2>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, st,
+                                              row_off);
+      case 4: return right_gather_seg_r<T, 4>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, st,
+                                              row_off);
+      case 6: return right_gather_seg_r<T, 6>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, st,
+                                              row_off);
+      default: return right_gather_seg_r<T, 8>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, st,
+                                              row_off);
     }
   }
   const int r = right_gather_rows(n, sizeof(T), k);
@@ -1166,7 +1236,7 @@ int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, c
               "n=%d too large for the right gather row block", n);
 #define APX_RG(RV) \
   return right_gather_r<T, RV>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, lam_padded, \
-                               max_ctas, ticket, col_chunks, tf32_operands, ready, x_early, st)
+                               max_ctas, ticket, col_chunks, tf32_operands, ready, x_early, row_off, st)
   switch (r) {
     case 1: APX_RG(1);
     case 2: APX_RG(2);
@@ -1178,6 +1248,25 @@ int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, c
     default: APX_RG(8);
   }
 #undef APX_RG
+}
+
+// Output columns [c_lo, c_hi) of X . Bhat for all m_rows rows of X, through the segmented gather
+// (any n that is a multiple of 512; c_lo, c_hi multiples of its 32 * CPT-column chunks):
+// lam: k x (c_hi - c_lo) column-aligned table of those columns; M: m_rows x (c_hi - c_lo).
+template <typename T>
+int launch_cycle_right_gather_cols(const T* X, const T* lam, const int* J, int k, int n, int m_rows, int c_lo,
+                                   int c_hi, T* M, cudaStream_t st) {
+  constexpr int CW = 32 * seg_cpt<T>();
+  APX_REQUIRE(n % kSegThreads == 0 && c_lo % CW == 0 && c_hi % CW == 0 && 0 <= c_lo && c_lo < c_hi && c_hi <= n,
+              "column-block gather needs n %% %d == 0 and %d-aligned blocks, got n=%d [%d, %d)", kSegThreads, CW, n,
+              c_lo, c_hi);
+  const int w = c_hi - c_lo;
+  switch (seg_rows(sizeof(T))) {
+    case 2: return right_gather_seg_r<T, 2>(X, nullptr, 0, lam, J, k, n, m_rows, 0, M, nullptr, nullptr, st, 0, c_lo, c_hi, w, w);
+    case 4: return right_gather_seg_r<T, 4>(X, nullptr, 0, lam, J, k, n, m_rows, 0, M, nullptr, nullptr, st, 0, c_lo, c_hi, w, w);
+    case 6: return right_gather_seg_r<T, 6>(X, nullptr, 0, lam, J, k, n, m_rows, 0, M, nullptr, nullptr, st, 0, c_lo, c_hi, w, w);
+    default: return right_gather_seg_r<T, 8>(X, nullptr, 0, lam, J, k, n, m_rows, 0, M, nullptr, nullptr, st, 0, c_lo, c_hi, w, w);
+  }
 }
 
 template <typename T>
@@ -1201,8 +1290,12 @@ int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st) {
   template int launch_cycle_materialize<T>(const T*, const int*, int, int, T*, cudaStream_t);                 \
   template int launch_cycle_left_gather<T>(const T*, const T*, const int*, int, int, int, T*, cudaStream_t);  \
   template int launch_cycle_right_gather<T>(const T*, const int*, int, const T*, const int*, int, int, int, int, T*, \
-                                            double*, double*, cudaStream_t, bool, int, int*, int, bool, int*, bool); \
-  template int launch_sumsq<T>(const T*, size_t, double*, int*, cudaStream_t);
+                                            double*, double*, cudaStream_t, bool, int, int*, int, bool, int*, bool, int); \
+  template int launch_sumsq<T>(const T*, size_t, double*, int*, cudaStream_t);                               \
+  template int launch_cycle_energies_rows<T>(const T*, int, int, int, double*, double*, cudaStream_t);       \
+  template int launch_cycle_extract_rows<T>(const T*, int, int, int, const int*, int, T*, cudaStream_t);      \
+  template int launch_cycle_left_gather_rows<T>(const T*, const T*, const int*, int, int, int, int, T*, cudaStream_t); \
+  template int launch_cycle_right_gather_cols<T>(const T*, const T*, const int*, int, int, int, int, int, T*, cudaStream_t);
 APX_INST(float)
 APX_INST(double)
 

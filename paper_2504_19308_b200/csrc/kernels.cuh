@@ -31,7 +31,20 @@ template <typename T>
 int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int m_rows,
                               int accumulate, T* M, double* msq_partial, double* xsq_partial, cudaStream_t st,
                               bool lam_padded = false, int max_ctas = 0, int* ticket = nullptr, int col_chunks = 1,
-                              bool tf32_operands = false, int* ready = nullptr, bool x_early = false);
+                              bool tf32_operands = false, int* ready = nullptr, bool x_early = false,
+                              int row_off = 0);
+// ---- row-sharded cycle product (local rows [0, m) of an n x n operand = global rows row_off + r)
+template <typename T>
+int launch_cycle_energies_rows(const T* A, int m, int row_off, int n, double* energies, double* partial,
+                               cudaStream_t st);
+template <typename T>
+int launch_cycle_extract_rows(const T* A, int m, int row_off, int n, const int* J, int k, T* lam, cudaStream_t st);
+template <typename T>
+int launch_cycle_left_gather_rows(const T* X, const T* lam, const int* J, int k, int n, int r_lo, int r_hi, T* M_rows,
+                                  cudaStream_t st);
+template <typename T>
+int launch_cycle_right_gather_cols(const T* X, const T* lam, const int* J, int k, int n, int m_rows, int c_lo,
+                                   int c_hi, T* M, cudaStream_t st);
 template <typename T>
 int launch_sumsq(const T* x, size_t cnt, double* partial, int* nparts, cudaStream_t st);
 int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st);

@@ -1,4 +1,6 @@
-"""The C4 mixed product sharded by rows of A and M over ranks (BASELINE config 4).
+"""Products sharded by rows of A and M over ranks: the C4 mixed product
+(BASELINE config 4) and the cycle product (configs 2 and 5; ``cycle_rows_steps``, whose only
+exchange before the product is the sum of the ranks' cycle-energy partials of A).
 
 Rank g holds the row block A_g = A[r0:r1] and the whole B; it produces M[r0:r1]. The per-rank plan
 is the single-device plan of apx_mixed_first_order (B's cycle decomposition and the persistent row
@@ -82,6 +84,62 @@ def mixed_rows_steps(A_rows, B, k_svd: int, k_cyc: int, order: int, omega, out=N
     scal[N.S_FRO2_A] = fin[0]  # device-side copies: no host synchronisation inside the product
     scal[N.S_FRO2_M] = fin[1]
     return {"M": M, "sel_b": sb[:k_cyc], "scalars": scal, "breakdown": fin[2], "ws": ws}
+
+
+def cycle_row_range(n: int, world: int, rank: int, align: int = 128) -> tuple[int, int]:
+    """Row block of `rank` for the sharded cycle product: boundaries r * n / world rounded to a
+    multiple of `align` (the column chunk of the large-n left product, 128 fp32 / 64 fp64)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+
+    def cut(r):
+        return n if r == world else min(n, align * round(r * n / (align * world)))
+
+    return cut(rank), cut(rank + 1)
+
+
+def cycle_rows_steps(A_rows, row0: int, B, k_a: int, k_b: int, order: int, out=None):
+    """One rank's share of the cycle product (C2 / C5 sharded by rows). A_rows
+    (m x n, global rows row0..row0+m) and B (n x n): device tensors of one real dtype. Yields the
+    tensor to be summed over ranks at each exchange point -- A's cycle energies over the rank's
+    rows (n fp64), then [||M_g||^2] -- and returns dict(M=rows of M, sel_a, sel_b, scalars)."""
+    m, n = A_rows.shape
+    if tuple(B.shape) != (n, n) or B.dtype != A_rows.dtype:
+        raise ValueError(f"B must be {n} x {n} of A's dtype, got {tuple(B.shape)} {B.dtype}")
+    if order not in (0, 1):
+        raise ValueError("order must be 0 or 1")
+    if A_rows.dtype not in (torch.float32, torch.float64):
+        raise ValueError("real fp32 / fp64 operands required")
+    code = N.APX_F32 if A_rows.dtype == torch.float32 else N.APX_F64
+    dev = A_rows.device
+    M = out if out is not None else torch.empty((m, n), dtype=A_rows.dtype, device=dev)
+    sa = torch.empty(max(k_a, 1), dtype=torch.int32, device=dev)
+    sb = torch.empty(max(k_b, 1), dtype=torch.int32, device=dev)
+    scal = torch.zeros(N.NSCALARS, dtype=torch.float64, device=dev)
+    ws = D.workspace(N.size("apx_cycle_rows_workspace", code, n, m, k_a, k_b, order))
+    energies = torch.empty(n, dtype=torch.float64, device=dev)
+    fin = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def phase(i, red_in, red_out):
+        N.call("apx_cycle_rows_phase", i, code, A_rows.data_ptr(), m, row0, B.data_ptr(), n, k_a, k_b, order,
+               M.data_ptr(), sa.data_ptr(), sb.data_ptr(), D.ptr(red_in), red_out.data_ptr(), scal.data_ptr(),
+               ws.data_ptr(), ws.numel(), D.stream_ptr())
+
+    phase(1, None, energies)
+    yield energies
+    phase(2, energies, fin)
+    yield fin
+    scal[N.S_FRO2_M] = fin[0]
+    return {"M": M, "sel_a": sa[:k_a], "sel_b": sb[:k_b], "scalars": scal, "ws": ws}
+
+
+def cycle_product_rows(A_rows, row0: int, B, k_a: int, k_b: int, order: int, group=None, out=None):
+    """This rank's rows of the cycle product; the two exchanges are torch.distributed all-reduces
+    (NCCL on the current stream for CUDA tensors)."""
+    import torch.distributed as dist
+
+    return _drive(cycle_rows_steps(A_rows, row0, B, k_a, k_b, order, out),
+                  lambda t: dist.all_reduce(t, group=group))
 
 
 def check_breakdown(result):

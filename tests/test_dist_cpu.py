@@ -119,3 +119,74 @@ def test_row_range_partition():
             assert all(abs(z - n / world) <= 64 for z in sizes)
     with pytest.raises(ValueError):
         row_range(128, 2, 2)
+
+
+# ---- the row-sharded cycle product's protocol (sharded.cycle_rows_steps) over gloo ----
+# Device phases replaced by the oracle restatement on CPU (test-only stand-ins): the rank's cycle
+# energy partials -> all-reduce -> selection from the summed energies -> the rank's product rows
+# (oracle.cycle_product_rows) -> all-reduce of ||M_g||^2. The concatenated rows must equal the
+# unsharded oracle product, and every rank must select the same cycles.
+
+def _toy_cycle_rows_steps(A, B, r0, r1, k):
+    import numpy as np
+    import oracle as O
+    n = A.shape[0]
+    i = np.arange(r0, r1)
+    e = torch.zeros(n, dtype=torch.float64)
+    for j in range(n):
+        e[j] = float(np.sum(A[i, (i - j) % n] ** 2))
+    yield e                                            # energy partials -> sum over ranks
+    JA = O.top_indices(np.sqrt(e.numpy()), k)
+    JB, lamB, _, _, _ = O.cycle_decompose(B, k)
+    rows = np.arange(r0, r1)
+    Mg = O.cycle_product_rows(rows, A[rows], JA, [B[(rows - j) % n] for j in JA], JB, lamB)
+    fin = torch.tensor([float(np.sum(Mg ** 2))], dtype=torch.float64)
+    yield fin                                          # ||M_g||^2 -> sum over ranks
+    return JA, Mg, float(fin[0])
+
+
+def _sharded_cycle_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle as O
+        from paper_2504_19308_b200.sharded import _drive, cycle_row_range
+        n, k = 256, 8
+        A, B = O.gen_cycle_operand(n, k, 31), O.gen_cycle_operand(n, k, 32)
+        r0, r1 = cycle_row_range(n, world, rank, align=64)
+        JA, Mg, fro2 = _drive(_toy_cycle_rows_steps(A, B, r0, r1, k), lambda t: dist.all_reduce(t))
+        q.put((rank, r0, r1, JA, Mg, fro2))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_sharded_cycle_protocol_gloo():
+    import numpy as np
+    import oracle as O
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_cycle_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted((q.get(timeout=120) for _ in range(world)), key=lambda o: o[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n, k = 256, 8
+    A, B = O.gen_cycle_operand(n, k, 31), O.gen_cycle_operand(n, k, 32)
+    M, rep = O.cycle_first_order_multiply(A, B, k, 1)
+    assert [o[1:3] for o in out] == [(0, 128), (128, 256)]
+    assert out[0][3] == out[1][3] == rep["selected_a"]
+    got = np.concatenate([o[4] for o in out], axis=0)
+    assert np.linalg.norm(got - M) <= 1e-12 * np.linalg.norm(M)
+    assert out[0][5] == out[1][5] == pytest.approx(float(np.sum(M ** 2)), rel=1e-12)
+
+
+def test_cycle_row_range_partition():
+    from paper_2504_19308_b200.sharded import cycle_row_range
+    for n, align in ((2048, 64), (16384, 128), (32768, 128)):
+        for world in (1, 2, 3, 4, 8):
+            blocks = [cycle_row_range(n, world, r, align) for r in range(world)]
+            assert blocks[0][0] == 0 and blocks[-1][1] == n
+            assert all(a[1] == b[0] and a[0] % align == 0 for a, b in zip(blocks, blocks[1:]))
