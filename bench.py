@@ -56,7 +56,7 @@ def gather_capture():
     `ncu --set full` capture (profiles/r*_gather_ncu.txt), or None."""
     import glob
     import re
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r*_gather_ncu.txt")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "r[0-9][0-9]_gather_ncu.txt")))
     if not files:
         return None
     vals = {}

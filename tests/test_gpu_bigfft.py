@@ -85,18 +85,31 @@ def _run_child(tmp_path, big):
 def test_four_step_path_matches_fused_and_oracle(tmp_path):
     big = _run_child(tmp_path, True)
     fused = _run_child(tmp_path, False)
-    for key in big:
-        if key.startswith("sel"):
-            assert np.array_equal(big[key], fused[key]), key
-        else:
-            assert rel(big[key], fused[key]) < 1e-12, key
+    from test_gpu_circulant import near_tie_ok
+    tied = set()
     for n, k in ((256, 5), (1024, 5), (300, 5), (997, 4)):
         A = O.gen_circulant_operand(n, 6, 11 + n)
         B = O.gen_circulant_operand(n, 6, 12 + n)
+        _, ma = O.circulant_decompose(A)
+        _, mb = O.circulant_decompose(B)
         for order in (0, 1):
-            sel = [int(v) for v in big[f"sel{n}_{order}"]]
-            Mo, _ = _oracle_with_protocol(A, B, k, order, sel[:k], sel[k:])
-            assert rel(big[f"M{n}_{order}"], Mo) < 1e-10
+            key = f"sel{n}_{order}"
+            sb, sf = [int(v) for v in big[key]], [int(v) for v in fused[key]]
+            # the two transforms round differently, so an exact conjugate-pair tie (t, n - t of a
+            # real operand) may break either way: allowed only as a near tie
+            if sb != sf:
+                near_tie_ok(sb[:k], sf[:k], ma)
+                near_tie_ok(sb[k:], sf[k:], mb)
+                tied.add(f"M{n}_{order}")
+            for out in (big, fused):
+                sel = [int(v) for v in out[key]]
+                Mo, _ = _oracle_with_protocol(A, B, k, order, sel[:k], sel[k:])
+                assert rel(out[f"M{n}_{order}"], Mo) < 1e-10
+    for key in big:
+        if not key.startswith("sel") and key not in tied:
+            assert rel(big[key], fused[key]) < 1e-12, key
+    for n, k in ((256, 5), (1024, 5), (300, 5), (997, 4)):
+        A = O.gen_circulant_operand(n, 6, 11 + n)
         S, mags = O.circulant_decompose(A)
         assert rel(big[f"cols{n}"], S) < 1e-12
         assert rel(big[f"mags{n}"], mags) < 1e-12
