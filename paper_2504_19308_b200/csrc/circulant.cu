@@ -11,6 +11,7 @@
 #include "../../include/apx.h"
 #include "common.cuh"
 #include "fft.cuh"
+#include <type_traits>
 #include "kernels.cuh"
 
 namespace apx {
@@ -239,6 +240,9 @@ __global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B
   const int c0 = 2 * blockIdx.x;
   const bool two = c0 + 1 < n;
   const double rs = rsqrt((double)n);
+  // real B: the two columns travel as one complex sequence b0 + i b1 through ONE forward
+  // transform Z, split afterwards as FB0[p] = (Z[p] + conj Z[-p]) / 2, FB1[p] = (Z[p] - conj Z[-p]) / 2i
+  constexpr bool kPack = std::is_same<T, double>::value;
   for (int p0 = threadIdx.x; p0 < n; p0 += 4 * blockDim.x) {
     double2 v0[4], v1[4];
 #pragma unroll
@@ -251,30 +255,63 @@ __global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B
     for (int u = 0; u < 4; ++u) {
       const int p = p0 + u * blockDim.x;
       if (p < n) {
-        x0[fsw(p, n)] = v0[u];
-        x1[fsw(p, n)] = v1[u];
+        if constexpr (kPack) {
+          x0[fsw(p, n)] = make_double2(v0[u].x, v1[u].x);
+        } else {
+          x0[fsw(p, n)] = v0[u];
+          x1[fsw(p, n)] = v1[u];
+        }
       }
     }
   }
   __syncthreads();
   fft_block(x0, scratch, n, roots, false);
-  fft_block(x1, scratch, n, roots, false);
-  double2 y0[kPP], y1[kPP];
+  if constexpr (kPack) {
+    double2 f0[kPP];  // FB1 goes straight to x1; FB0 waits in registers until every Z read is done
 #pragma unroll
-  for (int i = 0; i < kPP; ++i) {
-    const int p = threadIdx.x + i * blockDim.x;
-    double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
-    if (p < n) {
-      for (int q = 0; q < k; ++q) {
-        int src = p - s_sel[q];
-        if (src < 0) src += n;
-        const double2 l = __ldg(L + (size_t)q * n + p);
-        a0 = cadd(a0, cmul(l, cscale(x0[fsw(src, n)], rs)));
-        a1 = cadd(a1, cmul(l, cscale(x1[fsw(src, n)], rs)));
+    for (int i = 0; i < kPP; ++i) {
+      const int p = threadIdx.x + i * blockDim.x;
+      if (p < n) {
+        const double2 z = x0[fsw(p, n)], zm = x0[fsw(p == 0 ? 0 : n - p, n)];
+        f0[i] = make_double2(0.5 * (z.x + zm.x), 0.5 * (z.y - zm.y));
+        x1[fsw(p, n)] = make_double2(0.5 * (z.y + zm.y), 0.5 * (zm.x - z.x));
       }
     }
-    y0[i] = a0;
-    y1[i] = a1;
+    __syncthreads();
+#pragma unroll
+    for (int i = 0; i < kPP; ++i) {
+      const int p = threadIdx.x + i * blockDim.x;
+      if (p < n) x0[fsw(p, n)] = f0[i];
+    }
+    __syncthreads();
+  } else {
+    fft_block(x1, scratch, n, roots, false);
+  }
+  // term-major: the kPP positions' L_t loads (L2) of one term are independent, so all are in
+  // flight together (position-major, each thread waited one L2 latency per term and position);
+  // every position still sums its terms in ascending order
+  double2 y0[kPP], y1[kPP];
+#pragma unroll
+  for (int i = 0; i < kPP; ++i) y0[i] = y1[i] = make_double2(0.0, 0.0);
+  for (int q = 0; q < k; ++q) {
+    const int sq = s_sel[q];
+    const double2* Lq = L + (size_t)q * n;
+    double2 l[kPP];
+#pragma unroll
+    for (int i = 0; i < kPP; ++i) {
+      const int p = threadIdx.x + i * blockDim.x;
+      l[i] = p < n ? __ldg(Lq + p) : make_double2(0.0, 0.0);
+    }
+#pragma unroll
+    for (int i = 0; i < kPP; ++i) {
+      const int p = threadIdx.x + i * blockDim.x;
+      if (p < n) {
+        int src = p - sq;
+        if (src < 0) src += n;
+        y0[i] = cadd(y0[i], cmul(l[i], cscale(x0[fsw(src, n)], rs)));
+        y1[i] = cadd(y1[i], cmul(l[i], cscale(x1[fsw(src, n)], rs)));
+      }
+    }
   }
   __syncthreads();  // every gather read of x0 / x1 is done: reuse them for the inverse transforms
 #pragma unroll
@@ -300,7 +337,8 @@ __global__ void __launch_bounds__(512) circ_right2_kernel(const T* __restrict__ 
                                                           const int* __restrict__ selA, int ka,
                                                           const double2* __restrict__ LB, const int* __restrict__ selB,
                                                           int kb, const double2* __restrict__ roots,
-                                                          double2* __restrict__ M) {
+                                                          double2* __restrict__ M,
+                                                          const double2* __restrict__ Xpre) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* x0 = reinterpret_cast<double2*>(smem_raw);
   double2* x1 = x0 + n;
@@ -313,7 +351,14 @@ __global__ void __launch_bounds__(512) circ_right2_kernel(const T* __restrict__ 
   const int r0 = 2 * blockIdx.x;
   const bool two = r0 + 1 < n;
   const double rs = rsqrt((double)n);
-  {
+  if (Xpre != nullptr) {
+    // conj(dA) rows precomputed by big_dA_kernel (16-row blocks share every S_t and twiddle load:
+    // formed here, two rows per CTA, the S_t reads from L2 were the kernel's largest stall)
+    for (int c = threadIdx.x; c < n; c += blockDim.x) {
+      x0[fsw(c, n)] = __ldg(Xpre + (size_t)r0 * n + c);
+      x1[fsw(c, n)] = two ? __ldg(Xpre + (size_t)(r0 + 1) * n + c) : make_double2(0.0, 0.0);
+    }
+  } else {
     // Ahat[r][c] = sum_t S_t[(r - c) % n] * w^{t c} at the thread's columns c_i = tid + i * nt:
     // rows r0, r0+1 read S_t[d], S_t[d+1]; the twiddle of c_{i+1} is the one of c_i times
     // w^{t nt}, so each term takes two table loads per thread instead of one per column (the
@@ -351,22 +396,35 @@ __global__ void __launch_bounds__(512) circ_right2_kernel(const T* __restrict__ 
   __syncthreads();
   fft_block(x0, scratch, n, roots, false);
   fft_block(x1, scratch, n, roots, false);
+  // term-major (see circ_left2_kernel): kPP independent L_t loads in flight per term
   double2 y0[kPP], y1[kPP];
 #pragma unroll
-  for (int i = 0; i < kPP; ++i) {
-    const int p = threadIdx.x + i * blockDim.x;
-    double2 a0 = make_double2(0.0, 0.0), a1 = make_double2(0.0, 0.0);
-    if (p < n) {
-      for (int q = 0; q < kb; ++q) {
-        int src = p + sB[q];
+  for (int i = 0; i < kPP; ++i) y0[i] = y1[i] = make_double2(0.0, 0.0);
+  for (int q = 0; q < kb; ++q) {
+    const int sq = sB[q];
+    const double2* Lq = LB + (size_t)q * n;
+    // two half-batches of loads (a full batch of kPP spilled at the 128-register bound)
+#pragma unroll
+    for (int h = 0; h < kPP; h += kPP / 2) {
+      double2 l[kPP];
+#pragma unroll
+      for (int i = h; i < h + kPP / 2; ++i) {
+        const int p = threadIdx.x + i * blockDim.x;
+        int src = p + sq;
         if (src >= n) src -= n;
-        const double2 l = __ldg(LB + (size_t)q * n + src);
-        a0 = cadd(a0, cmulc(cscale(x0[fsw(src, n)], rs), l));
-        a1 = cadd(a1, cmulc(cscale(x1[fsw(src, n)], rs), l));
+        l[i] = p < n ? __ldg(Lq + src) : make_double2(0.0, 0.0);
+      }
+#pragma unroll
+      for (int i = h; i < h + kPP / 2; ++i) {
+        const int p = threadIdx.x + i * blockDim.x;
+        if (p < n) {
+          int src = p + sq;
+          if (src >= n) src -= n;
+          y0[i] = cadd(y0[i], cmulc(cscale(x0[fsw(src, n)], rs), l[i]));
+          y1[i] = cadd(y1[i], cmulc(cscale(x1[fsw(src, n)], rs), l[i]));
+        }
       }
     }
-    y0[i] = a0;
-    y1[i] = a1;
   }
   __syncthreads();
 #pragma unroll
@@ -809,7 +867,7 @@ __global__ void __launch_bounds__(256) big_left_gather_kernel(const double2* __r
 // is shared by the block's rows, and for a fixed row the lanes read consecutive S_q entries.
 constexpr int kDaRows = 16;
 template <typename T>
-__global__ void __launch_bounds__(256) big_dA_kernel(const T* __restrict__ A, int n, const double2* __restrict__ Ssel,
+__global__ void __launch_bounds__(256, 2) big_dA_kernel(const T* __restrict__ A, int n, const double2* __restrict__ Ssel,
                                                      const int* __restrict__ sel, int k,
                                                      const double2* __restrict__ roots, double2* __restrict__ X) {
   __shared__ int s_buf[512];
@@ -831,7 +889,7 @@ __global__ void __launch_bounds__(256) big_dA_kernel(const T* __restrict__ A, in
     for (int rr = 0; rr < kDaRows; ++rr) {
       int d = d0 + rr;
       if (d >= n) d -= n;
-      ah[rr] = cadd(ah[rr], cmul(__ldg(Sq + d), w));
+      ah[rr] = cmac(ah[rr], __ldg(Sq + d), w);
     }
   }
 #pragma unroll
@@ -967,7 +1025,19 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
     if (pairs) {
       auto fn = circ_right2_kernel<T>;
       APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      fn<<<(unsigned)ceil_div(n, 2), 512, smem, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M);
+      // conj(dA) = conj(A - Ahat) into S_a's storage (free once both spectra are copied out)
+      const double2* Xpre = nullptr;
+      static const bool inline_da = [] {
+        const char* e = getenv("APX_CIRC_DA_INLINE");  // A/B switch: Ahat formed inside the row kernel
+        return e != nullptr && atoi(e) != 0;
+      }();
+      if (!inline_da && n >= kDaRows) {  // (big_dA_kernel wraps d0 + rr < 2n once)
+        big_dA_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)ceil_div(n, kDaRows)), 256, 0, st>>>(
+            A, n, p.Ssel_a, sa, k, p.roots, p.S_a);
+        APX_LAUNCH_CHECK();
+        Xpre = p.S_a;
+      }
+      fn<<<(unsigned)ceil_div(n, 2), 512, smem, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M, Xpre);
     } else {
       auto fn = circ_right_kernel<T>;
       APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
