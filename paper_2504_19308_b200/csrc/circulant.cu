@@ -91,6 +91,50 @@ __global__ void __launch_bounds__(512) circ_decompose_rows_kernel(const T* __res
   for (int t = threadIdx.x; t < n; t += blockDim.x) m2[t] = 0.0;
   const double inv_n = 1.0 / n;
   const int j0 = blockIdx.x * cpc, j1 = min(n, j0 + cpc);
+  if constexpr (std::is_same<T, double>::value) {
+    // real rows in pairs: x_j + i x_{j+1} through ONE transform Z, split as
+    // F_j[t] = (Z[t] + conj Z[-t]) / 2, F_{j+1}[t] = (Z[t] - conj Z[-t]) / 2i; the next pair's
+    // loads are in flight (registers) while the current pair is transformed
+    if (n <= 8 * 512) {
+      double nx0[8], nx1[8];
+      auto load_pair = [&](int j) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = threadIdx.x + u * blockDim.x;
+          nx0[u] = (i < n && j < j1) ? __ldg(X + (size_t)j * n + i) : 0.0;
+          nx1[u] = (i < n && j + 1 < j1) ? __ldg(X + (size_t)(j + 1) * n + i) : 0.0;
+        }
+      };
+      load_pair(j0);
+      for (int j = j0; j < j1; j += 2) {
+#pragma unroll
+        for (int u = 0; u < 8; ++u) {
+          const int i = threadIdx.x + u * blockDim.x;
+          if (i < n) x[fsw(i, n)] = make_double2(nx0[u], nx1[u]);
+        }
+        __syncthreads();
+        if (j + 2 < j1) load_pair(j + 2);
+        fft_block(x, scratch, n, roots, false);
+        const bool two = j + 1 < j1;
+        const double h = 0.5 * inv_n;
+        for (int t = threadIdx.x; t < n; t += blockDim.x) {
+          const double2 z = x[fsw(t, n)], zm = x[fsw(t == 0 ? 0 : n - t, n)];
+          const double2 v0 = make_double2(h * (z.x + zm.x), h * (z.y - zm.y));
+          St[(size_t)j * n + t] = v0;
+          double a = fma(v0.x, v0.x, fma(v0.y, v0.y, m2[t]));
+          if (two) {
+            const double2 v1 = make_double2(h * (z.y + zm.y), h * (zm.x - z.x));
+            St[(size_t)(j + 1) * n + t] = v1;
+            a = fma(v1.x, v1.x, fma(v1.y, v1.y, a));
+          }
+          m2[t] = a;
+        }
+        __syncthreads();
+      }
+      for (int t = threadIdx.x; t < n; t += blockDim.x) mag2_part[(size_t)blockIdx.x * n + t] = m2[t];
+      return;
+    }
+  }
   for (int j = j0; j < j1; ++j) {
     for (int i = threadIdx.x; i < n; i += blockDim.x) x[fsw(i, n)] = ld_c<T>(X, (size_t)j * n + i);
     __syncthreads();
