@@ -309,27 +309,31 @@ __global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B
     }
   }
   __syncthreads();
-  fft_block(x0, scratch, n, roots, false);
+  // forward transforms end in plain order (fft_linear_ok): the shifted gathers below read
+  // unaligned runs, which the swizzle split over bank groups
+  const bool lin = fft_linear_ok(n);
+  auto ix = [&](int i) { return lin ? i : fsw(i, n); };
+  fft_block(x0, scratch, n, roots, false, true);
   if constexpr (kPack) {
     double2 f0[kPP];  // FB1 goes straight to x1; FB0 waits in registers until every Z read is done
 #pragma unroll
     for (int i = 0; i < kPP; ++i) {
       const int p = threadIdx.x + i * blockDim.x;
       if (p < n) {
-        const double2 z = x0[fsw(p, n)], zm = x0[fsw(p == 0 ? 0 : n - p, n)];
+        const double2 z = x0[ix(p)], zm = x0[ix(p == 0 ? 0 : n - p)];
         f0[i] = make_double2(0.5 * (z.x + zm.x), 0.5 * (z.y - zm.y));
-        x1[fsw(p, n)] = make_double2(0.5 * (z.y + zm.y), 0.5 * (zm.x - z.x));
+        x1[ix(p)] = make_double2(0.5 * (z.y + zm.y), 0.5 * (zm.x - z.x));
       }
     }
     __syncthreads();
 #pragma unroll
     for (int i = 0; i < kPP; ++i) {
       const int p = threadIdx.x + i * blockDim.x;
-      if (p < n) x0[fsw(p, n)] = f0[i];
+      if (p < n) x0[ix(p)] = f0[i];
     }
     __syncthreads();
   } else {
-    fft_block(x1, scratch, n, roots, false);
+    fft_block(x1, scratch, n, roots, false, true);
   }
   // term-major: the kPP positions' L_t loads (L2) of one term are independent, so all are in
   // flight together (position-major, each thread waited one L2 latency per term and position);
@@ -352,8 +356,8 @@ __global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B
       if (p < n) {
         int src = p - sq;
         if (src < 0) src += n;
-        y0[i] = cadd(y0[i], cmul(l[i], cscale(x0[fsw(src, n)], rs)));
-        y1[i] = cadd(y1[i], cmul(l[i], cscale(x1[fsw(src, n)], rs)));
+        y0[i] = cadd(y0[i], cmul(l[i], cscale(x0[ix(src)], rs)));
+        y1[i] = cadd(y1[i], cmul(l[i], cscale(x1[ix(src)], rs)));
       }
     }
   }
@@ -395,6 +399,12 @@ __global__ void __launch_bounds__(512) circ_right2_kernel(const T* __restrict__ 
   const int r0 = 2 * blockIdx.x;
   const bool two = r0 + 1 < n;
   const double rs = rsqrt((double)n);
+  // the epilogue's read-modify-write of M (term1, DRAM-resident by now): pull both rows toward
+  // L2 while the transforms run
+  if (threadIdx.x < 2 && r0 + threadIdx.x < n && ((uintptr_t)M & 15) == 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(M + (size_t)(r0 + threadIdx.x) * n),
+                 "r"((unsigned)(n * sizeof(double2)))
+                 : "memory");
   if (Xpre != nullptr) {
     // conj(dA) rows precomputed by big_dA_kernel (16-row blocks share every S_t and twiddle load:
     // formed here, two rows per CTA, the S_t reads from L2 were the kernel's largest stall)
@@ -438,6 +448,7 @@ __global__ void __launch_bounds__(512) circ_right2_kernel(const T* __restrict__ 
     }
   }
   __syncthreads();
+  // (plain-order transform output, as in circ_left2_kernel, measured 1% slower here)
   fft_block(x0, scratch, n, roots, false);
   fft_block(x1, scratch, n, roots, false);
   // term-major (see circ_left2_kernel): kPP independent L_t loads in flight per term

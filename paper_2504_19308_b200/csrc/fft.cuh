@@ -104,10 +104,20 @@ __device__ __forceinline__ int bitrev_order(int e, int logn) {
 // roots[k] = exp(-2 pi i k / n) for k < n (full table; pow2 transforms use the first n/2)
 void launch_roots(double2* roots, int n, cudaStream_t st);
 
+// True when fft_block(..., linear_out = true) can leave its result in plain order x[i] instead of
+// x[fsw(i)]: the last pass must be a radix-8 pass (log2 n a multiple of 3) with one group per
+// thread, so that all its reads can finish (barrier) before the unswizzled writes.
+__device__ __forceinline__ bool fft_linear_ok(int n) {
+  return is_pow2(n) && n >= 8 && ilog2(n) % 3 == 0 && (n >> 3) <= (int)blockDim.x;
+}
+
 // In-place transform of x[0..n) in shared memory; `scratch` (n entries) is used by the direct
-// DFT only. All threads of the CTA must call it (contains __syncthreads).
+// DFT only. All threads of the CTA must call it (contains __syncthreads). With linear_out (and
+// fft_linear_ok(n)) the output is in plain order: unaligned runs of consecutive elements -- the
+// frequency-domain gathers -- then read conflict-free, where the swizzle split them over bank
+// groups.
 __device__ inline void fft_block(double2* x, double2* scratch, int n, const double2* __restrict__ roots,
-                                 bool inverse) {
+                                 bool inverse, bool linear_out = false) {
   const int tid = threadIdx.x, nt = blockDim.x;
   if (n == 1) return;
   if (is_pow2(n)) {
@@ -126,8 +136,27 @@ __device__ inline void fft_block(double2* x, double2* scratch, int n, const doub
     // base + pos + m*h (h = 2^(s-1)) held in registers -- one shared-memory round trip and one
     // barrier per three stages; the same twiddles and butterfly order as the radix-2 stages below
     int s = 1;
+    const bool lin = linear_out && fft_linear_ok(n);
     for (; s + 2 <= logn; s += 3) {
       const int h = 1 << (s - 1);
+      if (lin && s + 3 > logn) {  // last pass: all reads, barrier, plain-order writes
+        const int g = tid;
+        double2 v[8];
+        const int pos = g & (h - 1);
+        const int base = (g >> (s - 1)) << (s + 2);
+        if (g < (n >> 3)) {
+#pragma unroll
+          for (int m = 0; m < 8; ++m) v[m] = x[fsw(base + pos + m * h, n)];
+          radix8_apply(v, radix8_twiddles(roots, pos << (logn - s - 2), inverse));
+        }
+        __syncthreads();
+        if (g < (n >> 3)) {
+#pragma unroll
+          for (int m = 0; m < 8; ++m) x[base + pos + m * h] = v[m];
+        }
+        __syncthreads();
+        continue;
+      }
       for (int g = tid; g < (n >> 3); g += nt) {
         const int pos = g & (h - 1);
         const int base = (g >> (s - 1)) << (s + 2);
