@@ -206,8 +206,11 @@ __global__ void cycle_scatter_kernel(const T* __restrict__ lam, const int* __res
 // K10: left gather on a column strip. The CTA keeps X[:, c0:c0+W] in shared memory (row stride
 // padded to avoid bank conflicts); thread = output row, W accumulators.
 // ------------------------------------------------------------------------------------------
+// 1024 threads: the strip's shared memory (up to (W + 1) n elements) leaves one CTA per SM at
+// the largest strips, so the CTA itself must carry enough warps to hide the lambda loads
+constexpr int kLeftThreads = 1024;
 template <typename T, int W>
-__global__ void __launch_bounds__(256) cycle_left_gather(const T* __restrict__ X, const T* __restrict__ lam,
+__global__ void __launch_bounds__(kLeftThreads) cycle_left_gather(const T* __restrict__ X, const T* __restrict__ lam,
                                                          const int* __restrict__ J, int k, int n, int accumulate,
                                                          T* __restrict__ M, int r_lo, int r_hi, int lam_ld) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -1050,9 +1053,9 @@ static int left_gather_w(const T* X, const T* lam, const int* J, int k, int n, i
   const int strips = (int)ceil_div(n, W);
   int groups = 1;
   const int rows = r_hi - r_lo;
-  if (strips < 2 * kNumSMs) groups = std::min<int>((int)ceil_div(2 * kNumSMs, strips), std::max(1, rows / 256));
+  if (strips < 2 * kNumSMs) groups = std::min<int>((int)ceil_div(2 * kNumSMs, strips), std::max(1, rows / kLeftThreads));
   dim3 grid((unsigned)strips, (unsigned)groups);
-  cycle_left_gather<T, W><<<grid, 256, smem, st>>>(X, lam, J, k, n, acc, M, r_lo, r_hi, lam_ld);
+  cycle_left_gather<T, W><<<grid, kLeftThreads, smem, st>>>(X, lam, J, k, n, acc, M, r_lo, r_hi, lam_ld);
   APX_LAUNCH_CHECK();
   return OK;
 }
