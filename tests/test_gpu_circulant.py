@@ -129,3 +129,22 @@ def test_validation(C):
         C.circulant_first_order_multiply(A, A, 5, 0)
     with pytest.raises(ValueError):
         C.circulant_first_order_multiply(A, A, 1, 2)
+
+
+@pytest.mark.parametrize("n", [64, 256, 97])
+def test_complex_operands_product(C, n):
+    """Complex A, B (accepted by the reference, circulant.py:73-91 / core.py:38-41): the row and
+    column kernels take their unpacked branch (no real-pair packing) -- checked against the oracle
+    under the near-tie protocol."""
+    rng = np.random.default_rng(n + 5)
+    A = O.gen_circulant_operand(n, 4, 21 + n) + 1j * O.gen_circulant_operand(n, 4, 22 + n)
+    B = O.gen_circulant_operand(n, 4, 23 + n) + 1j * rng.standard_normal((n, n)) * 1e-3
+    for order in (0, 1):
+        M, rep = C.circulant_first_order_multiply(A, B, 5, order)
+        Mo, ro = O.circulant_first_order_multiply(A, B, 5, order)
+        subs = near_tie_ok(rep.selected_a, ro["selected_a"], ro["magnitudes_a"])
+        subs += near_tie_ok(rep.selected_b, ro["selected_b"], ro["magnitudes_b"])
+        if subs:
+            Mo, ro = O.circulant_first_order_multiply(A, B, 5, order, force_sel_a=rep.selected_a,
+                                                      force_sel_b=rep.selected_b)
+        assert rel(M, Mo) < 1e-10
