@@ -16,7 +16,11 @@
  *     them into the reference's ApproxReport (report.py:8-36) fields.
  *   - Return value 0 = success; nonzero = APX_E_* code, message via apx_last_error() (thread
  *     local). APX_E_ARG maps to the reference's ValueError.
- *   - Reentrant: no global mutable state besides the thread-local error string.
+ *   - Thread state: the error string, the optional stage events (apx_set_stage_events) and, for
+ *     the multi-stream C4 plan, one pair of internal side streams per (host thread, device)
+ *     pair -- created lazily on the device that is current at the call. The only process-wide
+ *     state is the launch counter (an atomic). Calls from different threads never share streams;
+ *     calls from one thread on one device serialise on that thread's side streams.
  */
 #ifndef APX_H_
 #define APX_H_
@@ -144,9 +148,17 @@ int apx_topk_rows(const void* M, int64_t rows, int64_t cols, int k, const int32_
                   int32_t* sel, void* vals, void* ws, size_t ws_bytes, void* stream);
 
 /* sparse_dense_multiply (fsparse.py:142-165), S on the left: out (rows x p) = S X, S given as
- * rows x k (sel, vals complex128; -1 = unused slot), X complex128 with p columns, k <= 256. */
+ * rows x k (sel, vals complex128; -1 = unused slot), X complex128 with p columns, any k (the
+ * entries are staged through shared memory in tiles of 256). */
 int apx_sparse_rows_multiply(const int32_t* sel, const void* vals, int k, int64_t rows,
                              const void* X, int64_t p, void* out, void* stream);
+
+/* fourier_row_decompose (fsparse.py:92-105): F = W(rows of A) / sqrt(n); weights[k] =
+ * sqrt(n) ||F[:, k]||_2 (n fp64), directions = F[:, k] / ||F[:, k]|| (m x n complex128, zero
+ * column where the weight vanishes). A is APX_F64 or APX_C128, m x n. */
+size_t apx_fourier_row_decompose_workspace(int64_t m, int64_t n);
+int apx_fourier_row_decompose(int dtype, const void* A, int64_t m, int64_t n, double* weights,
+                              void* directions, void* ws, size_t ws_bytes, void* stream);
 
 /* ------------------------------------------------------------------ core.py primitives ---- */
 /* unitary_dft (core.py:82-97) on `batch` complex128 vectors (element i of vector b at

@@ -15,6 +15,7 @@ Restated paths that the reference does not ship (``SURVEY.md`` §8(c)):
 
 from __future__ import annotations
 
+import os
 import math
 import time
 
@@ -25,7 +26,8 @@ __all__ = [
     "frobenius", "relative_error", "top_indices", "component_count", "apriori_relative_error",
     "posterior_relative_error", "sketch_norm_estimate", "rsvd", "svd_first_order_multiply", "circulant_decompose",
     "circulant_materialize", "circulant_left_product", "circulant_right_product",
-    "circulant_first_order_multiply", "topk_rows", "fft_sparse_first_order_multiply", "cycle_product_rows",
+    "circulant_first_order_multiply", "topk_rows", "fourier_row_decompose", "fft_sparse_first_order_multiply",
+    "cycle_product_rows",
     "cycle_norms", "cycle_decompose", "cycle_materialize", "cycle_first_order_multiply",
     "mixed_first_order_multiply", "gen_haar_spectrum", "gen_cycle_operand",
     "gen_circulant_operand", "gen_c5_operand", "Report",
@@ -396,6 +398,19 @@ def topk_rows(M, k, force=None):
     return out, lists
 
 
+def fourier_row_decompose(A):
+    """fsparse.py:92-105 -- F = W(rows)/sqrt(n); weights sqrt(n)||f_k||, unit directions, zero
+    columns where the weight vanishes. Returns (weights, directions)."""
+    A = as_matrix(A)
+    n = A.shape[1]
+    F = unitary_dft(A, "forward", axis=1) / math.sqrt(n)
+    col = np.linalg.norm(F, axis=0)
+    directions = np.zeros_like(F)
+    nz = col > 0
+    directions[:, nz] = F[:, nz] / col[nz]
+    return math.sqrt(n) * col, directions
+
+
 def fft_sparse_first_order_multiply(A, B, k: int, order: int, sparsify_b: str = "rows", force_a=None,
                                     force_b=None):
     """fsparse.py:168-240 -- At = A W*, Bt = W B, per-row top-k of both, first-order product."""
@@ -442,6 +457,21 @@ def cycle_norms(A) -> np.ndarray:
     return np.linalg.norm(cycle_reorder(A, "left"), axis=0)
 
 
+def _cycle_norms_blocked(A, block: int = 256) -> np.ndarray:
+    """Column 2-norms of cycle_reorder(A, 'left') without the n x n index arrays: the layout is
+    gathered one row block at a time and the squares are accumulated row by row in ascending row
+    order -- the order of numpy's add.reduce along axis 0 in np.linalg.norm(lay, axis=0), so the
+    result is bitwise the full-layout one (checked in tests/test_oracle_golden.py)."""
+    n = A.shape[0]
+    acc = np.zeros((1, n))
+    j = np.arange(n)[None, :]
+    for r0 in range(0, n, block):
+        i = np.arange(r0, min(n, r0 + block))[:, None]
+        lay = A[i, (i - j) % n]
+        acc = np.add.reduce(np.concatenate([acc, lay * lay], axis=0), axis=0, keepdims=True)
+    return np.sqrt(acc[0])
+
+
 def cycle_decompose(A, k: int, force_sel=None):
     """Dominant-cycle split A = sum_{j in J} Lambda_j C^j + dA.
 
@@ -451,10 +481,10 @@ def cycle_decompose(A, k: int, force_sel=None):
     n = _square(A)
     if not 0 <= k <= n:
         raise ValueError(f"k={k} out of range [0, {n}]")
-    lay = cycle_reorder(A, "left")
-    norms = np.linalg.norm(lay, axis=0)
+    norms = _cycle_norms_blocked(A)
     J = list(force_sel) if force_sel is not None else top_indices(norms, k)
-    lam = np.ascontiguousarray(lay[:, J].T)
+    i = np.arange(n)
+    lam = np.ascontiguousarray(np.array([A[i, (i - j) % n] for j in J]).reshape(len(J), n))
     nA = float(np.linalg.norm(A))
     nd = math.sqrt(max(0.0, nA ** 2 - sum(float(norms[j]) ** 2 for j in J)))
     return J, lam, norms, nA, nd
@@ -487,10 +517,18 @@ def _cycle_left_apply(J, lam, X, rows=None) -> np.ndarray:
 
 
 def _cycle_right_apply(X, J, lam) -> np.ndarray:
-    """X (sum_t Lambda_t C^{J[t]}) = sum_t apply_cycle_power(X o lam_t, J[t], 'right')."""
+    """X (sum_t Lambda_t C^{J[t]}) = sum_t apply_cycle_power(X o lam_t, J[t], 'right'), ascending t.
+    The roll by -j is written as two slice adds (out[:, c] += (X o lam_t)[:, (c + j) % n]): the same
+    values in the same order as np.roll, without its temporary."""
     out = np.zeros(X.shape, dtype=np.result_type(X, lam))
+    tmp = np.empty(X.shape, dtype=out.dtype)
+    n = X.shape[1]
     for t, j in enumerate(J):
-        out += np.roll(X * lam[t][None, :], -j, axis=1)
+        j = int(j) % n
+        np.multiply(X, lam[t][None, :], out=tmp)
+        out[:, : n - j] += tmp[:, j:]
+        if j:
+            out[:, n - j:] += tmp[:, :j]
     return out
 
 
@@ -541,7 +579,8 @@ def cycle_first_order_multiply(A, B, k: int, order: int, kb: int | None = None,
 
 
 def mixed_first_order_multiply(A, B, k_svd: int, k_cyc: int, order: int, seed,
-                               power_iterations: int = 0, force_sel_b=None, rows=None):
+                               power_iterations: int = 0, force_sel_b=None, rows=None, block: int = 64,
+                               threads: int | None = None):
     """Mixed product (config C4): A by rSVD (svd.py:83-119, stream default_rng([seed,0])),
     B by its k_cyc dominant cycles.  order 1: Ahat.B + dA.Bhat (reference order);
     order 0: Ahat.Bhat.  ``rows`` evaluates only that row subset of M (bounded CPU sample)."""
@@ -561,8 +600,24 @@ def mixed_first_order_multiply(A, B, k_svd: int, k_cyc: int, order: int, seed,
     if order == 0:
         M = Us @ _cycle_right_apply(V.T, Jb, lb)
     else:
+        # dense parts with the (multithreaded) BLAS, then the cycle term dA . Bhat over row blocks:
+        # the blocks are independent (the same values whatever the thread count) and numpy
+        # releases the GIL in their elementwise passes, so the host's cores share them
+        M = Us @ (V.T @ B)
         dA = A[r] - Us @ V.T
-        M = Us @ (V.T @ B) + _cycle_right_apply(dA, Jb, lb)
+
+        def rows_block(b0):
+            M[b0:b0 + block] += _cycle_right_apply(dA[b0:b0 + block], Jb, lb)
+
+        starts = list(range(0, r.size, block))
+        nthr = max(1, min(len(starts), threads or os.cpu_count() or 1))
+        if nthr == 1:
+            for b0 in starts:
+                rows_block(b0)
+        else:
+            from concurrent.futures import ThreadPoolExecutor
+            with ThreadPoolExecutor(nthr) as ex:
+                list(ex.map(rows_block, starts))
     wall = time.perf_counter() - t0
     rep = _report("mixed", order, s.size, math.sqrt(fa), nB, _svd_resid(s, fa), ndB, M, n, wall)
     rep["selected_b"], rep["norms_b"] = Jb, nb_

@@ -53,6 +53,8 @@ SIGNATURES = {
     "apx_sfft_first_order": (C.c_int, [_i32, _vp, _vp, _i64, _i64, _i64, _i32, _i32, _i32, _vp, _vp, _vp, _vp,
                                        _vp, _sz, _vp]),
     "apx_topk_rows_workspace": (_sz, [_i64, _i64]),
+    "apx_fourier_row_decompose_workspace": (_sz, [_i64, _i64]),
+    "apx_fourier_row_decompose": (C.c_int, [_i32, _vp, _i64, _i64, _vp, _vp, _vp, _sz, _vp]),
     "apx_sparse_rows_multiply": (C.c_int, [_vp, _vp, _i32, _i64, _vp, _i64, _vp, _vp]),
     "apx_topk_rows": (C.c_int, [_vp, _i64, _i64, _i32, _vp, _vp, _vp, _vp, _sz, _vp]),
     "apx_rsvd_workspace": (_sz, [_i32, _i64, _i64, _i32]),

@@ -262,7 +262,7 @@ static void plan_mixed(Workspace& ws, MixedPlan& p, int dtype, int n, int l, int
   p.asq = ws.take<double>(std::max<int>(n, kNumSMs * 4));
   p.bsq = ws.take<double>(std::max<int>(n, kNumSMs * 4));
   p.ticket = ws.take<int>(4);
-  p.ready = ws.take<int>(n);
+  p.ready = ws.take<int>((size_t)n + 1 + qw_ctas);  // row-block flags, then the deferred-tile list
 }
 
 // fp32 GEMM stages of the mixed product on tcgen05 (umma.cu). Layout bits: 1 = A operand stored
@@ -311,11 +311,12 @@ struct UmmaStages {
   }
   // M[n x n] (+)= Q . W  (Q stored n x l, W stored l x n); optional ||M||^2 partials per CTA
   static int q_times_w(const float* Q, const float* W, float* M, int n, int l, cudaStream_t st, int acc = 0,
-                       double* sq = nullptr, const int* ready = nullptr, int ready_rows = 0) {
+                       double* sq = nullptr, const int* ready = nullptr, int ready_rows = 0,
+                       const int* progress = nullptr, int* defer = nullptr) {
     // accumulate: BN 128 / 2 stages, whose drained ring holds the C tile for the staged epilogue
     // (measured faster than a persistent double-buffered variant: 3 CTAs per SM = 12 epilogue warps)
     return umma_tma_gemm(2, acc ? 128 : 256, Q, l, W, n, M, n, 0, n, n, l, 1, acc, nullptr, 0, 1, st, sq, ready,
-                         ready_rows);
+                         ready_rows, progress, defer);
   }
   static int q_times_w_ctas(int n, int l, int acc) {
     return (int)(ceil_div(n, acc ? 128 : 256) * ceil_div(n, 128));
@@ -333,21 +334,28 @@ struct SideStream {
   cudaStream_t s = nullptr, hi = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr, b_ready = nullptr, hi_done = nullptr, b_read = nullptr;
 };
-static thread_local SideStream g_side;
+// Keyed by the current device: one host thread may drive several GPUs (or re-target with
+// cudaSetDevice), and each device gets its own pair of streams and events.
+constexpr int kMaxDevices = 64;
+static thread_local SideStream g_side[kMaxDevices];
 
 static int get_side(SideStream** out) {
-  if (!g_side.s) {
+  int dev = 0;
+  APX_CUDA(cudaGetDevice(&dev));
+  APX_REQUIRE(dev >= 0 && dev < kMaxDevices, "device ordinal %d out of range", dev);
+  SideStream& g = g_side[dev];
+  if (!g.s) {
     int least = 0, greatest = 0;
     APX_CUDA(cudaDeviceGetStreamPriorityRange(&least, &greatest));
-    APX_CUDA(cudaStreamCreateWithPriority(&g_side.s, cudaStreamNonBlocking, least));
-    APX_CUDA(cudaStreamCreateWithPriority(&g_side.hi, cudaStreamNonBlocking, greatest));
-    APX_CUDA(cudaEventCreateWithFlags(&g_side.fork, cudaEventDisableTiming));
-    APX_CUDA(cudaEventCreateWithFlags(&g_side.join, cudaEventDisableTiming));
-    APX_CUDA(cudaEventCreateWithFlags(&g_side.b_ready, cudaEventDisableTiming));
-    APX_CUDA(cudaEventCreateWithFlags(&g_side.hi_done, cudaEventDisableTiming));
-    APX_CUDA(cudaEventCreateWithFlags(&g_side.b_read, cudaEventDisableTiming));
+    APX_CUDA(cudaStreamCreateWithPriority(&g.s, cudaStreamNonBlocking, least));
+    APX_CUDA(cudaStreamCreateWithPriority(&g.hi, cudaStreamNonBlocking, greatest));
+    APX_CUDA(cudaEventCreateWithFlags(&g.fork, cudaEventDisableTiming));
+    APX_CUDA(cudaEventCreateWithFlags(&g.join, cudaEventDisableTiming));
+    APX_CUDA(cudaEventCreateWithFlags(&g.b_ready, cudaEventDisableTiming));
+    APX_CUDA(cudaEventCreateWithFlags(&g.hi_done, cudaEventDisableTiming));
+    APX_CUDA(cudaEventCreateWithFlags(&g.b_read, cudaEventDisableTiming));
   }
-  *out = &g_side;
+  *out = &g;
   return OK;
 }
 
@@ -362,7 +370,7 @@ static int gather_ctas(int nblk) {
     return e ? atoi(e) : 0;
   }();
   if (env > 0) return env;
-  return std::min(nblk, kNumSMs - kMinFreeSMs);
+  return std::max(1, std::min(nblk, device_sms() - kMinFreeSMs));
 }
 
 // Stage markers (bench.py): 0 start | hi: 1 B decomposed, 2 gather done | lo: 3 Y, 4 QR, 5 Bm,
@@ -375,8 +383,9 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
   const int grows = right_gather_rows(n, sizeof(float), kc);
   const int rblocks = (int)ceil_div(n, grows);
+  int* defer = p.ready + rblocks;  // [count, tiles...] of the bounded-wait Q.W epilogue
   if (order == 1) {
-    APX_CUDA(cudaMemsetAsync(p.ready, 0, rblocks * sizeof(int), st));
+    APX_CUDA(cudaMemsetAsync(p.ready, 0, (rblocks + 1) * sizeof(int), st));
     APX_CUDA(cudaMemsetAsync(p.ticket, 0, sizeof(int), st));  // the gather's (x_early launch)
   }
   SideStream* ss = nullptr;
@@ -450,12 +459,18 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   // running: each tile's operand pipeline and MMA run at once, and its epilogue waits (acquire)
   // only for the gather row blocks under it, so the HBM-bound read-modify-write of the finished
   // rows overlaps the shared-memory-bound gather on the SMs it leaves free, and the rest follows
-  // the gather's frontier onto the SMs it releases. The gather's CTAs are all resident before this
-  // launch (it is enqueued on hi well before the range finder ends), so the waits always progress.
+  // the gather's frontier onto the SMs it releases. The gather is enqueued on hi well before the
+  // range finder ends, so its CTAs are normally resident first; CUDA does not guarantee that
+  // across streams (MPS SM limits, co-tenants), so each tile's wait is bounded: a tile whose
+  // gather makes no progress for 20 ms defers itself, and qw_fixup_sum_kernel completes it after
+  // the gather (lo waits for hi first). Normally nothing is deferred and the fixup kernel is the
+  // fixed-order ||M||^2 sum it replaces.
   if (order == 1) {
-    APX_TRY(UmmaStages::q_times_w(Q, W, M, n, l, lo, 1, p.msq, p.ready, grows));
+    APX_TRY(UmmaStages::q_times_w(Q, W, M, n, l, lo, 1, p.msq, p.ready, grows, p.ticket, defer));
     stage_mark(7, lo);
-    APX_TRY(launch_sum_vector(p.msq, UmmaStages::q_times_w_ctas(n, l, 1), scal + APX_S_FRO2_M, lo));
+    APX_CUDA(cudaStreamWaitEvent(lo, ss->hi_done, 0));
+    APX_TRY(launch_qw_fixup_sum(Q, l, W, n, M, n, n, n, l, 128, defer, p.msq, UmmaStages::q_times_w_ctas(n, l, 1),
+                                scal + APX_S_FRO2_M, lo));
   }
   APX_CUDA(cudaEventRecord(ss->join, lo));
   // ---- main: join; (order 0) M = Q . W; the fixed-order sums ----------------------------------
@@ -512,7 +527,7 @@ static int run_mixed_rows_phase(int phase, const float* A, int m, const float* B
   float* lb = (float*)p.lam_b;
   if (phase == 1) {
     APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
-    APX_CUDA(cudaMemsetAsync(p.ready, 0, rblocks * sizeof(int), st));
+    APX_CUDA(cudaMemsetAsync(p.ready, 0, (rblocks + 1) * sizeof(int), st));
     APX_CUDA(cudaMemsetAsync(p.ticket, 0, sizeof(int), st));
     APX_CUDA(cudaEventRecord(ss->fork, st));
     APX_CUDA(cudaStreamWaitEvent(lo, ss->fork, 0));
@@ -569,10 +584,15 @@ static int run_mixed_rows_phase(int phase, const float* A, int m, const float* B
     // are queued behind each other on hi: a waiting Q.W grid could hold the SMs a later gather needs)
     if (flags & 1) APX_CUDA(cudaStreamWaitEvent(lo, ss->hi_done, 0));
     const int qw_ctas = (int)(ceil_div(n, order == 1 ? 128 : 256) * ceil_div(m, 128));
+    int* defer = order == 1 ? p.ready + rblocks : nullptr;  // bounded wait (see run_mixed_f32_umma)
     APX_TRY(umma_tma_gemm(2, order == 1 ? 128 : 256, Q, l, W, n, M, n, 0, m, n, l, 1, order == 1 ? 1 : 0, nullptr, 0,
-                          1, lo, p.msq, order == 1 ? p.ready : nullptr, grows));
-    APX_TRY(launch_sum_vector(p.msq, qw_ctas, fin + 1, lo));
+                          1, lo, p.msq, order == 1 ? p.ready : nullptr, grows, order == 1 ? p.ticket : nullptr,
+                          defer));
     APX_CUDA(cudaStreamWaitEvent(lo, ss->hi_done, 0));
+    if (order == 1)
+      APX_TRY(launch_qw_fixup_sum(Q, l, W, n, M, n, m, n, l, 128, defer, p.msq, qw_ctas, fin + 1, lo));
+    else
+      APX_TRY(launch_sum_vector(p.msq, qw_ctas, fin + 1, lo));
     APX_CUDA(cudaMemcpyAsync(fin, r.asum, sizeof(double), cudaMemcpyDeviceToDevice, lo));
     APX_TRY(launch_flag_to_double(cholqr_rows_flags(r.qr, r.qr_bytes, m, l), fin + 2, lo));
     APX_CUDA(cudaEventRecord(ss->join, lo));

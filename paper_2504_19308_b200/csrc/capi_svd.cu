@@ -31,7 +31,7 @@ struct Dgemm {
 
 // Per-operand buffers of the rSVD (sized for an m x n operand, sketch width l).
 struct Side {
-  double *Y, *Q, *Qt, *P, *Pt, *Ba, *Q2, *Q2t, *W, *Up, *S, *Vp, *VpT, *Qk, *Bk;
+  double *Y, *Q, *Qt, *P, *Pt, *Ba, *Q2, *Q2t, *W, *Up, *S, *Vp, *VpT, *Qk, *Bk, *svd_scratch;
   void* qr;
   size_t qr_bytes;
 };
@@ -53,6 +53,7 @@ void plan_side(Workspace& ws, Side& s, int m, int n, int l) {
   s.VpT = ws.take<double>((size_t)l * l);
   s.Qk = ws.take<double>((size_t)m * l);
   s.Bk = ws.take<double>((size_t)l * n);
+  s.svd_scratch = ws.take<double>(small_svd_scratch_doubles(l) + 1);
   s.qr_bytes = qr_ws_bytes((int)mx, l);
   s.qr = ws.take<char>(s.qr_bytes);
 }
@@ -79,7 +80,7 @@ int project_and_svd(const double* A, int m, int n, int l, const Side& s, const D
   if (!need_svd) return OK;
   APX_TRY((qr_orthonormalize<double, double>(s.Ba, 1, n, n, l, s.Q2, l, 1, s.Q2t, 1, n, s.qr, s.qr_bytes, 0, st)));
   APX_TRY(g(s.Ba, n, s.Q2, l, s.W, l, l, l, n, 0, st));  // W = Ba Q2 = R2^T
-  APX_TRY(launch_small_svd(s.W, l, s.Up, s.S, s.Vp, s.VpT, st));
+  APX_TRY(launch_small_svd(s.W, l, s.Up, s.S, s.Vp, s.VpT, st, s.svd_scratch));
   return OK;
 }
 
@@ -157,7 +158,7 @@ int apx_rsvd(int dtype, const void* A_, int64_t m, int64_t n, int l, int k, int 
              void* U_, double* sigma, void* V_, double* scalars, void* wsp, size_t ws_bytes, void* stream) {
   APX_REQUIRE(dtype == F64, "randomized_partial_svd: fp64 required");
   APX_REQUIRE(m >= 1 && n >= 1, "empty matrix");
-  APX_REQUIRE(l >= 1 && l <= 128 && l <= m && l <= n, "sketch width %d out of range", l);
+  APX_REQUIRE(l >= 1 && l <= m && l <= n, "sketch width %d out of range", l);
   APX_REQUIRE(k >= 1 && k <= l, "kept rank %d out of range [1, %d]", k, l);
   APX_REQUIRE(power_iterations >= 0, "power_iterations must be >= 0");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -195,7 +196,7 @@ int apx_qr(int dtype, const void* Y_, int64_t m, int64_t k, void* Q_, void* R_, 
            void* stream) {
   APX_REQUIRE(dtype == F64, "qr_decompose: fp64 required");
   APX_REQUIRE(m >= k, "need at least as many rows as columns, got %lld x %lld", (long long)m, (long long)k);
-  APX_REQUIRE(k >= 1 && k <= 128, "qr_decompose: 1 <= k <= 128 columns supported");
+  APX_REQUIRE(k >= 1, "qr_decompose: at least one column");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Workspace ws(wsp, ws_bytes);
   const size_t qb = qr_ws_bytes((int)m, (int)k);
@@ -296,8 +297,8 @@ int apx_svd_first_order(int dtype, const void* A_, const void* B_, int64_t m, in
                         const void* omega_b, void* M_, double* scalars, void* wsp, size_t ws_bytes, void* stream) {
   APX_REQUIRE(dtype == F64, "svd_first_order_multiply: fp64 required");
   APX_REQUIRE(m >= 1 && n >= 1 && p >= 1, "empty matrix");
-  APX_REQUIRE(l_a >= 1 && l_a <= 128 && l_a <= m && l_a <= n && k_a >= 1 && k_a <= l_a, "A sketch out of range");
-  APX_REQUIRE(l_b >= 1 && l_b <= 128 && l_b <= n && l_b <= p && k_b >= 1 && k_b <= l_b, "B sketch out of range");
+  APX_REQUIRE(l_a >= 1 && l_a <= m && l_a <= n && k_a >= 1 && k_a <= l_a, "A sketch out of range");
+  APX_REQUIRE(l_b >= 1 && l_b <= n && l_b <= p && k_b >= 1 && k_b <= l_b, "B sketch out of range");
   APX_REQUIRE(order == 0 || order == 1, "order must be 0 or 1");
   APX_REQUIRE(power_iterations >= 0, "power_iterations must be >= 0");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);

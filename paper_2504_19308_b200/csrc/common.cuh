@@ -12,7 +12,25 @@
 
 namespace apx {
 
-constexpr int kNumSMs = 148;  // B200
+// Grid-shape constant: the B200's SM count, used to size reduction grids, split-K factors and
+// partial-sum buffers. Results (fixed-order sums) depend on these shapes, so they are a constant,
+// not a device query: the same inputs give the same bits on any device. Grids whose correctness
+// or progress depends on how many CTAs are co-resident (the persistent gather) use
+// device_sms() instead.
+constexpr int kNumSMs = 148;
+
+// Multiprocessor count of the current device (queried once per device).
+inline int device_sms() {
+  static int cache[64] = {0};
+  int dev = 0;
+  if (cudaGetDevice(&dev) != cudaSuccess || dev < 0 || dev >= 64) return kNumSMs;
+  if (cache[dev] == 0) {
+    int v = 0;
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = kNumSMs;
+    cache[dev] = v;
+  }
+  return cache[dev];
+}
 
 // dtype codes used across the C-ABI (include/apx.h)
 enum DType : int { F32 = 0, F64 = 1, C64 = 2, C128 = 3 };

@@ -64,27 +64,49 @@ __global__ void __launch_bounds__(256) residual_kernel(const double2* __restrict
   if (threadIdx.x == 0) part[blockIdx.x] = acc;
 }
 
-// M[i, :] (+)= sum_q vals[i][q] * X[sel[i][q], :]   (k nonzeros per row of the left factor)
+// M[i, :] (+)= sum_q vals[i][q] * X[sel[i][q], :]   (k nonzeros per row of the left factor, any k:
+// the entries are staged through shared memory in tiles of kSpTile)
+constexpr int kSpTile = 256;
 __global__ void __launch_bounds__(256) sparse_rows_gemm_kernel(const int* __restrict__ sel,
                                                                const double2* __restrict__ vals, int k,
                                                                const double2* __restrict__ X, int p, int accumulate,
                                                                double2* __restrict__ M) {
   const int i = blockIdx.x;
-  __shared__ int sj[256];
-  __shared__ double2 sv[256];
-  for (int q = threadIdx.x; q < k && q < 256; q += blockDim.x) {
-    sj[q] = sel[(size_t)i * k + q];
-    sv[q] = vals[(size_t)i * k + q];
-  }
-  __syncthreads();
-  for (int c = threadIdx.x; c < p; c += blockDim.x) {
-    double2 acc = make_double2(0.0, 0.0);
-    for (int q = 0; q < k; ++q) {
-      const int j = sj[q];
-      if (j >= 0) acc = cadd(acc, cmul(sv[q], X[(size_t)j * p + c]));
+  __shared__ int sj[kSpTile];
+  __shared__ double2 sv[kSpTile];
+  // a CTA covers up to 4 column sweeps of 256 in registers; wider rows loop over column chunks
+  for (int c0 = 0; c0 < p; c0 += 4 * blockDim.x) {
+    double2 acc[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) acc[u] = make_double2(0.0, 0.0);
+    for (int q0 = 0; q0 < k; q0 += kSpTile) {
+      const int qn = min(kSpTile, k - q0);
+      __syncthreads();  // previous tile consumed
+      for (int q = threadIdx.x; q < qn; q += blockDim.x) {
+        sj[q] = sel[(size_t)i * k + q0 + q];
+        sv[q] = vals[(size_t)i * k + q0 + q];
+      }
+      __syncthreads();
+      for (int q = 0; q < qn; ++q) {
+        const int j = sj[q];
+        if (j < 0) continue;
+        const double2 v = sv[q];
+        const double2* xr = X + (size_t)j * p;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int c = c0 + u * blockDim.x + threadIdx.x;
+          if (c < p) acc[u] = cadd(acc[u], cmul(v, xr[c]));
+        }
+      }
     }
-    double2* pm = M + (size_t)i * p + c;
-    *pm = accumulate ? cadd(*pm, acc) : acc;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int c = c0 + u * blockDim.x + threadIdx.x;
+      if (c < p) {
+        double2* pm = M + (size_t)i * p + c;
+        *pm = accumulate ? cadd(*pm, acc[u]) : acc[u];
+      }
+    }
   }
 }
 
@@ -99,6 +121,31 @@ __global__ void merge_planes_kernel(const double* __restrict__ re, const double*
                                     double2* __restrict__ z) {
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < cnt; e += (size_t)gridDim.x * blockDim.x)
     z[e] = cadd(z[e], make_double2(re[e], im[e]));
+}
+
+// fourier_row_decompose (fsparse.py:92-105): F = W(rows) / sqrt(n) in place, then per column k
+// the 2-norm over the rows (one thread per column, rows in order: coalesced across the warp),
+// weights[k] = sqrt(n) ||f_k||, directions[:, k] = f_k / ||f_k|| (zero column where ||f_k|| = 0).
+__global__ void fourier_columns_kernel(double2* __restrict__ F, int m, int n, double inv_sqrt_n, double sqrt_n,
+                                       double* __restrict__ weights) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  double s = 0.0;
+  for (int i = 0; i < m; ++i) {
+    double2 v = F[(size_t)i * n + k];
+    v.x *= inv_sqrt_n;
+    v.y *= inv_sqrt_n;
+    F[(size_t)i * n + k] = v;
+    s = fma(v.x, v.x, fma(v.y, v.y, s));
+  }
+  const double nrm = sqrt(s);
+  weights[k] = sqrt_n * nrm;
+  const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+  for (int i = 0; i < m; ++i) {
+    double2 v = F[(size_t)i * n + k];
+    F[(size_t)i * n + k] = nrm > 0.0 ? make_double2(v.x / nrm, v.y / nrm) : make_double2(0.0, 0.0);
+  }
+  (void)inv;
 }
 
 static unsigned grid_for(size_t cnt) { return (unsigned)std::min<int64_t>(ceil_div(cnt, 256), kNumSMs * 8); }
@@ -281,10 +328,44 @@ int apx_sfft_first_order(int dtype, const void* A, const void* B, int64_t m, int
 // S . X with S given as rows x k (sel, vals), -1 marking unused slots; X is ? x p complex128.
 int apx_sparse_rows_multiply(const int32_t* sel, const void* vals, int k, int64_t rows, const void* X, int64_t p,
                              void* out, void* stream) {
-  APX_REQUIRE(rows >= 1 && p >= 1 && k >= 0 && k <= 256, "bad sparse multiply arguments (k <= 256)");
+  APX_REQUIRE(rows >= 1 && p >= 1 && k >= 0, "bad sparse multiply arguments");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   sparse_rows_gemm_kernel<<<(unsigned)rows, 256, 0, st>>>(sel, (const double2*)vals, k, (const double2*)X, (int)p, 0,
                                                           (double2*)out);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+size_t apx_fourier_row_decompose_workspace(int64_t m, int64_t n) {
+  Workspace ws(nullptr, 0, true);
+  ws.take<double2>((size_t)m * n);
+  ws.take<char>(apx_unitary_dft_workspace(n, m));
+  return ws.off;
+}
+
+// fourier_row_decompose (fsparse.py:92-105): A m x n (fp64 or complex128) -> weights (n fp64),
+// directions (m x n complex128).
+int apx_fourier_row_decompose(int dtype, const void* A, int64_t m, int64_t n, double* weights, void* directions,
+                              void* wsp, size_t ws_bytes, void* stream) {
+  APX_REQUIRE(dtype == F64 || dtype == C128, "fourier_row_decompose: fp64 or complex128 input");
+  APX_REQUIRE(m >= 1 && n >= 1, "empty matrix");
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  Workspace ws(wsp, ws_bytes);
+  double2* X = ws.take<double2>((size_t)m * n);
+  const size_t dft_bytes = apx_unitary_dft_workspace(n, m);
+  char* dft_ws = ws.take<char>(dft_bytes);
+  APX_WS_CHECK(ws);
+  const size_t mn = (size_t)m * n;
+  if (dtype == F64) {
+    APX_CUDA(cudaMemsetAsync(X, 0, mn * sizeof(double2), st));
+    APX_CUDA(cudaMemcpy2DAsync(X, sizeof(double2), A, sizeof(double), sizeof(double), mn, cudaMemcpyDeviceToDevice,
+                               st));
+  } else {
+    APX_CUDA(cudaMemcpyAsync(X, A, mn * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+  }
+  APX_TRY(apx_unitary_dft(X, directions, n, m, 1, n, 0, dft_ws, dft_bytes, stream));
+  fourier_columns_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>((double2*)directions, (int)m, (int)n,
+                                                                     1.0 / sqrt((double)n), sqrt((double)n), weights);
   APX_LAUNCH_CHECK();
   return OK;
 }

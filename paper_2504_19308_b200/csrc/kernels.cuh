@@ -78,7 +78,11 @@ int umma_set_variant(int v);
 int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                   int64_t ldc, int64_t c_split_stride, int M, int N, int K, int splits, int accumulate,
                   const int* mJ, int mk, int mod_n, cudaStream_t st, double* sq_partial = nullptr,
-                  const int* ready = nullptr, int ready_rows = 0);
+                  const int* ready = nullptr, int ready_rows = 0, const int* progress = nullptr,
+                  int* defer = nullptr);
+// deferred Q.W tiles of a ready-flag GEMM, then the fixed-order ||C||^2 sum (umma_tma.cu)
+int launch_qw_fixup_sum(const float* Q, int64_t ldq, const float* W, int64_t ldw, float* C, int64_t ldc, int M, int N,
+                        int K, int bn, int* defer, double* sq_partial, int parts, double* out, cudaStream_t st);
 int umma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
               int64_t c_split_stride, int M, int N, int K, int splits, int accumulate, const int* mJ, int mk,
               int mod_n, cudaStream_t st);
@@ -86,7 +90,10 @@ int umma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, i
 
 namespace apx {
 // ---- svd.cu ----
-int launch_small_svd(const double* W, int l, double* U, double* S, double* V, double* VT, cudaStream_t st);
+// l > 128 runs from a global scratch of small_svd_scratch_doubles(l) doubles
+size_t small_svd_scratch_doubles(int l);
+int launch_small_svd(const double* W, int l, double* U, double* S, double* V, double* VT, cudaStream_t st,
+                     double* scratch = nullptr);
 int launch_axpy2d(double* y, int64_t ldy, const double* x, int64_t ldx, int rows, int cols, double alpha,
                   const double* rowscale, int overwrite, cudaStream_t st);
 int launch_sumsq_prefix(const double* s, int k, double* out, cudaStream_t st);

@@ -15,7 +15,8 @@
 
 namespace apx {
 
-constexpr int kMaxL = 128;
+constexpr int kMaxL = 128;               // CholeskyQR2 fast path
+constexpr int kMaxHouseholderL = 12288;  // Householder: s_dot / s_tau in dynamic shared memory
 
 // ---- 64-row tile of a strided n x l matrix (l <= 64) into shared memory as fp64 -------------
 // Each of the 256 threads owns 16 elements; all 16 loads are issued before the first store, so a
@@ -536,7 +537,8 @@ __global__ void __launch_bounds__(1024) householder_qr_kernel(const TI* __restri
                                                               int64_t q2rs, int64_t q2cs) {
   if (!force && !(*flag)) return;
   __shared__ double red[32];
-  __shared__ double s_dot[kMaxL];
+  extern __shared__ double hh_smem[];  // s_dot[l], s_tau[l]
+  double* s_dot = hh_smem;
   __shared__ double s_scal[2];
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (size_t e = tid; e < (size_t)m * l; e += blockDim.x) {
@@ -593,7 +595,7 @@ __global__ void __launch_bounds__(1024) householder_qr_kernel(const TI* __restri
     __syncthreads();
   }
   // form Q = H_0 ... H_{l-1} [I; 0] in W; the taus sit on W's diagonal, copy them out first
-  __shared__ double s_tau[kMaxL];
+  double* s_tau = hh_smem + l;
   for (int j = tid; j < l; j += blockDim.x) s_tau[j] = W[(size_t)j * l + j];
   __syncthreads();
   for (size_t e = tid; e < (size_t)m * l; e += blockDim.x) {
@@ -705,7 +707,7 @@ static int launch_chol(const double* G, int l, double* R, double* rdiag, int* fl
 template <typename TI, typename TO>
 int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, int64_t qrs, int64_t qcs, TO* Q2,
                       int64_t q2rs, int64_t q2cs, void* wsp, size_t ws_bytes, int method, cudaStream_t st) {
-  APX_REQUIRE(l >= 1 && l <= kMaxL, "sketch width %d outside [1, %d]", l, kMaxL);
+  APX_REQUIRE(l >= 1 && l <= kMaxHouseholderL, "sketch width %d outside [1, %d]", l, kMaxHouseholderL);
   APX_REQUIRE(m >= l, "need at least as many rows as columns, got %d x %d", m, l);
   Workspace ws(wsp, ws_bytes);
   const int parts = (int)ceil_div(m, 64);
@@ -718,7 +720,9 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
   double* V = ws.take<double>((size_t)m * l);
   int* flag = ws.take<int>(4);
   APX_WS_CHECK(ws);
-  const bool householder_only = method == 1 || m <= 2 * l;
+  // wide sketches (l > kMaxL: beyond the register-blocked Cholesky/apply kernels) take the
+  // Householder path too
+  const bool householder_only = method == 1 || m <= 2 * l || l > kMaxL;
   reset_flag_kernel<<<1, 1, 0, st>>>(flag, householder_only ? 1 : 0);
   APX_LAUNCH_CHECK();
   if (!householder_only && l <= 64) {
@@ -749,7 +753,11 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
     APX_TRY(launch_chol(G, l, Rinv, rdiag, flag, st));
     APX_TRY((launch_apply<double, TO>(Q1, l, 1, m, l, Rinv, rdiag, flag, Q, qrs, qcs, Q2, q2rs, q2cs, st)));
   }
-  householder_qr_kernel<TI, TO><<<1, 1024, 0, st>>>(Y, rs, cs, m, l, flag, 0, W, V, Q, qrs, qcs, Q2, q2rs, q2cs);
+  const size_t hh_smem = (size_t)2 * l * sizeof(double);
+  APX_CUDA(cudaFuncSetAttribute(householder_qr_kernel<TI, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                (int)std::max<size_t>(hh_smem, 48 * 1024)));
+  householder_qr_kernel<TI, TO><<<1, 1024, hh_smem, st>>>(Y, rs, cs, m, l, flag, 0, W, V, Q, qrs, qcs, Q2, q2rs,
+                                                           q2cs);
   APX_LAUNCH_CHECK();
   return OK;
 }

@@ -1,7 +1,8 @@
 // Small dense SVD for the randomized SVD (K14; reference svd.py:113 -> LAPACK gesdd).
 //
-// One CTA runs one-sided (Hestenes) Jacobi on a square l x l matrix W (l <= 128) held
-// column-major in shared memory: W V' = U' S. Rounds of the circle tournament rotate l/2
+// One CTA runs one-sided (Hestenes) Jacobi on a square l x l matrix W held column-major in
+// shared memory (l <= 128) or, for wider sketches, in a global (L2-resident) scratch buffer:
+// W V' = U' S. Rounds of the circle tournament rotate l/2
 // disjoint column pairs in parallel (one half-warp per pair, lanes over rows, fp64), sweeps repeat
 // until no pair is rotated. Singular values come out as column norms, sorted descending (stable
 // on ties); columns with zero norm are completed to an orthonormal basis by Gram-Schmidt on unit
@@ -14,16 +15,20 @@ namespace apx {
 
 constexpr int kSvdMax = 128;
 
-__global__ void __launch_bounds__(512) hestenes_svd_kernel(const double* __restrict__ Win, int l,
-                                                           double* __restrict__ Uout, double* __restrict__ Sout,
-                                                           double* __restrict__ Vout, double* __restrict__ VoutT) {
+template <bool GLOBAL>
+__global__ void __launch_bounds__(GLOBAL ? 1024 : 512)
+    hestenes_svd_kernel(const double* __restrict__ Win, int l, double* __restrict__ Uout, double* __restrict__ Sout,
+                        double* __restrict__ Vout, double* __restrict__ VoutT, double* __restrict__ scratch) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int le = l + (l & 1);  // even number of columns (pad with a zero column)
-  double* Wc = reinterpret_cast<double*>(smem_raw);  // le columns x l rows, column-major
-  double* Vc = Wc + (size_t)le * l;                  // le x le
+  // GLOBAL: W, V, the norms, the permutation and the completion vector live in `scratch`
+  double* Wc = GLOBAL ? scratch : reinterpret_cast<double*>(smem_raw);  // le columns x l rows, column-major
+  double* Vc = Wc + (size_t)le * l;                                      // le x le
   __shared__ int s_rot;
-  __shared__ int perm[kSvdMax + 2];
-  __shared__ double norms[kSvdMax + 2];
+  __shared__ int perm_s[GLOBAL ? 1 : kSvdMax + 2];
+  __shared__ double norms_s[GLOBAL ? 1 : kSvdMax + 2];
+  int* perm = GLOBAL ? reinterpret_cast<int*>(Vc + (size_t)le * le + le) : perm_s;
+  double* norms = GLOBAL ? Vc + (size_t)le * le : norms_s;
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (int e = tid; e < le * l; e += blockDim.x) {
     const int j = e / l, i = e - j * l;
@@ -126,7 +131,8 @@ __global__ void __launch_bounds__(512) hestenes_svd_kernel(const double* __restr
     for (int r = 0; r < l; ++r) {
       if (norms[perm[r]] > 0.0) continue;
       for (int cand = 0; cand < l; ++cand) {
-        double v[kSvdMax];
+        double v_s[GLOBAL ? 1 : kSvdMax];
+        double* v = GLOBAL ? norms + 2 * le + 2 : v_s;
         for (int i = 0; i < l; ++i) v[i] = (i == cand) ? 1.0 : 0.0;
         for (int pass = 0; pass < 2; ++pass)
           for (int q = 0; q < l; ++q) {
@@ -147,12 +153,25 @@ __global__ void __launch_bounds__(512) hestenes_svd_kernel(const double* __restr
   }
 }
 
-int launch_small_svd(const double* W, int l, double* U, double* S, double* V, double* VT, cudaStream_t st) {
-  APX_REQUIRE(l >= 1 && l <= kSvdMax, "small SVD size %d outside [1, %d]", l, kSvdMax);
+size_t small_svd_scratch_doubles(int l) {
+  if (l <= kSvdMax) return 0;
+  const size_t le = (size_t)l + (l & 1);
+  return le * l + le * le + 2 * le + 2 + le + 8;  // W, V, norms, perm (as ints), completion vector
+}
+
+int launch_small_svd(const double* W, int l, double* U, double* S, double* V, double* VT, cudaStream_t st,
+                     double* scratch) {
+  APX_REQUIRE(l >= 1, "small SVD size %d", l);
+  if (l > kSvdMax) {
+    APX_REQUIRE(scratch != nullptr, "small SVD of size %d needs a scratch buffer", l);
+    hestenes_svd_kernel<true><<<1, 1024, 0, st>>>(W, l, U, S, V, VT, scratch);
+    APX_LAUNCH_CHECK();
+    return OK;
+  }
   const int le = l + (l & 1);
   const size_t smem = ((size_t)le * l + (size_t)le * le) * sizeof(double);
-  APX_CUDA(cudaFuncSetAttribute(hestenes_svd_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  hestenes_svd_kernel<<<1, 512, smem, st>>>(W, l, U, S, V, VT);
+  APX_CUDA(cudaFuncSetAttribute(hestenes_svd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  hestenes_svd_kernel<false><<<1, 512, smem, st>>>(W, l, U, S, V, VT, nullptr);
   APX_LAUNCH_CHECK();
   return OK;
 }

@@ -112,7 +112,8 @@ __global__ void __launch_bounds__(kThreads, 1)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     float* __restrict__ C, int64_t ldc, int64_t c_split_stride, int M, int N, int K,
                     int k_per_split, int accumulate, const int* __restrict__ mJ, int mk, int mod_n,
-                    double* __restrict__ sq_partial, int c_async, const int* __restrict__ ready, int ready_rows) {
+                    double* __restrict__ sq_partial, int c_async, const int* __restrict__ ready, int ready_rows,
+                    const int* __restrict__ progress, int* __restrict__ defer, unsigned long long stall_ns) {
   using CF = Cfg<BN, STAGES>;
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte alignment for the swizzled tiles
@@ -126,6 +127,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
   __shared__ int sJ[128];
   __shared__ double sq_red[4];
+  __shared__ int s_deferred;
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
@@ -236,7 +238,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     // C tile staged through the (drained) operand ring for a read-modify-write epilogue
     constexpr bool kStageC = !TRANS_OUT && (size_t)STAGES * CF::kStage >= (size_t)BM * BN * 4;
-    const bool stage_c = kStageC && accumulate && c_async;
+    bool stage_c = kStageC && accumulate && c_async;
     if (accumulate && !TRANS_OUT && !stage_c) {
       // the read-modify-write epilogue reads this CTA's C tile: start pulling it toward L2 now
       // (overlaps the main loop); 128 threads x BN/32 lines per row group
@@ -249,26 +251,66 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_wait(done, 0);
     fence_after();
+    bool deferred = false;
     if (ready != nullptr && accumulate) {
       // C rows are produced by a concurrent kernel (the persistent gather) that publishes one flag
       // per block of ready_rows rows: wait (acquire) for the blocks under this tile before reading
       // C. The operand pipeline above has already run, so only the read-modify-write waits.
       // The first epilogue warp polls one flag per lane (relaxed loads, all in flight at once),
       // then one fence turns the observed flags into an acquire for the whole CTA.
+      // Bounded wait: if the producer makes no progress at all (its `progress` counter -- the
+      // gather's row-block ticket -- stands still for stall_ns (20 ms), e.g. because none of its CTAs is
+      // resident under an MPS SM limit or a co-tenant), the tile is deferred instead: it leaves
+      // C untouched, records itself in `defer`, and qw_fixup_sum_kernel adds its Q.W after the
+      // producer finished (stream-ordered), so the SMs held here are released.
       if (warp == 2) {
         const int b0 = m0 / ready_rows, b1 = (min(M, m0 + BM) - 1) / ready_rows;
-        for (int bb = b0; bb <= b1; bb += 32) {
-          const int b = bb + lane;
-          while (!__all_sync(0xffffffffu, b > b1 || ld_relaxed_gpu(ready + b) != 0)) __nanosleep(128);
+        bool stalled = false;
+        unsigned long long t0 = 0;
+        int last = 0;
+        if (defer && lane == 0) {
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          last = ld_relaxed_gpu(progress);
         }
+        for (int bb = b0; bb <= b1 && !stalled; bb += 32) {
+          const int b = bb + lane;
+          while (!__all_sync(0xffffffffu, b > b1 || ld_relaxed_gpu(ready + b) != 0)) {
+            __nanosleep(128);
+            if (defer) {
+              int st = 0;
+              if (lane == 0) {
+                unsigned long long now;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                const int cur = ld_relaxed_gpu(progress);
+                if (cur != last) {
+                  last = cur;
+                  t0 = now;
+                } else if (now - t0 > stall_ns) {
+                  st = 1;
+                }
+              }
+              if (__shfl_sync(0xffffffffu, st, 0)) {
+                stalled = true;
+                break;
+              }
+            }
+          }
+        }
+        if (lane == 0) s_deferred = stalled ? 1 : 0;
         __threadfence();
       }
       asm volatile("bar.sync 2, 128;" ::: "memory");  // the four epilogue warps only
+      deferred = s_deferred != 0;
+    }
+    if (deferred && et == 0) {
+      const int slot = atomicAdd(defer, 1);
+      defer[1 + slot] = ((int)blockIdx.z * (int)gridDim.y + (int)blockIdx.y) * (int)gridDim.x + (int)blockIdx.x;
     }
     const int quarter = warp & 3;
     const int row = m0 + quarter * 32 + lane;
     float* Cz = C + (size_t)kz * c_split_stride;
     double sq = 0.0;  // sum of squares of the values this thread stores (sq_partial)
+    if (deferred) stage_c = false;
     if (stage_c) {
       // Each warp copies its 32 x BN slab of C into the ring with cp.async (every 16-byte granule
       // in flight at once), adds the accumulator in place, then streams the rows back out.
@@ -330,7 +372,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       sq += (double)sq32[0] + (double)sq32[1];
     }
 #pragma unroll 1
-    for (int j0 = 0; j0 < BN && !stage_c; j0 += 32) {
+    for (int j0 = 0; j0 < BN && !stage_c && !deferred; j0 += 32) {
       float v[32];
       if (ktiles > 0) {
         tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)j0, v);
@@ -442,10 +484,21 @@ static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t c
   return OK;
 }
 
+// Stall threshold of the bounded ready-flag wait; APX_QW_STALL_NS overrides it (tests set 0 to
+// force the deferral path).
+static unsigned long long stall_ns() {
+  static const unsigned long long v = [] {
+    const char* e = getenv("APX_QW_STALL_NS");
+    return e ? strtoull(e, nullptr, 10) : 20ull * 1000 * 1000;
+  }();
+  return v;
+}
+
 template <int BN, int STAGES, bool A_MN, bool B_MN, bool TRANS_OUT, bool MASK>
 static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                   int64_t c_split_stride, int M, int N, int K, int splits, int accumulate, const int* mJ, int mk,
-                  int mod_n, double* sq_partial, const int* ready, int ready_rows, cudaStream_t st) {
+                  int mod_n, double* sq_partial, const int* ready, int ready_rows, const int* progress,
+                  int* defer, cudaStream_t st) {
   using CF = Cfg<BN, STAGES>;
   CUtensorMap ta, tb;
   // A operand: K-major stored [M][K]; MN-major stored [K][M]
@@ -457,12 +510,57 @@ static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, floa
   APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem));
   const int c_async = ((uintptr_t)C % 16) == 0 && (ldc % 4) == 0 && (N % 4) == 0 && (c_split_stride % 4) == 0;
   fn<<<grid, kThreads, CF::kSmem, st>>>(ta, tb, C, ldc, c_split_stride, M, N, K, kps, accumulate, mJ, mk, mod_n,
-                                        sq_partial, c_async, ready, ready_rows);
+                                        sq_partial, c_async, ready, ready_rows, progress, defer, stall_ns());
   APX_LAUNCH_CHECK();
   return OK;
 }
 
 }  // namespace tma
+
+// Completes the tiles gemm_tma_kernel deferred (bounded wait: its producer made no progress)
+// and then sums the per-tile ||C||^2 partials exactly like sum_vector_kernel (1024 threads,
+// strided per-thread sums, fixed block tree), so the normal path's bits are unchanged. One CTA:
+// this only runs real work in the pathological no-co-residency case; normally defer[0] == 0.
+// The deferred tiles use fp32 FMAs on TF32-truncated operands (the tensor core's inputs).
+__global__ void __launch_bounds__(1024)
+    qw_fixup_sum_kernel(const float* __restrict__ Q, int64_t ldq, const float* __restrict__ W, int64_t ldw,
+                        float* __restrict__ C, int64_t ldc, int M, int N, int K, int bn, int* __restrict__ defer,
+                        double* __restrict__ sq_partial, int parts, double* __restrict__ out) {
+  __shared__ double sh[32];
+  const int cnt = defer[0];
+  const int gx = (int)ceil_div(N, bn);
+  for (int d = 0; d < cnt; ++d) {
+    const int tile = defer[1 + d];
+    const int m0 = (tile / gx) * tma::BM, n0 = (tile % gx) * bn;
+    double sq = 0.0;
+    for (int e = threadIdx.x; e < tma::BM * bn; e += blockDim.x) {
+      const int r = m0 + e / bn, c = n0 + e % bn;
+      if (r >= M || c >= N) continue;
+      float acc = 0.f;
+      for (int k = 0; k < K; ++k)
+        acc = fmaf(__uint_as_float(__float_as_uint(Q[(size_t)r * ldq + k]) & 0xffffe000u),
+                   __uint_as_float(__float_as_uint(W[(size_t)k * ldw + c]) & 0xffffe000u), acc);
+      const float val = C[(size_t)r * ldc + c] + acc;
+      C[(size_t)r * ldc + c] = val;
+      sq = fma((double)val, (double)val, sq);
+    }
+    sq = block_sum(sq, sh);
+    if (threadIdx.x == 0) sq_partial[tile] = sq;
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) defer[0] = 0;  // ready for the next product
+  double s = 0.0;
+  for (int i = threadIdx.x; i < parts; i += blockDim.x) s += sq_partial[i];
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0) *out = s;
+}
+
+int launch_qw_fixup_sum(const float* Q, int64_t ldq, const float* W, int64_t ldw, float* C, int64_t ldc, int M, int N,
+                        int K, int bn, int* defer, double* sq_partial, int parts, double* out, cudaStream_t st) {
+  qw_fixup_sum_kernel<<<1, 1024, 0, st>>>(Q, ldq, W, ldw, C, ldc, M, N, K, bn, defer, sq_partial, parts, out);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
 
 // Same contract as umma_gemm (umma.cu); requires 16-byte aligned bases and leading dimensions,
 // M, N multiples of 32 for MN-major operands. layout bits: 1 A MN-major, 2 B MN-major, 4 C^T.
@@ -471,9 +569,11 @@ static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, floa
 int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                   int64_t ldc, int64_t c_split_stride, int M, int N, int K, int splits, int accumulate,
                   const int* mJ, int mk, int mod_n, cudaStream_t st, double* sq_partial, const int* ready,
-                  int ready_rows) {
+                  int ready_rows, const int* progress, int* defer) {
   APX_REQUIRE(ready == nullptr || (accumulate && ready_rows > 0 && splits == 1 && !(layout & 4)),
               "umma_tma_gemm: ready flags need an accumulating, split-free, row-major C");
+  APX_REQUIRE(defer == nullptr || (ready != nullptr && progress != nullptr && sq_partial != nullptr),
+              "umma_tma_gemm: deferral needs ready flags, a progress counter and sq partials");
   APX_REQUIRE(mk <= 128, "umma_tma_gemm: at most 128 masked shifts");
   APX_REQUIRE(((uintptr_t)A % 16) == 0 && ((uintptr_t)B % 16) == 0 && (lda % 4) == 0 && (ldb % 4) == 0,
               "umma_tma_gemm: 16-byte aligned operands required");
@@ -485,7 +585,7 @@ int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* 
     return tma::launch<BNV, ST, (L & 1) != 0, (L & 2) != 0, (L & 4) != 0, MK>(A, lda, B, ldb, C, ldc,          \
                                                                               c_split_stride, M, N, K, splits, \
                                                                               accumulate, mJ, mk, mod_n,       \
-                                                                              sq_partial, ready, ready_rows, st);
+                                                                              sq_partial, ready, ready_rows, progress, defer, st);
   APX_TL(64, 4, 0, false) APX_TL(64, 4, 1, false) APX_TL(64, 4, 2, false) APX_TL(64, 4, 3, false)
   APX_TL(64, 4, 4, false) APX_TL(64, 4, 5, false) APX_TL(64, 4, 6, false) APX_TL(64, 4, 7, false)
   APX_TL(64, 4, 1, true) APX_TL(64, 4, 5, true)

@@ -79,16 +79,20 @@ class FourierRowSpectrum:
 
 
 def fourier_row_decompose(A) -> FourierRowSpectrum:
-    """fsparse.py:92-105 -- F = W(rows)/sqrt(n) on the device; weights / unit directions."""
-    A = D.as_host_matrix(A)
-    n = A.shape[1]
-    F = unitary_dft(A, "forward", axis=1) / math.sqrt(n)
-    col = np.linalg.norm(F, axis=0)
-    weights = math.sqrt(n) * col
-    directions = np.zeros_like(F)
-    nz = weights > 0
-    directions[:, nz] = F[:, nz] / col[nz]
-    return FourierRowSpectrum(weights=weights, directions=directions)
+    """fsparse.py:92-105 -- F = W(rows)/sqrt(n), weights sqrt(n)||f_k||, unit directions (zero
+    column where the weight vanishes): one row-DFT pass and one column pass on the device
+    (apx_fourier_row_decompose)."""
+    Ah = D.as_host_matrix(A)
+    m, n = Ah.shape
+    cplx = np.iscomplexobj(Ah)
+    dev = D.require_cuda()
+    Ad = torch.from_numpy(np.ascontiguousarray(Ah.astype(np.complex128 if cplx else np.float64))).to(dev)
+    weights = torch.empty(n, dtype=torch.float64, device=dev)
+    directions = torch.empty((m, n), dtype=torch.complex128, device=dev)
+    ws = D.workspace(N.size("apx_fourier_row_decompose_workspace", m, n))
+    N.call("apx_fourier_row_decompose", N.APX_C128 if cplx else N.APX_F64, Ad.data_ptr(), m, n, weights.data_ptr(),
+           directions.data_ptr(), ws.data_ptr(), ws.numel(), D.stream_ptr())
+    return FourierRowSpectrum(weights=weights.cpu().numpy(), directions=directions.cpu().numpy())
 
 
 def _row_budgets(k, rows: int, cols: int) -> list[int]:

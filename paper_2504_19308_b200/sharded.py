@@ -11,8 +11,11 @@ must be combined (apx_mixed_rows_phase, include/apx.h):
               -> sum of [||A_g||^2, ||M_g||^2]
 
 Only small factors cross ranks: two 64 x 64 fp64 Gram matrices, the 64 x n fp32 Bm (2 MiB at
-n = 8192) and two scalars -- the "all-gather of the small truncated factors" of the north star,
-as all-reduces. Every rank factors the same summed Gram, so the pass-2 decision and the
+n = 8192) and two scalars -- the "all-gather of the small truncated factors" of the north star.
+Each exchange is an all-gather followed by a local sum in rank order (``ordered_sum``, SURVEY.md
+§5 / §8(e)), never an NCCL all-reduce: the sum's bits then do not depend on the world size's
+reduction tree or NCCL's algorithm choice, every rank holds the identical sum, and the result is
+bitwise the lockstep (single-process) result. Every rank factors the same summed Gram, so the pass-2 decision and the
 orthonormal basis agree across ranks; B's cycle selection is computed on every rank from the same
 B (no exchange), so the selected indices are identical by construction.
 
@@ -134,12 +137,38 @@ def cycle_rows_steps(A_rows, row0: int, B, k_a: int, k_b: int, order: int, out=N
 
 
 def cycle_product_rows(A_rows, row0: int, B, k_a: int, k_b: int, order: int, group=None, out=None):
-    """This rank's rows of the cycle product; the two exchanges are torch.distributed all-reduces
-    (NCCL on the current stream for CUDA tensors)."""
+    """This rank's rows of the cycle product; the two exchanges are ordered all-gather sums
+    (``ordered_sum``: NCCL on the current stream for CUDA tensors)."""
+    return _drive(cycle_rows_steps(A_rows, row0, B, k_a, k_b, order, out), lambda t: ordered_sum(t, group))
+
+
+def rank_order_sum(parts):
+    """Sum of the per-rank tensors in rank order: ((p0 + p1) + p2) + ... (the order lockstep uses)."""
+    total = parts[0].clone()
+    for t in parts[1:]:
+        total += t
+    return total
+
+
+def ordered_sum(t, group=None):
+    """In place: t <- sum over ranks of t, as an all-gather plus a fixed rank-order local sum
+    (deterministic and identical on every rank, independent of NCCL's reduction algorithm).
+    NCCL groups gather into one buffer (ncclAllGather); other backends (gloo) gather a list."""
     import torch.distributed as dist
 
-    return _drive(cycle_rows_steps(A_rows, row0, B, k_a, k_b, order, out),
-                  lambda t: dist.all_reduce(t, group=group))
+    world = dist.get_world_size(group)
+    if world == 1:
+        return t
+    flat = t.contiguous().view(-1)
+    if dist.get_backend(group) == "nccl":
+        buf = torch.empty((world, flat.numel()), dtype=t.dtype, device=t.device)
+        dist.all_gather_into_tensor(buf, flat, group=group)
+        parts = list(buf.unbind(0))
+    else:
+        parts = [torch.empty_like(flat) for _ in range(world)]
+        dist.all_gather(parts, flat, group=group)
+    t.view(-1).copy_(rank_order_sum(parts))
+    return t
 
 
 def check_breakdown(result):
@@ -162,13 +191,10 @@ def _drive(gen, reduce):
 
 def mixed_product_rows(A_rows, B, k_svd: int, k_cyc: int, order: int, omega, group=None, out=None,
                        check: bool = True):
-    """This rank's rows of the C4 product; the exchanges are torch.distributed all-reduces (NCCL on
-    the current stream for CUDA tensors). check=False skips the (synchronising) breakdown check --
-    call check_breakdown(result) later."""
-    import torch.distributed as dist
-
-    r = _drive(mixed_rows_steps(A_rows, B, k_svd, k_cyc, order, omega, out),
-               lambda t: dist.all_reduce(t, group=group))
+    """This rank's rows of the C4 product; the exchanges are ordered all-gather sums
+    (``ordered_sum``: NCCL on the current stream for CUDA tensors). check=False skips the
+    (synchronising) breakdown check -- call check_breakdown(result) later."""
+    r = _drive(mixed_rows_steps(A_rows, B, k_svd, k_cyc, order, omega, out), lambda t: ordered_sum(t, group))
     return check_breakdown(r) if check else r
 
 
@@ -180,9 +206,7 @@ def lockstep(gens):
     pending = [next(g) for g in gens]
     results = [None] * len(gens)
     while True:
-        total = pending[0].clone()
-        for t in pending[1:]:
-            total += t
+        total = rank_order_sum(pending)
         nxt = []
         for i, (g, t) in enumerate(zip(gens, pending)):
             t.copy_(total)

@@ -118,8 +118,6 @@ def randomized_partial_svd(A, s: int, seed, power_iterations: int = 0,
         raise ValueError("power_iterations must be >= 0")
     rng = np.random.default_rng(seed)
     phi = rng.standard_normal((n, k))
-    if k > 128 or k > n:
-        raise ValueError(f"sketch width {k} outside the device range [1, min(128, n)]")
     U, S, V, scal = _rsvd_device(_dev64(Ah), k, k, power_iterations, phi)
     fro2 = float(scal[N.S_FRO2_A].item())
     return TruncatedSVD(U=U.cpu().numpy(), sigma=S.cpu().numpy(), V=V.cpu().numpy(), source_frobenius_sq=fro2)

@@ -145,6 +145,17 @@ def fsparse_cases():
     d["tk_T"] = T
     for k in range(0, 6):
         d[f"tk_{k}"] = rf.topk_sparsify(T, k).to_dense()
+    # fourier_row_decompose (fsparse.py:92-105): real, complex, n = 1, a rank-one row structure
+    # (all weight in f_0: zero directions elsewhere), an odd length
+    rf_rng = np.random.default_rng(401)
+    frs = {"real": rf_rng.standard_normal((5, 8)),
+           "cplx": rf_rng.standard_normal((7, 16)) + 1j * rf_rng.standard_normal((7, 16)),
+           "n1": rf_rng.standard_normal((3, 1)),
+           "const": np.outer(rf_rng.standard_normal(4), np.ones(6)),
+           "odd": rf_rng.standard_normal((6, 97))}
+    for tag, X in frs.items():
+        spec = rf.fourier_row_decompose(X)
+        d[f"frs_{tag}_A"], d[f"frs_{tag}_w"], d[f"frs_{tag}_d"] = X, spec.weights, spec.directions
     np.savez_compressed(os.path.join(OUT, "fsparse.npz"), **d)
 
 

@@ -55,7 +55,7 @@ def test_single_rank_no_collective():
 
 # ---- the row-sharded product's exchange protocol (paper_2504_19308_b200.sharded) over gloo ----
 # The device phases are replaced by their fp64 algebra on CPU tensors (test-only stand-ins); what
-# is checked is the host protocol the GPU path uses -- one in-place all-reduce per exchange point,
+# is checked is the host protocol the GPU path uses -- one in-place ordered sum per exchange point,
 # in order -- and that the row-block algebra reproduces the unsharded projection Q Q^T A.
 
 def _toy_rows_steps(A_rows, Omega):
@@ -73,13 +73,13 @@ def _sharded_worker(rank, world, port, q):
     os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        from paper_2504_19308_b200.sharded import _drive, row_range
+        from paper_2504_19308_b200.sharded import _drive, ordered_sum, row_range
         g = torch.Generator().manual_seed(7)
         n, l = 320, 8
         A = torch.randn(n, n, generator=g, dtype=torch.float64)
         Omega = torch.randn(n, l, generator=g, dtype=torch.float64)
         r0, r1 = row_range(n, world, rank)
-        P_rows = _drive(_toy_rows_steps(A[r0:r1], Omega), lambda t: dist.all_reduce(t))
+        P_rows = _drive(_toy_rows_steps(A[r0:r1], Omega), ordered_sum)
         q.put((rank, r0, r1, P_rows.numpy()))
     finally:
         dist.destroy_process_group()
@@ -150,11 +150,11 @@ def _sharded_cycle_worker(rank, world, port, q):
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
         import oracle as O
-        from paper_2504_19308_b200.sharded import _drive, cycle_row_range
+        from paper_2504_19308_b200.sharded import _drive, cycle_row_range, ordered_sum
         n, k = 256, 8
         A, B = O.gen_cycle_operand(n, k, 31), O.gen_cycle_operand(n, k, 32)
         r0, r1 = cycle_row_range(n, world, rank, align=64)
-        JA, Mg, fro2 = _drive(_toy_cycle_rows_steps(A, B, r0, r1, k), lambda t: dist.all_reduce(t))
+        JA, Mg, fro2 = _drive(_toy_cycle_rows_steps(A, B, r0, r1, k), ordered_sum)
         q.put((rank, r0, r1, JA, Mg, fro2))
     finally:
         dist.destroy_process_group()
@@ -190,3 +190,45 @@ def test_cycle_row_range_partition():
             blocks = [cycle_row_range(n, world, r, align) for r in range(world)]
             assert blocks[0][0] == 0 and blocks[-1][1] == n
             assert all(a[1] == b[0] and a[0] % align == 0 for a, b in zip(blocks, blocks[1:]))
+
+
+# ---- ordered_sum: all-gather + rank-order sum, bitwise equal on every rank ----
+
+def _ordered_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2504_19308_b200.sharded import ordered_sum
+        g = torch.Generator().manual_seed(100 + rank)
+        # magnitudes spread over 1e-8..1e8: a different summation order changes the last bits
+        t = torch.randn(4096, generator=g, dtype=torch.float64) * torch.logspace(-8, 8, 4096, dtype=torch.float64)
+        t32 = t.float().reshape(64, 64)
+        ordered_sum(t)
+        ordered_sum(t32)
+        q.put((rank, t.numpy().tobytes(), t32.numpy().tobytes()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_ordered_sum_bitwise_gloo():
+    import numpy as np
+    from paper_2504_19308_b200.sharded import rank_order_sum
+    world, port = 3, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_ordered_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted((q.get(timeout=120) for _ in range(world)), key=lambda o: o[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    parts = []
+    for r in range(world):
+        g = torch.Generator().manual_seed(100 + r)
+        parts.append(torch.randn(4096, generator=g, dtype=torch.float64) *
+                     torch.logspace(-8, 8, 4096, dtype=torch.float64))
+    want = rank_order_sum(parts).numpy().tobytes()
+    want32 = rank_order_sum([p.float().reshape(64, 64) for p in parts]).numpy().tobytes()
+    assert all(o[1] == want for o in out)          # identical bits on every rank = lockstep's order
+    assert all(o[2] == want32 for o in out)

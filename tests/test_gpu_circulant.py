@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from conftest import rel
+from conftest import check_report, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -47,6 +47,7 @@ def test_circulant_golden(C, golden, n):
         near_tie_ok(rep.selected_b, sel_b, mags_b)
         if rep.selected_a == list(g[f"cd{n}_sel"]) and rep.selected_b == sel_b:
             assert rel(M, ref) < 1e-10
+            check_report(rep, g[f"cd{n}_rep{order}"], rel_tol=1e-6, abs_tol=1e-9)
         else:  # re-run the oracle with the GPU's selections forced
             Mo, _ = O.circulant_first_order_multiply(A, B, k, order, rep.selected_a, rep.selected_b)
             assert rel(M, Mo) < 1e-10

@@ -7,7 +7,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from conftest import rel
+from conftest import check_report, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -60,6 +60,7 @@ def test_sfft_golden(F, golden, tag):
                 r = g[f"{tag}_rep{order}{mode}"]
                 assert rep.norm_da == pytest.approx(r[0], rel=1e-9, abs=1e-12)
                 assert rep.norm_db == pytest.approx(r[1], rel=1e-9, abs=1e-12)
+                check_report(rep, r, rel_tol=1e-9, abs_tol=1e-12)
 
 
 def test_topk_sparsify_golden(F, golden):
@@ -92,3 +93,49 @@ def test_sfft_vs_oracle_n256(F, mode):
     B = rng.standard_normal((256, 256))
     for order in (0, 1):
         parity(F, A, B, 16, order, mode)
+
+
+@pytest.mark.parametrize("k", [257, 700])
+@pytest.mark.parametrize("mode", ["rows", "cols"])
+def test_sfft_wide_k(F, k, mode):
+    """k > 256 kept entries per row (the sparse row gather stages its entries in 256-wide tiles;
+    the reference has no k limit, fsparse.py:168-240)."""
+    rng = np.random.default_rng(100 + k)
+    A = rng.standard_normal((1024, 1024))
+    B = rng.standard_normal((1024, 1024))
+    for order in (0, 1):
+        parity(F, A, B, k, order, mode)
+
+
+def test_sparse_dense_right_dense_column(F):
+    """B @ S where one column of S is kept by > 256 rows: the transposed bucket has > 256 entries
+    (fsparse.py:158-164 has no limit)."""
+    rng = np.random.default_rng(5)
+    M = rng.standard_normal((300, 40)) + 1j * rng.standard_normal((300, 40))
+    M[:, 7] *= 1e3
+    S = F.topk_sparsify(M, 3)
+    assert sum(1 for row in S.entries for j, _ in row if j == 7) == 300
+    Y = rng.standard_normal((9, 300))
+    assert np.allclose(F.sparse_dense_multiply(S, Y, "right"), Y @ S.to_dense(), rtol=0, atol=1e-9)
+    X = rng.standard_normal((40, 5))
+    assert np.allclose(F.sparse_dense_multiply(S, X, "left"), S.to_dense() @ X, rtol=0, atol=1e-9)
+
+
+@pytest.mark.parametrize("tag", ["real", "cplx", "n1", "const", "odd"])
+def test_fourier_row_decompose_golden(F, golden, tag):
+    """fsparse.py:92-105 on the device vs the reference's own output (weights, directions,
+    zero directions where the weight vanishes)."""
+    g = golden("fsparse")
+    spec = F.fourier_row_decompose(g[f"frs_{tag}_A"])
+    assert np.allclose(spec.weights, g[f"frs_{tag}_w"], rtol=1e-12, atol=1e-13)
+    assert np.allclose(spec.directions, g[f"frs_{tag}_d"], rtol=1e-12, atol=1e-13)
+    assert spec.directions.dtype == np.complex128
+
+
+def test_fourier_row_decompose_vs_oracle_large(F):
+    rng = np.random.default_rng(12)
+    A = rng.standard_normal((300, 1024))
+    spec = F.fourier_row_decompose(A)
+    w, d = O.fourier_row_decompose(A)
+    assert rel(spec.weights, w) < 1e-12 and rel(spec.directions, d) < 1e-12
+    assert np.sum(spec.weights ** 2) == pytest.approx(np.sum(A ** 2), rel=1e-12)

@@ -4,7 +4,7 @@ import numpy as np
 import pytest
 
 import oracle as O
-from conftest import rel
+from conftest import check_report, rel
 
 pytestmark = pytest.mark.gpu
 
@@ -25,6 +25,7 @@ def test_svd_product_golden(S, golden, tag):
         r = g[tag + f"_rep{order}"]
         assert rep.norm_da == pytest.approx(r[0], rel=1e-6, abs=1e-7 * np.linalg.norm(g[tag + "_A"]))
         assert rep.k == int(r[4])
+        check_report(rep, r, rel_tol=1e-6, abs_tol=1e-7)  # apriori / posterior estimates
 
 
 @pytest.mark.parametrize("tag", ["svd16_1_0", "svd32_2_1", "svd64_1_0", "svd64_2_2"])
@@ -139,3 +140,33 @@ def test_rectangular_and_errors(S):
         S.randomized_partial_svd(np.ones((4, 4)), 1, seed=0, power_iterations=-1)
     with pytest.raises(ValueError):
         S.randomized_partial_svd(np.ones((4, 4)), 1, seed=0, components=0)
+
+
+def test_wide_sketch_crit4c_shape(S):
+    """Sketch width > 128: the reference's crit 4c input shape (n=700, s=60 -> k=541,
+    pkg/tests/test_acceptance.py:187-198). Householder QR + global-memory Jacobi SVD."""
+    n, s = 700, 60
+    assert S.component_count(n, s) == 541
+    rng = np.random.default_rng(7)
+    A = rng.standard_normal((n, n)) * np.exp(-np.arange(n) / 50.0)[None, :]
+    d = S.randomized_partial_svd(A, s, 3)
+    do = O.rsvd(A, 541, np.random.default_rng(3))
+    assert d.k == 541
+    assert rel(d.sigma, do[1]) < 1e-10
+    rec = (d.U * d.sigma) @ d.V.T
+    reco = (do[0] * do[1]) @ do[2].T
+    assert rel(rec, reco) < 1e-9
+    assert np.allclose(d.U.T @ d.U, np.eye(541), atol=1e-10)
+    for order in (0, 1):
+        M, rep = S.svd_first_order_multiply(A, A, s, order, 2)
+        Mo, ro = O.svd_first_order_multiply(A, A, s, order, 2)
+        assert rel(M, Mo) < 1e-10
+        assert rep.k == 541
+
+
+def test_wide_sketch_qr(S):
+    rng = np.random.default_rng(8)
+    Y = rng.standard_normal((400, 200))
+    Q, R = S.qr_decompose(Y)
+    Qn, Rn = np.linalg.qr(Y)
+    assert rel(Q, Qn) < 1e-10 and rel(R, Rn) < 1e-10

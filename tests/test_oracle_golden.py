@@ -172,3 +172,11 @@ def test_sketch_norm_golden(golden):
         got = O.sketch_norm_estimate(g[f"sk_{name}_A"], g[f"sk_{name}_B"], k, seed)
         ref = float(g[f"sk_{name}_out"])
         assert abs(got - ref) <= 1e-12 * max(1.0, abs(ref)), name
+
+
+@pytest.mark.parametrize("tag", ["real", "cplx", "n1", "const", "odd"])
+def test_fourier_row_decompose_golden(golden, tag):
+    g = golden("fsparse")
+    w, d = O.fourier_row_decompose(g[f"frs_{tag}_A"])
+    assert np.allclose(w, g[f"frs_{tag}_w"], rtol=1e-12, atol=1e-13)
+    assert np.allclose(d, g[f"frs_{tag}_d"], rtol=1e-12, atol=1e-13)
