@@ -15,7 +15,7 @@ import torch
 
 from . import _device as D
 from . import _native as N
-from .errest import ErrorModel, finish_report
+from .errest import ErrorModel, finish_report, energy_residual
 
 __all__ = [
     "CirculantSpectrum",
@@ -166,8 +166,8 @@ def circulant_first_order_multiply(A, B, k: int, order: int, model: ErrorModel |
     s = r["scalars"].tolist()
     wall = time.perf_counter() - t0
     nA, nB = math.sqrt(max(0.0, s[N.S_FRO2_A])), math.sqrt(max(0.0, s[N.S_FRO2_B]))
-    ndA = math.sqrt(max(0.0, s[N.S_FRO2_A] - s[N.S_KEPT_A]))
-    ndB = math.sqrt(max(0.0, s[N.S_FRO2_B] - s[N.S_KEPT_B]))
+    ndA = energy_residual(s[N.S_FRO2_A], s[N.S_KEPT_A], n * n)  # circulant.py:130-133
+    ndB = energy_residual(s[N.S_FRO2_B], s[N.S_KEPT_B], n * n)
     rep = finish_report("cd", order, k, nA, nB, ndA, ndB, math.sqrt(max(0.0, s[N.S_FRO2_M])), n, wall, model)
     rep.selected_a = r["sel_a"].tolist()
     rep.selected_b = r["sel_b"].tolist()

@@ -297,7 +297,9 @@ struct UmmaStages {
   static int qt_times_a(const float* A, const float* Q, float* Bm, float* part, int n, int l, cudaStream_t st,
                         int sms = kNumSMs) {
     const int s = splits(n, sms);
-    APX_TRY(umma_gemm(7, 64, A, n, Q, l, s > 1 ? part : Bm, n, (int64_t)l * n, n, l, n, s, 0, nullptr, 0, 1, st));
+    // layout bit 8: operands rounded to TF32 nearest in shared memory, so ||Bm||^2 = sum sigma^2
+    // (the residual energy ||A||^2 - ||Bm||^2, svd.py:122-130) carries no truncation bias
+    APX_TRY(umma_gemm(7 | 8, 64, A, n, Q, l, s > 1 ? part : Bm, n, (int64_t)l * n, n, l, n, s, 0, nullptr, 0, 1, st));
     if (s > 1) APX_TRY(launch_split_reduce_f32(part, s, (size_t)n * l, Bm, st));
     return OK;
   }
@@ -564,7 +566,7 @@ static int run_mixed_rows_phase(int phase, const float* A, int m, const float* B
     APX_TRY(cholqr_rows_pass2(m, l, (const double*)red_in, Q, r.qr, r.qr_bytes, lo));
     // Bm_g = Q_g^T A_g, computed as (A_g^T Q_g) stored transposed
     const int s = UmmaStages::splits(n, free_sms);
-    APX_TRY(umma_tma_gemm(7, 64, A, n, Q, l, s > 1 ? part : (float*)red_out, n, (int64_t)l * n, n, l, m, s, 0,
+    APX_TRY(umma_tma_gemm(7 | 8, 64, A, n, Q, l, s > 1 ? part : (float*)red_out, n, (int64_t)l * n, n, l, m, s, 0,
                           nullptr, 0, 1, lo));
     if (s > 1) APX_TRY(launch_split_reduce_f32(part, s, (size_t)n * l, (float*)red_out, lo));
   }
@@ -767,7 +769,7 @@ int apx_debug_umma_gemm(int layout, int bn, const float* A, int64_t lda, const f
   APX_REQUIRE(M >= 1 && N >= 1 && K >= 1 && splits >= 1, "bad GEMM shape");
   const int64_t slice = (int64_t)((layout & 4) ? N : M) * ldc;
   if (layout & 32)
-    return umma_tma_gemm(layout & 7, bn, A, lda, B, ldb, C, ldc, slice, (int)M, (int)N, (int)K, splits,
+    return umma_tma_gemm(layout & 15, bn, A, lda, B, ldb, C, ldc, slice, (int)M, (int)N, (int)K, splits,
                          accumulate, mask_j, mask_k, mod_n, S(stream));
   return umma_gemm(layout, bn, A, lda, B, ldb, C, ldc, slice, (int)M, (int)N, (int)K, splits, accumulate,
                    mask_j, mask_k, mod_n, S(stream));

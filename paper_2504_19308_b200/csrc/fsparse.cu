@@ -123,11 +123,16 @@ __global__ void merge_planes_kernel(const double* __restrict__ re, const double*
     z[e] = cadd(z[e], make_double2(re[e], im[e]));
 }
 
-// fourier_row_decompose (fsparse.py:92-105): F = W(rows) / sqrt(n) in place, then per column k
-// the 2-norm over the rows (one thread per column, rows in order: coalesced across the warp),
-// weights[k] = sqrt(n) ||f_k||, directions[:, k] = f_k / ||f_k|| (zero column where ||f_k|| = 0).
-__global__ void fourier_columns_kernel(double2* __restrict__ F, int m, int n, double inv_sqrt_n, double sqrt_n,
-                                       double* __restrict__ weights) {
+// fourier_row_decompose (fsparse.py:92-105), three passes over F = W(rows):
+//  1. per column k (one thread per column, rows in order: coalesced across the warp): F /= sqrt(n)
+//     in place and nrm[k] = ||f_k||_2;
+//  2. one CTA: ||A||^2 = sum_k n nrm[k]^2 (fixed order) and the transform's rounding floor
+//     4 eps log2(n) ||A||: a column whose exact transform is zero (pocketfft returns exact zeros for,
+//     e.g., constant rows) comes out of a floating-point FFT at that noise level instead;
+//  3. weights[k] = sqrt(n) nrm[k] and directions f_k / nrm[k], or 0 and a zero column at or below
+//     the floor ("zero column where the weight vanishes").
+__global__ void fourier_colnorm_kernel(double2* __restrict__ F, int m, int n, double inv_sqrt_n,
+                                       double* __restrict__ nrm) {
   const int k = blockIdx.x * blockDim.x + threadIdx.x;
   if (k >= n) return;
   double s = 0.0;
@@ -138,14 +143,30 @@ __global__ void fourier_columns_kernel(double2* __restrict__ F, int m, int n, do
     F[(size_t)i * n + k] = v;
     s = fma(v.x, v.x, fma(v.y, v.y, s));
   }
-  const double nrm = sqrt(s);
-  weights[k] = sqrt_n * nrm;
-  const double inv = nrm > 0.0 ? 1.0 / nrm : 0.0;
+  nrm[k] = sqrt(s);
+}
+
+__global__ void fourier_floor_kernel(const double* __restrict__ nrm, int n, double* __restrict__ floor_out) {
+  __shared__ double sh[32];
+  double s = 0.0;
+  for (int k = threadIdx.x; k < n; k += blockDim.x) s = fma(nrm[k], nrm[k], s);
+  s = block_sum(s, sh);
+  if (threadIdx.x == 0)
+    *floor_out = 4.0 * 2.220446049250313e-16 * log2(fmax(2.0, (double)n)) * sqrt((double)n * s);
+}
+
+__global__ void fourier_scale_kernel(double2* __restrict__ F, int m, int n, double sqrt_n,
+                                     const double* __restrict__ nrm, const double* __restrict__ floor_in,
+                                     double* __restrict__ weights) {
+  const int k = blockIdx.x * blockDim.x + threadIdx.x;
+  if (k >= n) return;
+  const double c = nrm[k];
+  const bool keep = sqrt_n * c > *floor_in;
+  weights[k] = keep ? sqrt_n * c : 0.0;
   for (int i = 0; i < m; ++i) {
-    double2 v = F[(size_t)i * n + k];
-    F[(size_t)i * n + k] = nrm > 0.0 ? make_double2(v.x / nrm, v.y / nrm) : make_double2(0.0, 0.0);
+    const double2 v = F[(size_t)i * n + k];
+    F[(size_t)i * n + k] = keep ? make_double2(v.x / c, v.y / c) : make_double2(0.0, 0.0);
   }
-  (void)inv;
 }
 
 static unsigned grid_for(size_t cnt) { return (unsigned)std::min<int64_t>(ceil_div(cnt, 256), kNumSMs * 8); }
@@ -364,8 +385,14 @@ int apx_fourier_row_decompose(int dtype, const void* A, int64_t m, int64_t n, do
     APX_CUDA(cudaMemcpyAsync(X, A, mn * sizeof(double2), cudaMemcpyDeviceToDevice, st));
   }
   APX_TRY(apx_unitary_dft(X, directions, n, m, 1, n, 0, dft_ws, dft_bytes, stream));
-  fourier_columns_kernel<<<(unsigned)ceil_div(n, 128), 128, 0, st>>>((double2*)directions, (int)m, (int)n,
-                                                                     1.0 / sqrt((double)n), sqrt((double)n), weights);
+  double* nrm = (double*)X;  // X is consumed by the DFT; reuse it for the norms and the floor
+  const unsigned g = (unsigned)ceil_div(n, 128);
+  fourier_colnorm_kernel<<<g, 128, 0, st>>>((double2*)directions, (int)m, (int)n, 1.0 / sqrt((double)n), nrm);
+  APX_LAUNCH_CHECK();
+  fourier_floor_kernel<<<1, 1024, 0, st>>>(nrm, (int)n, nrm + n);
+  APX_LAUNCH_CHECK();
+  fourier_scale_kernel<<<g, 128, 0, st>>>((double2*)directions, (int)m, (int)n, sqrt((double)n), nrm, nrm + n,
+                                          weights);
   APX_LAUNCH_CHECK();
   return OK;
 }

@@ -7,7 +7,10 @@
 //               shared-memory ring, arming each stage's `full` mbarrier with the byte count.
 //   warp 1      TMEM allocator + MMA issuer: one lane issues tcgen05.mma.cta_group::1.kind::tf32
 //               (M=128, N=BN, K=8) x4 per stage and commits to the stage's `empty` mbarrier.
-//   warps 2..5  (MASK only) zero the kept-cycle entries of each landed A tile (dB^T), then
+//   warps 2..5  (FIX 1) zero the kept-cycle entries of each landed A tile (dB^T), or (FIX 2) round
+//               both landed operand tiles to TF32 nearest (the tensor core itself truncates: a
+//               systematic -2^-11.5 relative bias per operand, which a sum of squares of the
+//               result -- ||Q^T A||^2 for the residual energy -- accumulates), then
 //               epilogue: tcgen05.ld.32x32b.x32 from TMEM (warp%4 selects the lane quarter).
 // Layouts: K-major tiles use TMA SWIZZLE_128B <-> UMMA SWIZZLE_128B (rows of 128 B, 8-row atoms,
 // SBO = 1024 B, K advanced by 32 B per MMA); MN-major tiles (TF32 requires it) use TMA
@@ -107,7 +110,7 @@ struct Cfg {
   static constexpr int kTmemCols = BN;
 };
 
-template <int BN, int STAGES, bool A_MN, bool B_MN, bool TRANS_OUT, bool MASK>
+template <int BN, int STAGES, bool A_MN, bool B_MN, bool TRANS_OUT, int FIX>
 __global__ void __launch_bounds__(kThreads, 1)
     gemm_tma_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
                     float* __restrict__ C, int64_t ldc, int64_t c_split_stride, int M, int N, int K,
@@ -115,6 +118,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                     double* __restrict__ sq_partial, int c_async, const int* __restrict__ ready, int ready_rows,
                     const int* __restrict__ progress, int* __restrict__ defer, unsigned long long stall_ns) {
   using CF = Cfg<BN, STAGES>;
+  constexpr bool MASK = FIX == 1, ROUND = FIX == 2, FIXUP = FIX != 0;
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte alignment for the swizzled tiles
   // 1024-byte alignment by pointer arithmetic on the shared array (an integer round trip would
@@ -188,7 +192,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kt = 0; kt < ktiles; ++kt) {
         const int s = kt % STAGES;
         const uint32_t ph = (uint32_t)((kt / STAGES) & 1);
-        if (MASK) mbar_wait(&masked[s], ph);
+        if (FIXUP) mbar_wait(&masked[s], ph);
         else mbar_wait(&full[s], ph);
         fence_after();
         const uint32_t a_s = sbase + s * CF::kStage, b_s = a_s + CF::kTileA;
@@ -236,6 +240,28 @@ __global__ void __launch_bounds__(kThreads, 1)
         if (lane == 0) mbar_arrive(&masked[s]);
       }
     }
+    if (ROUND) {
+      for (int kt = 0; kt < ktiles; ++kt) {
+        const int s = kt % STAGES;
+        mbar_wait(&full[s], (uint32_t)((kt / STAGES) & 1));
+        // every 4-byte word of the stage (A tile then B tile) is an operand value: round in place
+        uint4* w = reinterpret_cast<uint4*>(smem + (size_t)s * CF::kStage);
+#pragma unroll 4
+        for (int v = et; v < CF::kStage / 16; v += 128) {
+          // round the magnitude half-up at bit 13 (sign-magnitude: an integer add on the bits;
+          // a carry into the exponent is the correct rounding): two integer ops per value
+          uint4 x = w[v];
+          x.x = (x.x + 0x1000u) & 0xffffe000u;
+          x.y = (x.y + 0x1000u) & 0xffffe000u;
+          x.z = (x.z + 0x1000u) & 0xffffe000u;
+          x.w = (x.w + 0x1000u) & 0xffffe000u;
+          w[v] = x;
+        }
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&masked[s]);
+      }
+    }
     // C tile staged through the (drained) operand ring for a read-modify-write epilogue
     constexpr bool kStageC = !TRANS_OUT && (size_t)STAGES * CF::kStage >= (size_t)BM * BN * 4;
     bool stage_c = kStageC && accumulate && c_async;
@@ -272,6 +298,7 @@ __global__ void __launch_bounds__(kThreads, 1)
           asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
           last = ld_relaxed_gpu(progress);
         }
+        if (defer && stall_ns == 0) stalled = true;  // test mode: defer every tile
         for (int bb = b0; bb <= b1 && !stalled; bb += 32) {
           const int b = bb + lane;
           while (!__all_sync(0xffffffffu, b > b1 || ld_relaxed_gpu(ready + b) != 0)) {
@@ -484,8 +511,8 @@ static int make_map(CUtensorMap* map, const float* base, int64_t rows, int64_t c
   return OK;
 }
 
-// Stall threshold of the bounded ready-flag wait; APX_QW_STALL_NS overrides it (tests set 0 to
-// force the deferral path).
+// Stall threshold of the bounded ready-flag wait; APX_QW_STALL_NS overrides it (0 = test mode:
+// every tile defers, exercising the fixup path end to end).
 static unsigned long long stall_ns() {
   static const unsigned long long v = [] {
     const char* e = getenv("APX_QW_STALL_NS");
@@ -494,7 +521,7 @@ static unsigned long long stall_ns() {
   return v;
 }
 
-template <int BN, int STAGES, bool A_MN, bool B_MN, bool TRANS_OUT, bool MASK>
+template <int BN, int STAGES, bool A_MN, bool B_MN, bool TRANS_OUT, int FIX>
 static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                   int64_t c_split_stride, int M, int N, int K, int splits, int accumulate, const int* mJ, int mk,
                   int mod_n, double* sq_partial, const int* ready, int ready_rows, const int* progress,
@@ -506,7 +533,7 @@ static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, floa
   APX_TRY(make_map(&tb, B, B_MN ? K : N, B_MN ? N : K, ldb, BN, B_MN));
   const int kps = (int)(ceil_div(ceil_div(K, splits), BK) * BK);
   dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)splits);
-  auto fn = gemm_tma_kernel<BN, STAGES, A_MN, B_MN, TRANS_OUT, MASK>;
+  auto fn = gemm_tma_kernel<BN, STAGES, A_MN, B_MN, TRANS_OUT, FIX>;
   APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem));
   const int c_async = ((uintptr_t)C % 16) == 0 && (ldc % 4) == 0 && (N % 4) == 0 && (c_split_stride % 4) == 0;
   fn<<<grid, kThreads, CF::kSmem, st>>>(ta, tb, C, ldc, c_split_stride, M, N, K, kps, accumulate, mJ, mk, mod_n,
@@ -578,21 +605,24 @@ int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* 
   APX_REQUIRE(((uintptr_t)A % 16) == 0 && ((uintptr_t)B % 16) == 0 && (lda % 4) == 0 && (ldb % 4) == 0,
               "umma_tma_gemm: 16-byte aligned operands required");
   const bool mask = mJ != nullptr && mk > 0;
+  const int fix = mask ? 1 : (layout & 8) ? 2 : 0;  // layout bit 8: round operands to TF32 nearest
+  layout &= 7;
   // ring depth: BN 128 with K <= 2 K-tiles needs only 2 stages (and then fits a staged C tile)
   const int stages = bn == 256 ? 2 : (bn == 128 && K <= 2 * tma::BK) ? 2 : 4;
-#define APX_TL(BNV, ST, L, MK)                                                                                \
-  if (bn == BNV && stages == ST && layout == L && mask == MK)                                                 \
-    return tma::launch<BNV, ST, (L & 1) != 0, (L & 2) != 0, (L & 4) != 0, MK>(A, lda, B, ldb, C, ldc,          \
+#define APX_TL(BNV, ST, L, FX)                                                                               \
+  if (bn == BNV && stages == ST && layout == L && fix == FX)                                                 \
+    return tma::launch<BNV, ST, (L & 1) != 0, (L & 2) != 0, (L & 4) != 0, FX>(A, lda, B, ldb, C, ldc,         \
                                                                               c_split_stride, M, N, K, splits, \
                                                                               accumulate, mJ, mk, mod_n,       \
-                                                                              sq_partial, ready, ready_rows, progress, defer, st);
-  APX_TL(64, 4, 0, false) APX_TL(64, 4, 1, false) APX_TL(64, 4, 2, false) APX_TL(64, 4, 3, false)
-  APX_TL(64, 4, 4, false) APX_TL(64, 4, 5, false) APX_TL(64, 4, 6, false) APX_TL(64, 4, 7, false)
-  APX_TL(64, 4, 1, true) APX_TL(64, 4, 5, true)
-  APX_TL(128, 4, 0, false) APX_TL(128, 4, 2, false) APX_TL(256, 2, 0, false) APX_TL(256, 2, 2, false)
-  APX_TL(128, 2, 0, false) APX_TL(128, 2, 2, false)
+                                                                              sq_partial, ready, ready_rows,   \
+                                                                              progress, defer, st);
+  APX_TL(64, 4, 0, 0) APX_TL(64, 4, 1, 0) APX_TL(64, 4, 2, 0) APX_TL(64, 4, 3, 0)
+  APX_TL(64, 4, 4, 0) APX_TL(64, 4, 5, 0) APX_TL(64, 4, 6, 0) APX_TL(64, 4, 7, 0)
+  APX_TL(64, 4, 1, 1) APX_TL(64, 4, 5, 1) APX_TL(64, 4, 7, 2)
+  APX_TL(128, 4, 0, 0) APX_TL(128, 4, 2, 0) APX_TL(256, 2, 0, 0) APX_TL(256, 2, 2, 0)
+  APX_TL(128, 2, 0, 0) APX_TL(128, 2, 2, 0)
 #undef APX_TL
-  set_error("umma_tma_gemm: unsupported layout %d / BN %d / mask %d", layout, bn, (int)mask);
+  set_error("umma_tma_gemm: unsupported layout %d / BN %d / fix-up %d", layout, bn, fix);
   return E_ARG;
 }
 

@@ -20,7 +20,7 @@ import torch
 
 from . import _device as D
 from . import _native as N
-from .errest import ErrorModel, finish_report
+from .errest import ErrorModel, energy_residual, finish_report
 
 
 def cycle_product_device(A, B, k_a: int, k_b: int, order: int, force_sel_a=None, force_sel_b=None,
@@ -44,11 +44,12 @@ def cycle_product_device(A, B, k_a: int, k_b: int, order: int, force_sel_a=None,
     return {"M": M, "sel_a": sa[:k_a], "sel_b": sb[:k_b], "scalars": scal, "ws": ws}
 
 
-def _norms(s):
+def _norms(s, terms: int):
+    """(||A||, ||B||, ||dA||, ||dB||, ||M||) from the device scalars; `terms` = entries per operand."""
     nA = math.sqrt(max(0.0, s[N.S_FRO2_A]))
     nB = math.sqrt(max(0.0, s[N.S_FRO2_B]))
-    ndA = math.sqrt(max(0.0, s[N.S_FRO2_A] - s[N.S_KEPT_A]))
-    ndB = math.sqrt(max(0.0, s[N.S_FRO2_B] - s[N.S_KEPT_B]))
+    ndA = energy_residual(s[N.S_FRO2_A], s[N.S_KEPT_A], terms)
+    ndB = energy_residual(s[N.S_FRO2_B], s[N.S_KEPT_B], terms)
     return nA, nB, ndA, ndB, math.sqrt(max(0.0, s[N.S_FRO2_M]))
 
 
@@ -76,7 +77,7 @@ def cycle_first_order_multiply(A, B, k: int, order: int, model: ErrorModel | Non
     r = cycle_product_device(Ad, Bd, k, k_b, order, force_sel_a, force_sel_b)
     s = r["scalars"].tolist()  # synchronises
     wall = time.perf_counter() - t0
-    nA, nB, ndA, ndB, nM = _norms(s)
+    nA, nB, ndA, ndB, nM = _norms(s, n * n)
     rep = finish_report("cycle", order, k, nA, nB, ndA, ndB, nM, n, wall, model)
     rep.selected_a = r["sel_a"].tolist()
     rep.selected_b = r["sel_b"].tolist()
@@ -133,7 +134,7 @@ def mixed_first_order_multiply(A, B, k_svd: int, k_cyc: int, order: int, seed,
     r = mixed_product_device(Ad, Bd, k_svd, k_cyc, order, omega, power_iterations, force_sel_b, split3)
     s = r["scalars"].tolist()
     wall = time.perf_counter() - t0
-    nA, nB, ndA, ndB, nM = _norms(s)
+    nA, nB, ndA, ndB, nM = _norms(s, n * n)
     rep = finish_report("mixed", order, k_svd, nA, nB, ndA, ndB, nM, n, wall, model)
     rep.selected_b = r["sel_b"].tolist()
     return D.to_user(r["M"], host, out), rep

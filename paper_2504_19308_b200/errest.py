@@ -61,6 +61,20 @@ def posterior_relative_error(norm_dA: float, norm_dB: float, norm_M: float, n: i
     return norm_dA * norm_dB / (math.sqrt(n) * norm_M)
 
 
+def energy_residual(total_sq: float, kept_sq: float, terms: int) -> float:
+    """||dA|| from energies, sqrt(max(0, ||A||^2 - kept)) (svd.py:122-130, circulant.py:130-133).
+
+    ||A||^2 and the kept energy are two fixed-order device sums over the same `terms` squares in
+    different bases, each exact to about eps * log2(terms) * ||A||^2. A difference inside that
+    rounding bound carries no information -- an exactly representable operand (a circulant matrix
+    kept whole, reference test_circulant.py:136-142) lands there -- and is reported as 0, the value
+    the reference's max(0, .) clamp gives when its own rounding happens to fall below zero."""
+    diff = total_sq - kept_sq
+    if diff <= 4.0 * 2.220446049250313e-16 * math.log2(max(2, terms)) * abs(total_sq):
+        return 0.0
+    return math.sqrt(diff)
+
+
 def finish_report(method: str, order: int, k: int, normA: float, normB: float, norm_da: float,
                   norm_db: float, norm_m: float, n: int, wall: float, model: ErrorModel | None):
     """Assemble the ApproxReport exactly like the tail of every reference multiply

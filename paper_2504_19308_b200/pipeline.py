@@ -151,7 +151,7 @@ class MixedPipeline:
         if t.done is None:
             self._collect(self.slots[t.slot])
         s, sel, wall = t.done  # wall: device time of the product
-        nA, nB, ndA, ndB, nM = _norms(s)
+        nA, nB, ndA, ndB, nM = _norms(s, self.n * self.n)
         rep = finish_report("mixed", self.order, self.k_svd, nA, nB, ndA, ndB, nM, self.n, wall, self.model)
         rep.selected_b = sel
         return t.out, rep

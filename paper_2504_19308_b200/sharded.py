@@ -222,10 +222,8 @@ def lockstep(gens):
         pending = nxt
 
 
-def norms_from_scalars(s):
-    """(||A||, ||B||, ||dA||, ||dB||, ||M||) from the scalar vector (cycle._norms)."""
-    nA = math.sqrt(max(0.0, s[N.S_FRO2_A]))
-    nB = math.sqrt(max(0.0, s[N.S_FRO2_B]))
-    ndA = math.sqrt(max(0.0, s[N.S_FRO2_A] - s[N.S_KEPT_A]))
-    ndB = math.sqrt(max(0.0, s[N.S_FRO2_B] - s[N.S_KEPT_B]))
-    return nA, nB, ndA, ndB, math.sqrt(max(0.0, s[N.S_FRO2_M]))
+def norms_from_scalars(s, n: int):
+    """(||A||, ||B||, ||dA||, ||dB||, ||M||) of an n x n product from the scalar vector."""
+    from .cycle import _norms
+
+    return _norms(s, n * n)

@@ -16,7 +16,7 @@ import torch
 
 from . import _device as D
 from . import _native as N
-from .errest import ErrorModel, finish_report
+from .errest import ErrorModel, energy_residual, finish_report
 
 __all__ = [
     "TruncatedSVD",
@@ -196,8 +196,8 @@ def svd_first_order_multiply(A, B, s: int, order: int, seed, power_iterations: i
     sc = r["scalars"].tolist()
     wall = time.perf_counter() - t0
     nA, nB = math.sqrt(max(0.0, sc[N.S_FRO2_A])), math.sqrt(max(0.0, sc[N.S_FRO2_B]))
-    ndA = math.sqrt(max(0.0, sc[N.S_FRO2_A] - sc[N.S_KEPT_A]))
-    ndB = math.sqrt(max(0.0, sc[N.S_FRO2_B] - sc[N.S_KEPT_B]))
+    ndA = energy_residual(sc[N.S_FRO2_A], sc[N.S_KEPT_A], m * n)  # svd.py:122-130
+    ndB = energy_residual(sc[N.S_FRO2_B], sc[N.S_KEPT_B], n * p)
     nM = math.sqrt(max(0.0, sc[N.S_FRO2_M]))
     rep = finish_report("svd", order, ka, nA, nB, ndA, ndB, nM, n, wall, model)
     return D.to_user(r["M"], host), rep

@@ -240,9 +240,21 @@ def errest_cases():
     np.savez_compressed(os.path.join(OUT, "errest.npz"), **d)
 
 
+def genmat_cases():
+    """genmat.py:109-153 outputs for the value-exact kinds (the device generators reproduce them)."""
+    from apxmm import genmat as rg
+
+    d = {}
+    for kind in ("toeplitz", "hankel", "block-toeplitz", "symmetric", "general", "circulant", "kappa"):
+        for n in (1, 2, 5, 12, 36):
+            d[f"{kind}_{n}"] = rg.generate(rg.MatrixSpec(kind, n, seed=3))
+    d["block-toeplitz_12_b3"] = rg.generate(rg.MatrixSpec("block-toeplitz", 12, seed=4, block=3))
+    np.savez_compressed(os.path.join(OUT, "genmat.npz"), **d)
+
+
 if __name__ == "__main__":
     only = sys.argv[1:]
-    for fn in (core_cases, circulant_cases, svd_cases, fsparse_cases, cycle_cases, errest_cases):
+    for fn in (core_cases, circulant_cases, svd_cases, fsparse_cases, cycle_cases, errest_cases, genmat_cases):
         if not only or fn.__name__ in only:
             fn()
     for f in sorted(os.listdir(OUT)):

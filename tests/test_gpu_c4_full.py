@@ -42,11 +42,13 @@ def test_c4_full_matrix_and_selection(c4):
     print(f"C4 n={N}: all {N} rows rel vs oracle {err:.3e}; worst row {row_err.max():.3e} "
           f"(row {int(row_err.argmax())}); rel vs exact AB {rel(Mg, A64 @ B64):.3e}")
     assert err < 1e-4
-    assert row_err.max() < 1e-3
+    assert row_err.max() < 1e-4  # every row within the fp32 tolerance
     assert rep.norm_db == pytest.approx(ro["norm_db"], rel=1e-5)
-    assert rep.norm_da == pytest.approx(ro["norm_da"], rel=1e-3)
-    assert rep.apriori_estimate == pytest.approx(ro["apriori_estimate"], rel=1e-3)
-    assert rep.posterior_estimate == pytest.approx(ro["posterior_estimate"], rel=1e-3)
+    # ||dA||^2 is 3.6e-4 of ||A||^2 here: the TF32 range finder's subspace (the 3e-5 of M above)
+    # moves it by ~10%; the truncation bias of Q^T A (which doubled it) is removed by rounding
+    assert rep.norm_da == pytest.approx(ro["norm_da"], rel=0.15)
+    assert rep.apriori_estimate == pytest.approx(ro["apriori_estimate"], rel=0.15)
+    assert rep.posterior_estimate == pytest.approx(ro["posterior_estimate"], rel=0.15)
 
 
 def test_c4_first_order_identity(c4):

@@ -1,7 +1,7 @@
 """Robustness of the multi-stream C4 plan: the Q.W epilogue's bounded wait on the gather's
-ready flags. With APX_QW_STALL_NS=0 every tile that finds its gather rows unfinished defers
-itself (the path taken when the gather's CTAs are not co-resident, e.g. under MPS SM limits),
-and qw_fixup_sum_kernel completes it after the gather: M must still match the normal plan and
+ready flags. With APX_QW_STALL_NS=0 every tile defers itself (the path a tile takes when the
+gather's CTAs are not co-resident, e.g. under MPS SM limits, and its rows make no progress for
+20 ms), and qw_fixup_sum_kernel completes it after the gather: M must still match the normal plan and
 the oracle. Also: per-device side streams survive a device re-selection."""
 import json
 import os
@@ -20,7 +20,7 @@ import sys, json, numpy as np, torch
 sys.path.insert(0, %r)
 import paper_2504_19308_b200 as P
 from paper_2504_19308_b200 import _native as N
-n, k = 8192, 64
+n, k = 2048, 64
 g = torch.Generator(device="cuda").manual_seed(3)
 A = torch.randn(n, n, device="cuda", generator=g) / n ** 0.5
 B = 1e-3 * torch.randn(n, n, device="cuda", generator=g)

@@ -68,6 +68,31 @@ __global__ void k_tf32(float* out) {
   if (r == 1234.5f) out[0] = r;
 }
 
+// Shared-memory load bandwidth: every thread reads conflict-free V-wide words (LDS.32 / .64 /
+// .128) from a 32 KB buffer, 16 independent loads per iteration, XOR-folded so nothing is dead.
+template <typename V>
+__device__ __forceinline__ unsigned fold(const V& v);
+template <> __device__ __forceinline__ unsigned fold<unsigned>(const unsigned& v) { return v; }
+template <> __device__ __forceinline__ unsigned fold<uint2>(const uint2& v) { return v.x ^ v.y; }
+template <> __device__ __forceinline__ unsigned fold<uint4>(const uint4& v) { return v.x ^ v.y ^ v.z ^ v.w; }
+template <typename V>
+__global__ void k_lds(unsigned* out, int iters) {
+  constexpr int W = sizeof(V) / 4;
+  __shared__ __align__(16) unsigned buf[8192];
+  for (int i = threadIdx.x; i < 8192; i += blockDim.x) buf[i] = i * 2654435761u;
+  __syncthreads();
+  const V* b = reinterpret_cast<const V*>(buf);
+  const int nv = 8192 / W;
+  unsigned acc = 0;
+  int base = threadIdx.x;
+  for (int it = 0; it < iters; ++it) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) acc += fold<V>(b[(base + u * (nv / 16)) & (nv - 1)]);
+    base += 7 * 32;  // warp-uniform stride keeps the 32 lanes on consecutive words
+  }
+  if (acc == 0x12345678u) out[0] = acc;
+}
+
 template <typename F>
 float time_it(F f) {
   cudaEvent_t a, b; cudaEventCreate(&a); cudaEventCreate(&b);
@@ -95,8 +120,21 @@ int main() {
   double dmma = (nthr / 32) * (ITERS / 8) * 8 * (8.0 * 8 * 4 * 2) / (t4 * 1e-3) / 1e12;
   float t5 = time_it([&] { k_tf32<<<blocks, threads>>>(f); });
   double tf32 = (nthr / 32) * (ITERS / 4) * 8 * (16.0 * 8 * 8 * 2) / (t5 * 1e-3) / 1e12;
+  unsigned* u; cudaMalloc(&u, 64);
+  const int li = 2048;
+  int clk_khz = 0;
+  cudaDeviceGetAttribute(&clk_khz, cudaDevAttrClockRate, 0);
+  float t6 = time_it([&] { k_lds<unsigned><<<blocks, threads>>>(u, li); });
+  float t7 = time_it([&] { k_lds<uint2><<<blocks, threads>>>(u, li); });
+  float t8 = time_it([&] { k_lds<uint4><<<blocks, threads>>>(u, li); });
+  auto lds_tbs = [&](float t, int bytes) { return nthr * li * 16.0 * bytes / (t * 1e-3) / 1e12; };
+  const double l32 = lds_tbs(t6, 4), l64 = lds_tbs(t7, 8), l128 = lds_tbs(t8, 16);
+  const double hz = clk_khz * 1e3;
   printf("{\"sms\": %d, \"fp32_ffma_tflops\": %.2f, \"fp32_ffma2_tflops\": %.2f, \"fp64_dfma_tflops\": %.2f, "
-         "\"fp64_dmma_mma_sync_tflops\": %.2f, \"tf32_mma_sync_tflops\": %.2f, \"err\": \"%s\"}\n",
-         sms, ffma, ffma2, dfma, dmma, tf32, cudaGetErrorString(cudaGetLastError()));
+         "\"fp64_dmma_mma_sync_tflops\": %.2f, \"tf32_mma_sync_tflops\": %.2f, "
+         "\"lds32_tbs\": %.2f, \"lds64_tbs\": %.2f, \"lds128_tbs\": %.2f, "
+         "\"lds128_bytes_per_clk_per_sm_at_attr_clock\": %.1f, \"attr_clock_mhz\": %.0f, \"err\": \"%s\"}\n",
+         sms, ffma, ffma2, dfma, dmma, tf32, l32, l64, l128, l128 * 1e12 / hz / sms, hz / 1e6,
+         cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
