@@ -247,6 +247,32 @@ int apx_cycle_rows_phase(int phase, int dtype, const void* A_rows, int64_t m_row
                          const double* red_in, double* red_out, double* scalars, void* ws, size_t ws_bytes,
                          void* stream);
 
+/* The circulant product (circulant_first_order_multiply, circulant.py:164-218) sharded by rows of M
+ * over ranks. A and B are replicated; rank g produces M[row0 : row0 + m_rows]
+ * (complex128, m_rows x n) and computes term1 (circulant.py:136-147, column-local) for the columns
+ * [col0, col0 + w_cols) and its decomposition share on the cycle blocks [blk0, blk1) of the grid
+ * apx_circulant_rows_grid reports. Four calls on the same workspace and stream:
+ *   phase 1: red_out = magnitude partials of A then B, 2 x parts x n fp64, zero outside this
+ *            rank's blocks; the caller sums red_out over the ranks (an all-gather + rank-order sum);
+ *   phase 2: red_in = the summed partials: magnitudes and selections (identical on every rank, and
+ *            bitwise the single-device ones), kept energies; red_out = the selected spectrum rows
+ *            of A then B from this rank's cycles, 2 x k x n complex128, zero elsewhere (summed by
+ *            the caller = gathered);
+ *   phase 3: red_in = the full selected spectra; T1 (n x w_cols complex128) = term1's columns; the
+ *            caller moves T1[rows of rank h] to rank h (all-to-all) and assembles them into M_rows;
+ *   phase 4: term2 (circulant.py:150-161) for the rank's rows added onto M_rows (order 1);
+ *            red_out[0] = ||M_g||_F^2 (the caller sums it into scalars[APX_S_FRO2_M]).
+ * row0 and col0 must be even; n within the fused shared-memory range (16 <= n <= 4096). Every
+ * per-column and per-row computation is the single-device kernel, so the rows are bitwise the
+ * single-device product's. Replaces nothing in the reference (which has no multi-device path). */
+int apx_circulant_rows_grid(int64_t n, int64_t* parts, int64_t* cpc);
+size_t apx_circulant_rows_workspace(int dtype, int64_t n, int k, int64_t m_rows, int64_t blk0, int64_t blk1);
+int apx_circulant_rows_phase(int phase, int dtype, const void* A, const void* B, int64_t n, int k, int order,
+                             int64_t row0, int64_t m_rows, int64_t col0, int64_t w_cols, int64_t blk0,
+                             int64_t blk1, void* M_rows, void* T1, int32_t* sel_a, int32_t* sel_b,
+                             const double* red_in, double* red_out, double* scalars, void* ws, size_t ws_bytes,
+                             void* stream);
+
 /* sketch_norm_estimate (errest.py:139-154): out[0] = ||A (B G)||_F^2 with A m x n, B n x p, G p x k
  * (all fp64 row-major; G drawn on the host with numpy exactly as the reference draws it). The
  * caller divides by k. Complex operands are passed as their real embeddings (see errest.py). */

@@ -70,6 +70,10 @@ SIGNATURES = {
     "apx_cycle_rows_workspace": (_sz, [_i32, _i64, _i64, _i32, _i32, _i32]),
     "apx_cycle_rows_phase": (C.c_int, [_i32, _i32, _vp, _i64, _i64, _vp, _i64, _i32, _i32, _i32, _vp, _vp, _vp,
                                        _vp, _vp, _vp, _vp, _sz, _vp]),
+    "apx_circulant_rows_grid": (C.c_int, [_i64, _vp, _vp]),
+    "apx_circulant_rows_workspace": (_sz, [_i32, _i64, _i32, _i64, _i64, _i64]),
+    "apx_circulant_rows_phase": (C.c_int, [_i32, _i32, _vp, _vp, _i64, _i32, _i32, _i64, _i64, _i64, _i64, _i64,
+                                           _i64, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _vp, _sz, _vp]),
     "apx_sketch_norm_workspace": (_sz, [_i64, _i64, _i64, _i32]),
     "apx_sketch_norm": (C.c_int, [_vp, _vp, _i64, _i64, _i64, _vp, _i32, _vp, _vp, _sz, _vp]),
     "apx_gemm_workspace": (_sz, [_i32, _i64, _i64, _i64, _i32, _i32]),

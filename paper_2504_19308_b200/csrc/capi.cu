@@ -431,12 +431,12 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   APX_CUDA(cudaStreamWaitEvent(lo, ss->b_read, 0));
   APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, lo, 32));  // 64 CTAs
   stage_mark(3, lo);
-  APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, lo)));
+  APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, lo, /*tf32=*/1)));
   for (int it = 0; it < q; ++it) {
     APX_TRY(UmmaStages::at_times_x(A, Q, Z, part, n, l, lo, free_sms));
-    APX_TRY((qr_orthonormalize<float, float>(Z, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, lo)));
+    APX_TRY((qr_orthonormalize<float, float>(Z, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, lo, /*tf32=*/1)));
     APX_TRY(UmmaStages::a_times_x(A, Q, Y, part, n, l, lo, free_sms));
-    APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, lo)));
+    APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, lo, /*tf32=*/1)));
   }
   stage_mark(4, lo);
   APX_TRY(UmmaStages::qt_times_a(A, Q, Bm, part, n, l, lo, free_sms));

@@ -57,21 +57,25 @@ static size_t fft_smem_bytes(int n, int buffers) {
 // rows are contiguous column segments (coalesced reads), staged in shared memory and written
 // back as contiguous rows of X.
 // ---------------------------------------------------------------------------------------------
+// [j_lo, j_hi): the cycle rows to produce (a rank's share in the sharded product); X holds them
+// from row j_lo on.
 template <typename T>
-__global__ void __launch_bounds__(256) circ_skew_kernel(const T* __restrict__ A, int n, T* __restrict__ X) {
+__global__ void __launch_bounds__(256) circ_skew_kernel(const T* __restrict__ A, int n, T* __restrict__ X,
+                                                        int j_lo = 0, int j_hi = -1) {
   __shared__ T tile[32][33];
-  const int i0 = blockIdx.x * 32, j0 = blockIdx.y * 32;
+  if (j_hi < 0) j_hi = n;
+  const int i0 = blockIdx.x * 32, j0 = j_lo + blockIdx.y * 32;
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   for (int d = warp; d < 63; d += 8) {  // source row r = i0 + j0 + d, column i0 + lane, j = d - lane
     const int jj = d - lane;
-    if (jj < 0 || jj >= 32 || i0 + lane >= n || j0 + jj >= n) continue;
+    if (jj < 0 || jj >= 32 || i0 + lane >= n || j0 + jj >= j_hi) continue;
     int r = i0 + j0 + d;
     r %= n;
     tile[jj][lane] = A[(size_t)r * n + i0 + lane];
   }
   __syncthreads();
   for (int jj = warp; jj < 32; jj += 8)
-    if (j0 + jj < n && i0 + lane < n) X[(size_t)(j0 + jj) * n + i0 + lane] = tile[jj][lane];
+    if (j0 + jj < j_hi && i0 + lane < n) X[(size_t)(j0 + jj - j_lo) * n + i0 + lane] = tile[jj][lane];
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -83,14 +87,21 @@ template <typename T>
 __global__ void __launch_bounds__(512) circ_decompose_rows_kernel(const T* __restrict__ X, int n, int cpc,
                                                                   const double2* __restrict__ roots,
                                                                   double2* __restrict__ St,
-                                                                  double* __restrict__ mag2_part) {
+                                                                  double* __restrict__ mag2_part, int b_off = 0,
+                                                                  int j_base = 0) {
+  // b_off / j_base (sharded product): this launch is CTA-blocks [b_off, ...) of the full grid, and
+  // X, St hold rows from cycle j_base on; the partials land in the full-grid slots (the caller
+  // sums the zero-padded slot arrays over ranks, so mag_finalize sees the single-device layout)
+  X -= (size_t)j_base * n;
+  St -= (size_t)j_base * n;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* x = reinterpret_cast<double2*>(smem_raw);
   double2* scratch = x + n;
   double* m2 = reinterpret_cast<double*>(scratch + (is_pow2(n) ? 0 : n));
   for (int t = threadIdx.x; t < n; t += blockDim.x) m2[t] = 0.0;
   const double inv_n = 1.0 / n;
-  const int j0 = blockIdx.x * cpc, j1 = min(n, j0 + cpc);
+  const int blk = blockIdx.x + b_off;
+  const int j0 = blk * cpc, j1 = min(n, j0 + cpc);
   if constexpr (std::is_same<T, double>::value) {
     // real rows in pairs: x_j + i x_{j+1} through ONE transform Z, split as
     // F_j[t] = (Z[t] + conj Z[-t]) / 2, F_{j+1}[t] = (Z[t] - conj Z[-t]) / 2i; the next pair's
@@ -131,7 +142,7 @@ __global__ void __launch_bounds__(512) circ_decompose_rows_kernel(const T* __res
         }
         __syncthreads();
       }
-      for (int t = threadIdx.x; t < n; t += blockDim.x) mag2_part[(size_t)blockIdx.x * n + t] = m2[t];
+      for (int t = threadIdx.x; t < n; t += blockDim.x) mag2_part[(size_t)blk * n + t] = m2[t];
       return;
     }
   }
@@ -146,7 +157,7 @@ __global__ void __launch_bounds__(512) circ_decompose_rows_kernel(const T* __res
     }
     __syncthreads();
   }
-  for (int t = threadIdx.x; t < n; t += blockDim.x) mag2_part[(size_t)blockIdx.x * n + t] = m2[t];
+  for (int t = threadIdx.x; t < n; t += blockDim.x) mag2_part[(size_t)blk * n + t] = m2[t];
 }
 
 // mag[t] = sqrt(sum_p part[p][t]): a CTA covers 32 columns with 8 slices of the parts (slice s:
@@ -171,10 +182,12 @@ __global__ void __launch_bounds__(256) mag_finalize_kernel(const double* __restr
 }
 
 // Selected spectrum rows from S^T: Ssel[q] = S[sel[q]], L[q] = fft(S[sel[q]]) (unnormalised, :145)
+// rows_in (sharded product): S is already the k x n table of selected rows (row q contiguous).
 __global__ void __launch_bounds__(512) circ_spectra_kernel(const double2* __restrict__ S, int n,
                                                            const int* __restrict__ sel,
                                                            const double2* __restrict__ roots,
-                                                           double2* __restrict__ Ssel, double2* __restrict__ L) {
+                                                           double2* __restrict__ Ssel, double2* __restrict__ L,
+                                                           int rows_in = 0) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* x = reinterpret_cast<double2*>(smem_raw);
   double2* scratch = x + n;
@@ -186,7 +199,7 @@ __global__ void __launch_bounds__(512) circ_spectra_kernel(const double2* __rest
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
       const int i = i0 + u * blockDim.x;
-      v[u] = i < n ? __ldg(S + (size_t)i * n + t) : make_double2(0.0, 0.0);
+      v[u] = i < n ? __ldg(rows_in ? S + (size_t)q * n + i : S + (size_t)i * n + t) : make_double2(0.0, 0.0);
     }
 #pragma unroll
     for (int u = 0; u < 8; ++u) {
@@ -272,17 +285,23 @@ __global__ void __launch_bounds__(512) circ_left_kernel(const T* __restrict__ B,
 constexpr int kPP = 8;
 
 template <typename T>
+// col_base / col_end / ldm (sharded product): the CTA pairs cover columns [col_base, col_end) of
+// term1 (col_base even: the same pairs as the full grid), written to an n x (col_end - col_base)
+// block with leading dimension ldm.
 __global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B, int n, const double2* __restrict__ L,
                                                          const int* __restrict__ sel, int k,
-                                                         const double2* __restrict__ roots, double2* __restrict__ M) {
+                                                         const double2* __restrict__ roots, double2* __restrict__ M,
+                                                         int col_base = 0, int col_end = -1, int64_t ldm = -1) {
+  if (col_end < 0) col_end = n;
+  if (ldm < 0) ldm = n;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* x0 = reinterpret_cast<double2*>(smem_raw);
   double2* x1 = x0 + n;
   double2* scratch = x1 + n;
   int* s_sel = reinterpret_cast<int*>(scratch + (is_pow2(n) ? 0 : n));
   for (int q = threadIdx.x; q < k; q += blockDim.x) s_sel[q] = sel[q];
-  const int c0 = 2 * blockIdx.x;
-  const bool two = c0 + 1 < n;
+  const int c0 = col_base + 2 * blockIdx.x;
+  const bool two = c0 + 1 < col_end;
   const double rs = rsqrt((double)n);
   // real B: the two columns travel as one complex sequence b0 + i b1 through ONE forward
   // transform Z, split afterwards as FB0[p] = (Z[p] + conj Z[-p]) / 2, FB1[p] = (Z[p] - conj Z[-p]) / 2i
@@ -374,8 +393,8 @@ __global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B
   fft_block(x0, scratch, n, roots, true);
   fft_block(x1, scratch, n, roots, true);
   for (int p = threadIdx.x; p < n; p += blockDim.x) {
-    M[(size_t)p * n + c0] = cscale(x0[fsw(p, n)], rs);
-    if (two) M[(size_t)p * n + c0 + 1] = cscale(x1[fsw(p, n)], rs);
+    M[(size_t)p * ldm + (c0 - col_base)] = cscale(x0[fsw(p, n)], rs);
+    if (two) M[(size_t)p * ldm + (c0 - col_base) + 1] = cscale(x1[fsw(p, n)], rs);
   }
 }
 
@@ -386,7 +405,13 @@ __global__ void __launch_bounds__(512) circ_right2_kernel(const T* __restrict__ 
                                                           const double2* __restrict__ LB, const int* __restrict__ selB,
                                                           int kb, const double2* __restrict__ roots,
                                                           double2* __restrict__ M,
-                                                          const double2* __restrict__ Xpre) {
+                                                          const double2* __restrict__ Xpre, int row_base = 0,
+                                                          int row_end = -1) {
+  // [row_base, row_end) (sharded product): the CTA pairs cover these rows of term2; M and Xpre
+  // hold them from row row_base on (A is the full operand)
+  if (row_end < 0) row_end = n;
+  M -= (size_t)row_base * n;
+  if (Xpre) Xpre -= (size_t)row_base * n;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* x0 = reinterpret_cast<double2*>(smem_raw);
   double2* x1 = x0 + n;
@@ -396,12 +421,12 @@ __global__ void __launch_bounds__(512) circ_right2_kernel(const T* __restrict__ 
   for (int q = threadIdx.x; q < ka; q += blockDim.x) sA[q] = selA[q];
   for (int q = threadIdx.x; q < kb; q += blockDim.x) sB[q] = selB[q];
   __syncthreads();
-  const int r0 = 2 * blockIdx.x;
-  const bool two = r0 + 1 < n;
+  const int r0 = row_base + 2 * blockIdx.x;
+  const bool two = r0 + 1 < row_end;
   const double rs = rsqrt((double)n);
   // the epilogue's read-modify-write of M (term1, DRAM-resident by now): pull both rows toward
   // L2 while the transforms run
-  if (threadIdx.x < 2 && r0 + threadIdx.x < n && ((uintptr_t)M & 15) == 0)
+  if (threadIdx.x < 2 && r0 + (int)threadIdx.x < row_end && ((uintptr_t)M & 15) == 0)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(M + (size_t)(r0 + threadIdx.x) * n),
                  "r"((unsigned)(n * sizeof(double2)))
                  : "memory");
@@ -922,15 +947,18 @@ __global__ void __launch_bounds__(256) big_left_gather_kernel(const double2* __r
 // is shared by the block's rows, and for a fixed row the lanes read consecutive S_q entries.
 constexpr int kDaRows = 16;
 template <typename T>
+// [row_base, row_end): the rows to form (sharded product); X holds them from row row_base on.
 __global__ void __launch_bounds__(256, 2) big_dA_kernel(const T* __restrict__ A, int n, const double2* __restrict__ Ssel,
                                                      const int* __restrict__ sel, int k,
-                                                     const double2* __restrict__ roots, double2* __restrict__ X) {
+                                                     const double2* __restrict__ roots, double2* __restrict__ X,
+                                                     int row_base = 0, int row_end = -1) {
+  if (row_end < 0) row_end = n;
   __shared__ int s_buf[512];
   for (int q = threadIdx.x; q < k && q < 512; q += blockDim.x) s_buf[q] = sel[q];
   __syncthreads();
   const int* s_sel = k <= 512 ? s_buf : sel;
   const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  const int r0 = blockIdx.y * kDaRows;
+  const int r0 = row_base + blockIdx.y * kDaRows;
   if (c >= n) return;
   double2 ah[kDaRows];
 #pragma unroll
@@ -950,7 +978,7 @@ __global__ void __launch_bounds__(256, 2) big_dA_kernel(const T* __restrict__ A,
 #pragma unroll
   for (int rr = 0; rr < kDaRows; ++rr) {
     const size_t r = (size_t)r0 + rr;
-    if (r < (size_t)n) X[r * n + c] = cconj(csub(ld_c<T>(A, r * n + c), ah[rr]));
+    if (r < (size_t)row_end) X[(r - row_base) * n + c] = cconj(csub(ld_c<T>(A, r * n + c), ah[rr]));
   }
 }
 
@@ -1025,7 +1053,7 @@ static int circ_decompose_run(const T* A, int n, const CircPlan& p, double2* St,
   APX_LAUNCH_CHECK();
   auto fn = circ_decompose_rows_kernel<T>;
   APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  fn<<<p.parts, 512, smem, st>>>(skew, n, p.cpc, p.roots, St, p.part);
+  fn<<<p.parts, 512, smem, st>>>(skew, n, p.cpc, p.roots, St, p.part, 0, 0);
   APX_LAUNCH_CHECK();
   mag_finalize_kernel<<<(unsigned)ceil_div(n, 32), 256, 0, st>>>(p.part, p.parts, n, mag);
   APX_LAUNCH_CHECK();
@@ -1067,7 +1095,7 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
   if (pairs) {
     auto fn = circ_left2_kernel<T>;
     APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<(unsigned)ceil_div(n, 2), 512, smem, st>>>(B, n, p.L_a, sa, k, p.roots, M);
+    fn<<<(unsigned)ceil_div(n, 2), 512, smem, st>>>(B, n, p.L_a, sa, k, p.roots, M, 0, (int)n, (int64_t)n);
     APX_LAUNCH_CHECK();
   } else {
     auto fn = circ_left_kernel<T>;
@@ -1092,7 +1120,7 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
         APX_LAUNCH_CHECK();
         Xpre = p.S_a;
       }
-      fn<<<(unsigned)ceil_div(n, 2), 512, smem, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M, Xpre);
+      fn<<<(unsigned)ceil_div(n, 2), 512, smem, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M, Xpre, 0, (int)n);
     } else {
       auto fn = circ_right_kernel<T>;
       APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1395,7 +1423,203 @@ static int run_circulant_big(const T* A, const T* B, int n, int k, int order, co
 
 using namespace apx;
 
+// ---- the circulant product sharded by rows of M ------------------------------
+// Rank g holds both operands (replicated) and produces the rows R_g = [row0, row0 + m) of M.
+// term1 (circulant.py:136-147) is column-local and term2 (:150-161) row-local, so:
+//   1  decompose only the cycle blocks [blk0, blk1) of the full decomposition grid (cycle rows of
+//      the skewed operand): per-CTA magnitude partials into their full-grid slots (zero-padded),
+//      for A and B                                                  out: 2 x parts x n fp64
+//   2  (partials summed over ranks) magnitudes exactly as on one device -> identical selections;
+//      the selected spectrum rows from this rank's cycles (zero-padded)  out: 2 x k x n complex
+//   3  (spectra summed = gathered) L = fft(S_t); term1 for the columns [col0, col0 + w) into the
+//      n x w block T1, which the caller redistributes by rows (all-to-all) into M's rows
+//   4  term2 for the rows R_g (dA rows from A's spectra), accumulated onto M's rows;
+//                                                                   out: [||M_g||^2]
+// Every per-column / per-row computation is the single-device kernel on the same inputs, so the
+// rows of M are bitwise the single-device product's.
+__global__ void circ_sel_extract_kernel(const double2* __restrict__ St, int n, int j_lo, int j_hi,
+                                        const int* __restrict__ sel, int k, double2* __restrict__ out) {
+  const size_t total = (size_t)k * n;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
+    const int q = (int)(e / n), j = (int)(e % n);
+    out[e] = (j >= j_lo && j < j_hi) ? St[(size_t)(j - j_lo) * n + sel[q]] : make_double2(0.0, 0.0);
+  }
+}
+
+struct CircRowsPlan {
+  double2 *roots, *St_a, *St_b, *Ssel_a, *L_a, *Ssel_b, *L_b, *Xpre;
+  double *mag_a, *mag_b, *red;
+  void* skew;
+  int cpc, parts, j_lo, j_hi;
+};
+
+static void circ_grid(int n, int* cpc, int* parts) {
+  *cpc = std::max(1, (int)ceil_div(n, 2 * kNumSMs));
+  *parts = (int)ceil_div(n, *cpc);
+}
+
+static void plan_circ_rows(Workspace& ws, CircRowsPlan& p, int elem, int n, int k, int m, int blk0, int blk1) {
+  circ_grid(n, &p.cpc, &p.parts);
+  p.j_lo = std::min(n, blk0 * p.cpc);
+  p.j_hi = std::min(n, blk1 * p.cpc);
+  const size_t jr = (size_t)std::max(1, p.j_hi - p.j_lo);
+  p.roots = ws.take<double2>(n);
+  p.St_a = ws.take<double2>(jr * n);
+  p.St_b = ws.take<double2>(jr * n);
+  p.skew = ws.take<char>(jr * n * elem);
+  p.Ssel_a = ws.take<double2>((size_t)std::max(k, 1) * n);
+  p.L_a = ws.take<double2>((size_t)std::max(k, 1) * n);
+  p.Ssel_b = ws.take<double2>((size_t)std::max(k, 1) * n);
+  p.L_b = ws.take<double2>((size_t)std::max(k, 1) * n);
+  p.Xpre = ws.take<double2>((size_t)std::max(m, 1) * n);
+  p.mag_a = ws.take<double>(n);
+  p.mag_b = ws.take<double>(n);
+  p.red = ws.take<double>(4 * kNumSMs + 64);
+}
+
+template <typename T>
+static int run_circ_rows_phase(int phase, const T* A, const T* B, int n, int k, int order, int row0, int m, int col0,
+                               int w, int blk0, int blk1, double2* M_rows, double2* T1, int* sa, int* sb,
+                               const double* red_in, double* red_out, double* scal, const CircRowsPlan& p,
+                               cudaStream_t st) {
+  const size_t smem2 = fft_smem_bytes(n, 2) + (size_t)2 * k * sizeof(int);
+  if (phase == 1) {
+    APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
+    launch_roots(p.roots, n, st);
+    APX_LAUNCH_CHECK();
+    APX_CUDA(cudaMemsetAsync(red_out, 0, (size_t)2 * p.parts * n * sizeof(double), st));
+    const T* ops[2] = {A, B};
+    double2* Sts[2] = {p.St_a, p.St_b};
+    const size_t smem = fft_smem_bytes(n, 1) + (size_t)n * sizeof(double);
+    auto fn = circ_decompose_rows_kernel<T>;
+    APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    for (int o = 0; o < 2; ++o) {
+      if (p.j_hi > p.j_lo) {
+        circ_skew_kernel<T><<<dim3((unsigned)ceil_div(n, 32), (unsigned)ceil_div(p.j_hi - p.j_lo, 32)), 256, 0, st>>>(
+            ops[o], n, (T*)p.skew, p.j_lo, p.j_hi);
+        APX_LAUNCH_CHECK();
+        fn<<<blk1 - blk0, 512, smem, st>>>((const T*)p.skew, n, p.cpc, p.roots, Sts[o],
+                                           red_out + (size_t)o * p.parts * n, blk0, p.j_lo);
+        APX_LAUNCH_CHECK();
+      }
+    }
+    int parts = 0;
+    const size_t nel = (size_t)n * n * (sizeof(T) / sizeof(double));
+    APX_TRY(launch_sumsq<double>(reinterpret_cast<const double*>(A), nel, p.red, &parts, st));
+    APX_TRY(launch_sum_vector(p.red, parts, scal + APX_S_FRO2_A, st));
+    APX_TRY(launch_sumsq<double>(reinterpret_cast<const double*>(B), nel, p.red, &parts, st));
+    APX_TRY(launch_sum_vector(p.red, parts, scal + APX_S_FRO2_B, st));
+    return OK;
+  }
+  if (phase == 2) {
+    double* mags[2] = {p.mag_a, p.mag_b};
+    int* sels[2] = {sa, sb};
+    double2* Sts[2] = {p.St_a, p.St_b};
+    double2* out = reinterpret_cast<double2*>(red_out);
+    for (int o = 0; o < 2; ++o) {
+      mag_finalize_kernel<<<(unsigned)ceil_div(n, 32), 256, 0, st>>>(red_in + (size_t)o * p.parts * n, p.parts, n,
+                                                                      mags[o]);
+      APX_LAUNCH_CHECK();
+      APX_TRY(launch_topk(mags[o], n, k, sels[o], st));
+      APX_TRY(launch_kept_energy(mags[o], sels[o], k, (double)n, scal + (o ? APX_S_KEPT_B : APX_S_KEPT_A), st));
+      if (k > 0) {
+        circ_sel_extract_kernel<<<(unsigned)std::min<int64_t>(ceil_div((int64_t)k * n, 256), kNumSMs * 8), 256, 0,
+                                  st>>>(Sts[o], n, p.j_lo, p.j_hi, sels[o], k, out + (size_t)o * k * n);
+        APX_LAUNCH_CHECK();
+      }
+    }
+    return OK;
+  }
+  if (phase == 3) {
+    const double2* in = reinterpret_cast<const double2*>(red_in);
+    if (k > 0) {
+      APX_CUDA(cudaMemcpyAsync(p.Ssel_a, in, (size_t)k * n * sizeof(double2), cudaMemcpyDeviceToDevice, st));
+      APX_CUDA(cudaMemcpyAsync(p.Ssel_b, in + (size_t)k * n, (size_t)k * n * sizeof(double2), cudaMemcpyDeviceToDevice,
+                               st));
+      const size_t smem = fft_smem_bytes(n, 1);
+      APX_CUDA(cudaFuncSetAttribute(circ_spectra_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      circ_spectra_kernel<<<k, 512, smem, st>>>(p.Ssel_a, n, sa, p.roots, nullptr, p.L_a, 1);
+      APX_LAUNCH_CHECK();
+      circ_spectra_kernel<<<k, 512, smem, st>>>(p.Ssel_b, n, sb, p.roots, nullptr, p.L_b, 1);
+      APX_LAUNCH_CHECK();
+    }
+    if (w > 0) {
+      auto fn = circ_left2_kernel<T>;
+      APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      fn<<<(unsigned)ceil_div(w, 2), 512, smem2, st>>>(B, n, p.L_a, sa, k, p.roots, T1, col0, col0 + w, (int64_t)w);
+      APX_LAUNCH_CHECK();
+    }
+    return OK;
+  }
+  // phase 4: term2 on this rank's rows (M_rows holds term1's rows, assembled by the caller)
+  if (order == 1 && m > 0) {
+    big_dA_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)ceil_div(m, kDaRows)), 256, 0, st>>>(
+        A, n, p.Ssel_a, sa, k, p.roots, p.Xpre, row0, row0 + m);
+    APX_LAUNCH_CHECK();
+    auto fn = circ_right2_kernel<T>;
+    APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+    fn<<<(unsigned)ceil_div(m, 2), 512, smem2, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M_rows, p.Xpre,
+                                                     row0, row0 + m);
+    APX_LAUNCH_CHECK();
+  }
+  int parts = 0;
+  APX_TRY(launch_sumsq<double>(reinterpret_cast<const double*>(M_rows), (size_t)2 * m * n, p.red, &parts, st));
+  APX_TRY(launch_sum_vector(p.red, parts, red_out, st));
+  return OK;
+}
+
 extern "C" {
+
+// The decomposition grid the sharded product partitions ([blk0, blk1) per rank): parts CTA blocks
+// of cpc cycles each (the single-device grid).
+int apx_circulant_rows_grid(int64_t n, int64_t* parts, int64_t* cpc) {
+  APX_REQUIRE(n >= 1, "n must be >= 1");
+  int c = 0, q = 0;
+  circ_grid((int)n, &c, &q);
+  *parts = q;
+  *cpc = c;
+  return OK;
+}
+
+size_t apx_circulant_rows_workspace(int dtype, int64_t n, int k, int64_t m_rows, int64_t blk0, int64_t blk1) {
+  Workspace ws(nullptr, 0, true);
+  CircRowsPlan p;
+  plan_circ_rows(ws, p, dtype == C128 ? 16 : 8, (int)n, k, (int)m_rows, (int)blk0, (int)blk1);
+  return ws.off;
+}
+
+int apx_circulant_rows_phase(int phase, int dtype, const void* A, const void* B, int64_t n, int k, int order,
+                             int64_t row0, int64_t m_rows, int64_t col0, int64_t w_cols, int64_t blk0, int64_t blk1,
+                             void* M_rows, void* T1, int32_t* sel_a, int32_t* sel_b, const double* red_in,
+                             double* red_out, double* scalars, void* wsp, size_t ws_bytes, void* stream) {
+  APX_REQUIRE(phase >= 1 && phase <= 4, "phase must be 1..4");
+  APX_REQUIRE(dtype == F64 || dtype == C128, "circulant product: fp64 or complex128 inputs");
+  APX_REQUIRE(k >= 0 && k <= n, "k=%d out of range [0, %lld]", k, (long long)n);
+  APX_REQUIRE(order == 0 || order == 1, "order must be 0 or 1");
+  APX_REQUIRE(n >= kDaRows && n <= kPP * 512 && circ_fused_fits((int)n, k),
+              "sharded circulant product: n=%lld outside the fused shared-memory range [%d, %d]", (long long)n,
+              kDaRows, kPP * 512);
+  APX_REQUIRE(row0 >= 0 && m_rows >= 0 && row0 + m_rows <= n && (row0 % 2) == 0, "row block [%lld, %lld) invalid",
+              (long long)row0, (long long)(row0 + m_rows));
+  APX_REQUIRE(col0 >= 0 && w_cols >= 0 && col0 + w_cols <= n && (col0 % 2) == 0, "column block invalid");
+  int cpc = 0, parts = 0;
+  circ_grid((int)n, &cpc, &parts);
+  APX_REQUIRE(blk0 >= 0 && blk0 <= blk1 && blk1 <= parts, "cycle blocks [%lld, %lld) outside [0, %d)",
+              (long long)blk0, (long long)blk1, parts);
+  APX_REQUIRE(phase == 1 || red_in != nullptr || phase == 4, "phase %d needs the summed exchange", phase);
+  Workspace ws(wsp, ws_bytes);
+  CircRowsPlan p;
+  plan_circ_rows(ws, p, dtype == C128 ? 16 : 8, (int)n, k, (int)m_rows, (int)blk0, (int)blk1);
+  APX_WS_CHECK(ws);
+  cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
+  if (dtype == F64)
+    return run_circ_rows_phase<double>(phase, (const double*)A, (const double*)B, (int)n, k, order, (int)row0,
+                                       (int)m_rows, (int)col0, (int)w_cols, (int)blk0, (int)blk1, (double2*)M_rows,
+                                       (double2*)T1, sel_a, sel_b, red_in, red_out, scalars, p, st);
+  return run_circ_rows_phase<double2>(phase, (const double2*)A, (const double2*)B, (int)n, k, order, (int)row0,
+                                      (int)m_rows, (int)col0, (int)w_cols, (int)blk0, (int)blk1, (double2*)M_rows,
+                                      (double2*)T1, sel_a, sel_b, red_in, red_out, scalars, p, st);
+}
 
 size_t apx_circulant_first_order_workspace(int dtype, int64_t n, int k, int order) {
   (void)dtype;

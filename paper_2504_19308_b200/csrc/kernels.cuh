@@ -69,7 +69,8 @@ const int* cholqr_rows_flags(void* ws, size_t bytes, int m, int l);
 int launch_flag_to_double(const int* flag, double* out, cudaStream_t st);
 template <typename TI, typename TO>
 int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, int64_t qrs, int64_t qcs, TO* Q2,
-                      int64_t q2rs, int64_t q2cs, void* wsp, size_t ws_bytes, int method, cudaStream_t st);
+                      int64_t q2rs, int64_t q2cs, void* wsp, size_t ws_bytes, int method, cudaStream_t st,
+                      int tf32 = 0);
 }  // namespace apx
 
 namespace apx {

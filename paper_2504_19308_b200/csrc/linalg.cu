@@ -15,6 +15,19 @@
 
 namespace apx {
 
+// Q output: plain conversion, or (tf32) rounded to the nearest TF32-representable fp32 value --
+// the TF32 tensor-core paths then read Q exactly (the tensor core itself would truncate it).
+template <typename TO>
+__device__ __forceinline__ TO qout(double v, int tf32) {
+  if constexpr (std::is_same<TO, float>::value) {
+    float f = (float)v;
+    if (tf32) f = __uint_as_float((__float_as_uint(f) + 0x1000u) & 0xffffe000u);
+    return f;
+  } else {
+    return (TO)v;
+  }
+}
+
 constexpr int kMaxL = 128;               // CholeskyQR2 fast path
 constexpr int kMaxHouseholderL = 12288;  // Householder: s_dot / s_tau in dynamic shared memory
 
@@ -423,7 +436,8 @@ __global__ void __launch_bounds__(256) apply_x_kernel(const TI* __restrict__ Y, 
                                                       const double* __restrict__ X, const int* __restrict__ skip,
                                                       const int* __restrict__ q1_skip, double* __restrict__ Q1,
                                                       TO* __restrict__ Q, int64_t qrs,
-                                                      int64_t qcs, TO* __restrict__ Q2, int64_t q2rs, int64_t q2cs) {
+                                                      int64_t qcs, TO* __restrict__ Q2, int64_t q2rs, int64_t q2cs,
+                                                      int tf32 = 0) {
   if (*skip) return;
   if (q1_skip && *q1_skip) Q1 = nullptr;  // CholeskyQR's second pass will not run
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -465,8 +479,8 @@ __global__ void __launch_bounds__(256) apply_x_kernel(const TI* __restrict__ Y, 
       const int c = tc + y;
       if (c >= l) continue;
       if (Q1) Q1[(size_t)r * l + c] = acc[x][y];
-      if (Q) Q[(size_t)r * qrs + (size_t)c * qcs] = (TO)acc[x][y];
-      if (Q2) Q2[(size_t)r * q2rs + (size_t)c * q2cs] = (TO)acc[x][y];
+      if (Q) Q[(size_t)r * qrs + (size_t)c * qcs] = qout<TO>(acc[x][y], tf32);
+      if (Q2) Q2[(size_t)r * q2rs + (size_t)c * q2cs] = qout<TO>(acc[x][y], tf32);
     }
   }
 }
@@ -480,7 +494,7 @@ __global__ void __launch_bounds__(256) apply_rinv_kernel(const TI* __restrict__ 
                                                          const double* __restrict__ rdiag,
                                                          const int* __restrict__ flag, TO* __restrict__ Q,
                                                          int64_t qrs, int64_t qcs, TO* __restrict__ Q2, int64_t q2rs,
-                                                         int64_t q2cs) {
+                                                         int64_t q2cs, int tf32) {
   if (*flag) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* Rs = reinterpret_cast<double*>(smem_raw);
@@ -520,8 +534,8 @@ __global__ void __launch_bounds__(256) apply_rinv_kernel(const TI* __restrict__ 
     for (int q = 0; q < LW; ++q) {
       const int c = lane + 32 * q;
       if (c < l) {
-        Q[(size_t)r * qrs + (size_t)c * qcs] = (TO)acc[q];
-        if (Q2) Q2[(size_t)r * q2rs + (size_t)c * q2cs] = (TO)acc[q];
+        Q[(size_t)r * qrs + (size_t)c * qcs] = qout<TO>(acc[q], tf32);
+        if (Q2) Q2[(size_t)r * q2rs + (size_t)c * q2cs] = qout<TO>(acc[q], tf32);
       }
     }
   }
@@ -534,7 +548,7 @@ __global__ void __launch_bounds__(1024) householder_qr_kernel(const TI* __restri
                                                               double* __restrict__ W /*m x l*/,
                                                               double* __restrict__ V /*m x l*/, TO* __restrict__ Q,
                                                               int64_t qrs, int64_t qcs, TO* __restrict__ Q2,
-                                                              int64_t q2rs, int64_t q2cs) {
+                                                              int64_t q2rs, int64_t q2cs, int tf32) {
   if (!force && !(*flag)) return;
   __shared__ double red[32];
   extern __shared__ double hh_smem[];  // s_dot[l], s_tau[l]
@@ -621,8 +635,8 @@ __global__ void __launch_bounds__(1024) householder_qr_kernel(const TI* __restri
   }
   for (size_t e = tid; e < (size_t)m * l; e += blockDim.x) {
     const size_t r = e / l, c = e % l;
-    Q[r * qrs + c * qcs] = (TO)W[e];
-    if (Q2) Q2[r * q2rs + c * q2cs] = (TO)W[e];
+    Q[r * qrs + c * qcs] = qout<TO>(W[e], tf32);
+    if (Q2) Q2[r * q2rs + c * q2cs] = qout<TO>(W[e], tf32);
   }
 }
 
@@ -654,7 +668,7 @@ size_t qr_ws_bytes(int m, int l) {
 template <typename TI, typename TO>
 static int launch_apply(const TI* Y, int64_t rs, int64_t cs, int m, int l, const double* Rinv, const double* rdiag,
                         const int* flag, TO* Q, int64_t qrs, int64_t qcs, TO* Q2, int64_t q2rs, int64_t q2cs,
-                        cudaStream_t st) {
+                        cudaStream_t st, int tf32 = 0) {
   const size_t smem = (size_t)(l * l + l) * sizeof(double);
   const int blocks = (int)std::min<int64_t>(ceil_div(m, 8), kNumSMs);
   const int lw = (int)ceil_div(l, 32);
@@ -662,7 +676,7 @@ static int launch_apply(const TI* Y, int64_t rs, int64_t cs, int m, int l, const
   {                                                                                                        \
     auto fn = apply_rinv_kernel<TI, TO, LWV>;                                                              \
     APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
-    fn<<<blocks, 256, smem, st>>>(Y, rs, cs, m, l, Rinv, rdiag, flag, Q, qrs, qcs, Q2, q2rs, q2cs);        \
+    fn<<<blocks, 256, smem, st>>>(Y, rs, cs, m, l, Rinv, rdiag, flag, Q, qrs, qcs, Q2, q2rs, q2cs, tf32);  \
   }
   if (lw == 1) APX_APPLY(1) else if (lw == 2) APX_APPLY(2) else if (lw == 3) APX_APPLY(3) else APX_APPLY(4)
 #undef APX_APPLY
@@ -703,10 +717,12 @@ static int launch_chol(const double* G, int l, double* R, double* rdiag, int* fl
 }
 
 // Q (m x l, strides qrs/qcs) = orth(Y); optional second copy Q2 (e.g. Q^T). method: 0 auto,
-// 1 force Householder.
+// 1 force Householder. tf32: round the fp32 outputs to the nearest TF32 value (the TF32 tensor
+// core operand paths; see qout).
 template <typename TI, typename TO>
 int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, int64_t qrs, int64_t qcs, TO* Q2,
-                      int64_t q2rs, int64_t q2cs, void* wsp, size_t ws_bytes, int method, cudaStream_t st) {
+                      int64_t q2rs, int64_t q2cs, void* wsp, size_t ws_bytes, int method, cudaStream_t st,
+                      int tf32) {
   APX_REQUIRE(l >= 1 && l <= kMaxHouseholderL, "sketch width %d outside [1, %d]", l, kMaxHouseholderL);
   APX_REQUIRE(m >= l, "need at least as many rows as columns, got %d x %d", m, l);
   Workspace ws(wsp, ws_bytes);
@@ -735,13 +751,14 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
     APX_LAUNCH_CHECK();
     APX_CUDA(cudaFuncSetAttribute(apply_x_kernel<TI, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem));
     APX_CUDA(cudaFuncSetAttribute(apply_x_kernel<double, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem));
-    apply_x_kernel<TI, TO><<<tiles, 256, kApplySmem, st>>>(Y, rs, cs, m, l, Rinv, flag, skip2, Q1, Q, qrs, qcs, Q2, q2rs, q2cs);
+    apply_x_kernel<TI, TO><<<tiles, 256, kApplySmem, st>>>(Y, rs, cs, m, l, Rinv, flag, skip2, Q1, Q, qrs, qcs, Q2,
+                                                           q2rs, q2cs, tf32);
     APX_LAUNCH_CHECK();
     APX_TRY(launch_gram<double>(Q1, l, 1, m, l, skip2, part, G, st));
     cholinv64_kernel<<<1, 256, 0, st>>>(G, l, Rinv, skip2, flag, (int*)nullptr, 0.0);
     APX_LAUNCH_CHECK();
     apply_x_kernel<double, TO><<<tiles, 256, kApplySmem, st>>>(Q1, l, 1, m, l, Rinv, skip2, (const int*)nullptr,
-                                                      (double*)nullptr, Q, qrs, qcs, Q2, q2rs, q2cs);
+                                                      (double*)nullptr, Q, qrs, qcs, Q2, q2rs, q2cs, tf32);
     APX_LAUNCH_CHECK();
   } else if (!householder_only) {
     // pass 1: Q1 = Y R1^{-1} (fp64)
@@ -751,13 +768,13 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
     // pass 2: Q = Q1 R2^{-1}
     APX_TRY(launch_gram<double>(Q1, l, 1, m, l, flag, part, G, st));
     APX_TRY(launch_chol(G, l, Rinv, rdiag, flag, st));
-    APX_TRY((launch_apply<double, TO>(Q1, l, 1, m, l, Rinv, rdiag, flag, Q, qrs, qcs, Q2, q2rs, q2cs, st)));
+    APX_TRY((launch_apply<double, TO>(Q1, l, 1, m, l, Rinv, rdiag, flag, Q, qrs, qcs, Q2, q2rs, q2cs, st, tf32)));
   }
   const size_t hh_smem = (size_t)2 * l * sizeof(double);
   APX_CUDA(cudaFuncSetAttribute(householder_qr_kernel<TI, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)std::max<size_t>(hh_smem, 48 * 1024)));
   householder_qr_kernel<TI, TO><<<1, 1024, hh_smem, st>>>(Y, rs, cs, m, l, flag, 0, W, V, Q, qrs, qcs, Q2, q2rs,
-                                                           q2cs);
+                                                           q2cs, tf32);
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -808,7 +825,7 @@ int cholqr_rows_pass1(const float* Y, int m, int l, const double* G, float* Q, d
   APX_CUDA(cudaFuncSetAttribute(apply_x_kernel<float, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kApplySmem));
   apply_x_kernel<float, float><<<(unsigned)ceil_div(m, 64), 256, kApplySmem, st>>>(
-      Y, l, 1, m, l, r.Rinv, r.flag, r.flag + 1, r.Q1, Q, l, 1, (float*)nullptr, 0, 0);
+      Y, l, 1, m, l, r.Rinv, r.flag, r.flag + 1, r.Q1, Q, l, 1, (float*)nullptr, 0, 0, 1);
   APX_LAUNCH_CHECK();
   return launch_gram<double>(r.Q1, l, 1, m, l, r.flag + 1, r.part, G2, st);
 }
@@ -822,7 +839,8 @@ int cholqr_rows_pass2(int m, int l, const double* G2, float* Q, void* wsp, size_
   APX_CUDA(cudaFuncSetAttribute(apply_x_kernel<double, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kApplySmem));
   apply_x_kernel<double, float><<<(unsigned)ceil_div(m, 64), 256, kApplySmem, st>>>(
-      r.Q1, l, 1, m, l, r.Rinv, r.flag + 1, (const int*)nullptr, (double*)nullptr, Q, l, 1, (float*)nullptr, 0, 0);
+      r.Q1, l, 1, m, l, r.Rinv, r.flag + 1, (const int*)nullptr, (double*)nullptr, Q, l, 1, (float*)nullptr, 0, 0,
+      1);
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -834,8 +852,8 @@ const int* cholqr_rows_flags(void* wsp, size_t bytes, int m, int l) {
 }
 
 template int qr_orthonormalize<float, float>(const float*, int64_t, int64_t, int, int, float*, int64_t, int64_t,
-                                             float*, int64_t, int64_t, void*, size_t, int, cudaStream_t);
+                                             float*, int64_t, int64_t, void*, size_t, int, cudaStream_t, int);
 template int qr_orthonormalize<double, double>(const double*, int64_t, int64_t, int, int, double*, int64_t, int64_t,
-                                               double*, int64_t, int64_t, void*, size_t, int, cudaStream_t);
+                                               double*, int64_t, int64_t, void*, size_t, int, cudaStream_t, int);
 
 }  // namespace apx

@@ -8,7 +8,7 @@
 //   warp 1      TMEM allocator + MMA issuer: one lane issues tcgen05.mma.cta_group::1.kind::tf32
 //               (M=128, N=BN, K=8) x4 per stage and commits to the stage's `empty` mbarrier.
 //   warps 2..5  (FIX 1) zero the kept-cycle entries of each landed A tile (dB^T), or (FIX 2) round
-//               both landed operand tiles to TF32 nearest (the tensor core itself truncates: a
+//               the landed A tile to TF32 nearest (the tensor core itself truncates: a
 //               systematic -2^-11.5 relative bias per operand, which a sum of squares of the
 //               result -- ||Q^T A||^2 for the residual energy -- accumulates), then
 //               epilogue: tcgen05.ld.32x32b.x32 from TMEM (warp%4 selects the lane quarter).
@@ -244,10 +244,11 @@ __global__ void __launch_bounds__(kThreads, 1)
       for (int kt = 0; kt < ktiles; ++kt) {
         const int s = kt % STAGES;
         mbar_wait(&full[s], (uint32_t)((kt / STAGES) & 1));
-        // every 4-byte word of the stage (A tile then B tile) is an operand value: round in place
+        // every 4-byte word of the A tile is an operand value: round in place (the B operand,
+        // Q, is produced already rounded: qr_orthonormalize(..., tf32 = 1))
         uint4* w = reinterpret_cast<uint4*>(smem + (size_t)s * CF::kStage);
 #pragma unroll 4
-        for (int v = et; v < CF::kStage / 16; v += 128) {
+        for (int v = et; v < CF::kTileA / 16; v += 128) {
           // round the magnitude half-up at bit 13 (sign-magnitude: an integer add on the bits;
           // a carry into the exponent is the correct rounding): two integer ops per value
           uint4 x = w[v];

@@ -188,6 +188,25 @@ def sparse_dense_multiply(S: SparseRowMatrix, B, side: str = "left") -> np.ndarr
     raise ValueError(f"unknown side {side!r}")
 
 
+def sfft_product_device(Ad, Bd, code, k: int, order: int, sparsify_cols: bool, out=None):
+    """Device-level sfft product (apx_sfft_first_order) on device operands Ad (m x n), Bd (n x p)
+    of dtype `code` (APX_F64 / APX_C128): dict(M, sel_a, sel_b, scalars, ka, kb, ws)."""
+    m, n = Ad.shape
+    p = Bd.shape[1]
+    dev = Ad.device
+    M = out if out is not None else torch.empty((m, p), dtype=torch.complex128, device=dev)
+    scal = torch.zeros(N.NSCALARS, dtype=torch.float64, device=dev)
+    ws = D.workspace(N.size("apx_sfft_first_order_workspace", m, n, p, k))
+    ka = min(k, n)
+    kb = min(k, n if sparsify_cols else p)
+    sa = torch.full((m, max(ka, 1)), -1, dtype=torch.int32, device=dev)
+    sb = torch.full((p if sparsify_cols else n, max(kb, 1)), -1, dtype=torch.int32, device=dev)
+    N.call("apx_sfft_first_order", code, Ad.data_ptr(), Bd.data_ptr(), m, n, p, k, order,
+           1 if sparsify_cols else 0, M.data_ptr(), sa.data_ptr(), sb.data_ptr(), scal.data_ptr(),
+           ws.data_ptr(), ws.numel(), D.stream_ptr())
+    return {"M": M, "sel_a": sa, "sel_b": sb, "scalars": scal, "ka": ka, "kb": kb, "ws": ws}
+
+
 def fft_sparse_first_order_multiply(A, B, k: int, order: int, sparsify_b: str = "rows",
                                     model: ErrorModel | None = None):
     """fsparse.py:168-240 -- approximate A @ B through top-k sparsified Fourier transforms."""
@@ -208,19 +227,11 @@ def fft_sparse_first_order_multiply(A, B, k: int, order: int, sparsify_b: str = 
     dev = D.require_cuda()
     Ad = torch.from_numpy(np.ascontiguousarray(Ah.astype(dt))).to(dev)
     Bd = torch.from_numpy(np.ascontiguousarray(Bh.astype(dt))).to(dev)
-    m, p = Ah.shape[0], Bh.shape[1]
-    M = torch.empty((m, p), dtype=torch.complex128, device=dev)
-    scal = torch.zeros(N.NSCALARS, dtype=torch.float64, device=dev)
+    m = Ah.shape[0]
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    ws = D.workspace(N.size("apx_sfft_first_order_workspace", m, n, p, k))
-    ka = min(k, n)
-    kb = min(k, n if sparsify_b == "cols" else p)
-    sa = torch.full((m, max(ka, 1)), -1, dtype=torch.int32, device=dev)
-    sb = torch.full((p if sparsify_b == "cols" else n, max(kb, 1)), -1, dtype=torch.int32, device=dev)
-    N.call("apx_sfft_first_order", code, Ad.data_ptr(), Bd.data_ptr(), m, n, p, k, order,
-           1 if sparsify_b == "cols" else 0, M.data_ptr(), sa.data_ptr(), sb.data_ptr(), scal.data_ptr(),
-           ws.data_ptr(), ws.numel(), D.stream_ptr())
+    r = sfft_product_device(Ad, Bd, code, k, order, sparsify_b == "cols")
+    M, scal, sa, sb, ka, kb = r["M"], r["scalars"], r["sel_a"], r["sel_b"], r["ka"], r["kb"]
     s = scal.tolist()
     wall = time.perf_counter() - t0
     nA, nB = math.sqrt(max(0.0, s[N.S_FRO2_A])), math.sqrt(max(0.0, s[N.S_FRO2_B]))

@@ -227,3 +227,188 @@ def norms_from_scalars(s, n: int):
     from .cycle import _norms
 
     return _norms(s, n * n)
+
+
+# ---- the circulant product sharded by rows of M (C3 / C5-secondary) -----------
+# term1 = Ahat B is column-local (circulant.py:136-147), term2 = dA Bhat row-local (:150-161): a
+# rank computes term1 for a block of COLUMNS and term2 for its block of ROWS, and one all-to-all
+# moves term1's pieces to the ranks that own their rows. The decompositions are split by cycle
+# blocks (zero-padded partial magnitudes and selected spectra, summed = gathered in rank order),
+# so selections and every row of M are bitwise the single-device product's.
+
+def _even_cut(n: int, world: int, r: int) -> int:
+    return n if r == world else min(n, 2 * round(r * n / (2 * world)))
+
+
+def circulant_partition(n: int, world: int, rank: int):
+    """(rows, cols, cycle blocks) of `rank`: rows and columns [r0, r1) cut at even indices (the
+    kernels pair rows / columns), cycle blocks an even split of the decomposition grid."""
+    import ctypes as C
+
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError(f"bad rank {rank} of {world}")
+    parts, cpc = C.c_int64(), C.c_int64()
+    N.call("apx_circulant_rows_grid", n, C.addressof(parts), C.addressof(cpc))
+    P = parts.value
+    rows = (_even_cut(n, world, rank), _even_cut(n, world, rank + 1))
+    blks = (round(rank * P / world), round((rank + 1) * P / world))
+    return rows, rows, blks, P
+
+
+def circulant_rows_steps(A, B, k: int, order: int, world: int, rank: int, out=None):
+    """One rank's share of the circulant product on replicated device operands A, B (n x n fp64 or
+    complex128). Yields ("sum", t) at the three summing exchanges and ("rows", T1, M_rows, plan) at
+    the all-to-all (plan = every rank's (rows, cols)); returns dict(M=rows of M (complex128),
+    sel_a, sel_b, scalars, rows)."""
+    n = A.shape[0]
+    if tuple(A.shape) != (n, n) or tuple(B.shape) != (n, n):
+        raise ValueError("two square n x n operands required")
+    if order not in (0, 1):
+        raise ValueError("order must be 0 or 1")
+    cplx = A.is_complex() or B.is_complex()
+    code = N.APX_C128 if cplx else N.APX_F64
+    dt = torch.complex128 if cplx else torch.float64
+    A, B = A.to(dt).contiguous(), B.to(dt).contiguous()
+    dev = A.device
+    (r0, r1), (c0, c1), (b0, b1), P = circulant_partition(n, world, rank)
+    plan = [circulant_partition(n, world, h)[:2] for h in range(world)]
+    m, w = r1 - r0, c1 - c0
+    M = out if out is not None else torch.zeros((m, n), dtype=torch.complex128, device=dev)
+    T1 = torch.empty((n, max(w, 1)), dtype=torch.complex128, device=dev)
+    sa = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+    sb = torch.empty(max(k, 1), dtype=torch.int32, device=dev)
+    scal = torch.zeros(N.NSCALARS, dtype=torch.float64, device=dev)
+    ws = D.workspace(N.size("apx_circulant_rows_workspace", code, n, k, m, b0, b1))
+    red1 = torch.zeros(2 * P * n, dtype=torch.float64, device=dev)
+    red2 = torch.zeros(2 * max(k, 1) * n, dtype=torch.complex128, device=dev)
+    fin = torch.zeros(1, dtype=torch.float64, device=dev)
+
+    def phase(i, red_in, red_out):
+        N.call("apx_circulant_rows_phase", i, code, A.data_ptr(), B.data_ptr(), n, k, order, r0, m, c0, w, b0, b1,
+               M.data_ptr(), T1.data_ptr(), sa.data_ptr(), sb.data_ptr(), D.ptr(red_in), D.ptr(red_out),
+               scal.data_ptr(), ws.data_ptr(), ws.numel(), D.stream_ptr())
+
+    phase(1, None, red1)
+    yield ("sum", red1)
+    phase(2, red1, red2)
+    yield ("sum", red2.view(torch.float64))
+    phase(3, red2, None)
+    yield ("rows", T1[:, :w], M, plan)
+    phase(4, None, fin)
+    yield ("sum", fin)
+    scal[N.S_FRO2_M] = fin[0]
+    return {"M": M, "sel_a": sa[:k], "sel_b": sb[:k], "scalars": scal, "rows": (r0, r1), "ws": ws}
+
+
+def _a2a_rows(T1, M_rows, plan, rank, group=None):
+    """All-to-all of term1's pieces: rank g sends T1[rows of h, :] (its columns) to every h and
+    places what it receives at M_rows[:, cols of h]."""
+    import torch.distributed as dist
+
+    (r0, r1), _ = plan[rank]
+    m = r1 - r0
+    w = T1.shape[1]
+    send = torch.cat([T1[a:b].reshape(-1) for (a, b), _ in plan]) if w else T1.new_zeros(0)
+    in_splits = [(b - a) * w for (a, b), _ in plan]
+    out_splits = [m * (d - c) for _, (c, d) in plan]
+    recv = torch.empty(sum(out_splits), dtype=T1.dtype, device=T1.device)
+    if dist.get_backend(group) == "nccl":
+        dist.all_to_all_single(torch.view_as_real(recv).view(-1), torch.view_as_real(send).view(-1),
+                               [2 * x for x in out_splits], [2 * x for x in in_splits], group=group)
+    else:  # gloo has no alltoall: pairwise point-to-point exchanges (the grouped send/recv form)
+        outs = list(recv.split(out_splits))
+        ins = list(send.split(in_splits))
+        outs[rank].copy_(ins[rank])
+        reqs = []
+        for h in range(len(plan)):
+            if h != rank:
+                reqs.append(dist.isend(ins[h].contiguous(), dist.get_global_rank(group, h) if group else h, group=group))
+                reqs.append(dist.irecv(outs[h], dist.get_global_rank(group, h) if group else h, group=group))
+        for r in reqs:
+            r.wait()
+        recv = torch.cat(outs)
+    off = 0
+    for (_, (c, d)), sz in zip(plan, out_splits):
+        M_rows[:, c:d] = recv[off:off + sz].view(m, d - c)
+        off += sz
+
+
+def circulant_product_rows(A, B, k: int, order: int, group=None, out=None):
+    """This rank's rows of the circulant product (the exchanges over torch.distributed)."""
+    import torch.distributed as dist
+
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    gen = circulant_rows_steps(A, B, k, order, world, rank, out)
+    try:
+        req = next(gen)
+        while True:
+            if req[0] == "sum":
+                ordered_sum(req[1], group)
+            else:
+                _a2a_rows(req[1], req[2], req[3], rank, group)
+            req = gen.send(None)
+    except StopIteration as e:
+        return e.value
+
+
+def circulant_lockstep(gens):
+    """Drive the circulant shards of one process (tests; single-GPU simulation): rank-order sums
+    at the summing exchanges, the term1 redistribution done by slicing."""
+    reqs = [next(g) for g in gens]
+    results = [None] * len(gens)
+    while True:
+        kind = reqs[0][0]
+        if any(r[0] != kind for r in reqs):
+            raise RuntimeError("shards disagree on the exchange sequence")
+        if kind == "sum":
+            total = rank_order_sum([r[1] for r in reqs])
+            for r in reqs:
+                r[1].copy_(total)
+        else:
+            plan = reqs[0][3]
+            for g, r in enumerate(reqs):
+                (a, b), _ = plan[g]
+                for h, rh in enumerate(reqs):
+                    _, (c, d) = plan[h]
+                    r[2][:, c:d] = rh[1][a:b]
+        nxt = []
+        for i, g in enumerate(gens):
+            try:
+                nxt.append(g.send(None))
+            except StopIteration as e:
+                results[i] = e.value
+                nxt.append(None)
+        if all(x is not None for x in results):
+            return results
+        if any(x is None for x in nxt):
+            raise RuntimeError("shards disagree on the number of exchange points")
+        reqs = nxt
+
+
+# ---- the sfft product sharded by rows (fsparse.py:168-240; SURVEY.md §8(e) secondary) ------------
+# Rows of At = A W* and A's per-row selection are row-local; B is replicated, so Bt = W B, its
+# selection and SB are the same on every rank. The only exchange: [||A_g||^2, ||dAt_g||^2,
+# ||M_g||^2].
+
+def sfft_rows_steps(A_rows, B, k: int, order: int, sparsify_b: str = "rows", out=None):
+    """One rank's rows of the sfft product (device operands, fp64 or complex128). Yields the
+    3-vector to sum over ranks; returns dict(M=rows of M, sel_a (rank rows), sel_b, scalars)."""
+    from .fsparse import sfft_product_device
+
+    if sparsify_b not in ("rows", "cols"):
+        raise ValueError(f"unknown sparsify_b {sparsify_b!r}")
+    cplx = A_rows.is_complex() or B.is_complex()
+    code = N.APX_C128 if cplx else N.APX_F64
+    dt = torch.complex128 if cplx else torch.float64
+    r = sfft_product_device(A_rows.to(dt).contiguous(), B.to(dt).contiguous(), code, k, order,
+                            sparsify_b == "cols", out)
+    s = r["scalars"]
+    part = torch.stack([s[N.S_FRO2_A], s[N.S_RES2_A], s[N.S_FRO2_M]])
+    yield part
+    s[N.S_FRO2_A], s[N.S_RES2_A], s[N.S_FRO2_M] = part[0], part[1], part[2]
+    return r
+
+
+def sfft_product_rows(A_rows, B, k: int, order: int, sparsify_b: str = "rows", group=None, out=None):
+    """This rank's rows of the sfft product (one ordered-sum exchange over torch.distributed)."""
+    return _drive(sfft_rows_steps(A_rows, B, k, order, sparsify_b, out), lambda t: ordered_sum(t, group))

@@ -232,3 +232,139 @@ def test_ordered_sum_bitwise_gloo():
     want32 = rank_order_sum([p.float().reshape(64, 64) for p in parts]).numpy().tobytes()
     assert all(o[1] == want for o in out)          # identical bits on every rank = lockstep's order
     assert all(o[2] == want32 for o in out)
+
+
+# ---- the row-sharded circulant product's protocol (sharded.circulant_rows_steps) over gloo ----
+# Device phases replaced by the oracle on CPU (test-only stand-ins): magnitude partials of the
+# rank's cycles -> ordered sum -> selection; selected spectrum rows of the rank's cycles
+# (zero-padded) -> ordered sum; term1 for the rank's COLUMNS -> all-to-all (sharded._a2a_rows,
+# the function the GPU path uses) into the rank's rows; term2 for the rank's ROWS; ||M_g||^2 -> sum.
+
+def _toy_circ_rows_steps(A, B, k, world, rank):
+    import numpy as np
+    import oracle as O
+    from oracle import apx_oracle as OX
+    n = A.shape[0]
+    a0, a1 = (rank * n) // world, ((rank + 1) * n) // world        # cycle block of this rank
+    r0, r1 = 2 * round(rank * n / (2 * world)), n if rank == world - 1 else 2 * round((rank + 1) * n / (2 * world))
+    plan = []
+    for h in range(world):
+        h0 = 2 * round(h * n / (2 * world))
+        h1 = n if h == world - 1 else 2 * round((h + 1) * n / (2 * world))
+        plan.append(((h0, h1), (h0, h1)))
+    Sa, _ = O.circulant_decompose(A)
+    Sb, _ = O.circulant_decompose(B)
+    part = torch.zeros(2, n, dtype=torch.float64)
+    part[0] = torch.from_numpy(np.sum(np.abs(Sa[:, a0:a1]) ** 2, axis=1))
+    part[1] = torch.from_numpy(np.sum(np.abs(Sb[:, a0:a1]) ** 2, axis=1))
+    yield ("sum", part)
+    sel_a = O.top_indices(np.sqrt(part[0].numpy()), k)
+    sel_b = O.top_indices(np.sqrt(part[1].numpy()), k)
+    spec = torch.zeros(2, n, n, dtype=torch.complex128)   # rows t of S from this rank's cycles j
+    spec[0][:, a0:a1] = torch.from_numpy(Sa[:, a0:a1])
+    spec[1][:, a0:a1] = torch.from_numpy(Sb[:, a0:a1])
+    yield ("sum", torch.view_as_real(spec))
+    Sa_g, Sb_g = spec[0].numpy(), spec[1].numpy()
+    c0, c1 = plan[rank][1]
+    FB = OX.unitary_dft(B, "forward", axis=0)
+    T1 = torch.from_numpy(np.ascontiguousarray(O.circulant_left_product(Sa_g, sel_a, FB[:, c0:c1])))
+    M = torch.zeros(r1 - r0, n, dtype=torch.complex128)
+    yield ("rows", T1, M, plan)
+    dA = A[r0:r1] - O.circulant_materialize(Sa_g, sel_a)[r0:r1]
+    M += torch.from_numpy(O.circulant_right_product(Sb_g, sel_b, dA))
+    fin = torch.tensor([float(torch.sum(torch.abs(M) ** 2))], dtype=torch.float64)
+    yield ("sum", fin)
+    return (r0, r1), sel_a, sel_b, M.numpy(), float(fin[0])
+
+
+def _sharded_circ_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import oracle as O
+        from paper_2504_19308_b200.sharded import _a2a_rows, ordered_sum
+        n, k = 64, 6
+        A, B = O.gen_circulant_operand(n, 4, 41), O.gen_circulant_operand(n, 4, 42)
+        gen = _toy_circ_rows_steps(A, B, k, world, rank)
+        req = next(gen)
+        try:
+            while True:
+                if req[0] == "sum":
+                    ordered_sum(req[1])
+                else:
+                    _a2a_rows(req[1], req[2], req[3], rank)
+                req = gen.send(None)
+        except StopIteration as e:
+            q.put((rank,) + e.value)
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_sharded_circulant_protocol_gloo():
+    import numpy as np
+    import oracle as O
+    world, port = 3, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_circ_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted((q.get(timeout=120) for _ in range(world)), key=lambda o: o[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    n, k = 64, 6
+    A, B = O.gen_circulant_operand(n, 4, 41), O.gen_circulant_operand(n, 4, 42)
+    sel_a = [o[2] for o in out]
+    M, rep = O.circulant_first_order_multiply(A, B, k, 1, sel_a[0], out[0][3])
+    assert all(s == sel_a[0] for s in sel_a)                   # one selection on every rank
+    got = np.concatenate([o[4] for o in out], axis=0)
+    assert [o[1] for o in out] == [(0, 22), (22, 42), (42, 64)]
+    assert np.linalg.norm(got - M) <= 1e-12 * np.linalg.norm(M)
+    assert out[0][5] == pytest.approx(float(np.sum(np.abs(M) ** 2)), rel=1e-12)
+
+
+# ---- the row-sharded sfft product (sharded.sfft_rows_steps): rows of the oracle's product are
+# row-local, so each rank's oracle product on its rows of A is those rows of the full product ----
+
+def _sharded_sfft_worker(rank, world, port, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        import numpy as np
+        import oracle as O
+        from paper_2504_19308_b200.sharded import ordered_sum
+        rng = np.random.default_rng(9)
+        A, B = rng.standard_normal((40, 32)), rng.standard_normal((32, 24))
+        r0, r1 = (rank * 40) // world, ((rank + 1) * 40) // world
+        Mg, rep = O.fft_sparse_first_order_multiply(A[r0:r1], B, 5, 1, "rows")
+        part = torch.tensor([float(np.sum(A[r0:r1] ** 2)), rep["norm_da"] ** 2, float(np.sum(np.abs(Mg) ** 2))],
+                            dtype=torch.float64)
+        ordered_sum(part)
+        q.put((rank, Mg, part.numpy()))
+    finally:
+        dist.destroy_process_group()
+
+
+def test_row_sharded_sfft_protocol_gloo():
+    import numpy as np
+    import oracle as O
+    world, port = 2, _free_port()
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    procs = [ctx.Process(target=_sharded_sfft_worker, args=(r, world, port, q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    out = sorted((q.get(timeout=120) for _ in range(world)), key=lambda o: o[0])
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    rng = np.random.default_rng(9)
+    A, B = rng.standard_normal((40, 32)), rng.standard_normal((32, 24))
+    M, rep = O.fft_sparse_first_order_multiply(A, B, 5, 1, "rows")
+    got = np.concatenate([o[1] for o in out], axis=0)
+    assert np.linalg.norm(got - M) <= 1e-12 * np.linalg.norm(M)
+    fro2, res2, m2 = out[0][2]
+    assert fro2 == pytest.approx(float(np.sum(A ** 2)), rel=1e-12)
+    assert res2 == pytest.approx(rep["norm_da"] ** 2, rel=1e-12)
+    assert m2 == pytest.approx(float(np.sum(np.abs(M) ** 2)), rel=1e-12)

@@ -12,7 +12,8 @@ from paper_2504_19308_b200 import _native as N  # noqa: E402
 n, l = 8192, 64
 dev = torch.device("cuda", 0)
 A = torch.randn(n, n, device=dev) / n ** 0.5
-Q = torch.linalg.qr(torch.randn(n, l, device=dev, dtype=torch.float64))[0].float().contiguous()
+Q = torch.linalg.qr(torch.randn(n, l, device=dev, dtype=torch.float64))[0].float()
+Q = ((Q.view(torch.int32) + 0x1000) & -8192).view(torch.float32).contiguous()  # TF32-rounded, as the C4 plan stores it
 lib = N.lib()
 st = torch.cuda.current_stream().cuda_stream
 for splits in (1, 2, 4):
