@@ -82,3 +82,19 @@ def test_sketch_validation_before_device():
         sketch_norm_estimate(np.eye(3), np.eye(4), 2, 0)
     with pytest.raises(ValueError):
         sketch_norm_estimate(np.eye(3), np.eye(3), 0, 0)
+
+
+def test_extend_bench_csv(tmp_path):
+    """clibench.extend_bench_csv: the reference's bench schema plus products/s and roofline columns."""
+    from paper_2504_19308_b200.clibench import EXTRA, extend_bench_csv
+    src = tmp_path / "b.csv"
+    src.write_text("method,order,n,kind_a,kind_b,s,k,rel_err,apriori_est,posterior_est,wall_time_s,seed\n"
+                   "svd,first,512,kappa,kappa,1,10,0.01,0.02,0.03,0.002,0\n"
+                   "naive,-,512,kappa,kappa,-,-,0,-,-,0.5,0\n")
+    dst = tmp_path / "b.gpu.csv"
+    assert extend_bench_csv(str(src), str(dst), 35.8, lambda m, n, k=0, c=0: 6.0 * k * n * n if m == "svd" else 2.0 * n ** 3) == 2
+    rows = [line.split(",") for line in dst.read_text().splitlines()]
+    assert rows[0][12:] == EXTRA
+    assert float(rows[1][12]) == pytest.approx(500.0)
+    assert float(rows[1][13]) == pytest.approx(6.0 * 10 * 512 * 512)
+    assert float(rows[1][16]) == pytest.approx(6.0 * 10 * 512 * 512 / 0.002 / 1e12 / 35.8, rel=1e-5)
