@@ -258,8 +258,11 @@ def cpu_product(cfg, ops):
         A, B = ops
         M, rep = O.cycle_first_order_multiply(A, B, 32, 1)
     elif cfg == "c3":
-        A, B = ops
-        M, rep = O.circulant_first_order_multiply(A, B, 16, 1)
+        A, B = ops[:2]
+        # near-tie protocol: the operands' conjugate-pair spectra tie exactly at
+        # the selection boundary, so the oracle runs with the GPU's selections when they are given
+        sel = ops[2] if len(ops) > 2 else (None, None)
+        M, rep = O.circulant_first_order_multiply(A, B, 16, 1, sel[0], sel[1])
     else:
         raise ValueError(cfg)
     return time.perf_counter() - t0, M, rep
@@ -609,7 +612,9 @@ def _secondary_setup(cfg, rank, world, dev):
         out.update(step=step, units=1, n=n, dtype="f64", bound="fp64 (DFMA)", flops=12.5e9,
                    peak_key="fp64_dfma_tflops", bytes_alt=80.0 * n * n,
                    note="one product per step; roofline T* = max(80n^2 B / HBM, 12.5 GFLOP / DFMA) (SURVEY §8(d))",
-                   host_ops=lambda: (A.cpu().numpy(), B.cpu().numpy()),
+                   host_ops=lambda: (A.cpu().numpy(), B.cpu().numpy(),
+                                     (res["r"]["sel_a"].tolist(), res["r"]["sel_b"].tolist()) if "r" in res
+                                     else (None, None)),
                    api=lambda Ah, Bh: P.circulant_first_order_multiply(Ah, Bh, 16, 1),
                    dev_out=lambda: M, keep=(A, B, M, res))
     elif cfg in ("c5", "c5c"):
@@ -704,6 +709,17 @@ def run_secondary(args, rank, world, local_rank):
         Mg = st["dev_out"]().cpu().numpy()
         line["parity_vs_oracle"] = {"rel": float(np.linalg.norm(Mg - Mo) / np.linalg.norm(Mo)),
                                     "tol": 1e-10, "note": "first product of the step's batch"}
+        if cfg == "c3":  # near-tie protocol: the oracle's own picks vs the GPU's (forced above)
+            import oracle as O
+            subs, worst = 0, 0.0
+            for key, gsel in (("magnitudes_a", ops[2][0]), ("magnitudes_b", ops[2][1])):
+                mags = ro[key]
+                own = O.top_indices(mags, 16)
+                for a, b in zip(sorted(set(gsel) - set(own)), sorted(set(own) - set(gsel))):
+                    subs += 1
+                    worst = max(worst, abs(mags[a] - mags[b]) / np.spacing(np.max(mags)))
+            line["parity_vs_oracle"]["near_tie_substitutions"] = subs
+            line["parity_vs_oracle"]["worst_tie_gap_ulps"] = worst
     print(json.dumps(line), flush=True)
 
 

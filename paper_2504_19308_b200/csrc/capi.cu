@@ -718,6 +718,7 @@ size_t apx_cycle_first_order_workspace(int dtype, int64_t n, int k_a, int k_b, i
 int apx_cycle_first_order(int dtype, const void* A, const void* B, int64_t n, int k_a, int k_b, int order,
                           const int32_t* force_sel_a, const int32_t* force_sel_b, void* M, int32_t* sel_a,
                           int32_t* sel_b, double* scalars, void* wsp, size_t ws_bytes, void* stream) {
+  APX_NVTX("apx_cycle_first_order");
   APX_REQUIRE(dtype == F32 || dtype == F64, "cycle product: real dtype required");
   APX_REQUIRE(n >= 1 && n <= 46340, "n=%lld out of range", (long long)n);
   APX_REQUIRE(k_a >= 0 && k_a <= n && k_b >= 0 && k_b <= n, "k out of range [0, %lld]", (long long)n);
@@ -744,6 +745,7 @@ int apx_cycle_rows_phase(int phase, int dtype, const void* A_rows, int64_t m_row
                          int64_t n, int k_a, int k_b, int order, void* M_rows, int32_t* sel_a, int32_t* sel_b,
                          const double* red_in, double* red_out, double* scalars, void* wsp, size_t ws_bytes,
                          void* stream) {
+  APX_NVTX("apx_cycle_rows_phase");
   APX_REQUIRE(phase == 1 || phase == 2, "phase must be 1 or 2");
   APX_REQUIRE(dtype == F32 || dtype == F64, "cycle product: real dtype required");
   APX_REQUIRE(n >= 1 && n <= 46340, "n=%lld out of range", (long long)n);
@@ -794,6 +796,7 @@ int apx_mixed_rows_phase(int phase, const float* A_rows, int64_t m_rows, const f
                          int k_cyc, int order, int flags, const float* omega, float* M_rows, int32_t* sel_b,
                          const void* red_in, void* red_out, double* scalars, void* wsp, size_t ws_bytes,
                          void* stream) {
+  APX_NVTX("apx_mixed_rows_phase");
   APX_REQUIRE(phase >= 1 && phase <= 4, "phase must be 1..4");
   APX_REQUIRE(n >= 128 && n <= 46340 && (n % 32) == 0, "n=%lld: the sharded product needs n %% 32 == 0, n >= 128",
               (long long)n);
@@ -813,6 +816,7 @@ int apx_mixed_rows_phase(int phase, const float* A_rows, int64_t m_rows, const f
 int apx_mixed_first_order(int dtype, const void* A, const void* B, int64_t n, int k_svd, int k_cyc, int order,
                           int power_iterations, const void* omega, const int32_t* force_sel_b, int flags, void* M,
                           int32_t* sel_b, double* scalars, void* wsp, size_t ws_bytes, void* stream) {
+  APX_NVTX("apx_mixed_first_order");
   APX_REQUIRE(dtype == F32 || dtype == F64, "mixed product: real dtype required");
   APX_REQUIRE(n >= 2 && n <= 46340, "n=%lld out of range", (long long)n);
   APX_REQUIRE(k_svd >= 1 && k_svd <= 128 && k_svd <= n, "k_svd=%d out of range [1, min(n,128)]", k_svd);

@@ -156,6 +156,7 @@ size_t apx_rsvd_workspace(int dtype, int64_t m, int64_t n, int l) {
 
 int apx_rsvd(int dtype, const void* A_, int64_t m, int64_t n, int l, int k, int power_iterations, const void* omega,
              void* U_, double* sigma, void* V_, double* scalars, void* wsp, size_t ws_bytes, void* stream) {
+  APX_NVTX("apx_rsvd");
   APX_REQUIRE(dtype == F64, "randomized_partial_svd: fp64 required");
   APX_REQUIRE(m >= 1 && n >= 1, "empty matrix");
   APX_REQUIRE(l >= 1 && l <= m && l <= n, "sketch width %d out of range", l);
@@ -194,6 +195,7 @@ size_t apx_qr_workspace(int dtype, int64_t m, int64_t k) {
 
 int apx_qr(int dtype, const void* Y_, int64_t m, int64_t k, void* Q_, void* R_, void* wsp, size_t ws_bytes,
            void* stream) {
+  APX_NVTX("apx_qr");
   APX_REQUIRE(dtype == F64, "qr_decompose: fp64 required");
   APX_REQUIRE(m >= k, "need at least as many rows as columns, got %lld x %lld", (long long)m, (long long)k);
   APX_REQUIRE(k >= 1, "qr_decompose: at least one column");
@@ -226,6 +228,7 @@ size_t apx_sketch_norm_workspace(int64_t m, int64_t n, int64_t p, int k) {
 
 int apx_sketch_norm(const double* A, const double* B, int64_t m, int64_t n, int64_t p, const double* G, int k,
                     double* out, void* wsp, size_t ws_bytes, void* stream) {
+  APX_NVTX("apx_sketch_norm");
   APX_REQUIRE(m >= 1 && n >= 1 && p >= 1, "sketch_norm: empty operand");
   APX_REQUIRE(k >= 1, "k must be >= 1");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -258,6 +261,7 @@ size_t apx_gemm_workspace(int dtype, int64_t M, int64_t N, int64_t K, int trans_
 int apx_gemm(int dtype, int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const void* A, int64_t lda,
              const void* B, int64_t ldb, void* C, int64_t ldc, int accumulate, void* wsp, size_t ws_bytes,
              void* stream) {
+  APX_NVTX("apx_gemm");
   APX_REQUIRE(dtype == F32 || dtype == F64, "gemm: real dtype required");
   APX_REQUIRE(M >= 1 && N >= 1 && K >= 1, "gemm: empty operand");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -295,6 +299,7 @@ size_t apx_svd_first_order_workspace(int dtype, int64_t m, int64_t n, int64_t p,
 int apx_svd_first_order(int dtype, const void* A_, const void* B_, int64_t m, int64_t n, int64_t p, int l_a, int k_a,
                         int l_b, int k_b, int power_iterations, int order, const void* omega_a,
                         const void* omega_b, void* M_, double* scalars, void* wsp, size_t ws_bytes, void* stream) {
+  APX_NVTX("apx_svd_first_order");
   APX_REQUIRE(dtype == F64, "svd_first_order_multiply: fp64 required");
   APX_REQUIRE(m >= 1 && n >= 1 && p >= 1, "empty matrix");
   APX_REQUIRE(l_a >= 1 && l_a <= m && l_a <= n && k_a >= 1 && k_a <= l_a, "A sketch out of range");

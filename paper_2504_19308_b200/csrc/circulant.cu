@@ -187,7 +187,7 @@ __global__ void __launch_bounds__(512) circ_spectra_kernel(const double2* __rest
                                                            const int* __restrict__ sel,
                                                            const double2* __restrict__ roots,
                                                            double2* __restrict__ Ssel, double2* __restrict__ L,
-                                                           int rows_in = 0) {
+                                                           int rows_in, double scale) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* x = reinterpret_cast<double2*>(smem_raw);
   double2* scratch = x + n;
@@ -212,7 +212,7 @@ __global__ void __launch_bounds__(512) circ_spectra_kernel(const double2* __rest
   }
   __syncthreads();
   fft_block(x, scratch, n, roots, false);
-  for (int i = threadIdx.x; i < n; i += blockDim.x) L[(size_t)q * n + i] = x[fsw(i, n)];
+  for (int i = threadIdx.x; i < n; i += blockDim.x) L[(size_t)q * n + i] = cscale(x[fsw(i, n)], scale);
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -259,20 +259,20 @@ __global__ void __launch_bounds__(512) circ_left_kernel(const T* __restrict__ B,
       }
 #pragma unroll
       for (int u = 0; u < 4; u += 2) {
-        acc = cadd(acc, cmul(lv[u], cscale(xv[u], rs)));
-        acc2 = cadd(acc2, cmul(lv[u + 1], cscale(xv[u + 1], rs)));
+        acc = cmac(acc, lv[u], xv[u]);
+        acc2 = cmac(acc2, lv[u + 1], xv[u + 1]);
       }
     }
     for (; q < k; ++q) {
       int src = p - sel[q];
       if (src < 0) src += n;
-      acc = cadd(acc, cmul(__ldg(L + (size_t)q * n + p), cscale(x[fsw(src, n)], rs)));
+      acc = cmac(acc, __ldg(L + (size_t)q * n + p), x[fsw(src, n)]);
     }
     y[fsw(p, n)] = cadd(acc, acc2);
   }
   __syncthreads();
   fft_block(y, scratch, n, roots, true);
-  for (int p = threadIdx.x; p < n; p += blockDim.x) M[(size_t)p * n + c] = cscale(y[fsw(p, n)], rs);
+  for (int p = threadIdx.x; p < n; p += blockDim.x) M[(size_t)p * n + c] = y[fsw(p, n)];
 }
 
 // ---------------------------------------------------------------------------------------------
@@ -375,8 +375,8 @@ __global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B
       if (p < n) {
         int src = p - sq;
         if (src < 0) src += n;
-        y0[i] = cadd(y0[i], cmul(l[i], cscale(x0[ix(src)], rs)));
-        y1[i] = cadd(y1[i], cmul(l[i], cscale(x1[ix(src)], rs)));
+        y0[i] = cmac(y0[i], l[i], x0[ix(src)]);
+        y1[i] = cmac(y1[i], l[i], x1[ix(src)]);
       }
     }
   }
@@ -393,8 +393,8 @@ __global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B
   fft_block(x0, scratch, n, roots, true);
   fft_block(x1, scratch, n, roots, true);
   for (int p = threadIdx.x; p < n; p += blockDim.x) {
-    M[(size_t)p * ldm + (c0 - col_base)] = cscale(x0[fsw(p, n)], rs);
-    if (two) M[(size_t)p * ldm + (c0 - col_base) + 1] = cscale(x1[fsw(p, n)], rs);
+    M[(size_t)p * ldm + (c0 - col_base)] = x0[fsw(p, n)];
+    if (two) M[(size_t)p * ldm + (c0 - col_base) + 1] = x1[fsw(p, n)];
   }
 }
 
@@ -500,8 +500,8 @@ __global__ void __launch_bounds__(512) circ_right2_kernel(const T* __restrict__ 
         if (p < n) {
           int src = p + sq;
           if (src >= n) src -= n;
-          y0[i] = cadd(y0[i], cmulc(cscale(x0[fsw(src, n)], rs), l[i]));
-          y1[i] = cadd(y1[i], cmulc(cscale(x1[fsw(src, n)], rs), l[i]));
+          y0[i] = cmacc(y0[i], x0[fsw(src, n)], l[i]);
+          y1[i] = cmacc(y1[i], x1[fsw(src, n)], l[i]);
         }
       }
     }
@@ -520,8 +520,8 @@ __global__ void __launch_bounds__(512) circ_right2_kernel(const T* __restrict__ 
   fft_block(x1, scratch, n, roots, true);
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
     double2* pm = M + (size_t)r0 * n + c;
-    *pm = cadd(*pm, cconj(cscale(x0[fsw(c, n)], rs)));
-    if (two) pm[n] = cadd(pm[n], cconj(cscale(x1[fsw(c, n)], rs)));
+    *pm = cadd(*pm, cconj(x0[fsw(c, n)]));
+    if (two) pm[n] = cadd(pm[n], cconj(x1[fsw(c, n)]));
   }
 }
 
@@ -593,21 +593,21 @@ __global__ void __launch_bounds__(512) circ_right_kernel(const T* __restrict__ A
       }
 #pragma unroll
       for (int u = 0; u < 4; u += 2) {
-        acc = cadd(acc, cmulc(cscale(xv[u], rs), lv[u]));
-        acc2 = cadd(acc2, cmulc(cscale(xv[u + 1], rs), lv[u + 1]));
+        acc = cmacc(acc, xv[u], lv[u]);
+        acc2 = cmacc(acc2, xv[u + 1], lv[u + 1]);
       }
     }
     for (; q < kb; ++q) {
       int src = p + selB[q];
       if (src >= n) src -= n;
-      acc = cadd(acc, cmulc(cscale(x[fsw(src, n)], rs), __ldg(LB + (size_t)q * n + src)));
+      acc = cmacc(acc, x[fsw(src, n)], __ldg(LB + (size_t)q * n + src));
     }
     y[fsw(p, n)] = cadd(acc, acc2);
   }
   __syncthreads();
   fft_block(y, scratch, n, roots, true);
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
-    const double2 v = cconj(cscale(y[fsw(c, n)], rs));
+    const double2 v = cconj(y[fsw(c, n)]);
     double2* pm = M + (size_t)r * n + c;
     *pm = cadd(*pm, v);
   }
@@ -1065,7 +1065,10 @@ static int circ_spectra_run(const double2* S, int n, const int* sel, int k, cons
   if (k <= 0) return OK;
   const size_t smem = fft_smem_bytes(n, 1);
   APX_CUDA(cudaFuncSetAttribute(circ_spectra_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  circ_spectra_kernel<<<k, 512, smem, st>>>(S, n, sel, roots, Ssel, L);
+  // L carries both unitary factors of the fused products (rs for the forward and rs for the
+  // inverse transform, an exact power-of-two scale for power-of-two n): the gathers and the
+  // outputs need no scaling of their own
+  circ_spectra_kernel<<<k, 512, smem, st>>>(S, n, sel, roots, Ssel, L, 0, 1.0 / n);
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -1538,9 +1541,9 @@ static int run_circ_rows_phase(int phase, const T* A, const T* B, int n, int k, 
                                st));
       const size_t smem = fft_smem_bytes(n, 1);
       APX_CUDA(cudaFuncSetAttribute(circ_spectra_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-      circ_spectra_kernel<<<k, 512, smem, st>>>(p.Ssel_a, n, sa, p.roots, nullptr, p.L_a, 1);
+      circ_spectra_kernel<<<k, 512, smem, st>>>(p.Ssel_a, n, sa, p.roots, nullptr, p.L_a, 1, 1.0 / n);
       APX_LAUNCH_CHECK();
-      circ_spectra_kernel<<<k, 512, smem, st>>>(p.Ssel_b, n, sb, p.roots, nullptr, p.L_b, 1);
+      circ_spectra_kernel<<<k, 512, smem, st>>>(p.Ssel_b, n, sb, p.roots, nullptr, p.L_b, 1, 1.0 / n);
       APX_LAUNCH_CHECK();
     }
     if (w > 0) {
@@ -1592,6 +1595,7 @@ int apx_circulant_rows_phase(int phase, int dtype, const void* A, const void* B,
                              int64_t row0, int64_t m_rows, int64_t col0, int64_t w_cols, int64_t blk0, int64_t blk1,
                              void* M_rows, void* T1, int32_t* sel_a, int32_t* sel_b, const double* red_in,
                              double* red_out, double* scalars, void* wsp, size_t ws_bytes, void* stream) {
+  APX_NVTX("apx_circulant_rows_phase");
   APX_REQUIRE(phase >= 1 && phase <= 4, "phase must be 1..4");
   APX_REQUIRE(dtype == F64 || dtype == C128, "circulant product: fp64 or complex128 inputs");
   APX_REQUIRE(k >= 0 && k <= n, "k=%d out of range [0, %lld]", k, (long long)n);
@@ -1638,6 +1642,7 @@ size_t apx_circulant_first_order_workspace(int dtype, int64_t n, int k, int orde
 int apx_circulant_first_order(int dtype, const void* A, const void* B, int64_t n, int k, int order,
                               const int32_t* force_sel_a, const int32_t* force_sel_b, void* M, int32_t* sel_a,
                               int32_t* sel_b, double* scalars, void* wsp, size_t ws_bytes, void* stream) {
+  APX_NVTX("apx_circulant_first_order");
   APX_REQUIRE(dtype == F64 || dtype == C128, "circulant product: fp64 or complex128 inputs");
   APX_REQUIRE(k >= 0 && k <= n, "k=%d out of range [0, %lld]", k, (long long)n);
   APX_REQUIRE(order == 0 || order == 1, "order must be 0 or 1");
@@ -1687,6 +1692,7 @@ size_t apx_circulant_decompose_workspace(int dtype, int64_t n) {
 
 int apx_circulant_decompose(int dtype, const void* A, int64_t n, void* columns, double* magnitudes, void* wsp,
                             size_t ws_bytes, void* stream) {
+  APX_NVTX("apx_circulant_decompose");
   APX_REQUIRE(dtype == F64 || dtype == C128, "circulant_decompose: fp64 or complex128 input");
   APX_REQUIRE(n >= 1 && (decompose_fits(n) || big_fft_ok(n)),
               "n=%lld: beyond the shared-memory transforms only powers of two up to 2^18 are supported",
@@ -1794,6 +1800,7 @@ size_t apx_unitary_dft_workspace(int64_t n, int64_t batch) {
 // x[b*dist + i*stride]; forward applies W (e^{-2 pi i pq/n}/sqrt(n)), inverse W*.
 int apx_unitary_dft(const void* x, void* y, int64_t n, int64_t batch, int64_t stride, int64_t dist, int inverse,
                     void* wsp, size_t ws_bytes, void* stream) {
+  APX_NVTX("apx_unitary_dft");
   APX_REQUIRE(n >= 1, "transform length must be >= 1");
   APX_REQUIRE(dft_fits(n) || big_fft_ok(n),
               "transform length %lld: beyond shared memory only powers of two up to 2^18 are supported",

@@ -10,7 +10,20 @@
 #include <algorithm>
 #include <type_traits>
 
+#include <nvtx3/nvToolsExt.h>
+
 namespace apx {
+
+// NVTX range over a C-ABI call (SURVEY.md §5 tracing): host-side push/pop around the enqueue of a
+// product's kernels, visible in Nsight Systems / ncu --nvtx timelines; header-only NVTX3, a no-op
+// unless a tool injects itself.
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+  NvtxRange(const NvtxRange&) = delete;
+  NvtxRange& operator=(const NvtxRange&) = delete;
+};
+#define APX_NVTX(name) ::apx::NvtxRange apx_nvtx_range_(name)
 
 // Grid-shape constant: the B200's SM count, used to size reduction grids, split-K factors and
 // partial-sum buffers. Results (fixed-order sums) depend on these shapes, so they are a constant,

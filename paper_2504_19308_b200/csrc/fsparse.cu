@@ -250,6 +250,7 @@ size_t apx_sfft_first_order_workspace(int64_t m, int64_t n, int64_t p, int k) {
 int apx_sfft_first_order(int dtype, const void* A, const void* B, int64_t m, int64_t n, int64_t p, int k, int order,
                          int sparsify_cols, void* M_, int32_t* sel_a, int32_t* sel_b, double* scal, void* wsp,
                          size_t ws_bytes, void* stream) {
+  APX_NVTX("apx_sfft_first_order");
   APX_REQUIRE(dtype == F64 || dtype == C128, "sfft product: fp64 or complex128 inputs");
   APX_REQUIRE(m >= 1 && n >= 1 && p >= 1, "empty operand");
   APX_REQUIRE(k >= 0, "k=%d must be >= 0", k);
@@ -368,6 +369,7 @@ size_t apx_fourier_row_decompose_workspace(int64_t m, int64_t n) {
 // directions (m x n complex128).
 int apx_fourier_row_decompose(int dtype, const void* A, int64_t m, int64_t n, double* weights, void* directions,
                               void* wsp, size_t ws_bytes, void* stream) {
+  APX_NVTX("apx_fourier_row_decompose");
   APX_REQUIRE(dtype == F64 || dtype == C128, "fourier_row_decompose: fp64 or complex128 input");
   APX_REQUIRE(m >= 1 && n >= 1, "empty matrix");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
@@ -405,6 +407,7 @@ size_t apx_topk_rows_workspace(int64_t rows, int64_t cols) {
 
 int apx_topk_rows(const void* M, int64_t rows, int64_t cols, int k, const int32_t* budget, int32_t* sel, void* vals,
                   void* wsp, size_t ws_bytes, void* stream) {
+  APX_NVTX("apx_topk_rows");
   APX_REQUIRE(rows >= 1 && cols >= 1 && k >= 1, "bad topk_rows arguments");
   cudaStream_t st = reinterpret_cast<cudaStream_t>(stream);
   Workspace ws(wsp, ws_bytes);
