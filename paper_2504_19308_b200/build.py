@@ -16,12 +16,13 @@ import sys
 HERE = os.path.dirname(os.path.abspath(__file__))
 ROOT = os.path.dirname(HERE)
 CSRC = os.path.join(HERE, "csrc")
-OBJ = os.path.join(ROOT, "build", "apx")
-LIB = os.path.join(HERE, "_apx.so")
+CHECKED = os.environ.get("APX_CHECKED", "0") not in ("", "0")  # device bounds checks (APX_DCHECK)
+OBJ = os.path.join(ROOT, "build", "apx_checked" if CHECKED else "apx")
+LIB = os.path.join(HERE, "_apx_checked.so" if CHECKED else "_apx.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 FLAGS = ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC", "--expt-relaxed-constexpr",
-         "-I" + os.path.join(ROOT, "include")]
+         "-I" + os.path.join(ROOT, "include")] + (["-DAPX_CHECKED"] if CHECKED else [])
 
 
 def _headers_mtime() -> float:

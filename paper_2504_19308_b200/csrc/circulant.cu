@@ -88,11 +88,13 @@ __global__ void __launch_bounds__(512) circ_decompose_rows_kernel(const T* __res
                                                                   const double2* __restrict__ roots,
                                                                   double2* __restrict__ St,
                                                                   double* __restrict__ mag2_part, int b_off = 0,
-                                                                  int j_base = 0) {
+                                                                  int j_base = 0, int direct = 0) {
   // b_off / j_base (sharded product): this launch is CTA-blocks [b_off, ...) of the full grid, and
   // X, St hold rows from cycle j_base on; the partials land in the full-grid slots (the caller
   // sums the zero-padded slot arrays over ranks, so mag_finalize sees the single-device layout)
-  X -= (size_t)j_base * n;
+  // direct (real operands, n <= 4096): X is the operand A itself and the cycle rows are read off
+  // its diagonals -- no skewed copy (whose parallelogram tiles read A twice and wrote X once)
+  if (!direct) X -= (size_t)j_base * n;
   St -= (size_t)j_base * n;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* x = reinterpret_cast<double2*>(smem_raw);
@@ -108,20 +110,45 @@ __global__ void __launch_bounds__(512) circ_decompose_rows_kernel(const T* __res
     // loads are in flight (registers) while the current pair is transformed
     if (n <= 8 * 512) {
       double nx0[8], nx1[8];
+      // direct: the thread's unit u is ROW r of A, which holds x_j[(r - j) mod n] and, one column
+      // to the left, x_{j+1}[(r - j - 1) mod n] (usually one 32-byte sector for both)
       auto load_pair = [&](int j) {
 #pragma unroll
         for (int u = 0; u < 8; ++u) {
           const int i = threadIdx.x + u * blockDim.x;
-          nx0[u] = (i < n && j < j1) ? __ldg(X + (size_t)j * n + i) : 0.0;
-          nx1[u] = (i < n && j + 1 < j1) ? __ldg(X + (size_t)(j + 1) * n + i) : 0.0;
+          if (direct) {
+            int c = i - j;
+            if (c < 0) c += n;
+            const int c1 = c == 0 ? n - 1 : c - 1;
+            nx0[u] = (i < n && j < j1) ? __ldg(X + (size_t)i * n + c) : 0.0;
+            nx1[u] = (i < n && j + 1 < j1) ? __ldg(X + (size_t)i * n + c1) : 0.0;
+          } else {
+            nx0[u] = (i < n && j < j1) ? __ldg(X + (size_t)j * n + i) : 0.0;
+            nx1[u] = (i < n && j + 1 < j1) ? __ldg(X + (size_t)(j + 1) * n + i) : 0.0;
+          }
         }
       };
       load_pair(j0);
       for (int j = j0; j < j1; j += 2) {
+        if (direct) {
+          double* xd = reinterpret_cast<double*>(x);
 #pragma unroll
-        for (int u = 0; u < 8; ++u) {
-          const int i = threadIdx.x + u * blockDim.x;
-          if (i < n) x[fsw(i, n)] = make_double2(nx0[u], nx1[u]);
+          for (int u = 0; u < 8; ++u) {
+            const int r = threadIdx.x + u * blockDim.x;
+            if (r < n) {
+              int c = r - j;
+              if (c < 0) c += n;
+              const int c1 = c == 0 ? n - 1 : c - 1;
+              xd[2 * fsw(c, n)] = nx0[u];
+              xd[2 * fsw(c1, n) + 1] = nx1[u];
+            }
+          }
+        } else {
+#pragma unroll
+          for (int u = 0; u < 8; ++u) {
+            const int i = threadIdx.x + u * blockDim.x;
+            if (i < n) x[fsw(i, n)] = make_double2(nx0[u], nx1[u]);
+          }
         }
         __syncthreads();
         if (j + 2 < j1) load_pair(j + 2);
@@ -306,13 +333,22 @@ __global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B
   // real B: the two columns travel as one complex sequence b0 + i b1 through ONE forward
   // transform Z, split afterwards as FB0[p] = (Z[p] + conj Z[-p]) / 2, FB1[p] = (Z[p] - conj Z[-p]) / 2i
   constexpr bool kPack = std::is_same<T, double>::value;
+  // the two real columns of a row are one 16-byte load (c0 even, n even)
+  const bool pair_ld = kPack && two && (n & 1) == 0;
   for (int p0 = threadIdx.x; p0 < n; p0 += 4 * blockDim.x) {
     double2 v0[4], v1[4];
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
       const int p = p0 + u * blockDim.x;
-      v0[u] = p < n ? ld_c<T>(B, (size_t)p * n + c0) : make_double2(0.0, 0.0);
-      v1[u] = (p < n && two) ? ld_c<T>(B, (size_t)p * n + c0 + 1) : make_double2(0.0, 0.0);
+      if (pair_ld) {
+        const double2 b2 = p < n ? __ldg(reinterpret_cast<const double2*>(B + (size_t)p * n + c0))
+                                 : make_double2(0.0, 0.0);
+        v0[u] = make_double2(b2.x, 0.0);
+        v1[u] = make_double2(b2.y, 0.0);
+      } else {
+        v0[u] = p < n ? ld_c<T>(B, (size_t)p * n + c0) : make_double2(0.0, 0.0);
+        v1[u] = (p < n && two) ? ld_c<T>(B, (size_t)p * n + c0 + 1) : make_double2(0.0, 0.0);
+      }
     }
 #pragma unroll
     for (int u = 0; u < 4; ++u) {
@@ -375,6 +411,7 @@ __global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B
       if (p < n) {
         int src = p - sq;
         if (src < 0) src += n;
+        APX_DCHECK(src >= 0 && src < n && sq >= 0 && sq < n);
         y0[i] = cmac(y0[i], l[i], x0[ix(src)]);
         y1[i] = cmac(y1[i], l[i], x1[ix(src)]);
       }
@@ -392,9 +429,18 @@ __global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B
   __syncthreads();
   fft_block(x0, scratch, n, roots, true);
   fft_block(x1, scratch, n, roots, true);
+  // the two complex outputs of a row are adjacent: one 32-byte store (STG.256) when aligned
+  const bool pair_st = two && ((ldm | (c0 - col_base)) & 1) == 0 && ((uintptr_t)M & 31) == 0;
   for (int p = threadIdx.x; p < n; p += blockDim.x) {
-    M[(size_t)p * ldm + (c0 - col_base)] = x0[fsw(p, n)];
-    if (two) M[(size_t)p * ldm + (c0 - col_base) + 1] = x1[fsw(p, n)];
+    double2* dst = M + (size_t)p * ldm + (c0 - col_base);
+    const double2 a = x0[fsw(p, n)], b = x1[fsw(p, n)];
+    if (pair_st) {
+      asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
+                   : "memory");
+    } else {
+      dst[0] = a;
+      if (two) dst[1] = b;
+    }
   }
 }
 
@@ -406,7 +452,7 @@ __global__ void __launch_bounds__(512) circ_right2_kernel(const T* __restrict__ 
                                                           int kb, const double2* __restrict__ roots,
                                                           double2* __restrict__ M,
                                                           const double2* __restrict__ Xpre, int row_base = 0,
-                                                          int row_end = -1) {
+                                                          int row_end = -1, int lin_out = 0) {
   // [row_base, row_end) (sharded product): the CTA pairs cover these rows of term2; M and Xpre
   // hold them from row row_base on (A is the full operand)
   if (row_end < 0) row_end = n;
@@ -473,9 +519,11 @@ __global__ void __launch_bounds__(512) circ_right2_kernel(const T* __restrict__ 
     }
   }
   __syncthreads();
-  // (plain-order transform output, as in circ_left2_kernel, measured 1% slower here)
-  fft_block(x0, scratch, n, roots, false);
-  fft_block(x1, scratch, n, roots, false);
+  // lin_out: the forward transforms end in plain order (fft_linear_ok) so the shifted gathers below
+  // read unaligned runs conflict-free (the XOR swizzle splits them over bank groups)
+  const bool lin = lin_out && fft_linear_ok(n);
+  fft_block(x0, scratch, n, roots, false, lin);
+  fft_block(x1, scratch, n, roots, false, lin);
   // term-major (see circ_left2_kernel): kPP independent L_t loads in flight per term
   double2 y0[kPP], y1[kPP];
 #pragma unroll
@@ -500,8 +548,10 @@ __global__ void __launch_bounds__(512) circ_right2_kernel(const T* __restrict__ 
         if (p < n) {
           int src = p + sq;
           if (src >= n) src -= n;
-          y0[i] = cmacc(y0[i], x0[fsw(src, n)], l[i]);
-          y1[i] = cmacc(y1[i], x1[fsw(src, n)], l[i]);
+          APX_DCHECK(src >= 0 && src < n);
+          const int sx = lin ? src : fsw(src, n);
+          y0[i] = cmacc(y0[i], x0[sx], l[i]);
+          y1[i] = cmacc(y1[i], x1[sx], l[i]);
         }
       }
     }
@@ -982,6 +1032,81 @@ __global__ void __launch_bounds__(256, 2) big_dA_kernel(const T* __restrict__ A,
   }
 }
 
+// Same result as big_dA_kernel with the S_q reads staged through shared memory: for the CTA's
+// 256 columns x kDaRows rows, d = r - c spans one window of 256 + kDaRows - 1 consecutive
+// (cyclic) indices per term, so the k windows (k x 271 x 16 B = 69 KB at k = 16) are loaded once,
+// coalesced, and every thread's 16 reads per term are conflict-free LDS.128 (the lanes' d are
+// consecutive) instead of L2 loads (big_dA_kernel: 74% of its stalls waited on them). The
+// twiddle of (q, c) is loaded one term ahead. k <= kDaWinMaxK (smem).
+constexpr int kDaWinMaxK = 48;
+template <typename T>
+__global__ void __launch_bounds__(256, 2) big_dA_win_kernel(const T* __restrict__ A, int n,
+                                                         const double2* __restrict__ Ssel,
+                                                         const int* __restrict__ sel, int k,
+                                                         const double2* __restrict__ roots,
+                                                         double2* __restrict__ X, int row_base, int row_end) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int W = 256 + kDaRows - 1;
+  double2* win = reinterpret_cast<double2*>(smem_raw);  // k x W
+  // twiddles w_q(c0 + l) = conj(roots[t_q (c0 + l) mod n]), factored as base_q * hi_q[l >> 4] *
+  // lo_q[l & 15]: 33 table loads per term per CTA instead of one scattered load per (term, thread)
+  __shared__ double2 tw_base[kDaWinMaxK], tw_lo[kDaWinMaxK][16], tw_hi[kDaWinMaxK][16];
+  const int tid = threadIdx.x;
+  const int c0 = blockIdx.x * 256;
+  for (int e = tid; e < k * 33; e += blockDim.x) {
+    const int q = e / 33, j = e - q * 33;
+    const int t = sel[q];
+    if (j == 32) tw_base[q] = cconj(__ldg(roots + mulmod_n(t, c0 % n, n)));
+    else if (j < 16) tw_lo[q][j] = cconj(__ldg(roots + mulmod_n(t, j % n, n)));
+    else tw_hi[q][j - 16] = cconj(__ldg(roots + mulmod_n(t, (16 * (j - 16)) % n, n)));
+  }
+  const int r0 = row_base + blockIdx.y * kDaRows;
+  // window j of term q holds S_q[(r0 - c0 - 255 + j) mod n]; thread tid, row rr reads j = 255 - tid + rr
+  int dbase = (r0 - c0 - 255) % n;
+  if (dbase < 0) dbase += n;
+  for (int e = tid; e < k * W; e += blockDim.x) {
+    const int q = e / W, j = e - q * W;
+    int d = dbase + j;
+    if (d >= n) d -= n;
+    win[e] = __ldg(Ssel + (size_t)q * n + d);
+  }
+  __syncthreads();
+  const int c = c0 + tid;
+  if (c >= n) return;
+  double2 ah[kDaRows];
+#pragma unroll
+  for (int rr = 0; rr < kDaRows; ++rr) ah[rr] = make_double2(0.0, 0.0);
+  for (int q = 0; q < k; ++q) {
+    const double2 w = cmul(cmul(tw_base[q], tw_hi[q][tid >> 4]), tw_lo[q][tid & 15]);
+    const double2* wq = win + (size_t)q * W + (255 - tid);
+    APX_DCHECK(255 - tid + kDaRows - 1 < W);
+#pragma unroll
+    for (int rr = 0; rr < kDaRows; ++rr) ah[rr] = cmac(ah[rr], wq[rr], w);
+  }
+#pragma unroll
+  for (int rr = 0; rr < kDaRows; ++rr) {
+    const size_t r = (size_t)r0 + rr;
+    if (r < (size_t)row_end) X[(r - row_base) * n + c] = cconj(csub(ld_c<T>(A, r * n + c), ah[rr]));
+  }
+}
+
+// conj(dA) rows [row_base, row_end) into X (rows from row_base on): the windowed kernel when the
+// k windows fit shared memory, else the L2 kernel
+template <typename T>
+static int launch_big_dA(const T* A, int n, const double2* Ssel, const int* sel, int k, const double2* roots,
+                         double2* X, int row_base, int row_end, cudaStream_t st) {
+  const dim3 grid((unsigned)ceil_div(n, 256), (unsigned)ceil_div(row_end - row_base, kDaRows));
+  if (k <= kDaWinMaxK && n >= 256 && getenv("APX_DA_L2") == nullptr) {
+    const size_t smem = (size_t)std::max(k, 1) * (256 + kDaRows - 1) * sizeof(double2);
+    APX_CUDA(cudaFuncSetAttribute(big_dA_win_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    big_dA_win_kernel<T><<<grid, 256, smem, st>>>(A, n, Ssel, sel, k, roots, X, row_base, row_end);
+  } else {
+    big_dA_kernel<T><<<grid, 256, 0, st>>>(A, n, Ssel, sel, k, roots, X, row_base, row_end);
+  }
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
 // term2: Y[r][p] = sum_q (rs * X[r][(p + s_q) % n]) * conj(L_q[(p + s_q) % n])
 __global__ void __launch_bounds__(256) big_right_gather_kernel(const double2* __restrict__ X, int n,
                                                                const double2* __restrict__ L, const int* __restrict__ sel,
@@ -1044,16 +1169,32 @@ static void plan_circ(Workspace& ws, CircPlan& p, int n, int k, bool need_sa_ful
   p.red = ws.take<double>(4 * kNumSMs + 64);
 }
 
+// term2's forward transforms in plain order (APX_R2_SWIZZLED=1: the XOR-swizzled order, A/B)
+static int right2_linear() {
+  static const int v = getenv("APX_R2_SWIZZLED") == nullptr ? 1 : 0;
+  return v;
+}
+
+// real operands whose transform runs in the packed-pair branch read the diagonals directly
+template <typename T>
+static int decompose_direct(int n) {
+  static const bool off = getenv("APX_CIRC_SKEW") != nullptr;  // A/B switch: the skewed-copy path
+  return std::is_same<T, double>::value && n <= 8 * 512 && !off;
+}
+
 // S^T (St[j][t] = S[t][j]) and the magnitudes; `skew` is n x n scratch of T
 template <typename T>
 static int circ_decompose_run(const T* A, int n, const CircPlan& p, double2* St, double* mag, T* skew,
                               cudaStream_t st) {
   const size_t smem = fft_smem_bytes(n, 1) + (size_t)n * sizeof(double);
-  circ_skew_kernel<T><<<dim3((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32)), 256, 0, st>>>(A, n, skew);
-  APX_LAUNCH_CHECK();
+  const int direct = decompose_direct<T>(n);
+  if (!direct) {
+    circ_skew_kernel<T><<<dim3((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32)), 256, 0, st>>>(A, n, skew);
+    APX_LAUNCH_CHECK();
+  }
   auto fn = circ_decompose_rows_kernel<T>;
   APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  fn<<<p.parts, 512, smem, st>>>(skew, n, p.cpc, p.roots, St, p.part, 0, 0);
+  fn<<<p.parts, 512, smem, st>>>(direct ? A : skew, n, p.cpc, p.roots, St, p.part, 0, 0, direct);
   APX_LAUNCH_CHECK();
   mag_finalize_kernel<<<(unsigned)ceil_div(n, 32), 256, 0, st>>>(p.part, p.parts, n, mag);
   APX_LAUNCH_CHECK();
@@ -1118,12 +1259,10 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
         return e != nullptr && atoi(e) != 0;
       }();
       if (!inline_da && n >= kDaRows) {  // (big_dA_kernel wraps d0 + rr < 2n once)
-        big_dA_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)ceil_div(n, kDaRows)), 256, 0, st>>>(
-            A, n, p.Ssel_a, sa, k, p.roots, p.S_a);
-        APX_LAUNCH_CHECK();
+        APX_TRY(launch_big_dA<T>(A, n, p.Ssel_a, sa, k, p.roots, p.S_a, 0, n, st));
         Xpre = p.S_a;
       }
-      fn<<<(unsigned)ceil_div(n, 2), 512, smem, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M, Xpre, 0, (int)n);
+      fn<<<(unsigned)ceil_div(n, 2), 512, smem, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M, Xpre, 0, (int)n, right2_linear());
     } else {
       auto fn = circ_right_kernel<T>;
       APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1399,9 +1538,7 @@ static int run_circulant_big(const T* A, const T* B, int n, int k, int order, co
   stage_mark(2, st);
   if (order == 1) {
     // term2 = dA . Bhat, row-local: conj(dA) rows, FFT, gather with conj(L_B), inverse FFT, conj
-    big_dA_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)ceil_div(n, kDaRows)), 256, 0, st>>>(
-        A, n, p.Ssel_a, sa, k, p.rootsn, p.W1);
-    APX_LAUNCH_CHECK();
+    APX_TRY(launch_big_dA<T>(A, n, p.Ssel_a, sa, k, p.rootsn, p.W1, 0, n, st));
     APX_TRY(big_fft_rows<double2>(p.f, p.W1, p.W1, p.W2, n, false, 1.0, st));
     big_right_gather_kernel<<<gather_grid, 256, 0, st>>>(p.W2, n, p.L_b, sb, k, rs, p.W1);
     APX_LAUNCH_CHECK();
@@ -1445,6 +1582,7 @@ __global__ void circ_sel_extract_kernel(const double2* __restrict__ St, int n, i
   const size_t total = (size_t)k * n;
   for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < total; e += (size_t)gridDim.x * blockDim.x) {
     const int q = (int)(e / n), j = (int)(e % n);
+    APX_DCHECK(sel[q] >= 0 && sel[q] < n);
     out[e] = (j >= j_lo && j < j_hi) ? St[(size_t)(j - j_lo) * n + sel[q]] : make_double2(0.0, 0.0);
   }
 }
@@ -1498,11 +1636,14 @@ static int run_circ_rows_phase(int phase, const T* A, const T* B, int n, int k, 
     APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     for (int o = 0; o < 2; ++o) {
       if (p.j_hi > p.j_lo) {
-        circ_skew_kernel<T><<<dim3((unsigned)ceil_div(n, 32), (unsigned)ceil_div(p.j_hi - p.j_lo, 32)), 256, 0, st>>>(
-            ops[o], n, (T*)p.skew, p.j_lo, p.j_hi);
-        APX_LAUNCH_CHECK();
-        fn<<<blk1 - blk0, 512, smem, st>>>((const T*)p.skew, n, p.cpc, p.roots, Sts[o],
-                                           red_out + (size_t)o * p.parts * n, blk0, p.j_lo);
+        const int direct = decompose_direct<T>(n);
+        if (!direct) {
+          circ_skew_kernel<T><<<dim3((unsigned)ceil_div(n, 32), (unsigned)ceil_div(p.j_hi - p.j_lo, 32)), 256, 0,
+                                st>>>(ops[o], n, (T*)p.skew, p.j_lo, p.j_hi);
+          APX_LAUNCH_CHECK();
+        }
+        fn<<<blk1 - blk0, 512, smem, st>>>(direct ? ops[o] : (const T*)p.skew, n, p.cpc, p.roots, Sts[o],
+                                           red_out + (size_t)o * p.parts * n, blk0, p.j_lo, direct);
         APX_LAUNCH_CHECK();
       }
     }
@@ -1556,13 +1697,11 @@ static int run_circ_rows_phase(int phase, const T* A, const T* B, int n, int k, 
   }
   // phase 4: term2 on this rank's rows (M_rows holds term1's rows, assembled by the caller)
   if (order == 1 && m > 0) {
-    big_dA_kernel<T><<<dim3((unsigned)ceil_div(n, 256), (unsigned)ceil_div(m, kDaRows)), 256, 0, st>>>(
-        A, n, p.Ssel_a, sa, k, p.roots, p.Xpre, row0, row0 + m);
-    APX_LAUNCH_CHECK();
+    APX_TRY(launch_big_dA<T>(A, n, p.Ssel_a, sa, k, p.roots, p.Xpre, row0, row0 + m, st));
     auto fn = circ_right2_kernel<T>;
     APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     fn<<<(unsigned)ceil_div(m, 2), 512, smem2, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M_rows, p.Xpre,
-                                                     row0, row0 + m);
+                                                     row0, row0 + m, right2_linear());
     APX_LAUNCH_CHECK();
   }
   int parts = 0;

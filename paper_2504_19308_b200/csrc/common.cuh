@@ -45,6 +45,26 @@ inline int device_sms() {
   return cache[dev];
 }
 
+// Device-side bounds checks of the checked build (APX_CHECKED=1 python -m
+// paper_2504_19308_b200.build -> _apx_checked.so, selected with APX_LIB): a failed check prints the
+// condition and location and traps, so the calling test fails loudly. compute-sanitizer is closed
+// on this pool; these checks on the index computations of the main kernels, run over small cases
+// of every path (tools/sanitize_cases.py) and the parity tests, stand in for memcheck.
+#ifdef APX_CHECKED
+#define APX_DCHECK(cond)                                                                            \
+  do {                                                                                              \
+    if (!(cond)) {                                                                                  \
+      printf("APX_DCHECK failed: %s at %s:%d (block %d,%d thread %d)\n", #cond, __FILE__, __LINE__, \
+             (int)blockIdx.x, (int)blockIdx.y, (int)threadIdx.x);                                  \
+      __trap();                                                                                     \
+    }                                                                                               \
+  } while (0)
+#else
+#define APX_DCHECK(cond) \
+  do {                   \
+  } while (0)
+#endif
+
 // dtype codes used across the C-ABI (include/apx.h)
 enum DType : int { F32 = 0, F64 = 1, C64 = 2, C128 = 3 };
 

@@ -367,6 +367,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
     if (blk >= nblk) break;
     const int r0 = blk * R;
     const int rows = min(R, m_rows - r0);
+    APX_DCHECK(rows > 0 && rows <= R);
     // coalesced row reads, interleaved shared-memory writes; rows past the end are zero.
     // The row block is read in batches of 16-byte vectors with all RP rows' loads issued before
     // any is stored, so a CTA pays ~one DRAM latency per batch instead of one per element.
@@ -484,6 +485,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
               // (c + jt) mod n as an unsigned min: c + jt - n wraps above c + jt unless c + jt >= n
               unsigned m = (unsigned)(c + jt);
               m = min(m, m - (unsigned)n);
+              APX_DCHECK(m < (unsigned)n && jt >= 0 && jt < n);
               mm[u][q] = (int)m;
               lv[u][q] = ldg_nc_ordered(lrow + c);
               if constexpr (TRUNC) lv[u][q] = tf32_trunc(lv[u][q]);

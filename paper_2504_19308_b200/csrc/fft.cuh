@@ -130,6 +130,7 @@ __device__ inline void fft_block(double2* x, double2* scratch, int n, const doub
       const int i = bitrev_order(e, logn);
       const int j = (int)(__brev((unsigned)i) >> (32 - logn));
       if (i < j) {
+        APX_DCHECK(i < n && j < n);
         const double2 t = x[fsw(i, n)];
         x[fsw(i, n)] = x[fsw(j, n)];
         x[fsw(j, n)] = t;
@@ -165,6 +166,7 @@ __device__ inline void fft_block(double2* x, double2* scratch, int n, const doub
         const int pos = g & (h - 1);
         const int base = (g >> (s - 1)) << (s + 2);
         double2 v[8];
+        APX_DCHECK(base + pos + 7 * h < n);
 #pragma unroll
         for (int m = 0; m < 8; ++m) v[m] = x[fsw(base + pos + m * h, n)];
         radix8_apply(v, radix8_twiddles(roots, pos << (logn - s - 2), inverse));

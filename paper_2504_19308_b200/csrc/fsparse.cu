@@ -40,6 +40,7 @@ __global__ void scatter_kept_kernel(const double2* __restrict__ X, int rows, int
     const int b = e / k, q = e - b * k;
     const int j = sel[(size_t)b * k + q];
     double2 v = make_double2(0.0, 0.0);
+    APX_DCHECK(j < (by_cols ? rows : cols));
     if (j >= 0) {
       const size_t idx = by_cols ? (size_t)j * cols + b : (size_t)b * cols + j;
       v = X[idx];
@@ -90,6 +91,7 @@ __global__ void __launch_bounds__(256) sparse_rows_gemm_kernel(const int* __rest
       for (int q = 0; q < qn; ++q) {
         const int j = sj[q];
         if (j < 0) continue;
+        APX_DCHECK(q < kSpTile);
         const double2 v = sv[q];
         const double2* xr = X + (size_t)j * p;
 #pragma unroll

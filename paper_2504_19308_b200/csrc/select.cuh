@@ -161,6 +161,7 @@ __device__ inline void topk_select_block(const double* __restrict__ w, int n, in
         const unsigned long long key = kr[q] & M;
         bool take = key > T;
         if (key == T) { take = e < krem; ++e; }
+        APX_DCHECK(!take || pos < k);
         if (take) sel[pos++] = lo + q;
       }
   } else {
@@ -168,6 +169,7 @@ __device__ inline void topk_select_block(const double* __restrict__ w, int n, in
       unsigned long long key = dkey(w[i]) & M;
       bool take = key > T;
       if (key == T) { take = e < krem; ++e; }
+      APX_DCHECK(!take || pos < k);
       if (take) sel[pos++] = i;
     }
   }

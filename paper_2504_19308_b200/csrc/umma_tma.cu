@@ -135,6 +135,7 @@ __global__ void __launch_bounds__(kThreads, 1)
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int m0 = blockIdx.y * BM, n0 = blockIdx.x * BN;
+  APX_DCHECK(m0 < M && n0 < N);
   const int kz = blockIdx.z;
   const int kbeg = kz * k_per_split, kend = min(K, kbeg + k_per_split);
   const int ktiles = (int)ceil_div(max(0, kend - kbeg), BK);
@@ -332,6 +333,7 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     if (deferred && et == 0) {
       const int slot = atomicAdd(defer, 1);
+      APX_DCHECK(slot < (int)(gridDim.x * gridDim.y * gridDim.z));
       defer[1 + slot] = ((int)blockIdx.z * (int)gridDim.y + (int)blockIdx.y) * (int)gridDim.x + (int)blockIdx.x;
     }
     const int quarter = warp & 3;
