@@ -375,6 +375,17 @@ static int gather_ctas(int nblk) {
   return std::max(1, std::min(nblk, device_sms() - kMinFreeSMs));
 }
 
+// SM budget the Y = A Omega GEMM sizes its K split for (APX_Y_SMS, tuning knob). Default 64: two
+// K slices (128 CTAs) -- Y starts before the gather holds its SMs (tools/c4_sweep.sh: 978 vs 963
+// products/s for 32, the round-1 setting, and 967 for 148)
+static int y_sm_budget() {
+  static const int v = [] {
+    const char* e = getenv("APX_Y_SMS");
+    return e ? std::max(1, atoi(e)) : 64;
+  }();
+  return v;
+}
+
 // Stage markers (bench.py): 0 start | hi: 1 B decomposed, 2 gather done | lo: 3 Y, 4 QR, 5 Bm,
 // 9 W GEMM, 6 W correction, 7 M += Q.W (order 1; on the main stream after the join for order 0)
 // | main: 8 end.
@@ -429,7 +440,7 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
   // finder then fits on the SMs the persistent gather leaves free
   // (waiting for the extraction instead -- Y entirely after B's stage -- measured the same)
   APX_CUDA(cudaStreamWaitEvent(lo, ss->b_read, 0));
-  APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, lo, 32));  // 64 CTAs
+  APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, lo, y_sm_budget()));
   stage_mark(3, lo);
   APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, lo, /*tf32=*/1)));
   for (int it = 0; it < q; ++it) {

@@ -318,7 +318,8 @@ template <typename T>
 __global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B, int n, const double2* __restrict__ L,
                                                          const int* __restrict__ sel, int k,
                                                          const double2* __restrict__ roots, double2* __restrict__ M,
-                                                         int col_base = 0, int col_end = -1, int64_t ldm = -1) {
+                                                         int col_base = 0, int col_end = -1, int64_t ldm = -1,
+                                                         int stage_l = 0) {
   if (col_end < 0) col_end = n;
   if (ldm < 0) ldm = n;
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -327,6 +328,31 @@ __global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B
   double2* scratch = x1 + n;
   int* s_sel = reinterpret_cast<int*>(scratch + (is_pow2(n) ? 0 : n));
   for (int q = threadIdx.x; q < k; q += blockDim.x) s_sel[q] = sel[q];
+  // stage_l (n == 2 * kPP/2 * blockDim): the L_t rows reach shared memory by bulk async copies, in
+  // half rows (positions i < kPP/2 of every thread lie in the first half), double-buffered and
+  // started before the transform, so the gather's L reads are conflict-free shared loads instead
+  // of L2 round trips (its largest stall). Stage s = (term s / 2, half s % 2) uses buffer s % 2.
+  const int half = n / 2;
+  double2* Lb = reinterpret_cast<double2*>(
+      (reinterpret_cast<uintptr_t>(s_sel + k) + 127) & ~static_cast<uintptr_t>(127));
+  uint64_t* lbar = reinterpret_cast<uint64_t*>(Lb + 2 * half);
+  const bool stage = stage_l && k > 0;
+  auto issue = [&](int st) {
+    const uint32_t bytes = (uint32_t)(half * sizeof(double2));
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&lbar[st & 1]);
+    const uint32_t dst = (uint32_t)__cvta_generic_to_shared(Lb + (st & 1) * half);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(bar), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(dst),
+                 "l"(L + (size_t)(st >> 1) * n + (st & 1) * half), "r"(bytes), "r"(bar)
+                 : "memory");
+  };
+  if (stage && threadIdx.x == 0) {
+    for (int b = 0; b < 2; ++b)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&lbar[b])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    issue(0);
+    if (2 * k > 1) issue(1);
+  }
   const int c0 = col_base + 2 * blockIdx.x;
   const bool two = c0 + 1 < col_end;
   const double rs = rsqrt((double)n);
@@ -396,7 +422,40 @@ __global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B
   double2 y0[kPP], y1[kPP];
 #pragma unroll
   for (int i = 0; i < kPP; ++i) y0[i] = y1[i] = make_double2(0.0, 0.0);
-  for (int q = 0; q < k; ++q) {
+  if (stage) {
+    auto half_terms = [&](const double2* Lh, int sq, auto ibase) {
+      constexpr int I0 = decltype(ibase)::value;
+#pragma unroll
+      for (int i = I0; i < I0 + kPP / 2; ++i) {
+        const int p = threadIdx.x + i * blockDim.x;
+        int src = p - sq;
+        if (src < 0) src += n;
+        APX_DCHECK(src >= 0 && src < n && p - I0 * (int)blockDim.x < half);
+        const double2 l = Lh[p - I0 * blockDim.x];
+        y0[i] = cmac(y0[i], l, x0[ix(src)]);
+        y1[i] = cmac(y1[i], l, x1[ix(src)]);
+      }
+    };
+    for (int st = 0; st < 2 * k; ++st) {
+      const int b = st & 1;
+      const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&lbar[b]);
+      const uint32_t ph = (uint32_t)((st >> 1) & 1);
+      asm volatile(
+          "{\n.reg .pred p;\nLW_%=:\n"
+          "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+          "@!p bra LW_%=;\n}\n" ::"r"(bar),
+          "r"(ph)
+          : "memory");
+      const int sq = s_sel[st >> 1];
+      if (b == 0)
+        half_terms(Lb, sq, std::integral_constant<int, 0>());
+      else
+        half_terms(Lb + half, sq, std::integral_constant<int, kPP / 2>());
+      __syncthreads();  // buffer b drained
+      if (threadIdx.x == 0 && st + 2 < 2 * k) issue(st + 2);
+    }
+  }
+  for (int q = 0; q < k && !stage; ++q) {
     const int sq = s_sel[q];
     const double2* Lq = L + (size_t)q * n;
     double2 l[kPP];
@@ -1169,6 +1228,16 @@ static void plan_circ(Workspace& ws, CircPlan& p, int n, int k, bool need_sa_ful
   p.red = ws.take<double>(4 * kNumSMs + 64);
 }
 
+// term1's L rows staged in shared memory by bulk async copies (circ_left2_kernel stage_l; n = 4096:
+// kPP positions of 512 threads, halves = the threads' first / second kPP/2 positions). Measured
+// neutral to slightly slower at C3 (0.704 vs 0.684 ms: the gather is not waiting on L2 for L), so
+// it is off by default; APX_L2_STAGE=1 turns it on (A/B).
+static int left2_stage_l(int n, int k) {
+  static const bool on = getenv("APX_L2_STAGE") != nullptr;
+  return on && n == kPP * 512 && k > 0;
+}
+static size_t left2_stage_bytes(int n) { return 128 + (size_t)n * sizeof(double2) + 2 * sizeof(uint64_t); }
+
 // term2's forward transforms in plain order (APX_R2_SWIZZLED=1: the XOR-swizzled order, A/B)
 static int right2_linear() {
   static const int v = getenv("APX_R2_SWIZZLED") == nullptr ? 1 : 0;
@@ -1238,8 +1307,11 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
   const bool pairs = n >= 2 && n <= kPP * 512;  // two columns / rows per CTA (same smem footprint)
   if (pairs) {
     auto fn = circ_left2_kernel<T>;
-    APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<(unsigned)ceil_div(n, 2), 512, smem, st>>>(B, n, p.L_a, sa, k, p.roots, M, 0, (int)n, (int64_t)n);
+    const int stage_l = left2_stage_l(n, k);
+    const size_t smem_l = smem + (stage_l ? left2_stage_bytes(n) : 0);
+    APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_l));
+    fn<<<(unsigned)ceil_div(n, 2), 512, smem_l, st>>>(B, n, p.L_a, sa, k, p.roots, M, 0, (int)n, (int64_t)n,
+                                                      stage_l);
     APX_LAUNCH_CHECK();
   } else {
     auto fn = circ_left_kernel<T>;
@@ -1690,7 +1762,11 @@ static int run_circ_rows_phase(int phase, const T* A, const T* B, int n, int k, 
     if (w > 0) {
       auto fn = circ_left2_kernel<T>;
       APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-      fn<<<(unsigned)ceil_div(w, 2), 512, smem2, st>>>(B, n, p.L_a, sa, k, p.roots, T1, col0, col0 + w, (int64_t)w);
+      const int stage_l = left2_stage_l(n, k);
+      const size_t smem_l = smem2 + (stage_l ? left2_stage_bytes(n) : 0);
+      APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_l));
+      fn<<<(unsigned)ceil_div(w, 2), 512, smem_l, st>>>(B, n, p.L_a, sa, k, p.roots, T1, col0, col0 + w, (int64_t)w,
+                                                        stage_l);
       APX_LAUNCH_CHECK();
     }
     return OK;

@@ -640,6 +640,185 @@ __global__ void __launch_bounds__(1024) householder_qr_kernel(const TI* __restri
   }
 }
 
+// ---- fused CholeskyQR2 for sketches that fit one CTA's shared memory (C1: 512 x 40 fp64) ----------
+// One CTA (512 threads) does both passes of CholeskyQR2 with Y resident in shared memory (row-major,
+// pitch LP = 4 * ceil(l / 4) + 2 doubles: an odd number of 16-byte granules, so the lanes' rows
+// spread over the bank groups):
+//   Gram      4 x 4 register blocks of the upper block triangle, S row slices per block pair in S
+//             consecutive lanes, reduced by a fixed xor-shuffle tree (16 FMAs per 4 LDS.128);
+//   Cholesky  right-looking over all threads, two barriers per pivot; the trailing update walks a
+//             pair table that lists the triangle from the last row up, so step p's entries are the
+//             table's first (l-p-1)(l-p)/2 (one per thread);
+//   R^{-1}    rows from the bottom, each row's entries in parallel (4 lanes per entry);
+//   apply     Q = Y R^{-1} row-locally in place: thread = row, column chunks of 8 from the last
+//             down (chunk c only reads Y columns <= its own, R^{-1} being upper triangular), 8
+//             accumulators in registers, each Y value (LDS.64) against a broadcast row of R^{-1}.
+// (A one-warp Cholesky and R^{-1} were a serial chain: 47% of the kernel's stalls sat at the barrier
+// waiting for them.)
+// The ten kernels of the unfused path (Gram partials and reduce, Cholesky-inverse, apply, twice, plus
+// the flag reset) become one; the 4 l eps max(diag G) breakdown rule and the Householder fallback
+// (the kernel launched after, gated by the flag) are those of cholinv64_kernel.
+constexpr int kSmallQRThreads = 512;
+constexpr int kSmallQRMaxL = 64;
+static int small_lp(int l) { return 4 * (int)ceil_div(l, 4) + 2; }
+size_t qr_small_smem(int m, int l) {
+  return ((size_t)m * small_lp(l) + 2 * (size_t)l * l + l + 1) * sizeof(double) +
+         (size_t)l * (l + 1) / 2 * sizeof(int);
+}
+bool qr_small_fits(int m, int l) {
+  return l <= kSmallQRMaxL && m <= kSmallQRThreads && m > 2 * l && qr_small_smem(m, l) <= 220 * 1024;
+}
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(kSmallQRThreads) qr_small_kernel(const TI* __restrict__ Y, int64_t rs, int64_t cs,
+                                                                   int m, int l, int* __restrict__ flag,
+                                                                   TO* __restrict__ Q, int64_t qrs, int64_t qcs,
+                                                                   TO* __restrict__ Q2, int64_t q2rs, int64_t q2cs,
+                                                                   int tf32) {
+  extern __shared__ __align__(16) double qs_smem[];
+  const int LB = (int)ceil_div(l, 4), LP = 4 * LB + 2;
+  double* Ys = qs_smem;                  // m x LP, row-major
+  double* G = Ys + (size_t)m * LP;       // l x l: Gram, then R in the upper triangle
+  double* X = G + (size_t)l * l;         // l x l: R^{-1} (upper triangle), row-major
+  double* rdiag = X + (size_t)l * l;     // 1 / R[j][j] (+ the breakdown tolerance at [l])
+  int* pairs = reinterpret_cast<int*>(rdiag + l + 1);
+  __shared__ int s_bad;
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < m * LP; e += blockDim.x) {
+    const int r = e / LP, i = e - r * LP;
+    Ys[e] = i < l ? (double)Y[(size_t)r * rs + (size_t)i * cs] : 0.0;
+  }
+  for (int e = tid; e < l * (l + 1) / 2; e += blockDim.x) {
+    int i = l - 1, rem = e;  // row l-1 has 1 entry, row l-2 has 2, ...
+    while (rem >= l - i) { rem -= l - i; --i; }
+    pairs[e] = (i << 8) | (i + rem);
+  }
+  if (tid == 0) s_bad = 0;
+  // block pairs (I <= J) and row slices per pair (a power of two <= 32)
+  const int npb = LB * (LB + 1) / 2;
+  int S = 1;
+  while (S < 32 && 2 * S * npb <= (int)blockDim.x) S *= 2;
+  __syncthreads();
+  for (int pass = 0; pass < 2; ++pass) {
+    // ---- Gram (upper block triangle) ----
+    const int pr = tid / S, sl = tid - pr * S;
+    int I = 0, J = 0;
+    if (pr < npb) {
+      int rem = pr;
+      while (rem >= LB - I) { rem -= LB - I; ++I; }
+      J = I + rem;
+    }
+    double acc[4][4];
+#pragma unroll
+    for (int a = 0; a < 4; ++a)
+#pragma unroll
+      for (int b = 0; b < 4; ++b) acc[a][b] = 0.0;
+    if (pr < npb) {
+      for (int r = sl; r < m; r += S) {
+        const double2* row = reinterpret_cast<const double2*>(Ys + (size_t)r * LP);
+        const double2 a01 = row[2 * I], a23 = row[2 * I + 1], b01 = row[2 * J], b23 = row[2 * J + 1];
+        const double av[4] = {a01.x, a01.y, a23.x, a23.y}, bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+        for (int a = 0; a < 4; ++a)
+#pragma unroll
+          for (int b = 0; b < 4; ++b) acc[a][b] = fma(av[a], bv[b], acc[a][b]);
+      }
+    }
+    // the S lanes of a pair are consecutive and aligned: a fixed xor tree over them
+    for (int o = 1; o < S; o <<= 1) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) acc[a][b] += __shfl_xor_sync(0xffffffffu, acc[a][b], o);
+    }
+    if (pr < npb && sl == 0) {
+#pragma unroll
+      for (int a = 0; a < 4; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) {
+          const int i = 4 * I + a, j = 4 * J + b;
+          if (i <= j && j < l) G[i * l + j] = acc[a][b];
+        }
+    }
+    __syncthreads();
+    // ---- Cholesky (right-looking, all threads: two barriers per pivot) ----
+    if (tid < 32) {
+      double md = 0.0;
+      for (int i = lane; i < l; i += 32) md = fmax(md, G[i * l + i]);
+      for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
+      if (lane == 0) rdiag[l] = 4.0 * l * 2.220446049250313e-16 * md;  // breakdown tolerance
+    }
+    __syncthreads();
+    const double tol = rdiag[l];
+    for (int p = 0; p < l; ++p) {
+      double piv = G[p * l + p];
+      if (!(piv > tol)) {
+        if (tid == 0) s_bad = 1;
+        piv = 1.0;
+      }
+      const double rsq = rsqrt(piv);
+      __syncthreads();  // every thread has read the pivot
+      for (int j = p + 1 + tid; j < l; j += blockDim.x) G[p * l + j] *= rsq;
+      if (tid == 0) {
+        G[p * l + p] = piv * rsq;
+        rdiag[p] = rsq;
+      }
+      __syncthreads();
+      const int T = (l - p - 1) * (l - p) / 2;
+      for (int e = tid; e < T; e += blockDim.x) {
+        const int ij = pairs[e], i = ij >> 8, j = ij & 255;
+        G[i * l + j] = fma(-G[p * l + i], G[p * l + j], G[i * l + j]);
+      }
+    }
+    __syncthreads();
+    if (s_bad) {
+      if (tid == 0) *flag = 1;  // the Householder kernel recomputes Q
+      return;
+    }
+    // ---- X = R^{-1} (upper), rows from the bottom: X[i][j] = -rdiag[i] sum_{q=i+1..j} R[i][q] X[q][j];
+    // row i's entries are independent, each summed by 4 lanes (fixed xor tree) ----
+    for (int i = l - 1; i >= 0; --i) {
+      const int j = i + (tid >> 2), part = tid & 3;
+      double t = 0.0;
+      if (j < l && j > i)
+        for (int q = i + 1 + part; q <= j; q += 4) t = fma(G[i * l + q], X[q * l + j], t);
+      t += __shfl_xor_sync(0xffffffffu, t, 1);
+      t += __shfl_xor_sync(0xffffffffu, t, 2);
+      if (part == 0 && j < l) X[i * l + j] = j == i ? rdiag[i] : -t * rdiag[i];
+      __syncthreads();
+    }
+    // ---- apply: row r of Q = row r of Y times R^{-1}, in place. The row is the thread's alone, and
+    // the column chunks of 8 go from the last down: chunk c reads Y columns <= its own (X upper
+    // triangular), all still unwritten ----
+    if (tid < m) {
+      double* yr = Ys + (size_t)tid * LP;
+      for (int c0 = 8 * ((l - 1) >> 3); c0 >= 0; c0 -= 8) {
+        double qv[8];
+#pragma unroll
+        for (int u = 0; u < 8; ++u) qv[u] = 0.0;
+        const int kend = min(l, c0 + 8);
+        for (int k = 0; k < kend; ++k) {
+          const double y = yr[k];
+          const double* xk = X + k * l + c0;
+#pragma unroll
+          for (int u = 0; u < 8; ++u)
+            if (c0 + u < l && c0 + u >= k) qv[u] = fma(y, xk[u], qv[u]);
+        }
+#pragma unroll
+        for (int u = 0; u < 8; ++u)
+          if (c0 + u < l) yr[c0 + u] = qv[u];
+      }
+    }
+    __syncthreads();
+  }
+  for (int e = tid; e < m * l; e += blockDim.x) {
+    const int r = e / l, i = e - r * l;
+    const double v = Ys[(size_t)r * LP + i];
+    Q[(size_t)r * qrs + (size_t)i * qcs] = qout<TO>(v, tf32);
+    if (Q2) Q2[(size_t)r * q2rs + (size_t)i * q2cs] = qout<TO>(v, tf32);
+  }
+}
+
 __global__ void reset_flag_kernel(int* flag, int v) { *flag = v; }
 __global__ void flag_to_double_kernel(const int* flag, double* out) { *out = (double)*flag; }
 
@@ -741,7 +920,19 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
   const bool householder_only = method == 1 || m <= 2 * l || l > kMaxL;
   reset_flag_kernel<<<1, 1, 0, st>>>(flag, householder_only ? 1 : 0);
   APX_LAUNCH_CHECK();
-  if (!householder_only && l <= 64) {
+  // APX_QR_FUSED=1: fp64 sketches that fit one CTA take the fused CholeskyQR2 (qr_small_kernel). It
+  // is off by default: one CTA runs the O(m l^2) work latency-bound on a single SM, 160 us per QR
+  // at 512 x 40 against ~110 us for the unfused chain whose Gram and apply kernels spread over the
+  // SMs (C1: 2.98 vs 2.38 ms per product, batched 7.9k vs 10.1k products/s).
+  static const bool fused = getenv("APX_QR_FUSED") != nullptr;
+  const bool small = fused && !householder_only && sizeof(TO) == 8 && qr_small_fits(m, l);
+  if (small) {
+    const size_t smem = qr_small_smem(m, l);
+    APX_CUDA(cudaFuncSetAttribute(qr_small_kernel<TI, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    qr_small_kernel<TI, TO><<<1, kSmallQRThreads, smem, st>>>(Y, rs, cs, m, l, flag, Q, qrs, qcs, Q2, q2rs, q2cs,
+                                                               tf32);
+    APX_LAUNCH_CHECK();
+  } else if (!householder_only && l <= 64) {
     // fast path: CholeskyQR with R^{-1}; second pass only when the conditioning requires it
     int* skip2 = flag + 1;
     const double skip_kappa = sizeof(TO) == 4 ? 3.0e4 : 0.0;
