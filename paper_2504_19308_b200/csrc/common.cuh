@@ -130,7 +130,12 @@ inline cudaError_t launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, s
   attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
   attr[0].val.programmaticStreamSerializationAllowed = 1;
   cfg.attrs = attr;
-  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  // inside a CUDA-graph capture (batch.GraphBatch: many independent products on concurrent
+  // streams) launch gaps are already gone, and early-launched dependents would hold SM slots the
+  // other products' kernels need (C1 batched: 8.3k vs 10.1k products/s), so capture uses plain edges
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  const bool capturing = cudaStreamIsCapturing(st, &cap) == cudaSuccess && cap != cudaStreamCaptureStatusNone;
+  cfg.numAttrs = (pdl_enabled() && !capturing) ? 1 : 0;
   return cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...);
 }
 

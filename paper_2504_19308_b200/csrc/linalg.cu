@@ -68,6 +68,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) gram_partial_kernel(const T* __restrict__ Y, int64_t rs, int64_t cs, int m,
                                                            int l, const int* __restrict__ skip,
                                                            double* __restrict__ part) {
+  pdl_trigger();  // programmatic dependent launch: the next QR stage may start launching
+  pdl_wait();
   if (skip && *skip) return;
   __shared__ __align__(16) double Ys[64][kTP];  // [r][i]
   load_tile64<false>(Y, rs, cs, m, l, blockIdx.x * 64, Ys);
@@ -107,6 +109,8 @@ template <typename T>
 __global__ void __launch_bounds__(256) gram_partial_wide_kernel(const T* __restrict__ Y, int64_t rs, int64_t cs, int m,
                                                            int l, int rows_per, const int* __restrict__ skip,
                                                            double* __restrict__ part) {
+  pdl_trigger();  // programmatic dependent launch: the next QR stage may start launching
+  pdl_wait();
   if (skip && *skip) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* Ys = reinterpret_cast<double*>(smem_raw);  // rows_per x LP
@@ -155,6 +159,8 @@ __global__ void __launch_bounds__(256) gram_partial_wide_kernel(const T* __restr
 // partials; the 8 group sums are combined in a fixed order (deterministic).
 __global__ void __launch_bounds__(256) gram_reduce_kernel(const double* __restrict__ part, int parts, int l,
                                                           const int* __restrict__ skip, double* __restrict__ G) {
+  pdl_trigger();  // programmatic dependent launch: the next QR stage may start launching
+  pdl_wait();
   if (skip && *skip) return;
   __shared__ double red[8][33];
   const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
@@ -188,6 +194,8 @@ __global__ void __launch_bounds__(256) gram_reduce_kernel(const double* __restri
 // kernel solves q R = y row by row.
 __global__ void __launch_bounds__(32) chol_kernel(const double* __restrict__ Gin, int l, double* __restrict__ Rout,
                                                   double* __restrict__ rdiag, int* __restrict__ flag) {
+  pdl_trigger();  // programmatic dependent launch: the next QR stage may start launching
+  pdl_wait();
   if (*flag) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* Gs = reinterpret_cast<double*>(smem_raw);  // column-major copy: Gs[c * l + r] = G[r][c]
@@ -242,6 +250,8 @@ __global__ void __launch_bounds__(32) chol_kernel(const double* __restrict__ Gin
 // predicated on j < r <= c). 64 steps x ~70 predicated FMAs + one 64-thread barrier each.
 __global__ void __launch_bounds__(64) chol64_kernel(const double* __restrict__ Gin, int l, double* __restrict__ Rout,
                                                     double* __restrict__ rdiag, int* __restrict__ flag) {
+  pdl_trigger();  // programmatic dependent launch: the next QR stage may start launching
+  pdl_wait();
   if (*flag) return;
   __shared__ double rowj[64];
   __shared__ double s_inv;
@@ -322,6 +332,8 @@ __global__ void __launch_bounds__(64) chol64_kernel(const double* __restrict__ G
 __global__ void __launch_bounds__(256) cholinv64_kernel(const double* __restrict__ Gin, int l, double* __restrict__ Xout,
                                                         const int* __restrict__ gate, int* __restrict__ breakdown,
                                                         int* __restrict__ skip_out, double skip_kappa) {
+  pdl_trigger();  // programmatic dependent launch: the next QR stage may start launching
+  pdl_wait();
   if (*gate) return;
   __shared__ __align__(16) double rowL[2][64];
   __shared__ __align__(16) double rowR[2][64];
@@ -438,6 +450,8 @@ __global__ void __launch_bounds__(256) apply_x_kernel(const TI* __restrict__ Y, 
                                                       TO* __restrict__ Q, int64_t qrs,
                                                       int64_t qcs, TO* __restrict__ Q2, int64_t q2rs, int64_t q2cs,
                                                       int tf32 = 0) {
+  pdl_trigger();  // programmatic dependent launch: the next QR stage may start launching
+  pdl_wait();
   if (*skip) return;
   if (q1_skip && *q1_skip) Q1 = nullptr;  // CholeskyQR's second pass will not run
   extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -495,6 +509,8 @@ __global__ void __launch_bounds__(256) apply_rinv_kernel(const TI* __restrict__ 
                                                          const int* __restrict__ flag, TO* __restrict__ Q,
                                                          int64_t qrs, int64_t qcs, TO* __restrict__ Q2, int64_t q2rs,
                                                          int64_t q2cs, int tf32) {
+  pdl_trigger();  // programmatic dependent launch: the next QR stage may start launching
+  pdl_wait();
   if (*flag) return;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double* Rs = reinterpret_cast<double*>(smem_raw);
@@ -549,6 +565,8 @@ __global__ void __launch_bounds__(1024) householder_qr_kernel(const TI* __restri
                                                               double* __restrict__ V /*m x l*/, TO* __restrict__ Q,
                                                               int64_t qrs, int64_t qcs, TO* __restrict__ Q2,
                                                               int64_t q2rs, int64_t q2cs, int tf32) {
+  pdl_trigger();  // programmatic dependent launch: the next QR stage may start launching
+  pdl_wait();
   if (!force && !(*flag)) return;
   __shared__ double red[32];
   extern __shared__ double hh_smem[];  // s_dot[l], s_tau[l]
@@ -819,7 +837,11 @@ __global__ void __launch_bounds__(kSmallQRThreads) qr_small_kernel(const TI* __r
   }
 }
 
-__global__ void reset_flag_kernel(int* flag, int v) { *flag = v; }
+__global__ void reset_flag_kernel(int* flag, int v) {
+  pdl_trigger();
+  pdl_wait();
+  *flag = v;
+}
 __global__ void flag_to_double_kernel(const int* flag, double* out) { *out = (double)*flag; }
 
 int launch_flag_to_double(const int* flag, double* out, cudaStream_t st) {
@@ -855,7 +877,8 @@ static int launch_apply(const TI* Y, int64_t rs, int64_t cs, int m, int l, const
   {                                                                                                        \
     auto fn = apply_rinv_kernel<TI, TO, LWV>;                                                              \
     APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));            \
-    fn<<<blocks, 256, smem, st>>>(Y, rs, cs, m, l, Rinv, rdiag, flag, Q, qrs, qcs, Q2, q2rs, q2cs, tf32);  \
+    APX_CUDA(launch_pdl(fn, dim3(blocks), dim3(256), smem, st, Y, rs, cs, m, l, Rinv, rdiag, flag, Q, qrs, qcs, Q2, \
+                        q2rs, q2cs, tf32));                                                                \
   }
   if (lw == 1) APX_APPLY(1) else if (lw == 2) APX_APPLY(2) else if (lw == 3) APX_APPLY(3) else APX_APPLY(4)
 #undef APX_APPLY
@@ -868,29 +891,30 @@ static int launch_gram(const TI* Y, int64_t rs, int64_t cs, int m, int l, const 
                        cudaStream_t st) {
   const int parts = (int)ceil_div(m, 64);
   if (l <= 64) {
-    gram_partial_kernel<TI><<<parts, 256, 0, st>>>(Y, rs, cs, m, l, skip, part);
+    APX_CUDA(launch_pdl(gram_partial_kernel<TI>, dim3(parts), dim3(256), 0, st, Y, rs, cs, m, l, skip, part));
     APX_LAUNCH_CHECK();
   } else {
     const size_t smem = (size_t)64 * (ceil_div(l, 4) * 4 + 4) * sizeof(double);
     auto fn = gram_partial_wide_kernel<TI>;
     APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    fn<<<parts, 256, smem, st>>>(Y, rs, cs, m, l, 64, skip, part);
+    APX_CUDA(launch_pdl(fn, dim3(parts), dim3(256), smem, st, Y, rs, cs, m, l, 64, skip, part));
     APX_LAUNCH_CHECK();
   }
-  gram_reduce_kernel<<<(unsigned)ceil_div(l * l, 32), 256, 0, st>>>(part, parts, l, skip, G);
+  APX_CUDA(launch_pdl(gram_reduce_kernel, dim3((unsigned)ceil_div(l * l, 32)), dim3(256), 0, st, (const double*)part,
+                      parts, l, skip, G));
   APX_LAUNCH_CHECK();
   return OK;
 }
 
 static int launch_chol(const double* G, int l, double* R, double* rdiag, int* flag, cudaStream_t st) {
   if (l <= 64) {
-    chol64_kernel<<<1, 64, 0, st>>>(G, l, R, rdiag, flag);
+    APX_CUDA(launch_pdl(chol64_kernel, dim3(1), dim3(64), 0, st, G, l, R, rdiag, flag));
     APX_LAUNCH_CHECK();
     return OK;
   }
   const size_t smem = (size_t)l * l * sizeof(double);
   APX_CUDA(cudaFuncSetAttribute(chol_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  chol_kernel<<<1, 32, smem, st>>>(G, l, R, rdiag, flag);
+  APX_CUDA(launch_pdl(chol_kernel, dim3(1), dim3(32), smem, st, G, l, R, rdiag, flag));
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -918,7 +942,7 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
   // wide sketches (l > kMaxL: beyond the register-blocked Cholesky/apply kernels) take the
   // Householder path too
   const bool householder_only = method == 1 || m <= 2 * l || l > kMaxL;
-  reset_flag_kernel<<<1, 1, 0, st>>>(flag, householder_only ? 1 : 0);
+  APX_CUDA(launch_pdl(reset_flag_kernel, dim3(1), dim3(1), 0, st, flag, householder_only ? 1 : 0));
   APX_LAUNCH_CHECK();
   // APX_QR_FUSED=1: fp64 sketches that fit one CTA take the fused CholeskyQR2 (qr_small_kernel). It
   // is off by default: one CTA runs the O(m l^2) work latency-bound on a single SM, 160 us per QR
@@ -938,18 +962,22 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
     const double skip_kappa = sizeof(TO) == 4 ? 3.0e4 : 0.0;
     const int tiles = (int)ceil_div(m, 64);
     APX_TRY(launch_gram<TI>(Y, rs, cs, m, l, flag, part, G, st));
-    cholinv64_kernel<<<1, 256, 0, st>>>(G, l, Rinv, flag, flag, skip2, skip_kappa);
+    APX_CUDA(launch_pdl(cholinv64_kernel, dim3(1), dim3(256), 0, st, (const double*)G, l, Rinv, (const int*)flag, flag,
+                        skip2, skip_kappa));
     APX_LAUNCH_CHECK();
     APX_CUDA(cudaFuncSetAttribute(apply_x_kernel<TI, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem));
     APX_CUDA(cudaFuncSetAttribute(apply_x_kernel<double, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem));
-    apply_x_kernel<TI, TO><<<tiles, 256, kApplySmem, st>>>(Y, rs, cs, m, l, Rinv, flag, skip2, Q1, Q, qrs, qcs, Q2,
-                                                           q2rs, q2cs, tf32);
+    APX_CUDA(launch_pdl(apply_x_kernel<TI, TO>, dim3(tiles), dim3(256), kApplySmem, st, Y, rs, cs, m, l,
+                        (const double*)Rinv, (const int*)flag, (const int*)skip2, Q1, Q, qrs, qcs, Q2, q2rs, q2cs,
+                        tf32));
     APX_LAUNCH_CHECK();
     APX_TRY(launch_gram<double>(Q1, l, 1, m, l, skip2, part, G, st));
-    cholinv64_kernel<<<1, 256, 0, st>>>(G, l, Rinv, skip2, flag, (int*)nullptr, 0.0);
+    APX_CUDA(launch_pdl(cholinv64_kernel, dim3(1), dim3(256), 0, st, (const double*)G, l, Rinv, (const int*)skip2, flag,
+                        (int*)nullptr, 0.0));
     APX_LAUNCH_CHECK();
-    apply_x_kernel<double, TO><<<tiles, 256, kApplySmem, st>>>(Q1, l, 1, m, l, Rinv, skip2, (const int*)nullptr,
-                                                      (double*)nullptr, Q, qrs, qcs, Q2, q2rs, q2cs, tf32);
+    APX_CUDA(launch_pdl(apply_x_kernel<double, TO>, dim3(tiles), dim3(256), kApplySmem, st, (const double*)Q1,
+                        (int64_t)l, (int64_t)1, m, l, (const double*)Rinv, (const int*)skip2, (const int*)nullptr,
+                        (double*)nullptr, Q, qrs, qcs, Q2, q2rs, q2cs, tf32));
     APX_LAUNCH_CHECK();
   } else if (!householder_only) {
     // pass 1: Q1 = Y R1^{-1} (fp64)
@@ -964,8 +992,8 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
   const size_t hh_smem = (size_t)2 * l * sizeof(double);
   APX_CUDA(cudaFuncSetAttribute(householder_qr_kernel<TI, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)std::max<size_t>(hh_smem, 48 * 1024)));
-  householder_qr_kernel<TI, TO><<<1, 1024, hh_smem, st>>>(Y, rs, cs, m, l, flag, 0, W, V, Q, qrs, qcs, Q2, q2rs,
-                                                           q2cs, tf32);
+  APX_CUDA(launch_pdl(householder_qr_kernel<TI, TO>, dim3(1), dim3(1024), hh_smem, st, Y, rs, cs, m, l,
+                      (const int*)flag, 0, W, V, Q, qrs, qcs, Q2, q2rs, q2cs, tf32));
   APX_LAUNCH_CHECK();
   return OK;
 }
