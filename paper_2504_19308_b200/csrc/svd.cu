@@ -14,6 +14,9 @@
 namespace apx {
 
 constexpr int kSvdMax = 128;
+#ifdef APX_CHECKED
+constexpr bool getenv_sweeps_debug = true;  // the checked build reports the sweep count
+#endif
 
 template <bool GLOBAL>
 __global__ void __launch_bounds__(GLOBAL ? 1024 : 512)
@@ -29,6 +32,8 @@ __global__ void __launch_bounds__(GLOBAL ? 1024 : 512)
   __shared__ double norms_s[GLOBAL ? 1 : kSvdMax + 2];
   int* perm = GLOBAL ? reinterpret_cast<int*>(Vc + (size_t)le * le + le) : perm_s;
   double* norms = GLOBAL ? Vc + (size_t)le * le : norms_s;
+  __shared__ double nrm2_s[GLOBAL ? 1 : kSvdMax + 2];
+  double* nrm2 = GLOBAL ? norms + 3 * le + 2 + l : nrm2_s;  // GLOBAL: after the completion vector
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5, nw = blockDim.x >> 5;
   for (int e = tid; e < le * l; e += blockDim.x) {
     const int j = e / l, i = e - j * l;
@@ -40,12 +45,21 @@ __global__ void __launch_bounds__(GLOBAL ? 1024 : 512)
   }
   __syncthreads();
   const double eps = 2.220446049250313e-16;
+  const double tol2 = (eps * l) * (eps * l);
   for (int sweep = 0; sweep < 60; ++sweep) {
+    // squared column norms, exact at the start of every sweep, then carried through the sweep's
+    // rotations (||a'||^2 = al - t ga, ||b'||^2 = be + t ga): one dot product per pair instead of three
+    for (int j = warp; j < le; j += nw) {
+      double q = 0.0;
+      if (j < l)
+        for (int i = lane; i < l; i += 32) q = fma(Wc[(size_t)j * l + i], Wc[(size_t)j * l + i], q);
+      q = warp_sum(q);
+      if (lane == 0) nrm2[j] = q;
+    }
     if (tid == 0) s_rot = 0;
     __syncthreads();
     for (int round = 0; round < le - 1; ++round) {
-      // half-warp per column pair (16 lanes over the rows): up to 2 * nw pairs per pass, and the
-      // three dot products reduce together (4 interleaved xor-shuffle levels)
+      // half-warp per column pair (16 lanes over the rows): up to 2 * nw pairs per pass
       const int half = lane >> 4, hl = lane & 15;
       for (int p0 = 2 * warp; p0 < le / 2; p0 += 2 * nw) {
         const int pr = p0 + half;
@@ -59,41 +73,71 @@ __global__ void __launch_bounds__(GLOBAL ? 1024 : 512)
         }
         double* wa = Wc + (size_t)a * l;
         double* wb = Wc + (size_t)b * l;
-        double al = 0.0, be = 0.0, ga = 0.0;
-        if (active)
-          for (int i = hl; i < l; i += 16) {
-            const double x = wa[i], y = wb[i];
-            al = fma(x, x, al);
-            be = fma(y, y, be);
-            ga = fma(x, y, ga);
-          }
+        double* va = Vc + (size_t)a * le;
+        double* vb = Vc + (size_t)b * le;
+        // shared-memory kernel (l <= 128): the pair's W and V entries in registers, all loads
+        // issued before the reduction; the global-scratch kernel (wide sketches) re-reads them
+        constexpr int kR = GLOBAL ? 1 : (kSvdMax + 15) / 16;
+        double xw[kR], yw[kR], xv[kR], yv[kR];
+        double ga = 0.0;
+        if (GLOBAL) {
+          if (active)
+            for (int i = hl; i < l; i += 16) ga = fma(wa[i], wb[i], ga);
+        } else {
 #pragma unroll
-        for (int o = 8; o > 0; o >>= 1) {
-          al += __shfl_xor_sync(0xffffffffu, al, o);
-          be += __shfl_xor_sync(0xffffffffu, be, o);
-          ga += __shfl_xor_sync(0xffffffffu, ga, o);
+          for (int u = 0; u < kR; ++u) {
+            const int i = hl + 16 * u;
+            xw[u] = (active && i < l) ? wa[i] : 0.0;
+            yw[u] = (active && i < l) ? wb[i] : 0.0;
+            xv[u] = (active && i < le) ? va[i] : 0.0;
+            yv[u] = (active && i < le) ? vb[i] : 0.0;
+            ga = fma(xw[u], yw[u], ga);
+          }
         }
-        if (active && ga != 0.0 && fabs(ga) > eps * l * sqrt(al * be)) {
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
+        const double al = active ? nrm2[a] : 0.0, be = active ? nrm2[b] : 0.0;
+        if (active && ga != 0.0 && ga * ga > tol2 * al * be) {
           const double zeta = (be - al) / (2.0 * ga);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(1.0 + zeta * zeta));
-          const double c = 1.0 / sqrt(1.0 + t * t), s = c * t;
-          for (int i = hl; i < l; i += 16) {
-            const double x = wa[i], y = wb[i];
-            wa[i] = c * x - s * y;
-            wb[i] = s * x + c * y;
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
+          const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+          if (GLOBAL) {
+            for (int i = hl; i < l; i += 16) {
+              const double x = wa[i], y = wb[i];
+              wa[i] = c * x - sn * y;
+              wb[i] = sn * x + c * y;
+            }
+            for (int i = hl; i < le; i += 16) {
+              const double x = va[i], y = vb[i];
+              va[i] = c * x - sn * y;
+              vb[i] = sn * x + c * y;
+            }
+          } else {
+#pragma unroll
+            for (int u = 0; u < kR; ++u) {
+              const int i = hl + 16 * u;
+              if (i < l) {
+                wa[i] = c * xw[u] - sn * yw[u];
+                wb[i] = sn * xw[u] + c * yw[u];
+              }
+              if (i < le) {
+                va[i] = c * xv[u] - sn * yv[u];
+                vb[i] = sn * xv[u] + c * yv[u];
+              }
+            }
           }
-          double* va = Vc + (size_t)a * le;
-          double* vb = Vc + (size_t)b * le;
-          for (int i = hl; i < le; i += 16) {
-            const double x = va[i], y = vb[i];
-            va[i] = c * x - s * y;
-            vb[i] = s * x + c * y;
+          if (hl == 0) {
+            nrm2[a] = al - t * ga;
+            nrm2[b] = be + t * ga;
+            s_rot = 1;
           }
-          if (hl == 0) s_rot = 1;
         }
       }
       __syncthreads();
     }
+#ifdef APX_CHECKED
+    if (!s_rot && tid == 0 && getenv_sweeps_debug) printf("hestenes l=%d converged after %d sweeps\n", l, sweep + 1);
+#endif
     if (!s_rot) break;
     __syncthreads();
   }
@@ -156,7 +200,7 @@ __global__ void __launch_bounds__(GLOBAL ? 1024 : 512)
 size_t small_svd_scratch_doubles(int l) {
   if (l <= kSvdMax) return 0;
   const size_t le = (size_t)l + (l & 1);
-  return le * l + le * le + 2 * le + 2 + le + 8;  // W, V, norms, perm (as ints), completion vector
+  return le * l + le * le + 2 * le + 2 + le + 8 + le + 2;  // W, V, norms, perm, completion vector, nrm2
 }
 
 int launch_small_svd(const double* W, int l, double* U, double* S, double* V, double* VT, cudaStream_t st,
