@@ -53,14 +53,28 @@ WORKLOADS = {
 }
 # Stage markers recorded by the C4 plan (capi.cu run_mixed_f32_umma): 0 start | hi stream: 1 B
 # decomposed, 2 gather done | lo stream: 3 Y, 4 QR, 5 Bm, 9 W GEMM, 6 W | main: 7 M += Q.W, 8 end.
-N_MARKS = 10
-SPANS = {  # name -> (start marker, end marker); "join" = the later of markers 2 and 7
+N_MARKS = 12
+# C4 stage markers (capi.cu run_mixed_f32_resid / run_mixed_f32_umma): name -> (start, end);
+# "join" = the later of markers 2 and 7. GATHER_MARKS: the gather's own span (timed region).
+SPANS = {
+    "B: cycle norms+select+extract+f16 lambda' [hi]": (0, 1),
+    "Y = A.Omega (tcgen05 TF32) [lo]": (0, 3),
+    "QR (CholeskyQR) [lo]": (3, 4),
+    "Bm = Q^T A (+||A||^2, ||Bm||^2; A tiles rounded to TF32) [lo]": (4, 5),
+    "dA = A - [Q|Q].[Bm_hi;Bm_lo] -> scaled f16 (tcgen05, fused epilogue) [lo]": (5, 10),
+    "M = dA.Bhat (persistent f16 row gather) [hi]": (11, 2),
+    "W0 = Bm.B (tcgen05 TF32) [lo]": (10, 9),
+    "W = W0 - Bm.Bhat_tf32 + Bm.Bhat (gathers), hi/lo split [lo]": (9, 6),
+    "M += [Q|Q].[W_hi;W_lo] (+||M||^2; each tile waits for its gather rows) [lo]": (6, 7),
+    "after the join (fixed-order sums)": ("join", 8),
+}
+SPANS_DIRECT = {
     "B: cycle norms+select+extract [hi]": (0, 1),
     "M = A.Bhat (persistent row gather) [hi]": (1, 2),
     "Y = A.Omega (tcgen05 TF32) [lo]": (0, 3),
     "QR (CholeskyQR) [lo]": (3, 4),
     "Bm = Q^T A (+||Bm||^2; operands rounded to TF32) [lo]": (4, 5),
-    "W0 = Bm.B (tcgen05 TF32) [lo]": (5, 9),
+    "W0 = Bm.B (tcgen05 TF32) [lo]": (10, 9),
     "W = W0 - Bm.Bhat (TF32-exact gather) [lo]": (9, 6),
     "M += Q.W (+||M||^2; each tile waits for its gather rows) [lo]": (6, 7),
     "after the join (fixed-order sums)": ("join", 8),
@@ -288,8 +302,12 @@ def run_c4(args, rank, world, local_rank):
     omega = torch.from_numpy(P.cycle.draw_sketch(n, K_SVD, seed)).to(dev, torch.float32)
     M = torch.empty(n, n, device=dev, dtype=torch.float32)
 
+    direct = args.plan == "direct"
+    spans = SPANS_DIRECT if direct else SPANS
+    g0 = 1 if direct else 11  # marker opening the gather's span
+
     def step(out=M):
-        return P.mixed_product_device(A, B, K_SVD, K_CYC, 1, omega, 0, None, False, out=out)
+        return P.mixed_product_device(A, B, K_SVD, K_CYC, 1, omega, 0, None, False, out=out, direct=direct)
 
     for _ in range(args.warmup):
         step()
@@ -303,8 +321,12 @@ def run_c4(args, rank, world, local_rank):
         for e in row:
             e.record()
     torch.cuda.synchronize()
-    gptr = [(ctypes.c_void_p * N_MARKS)(*([None, row[0].cuda_event, row[1].cuda_event] + [None] * (N_MARKS - 3)))
-            for row in gev]
+    def gather_marks(row):
+        m = [None] * N_MARKS
+        m[g0], m[2] = row[0].cuda_event, row[1].cuda_event
+        return (ctypes.c_void_p * N_MARKS)(*m)
+
+    gptr = [gather_marks(row) for row in gev]
     it = iter(range(args.steps))
 
     def timed_step():
@@ -339,7 +361,7 @@ def run_c4(args, rank, world, local_rank):
         return t[b] - ta
 
     stage_ms = {name: statistics.mean(span_ms(evs[s], a, b) for s in range(args.steps))
-                for name, (a, b) in SPANS.items()}
+                for name, (a, b) in spans.items()}
 
     # ---- e2e: public API with pinned host buffers (H2D inputs, D2H result, every step) ----
     # MixedPipeline (the host-to-host serving API): each product copies its full A, B in and its
@@ -386,12 +408,15 @@ def run_c4(args, rank, world, local_rank):
         peak, peak_kind = hbm_peak()
         pk = pipe_peaks()
         cap = gather_capture()
-        alg_bytes = 8.0 * n * n  # A read + M write (fp32); Q.W accumulates onto it afterwards
+        # gather: (direct) fp32 A read + M write, Q.W accumulated onto M afterwards; (residual plan)
+        # f16 dA read + M write, Q.W accumulated afterwards
+        alg_bytes = (8.0 if direct else 6.0) * n * n
         achieved = alg_bytes / (gather_ms_timed * 1e-3) / 1e9
         total_alg_bytes = 24.0 * n * n  # SURVEY §8(d) C4 algorithmic bytes per product
-        lds_bytes = 4.0 * K_CYC * n * n  # one fp32 shared-memory operand per FMA (k n^2 FMAs)
+        # one shared-memory operand per FMA (k n^2 FMAs): fp32 (direct) or f16 (residual plan)
+        lds_bytes = (4.0 if direct else 2.0) * K_CYC * n * n
         lds_achieved = lds_bytes / (gather_ms_timed * 1e-3) / 1e12
-        lds_peak = pk.get("lds64_tbs")
+        lds_peak = pk.get("lds64_tbs" if direct else "lds128_tbs")
         from paper_2504_19308_b200.cycle import _norms
         nA, nB, ndA, ndB, nM = _norms(s, n * n)
         line = {
@@ -401,12 +426,17 @@ def run_c4(args, rank, world, local_rank):
             "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": WORKLOADS["c4"], "n": n, "k_svd": K_SVD, "k_cyc": K_CYC, "order": 1,
                        "power_iterations": 0, "gemm": "tcgen05 kind::tf32 (TMA, warp-specialized)",
+                       "plan": ("direct: M = A.Bhat (fp32 gather) + Q.W" if direct else
+                                "residual: M = Q.(Bm.B) + dA.Bhat, dA and lambda' in scaled f16 (FHFMA, fp32 "
+                                "accumulation), Q.(.) as a K=2l TF32 hi/lo GEMM"),
                        "parallelism": f"replicas x{world} (one product per GPU per step)",
                        "l2": "inputs larger than L2 (2 x 256 MiB fp32); no flush",
                        "sketch": "Omega drawn once on the host (numpy default_rng([7,0]), the reference's "
                                  "stream) outside the device-timed region; e2e draws it per product"},
             "clocks": clocks, "e2e": e2e, "gpu_launches": int(launches),
-            "roofline": {"bound": "hbm", "kernel": "cycle_right_gather (M = A.Bhat, persistent)",
+            "roofline": {"bound": "hbm",
+                         "kernel": ("cycle_right_gather (M = A.Bhat, persistent)" if direct else
+                                    "cycle_gather_f16_kernel (M = dA.Bhat, persistent, f16 operands)"),
                          "achieved": achieved, "peak": peak, "unit": "GB/s", "frac": achieved / peak,
                          "traffic": cap["traffic"] if cap else None, "peak_kind": peak_kind,
                          "alg_bytes_per_launch": alg_bytes,
@@ -834,6 +864,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--config", default="c4", choices=sorted(WORKLOADS))
     ap.add_argument("--n", type=int, default=N_DEFAULT)
+    ap.add_argument("--plan", default="resid", choices=["resid", "direct"],
+                    help="C4: residual plan (f16 gather over dA, default) or the all-fp32 gather over A")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--shard", default="auto", choices=["auto", "replicas", "rows"],

@@ -234,7 +234,18 @@ struct MixedPlan {
   int* ticket;
   int* ready;  // per gather row block: 1 once its M rows are final (consumed by M += Q.W on lo)
   int n_part_rows;
+  // residual plan (mixed_f16.cu): [Q | Q], the TF32 hi/lo split of W, f16 lambda', f16 dA
+  // (row-block interleaved); null when the shape does not fit it
+  float *Q2 = nullptr, *W2 = nullptr;
+  uint16_t *lamh = nullptr, *dAh = nullptr;
 };
+
+// The residual plan's shape conditions (run_mixed_f32_resid): fp32, l = 64, a row fits shared
+// memory as 8 f16 rows, n a multiple of the gather's 4 x 128-column thread groups.
+static bool resid_shape_ok(int dtype, int n, int l, int kc) {
+  return dtype == F32 && l == 64 && kc >= 1 && kc <= 128 && gather_f16_threads(n) > 0 &&
+         gather_f16_smem(n, pad8(kc)) <= 220 * 1024;
+}
 
 static int mixed_gemm_splits(int n, int l) {
   return std::max(gemm_splits(n, l, n, 128, 64), gemm_splits(l, n, n, 64, 128));
@@ -263,6 +274,12 @@ static void plan_mixed(Workspace& ws, MixedPlan& p, int dtype, int n, int l, int
   p.bsq = ws.take<double>(std::max<int>(n, kNumSMs * 4));
   p.ticket = ws.take<int>(4);
   p.ready = ws.take<int>((size_t)n + 1 + qw_ctas);  // row-block flags, then the deferred-tile list
+  if (resid_shape_ok(dtype, n, l, kc)) {
+    p.Q2 = ws.take<float>((size_t)n * 2 * l);
+    p.W2 = ws.take<float>((size_t)n * 2 * l);
+    p.lamh = ws.take<uint16_t>((size_t)pad8(kc) * n);
+    p.dAh = ws.take<uint16_t>((size_t)ceil_div(n, 8) * 8 * n);
+  }
 }
 
 // fp32 GEMM stages of the mixed product on tcgen05 (umma.cu). Layout bits: 1 = A operand stored
@@ -496,6 +513,127 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
     APX_TRY(launch_sumsq<float>(A, (size_t)n * n, p.asq, &parts, st));
     APX_TRY(launch_sum_vector(p.asq, parts, scal + APX_S_FRO2_A, st));
   }
+  stage_mark(8, st);
+  return OK;
+}
+
+// ---- residual plan of the C4 product (order 1; mixed_f16.cu explains the algebra) ----------------
+// M = Q.(Bm.B) + (A - Q.Bm).Bhat: the gather runs over the f16 residual dA instead of the fp32 A,
+// i.e. 2 shared-memory bytes per FMA instead of 4.
+//   hi: Y = A Omega, CholeskyQR, Bm = Q^T A (+||A||^2 from the rounded A tiles), Bm := tf32(Bm),
+//       dA = A - Q.Bm stored as f16 (fused epilogue), then the persistent f16 gather M = dA.Bhat
+//       on all but 16 SMs, publishing a flag per 8-row block
+//   lo: B's cycle decomposition and lambda' (fp32 and scaled f16) during the QR | on the 16 SMs
+//       the gather leaves: W = Bm.B (TF32 GEMM minus the TF32-exact gather plus the fp32 gather),
+//       hi/lo split, M += [Q|Q].[W_hi; W_lo] (+||M||^2) following the gather's row flags (bounded
+//       wait + fixup as in run_mixed_f32_umma). (Measured alternative: M = Q.W first, then the
+//       gather as a read-modify-write on every SM -- the W chain then sits on the critical path:
+//       979 vs 1132 products/s.)
+// Stage markers: 0 start | hi: 3 Y, 4 QR, 5 Bm, 10 dA, 11 gather start, 2 gather end |
+// lo: 1 B decomposed, 9 W GEMM, 6 W, 7 M += Q.W | 8 end.
+static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int kc, int q, const float* Omega,
+                               const int* fb, float* M, int* sb, double* scal, const MixedPlan& p, cudaStream_t st) {
+  stage_mark(0, st);
+  APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
+  const int grows = 8;  // the f16 gather's row block
+  const int rblocks = (int)ceil_div(n, grows);
+  int* defer = p.ready + rblocks;
+  APX_CUDA(cudaMemsetAsync(p.ready, 0, (rblocks + 1) * sizeof(int), st));
+  SideStream* ss = nullptr;
+  APX_TRY(get_side(&ss));
+  APX_CUDA(cudaEventRecord(ss->fork, st));
+  APX_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
+  APX_CUDA(cudaStreamWaitEvent(ss->hi, ss->fork, 0));
+  // The critical path is A's chain (Y -> QR -> Bm -> dA -> gather), so it runs on the
+  // high-priority stream; B's decomposition and the W chain fill in on the low-priority one.
+  const cudaStream_t hi = ss->hi, lo = ss->s;
+  const int gctas = gather_ctas(rblocks);
+  const int free_sms = std::max(8, kNumSMs - gctas);
+  const int kp = pad8(kc);
+  float *Y = (float*)p.Y, *Q = (float*)p.Q, *Qt = (float*)p.Qt, *Z = (float*)p.Z, *Bm = (float*)p.Bm,
+        *W = (float*)p.W, *part = (float*)p.part;
+  // ---- hi: Y = A Omega on the whole GPU, then CholeskyQR -------------------------------------------
+  APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, hi, kNumSMs));
+  stage_mark(3, hi);
+  APX_CUDA(cudaEventRecord(ss->b_read, hi));
+  // ---- lo: B's cycle decomposition and the f16 lambda' table, overlapping the latency-bound QR: the
+  // energy pass keeps half the CTA slots free so the QR's kernels launch at once ---------------------
+  APX_CUDA(cudaStreamWaitEvent(lo, ss->b_read, 0));
+  if (fb) {
+    APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, lo, 4));
+    APX_CUDA(cudaMemcpyAsync(sb, fb, kc * sizeof(int), cudaMemcpyDeviceToDevice, lo));
+    APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, lo));
+  } else {
+    APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, nullptr, p.partial, lo, 4));
+    APX_TRY(launch_topk(p.nr_b, n, kc, sb, lo, p.nr_b, 1.0, scal + APX_S_KEPT_B, p.en_b, scal + APX_S_FRO2_B));
+  }
+  float* lb = (float*)p.lam_b;
+  APX_TRY(launch_cycle_extract<float>(B, n, sb, kc, lb, lo, /*aligned=*/true));
+  APX_TRY(zero_pad_rows<float>(lb, kc, n, lo));
+  APX_TRY(launch_lam_f16(lb, kp, n, scal + APX_S_FRO2_B, p.lamh, lo));
+  APX_CUDA(cudaEventRecord(ss->b_ready, lo));
+  stage_mark(1, lo);
+  // ---- hi: QR, Bm (+||A||^2), dA in f16 -----------------------------------------------------------
+  APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, hi, /*tf32=*/1)));
+  for (int it = 0; it < q; ++it) {
+    APX_TRY(UmmaStages::at_times_x(A, Q, Z, part, n, l, hi));
+    APX_TRY((qr_orthonormalize<float, float>(Z, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, hi, /*tf32=*/1)));
+    APX_TRY(UmmaStages::a_times_x(A, Q, Y, part, n, l, hi));
+    APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, hi, /*tf32=*/1)));
+  }
+  stage_mark(4, hi);
+  {
+    // Bm = Q^T A with the A tiles rounded to TF32 (FIX 3): the rounding warps also sum the
+    // squares of every A element they touch (each exactly once) -> ||A||^2 partials
+    const int s = UmmaStages::splits(n);
+    APX_TRY(umma_tma_gemm(7 | 8 | 16, 64, A, n, Q, l, s > 1 ? part : Bm, n, (int64_t)l * n, n, l, n, s, 0, nullptr, 0,
+                          1, hi, p.asq));
+    if (s > 1) APX_TRY(launch_split_reduce_f32(part, s, (size_t)n * l, Bm, hi));
+    APX_TRY(launch_sum_vector(p.asq, (int)(ceil_div(n, 128) * s), scal + APX_S_FRO2_A, hi));
+  }
+  // ||Bm||^2 (= sum sigma^2, the kept energy of the report) from Bm as formed; then Bm := tf32(Bm)
+  // (the algebra holds for any Bm -- but the energy difference ||A||^2 - ||Bm||^2 would feel the
+  // rounding: ~2e-5 of ||Bm||^2 when a few rows carry the energy): with Q TF32-exact too, Q.Bm is
+  // exact on the tensor core at K = l
+  int parts = 0;
+  APX_TRY(launch_sumsq<float>(Bm, (size_t)l * n, p.bsq, &parts, hi));
+  APX_TRY(launch_sum_vector(p.bsq, parts, scal + APX_S_KEPT_A, hi));
+  APX_TRY(launch_round_tf32(Bm, (size_t)l * n, hi));
+  APX_TRY(launch_dup_cols(Q, n, l, p.Q2, hi));
+  stage_mark(5, hi);
+  APX_TRY(umma_tma_gemm(2 | 32, 128, Q, l, Bm, n, const_cast<float*>(A), n, 0, n, n, l, 1, 0, nullptr, 0, 1, hi,
+                        nullptr, nullptr, 0, nullptr, nullptr, p.dAh, scal + APX_S_FRO2_A));
+  stage_mark(10, hi);
+  cudaEvent_t da_ready = ss->join;  // reused: recorded again at the end of lo
+  APX_CUDA(cudaEventRecord(da_ready, hi));
+  // ---- hi: the f16 gather M = dA . Bhat -------------------------------------------------------------
+  APX_CUDA(cudaStreamWaitEvent(hi, ss->b_ready, 0));
+  stage_mark(11, hi);
+  APX_TRY(launch_gather_f16(p.dAh, p.lamh, sb, kc, kp, n, n, M, scal + APX_S_FRO2_A, scal + APX_S_FRO2_B, p.ticket,
+                            p.ready, gctas, hi));
+  stage_mark(2, hi);
+  APX_CUDA(cudaEventRecord(ss->hi_done, hi));
+  // ---- lo: W = Bm . B at fp32 accuracy, then M += [Q|Q].[W_hi; W_lo] behind the gather's frontier --
+  // (after dA: the W GEMM's HBM pass would otherwise slow the critical dA pass)
+  APX_CUDA(cudaStreamWaitEvent(lo, da_ready, 0));
+  const int wblocks = (int)ceil_div(l, right_gather_rows(n, sizeof(float), kc));
+  const int wchunks = std::max(1, std::min(8, (int)ceil_div(5 * free_sms, wblocks)));
+  APX_TRY(UmmaStages::bm_times_db(B, Bm, W, part, n, l, nullptr, 0, lo, free_sms));
+  stage_mark(9, lo);
+  APX_TRY(launch_cycle_right_gather<float>(Bm, nullptr, 0, lb, sb, kc, n, l, -1, W, nullptr, nullptr, lo, true, 0,
+                                           nullptr, wchunks, /*tf32_operands=*/true));
+  APX_TRY(launch_cycle_right_gather<float>(Bm, nullptr, 0, lb, sb, kc, n, l, 1, W, nullptr, nullptr, lo, true, 0,
+                                           nullptr, wchunks, /*tf32_operands=*/false));
+  APX_TRY(launch_split_tf32(W, (size_t)l * n, p.W2, lo));
+  stage_mark(6, lo);
+  APX_TRY(UmmaStages::q_times_w(p.Q2, p.W2, M, n, 2 * l, lo, 1, p.msq, p.ready, grows, p.ticket, defer));
+  stage_mark(7, lo);
+  APX_CUDA(cudaStreamWaitEvent(lo, ss->hi_done, 0));
+  APX_TRY(launch_qw_fixup_sum(p.Q2, 2 * l, p.W2, n, M, n, n, n, 2 * l, 128, defer, p.msq,
+                              UmmaStages::q_times_w_ctas(n, 2 * l, 1), scal + APX_S_FRO2_M, lo));
+  APX_CUDA(cudaEventRecord(ss->join, lo));
+  APX_CUDA(cudaStreamWaitEvent(st, ss->join, 0));
+  APX_CUDA(cudaStreamWaitEvent(st, ss->hi_done, 0));
   stage_mark(8, st);
   return OK;
 }
@@ -842,6 +980,10 @@ int apx_mixed_first_order(int dtype, const void* A, const void* B, int64_t n, in
   // tcgen05 path: fp32, l == 64 (one N=64 tile), n a multiple of 4 (16-byte rows), <= 128 masked
   // cycles; 3xTF32 requests and other shapes use the mma.sync path
   const bool umma_ok = dtype == F32 && !split3 && k_svd == 64 && (n % 4) == 0 && k_cyc <= 128 && !(flags & 2);
+  // residual plan (f16 gather over dA) unless flag 4 asks for the all-fp32 gather over A
+  if (umma_ok && order == 1 && p.dAh != nullptr && !(flags & 4))
+    return run_mixed_f32_resid((const float*)A, (const float*)B, (int)n, k_svd, k_cyc, power_iterations,
+                               (const float*)omega, force_sel_b, (float*)M, sel_b, scalars, p, S(stream));
   if (umma_ok)
     return run_mixed_f32_umma((const float*)A, (const float*)B, (int)n, k_svd, k_cyc, order, power_iterations,
                               (const float*)omega, force_sel_b, (float*)M, sel_b, scalars, p, S(stream));

@@ -209,4 +209,21 @@ __device__ __forceinline__ T block_sum(T v, T* sh) {
   return r;
 }
 
+// ---- scaled f16 storage of the mixed product's residual term (see mixed_f16.cu) ---------------
+// Binary exponent e with ||X||_F < 2^e (fro2 = ||X||_F^2): scaling X by 2^(15 - e) keeps every
+// entry below 2^15 < 65504 (|x_ij| <= ||X||_F), so no value can overflow f16. Zero or non-finite
+// norms give e = 0; e is clamped so the fp32 scale factors stay normal.
+__host__ __device__ inline int f16_scale_exp(double fro2) {
+  if (!(fro2 > 0.0) || !(fro2 < 1e300)) return 0;
+  int e = 0;
+  frexp(sqrt(fro2), &e);
+  return e < -100 ? -100 : (e > 140 ? 140 : e);
+}
+// two floats -> packed f16x2, round to nearest even (lo in bits 0..15)
+__device__ __forceinline__ uint32_t pack_half2(float lo, float hi) {
+  uint32_t d;
+  asm("cvt.rn.f16x2.f32 %0, %1, %2;" : "=r"(d) : "f"(hi), "f"(lo));
+  return d;
+}
+
 }  // namespace apx

@@ -938,10 +938,11 @@ static int set_smem(const void* fn, size_t bytes) {
   return OK;
 }
 
-static int energy_groups(int n, int* rows_per_chunk) {
+static int energy_groups(int n, int* rows_per_chunk, int ctas_per_sm = 8) {
   const int cblocks = (int)ceil_div(n, 256);
-  // one full wave of 8 CTAs per SM (launch bounds (256, 8)): rounding up left a 0.33-wave tail
-  int groups = std::max(1, (kNumSMs * 8) / cblocks);
+  // one full wave of 8 CTAs per SM (launch bounds (256, 8)): rounding up left a 0.33-wave tail;
+  // fewer CTAs per SM leave room for a concurrent latency-bound chain (the C4 residual plan's QR)
+  int groups = std::max(1, (kNumSMs * ctas_per_sm) / cblocks);
   // at most 40 row groups: the finalize sums one column's groups per thread (n threads), so a
   // small n with many groups made it the slow part (53 us at n = 2048 with 128 groups)
   groups = std::max(1, std::min({groups, (int)ceil_div(n, 16), 40}));
@@ -957,9 +958,9 @@ size_t cycle_energy_ws(int n) {
 
 template <typename T>
 int launch_cycle_energies(const T* A, int n, double* energies, double* norms, double* fro2, double* partial,
-                          cudaStream_t st) {
+                          cudaStream_t st, int ctas_per_sm) {
   int rpc;
-  const int groups = energy_groups(n, &rpc);
+  const int groups = energy_groups(n, &rpc, ctas_per_sm);
   const unsigned cb = (unsigned)ceil_div(n, 256);
   dim3 grid(cb, (unsigned)groups);
   // separate finalize: the fused last-CTA reduce (counters != nullptr) measured 63 us vs 44 + 7
@@ -1290,7 +1291,7 @@ int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st) {
 }
 
 #define APX_INST(T)                                                                                            \
-  template int launch_cycle_energies<T>(const T*, int, double*, double*, double*, double*, cudaStream_t);     \
+  template int launch_cycle_energies<T>(const T*, int, double*, double*, double*, double*, cudaStream_t, int);     \
   template int launch_cycle_extract<T>(const T*, int, const int*, int, T*, cudaStream_t, bool);                   \
   template int launch_cycle_materialize<T>(const T*, const int*, int, int, T*, cudaStream_t);                 \
   template int launch_cycle_left_gather<T>(const T*, const T*, const int*, int, int, int, T*, cudaStream_t);  \

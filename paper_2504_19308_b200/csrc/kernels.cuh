@@ -13,7 +13,7 @@ int right_gather_rows_plain(int n, size_t elem, int k);
 int right_gather_seg_rows(int n, size_t elem, int k);
 template <typename T>
 int launch_cycle_energies(const T* A, int n, double* energies, double* norms, double* fro2, double* partial,
-                          cudaStream_t st);
+                          cudaStream_t st, int ctas_per_sm = 8);
 // top-k selection (select.cuh); optionally fused: *kept = kept_scale * sum_t kept_w[sel[t]]^2 and
 // *total = sum_i tot_w[i]
 int launch_topk(const double* w, int n, int k, int* sel, cudaStream_t st, const double* kept_w = nullptr,
@@ -80,10 +80,20 @@ int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* 
                   int64_t ldc, int64_t c_split_stride, int M, int N, int K, int splits, int accumulate,
                   const int* mJ, int mk, int mod_n, cudaStream_t st, double* sq_partial = nullptr,
                   const int* ready = nullptr, int ready_rows = 0, const int* progress = nullptr,
-                  int* defer = nullptr);
+                  int* defer = nullptr, uint16_t* hout = nullptr, const double* hscale = nullptr);
 // deferred Q.W tiles of a ready-flag GEMM, then the fixed-order ||C||^2 sum (umma_tma.cu)
 int launch_qw_fixup_sum(const float* Q, int64_t ldq, const float* W, int64_t ldw, float* C, int64_t ldc, int M, int N,
                         int K, int bn, int* defer, double* sq_partial, int parts, double* out, cudaStream_t st);
+// ---- mixed_f16.cu (residual plan of the C4 product) ----
+int launch_split_tf32(const float* X, size_t count, float* X2, cudaStream_t st);
+int launch_dup_cols(const float* Q, int rows, int l, float* Q2, cudaStream_t st);
+int launch_round_tf32(float* X, size_t count, cudaStream_t st);
+int gather_f16_threads(int n);
+size_t gather_f16_smem(int n, int kp);
+int launch_lam_f16(const float* lam, int kp, int n, const double* fro2_b, uint16_t* out, cudaStream_t st);
+int launch_gather_f16(const uint16_t* Xh, const uint16_t* lamh, const int* J, int k, int kp, int n, int m_rows, float* M,
+                      const double* fro2_a, const double* fro2_b, int* ticket, int* ready, int ctas, cudaStream_t st,
+                      double* msq_partial = nullptr);
 int umma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
               int64_t c_split_stride, int M, int N, int K, int splits, int accumulate, const int* mJ, int mk,
               int mod_n, cudaStream_t st);

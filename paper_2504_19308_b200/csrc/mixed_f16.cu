@@ -1,0 +1,356 @@
+// Residual plan of the mixed rSVD x cycles product (config C4, fp32, order 1).
+//
+// The order-1 product is  M = Ahat.B + dA.Bhat  (Ahat = Q Q^T A, dA = A - Ahat, Bhat = the k_cyc
+// kept cycles of B; the reference's svd_first_order_multiply structure, svd.py:174-177). With
+// Bm = Q^T A (whatever the TF32 GEMM returns) it is evaluated as
+//
+//     M = Q . (Bm . B)  +  (A - Q . Bm) . Bhat                                   (1)
+//
+// which equals A.Bhat + Q Bm dB for ANY Bm -- so Bm's own rounding never enters M beyond the tiny
+// Q Bm dB term -- provided both sides use the same Bm and each product is formed accurately:
+//   * Q . (Bm . B): Bm . B = [TF32 GEMM Bm.B] - [TF32-truncated gather Bm.Bhat] + [fp32 gather
+//     Bm.Bhat]; the first two cancel exactly on the kept cycles (the round-1 W trick), so the
+//     result has TF32 error only relative to Bm.dB. The outer product by Q (TF32-exact from the QR)
+//     runs on the tensor core as a K = 2l GEMM [Q | Q] . [hi(W); lo(W)] (hi/lo: TF32 split), i.e.
+//     at fp32 accuracy.
+//   * dA = A - Q . Bm: Bm is rounded to TF32 once it is formed (Bm := tf32(Bm) -- (1) holds for
+//     any Bm), so with Q TF32-exact as well every tensor-core product is exact and the K = l GEMM
+//     is fp32-accurate; the subtraction and the f16 store are fused into its epilogue
+//     (gemm_tma_kernel FIX 4).
+//   * dA . Bhat: dA carries ~1.8% of ||M|| at C4 (residual energy 3.4e-4 of ||A||^2), so it is
+//     stored as scaled f16 (2^(15-e_A) dA, e_A from ||A||_F: no entry can overflow) and the
+//     kept-cycle diagonals as scaled f16 too (2^(15-e_B) lambda', e_B from ||B||_F); the gather
+//     multiplies them with FHFMA (fma.rn.f32.f16: f16 x f16 products, fp32 accumulation) and
+//     rescales by 2^(e_A + e_B - 30) once per output. Each shared-memory operand is now 2 bytes
+//     instead of 4, which halves the gather's shared-memory bytes per FMA -- the gather's
+//     limiter. f16 rounding (2^-11 relative) on a term of 1.8% of M adds
+//     ~4e-6 relative error (north_star allows reduced-precision operands where the fp32 1e-4
+//     tolerance allows; measured parity in tests/test_gpu_mixed.py and bench.py).
+//
+// Kernels here: TF32 rounding and the hi/lo split, [Q | Q], the f16 lambda' table, the f16 gather.
+#include <cuda_fp16.h>
+
+#include "common.cuh"
+#include "kernels.cuh"
+
+namespace apx {
+
+namespace {
+
+__device__ __forceinline__ float tf32_rn(float x) {
+  return __uint_as_float((__float_as_uint(x) + 0x1000u) & 0xffffe000u);
+}
+
+// X2[0:rows] = tf32(X), X2[rows:2 rows] = tf32(X - tf32(X)) (X - tf32(X) is exact in fp32)
+__global__ void split_tf32_kernel(const float* __restrict__ X, size_t count, float* __restrict__ X2) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    const float x = X[i];
+    const float hi = tf32_rn(x);
+    X2[i] = hi;
+    X2[count + i] = tf32_rn(x - hi);
+  }
+}
+
+// X = tf32(X) in place (round to nearest, ties away)
+__global__ void round_tf32_kernel(float* __restrict__ X, size_t count) {
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x)
+    X[i] = tf32_rn(X[i]);
+}
+
+// Q2 = [Q | Q] (rows x 2l)
+__global__ void dup_cols_kernel(const float* __restrict__ Q, int rows, int l, float* __restrict__ Q2) {
+  const size_t count = (size_t)rows * l;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    const size_t r = i / l, c = i - r * l;
+    const float v = Q[i];
+    Q2[r * 2 * l + c] = v;
+    Q2[r * 2 * l + l + c] = v;
+  }
+}
+
+// f16 lambda' table in the gather's thread order: entry (t, g * NT + tid) holds the CPT columns
+// g * CPT NT + q * NT + tid (q < CPT) of row t as CPT/2 packed f16x2 words, scaled by 2^(15 - e_B)
+__global__ void lam_f16_kernel(const float* __restrict__ lam, int kp, int n, int nt, int cpt,
+                               const double* __restrict__ fro2_b, uint32_t* __restrict__ out) {
+  const float s = ldexpf(1.f, 15 - f16_scale_exp(*fro2_b));
+  const int per_row = n / cpt;
+  const size_t count = (size_t)kp * per_row;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
+    const int t = (int)(i / per_row), e = (int)(i - (size_t)t * per_row);
+    const int g = e / nt, tid = e - g * nt;
+    const float* row = lam + (size_t)t * n + (size_t)g * cpt * nt + tid;
+    for (int w = 0; w < cpt / 2; ++w)
+      out[i * (cpt / 2) + w] = pack_half2(s * row[(2 * w) * nt], s * row[(2 * w + 1) * nt]);
+  }
+}
+
+__device__ __forceinline__ float fhfma(unsigned short a, unsigned short b, float c) {
+  float d;
+  asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d) : "h"(a), "h"(b), "f"(c));
+  return d;
+}
+__device__ __forceinline__ unsigned short lo16(uint32_t v) { return (unsigned short)(v & 0xffffu); }
+__device__ __forceinline__ unsigned short hi16(uint32_t v) { return (unsigned short)(v >> 16); }
+
+template <int W>
+__device__ __forceinline__ void ldg_nc_words(const uint32_t* p, uint32_t (&v)[W]) {
+  if constexpr (W == 1) {
+    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v[0]) : "l"(p));
+  } else {
+    static_assert(W == 2, "1 or 2 words");
+    asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "l"(p));
+  }
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"((uint32_t)__cvta_generic_to_shared(b)), "r"(c));
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
+  asm volatile(
+      "{\n.reg .pred p;\nW_%=:\n"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+      "@!p bra W_%=;\n}\n" ::"r"((uint32_t)__cvta_generic_to_shared(b)),
+      "r"(phase)
+      : "memory");
+}
+
+constexpr int kHR = 8;  // rows per block: 8 halves = one 16-byte vector per column
+constexpr int kHU = 4;  // shifts per lambda batch
+
+// M[r0 + i, c] = 2^(e_A + e_B - 30) sum_t dAh[r0 + i, (c + J_t) mod n] * lamh_t[c], i < 8.
+// Xh: ceil(m_rows / 8) blocks of n uint4 (block b, column m = rows 8b..8b+7 of column m as f16);
+// one block is one contiguous 16 n-byte run, staged into shared memory by ONE bulk async copy.
+// Thread tid owns columns g * CPT NT + q * NT + tid of each column group g; per shift it loads
+// one CPT-half vector of lambda' (its CPT columns) and, per column, one 16-byte shared vector (8
+// rows) feeding 8 FHFMAs: per warp CPT x 4 shared wavefronts + CPT/2 lambda' wavefronts per
+// 256 CPT FMAs (the fp32 gather: 7 per 192). Persistent CTAs pull row blocks from `ticket`,
+// prefetch the next block into L2 during the last column group, and publish each finished
+// block in `ready` (consumed by M += Q.W, see run_mixed_f32_resid).
+// RMW: M += (instead of =) the gather -- each column group's old M values are loaded at the
+// group's start (their latency hides under the shift loop) -- and the per-block ||M||^2 partials
+// of the final values go to msq_partial[blk] (fixed-order block sum).
+template <int NT, int CPT, bool RMW>
+__global__ void __launch_bounds__(NT, 1)
+    cycle_gather_f16_kernel(const uint4* __restrict__ Xh, const uint32_t* __restrict__ lamh,
+                            const int* __restrict__ J, int k, int kp, int n, int m_rows, float* __restrict__ M,
+                            const double* __restrict__ fro2_a, const double* __restrict__ fro2_b,
+                            int* __restrict__ ticket, int* __restrict__ ready, double* __restrict__ msq_partial) {
+  constexpr int LW = CPT / 2;  // lambda' words per thread per shift
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint4* Xs = reinterpret_cast<uint4*>(smem_raw);
+  int* sJ = reinterpret_cast<int*>(Xs + n);
+  __shared__ __align__(8) uint64_t bar;
+  __shared__ int s_blk, s_nxt;
+  __shared__ double red[32];
+  const int tid = threadIdx.x;
+  const int nblk = (int)ceil_div(m_rows, kHR);
+  const float inv = ldexpf(1.f, f16_scale_exp(*fro2_a) + f16_scale_exp(*fro2_b) - 30);
+  for (int t = tid; t < kp; t += NT) sJ[t] = t < k ? J[t] : 0;  // padded shifts: zero lambda' rows
+  if (tid == 0) {
+    mbar_init(&bar, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    s_nxt = -1;
+  }
+  const uint32_t bytes = (uint32_t)n * 16u;
+  const int groups = n / (CPT * NT);
+  for (int it = 0;; ++it) {
+    if (tid == 0) {
+      s_blk = (s_nxt < 0) ? atomicAdd(ticket, 1) : s_nxt;
+      s_nxt = -1;
+      if (s_blk < nblk) {
+        // the previous block's generic-proxy reads of Xs are ordered before this async write by
+        // the barrier that ended it; the proxy fence makes that ordering hold across proxies
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
+                         (uint32_t)__cvta_generic_to_shared(&bar)),
+                     "r"(bytes)
+                     : "memory");
+        asm volatile(
+            "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                (uint32_t)__cvta_generic_to_shared(Xs)),
+            "l"(Xh + (size_t)s_blk * n), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(&bar))
+            : "memory");
+      }
+    }
+    __syncthreads();
+    const int blk = s_blk;
+    if (blk >= nblk) break;
+    const int r0 = blk * kHR;
+    const int rows = min(kHR, m_rows - r0);
+    mbar_wait(&bar, (uint32_t)(it & 1));
+    double msq = 0.0;
+    for (int g = 0; g < groups; ++g) {
+      if (g == groups - 1 && tid == 0) {
+        const int nx = atomicAdd(ticket, 1);
+        s_nxt = nx;
+        if (nx < nblk)
+          asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(Xh + (size_t)nx * n), "r"(bytes) : "memory");
+      }
+      const int cbase = g * CPT * NT + tid;
+      float mold[RMW ? CPT : 1][RMW ? kHR : 1];
+      if constexpr (RMW) {
+#pragma unroll
+        for (int r = 0; r < kHR; ++r)
+#pragma unroll
+          for (int q = 0; q < CPT; ++q)
+            mold[q][r] = r < rows ? __ldcg(M + (size_t)(r0 + r) * n + cbase + q * NT) : 0.f;
+      }
+      const uint32_t* lrow = lamh + ((size_t)g * NT + tid) * LW;
+      const size_t lstride = (size_t)(n / CPT) * LW;
+      float acc[CPT][kHR];
+#pragma unroll
+      for (int q = 0; q < CPT; ++q)
+#pragma unroll
+        for (int r = 0; r < kHR; ++r) acc[q][r] = 0.f;
+      // batch b + 1's lambda' loads are in flight while batch b is consumed
+      uint32_t lvA[kHU][LW], lvB[kHU][LW];
+#pragma unroll
+      for (int u = 0; u < kHU; ++u) ldg_nc_words<LW>(lrow + (size_t)u * lstride, lvA[u]);
+      auto compute = [&](int t0, const uint32_t (&lv)[kHU][LW]) {
+#pragma unroll
+        for (int u = 0; u < kHU; ++u) {
+          const int jt = sJ[t0 + u];
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) {
+            unsigned m = (unsigned)(cbase + q * NT + jt);
+            m = min(m, m - (unsigned)n);
+            APX_DCHECK(m < (unsigned)n);
+            const uint4 x = Xs[m];
+            const unsigned short l = (q & 1) ? hi16(lv[u][q >> 1]) : lo16(lv[u][q >> 1]);
+            acc[q][0] = fhfma(lo16(x.x), l, acc[q][0]);
+            acc[q][1] = fhfma(hi16(x.x), l, acc[q][1]);
+            acc[q][2] = fhfma(lo16(x.y), l, acc[q][2]);
+            acc[q][3] = fhfma(hi16(x.y), l, acc[q][3]);
+            acc[q][4] = fhfma(lo16(x.z), l, acc[q][4]);
+            acc[q][5] = fhfma(hi16(x.z), l, acc[q][5]);
+            acc[q][6] = fhfma(lo16(x.w), l, acc[q][6]);
+            acc[q][7] = fhfma(hi16(x.w), l, acc[q][7]);
+          }
+        }
+      };
+      for (int t0 = 0; t0 < kp; t0 += 2 * kHU) {
+        if (t0 + kHU < kp) {
+#pragma unroll
+          for (int u = 0; u < kHU; ++u) ldg_nc_words<LW>(lrow + (size_t)(t0 + kHU + u) * lstride, lvB[u]);
+        }
+        compute(t0, lvA);
+        if (t0 + kHU >= kp) break;
+        if (t0 + 2 * kHU < kp) {
+#pragma unroll
+          for (int u = 0; u < kHU; ++u) ldg_nc_words<LW>(lrow + (size_t)(t0 + 2 * kHU + u) * lstride, lvA[u]);
+        }
+        compute(t0 + kHU, lvB);
+      }
+#pragma unroll
+      for (int r = 0; r < kHR; ++r)
+        if (r < rows) {
+          float* mp = M + (size_t)(r0 + r) * n + cbase;
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) {
+            if constexpr (RMW) {
+              const float v = fmaf(acc[q][r], inv, mold[q][r]);
+              mp[q * NT] = v;
+              msq = fma((double)v, (double)v, msq);
+            } else {
+              mp[q * NT] = acc[q][r] * inv;
+            }
+          }
+        }
+    }
+    if constexpr (RMW) {
+      msq = block_sum(msq, red);
+      if (tid == 0) msq_partial[blk] = msq;
+    }
+    __syncthreads();  // every M store of the block, and every read of Xs, precede what follows
+    if (tid == 0 && ready) {
+      __threadfence();
+      atomicExch(ready + blk, 1);
+    }
+  }
+}
+
+// gather shape (threads per CTA = column stride, columns per thread): APX_F16_CFG="NTxCPT"
+// overrides (tuning); the default is the largest NT of the preferred CPT that tiles n
+struct F16Cfg {
+  int nt, cpt;
+};
+F16Cfg f16_cfg(int n) {
+  static const F16Cfg env = [] {
+    F16Cfg c{0, 0};
+    if (const char* e = getenv("APX_F16_CFG")) sscanf(e, "%dx%d", &c.nt, &c.cpt);
+    return c;
+  }();
+  if (env.nt > 0 && (env.cpt == 2 || env.cpt == 4) && n % (env.nt * env.cpt) == 0) return env;
+  // two columns per thread: the same shared/L1 wavefronts per FMA as four, and registers left for
+  // the read-modify-write's old values (126 at 512 threads, no spills)
+  if (n % 1024 == 0) return {512, 2};
+  if (n % 512 == 0) return {256, 2};
+  return {0, 0};
+}
+
+}  // namespace
+
+int launch_split_tf32(const float* X, size_t count, float* X2, cudaStream_t st) {
+  const unsigned blocks = (unsigned)std::min<size_t>(ceil_div(count, (size_t)256), (size_t)kNumSMs * 8);
+  split_tf32_kernel<<<blocks, 256, 0, st>>>(X, count, X2);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+int launch_round_tf32(float* X, size_t count, cudaStream_t st) {
+  const unsigned blocks = (unsigned)std::min<size_t>(ceil_div(count, (size_t)256), (size_t)kNumSMs * 8);
+  round_tf32_kernel<<<blocks, 256, 0, st>>>(X, count);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+int launch_dup_cols(const float* Q, int rows, int l, float* Q2, cudaStream_t st) {
+  const unsigned blocks = (unsigned)std::min<size_t>(ceil_div((size_t)rows * l, (size_t)256), (size_t)kNumSMs * 8);
+  dup_cols_kernel<<<blocks, 256, 0, st>>>(Q, rows, l, Q2);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+// threads per CTA (= column stride) of the f16 gather for n, or 0 when n does not fit its layout
+int gather_f16_threads(int n) { return f16_cfg(n).nt; }
+
+size_t gather_f16_smem(int n, int kp) { return (size_t)n * 16 + (size_t)kp * sizeof(int); }
+
+int launch_lam_f16(const float* lam, int kp, int n, const double* fro2_b, uint16_t* out, cudaStream_t st) {
+  const F16Cfg c = f16_cfg(n);
+  APX_REQUIRE(c.nt > 0, "f16 gather: n=%d must be a multiple of 512", n);
+  const size_t count = (size_t)kp * (n / c.cpt);
+  const unsigned blocks = (unsigned)std::min<size_t>(ceil_div(count, (size_t)256), (size_t)kNumSMs * 8);
+  lam_f16_kernel<<<blocks, 256, 0, st>>>(lam, kp, n, c.nt, c.cpt, fro2_b, reinterpret_cast<uint32_t*>(out));
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+int launch_gather_f16(const uint16_t* Xh, const uint16_t* lamh, const int* J, int k, int kp, int n, int m_rows, float* M,
+                      const double* fro2_a, const double* fro2_b, int* ticket, int* ready, int ctas, cudaStream_t st,
+                      double* msq_partial) {
+  const F16Cfg c = f16_cfg(n);
+  APX_REQUIRE(c.nt > 0, "f16 gather: n=%d must be a multiple of 512", n);
+  APX_REQUIRE(kp % (2 * kHU) == 0 && kp > 0, "f16 gather: shift count %d must be a positive multiple of 8", kp);
+  const size_t smem = gather_f16_smem(n, kp);
+  APX_REQUIRE(smem <= 220 * 1024, "f16 gather: n=%d needs %zu bytes of shared memory", n, smem);
+  const int nblk = (int)ceil_div(m_rows, kHR);
+  const unsigned grid = (unsigned)std::max(1, std::min(nblk, ctas));
+  APX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
+  auto go = [&](auto kern) -> int {
+    APX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, c.nt, smem, st>>>(reinterpret_cast<const uint4*>(Xh), reinterpret_cast<const uint32_t*>(lamh), J, k,
+                                   kp, n, m_rows, M, fro2_a, fro2_b, ticket, ready, msq_partial);
+    APX_LAUNCH_CHECK();
+    return OK;
+  };
+#define APX_F16(NTV, CPTV)                                                                        \
+  if (c.nt == NTV && c.cpt == CPTV)                                                                \
+    return msq_partial ? go(cycle_gather_f16_kernel<NTV, CPTV, true>) : go(cycle_gather_f16_kernel<NTV, CPTV, false>);
+  APX_F16(512, 4) APX_F16(256, 4) APX_F16(128, 4) APX_F16(1024, 2) APX_F16(512, 2) APX_F16(256, 2)
+#undef APX_F16
+  set_error("f16 gather: unsupported shape %dx%d", c.nt, c.cpt);
+  return E_ARG;
+}
+
+}  // namespace apx

@@ -116,9 +116,15 @@ __global__ void __launch_bounds__(kThreads, 1)
                     float* __restrict__ C, int64_t ldc, int64_t c_split_stride, int M, int N, int K,
                     int k_per_split, int accumulate, const int* __restrict__ mJ, int mk, int mod_n,
                     double* __restrict__ sq_partial, int c_async, const int* __restrict__ ready, int ready_rows,
-                    const int* __restrict__ progress, int* __restrict__ defer, unsigned long long stall_ns) {
+                    const int* __restrict__ progress, int* __restrict__ defer, unsigned long long stall_ns,
+                    uint16_t* __restrict__ hout, const double* __restrict__ hscale) {
   using CF = Cfg<BN, STAGES>;
-  constexpr bool MASK = FIX == 1, ROUND = FIX == 2, FIXUP = FIX != 0;
+  // FIX 3: FIX 2 plus the sum of squares of the A operand (before rounding) into sq_partial.
+  // FIX 4: residual epilogue -- C is an fp32 INPUT X; the CTA writes f16(2^(15-e) (X - acc)) to
+  // hout in the row-block-interleaved layout of the f16 gather (8 rows x 2 bytes per column),
+  // e = f16_scale_exp(*hscale) (hscale = ||X||_F^2, so no value can overflow f16).
+  constexpr bool MASK = FIX == 1, ROUND = FIX == 2 || FIX == 3, FIXUP = FIX >= 1 && FIX <= 3;
+  constexpr bool OPSQ = FIX == 3, DELTA = FIX == 4;
   extern __shared__ unsigned char smem_raw[];
   // 1024-byte alignment for the swizzled tiles
   // 1024-byte alignment by pointer arithmetic on the shared array (an integer round trip would
@@ -211,6 +217,7 @@ __global__ void __launch_bounds__(kThreads, 1)
   } else {
     // ---------------- mask fix-up (dB^T) + epilogue ----------------
     const int et = threadIdx.x - 64;  // 0..127
+    double osq = 0.0;                  // FIX 3: this thread's share of the A operand's squares
     if (MASK) {
       for (int kt = 0; kt < ktiles; ++kt) {
         const int s = kt % STAGES;
@@ -248,17 +255,25 @@ __global__ void __launch_bounds__(kThreads, 1)
         // every 4-byte word of the A tile is an operand value: round in place (the B operand,
         // Q, is produced already rounded: qr_orthonormalize(..., tf32 = 1))
         uint4* w = reinterpret_cast<uint4*>(smem + (size_t)s * CF::kStage);
+        float osq32 = 0.f;
 #pragma unroll 4
         for (int v = et; v < CF::kTileA / 16; v += 128) {
           // round the magnitude half-up at bit 13 (sign-magnitude: an integer add on the bits;
           // a carry into the exponent is the correct rounding): two integer ops per value
           uint4 x = w[v];
+          if constexpr (OPSQ) {
+            osq32 = fmaf(__uint_as_float(x.x), __uint_as_float(x.x), osq32);
+            osq32 = fmaf(__uint_as_float(x.y), __uint_as_float(x.y), osq32);
+            osq32 = fmaf(__uint_as_float(x.z), __uint_as_float(x.z), osq32);
+            osq32 = fmaf(__uint_as_float(x.w), __uint_as_float(x.w), osq32);
+          }
           x.x = (x.x + 0x1000u) & 0xffffe000u;
           x.y = (x.y + 0x1000u) & 0xffffe000u;
           x.z = (x.z + 0x1000u) & 0xffffe000u;
           x.w = (x.w + 0x1000u) & 0xffffe000u;
           w[v] = x;
         }
+        osq += (double)osq32;  // one short fp32 partial per K-tile, folded in fp64
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         __syncwarp();
         if (lane == 0) mbar_arrive(&masked[s]);
@@ -267,6 +282,14 @@ __global__ void __launch_bounds__(kThreads, 1)
     // C tile staged through the (drained) operand ring for a read-modify-write epilogue
     constexpr bool kStageC = !TRANS_OUT && (size_t)STAGES * CF::kStage >= (size_t)BM * BN * 4;
     bool stage_c = kStageC && accumulate && c_async;
+    if (DELTA) {
+      // the residual epilogue stages this CTA's X tile (an HBM read): pull it into L2 during the
+      // main loop, one 128-byte line per thread per step
+      for (int e = et; e < BM * (BN / 32); e += 128) {
+        const int r = m0 + e / (BN / 32), c = n0 + (e % (BN / 32)) * 32;
+        if (r < M && c < N) asm volatile("prefetch.global.L2 [%0];" ::"l"(C + (size_t)r * ldc + c));
+      }
+    }
     if (accumulate && !TRANS_OUT && !stage_c) {
       // the read-modify-write epilogue reads this CTA's C tile: start pulling it toward L2 now
       // (overlaps the main loop); 128 threads x BN/32 lines per row group
@@ -279,6 +302,71 @@ __global__ void __launch_bounds__(kThreads, 1)
     }
     mbar_wait(done, 0);
     fence_after();
+    if constexpr (DELTA) {
+      // X tile staged through the drained ring (cp.async, XOR-swizzled granules as in the
+      // read-modify-write path below), v = s (X - acc) in place, then 8-row groups stored as one
+      // 16-byte f16 vector per column: a warp writes 32 consecutive columns = 512 contiguous bytes
+      static_assert((size_t)STAGES * CF::kStage >= (size_t)BM * BN * 4, "residual epilogue needs the staged tile");
+      const int quarter = warp & 3;
+      constexpr int GPR = BN / 4;
+      float* creg = reinterpret_cast<float*>(smem) + (size_t)quarter * 32 * BN;
+      const int rbase = m0 + quarter * 32;
+      const float* X = C;
+#pragma unroll 4
+      for (int g = lane; g < 32 * GPR; g += 32) {
+        const int r = g / GPR, gc = g - r * GPR;
+        const int rg = rbase + r, cg = n0 + gc * 4;
+        const bool ok = rg < M && cg < N;
+        const float* src = ok ? X + (size_t)rg * ldc + cg : X;
+        asm volatile("cp.async.cg.shared.global [%0], [%1], 16, %2;" ::"r"(saddr(creg + r * BN + ((gc ^ (r & 7)) << 2))),
+                     "l"(src), "r"(ok ? 16 : 0)
+                     : "memory");
+      }
+      asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
+      __syncwarp();
+      const float sc = ldexpf(1.f, 15 - f16_scale_exp(*hscale));
+#pragma unroll 1
+      for (int j0 = 0; j0 < BN; j0 += 32) {
+        float v[32];
+        if (ktiles > 0) {
+          tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)j0, v);
+        } else {
+#pragma unroll
+          for (int i = 0; i < 32; ++i) v[i] = 0.f;
+        }
+        float* rowp = creg + lane * BN;
+#pragma unroll
+        for (int i = 0; i < 8; ++i) {
+          float4* p4 = reinterpret_cast<float4*>(rowp + ((((j0 >> 2) + i) ^ (lane & 7)) << 2));
+          float4 o = *p4;
+          o.x = sc * (o.x - v[4 * i]);
+          o.y = sc * (o.y - v[4 * i + 1]);
+          o.z = sc * (o.z - v[4 * i + 2]);
+          o.w = sc * (o.w - v[4 * i + 3]);
+          *p4 = o;
+        }
+      }
+      __syncwarp();
+#pragma unroll 1
+      for (int g8 = 0; g8 < 4; ++g8) {
+        const int r8 = rbase + 8 * g8;
+        if (r8 >= M) break;
+        uint4* dst = reinterpret_cast<uint4*>(hout) + (size_t)(r8 >> 3) * N + n0;
+#pragma unroll
+        for (int j0 = 0; j0 < BN; j0 += 32) {
+          const int c = j0 + lane;
+          uint32_t w[4];
+#pragma unroll
+          for (int h = 0; h < 4; ++h) {
+            const int ra = 8 * g8 + 2 * h, rb = ra + 1;
+            const float a = creg[ra * BN + ((((c >> 2) ^ (ra & 7))) << 2) + (c & 3)];
+            const float b = creg[rb * BN + ((((c >> 2) ^ (rb & 7))) << 2) + (c & 3)];
+            w[h] = pack_half2(a, b);
+          }
+          if (n0 + c < N) dst[c] = make_uint4(w[0], w[1], w[2], w[3]);
+        }
+      }
+    } else {
     bool deferred = false;
     if (ready != nullptr && accumulate) {
       // C rows are produced by a concurrent kernel (the persistent gather) that publishes one flag
@@ -454,6 +542,7 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
     }
     if (sq_partial) {
+      if constexpr (OPSQ) sq = osq;
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
       if (lane == 0) sq_red[quarter] = sq;
@@ -462,6 +551,7 @@ __global__ void __launch_bounds__(kThreads, 1)
         sq_partial[((size_t)blockIdx.z * gridDim.y + blockIdx.y) * gridDim.x + blockIdx.x] =
             (sq_red[0] + sq_red[1]) + (sq_red[2] + sq_red[3]);
     }
+    }  // !DELTA
   }
   fence_before();
   __syncthreads();
@@ -528,7 +618,7 @@ template <int BN, int STAGES, bool A_MN, bool B_MN, bool TRANS_OUT, int FIX>
 static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                   int64_t c_split_stride, int M, int N, int K, int splits, int accumulate, const int* mJ, int mk,
                   int mod_n, double* sq_partial, const int* ready, int ready_rows, const int* progress,
-                  int* defer, cudaStream_t st) {
+                  int* defer, uint16_t* hout, const double* hscale, cudaStream_t st) {
   using CF = Cfg<BN, STAGES>;
   CUtensorMap ta, tb;
   // A operand: K-major stored [M][K]; MN-major stored [K][M]
@@ -540,7 +630,8 @@ static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, floa
   APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem));
   const int c_async = ((uintptr_t)C % 16) == 0 && (ldc % 4) == 0 && (N % 4) == 0 && (c_split_stride % 4) == 0;
   fn<<<grid, kThreads, CF::kSmem, st>>>(ta, tb, C, ldc, c_split_stride, M, N, K, kps, accumulate, mJ, mk, mod_n,
-                                        sq_partial, c_async, ready, ready_rows, progress, defer, stall_ns());
+                                        sq_partial, c_async, ready, ready_rows, progress, defer, stall_ns(), hout,
+                                        hscale);
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -599,7 +690,7 @@ int launch_qw_fixup_sum(const float* Q, int64_t ldq, const float* W, int64_t ldw
 int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                   int64_t ldc, int64_t c_split_stride, int M, int N, int K, int splits, int accumulate,
                   const int* mJ, int mk, int mod_n, cudaStream_t st, double* sq_partial, const int* ready,
-                  int ready_rows, const int* progress, int* defer) {
+                  int ready_rows, const int* progress, int* defer, uint16_t* hout, const double* hscale) {
   APX_REQUIRE(ready == nullptr || (accumulate && ready_rows > 0 && splits == 1 && !(layout & 4)),
               "umma_tma_gemm: ready flags need an accumulating, split-free, row-major C");
   APX_REQUIRE(defer == nullptr || (ready != nullptr && progress != nullptr && sq_partial != nullptr),
@@ -608,20 +699,26 @@ int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* 
   APX_REQUIRE(((uintptr_t)A % 16) == 0 && ((uintptr_t)B % 16) == 0 && (lda % 4) == 0 && (ldb % 4) == 0,
               "umma_tma_gemm: 16-byte aligned operands required");
   const bool mask = mJ != nullptr && mk > 0;
-  const int fix = mask ? 1 : (layout & 8) ? 2 : 0;  // layout bit 8: round operands to TF32 nearest
+  // layout bit 8: round the A operand to TF32 nearest (+ bit 16: its sum of squares into
+  // sq_partial); bit 32: residual epilogue (C is the fp32 input X, the f16 result goes to hout)
+  const int fix = mask ? 1 : (layout & 32) ? 4 : (layout & 8) ? ((layout & 16) ? 3 : 2) : 0;
+  APX_REQUIRE(fix != 4 || (hout != nullptr && hscale != nullptr && splits == 1 && (layout & 7) == 2 && bn == 128 &&
+                           ((uintptr_t)hout % 16) == 0 && (N % 4) == 0 && ((uintptr_t)C % 16) == 0 && (ldc % 4) == 0),
+              "umma_tma_gemm: residual epilogue needs hout, hscale, layout 2, BN 128, no split, aligned X");
   layout &= 7;
-  // ring depth: BN 128 with K <= 2 K-tiles needs only 2 stages (and then fits a staged C tile)
-  const int stages = bn == 256 ? 2 : (bn == 128 && K <= 2 * tma::BK) ? 2 : 4;
+  // ring depth: BN 128 with K <= 4 K-tiles runs 2 stages (64 KB: three CTAs per SM, and the
+  // drained ring holds a staged C tile)
+  const int stages = bn == 256 ? 2 : (bn == 128 && K <= 4 * tma::BK) ? 2 : 4;
 #define APX_TL(BNV, ST, L, FX)                                                                               \
   if (bn == BNV && stages == ST && layout == L && fix == FX)                                                 \
     return tma::launch<BNV, ST, (L & 1) != 0, (L & 2) != 0, (L & 4) != 0, FX>(A, lda, B, ldb, C, ldc,         \
                                                                               c_split_stride, M, N, K, splits, \
                                                                               accumulate, mJ, mk, mod_n,       \
                                                                               sq_partial, ready, ready_rows,   \
-                                                                              progress, defer, st);
+                                                                              progress, defer, hout, hscale, st);
   APX_TL(64, 4, 0, 0) APX_TL(64, 4, 1, 0) APX_TL(64, 4, 2, 0) APX_TL(64, 4, 3, 0)
   APX_TL(64, 4, 4, 0) APX_TL(64, 4, 5, 0) APX_TL(64, 4, 6, 0) APX_TL(64, 4, 7, 0)
-  APX_TL(64, 4, 1, 1) APX_TL(64, 4, 5, 1) APX_TL(64, 4, 7, 2)
+  APX_TL(64, 4, 1, 1) APX_TL(64, 4, 5, 1) APX_TL(64, 4, 7, 2) APX_TL(64, 4, 7, 3) APX_TL(128, 2, 2, 4)
   APX_TL(128, 4, 0, 0) APX_TL(128, 4, 2, 0) APX_TL(256, 2, 0, 0) APX_TL(256, 2, 2, 0)
   APX_TL(128, 2, 0, 0) APX_TL(128, 2, 2, 0)
 #undef APX_TL

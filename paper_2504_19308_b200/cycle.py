@@ -94,8 +94,12 @@ def draw_sketch(n: int, k: int, seed) -> "np.ndarray":
 
 
 def mixed_product_device(A, B, k_svd: int, k_cyc: int, order: int, omega, power_iterations: int = 0,
-                         force_sel_b=None, split3: bool = False, out=None):
-    """Device-level mixed product (config C4). omega: device tensor n x k_svd (A's dtype)."""
+                         force_sel_b=None, split3: bool = False, out=None, direct: bool = False):
+    """Device-level mixed product (config C4). omega: device tensor n x k_svd (A's dtype).
+
+    fp32 order 1 runs the residual plan (M = Q (Bm B) + dA Bhat with dA in scaled f16, see
+    csrc/mixed_f16.cu) where the shape allows; ``direct=True`` forces the all-fp32 plan
+    (M = A Bhat + Q W with the gather over A)."""
     n = A.shape[0]
     code = N.APX_F32 if A.dtype == torch.float32 else N.APX_F64
     dev = A.device
@@ -105,16 +109,17 @@ def mixed_product_device(A, B, k_svd: int, k_cyc: int, order: int, omega, power_
     scal = torch.zeros(N.NSCALARS, dtype=torch.float64, device=dev)
     ws = D.workspace(N.size("apx_mixed_first_order_workspace", code, n, k_svd, k_cyc, order))
     N.call("apx_mixed_first_order", code, A.data_ptr(), B.data_ptr(), n, k_svd, k_cyc, order,
-           power_iterations, omega.data_ptr(), D.ptr(fb), 1 if split3 else 0, M.data_ptr(),
+           power_iterations, omega.data_ptr(), D.ptr(fb), (1 if split3 else 0) | (4 if direct else 0), M.data_ptr(),
            sb.data_ptr(), scal.data_ptr(), ws.data_ptr(), ws.numel(), D.stream_ptr())
     return {"M": M, "sel_b": sb[:k_cyc], "scalars": scal, "ws": ws}
 
 
 def mixed_first_order_multiply(A, B, k_svd: int, k_cyc: int, order: int, seed,
                                power_iterations: int = 0, model: ErrorModel | None = None,
-                               force_sel_b=None, split3: bool = False, out=None):
+                               force_sel_b=None, split3: bool = False, out=None, direct: bool = False):
     """Approximate A @ B with A truncated by randomized SVD (rank k_svd, svd.py:83-119) and B by
-    its k_cyc dominant cycles (config C4). Returns (M, ApproxReport(method="mixed"))."""
+    its k_cyc dominant cycles (config C4). Returns (M, ApproxReport(method="mixed")).
+    ``direct``: see mixed_product_device."""
     Ad, _, host = D.as_device_matrix(A, real_only=True)
     Bd, _, _ = D.as_device_matrix(B, real_only=True)
     n = Ad.shape[0]
@@ -131,7 +136,8 @@ def mixed_first_order_multiply(A, B, k_svd: int, k_cyc: int, order: int, seed,
     omega = torch.from_numpy(draw_sketch(n, k_svd, seed)).to(device=Ad.device, dtype=Ad.dtype)
     torch.cuda.synchronize()
     t0 = time.perf_counter()
-    r = mixed_product_device(Ad, Bd, k_svd, k_cyc, order, omega, power_iterations, force_sel_b, split3)
+    r = mixed_product_device(Ad, Bd, k_svd, k_cyc, order, omega, power_iterations, force_sel_b, split3,
+                             direct=direct)
     s = r["scalars"].tolist()
     wall = time.perf_counter() - t0
     nA, nB, ndA, ndB, nM = _norms(s, n * n)

@@ -37,20 +37,71 @@ def test_mixed_fp64_vs_oracle(P, n, ks, kc, q, order):
     assert rep.norm_db == pytest.approx(ro["norm_db"], rel=1e-6)
 
 
-@pytest.mark.parametrize("split3", [False, True])
-def test_mixed_fp32_c4_shape(P, split3):
-    """C4 structure (sigma_i=(i+1)^-1.5 Haar A; 64-cycle B) at n=1024, fp32 tensors, tol 1e-4."""
+@pytest.mark.parametrize("split3,direct", [(False, False), (False, True), (True, False)])
+def test_mixed_fp32_c4_shape(P, split3, direct):
+    """C4 structure (sigma_i=(i+1)^-1.5 Haar A; 64-cycle B) at n=1024, fp32 tensors, tol 1e-4:
+    the residual plan (default: f16 gather over dA), the all-fp32 plan (direct) and 3xTF32."""
     n, k = 1024, 64
     A = O.gen_haar_spectrum(n, (np.arange(n) + 1.0) ** -1.5, 8).astype(np.float32)
     B = O.gen_cycle_operand(n, 64, 9).astype(np.float32)
     Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
-    M, rep = P.mixed_first_order_multiply(Ad, Bd, k, k, 1, seed=4, split3=split3)
+    M, rep = P.mixed_first_order_multiply(Ad, Bd, k, k, 1, seed=4, split3=split3, direct=direct)
     assert M.dtype == torch.float32
     Mo, ro = O.mixed_first_order_multiply(A.astype(np.float64), B.astype(np.float64), k, k, 1, 4)
     assert rep.selected_b == ro["selected_b"]
     err = rel(M.cpu().numpy(), Mo)
-    print(f"fp32 mixed n={n} split3={split3}: rel vs oracle {err:.3e}")
+    print(f"fp32 mixed n={n} split3={split3} direct={direct}: rel vs oracle {err:.3e}")
     assert err < 1e-4
+    assert rep.posterior_estimate == pytest.approx(ro["posterior_estimate"], rel=0.15)
+
+
+def _device_norms(P, A, B, kc, seed, direct):
+    """(||A||^2, ||M||^2) from the device scalars of one product."""
+    from paper_2504_19308_b200 import _native as N
+    n = A.shape[0]
+    omega = torch.from_numpy(P.cycle.draw_sketch(n, 64, seed)).cuda().float()
+    r = P.mixed_product_device(A, B, 64, kc, 1, omega, direct=direct)
+    s = r["scalars"].tolist()
+    return s[N.S_FRO2_A], s[N.S_FRO2_M], r["M"]
+
+
+@pytest.mark.parametrize("n,kc,seed", [(512, 64, 1), (1536, 40, 2), (2048, 128, 3), (1024, 1, 4)])
+def test_mixed_resid_plan_vs_oracle(P, n, kc, seed):
+    """Residual plan shapes: thread groups of 128/256/512 columns, k_cyc from 1 to 128 (the f16
+    lambda' table's zero padding), ||A||, ||M|| and the selection vs the fp64 oracle."""
+    A = O.gen_haar_spectrum(n, (np.arange(n) + 1.0) ** -1.5, seed).astype(np.float32)
+    B = O.gen_cycle_operand(n, kc, seed + 50).astype(np.float32)  # dB = the noise: TF32-small
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    M, rep = P.mixed_first_order_multiply(Ad, Bd, 64, kc, 1, seed=seed)
+    Md, repd = P.mixed_first_order_multiply(Ad, Bd, 64, kc, 1, seed=seed, direct=True)
+    Mo, ro = O.mixed_first_order_multiply(A.astype(np.float64), B.astype(np.float64), 64, kc, 1, seed)
+    assert rep.selected_b == ro["selected_b"] == repd.selected_b
+    e_r, e_d = rel(M.cpu().numpy(), Mo), rel(Md.cpu().numpy(), Mo)
+    print(f"n={n} kc={kc}: residual plan {e_r:.3e}, direct plan {e_d:.3e}")
+    assert e_r < 1e-4 and e_d < 1e-4
+    # energy difference (3e-4 of ||A||^2): the plans split the Bm GEMM differently
+    assert rep.norm_da == pytest.approx(repd.norm_da, rel=2e-2)
+    fa, fm, Mr = _device_norms(P, Ad, Bd, kc, seed, False)
+    assert fa == pytest.approx(float(np.sum(A.astype(np.float64) ** 2)), rel=1e-6)
+    assert fm == pytest.approx(float(torch.sum(Mr.double() ** 2)), rel=1e-6)
+    assert fm == pytest.approx(ro["norm_m"] ** 2, rel=2e-4)
+
+
+def test_mixed_resid_plan_extreme_scales(P):
+    """The f16 scalings come from ||A||_F and ||B||_F: operands scaled by powers of two far outside
+    f16's range give the same relative result, with no f16 overflow or flush (the scales are
+    bounded by the fp32 range finder's Gram matrix, which must stay finite)."""
+    n, k = 512, 32
+    A = O.gen_haar_spectrum(n, (np.arange(n) + 1.0) ** -1.5, 5).astype(np.float32)
+    B = O.gen_cycle_operand(n, k, 6).astype(np.float32)
+    Mo, _ = O.mixed_first_order_multiply(A.astype(np.float64), B.astype(np.float64), 64, k, 1, 9)
+    for sa, sb in [(2.0 ** 20, 2.0 ** -20), (2.0 ** -24, 1.0), (1.0, 2.0 ** 24), (2.0 ** -12, 2.0 ** -12)]:
+        Ad = torch.from_numpy(A * np.float32(sa)).cuda()
+        Bd = torch.from_numpy(B * np.float32(sb)).cuda()
+        M, rep = P.mixed_first_order_multiply(Ad, Bd, 64, k, 1, seed=9)
+        err = rel(M.double().cpu().numpy() / (sa * sb), Mo)
+        assert np.isfinite(M.cpu().numpy()).all()
+        assert err < 1e-4, (sa, sb, err)
 
 
 def test_mixed_rank_deficient_sketch_fp64(P):

@@ -3,6 +3,7 @@
 // Timed with CUDA events; prints one JSON line.
 #include <cstdio>
 #include <cuda_runtime.h>
+#include <cuda_fp16.h>
 
 #define ITERS 4096
 __global__ void k_ffma(float* out, float s) {
@@ -27,6 +28,25 @@ __global__ void k_ffma2(float* out, float s) {
     for (int i = 0; i < 16; ++i) asm volatile("fma.rn.f32x2 %0, %0, %1, %2;" : "+l"(a[i]) : "l"(ss), "l"(hh));
   }
   float r = 0; for (int i = 0; i < 16; ++i) { float2 v = *reinterpret_cast<float2*>(&a[i]); r += v.x + v.y; }
+  if (r == 1234.5f) out[0] = r;
+}
+// mixed-precision FMA (sm_100: FHFMA): f16 x f16 products accumulated in fp32, the half operands
+// taken from the .H0 / .H1 halves of packed registers (the f16 residual gather's inner op)
+__global__ void k_fhfma(float* out, float s) {
+  float a[16];
+#pragma unroll
+  for (int i = 0; i < 16; ++i) a[i] = threadIdx.x * 1e-3f + i;
+  const unsigned x = 0x3c003bffu ^ (unsigned)threadIdx.x;  // two halves
+  unsigned short lo = (unsigned short)(x & 0xffff), hi = (unsigned short)(x >> 16);
+  unsigned short l = __half_as_ushort(__float2half_rn(s));  // scalar half operand
+  for (int it = 0; it < ITERS; ++it) {
+#pragma unroll
+    for (int i = 0; i < 16; ++i) {
+      if (i & 1) asm volatile("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(a[i]) : "h"(hi), "h"(l));
+      else asm volatile("fma.rn.f32.f16 %0, %1, %2, %0;" : "+f"(a[i]) : "h"(lo), "h"(l));
+    }
+  }
+  float r = 0; for (int i = 0; i < 16; ++i) r += a[i];
   if (r == 1234.5f) out[0] = r;
 }
 __global__ void k_dfma(double* out, double s) {
@@ -114,6 +134,8 @@ int main() {
   double ffma = nthr * ITERS * 16 * 2 / (t1 * 1e-3) / 1e12;
   float t2 = time_it([&] { k_ffma2<<<blocks, threads>>>(f, 0.999f); });
   double ffma2 = nthr * ITERS * 16 * 4 / (t2 * 1e-3) / 1e12;
+  float t2h = time_it([&] { k_fhfma<<<blocks, threads>>>(f, 0.999f); });
+  double fhfma = nthr * ITERS * 16 * 2 / (t2h * 1e-3) / 1e12;
   float t3 = time_it([&] { k_dfma<<<blocks, threads>>>(d, 0.999); });
   double dfma = nthr * (ITERS / 4) * 16 * 2 / (t3 * 1e-3) / 1e12;
   float t4 = time_it([&] { k_dmma<<<blocks, threads>>>(d); });
@@ -130,11 +152,11 @@ int main() {
   auto lds_tbs = [&](float t, int bytes) { return nthr * li * 16.0 * bytes / (t * 1e-3) / 1e12; };
   const double l32 = lds_tbs(t6, 4), l64 = lds_tbs(t7, 8), l128 = lds_tbs(t8, 16);
   const double hz = clk_khz * 1e3;
-  printf("{\"sms\": %d, \"fp32_ffma_tflops\": %.2f, \"fp32_ffma2_tflops\": %.2f, \"fp64_dfma_tflops\": %.2f, "
+  printf("{\"sms\": %d, \"fp32_ffma_tflops\": %.2f, \"fp32_ffma2_tflops\": %.2f, \"f16f32_fhfma_tflops\": %.2f, \"fp64_dfma_tflops\": %.2f, "
          "\"fp64_dmma_mma_sync_tflops\": %.2f, \"tf32_mma_sync_tflops\": %.2f, "
          "\"lds32_tbs\": %.2f, \"lds64_tbs\": %.2f, \"lds128_tbs\": %.2f, "
          "\"lds128_bytes_per_clk_per_sm_at_attr_clock\": %.1f, \"attr_clock_mhz\": %.0f, \"err\": \"%s\"}\n",
-         sms, ffma, ffma2, dfma, dmma, tf32, l32, l64, l128, l128 * 1e12 / hz / sms, hz / 1e6,
+         sms, ffma, ffma2, fhfma, dfma, dmma, tf32, l32, l64, l128, l128 * 1e12 / hz / sms, hz / 1e6,
          cudaGetErrorString(cudaGetLastError()));
   return 0;
 }
