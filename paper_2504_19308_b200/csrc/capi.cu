@@ -626,7 +626,17 @@ static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int
                                            nullptr, wchunks, /*tf32_operands=*/false));
   APX_TRY(launch_split_tf32(W, (size_t)l * n, p.W2, lo));
   stage_mark(6, lo);
-  APX_TRY(UmmaStages::q_times_w(p.Q2, p.W2, M, n, 2 * l, lo, 1, p.msq, p.ready, grows, p.ticket, defer));
+  // one tile per CTA (3 CTAs per SM on the SMs the gather leaves free). APX_QW_PERSIST=1: the
+  // persistent, TMEM double-buffered, dynamically scheduled kernel with TMA epilogues instead (same
+  // tile numbering, so the fixup is shared) -- faster alone (111 vs 114 us RMW, 75 vs 121 us plain
+  // store at n = 8192) but one CTA per SM beside the gather: 1109 vs 1133 products/s.
+  static const bool persist = getenv("APX_QW_PERSIST") != nullptr;
+  if (persist) {
+    APX_TRY(umma_persist_gemm(p.Q2, 2 * l, p.W2, n, M, n, n, n, 2 * l, 1, lo, p.msq, p.ready, grows, p.ticket, defer,
+                              device_sms(), 128, p.ticket + 1));
+  } else {
+    APX_TRY(UmmaStages::q_times_w(p.Q2, p.W2, M, n, 2 * l, lo, 1, p.msq, p.ready, grows, p.ticket, defer));
+  }
   stage_mark(7, lo);
   APX_CUDA(cudaStreamWaitEvent(lo, ss->hi_done, 0));
   APX_TRY(launch_qw_fixup_sum(p.Q2, 2 * l, p.W2, n, M, n, n, n, 2 * l, 128, defer, p.msq,
@@ -919,6 +929,12 @@ int apx_debug_umma_gemm(int layout, int bn, const float* A, int64_t lda, const f
                         int mask_k, int mod_n, void* stream) {
   APX_REQUIRE(M >= 1 && N >= 1 && K >= 1 && splits >= 1, "bad GEMM shape");
   const int64_t slice = (int64_t)((layout & 4) ? N : M) * ldc;
+  if (layout & 64) {  // persistent tile loop (layout 2 only); mod_n = CTA count (0: one per SM);
+    // layout bit 128: dynamic tile scheduling with mask_j as the (int) ticket counter
+    APX_REQUIRE((layout & 7) == 2 && splits == 1 && mask_k == 0, "persistent GEMM: layout 2, no split, no mask");
+    return umma_persist_gemm(A, lda, B, ldb, C, ldc, (int)M, (int)N, (int)K, accumulate, S(stream), nullptr, nullptr,
+                             0, nullptr, nullptr, mod_n, bn, (layout & 128) ? const_cast<int32_t*>(mask_j) : nullptr);
+  }
   if (layout & 32)
     return umma_tma_gemm(layout & 15, bn, A, lda, B, ldb, C, ldc, slice, (int)M, (int)N, (int)K, splits,
                          accumulate, mask_j, mask_k, mod_n, S(stream));

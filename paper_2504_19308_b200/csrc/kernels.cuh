@@ -81,6 +81,10 @@ int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* 
                   const int* mJ, int mk, int mod_n, cudaStream_t st, double* sq_partial = nullptr,
                   const int* ready = nullptr, int ready_rows = 0, const int* progress = nullptr,
                   int* defer = nullptr, uint16_t* hout = nullptr, const double* hscale = nullptr);
+int umma_persist_gemm(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int M, int N,
+                      int K, int accumulate, cudaStream_t st, double* sq_partial = nullptr, const int* ready = nullptr,
+                      int ready_rows = 0, const int* progress = nullptr, int* defer = nullptr, int ctas = 0,
+                      int bn = 128, int* ticket = nullptr);
 // deferred Q.W tiles of a ready-flag GEMM, then the fixed-order ||C||^2 sum (umma_tma.cu)
 int launch_qw_fixup_sum(const float* Q, int64_t ldq, const float* W, int64_t ldw, float* C, int64_t ldc, int M, int N,
                         int K, int bn, int* defer, double* sq_partial, int parts, double* out, cudaStream_t st);

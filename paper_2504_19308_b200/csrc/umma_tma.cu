@@ -636,6 +636,323 @@ static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, floa
   return OK;
 }
 
+
+// ---- persistent n x n tile loop: C[M x N] (=|+=) A[M x K] . B[K x N] ------------------------------
+// A K-major (row-major [M][K]), B MN-major (row-major [K][N]); the C4 product's M (+)= Q.W with a
+// short K (2l = 128). One CTA per SM walks tiles t = blockIdx.x + i * gridDim.x (row-band-major:
+// t = band * ceil(N/BN) + column tile), with the accumulator double-buffered in TMEM
+// (2 x BN columns): the MMA warp fills buffer (i+1)&1 while the epilogue warps drain buffer i&1,
+// and the TMA producer streams the K-chunks of the next tiles through a 4-stage ring. So the
+// HBM-bound epilogue (the C tile's read-modify-write) overlaps the next tile's operand loads,
+// which the one-tile-per-CTA kernel above serialises (~48% of the HBM bandwidth at 3 CTAs per SM).
+// Epilogue: 32 x 32 chunks transposed through shared memory (row-contiguous 128-byte stores),
+// ACC: all 16 old values of a half-chunk loaded before the first store; ready flags, bounded wait,
+// deferral and per-tile ||C||^2 partials exactly as gemm_tma_kernel (same tile numbering, so
+// qw_fixup_sum_kernel completes deferred tiles unchanged).
+constexpr int kPStages = 3;
+constexpr int kPQueue = 4;  // tile-id queue depth (dynamic scheduling)
+template <int BN>
+struct PCfg {
+  static constexpr int kTileA = BM * BK * 4;
+  static constexpr int kTileB = BN * BK * 4;
+  static constexpr int kStage = kTileA + kTileB;
+  static constexpr int kSlab = 32 * BN * 4;                // one epilogue warp's 32 x BN slab of C
+  static constexpr int kStaging = 4 * 2 * kSlab;           // double-buffered per warp
+  static constexpr size_t kSmem = (size_t)kPStages * kStage + kStaging + 1024 + 512;
+  static constexpr int kTmemCols = 2 * BN;
+};
+
+__device__ __forceinline__ void tma_store_2d(const CUtensorMap* map, int c0, int c1, uint32_t src) {
+  asm volatile("cp.async.bulk.tensor.2d.global.shared::cta.bulk_group [%0, {%1, %2}], [%3];" ::"l"(map), "r"(c0),
+               "r"(c1), "r"(src)
+               : "memory");
+}
+
+// Tile order: with `ticket` (dynamic), the producer claims tiles in ascending order from a global
+// counter and passes each id to the MMA warp and the epilogue through a kPQueue-deep shared queue
+// (tile_ready: producer -> consumers, release/acquire; tile_free: 1 MMA + 4 epilogue arrivals), so
+// whichever CTAs are resident work the lowest open tiles -- required when the CTAs only get SMs as a
+// concurrent kernel releases them and the epilogues wait on that kernel's row flags. Without a
+// ticket the tiles are strided statically (t = blockIdx.x + i * gridDim.x).
+// Epilogue: TMA in and out. Each epilogue warp owns a double-buffered 32 x BN slab of C laid out
+// as BN/32 boxes of 32 x 32 fp32 in the 128-byte swizzle (granule g of row r at g ^ (r & 7)): the
+// old C slab (ACC) arrives by TMA (issued before the accumulator wait, so it overlaps the MMAs),
+// the lane owning row r adds its TMEM row into its granules (conflict-free 16-byte accesses), and
+// one TMA store per box writes the slab back; the slab is reused two tiles later, after the
+// store has finished reading it (bulk wait_group.read).
+template <int BN, bool ACC>
+__global__ void __launch_bounds__(kThreads, 1)
+    gemm_persist_kernel(const __grid_constant__ CUtensorMap tmA, const __grid_constant__ CUtensorMap tmB,
+                        const __grid_constant__ CUtensorMap tmC, int M, int N, int K, double* __restrict__ sq_partial,
+                        const int* __restrict__ ready, int ready_rows, const int* __restrict__ progress,
+                        int* __restrict__ defer, unsigned long long stall_ns, int* __restrict__ ticket) {
+  using CF = PCfg<BN>;
+  extern __shared__ unsigned char smem_raw[];
+  unsigned char* smem = smem_raw + ((1024u - (saddr(smem_raw) & 1023u)) & 1023u);
+  unsigned char* stg = smem + (size_t)kPStages * CF::kStage;
+  uint64_t* full = reinterpret_cast<uint64_t*>(stg + CF::kStaging);
+  uint64_t* empty = full + kPStages;
+  uint64_t* acc_full = empty + kPStages;
+  uint64_t* acc_empty = acc_full + 2;
+  uint64_t* tile_ready = acc_empty + 2;
+  uint64_t* tile_free = tile_ready + kPQueue;
+  uint64_t* cbar = tile_free + kPQueue;  // [warp 0..3][slab 0..1]: the old C slab landed
+  int* tile_id = reinterpret_cast<int*>(cbar + 8);
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(tile_id + kPQueue);
+  __shared__ double sq_red[4];
+  __shared__ int s_deferred[4];
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int nct = (int)ceil_div(N, BN);
+  const int tiles = (int)ceil_div(M, BM) * nct;
+  const int kchunks = (int)ceil_div(K, BK);
+  if (warp == 0 && lane == 0) {
+    for (int s = 0; s < kPStages; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&acc_full[b], 1);
+      mbar_init(&acc_empty[b], 4);  // one arrival per epilogue warp
+    }
+    for (int q = 0; q < kPQueue; ++q) {
+      mbar_init(&tile_ready[q], 1);
+      mbar_init(&tile_free[q], 5);  // the MMA lane + one lane per epilogue warp
+    }
+    for (int q = 0; q < 8; ++q) mbar_init(&cbar[q], 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmA) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmB) : "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&tmC) : "memory");
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(saddr(tmem_slot)),
+                 "r"(CF::kTmemCols));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  fence_before();
+  __syncthreads();
+  fence_after();
+  const uint32_t tmem = *tmem_slot;
+  const uint32_t sbase = saddr(smem);
+  // consumer side of the tile queue: the i-th tile id (>= tiles: done)
+  auto next_tile = [&](int i, int t_static) -> int {
+    if (!ticket) return t_static;
+    const int q = i % kPQueue;
+    mbar_wait(&tile_ready[q], (uint32_t)((i / kPQueue) & 1));
+    return tile_id[q];
+  };
+  auto release_tile = [&](int i) {
+    if (ticket) mbar_arrive(&tile_free[i % kPQueue]);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      int g = 0;  // global K-chunk counter over this CTA's tiles
+      for (int i = 0;; ++i) {
+        int t;
+        if (ticket) {
+          const int q = i % kPQueue;
+          if (i >= kPQueue) mbar_wait(&tile_free[q], (uint32_t)(((i / kPQueue) - 1) & 1));
+          t = atomicAdd(ticket, 1);
+          tile_id[q] = t;
+          mbar_arrive(&tile_ready[q]);
+        } else {
+          t = blockIdx.x + i * gridDim.x;
+        }
+        if (t >= tiles) break;
+        const int m0 = (t / nct) * BM, n0 = (t % nct) * BN;
+        for (int kc = 0; kc < kchunks; ++kc, ++g) {
+          const int s = g % kPStages;
+          if (g >= kPStages) mbar_wait(&empty[s], (uint32_t)(((g / kPStages) - 1) & 1));
+          mbar_expect_tx(&full[s], (uint32_t)CF::kStage);
+          const uint32_t a_s = sbase + s * CF::kStage, b_s = a_s + CF::kTileA;
+          const int k0 = kc * BK;
+          tma_load_2d(a_s, &tmA, k0, m0, &full[s]);
+#pragma unroll
+          for (int a = 0; a < BN / 32; ++a) tma_load_2d(b_s + a * 4096, &tmB, n0 + 32 * a, k0, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    constexpr uint32_t id = idesc(BM, BN, false, true);
+    if (lane == 0) {
+      int g = 0;
+      for (int i = 0;; ++i) {
+        const int t = next_tile(i, blockIdx.x + i * gridDim.x);
+        release_tile(i);
+        if (t >= tiles) break;
+        const int b = i & 1;
+        if (i >= 2) mbar_wait(&acc_empty[b], (uint32_t)(((i >> 1) - 1) & 1));
+        fence_after();
+        const uint32_t d = tmem + (uint32_t)(b * BN);
+        for (int kc = 0; kc < kchunks; ++kc, ++g) {
+          const int s = g % kPStages;
+          mbar_wait(&full[s], (uint32_t)((g / kPStages) & 1));
+          fence_after();
+          const uint32_t a_s = sbase + s * CF::kStage, b_s = a_s + CF::kTileA;
+#pragma unroll
+          for (int kk = 0; kk < BK / 8; ++kk)
+            mma(d, desc(a_s + kk * 32, 16, 1024, 2), desc(b_s + kk * 1024, 4096, 512, 1), id,
+                (kc > 0 || kk > 0) ? 1u : 0u);
+          commit(&empty[s]);
+        }
+        commit(&acc_full[b]);
+      }
+    }
+  } else {
+    const int quarter = warp & 3, ew = warp - 2;
+    int loads = 0;  // per slab: C loads issued so far (mbarrier phase)
+    int lslab0 = 0, lslab1 = 0;
+    for (int i = 0;; ++i) {
+      int t = 0;
+      if (lane == 0) t = next_tile(i, blockIdx.x + i * gridDim.x);
+      t = __shfl_sync(0xffffffffu, t, 0);
+      __syncwarp();
+      if (lane == 0) release_tile(i);
+      if (t >= tiles) break;
+      const int b = i & 1;  // TMEM buffer and slab
+      const int m0 = (t / nct) * BM, n0 = (t % nct) * BN;
+      const int rbase = m0 + quarter * 32;
+      unsigned char* slab = stg + (size_t)(ew * 2 + b) * CF::kSlab;
+      const uint32_t slab_s = saddr(slab);
+      uint64_t* cb = &cbar[ew * 2 + b];
+      bool deferred = false;
+      if (ACC && ready != nullptr) {
+        // wait (acquire) for the producer's row blocks under this warp's 32 rows; bounded as in
+        // gemm_tma_kernel: a producer without progress for stall_ns defers the tile
+        const int b0 = rbase / ready_rows, b1 = (min(M, rbase + 32) - 1) / ready_rows;
+        bool stalled = defer != nullptr && stall_ns == 0;
+        unsigned long long t0 = 0;
+        int last = 0;
+        if (defer && lane == 0) {
+          asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+          last = ld_relaxed_gpu(progress);
+        }
+        for (int bb = b0; bb <= b1 && !stalled && rbase < M; bb += 32) {
+          const int fb = bb + lane;
+          while (!__all_sync(0xffffffffu, fb > b1 || ld_relaxed_gpu(ready + fb) != 0)) {
+            __nanosleep(128);
+            if (defer) {
+              int st = 0;
+              if (lane == 0) {
+                unsigned long long now;
+                asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+                const int cur = ld_relaxed_gpu(progress);
+                if (cur != last) {
+                  last = cur;
+                  t0 = now;
+                } else if (now - t0 > stall_ns) {
+                  st = 1;
+                }
+              }
+              if (__shfl_sync(0xffffffffu, st, 0)) {
+                stalled = true;
+                break;
+              }
+            }
+          }
+        }
+        __threadfence();
+        // the tile is deferred (whole: the fixup kernel redoes all 128 rows) if any warp stalled
+        if (lane == 0) s_deferred[quarter] = stalled ? 1 : 0;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        deferred = (s_deferred[0] | s_deferred[1] | s_deferred[2] | s_deferred[3]) != 0;
+        asm volatile("bar.sync 1, 128;" ::: "memory");  // s_deferred is rewritten by the next tile
+        if (deferred && threadIdx.x == 64) {
+          const int slot = atomicAdd(defer, 1);
+          defer[1 + slot] = t;
+        }
+      }
+      // this slab's previous TMA store (tile i - 2) must have finished reading it
+      if (lane == 0) asm volatile("cp.async.bulk.wait_group.read 1;" ::: "memory");
+      __syncwarp();
+      uint32_t cphase = 0;
+      const bool load_c = ACC && !deferred && rbase < M;
+      if (load_c) {
+        int& nl = b ? lslab1 : lslab0;
+        cphase = (uint32_t)(nl & 1);
+        ++nl;
+        if (lane == 0) {
+          mbar_expect_tx(cb, (uint32_t)CF::kSlab);
+#pragma unroll
+          for (int j = 0; j < BN / 32; ++j) tma_load_2d(slab_s + j * 4096, &tmC, n0 + 32 * j, rbase, cb);
+        }
+      }
+      (void)loads;
+      mbar_wait(&acc_full[b], (uint32_t)((i >> 1) & 1));
+      fence_after();
+      double sq = 0.0;
+      float v[BN / 32][32];
+#pragma unroll
+      for (int j = 0; j < BN / 32; ++j)
+        tmem_ld32(tmem + ((uint32_t)(quarter * 32) << 16) + (uint32_t)(b * BN + j * 32), v[j]);
+      fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&acc_empty[b]);  // the MMA warp may refill this buffer
+      if (!deferred && rbase < M) {
+        if (load_c) mbar_wait(cb, cphase);
+        float sq32 = 0.f;
+#pragma unroll
+        for (int j = 0; j < BN / 32; ++j)
+#pragma unroll
+          for (int i4 = 0; i4 < 8; ++i4) {
+            float4* p4 = reinterpret_cast<float4*>(slab + j * 4096 + lane * 128 + ((i4 ^ (lane & 7)) << 4));
+            float4 o = ACC ? *p4 : make_float4(0.f, 0.f, 0.f, 0.f);
+            o.x += v[j][4 * i4];
+            o.y += v[j][4 * i4 + 1];
+            o.z += v[j][4 * i4 + 2];
+            o.w += v[j][4 * i4 + 3];
+            *p4 = o;
+            sq32 = fmaf(o.x, o.x, fmaf(o.y, o.y, fmaf(o.z, o.z, fmaf(o.w, o.w, sq32))));
+          }
+        sq = (double)sq32;  // rows / columns past the edge hold zeros (TMA zero fill, zero operands)
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        __syncwarp();
+        if (lane == 0) {
+#pragma unroll
+          for (int j = 0; j < BN / 32; ++j) tma_store_2d(&tmC, n0 + 32 * j, rbase, slab_s + j * 4096);
+          asm volatile("cp.async.bulk.commit_group;" ::: "memory");
+        }
+      }
+      if (sq_partial) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) sq += __shfl_xor_sync(0xffffffffu, sq, o);
+        if (lane == 0) sq_red[quarter] = sq;
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+        if (threadIdx.x == 64) sq_partial[t] = deferred ? 0.0 : (sq_red[0] + sq_red[1]) + (sq_red[2] + sq_red[3]);
+        asm volatile("bar.sync 1, 128;" ::: "memory");
+      }
+    }
+    if (lane == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");  // stores complete
+  }
+  fence_before();
+  __syncthreads();
+  if (warp == 1) {
+    fence_after();
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(CF::kTmemCols));
+  }
+}
+
+template <int BN, bool ACC>
+static int launch_persist(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int M,
+                          int N, int K, double* sq_partial, const int* ready, int ready_rows, const int* progress,
+                          int* defer, int ctas, int* ticket, cudaStream_t st) {
+  using CF = PCfg<BN>;
+  CUtensorMap ta, tb, tc;
+  APX_TRY(make_map(&ta, A, M, K, lda, BM, false));
+  APX_TRY(make_map(&tb, B, K, N, ldb, BN, true));
+  APX_TRY(make_map(&tc, C, M, N, ldc, 32, false));  // 32 x 32 boxes, 128-byte swizzle
+  const int tiles = (int)(ceil_div(M, BM) * ceil_div(N, BN));
+  auto fn = gemm_persist_kernel<BN, ACC>;
+  APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem));
+  if (ticket) APX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
+  fn<<<(unsigned)std::max(1, std::min(tiles, ctas)), kThreads, CF::kSmem, st>>>(
+      ta, tb, tc, M, N, K, sq_partial, ready, ready_rows, progress, defer, stall_ns(), ticket);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
 }  // namespace tma
 
 // Completes the tiles gemm_tma_kernel deferred (bounded wait: its producer made no progress)
@@ -724,6 +1041,31 @@ int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* 
 #undef APX_TL
   set_error("umma_tma_gemm: unsupported layout %d / BN %d / fix-up %d", layout, bn, fix);
   return E_ARG;
+}
+
+// Persistent C[M x N] (=|+=) A[M x K] . B[K x N] (A row-major [M][K], B row-major [K][N], 16-byte
+// aligned, N a multiple of 32): the tile loop of gemm_persist_kernel on `ctas` CTAs (default: one
+// per SM). Same ready / defer / sq_partial contract as umma_tma_gemm (one partial per 128 x BN tile,
+// tile = row band * ceil(N / BN) + column tile).
+int umma_persist_gemm(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int M, int N,
+                      int K, int accumulate, cudaStream_t st, double* sq_partial, const int* ready, int ready_rows,
+                      const int* progress, int* defer, int ctas, int bn, int* ticket) {
+  APX_REQUIRE(ready == nullptr || (accumulate && ready_rows > 0), "umma_persist_gemm: ready flags need accumulate");
+  APX_REQUIRE(defer == nullptr || (ready != nullptr && progress != nullptr && sq_partial != nullptr),
+              "umma_persist_gemm: deferral needs ready flags, a progress counter and sq partials");
+  APX_REQUIRE(((uintptr_t)A % 16) == 0 && ((uintptr_t)B % 16) == 0 && ((uintptr_t)C % 16) == 0 && (lda % 4) == 0 &&
+                  (ldb % 4) == 0 && (ldc % 4) == 0 && (N % 32) == 0 && K >= 1,
+              "umma_persist_gemm: 16-byte aligned operands and N %% 32 == 0 required");
+  if (ctas <= 0) ctas = device_sms();
+  if (bn == 64)
+    return accumulate ? tma::launch_persist<64, true>(A, lda, B, ldb, C, ldc, M, N, K, sq_partial, ready, ready_rows,
+                                                      progress, defer, ctas, ticket, st)
+                      : tma::launch_persist<64, false>(A, lda, B, ldb, C, ldc, M, N, K, sq_partial, ready,
+                                                       ready_rows, progress, defer, ctas, ticket, st);
+  return accumulate ? tma::launch_persist<128, true>(A, lda, B, ldb, C, ldc, M, N, K, sq_partial, ready, ready_rows,
+                                                     progress, defer, ctas, ticket, st)
+                    : tma::launch_persist<128, false>(A, lda, B, ldb, C, ldc, M, N, K, sq_partial, ready, ready_rows,
+                                                      progress, defer, ctas, ticket, st);
 }
 
 }  // namespace apx

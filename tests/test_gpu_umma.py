@@ -31,9 +31,13 @@ def run(layout, bn, M, N, K, splits=1, accumulate=0, mask=None, mod_n=1, trans_o
     dm = None
     if mask is not None:
         dm = torch.tensor(mask, dtype=torch.int32).cuda()
+    if layout & 128:  # persistent GEMM with dynamic tiles: the ticket counter rides in mask_j
+        dm = torch.zeros(4, dtype=torch.int32).cuda()
     Nn.call("apx_debug_umma_gemm", layout, bn, dA.data_ptr(), A_st.shape[1], dB.data_ptr(), B_st.shape[1],
             dC.data_ptr(), ldc, M, N, K, splits, accumulate, None if dm is None else dm.data_ptr(),
             0 if mask is None else len(mask), mod_n, None)
+    if layout & 128:
+        assert int(dm[0]) >= 1  # the producers claimed tiles (and each its terminating ticket)
     torch.cuda.synchronize()
     C = dC.cpu().numpy().reshape(splits, rows_c, ldc)
     a64 = a.astype(np.float64)
@@ -102,3 +106,16 @@ def test_umma_tma_staged_c_accumulate(layout):
     assert run(32 | layout, 128, 200, 260, 40, accumulate=1) < 1e-5
     assert run(32 | layout, 128, 256, 256, 128, accumulate=1) < 1e-5  # 4-stage ring: L2-prefetch path
 
+
+
+@pytest.mark.parametrize("bn", [64, 128])
+@pytest.mark.parametrize("accumulate", [0, 1])
+def test_umma_persistent_tile_loop(bn, accumulate):
+    """Persistent double-buffered GEMM (gemm_persist_kernel): few CTAs walking many tiles (TMEM
+    buffer reuse, ring phases across tiles), static and dynamic (ticket + shared tile queue) tile
+    order, K = 128 and 64, ragged M and K."""
+    for dyn in (0, 128):
+        for ctas in (1, 3, 0):
+            assert run(dyn | 64 | 2, bn, 512, 512, 128, accumulate=accumulate, mod_n=ctas) < 1e-5
+        assert run(dyn | 64 | 2, bn, 300, 256, 64, accumulate=accumulate, mod_n=5) < 1e-5
+        assert run(dyn | 64 | 2, bn, 256, 384, 40, accumulate=accumulate, mod_n=2) < 1e-5

@@ -1,0 +1,6 @@
+set -u
+O=gpurun_out
+timeout 300 python -m pytest tests/test_gpu_umma.py -x -q > $O/t_umma.log 2>&1; echo "umma rc=$?"
+timeout 600 python -m pytest tests/test_gpu_mixed.py tests/test_gpu_robust.py tests/test_gpu_c4_full.py -x -q -s > $O/t_mixed.log 2>&1; echo "tests rc=$?"
+python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > $O/b_resid.json 2> $O/b_resid.err; echo "rc=$?"
+APX_QW_TILE=1 python bench.py --steps 20 --warmup 5 --no-cpu-baseline --no-e2e > $O/b_resid2.json 2> $O/b_resid2.err; echo "rc=$?"
