@@ -534,16 +534,21 @@ static int run_mixed_f32_umma(const float* A, const float* B, int n, int l, int 
 static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int kc, int q, const float* Omega,
                                const int* fb, float* M, int* sb, double* scal, const MixedPlan& p, cudaStream_t st) {
   stage_mark(0, st);
-  APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
   const int grows = 8;  // the f16 gather's row block
   const int rblocks = (int)ceil_div(n, grows);
   int* defer = p.ready + rblocks;
-  APX_CUDA(cudaMemsetAsync(p.ready, 0, (rblocks + 1) * sizeof(int), st));
   SideStream* ss = nullptr;
   APX_TRY(get_side(&ss));
   APX_CUDA(cudaEventRecord(ss->fork, st));
   APX_CUDA(cudaStreamWaitEvent(ss->s, ss->fork, 0));
   APX_CUDA(cudaStreamWaitEvent(ss->hi, ss->fork, 0));
+  // the resets go to lo, off the critical path: the scalars, the gather's row flags and deferral
+  // list, the tickets and the finalize counter; hi picks them up through `b_read` (before the Bm
+  // finalize) and `b_ready` (before the gather)
+  APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), ss->s));
+  APX_CUDA(cudaMemsetAsync(p.ready, 0, (rblocks + 1) * sizeof(int), ss->s));
+  APX_CUDA(cudaMemsetAsync(p.ticket, 0, 4 * sizeof(int), ss->s));
+  APX_CUDA(cudaEventRecord(ss->b_read, ss->s));
   // The critical path is A's chain (Y -> QR -> Bm -> dA -> gather), so it runs on the
   // high-priority stream; B's decomposition and the W chain fill in on the low-priority one.
   const cudaStream_t hi = ss->hi, lo = ss->s;
@@ -553,18 +558,32 @@ static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int
   float *Y = (float*)p.Y, *Q = (float*)p.Q, *Qt = (float*)p.Qt, *Z = (float*)p.Z, *Bm = (float*)p.Bm,
         *W = (float*)p.W, *part = (float*)p.part;
   // ---- hi: Y = A Omega on the whole GPU, then CholeskyQR -------------------------------------------
+  // B's energy pass (HBM-bound) runs after Y = A Omega, overlapping the latency-bound QR, at the
+  // full 8 CTAs per SM so it is over quickly (a long, thin energy pass slows the QR's loads: the
+  // QR's span grew 117 -> 240 us as its CTAs per SM went 8 -> 1). Concurrent with Y instead
+  // (APX_B_ORDER=0) delays Y by the shared bandwidth and measured the same (1122 vs 1121).
+  static const int b_after_y = [] {
+    const char* e = getenv("APX_B_ORDER");
+    return e ? atoi(e) : 1;
+  }();
+  static const int en_cps = [] {  // energy-pass CTAs per SM (APX_EN_CPS, tuning knob)
+    const char* e = getenv("APX_EN_CPS");
+    return e ? std::max(1, std::min(8, atoi(e))) : 8;
+  }();
   APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, hi, kNumSMs));
   stage_mark(3, hi);
-  APX_CUDA(cudaEventRecord(ss->b_read, hi));
-  // ---- lo: B's cycle decomposition and the f16 lambda' table, overlapping the latency-bound QR: the
-  // energy pass keeps half the CTA slots free so the QR's kernels launch at once ---------------------
-  APX_CUDA(cudaStreamWaitEvent(lo, ss->b_read, 0));
+  APX_CUDA(cudaStreamWaitEvent(hi, ss->b_read, 0));  // lo's resets (long done)
+  if (b_after_y) {
+    APX_CUDA(cudaEventRecord(ss->b_read, hi));
+    APX_CUDA(cudaStreamWaitEvent(lo, ss->b_read, 0));
+  }
+  // ---- lo: B's cycle decomposition and the f16 lambda' table -----------------------------------
   if (fb) {
-    APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, lo, 4));
+    APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, lo, en_cps));
     APX_CUDA(cudaMemcpyAsync(sb, fb, kc * sizeof(int), cudaMemcpyDeviceToDevice, lo));
     APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, lo));
   } else {
-    APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, nullptr, p.partial, lo, 4));
+    APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, nullptr, p.partial, lo, en_cps));
     APX_TRY(launch_topk(p.nr_b, n, kc, sb, lo, p.nr_b, 1.0, scal + APX_S_KEPT_B, p.en_b, scal + APX_S_FRO2_B));
   }
   float* lb = (float*)p.lam_b;
@@ -584,22 +603,19 @@ static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int
   stage_mark(4, hi);
   {
     // Bm = Q^T A with the A tiles rounded to TF32 (FIX 3): the rounding warps also sum the
-    // squares of every A element they touch (each exactly once) -> ||A||^2 partials
+    // squares of every A element they touch (each exactly once) -> ||A||^2 partials. Then one
+    // finalize kernel: split-K sum, ||Bm||^2 (= sum sigma^2, the report's kept energy) from Bm as
+    // formed, Bm := tf32(Bm) (the algebra holds for any Bm -- but the energy difference
+    // ||A||^2 - ||Bm||^2 would feel the rounding: ~2e-5 of ||Bm||^2 when a few rows carry the
+    // energy; with Q TF32-exact too, Q.Bm is then exact on the tensor core at K = l), [Q | Q], and
+    // the fixed-order sums of both norms.
     const int s = UmmaStages::splits(n);
-    APX_TRY(umma_tma_gemm(7 | 8 | 16, 64, A, n, Q, l, s > 1 ? part : Bm, n, (int64_t)l * n, n, l, n, s, 0, nullptr, 0,
-                          1, hi, p.asq));
-    if (s > 1) APX_TRY(launch_split_reduce_f32(part, s, (size_t)n * l, Bm, hi));
-    APX_TRY(launch_sum_vector(p.asq, (int)(ceil_div(n, 128) * s), scal + APX_S_FRO2_A, hi));
+    APX_TRY(umma_tma_gemm(7 | 8 | 16, 64, A, n, Q, l, part, n, (int64_t)l * n, n, l, n, s, 0, nullptr, 0, 1, hi,
+                          p.asq));
+    stage_mark(16, hi);
+    APX_TRY(launch_bm_finalize(part, s, l, n, Bm, Q, p.Q2, p.bsq, p.asq, (int)(ceil_div(n, 128) * s),
+                               reinterpret_cast<unsigned*>(p.ticket + 2), scal + APX_S_KEPT_A, scal + APX_S_FRO2_A, hi));
   }
-  // ||Bm||^2 (= sum sigma^2, the kept energy of the report) from Bm as formed; then Bm := tf32(Bm)
-  // (the algebra holds for any Bm -- but the energy difference ||A||^2 - ||Bm||^2 would feel the
-  // rounding: ~2e-5 of ||Bm||^2 when a few rows carry the energy): with Q TF32-exact too, Q.Bm is
-  // exact on the tensor core at K = l
-  int parts = 0;
-  APX_TRY(launch_sumsq<float>(Bm, (size_t)l * n, p.bsq, &parts, hi));
-  APX_TRY(launch_sum_vector(p.bsq, parts, scal + APX_S_KEPT_A, hi));
-  APX_TRY(launch_round_tf32(Bm, (size_t)l * n, hi));
-  APX_TRY(launch_dup_cols(Q, n, l, p.Q2, hi));
   stage_mark(5, hi);
   APX_TRY(umma_tma_gemm(2 | 32, 128, Q, l, Bm, n, const_cast<float*>(A), n, 0, n, n, l, 1, 0, nullptr, 0, 1, hi,
                         nullptr, nullptr, 0, nullptr, nullptr, p.dAh, scal + APX_S_FRO2_A));

@@ -92,6 +92,9 @@ int launch_qw_fixup_sum(const float* Q, int64_t ldq, const float* W, int64_t ldw
 int launch_split_tf32(const float* X, size_t count, float* X2, cudaStream_t st);
 int launch_dup_cols(const float* Q, int rows, int l, float* Q2, cudaStream_t st);
 int launch_round_tf32(float* X, size_t count, cudaStream_t st);
+int launch_bm_finalize(const float* part, int splits, int l, int n, float* Bm, const float* Q, float* Q2,
+                       double* bsq_part, const double* asq_part, int asq_parts, unsigned* counter, double* kept_out,
+                       double* fro2_out, cudaStream_t st);
 int gather_f16_threads(int n);
 size_t gather_f16_smem(int n, int kp);
 int launch_lam_f16(const float* lam, int kp, int n, const double* fro2_b, uint16_t* out, cudaStream_t st);

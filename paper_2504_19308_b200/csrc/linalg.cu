@@ -329,6 +329,26 @@ __global__ void __launch_bounds__(64) chol64_kernel(const double* __restrict__ G
 // skipped: with fp32 outputs one fp64 pass already leaves ||Q^T Q - I|| <~ u64 * kappa^2, so
 // kappa_F <= skip_kappa skips pass 2 (skip_out = 1). A pivot below 4*l*eps*max(diag G) raises
 // the breakdown flag (Householder fallback).
+// fp64 reciprocal and reciprocal square root for positive normal x: the MUFU seeds refined by two
+// Newton steps (full double precision), without the library routines' special-case branches
+__device__ __forceinline__ double fast_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  double e = fma(-h * y, y, 0.5);
+  y = fma(y, e, y);
+  e = fma(-h * y, y, 0.5);
+  return fma(y, e, y);
+}
+
 __global__ void __launch_bounds__(256) cholinv64_kernel(const double* __restrict__ Gin, int l, double* __restrict__ Xout,
                                                         const int* __restrict__ gate, int* __restrict__ breakdown,
                                                         int* __restrict__ skip_out, double skip_kappa) {
@@ -370,10 +390,9 @@ __global__ void __launch_bounds__(256) cholinv64_kernel(const double* __restrict
     __syncthreads();
     double p = bl[j];
     if (!(p > tol)) bad = true;  // uniform: every thread reads the same pivot
-    if (!(p > 0.0)) p = 1.0;     // keep the (discarded) arithmetic finite after a breakdown
-    const double rsq = rsqrt(p);
+    if (!(p > 1e-300)) p = 1.0;  // keep the (discarded) arithmetic finite after a breakdown
     if (r > j) {
-      const double f = bl[r] * (rsq * rsq);  // A[r][j] / p, with A[r][j] = A[j][r]
+      const double f = bl[r] * fast_rcp(p);  // A[r][j] / p, with A[r][j] = A[j][r]
       if (c0 + 15 > j) {
 #pragma unroll
         for (int u = 0; u < 16; u += 2) {
@@ -391,6 +410,7 @@ __global__ void __launch_bounds__(256) cholinv64_kernel(const double* __restrict
         }
       }
     } else if (r == j) {
+      const double rsq = fast_rsqrt(p);
 #pragma unroll
       for (int u = 0; u < 16; ++u) {
         wl[u] *= rsq;
@@ -962,15 +982,18 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
     const double skip_kappa = sizeof(TO) == 4 ? 3.0e4 : 0.0;
     const int tiles = (int)ceil_div(m, 64);
     APX_TRY(launch_gram<TI>(Y, rs, cs, m, l, flag, part, G, st));
+    stage_mark(12, st);  // fine-grained trace markers (bench.py C4 timeline); no-ops unless armed
     APX_CUDA(launch_pdl(cholinv64_kernel, dim3(1), dim3(256), 0, st, (const double*)G, l, Rinv, (const int*)flag, flag,
                         skip2, skip_kappa));
     APX_LAUNCH_CHECK();
+    stage_mark(13, st);
     APX_CUDA(cudaFuncSetAttribute(apply_x_kernel<TI, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem));
     APX_CUDA(cudaFuncSetAttribute(apply_x_kernel<double, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem));
     APX_CUDA(launch_pdl(apply_x_kernel<TI, TO>, dim3(tiles), dim3(256), kApplySmem, st, Y, rs, cs, m, l,
                         (const double*)Rinv, (const int*)flag, (const int*)skip2, Q1, Q, qrs, qcs, Q2, q2rs, q2cs,
                         tf32));
     APX_LAUNCH_CHECK();
+    stage_mark(14, st);
     APX_TRY(launch_gram<double>(Q1, l, 1, m, l, skip2, part, G, st));
     APX_CUDA(launch_pdl(cholinv64_kernel, dim3(1), dim3(256), 0, st, (const double*)G, l, Rinv, (const int*)skip2, flag,
                         (int*)nullptr, 0.0));
@@ -979,6 +1002,7 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
                         (int64_t)l, (int64_t)1, m, l, (const double*)Rinv, (const int*)skip2, (const int*)nullptr,
                         (double*)nullptr, Q, qrs, qcs, Q2, q2rs, q2cs, tf32));
     APX_LAUNCH_CHECK();
+    stage_mark(15, st);
   } else if (!householder_only) {
     // pass 1: Q1 = Y R1^{-1} (fp64)
     APX_TRY(launch_gram<TI>(Y, rs, cs, m, l, flag, part, G, st));

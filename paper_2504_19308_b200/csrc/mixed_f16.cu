@@ -57,6 +57,55 @@ __global__ void round_tf32_kernel(float* __restrict__ X, size_t count) {
     X[i] = tf32_rn(X[i]);
 }
 
+// Residual plan, after the Bm = Q^T A GEMM (one launch instead of seven): Bm = sum of the split-K
+// partials (fixed order, fp64 -- split_reduce_kernel's arithmetic), ||Bm||^2 from Bm as formed,
+// Bm := tf32(Bm), Q2 = [Q | Q]; per-CTA ||Bm||^2 partials, and the last CTA to finish (atomic
+// counter, reset for the next product) sums them and the ||A||^2 partials of the GEMM in a fixed
+// order into kept_out and fro2_out.
+constexpr int kFinThreads = 256;
+__global__ void __launch_bounds__(kFinThreads)
+    bm_finalize_kernel(const float* __restrict__ part, int splits, int l, int n, float* __restrict__ Bm,
+                       const float* __restrict__ Q, float* __restrict__ Q2, double* __restrict__ bsq_part,
+                       const double* __restrict__ asq_part, int asq_parts, unsigned* __restrict__ counter,
+                       double* __restrict__ kept_out, double* __restrict__ fro2_out) {
+  pdl_wait();
+  __shared__ double red[32];
+  __shared__ bool last;
+  const size_t count = (size_t)l * n;
+  double sq = 0.0;
+  for (size_t e = blockIdx.x * (size_t)blockDim.x + threadIdx.x; e < count; e += (size_t)gridDim.x * blockDim.x) {
+    double v = 0.0;
+    for (int z = 0; z < splits; ++z) v += (double)part[(size_t)z * count + e];
+    const float b = (float)v;
+    sq = fma((double)b, (double)b, sq);
+    Bm[e] = tf32_rn(b);
+    const size_t r = e / l, c = e - r * l;  // Q is n x l: same element count
+    const float q = Q[e];
+    Q2[r * 2 * l + c] = q;
+    Q2[r * 2 * l + l + c] = q;
+  }
+  sq = block_sum(sq, red);
+  if (threadIdx.x == 0) {
+    bsq_part[blockIdx.x] = sq;
+    __threadfence();
+    last = atomicAdd(counter, 1u) == gridDim.x - 1;
+  }
+  __syncthreads();
+  if (!last) return;
+  __threadfence();
+  double k = 0.0, a = 0.0;
+  for (int i = threadIdx.x; i < (int)gridDim.x; i += blockDim.x) k += bsq_part[i];
+  for (int i = threadIdx.x; i < asq_parts; i += blockDim.x) a += asq_part[i];
+  k = block_sum(k, red);
+  __syncthreads();
+  a = block_sum(a, red);
+  if (threadIdx.x == 0) {
+    *kept_out = k;
+    *fro2_out = a;
+    *counter = 0u;
+  }
+}
+
 // Q2 = [Q | Q] (rows x 2l)
 __global__ void dup_cols_kernel(const float* __restrict__ Q, int rows, int l, float* __restrict__ Q2) {
   const size_t count = (size_t)rows * l;
@@ -144,6 +193,7 @@ __global__ void __launch_bounds__(NT, 1)
   __shared__ double red[32];
   const int tid = threadIdx.x;
   const int nblk = (int)ceil_div(m_rows, kHR);
+  pdl_wait();  // programmatic dependent launch: the previous kernel's outputs (dA) are read below
   const float inv = ldexpf(1.f, f16_scale_exp(*fro2_a) + f16_scale_exp(*fro2_b) - 30);
   for (int t = tid; t < kp; t += NT) sJ[t] = t < k ? J[t] : 0;  // padded shifts: zero lambda' rows
   if (tid == 0) {
@@ -297,6 +347,16 @@ int launch_split_tf32(const float* X, size_t count, float* X2, cudaStream_t st) 
   return OK;
 }
 
+int launch_bm_finalize(const float* part, int splits, int l, int n, float* Bm, const float* Q, float* Q2,
+                       double* bsq_part, const double* asq_part, int asq_parts, unsigned* counter, double* kept_out,
+                       double* fro2_out, cudaStream_t st) {
+  const unsigned blocks = (unsigned)std::min<size_t>(ceil_div((size_t)l * n, (size_t)kFinThreads), (size_t)kNumSMs * 4);
+  APX_CUDA(launch_pdl(bm_finalize_kernel, dim3(blocks), dim3(kFinThreads), 0, st, part, splits, l, n, Bm, Q, Q2,
+                      bsq_part, asq_part, asq_parts, counter, kept_out, fro2_out));
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
 int launch_round_tf32(float* X, size_t count, cudaStream_t st) {
   const unsigned blocks = (unsigned)std::min<size_t>(ceil_div(count, (size_t)256), (size_t)kNumSMs * 8);
   round_tf32_kernel<<<blocks, 256, 0, st>>>(X, count);
@@ -339,8 +399,9 @@ int launch_gather_f16(const uint16_t* Xh, const uint16_t* lamh, const int* J, in
   APX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
   auto go = [&](auto kern) -> int {
     APX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, c.nt, smem, st>>>(reinterpret_cast<const uint4*>(Xh), reinterpret_cast<const uint32_t*>(lamh), J, k,
-                                   kp, n, m_rows, M, fro2_a, fro2_b, ticket, ready, msq_partial);
+    APX_CUDA(launch_pdl(kern, dim3(grid), dim3(c.nt), smem, st, reinterpret_cast<const uint4*>(Xh),
+                        reinterpret_cast<const uint32_t*>(lamh), J, k, kp, n, m_rows, M, fro2_a, fro2_b, ticket, ready,
+                        msq_partial));
     APX_LAUNCH_CHECK();
     return OK;
   };

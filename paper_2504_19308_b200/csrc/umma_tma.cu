@@ -162,6 +162,9 @@ __global__ void __launch_bounds__(kThreads, 1)
                  "r"(CF::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  // programmatic dependent launch: the prologue above (barriers, TMEM, tensor-map prefetch) ran
+  // while the previous kernel drained; its outputs are read only after this wait
+  pdl_wait();
   for (int t = threadIdx.x; t < mk && t < 128; t += kThreads) sJ[t] = mJ[t];
   fence_before();
   __syncthreads();
@@ -629,9 +632,9 @@ static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, floa
   auto fn = gemm_tma_kernel<BN, STAGES, A_MN, B_MN, TRANS_OUT, FIX>;
   APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem));
   const int c_async = ((uintptr_t)C % 16) == 0 && (ldc % 4) == 0 && (N % 4) == 0 && (c_split_stride % 4) == 0;
-  fn<<<grid, kThreads, CF::kSmem, st>>>(ta, tb, C, ldc, c_split_stride, M, N, K, kps, accumulate, mJ, mk, mod_n,
-                                        sq_partial, c_async, ready, ready_rows, progress, defer, stall_ns(), hout,
-                                        hscale);
+  APX_CUDA(launch_pdl(fn, grid, dim3(kThreads), CF::kSmem, st, ta, tb, C, ldc, c_split_stride, M, N, K, kps,
+                      accumulate, mJ, mk, mod_n, sq_partial, c_async, ready, ready_rows, progress, defer, stall_ns(),
+                      hout, hscale));
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -730,6 +733,7 @@ __global__ void __launch_bounds__(kThreads, 1)
                  "r"(CF::kTmemCols));
     asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
   }
+  pdl_wait();  // programmatic dependent launch (see gemm_tma_kernel)
   fence_before();
   __syncthreads();
   fence_after();
@@ -947,8 +951,8 @@ static int launch_persist(const float* A, int64_t lda, const float* B, int64_t l
   auto fn = gemm_persist_kernel<BN, ACC>;
   APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)CF::kSmem));
   if (ticket) APX_CUDA(cudaMemsetAsync(ticket, 0, sizeof(int), st));
-  fn<<<(unsigned)std::max(1, std::min(tiles, ctas)), kThreads, CF::kSmem, st>>>(
-      ta, tb, tc, M, N, K, sq_partial, ready, ready_rows, progress, defer, stall_ns(), ticket);
+  APX_CUDA(launch_pdl(fn, dim3((unsigned)std::max(1, std::min(tiles, ctas))), dim3(kThreads), CF::kSmem, st, ta, tb,
+                      tc, M, N, K, sq_partial, ready, ready_rows, progress, defer, stall_ns(), ticket));
   APX_LAUNCH_CHECK();
   return OK;
 }

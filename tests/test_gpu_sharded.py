@@ -45,7 +45,7 @@ def test_one_shard_equals_single_device(P, order):
     A, B = _operands(n, 40)
     Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
     omega = torch.from_numpy(P.draw_sketch(n, k, 3)).cuda().float()
-    ref = P.mixed_product_device(Ad, Bd, k, k, order, omega)
+    ref = P.mixed_product_device(Ad, Bd, k, k, order, omega, direct=True)  # the plan the phases cut
     M, res = _sharded(P, Ad, Bd, omega, 1, order)
     torch.cuda.synchronize()
     assert torch.equal(res[0]["sel_b"], ref["sel_b"])
@@ -62,7 +62,7 @@ def test_shards_vs_single_device_and_oracle(P, world):
     A, B = _operands(n, 50 + world)
     Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
     omega = torch.from_numpy(P.draw_sketch(n, k, 7)).cuda().float()
-    ref = P.mixed_product_device(Ad, Bd, k, k, 1, omega)
+    ref = P.mixed_product_device(Ad, Bd, k, k, 1, omega, direct=True)
     M, res = _sharded(P, Ad, Bd, omega, world)
     for r in res:
         assert torch.equal(r["sel_b"], ref["sel_b"])

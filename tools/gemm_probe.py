@@ -41,6 +41,15 @@ def timeit(f, reps=20):
     return s.elapsed_time(e) / reps * 1e3
 
 
+# Y = A . Omega (n x n . n x 64, 4-way split-K as the residual plan launches it)
+A = torch.randn(n, n, device=dev)
+Om = torch.randn(n, 64, device=dev)
+Yp = torch.empty(4, n, 64, device=dev)
+for sp in (1, 2, 4):
+    us = timeit(lambda: N.call("apx_debug_umma_gemm", 32 | 2, 64, A.data_ptr(), n, Om.data_ptr(), 64, Yp.data_ptr(),
+                               64, n, 64, n, sp, 0, None, 0, 1, None))
+    print(f"Y = A.Omega split {sp}: {us:8.1f} us  {4 * n * n / us / 1e3:7.0f} GB/s")
+del A
 for acc in (0, 1):
     by = (8 if acc else 4) * n * n
     for name, f in [("tile bn128" if acc else "tile bn256", lambda: call(32 | 2, 128 if acc else 256, acc)),
