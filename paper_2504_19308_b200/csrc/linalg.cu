@@ -458,6 +458,15 @@ __global__ void __launch_bounds__(256) cholinv64_kernel(const double* __restrict
   }
 }
 
+// Cholesky-inverse launch for l <= 64. (Measured alternative: the same elimination on 1024 threads,
+// 4 + 4 columns per thread, was slower -- 65 vs 55 us in the C4 chain, C1 2.19 vs 2.11 ms. The
+// step is bound by its owner warp: rows j and j+1 sit in one warp, so row j's scaling and row
+// j+1's update serialise before row j+1 can be published; tools/chol_probe2.cu, fp64_issue_probe.cu.)
+static cudaError_t launch_cholinv64(const double* G, int l, double* X, const int* gate, int* breakdown, int* skip_out,
+                                   double skip_kappa, cudaStream_t st) {
+  return launch_pdl(cholinv64_kernel, dim3(1), dim3(256), 0, st, G, l, X, gate, breakdown, skip_out, skip_kappa);
+}
+
 // ---- Q = Y X (X = R^{-1} upper, l <= 64) over 64-row tiles ---------------------------------
 // CTA = 64 rows x 64 columns of Q, 256 threads on a 16 x 16 grid of 4 x 4 blocks. The Y tile is
 // staged transposed (Ys[i][r], fp64) with all loads in flight at once, X zero-padded to 64 x 64.
@@ -983,8 +992,7 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
     const int tiles = (int)ceil_div(m, 64);
     APX_TRY(launch_gram<TI>(Y, rs, cs, m, l, flag, part, G, st));
     stage_mark(12, st);  // fine-grained trace markers (bench.py C4 timeline); no-ops unless armed
-    APX_CUDA(launch_pdl(cholinv64_kernel, dim3(1), dim3(256), 0, st, (const double*)G, l, Rinv, (const int*)flag, flag,
-                        skip2, skip_kappa));
+    APX_CUDA(launch_cholinv64((const double*)G, l, Rinv, (const int*)flag, flag, skip2, skip_kappa, st));
     APX_LAUNCH_CHECK();
     stage_mark(13, st);
     APX_CUDA(cudaFuncSetAttribute(apply_x_kernel<TI, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kApplySmem));
@@ -995,8 +1003,7 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
     APX_LAUNCH_CHECK();
     stage_mark(14, st);
     APX_TRY(launch_gram<double>(Q1, l, 1, m, l, skip2, part, G, st));
-    APX_CUDA(launch_pdl(cholinv64_kernel, dim3(1), dim3(256), 0, st, (const double*)G, l, Rinv, (const int*)skip2, flag,
-                        (int*)nullptr, 0.0));
+    APX_CUDA(launch_cholinv64((const double*)G, l, Rinv, (const int*)skip2, flag, (int*)nullptr, 0.0, st));
     APX_LAUNCH_CHECK();
     APX_CUDA(launch_pdl(apply_x_kernel<double, TO>, dim3(tiles), dim3(256), kApplySmem, st, (const double*)Q1,
                         (int64_t)l, (int64_t)1, m, l, (const double*)Rinv, (const int*)skip2, (const int*)nullptr,
@@ -1063,7 +1070,7 @@ int cholqr_rows_pass1(const float* Y, int m, int l, const double* G, float* Q, d
   APX_WS_CHECK(ws);
   APX_CUDA(cudaMemsetAsync(r.flag, 0, 4 * sizeof(int), st));
   APX_CUDA(cudaMemsetAsync(G2, 0, (size_t)l * l * sizeof(double), st));  // stays zero if pass 2 is skipped
-  cholinv64_kernel<<<1, 256, 0, st>>>(G, l, r.Rinv, r.flag, r.flag, r.flag + 1, 3.0e4);
+  APX_CUDA(launch_cholinv64(G, l, r.Rinv, r.flag, r.flag, r.flag + 1, 3.0e4, st));
   APX_LAUNCH_CHECK();
   APX_CUDA(cudaFuncSetAttribute(apply_x_kernel<float, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kApplySmem));
@@ -1077,7 +1084,7 @@ int cholqr_rows_pass2(int m, int l, const double* G2, float* Q, void* wsp, size_
   Workspace ws(wsp, bytes);
   RowsQR r = plan_rows_qr(ws, m, l);
   APX_WS_CHECK(ws);
-  cholinv64_kernel<<<1, 256, 0, st>>>(G2, l, r.Rinv, r.flag + 1, r.flag, (int*)nullptr, 0.0);
+  APX_CUDA(launch_cholinv64(G2, l, r.Rinv, r.flag + 1, r.flag, (int*)nullptr, 0.0, st));
   APX_LAUNCH_CHECK();
   APX_CUDA(cudaFuncSetAttribute(apply_x_kernel<double, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 (int)kApplySmem));

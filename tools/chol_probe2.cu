@@ -4,6 +4,17 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cuda_runtime.h>
+__device__ __forceinline__ double fast_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  double e = fma(-h * y, y, 0.5);
+  y = fma(y, e, y);
+  e = fma(-h * y, y, 0.5);
+  return fma(y, e, y);
+}
+// VAR 5: var1 with the fast rsqrt; 6: var0 with the fast rsqrt; 7: var1 without any rsqrt;
+// 8: var1 without the row scaling
 template <int VAR>
 __global__ void __launch_bounds__(256) probe(const double* Gin, int l, double* out, long long* tsteps) {
   __shared__ __align__(16) double rowL[2][64];
@@ -31,10 +42,14 @@ __global__ void __launch_bounds__(256) probe(const double* Gin, int l, double* o
     }
     __syncthreads();
     if (VAR == 3) { if (t == 0) tsteps[j] = clock64() - t0; continue; }
-    double p = bl[j];
+    double p = VAR == 10 ? 100.0 + j : bl[j];
     if (!(p > 0.0)) p = 1.0;
-    const double rsq = VAR == 2 ? p : rsqrt(p);
-    if (r > j && VAR != 1) {
+    const double rsq = (VAR == 2 || VAR == 7 || VAR == 9 || VAR == 10) ? p : (VAR == 5 || VAR == 6) ? fast_rsqrt(p) : rsqrt(p);
+    if (VAR == 9) {
+      const double sc = (r == j) ? rsq : 1.0;
+#pragma unroll
+      for (int u = 0; u < 16; ++u) { wl[u] *= sc; wr[u] *= sc; }
+    } else if (r > j && VAR != 1 && VAR != 5 && VAR != 7 && VAR != 8 && VAR != 10) {
       const double f = bl[r] * (rsq * rsq);
       if (c0 + 15 > j) {
 #pragma unroll
@@ -52,7 +67,7 @@ __global__ void __launch_bounds__(256) probe(const double* Gin, int l, double* o
           wr[u + 1] = fma(-f, bv.y, wr[u + 1]);
         }
       }
-    } else if (r == j) {
+    } else if (r == j && VAR != 8) {
 #pragma unroll
       for (int u = 0; u < 16; ++u) { wl[u] *= rsq; wr[u] *= rsq; }
     }
@@ -82,7 +97,7 @@ int main() {
     cudaMemcpy(hts, ts, 64 * 8, cudaMemcpyDeviceToHost);                                    \
     printf("\"var%d\": {\"us_per_launch\": %.2f, \"cyc_first8\": %lld, \"cyc_total\": %lld}, ", V, ms * 1000 / 20, hts[7], hts[63]); \
   }
-  RUN(0) RUN(1) RUN(2) RUN(3) RUN(4)
+  RUN(0) RUN(1) RUN(2) RUN(3) RUN(4) RUN(5) RUN(6) RUN(7) RUN(8) RUN(9) RUN(10)
   printf("\"done\": 1}\n");
   return 0;
 }
