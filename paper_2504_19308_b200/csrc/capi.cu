@@ -352,6 +352,7 @@ struct UmmaStages {
 struct SideStream {
   cudaStream_t s = nullptr, hi = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr, b_ready = nullptr, hi_done = nullptr, b_read = nullptr;
+  cudaEvent_t aux_fork = nullptr, aux_join = nullptr;  // side_fork / side_join (other products)
 };
 // Keyed by the current device: one host thread may drive several GPUs (or re-target with
 // cudaSetDevice), and each device gets its own pair of streams and events.
@@ -373,8 +374,37 @@ static int get_side(SideStream** out) {
     APX_CUDA(cudaEventCreateWithFlags(&g.b_ready, cudaEventDisableTiming));
     APX_CUDA(cudaEventCreateWithFlags(&g.hi_done, cudaEventDisableTiming));
     APX_CUDA(cudaEventCreateWithFlags(&g.b_read, cudaEventDisableTiming));
+    APX_CUDA(cudaEventCreateWithFlags(&g.aux_fork, cudaEventDisableTiming));
+    APX_CUDA(cudaEventCreateWithFlags(&g.aux_join, cudaEventDisableTiming));
   }
   *out = &g;
+  return OK;
+}
+
+// Fork / join of the calling thread's low-priority side stream on the current device, for products
+// whose two operand decompositions are independent (apx_svd_first_order): *side = st when `st` is
+// being captured into a CUDA graph (batched products already run concurrently there, and a shared
+// side stream would serialise the captured products).
+int side_fork(cudaStream_t st, cudaStream_t* side) {
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  APX_CUDA(cudaStreamIsCapturing(st, &cap));
+  if (cap != cudaStreamCaptureStatusNone) {
+    *side = st;
+    return OK;
+  }
+  SideStream* ss = nullptr;
+  APX_TRY(get_side(&ss));
+  APX_CUDA(cudaEventRecord(ss->aux_fork, st));
+  APX_CUDA(cudaStreamWaitEvent(ss->s, ss->aux_fork, 0));
+  *side = ss->s;
+  return OK;
+}
+int side_join(cudaStream_t st, cudaStream_t side) {
+  if (side == st) return OK;
+  SideStream* ss = nullptr;
+  APX_TRY(get_side(&ss));
+  APX_CUDA(cudaEventRecord(ss->aux_join, side));
+  APX_CUDA(cudaStreamWaitEvent(st, ss->aux_join, 0));
   return OK;
 }
 

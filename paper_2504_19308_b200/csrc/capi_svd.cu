@@ -93,6 +93,7 @@ size_t svd_first_order_ws(int m, int n, int p, int la, int lb) {
   ws.take<double>((size_t)lm * p * 3 + (size_t)lm * lm * 2 + (size_t)m * lm * 2);
   ws.take<double>((size_t)16 * mx * lm);  // split-K scratch
   ws.take<double>(4 * kNumSMs + 64);
+  ws.take<double>((size_t)16 * mx * lm);  // split-K scratch of B's decomposition (side stream)
   return ws.off;
 }
 
@@ -323,14 +324,20 @@ int apx_svd_first_order(int dtype, const void* A_, const void* B_, int64_t m, in
   double* P2 = P + (size_t)mi * lm;
   Dgemm g{ws.take<double>((size_t)16 * mx * lm), (size_t)16 * mx * lm};
   double* red = ws.take<double>(4 * kNumSMs + 64);
+  Dgemm g2{ws.take<double>((size_t)16 * mx * lm), (size_t)16 * mx * lm};
   APX_WS_CHECK(ws);
   APX_CUDA(cudaMemsetAsync(scalars, 0, APX_NSCALARS * sizeof(double), st));
   stage_mark(0, st);
-  // operand decompositions (independent sketches: default_rng([seed,0]) / ([seed,1]), svd.py:161-162)
+  // operand decompositions (independent sketches: default_rng([seed,0]) / ([seed,1]), svd.py:161-162):
+  // two latency-bound chains of small kernels (~5 QRs each), so B's runs on the side stream
+  // concurrently with A's (each with its own buffers and split-K scratch)
+  cudaStream_t sb = st;
+  APX_TRY(side_fork(st, &sb));
   APX_TRY(range_finder(A, mi, ni, l_a, power_iterations, (const double*)omega_a, a, g, st));
   APX_TRY(project_and_svd(A, mi, ni, l_a, a, g, k_a < l_a, st));
-  APX_TRY(range_finder(B, ni, pi, l_b, power_iterations, (const double*)omega_b, b, g, st));
-  APX_TRY(project_and_svd(B, ni, pi, l_b, b, g, k_b < l_b, st));
+  APX_TRY(range_finder(B, ni, pi, l_b, power_iterations, (const double*)omega_b, b, g2, sb));
+  APX_TRY(project_and_svd(B, ni, pi, l_b, b, g2, k_b < l_b, sb));
+  APX_TRY(side_join(st, sb));
   stage_mark(1, st);
   // truncation of an oversampled sketch: Qk = Q U'[:, :k], Bk = diag(S_k) V'^T[:k] Q2^T
   const double *Qa = a.Q, *Ba = a.Ba, *Qb = b.Q, *Bb = b.Ba;

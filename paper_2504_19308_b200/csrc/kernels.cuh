@@ -88,6 +88,9 @@ int umma_persist_gemm(const float* A, int64_t lda, const float* B, int64_t ldb, 
 // deferred Q.W tiles of a ready-flag GEMM, then the fixed-order ||C||^2 sum (umma_tma.cu)
 int launch_qw_fixup_sum(const float* Q, int64_t ldq, const float* W, int64_t ldw, float* C, int64_t ldc, int M, int N,
                         int K, int bn, int* defer, double* sq_partial, int parts, double* out, cudaStream_t st);
+// ---- capi.cu: the calling thread's side stream (fork from / join back into `st`) ----
+int side_fork(cudaStream_t st, cudaStream_t* side);
+int side_join(cudaStream_t st, cudaStream_t side);
 // ---- mixed_f16.cu (residual plan of the C4 product) ----
 int launch_split_tf32(const float* X, size_t count, float* X2, cudaStream_t st);
 int launch_dup_cols(const float* Q, int rows, int l, float* Q2, cudaStream_t st);

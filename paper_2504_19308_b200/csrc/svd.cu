@@ -18,7 +18,29 @@ constexpr int kSvdMax = 128;
 constexpr bool getenv_sweeps_debug = true;  // the checked build reports the sweep count
 #endif
 
-template <bool GLOBAL>
+// fp64 reciprocal / reciprocal square root for positive normal x (MUFU seed + two Newton steps,
+// no special-case branches): the rotation angle is on every round's critical path
+__device__ __forceinline__ double svd_rcp(double x) {
+  double y;
+  asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  double e = fma(-x, y, 1.0);
+  y = fma(y, e, y);
+  e = fma(-x, y, 1.0);
+  return fma(y, e, y);
+}
+__device__ __forceinline__ double svd_rsqrt(double x) {
+  double y;
+  asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(x));
+  const double h = 0.5 * x;
+  double e = fma(-h * y, y, 0.5);
+  y = fma(y, e, y);
+  e = fma(-h * y, y, 0.5);
+  return fma(y, e, y);
+}
+
+// KR: rows per lane of a pair's half-warp (ceil(l / 16)); the shared-memory kernel is
+// instantiated for l <= 32, 48, 64, 128 so a small sketch does not carry zero-padded registers
+template <bool GLOBAL, int KR = (kSvdMax + 15) / 16>
 __global__ void __launch_bounds__(GLOBAL ? 1024 : 512)
     hestenes_svd_kernel(const double* __restrict__ Win, int l, double* __restrict__ Uout, double* __restrict__ Sout,
                         double* __restrict__ Vout, double* __restrict__ VoutT, double* __restrict__ scratch) {
@@ -77,7 +99,7 @@ __global__ void __launch_bounds__(GLOBAL ? 1024 : 512)
         double* vb = Vc + (size_t)b * le;
         // shared-memory kernel (l <= 128): the pair's W and V entries in registers, all loads
         // issued before the reduction; the global-scratch kernel (wide sketches) re-reads them
-        constexpr int kR = GLOBAL ? 1 : (kSvdMax + 15) / 16;
+        constexpr int kR = GLOBAL ? 1 : KR;
         double xw[kR], yw[kR], xv[kR], yv[kR];
         double ga = 0.0;
         if (GLOBAL) {
@@ -98,9 +120,10 @@ __global__ void __launch_bounds__(GLOBAL ? 1024 : 512)
         for (int o = 8; o > 0; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
         const double al = active ? nrm2[a] : 0.0, be = active ? nrm2[b] : 0.0;
         if (active && ga != 0.0 && ga * ga > tol2 * al * be) {
-          const double zeta = (be - al) / (2.0 * ga);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) / (fabs(zeta) + sqrt(fma(zeta, zeta, 1.0)));
-          const double c = rsqrt(fma(t, t, 1.0)), sn = c * t;
+          const double zeta = (be - al) * svd_rcp(2.0 * fabs(ga)) * (ga > 0.0 ? 1.0 : -1.0);
+          const double z2 = fma(zeta, zeta, 1.0);
+          const double t = (zeta >= 0.0 ? 1.0 : -1.0) * svd_rcp(fabs(zeta) + z2 * svd_rsqrt(z2));
+          const double c = svd_rsqrt(fma(t, t, 1.0)), sn = c * t;
           if (GLOBAL) {
             for (int i = hl; i < l; i += 16) {
               const double x = wa[i], y = wb[i];
@@ -214,10 +237,16 @@ int launch_small_svd(const double* W, int l, double* U, double* S, double* V, do
   }
   const int le = l + (l & 1);
   const size_t smem = ((size_t)le * l + (size_t)le * le) * sizeof(double);
-  APX_CUDA(cudaFuncSetAttribute(hestenes_svd_kernel<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  hestenes_svd_kernel<false><<<1, 512, smem, st>>>(W, l, U, S, V, VT, nullptr);
-  APX_LAUNCH_CHECK();
-  return OK;
+  auto go = [&](auto kern) -> int {
+    APX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<1, 512, smem, st>>>(W, l, U, S, V, VT, nullptr);
+    APX_LAUNCH_CHECK();
+    return OK;
+  };
+  if (le <= 32) return go(hestenes_svd_kernel<false, 2>);
+  if (le <= 48) return go(hestenes_svd_kernel<false, 3>);
+  if (le <= 64) return go(hestenes_svd_kernel<false, 4>);
+  return go(hestenes_svd_kernel<false, 8>);
 }
 
 // y[i*ldy + j] (+)= alpha * x[i*ldx + j] * (rowscale ? rowscale[i] : 1), i < rows, j < cols
