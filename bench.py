@@ -53,7 +53,7 @@ WORKLOADS = {
 }
 # Stage markers recorded by the C4 plan (capi.cu run_mixed_f32_umma): 0 start | hi stream: 1 B
 # decomposed, 2 gather done | lo stream: 3 Y, 4 QR, 5 Bm, 9 W GEMM, 6 W | main: 7 M += Q.W, 8 end.
-N_MARKS = 17
+N_MARKS = 18
 # C4 stage markers (capi.cu run_mixed_f32_resid / run_mixed_f32_umma): name -> (start, end);
 # "join" = the later of markers 2 and 7. GATHER_MARKS: the gather's own span (timed region).
 SPANS = {
@@ -365,7 +365,7 @@ def run_c4(args, rank, world, local_rank):
     # critical-path timeline of the residual plan (hi stream), ms from the product's start
     timeline = None
     if not direct:
-        marks = {"Y": 3, "QR gram": 12, "QR cholinv": 13, "QR apply": 14, "QR pass 2 (gated)": 15, "QR done": 4,
+        marks = {"Y start": 17, "Y": 3, "QR gram": 12, "QR cholinv": 13, "QR apply": 14, "QR pass 2 (gated)": 15, "QR done": 4,
                  "Bm GEMM": 16, "Bm finalize": 5, "dA": 10, "gather start": 11, "gather end": 2, "end": 8}
         timeline = {k: round(statistics.mean(evs[s][0].elapsed_time(evs[s][i]) for s in range(args.steps)), 4)
                     for k, i in marks.items()}

@@ -600,7 +600,9 @@ static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int
     const char* e = getenv("APX_EN_CPS");
     return e ? std::max(1, std::min(8, atoi(e))) : 8;
   }();
-  APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, hi, kNumSMs));
+  stage_mark(17, hi);
+  static const int y_sms = getenv("APX_Y_SMS") ? y_sm_budget() : kNumSMs;  // tuning knob
+  APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, hi, y_sms));
   stage_mark(3, hi);
   APX_CUDA(cudaStreamWaitEvent(hi, ss->b_read, 0));  // lo's resets (long done)
   if (b_after_y) {

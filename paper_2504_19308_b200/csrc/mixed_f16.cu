@@ -253,13 +253,18 @@ __global__ void __launch_bounds__(NT, 1)
 #pragma unroll
         for (int r = 0; r < kHR; ++r) acc[q][r] = 0.f;
       // batch b + 1's lambda' loads are in flight while batch b is consumed
+      // (the batch's shifts ride along: their shared loads head each column's index chain)
       uint32_t lvA[kHU][LW], lvB[kHU][LW];
+      int jA[kHU], jB[kHU];
 #pragma unroll
-      for (int u = 0; u < kHU; ++u) ldg_nc_words<LW>(lrow + (size_t)u * lstride, lvA[u]);
-      auto compute = [&](int t0, const uint32_t (&lv)[kHU][LW]) {
+      for (int u = 0; u < kHU; ++u) {
+        ldg_nc_words<LW>(lrow + (size_t)u * lstride, lvA[u]);
+        jA[u] = sJ[u];
+      }
+      auto compute = [&](const int (&jv)[kHU], const uint32_t (&lv)[kHU][LW]) {
 #pragma unroll
         for (int u = 0; u < kHU; ++u) {
-          const int jt = sJ[t0 + u];
+          const int jt = jv[u];
 #pragma unroll
           for (int q = 0; q < CPT; ++q) {
             unsigned m = (unsigned)(cbase + q * NT + jt);
@@ -281,15 +286,21 @@ __global__ void __launch_bounds__(NT, 1)
       for (int t0 = 0; t0 < kp; t0 += 2 * kHU) {
         if (t0 + kHU < kp) {
 #pragma unroll
-          for (int u = 0; u < kHU; ++u) ldg_nc_words<LW>(lrow + (size_t)(t0 + kHU + u) * lstride, lvB[u]);
+          for (int u = 0; u < kHU; ++u) {
+            ldg_nc_words<LW>(lrow + (size_t)(t0 + kHU + u) * lstride, lvB[u]);
+            jB[u] = sJ[t0 + kHU + u];
+          }
         }
-        compute(t0, lvA);
+        compute(jA, lvA);
         if (t0 + kHU >= kp) break;
         if (t0 + 2 * kHU < kp) {
 #pragma unroll
-          for (int u = 0; u < kHU; ++u) ldg_nc_words<LW>(lrow + (size_t)(t0 + 2 * kHU + u) * lstride, lvA[u]);
+          for (int u = 0; u < kHU; ++u) {
+            ldg_nc_words<LW>(lrow + (size_t)(t0 + 2 * kHU + u) * lstride, lvA[u]);
+            jA[u] = sJ[t0 + 2 * kHU + u];
+          }
         }
-        compute(t0 + kHU, lvB);
+        compute(jB, lvB);
       }
 #pragma unroll
       for (int r = 0; r < kHR; ++r)

@@ -60,7 +60,7 @@ class MixedPipeline:
 
     def __init__(self, n: int, k_svd: int, k_cyc: int, order: int = 1, depth: int = 2,
                  power_iterations: int = 0, split3: bool = False, dtype=torch.float32,
-                 model: ErrorModel | None = None):
+                 model: ErrorModel | None = None, direct: bool = False):
         if order not in (0, 1):
             raise ValueError("order must be 0 or 1")
         if not 1 <= k_svd <= n or not 0 <= k_cyc <= n:
@@ -72,6 +72,7 @@ class MixedPipeline:
         self.dev = D.require_cuda()
         self.n, self.k_svd, self.k_cyc, self.order = n, k_svd, k_cyc, order
         self.q, self.split3, self.dtype, self.model = power_iterations, split3, dtype, model
+        self.flags = (1 if split3 else 0) | (4 if direct else 0)  # direct: the all-fp32 plan
         self.code = N.APX_F32 if dtype == torch.float32 else N.APX_F64
         wsb = N.size("apx_mixed_first_order_workspace", self.code, n, k_svd, k_cyc, order)
         self.slots = []
@@ -124,7 +125,7 @@ class MixedPipeline:
             self.s_comp.wait_event(sl.ev_in)
             sl.ev_start.record(self.s_comp)
             N.call("apx_mixed_first_order", self.code, sl.A.data_ptr(), sl.B.data_ptr(), self.n, self.k_svd,
-                   self.k_cyc, self.order, self.q, sl.omega.data_ptr(), None, 1 if self.split3 else 0,
+                   self.k_cyc, self.order, self.q, sl.omega.data_ptr(), None, self.flags,
                    sl.M.data_ptr(), sl.sel.data_ptr(), sl.scal.data_ptr(), sl.ws.data_ptr(), sl.ws.numel(),
                    self.s_comp.cuda_stream)
             sl.ev_comp.record(self.s_comp)
