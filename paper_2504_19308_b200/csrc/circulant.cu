@@ -511,7 +511,8 @@ __global__ void __launch_bounds__(512) circ_right2_kernel(const T* __restrict__ 
                                                           int kb, const double2* __restrict__ roots,
                                                           double2* __restrict__ M,
                                                           const double2* __restrict__ Xpre, int row_base = 0,
-                                                          int row_end = -1, int lin_out = 0) {
+                                                          int row_end = -1, int lin_out = 0,
+                                                          double* __restrict__ msq_part = nullptr) {
   // [row_base, row_end) (sharded product): the CTA pairs cover these rows of term2; M and Xpre
   // hold them from row row_base on (A is the full operand)
   if (row_end < 0) row_end = n;
@@ -627,10 +628,22 @@ __global__ void __launch_bounds__(512) circ_right2_kernel(const T* __restrict__ 
   __syncthreads();
   fft_block(x0, scratch, n, roots, true);
   fft_block(x1, scratch, n, roots, true);
+  double msq = 0.0;  // ||M||^2 of the two finished rows (msq_part: one fixed-order partial per CTA)
   for (int c = threadIdx.x; c < n; c += blockDim.x) {
     double2* pm = M + (size_t)r0 * n + c;
-    *pm = cadd(*pm, cconj(x0[fsw(c, n)]));
-    if (two) pm[n] = cadd(pm[n], cconj(x1[fsw(c, n)]));
+    const double2 v0 = cadd(*pm, cconj(x0[fsw(c, n)]));
+    *pm = v0;
+    msq = fma(v0.x, v0.x, fma(v0.y, v0.y, msq));
+    if (two) {
+      const double2 v1 = cadd(pm[n], cconj(x1[fsw(c, n)]));
+      pm[n] = v1;
+      msq = fma(v1.x, v1.x, fma(v1.y, v1.y, msq));
+    }
+  }
+  if (msq_part != nullptr) {
+    __shared__ double red[32];
+    msq = block_sum(msq, red);
+    if (threadIdx.x == 0) msq_part[blockIdx.x] = msq;
   }
 }
 
@@ -1209,6 +1222,7 @@ __global__ void __launch_bounds__(256) acc_conj_kernel(const double2* __restrict
 struct CircPlan {
   double2 *roots, *S_a, *S_b, *Ssel_a, *L_a, *Ssel_b, *L_b;
   double *part, *mag_a, *mag_b, *red;
+  double *red2, *msq;  // side-stream ||A||^2 / ||B||^2 partials; per-CTA ||M||^2 of term2's epilogue
   int cpc, parts;
 };
 
@@ -1226,6 +1240,8 @@ static void plan_circ(Workspace& ws, CircPlan& p, int n, int k, bool need_sa_ful
   p.mag_a = ws.take<double>(n);
   p.mag_b = ws.take<double>(n);
   p.red = ws.take<double>(4 * kNumSMs + 64);
+  p.red2 = ws.take<double>(4 * kNumSMs + 64);
+  p.msq = ws.take<double>((size_t)ceil_div(n, 2) + 1);
 }
 
 // term1's L rows staged in shared memory by bulk async copies (circ_left2_kernel stage_l; n = 4096:
@@ -1288,6 +1304,17 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
                          int* sa, int* sb, double* scal, const CircPlan& p, cudaStream_t st) {
   stage_mark(0, st);
   APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), st));
+  // ||A||^2 and ||B||^2 on the side stream: HBM passes under the L1-pipe-bound transform kernels
+  cudaStream_t side = st;
+  APX_TRY(side_fork(st, &side));
+  {
+    int sp = 0;
+    const size_t nel = (size_t)n * n * (sizeof(T) / sizeof(double));
+    APX_TRY(launch_sumsq<double>(reinterpret_cast<const double*>(A), nel, p.red2, &sp, side));
+    APX_TRY(launch_sum_vector(p.red2, sp, scal + APX_S_FRO2_A, side));
+    APX_TRY(launch_sumsq<double>(reinterpret_cast<const double*>(B), nel, p.red2, &sp, side));
+    APX_TRY(launch_sum_vector(p.red2, sp, scal + APX_S_FRO2_B, side));
+  }
   launch_roots(p.roots, n, st);
   APX_LAUNCH_CHECK();
   T* skew = reinterpret_cast<T*>(M);  // M (n x n complex) is scratch until the left product
@@ -1334,7 +1361,8 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
         APX_TRY(launch_big_dA<T>(A, n, p.Ssel_a, sa, k, p.roots, p.S_a, 0, n, st));
         Xpre = p.S_a;
       }
-      fn<<<(unsigned)ceil_div(n, 2), 512, smem, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M, Xpre, 0, (int)n, right2_linear());
+      fn<<<(unsigned)ceil_div(n, 2), 512, smem, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M, Xpre, 0, (int)n,
+                                                      right2_linear(), p.msq);
     } else {
       auto fn = circ_right_kernel<T>;
       APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
@@ -1343,14 +1371,14 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
     APX_LAUNCH_CHECK();
   }
   stage_mark(3, st);
-  int parts = 0;
-  APX_TRY(launch_sumsq<double>(reinterpret_cast<const double*>(M), (size_t)2 * n * n, p.red, &parts, st));
-  APX_TRY(launch_sum_vector(p.red, parts, scal + APX_S_FRO2_M, st));
-  const size_t nel = (size_t)n * n * (sizeof(T) / sizeof(double));
-  APX_TRY(launch_sumsq<double>(reinterpret_cast<const double*>(A), nel, p.red, &parts, st));
-  APX_TRY(launch_sum_vector(p.red, parts, scal + APX_S_FRO2_A, st));
-  APX_TRY(launch_sumsq<double>(reinterpret_cast<const double*>(B), nel, p.red, &parts, st));
-  APX_TRY(launch_sum_vector(p.red, parts, scal + APX_S_FRO2_B, st));
+  if (order == 1 && pairs) {  // term2's epilogue left one ||M||^2 partial per CTA
+    APX_TRY(launch_sum_vector(p.msq, (int)ceil_div(n, 2), scal + APX_S_FRO2_M, st));
+  } else {
+    int parts = 0;
+    APX_TRY(launch_sumsq<double>(reinterpret_cast<const double*>(M), (size_t)2 * n * n, p.red, &parts, st));
+    APX_TRY(launch_sum_vector(p.red, parts, scal + APX_S_FRO2_M, st));
+  }
+  APX_TRY(side_join(st, side));
   stage_mark(4, st);
   return OK;
 }
@@ -1777,7 +1805,7 @@ static int run_circ_rows_phase(int phase, const T* A, const T* B, int n, int k, 
     auto fn = circ_right2_kernel<T>;
     APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
     fn<<<(unsigned)ceil_div(m, 2), 512, smem2, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M_rows, p.Xpre,
-                                                     row0, row0 + m, right2_linear());
+                                                     row0, row0 + m, right2_linear(), (double*)nullptr);
     APX_LAUNCH_CHECK();
   }
   int parts = 0;
