@@ -11,6 +11,7 @@
 #include "../../include/apx.h"
 #include "common.cuh"
 #include "fft.cuh"
+#include "fft16.cuh"
 #include <type_traits>
 #include "kernels.cuh"
 
@@ -501,6 +502,150 @@ __global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B
       if (two) dst[1] = b;
     }
   }
+}
+
+// ---------------------------------------------------------------------------------------------
+// term1 for n = 4096, real B, two columns per CTA on the radix-16 transform (fft16.cuh):
+//   1. the first half of the CTA (256 threads) packs the two real columns as Z = b0 + i b1 and runs
+//      one forward fft4096_r16 from the global loads; Z goes to shared memory in plain order;
+//   2. all 512 threads gather for positions p = tid + 512 i: with q = p - s_t, P = sum_t L_t[p] Z[q]
+//      and N = sum_t L_t[p] conj Z[-q], so FB0 . L = (P + N) / 2 and FB1 . L = (P - N) / 2i -- the
+//      split of Z into FB0 and FB1 needs no pass of its own;
+//   3. each half runs the inverse transform of one column and writes it from its registers.
+// Shared traffic per column ~1.6 MB against ~2.2 MB for circ_left2_kernel (each transform: two
+// exchanges instead of bit reversal plus four radix-8 passes). (Four columns per CTA, which would
+// halve the L_t traffic, needs 64 accumulator doubles per thread and spilled.)
+// ---------------------------------------------------------------------------------------------
+__global__ void __launch_bounds__(512) circ_left2_r16_kernel(const double* __restrict__ B, const double2* __restrict__ L,
+                                                             const int* __restrict__ sel, int k,
+                                                             const double2* __restrict__ roots, double2* __restrict__ M) {
+  constexpr int n = 4096;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* buf0 = reinterpret_cast<double2*>(smem_raw);
+  double2* buf1 = buf0 + kFFT16Buf;
+  int* s_sel = reinterpret_cast<int*>(buf1 + kFFT16Buf);
+  const int tid = threadIdx.x, half = tid >> 8, t = tid & 255;
+  for (int q = tid; q < k; q += blockDim.x) s_sel[q] = sel[q];
+  const int c0 = 2 * blockIdx.x;
+  if (half == 0) {
+    // columns c0, c0 + 1 of rows t + 256 m: one 16-byte load per row
+    double2 v[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = __ldg(reinterpret_cast<const double2*>(B + (size_t)(t + 256 * m) * n + c0));
+    fft4096_r16<false>(v, buf0, roots, t, 1);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) buf1[t + 256 * m] = v[m];
+  }
+  __syncthreads();
+  double2 P[kPP], N[kPP];
+#pragma unroll
+  for (int i = 0; i < kPP; ++i) P[i] = N[i] = make_double2(0.0, 0.0);
+  for (int q = 0; q < k; ++q) {
+    const int sq = s_sel[q];
+    const double2* Lq = L + (size_t)q * n;
+    double2 l[kPP];
+#pragma unroll
+    for (int i = 0; i < kPP; ++i) l[i] = __ldg(Lq + tid + 512 * i);
+#pragma unroll
+    for (int i = 0; i < kPP; ++i) {
+      const int p = tid + 512 * i;
+      const int src = (p - sq) & (n - 1), neg = (n - src) & (n - 1);
+      P[i] = cmac(P[i], l[i], buf1[src]);
+      N[i] = cmacc(N[i], l[i], buf1[neg]);  // l * conj(Z[-q])
+    }
+  }
+  __syncthreads();  // every Z read done: the buffers take the two columns' gather results
+#pragma unroll
+  for (int i = 0; i < kPP; ++i) {
+    const int p = tid + 512 * i;
+    // FB0 . L = (P + N) / 2 -> column c0; FB1 . L = (P - N) / 2i -> column c0 + 1
+    buf0[p] = make_double2(0.5 * (P[i].x + N[i].x), 0.5 * (P[i].y + N[i].y));
+    buf1[p] = make_double2(0.5 * (P[i].y - N[i].y), -0.5 * (P[i].x - N[i].x));
+  }
+  __syncthreads();
+  double2* xb = half ? buf1 : buf0;
+  double2 v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) v[m] = xb[t + 256 * m];
+  fft4096_r16<true>(v, xb, roots, t, 1 + half);
+  const int col = c0 + half;
+#pragma unroll
+  for (int m = 0; m < 16; ++m) M[(size_t)(t + 256 * m) * n + col] = v[m];
+}
+
+// term2 for n = 4096 on the radix-16 transform, two rows per CTA, from the precomputed conj(dA)
+// rows (big_dA_win_kernel): each half transforms one row from its global loads, both rows go to
+// shared memory in plain order, all 512 threads gather (y += x[(p + s) mod n] conj L_s[(p + s) mod n]
+// for both rows, one L load per pair), each half inverse-transforms one row and adds conj of it onto
+// M's row straight from its registers (coalesced over t), with one ||M||^2 partial per CTA.
+__global__ void __launch_bounds__(512) circ_right2_r16_kernel(const double2* __restrict__ Xpre,
+                                                              const double2* __restrict__ LB,
+                                                              const int* __restrict__ selB, int kb,
+                                                              const double2* __restrict__ roots,
+                                                              double2* __restrict__ M, double* __restrict__ msq_part) {
+  constexpr int n = 4096;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* buf0 = reinterpret_cast<double2*>(smem_raw);
+  double2* buf1 = buf0 + kFFT16Buf;
+  int* sB = reinterpret_cast<int*>(buf1 + kFFT16Buf);
+  __shared__ double red[32];
+  const int tid = threadIdx.x, half = tid >> 8, t = tid & 255;
+  for (int q = tid; q < kb; q += blockDim.x) sB[q] = selB[q];
+  const int row = 2 * blockIdx.x + half;
+  double2* xb = half ? buf1 : buf0;
+  // the epilogue's read-modify-write of M (term1, DRAM-resident by now): pull the row toward L2
+  if (t == 0 && ((uintptr_t)M & 15) == 0)
+    asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(M + (size_t)row * n),
+                 "r"((unsigned)(n * sizeof(double2)))
+                 : "memory");
+  double2 v[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) v[m] = __ldg(Xpre + (size_t)row * n + t + 256 * m);
+  fft4096_r16<false>(v, xb, roots, t, 1 + half);
+#pragma unroll
+  for (int m = 0; m < 16; ++m) xb[t + 256 * m] = v[m];
+  __syncthreads();
+  double2 y0[kPP], y1[kPP];
+#pragma unroll
+  for (int i = 0; i < kPP; ++i) y0[i] = y1[i] = make_double2(0.0, 0.0);
+  for (int q = 0; q < kb; ++q) {
+    const int sq = sB[q];
+    const double2* Lq = LB + (size_t)q * n;
+    // two half-batches of L loads in flight (as circ_right2_kernel)
+#pragma unroll
+    for (int h = 0; h < kPP; h += kPP / 2) {
+      double2 l[kPP];
+#pragma unroll
+      for (int i = h; i < h + kPP / 2; ++i) l[i] = __ldg(Lq + ((tid + 512 * i + sq) & (n - 1)));
+#pragma unroll
+      for (int i = h; i < h + kPP / 2; ++i) {
+        const int src = (tid + 512 * i + sq) & (n - 1);
+        y0[i] = cmacc(y0[i], buf0[src], l[i]);
+        y1[i] = cmacc(y1[i], buf1[src], l[i]);
+      }
+    }
+  }
+  __syncthreads();  // every gather read done
+#pragma unroll
+  for (int i = 0; i < kPP; ++i) {
+    buf0[tid + 512 * i] = y0[i];
+    buf1[tid + 512 * i] = y1[i];
+  }
+  __syncthreads();
+#pragma unroll
+  for (int m = 0; m < 16; ++m) v[m] = xb[t + 256 * m];
+  fft4096_r16<true>(v, xb, roots, t, 1 + half);
+  double msq = 0.0;
+  double2* mr = M + (size_t)row * n;
+#pragma unroll
+  for (int m = 0; m < 16; ++m) {
+    const double2 o = mr[t + 256 * m];
+    const double2 nv = make_double2(o.x + v[m].x, o.y - v[m].y);  // + conj
+    mr[t + 256 * m] = nv;
+    msq = fma(nv.x, nv.x, fma(nv.y, nv.y, msq));
+  }
+  msq = block_sum(msq, red);
+  if (tid == 0 && msq_part) msq_part[blockIdx.x] = msq;
 }
 
 template <typename T>
@@ -1332,7 +1477,13 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
   stage_mark(1, st);
   const size_t smem = fft_smem_bytes(n, 2) + (size_t)2 * k * sizeof(int);  // + staged selections
   const bool pairs = n >= 2 && n <= kPP * 512;  // two columns / rows per CTA (same smem footprint)
-  if (pairs) {
+  static const bool r16_off = getenv("APX_CIRC_R16") != nullptr && atoi(getenv("APX_CIRC_R16")) == 0;
+  if (std::is_same<T, double>::value && n == 4096 && !r16_off) {
+    const size_t smem2r = (size_t)2 * kFFT16Buf * sizeof(double2) + (size_t)k * sizeof(int);
+    APX_CUDA(cudaFuncSetAttribute(circ_left2_r16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2r));
+    circ_left2_r16_kernel<<<n / 2, 512, smem2r, st>>>(reinterpret_cast<const double*>(B), p.L_a, sa, k, p.roots, M);
+    APX_LAUNCH_CHECK();
+  } else if (pairs) {
     auto fn = circ_left2_kernel<T>;
     const int stage_l = left2_stage_l(n, k);
     const size_t smem_l = smem + (stage_l ? left2_stage_bytes(n) : 0);
@@ -1361,8 +1512,14 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
         APX_TRY(launch_big_dA<T>(A, n, p.Ssel_a, sa, k, p.roots, p.S_a, 0, n, st));
         Xpre = p.S_a;
       }
-      fn<<<(unsigned)ceil_div(n, 2), 512, smem, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M, Xpre, 0, (int)n,
-                                                      right2_linear(), p.msq);
+      if (Xpre != nullptr && n == 4096 && !r16_off) {
+        const size_t smem2r = (size_t)2 * kFFT16Buf * sizeof(double2) + (size_t)k * sizeof(int);
+        APX_CUDA(cudaFuncSetAttribute(circ_right2_r16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2r));
+        circ_right2_r16_kernel<<<n / 2, 512, smem2r, st>>>(Xpre, p.L_b, sb, k, p.roots, M, p.msq);
+      } else {
+        fn<<<(unsigned)ceil_div(n, 2), 512, smem, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M, Xpre, 0,
+                                                        (int)n, right2_linear(), p.msq);
+      }
     } else {
       auto fn = circ_right_kernel<T>;
       APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
