@@ -188,6 +188,112 @@ __global__ void __launch_bounds__(512) circ_decompose_rows_kernel(const T* __res
   for (int t = threadIdx.x; t < n; t += blockDim.x) mag2_part[(size_t)blk * n + t] = m2[t];
 }
 
+// The decomposition for real operands at n = 4096 on the radix-16 transform: the two halves of
+// the CTA take alternate cycle pairs of the CTA's range [j0, j1). A pair (x_j, x_{j+1}) is staged
+// from A's diagonals exactly as the direct path of circ_decompose_rows_kernel (thread unit = row
+// i of A: x_j[(i - j) mod n] and x_{j+1}[(i - j - 1) mod n]), read back as Z[t + 256 m] into the
+// transform's registers, transformed, and split F_j = (Z[t] + conj Z[-t]) / 2n, F_{j+1} =
+// (Z[t] - conj Z[-t]) / 2in with the conjugate partners read from the plain-order copy; each thread
+// keeps the magnitude partials of its 16 frequencies t + 256 m in registers, and the two halves'
+// partials are added (half 0 + half 1) into the CTA's slot of mag2_part. Same CTA grid and slots as
+// circ_decompose_rows_kernel (b_off / j_base for the sharded product).
+__global__ void __launch_bounds__(512) circ_decompose_r16_kernel(const double* __restrict__ A, int cpc,
+                                                                 const double2* __restrict__ roots,
+                                                                 double2* __restrict__ St,
+                                                                 double* __restrict__ mag2_part, int b_off,
+                                                                 int j_base) {
+  constexpr int n = 4096;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, half = tid >> 8, t = tid & 255, bar = 1 + half;
+  double2* buf = reinterpret_cast<double2*>(smem_raw) + (size_t)half * kFFT16Buf;
+  double* bufd = reinterpret_cast<double*>(buf);
+  St -= (size_t)j_base * n;
+  const int blk = blockIdx.x + b_off;
+  const int j0 = blk * cpc, j1 = min(n, j0 + cpc);
+  const double h = 0.5 / n;
+  double m2[16];
+#pragma unroll
+  for (int m = 0; m < 16; ++m) m2[m] = 0.0;
+  for (int j = j0 + 2 * half; j < j1; j += 4) {
+    {
+      // all 32 loads in flight before the first store (a prefetch of the next pair spilled)
+      double xr[16], xi[16];
+#pragma unroll
+      for (int m = 0; m < 16; ++m) {
+        const int i = t + 256 * m;
+        const int c = (i - j) & (n - 1), c1 = (c - 1) & (n - 1);
+        xr[m] = __ldg(A + (size_t)i * n + c);
+        xi[m] = j + 1 < j1 ? __ldg(A + (size_t)i * n + c1) : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < 16; ++m) {
+        const int i = t + 256 * m;
+        const int c = (i - j) & (n - 1), c1 = (c - 1) & (n - 1);
+        bufd[2 * c] = xr[m];
+        bufd[2 * c1 + 1] = xi[m];
+      }
+    }
+    named_bar(bar, 256);
+    double2 v[16];
+#pragma unroll
+    for (int m = 0; m < 16; ++m) v[m] = buf[t + 256 * m];
+    named_bar(bar, 256);  // every read of the staged pair done before the transform writes
+    fft4096_r16<false>(v, buf, roots, t, bar);
+#pragma unroll
+    for (int m = 0; m < 16; ++m) buf[t + 256 * m] = v[m];
+    named_bar(bar, 256);
+    const bool two = j + 1 < j1;
+#pragma unroll
+    for (int m = 0; m < 16; ++m) {
+      const int tau = t + 256 * m;
+      const double2 z = v[m], zm = buf[(n - tau) & (n - 1)];
+      const double2 f0 = make_double2(h * (z.x + zm.x), h * (z.y - zm.y));
+      St[(size_t)j * n + tau] = f0;
+      double a = fma(f0.x, f0.x, fma(f0.y, f0.y, m2[m]));
+      if (two) {
+        const double2 f1 = make_double2(h * (z.y + zm.y), h * (zm.x - z.x));
+        St[(size_t)(j + 1) * n + tau] = f1;
+        a = fma(f1.x, f1.x, fma(f1.y, f1.y, a));
+      }
+      m2[m] = a;
+    }
+    named_bar(bar, 256);  // the conjugate-partner reads done before the next pair is staged
+  }
+  __syncthreads();
+  double* other = reinterpret_cast<double*>(smem_raw);  // half 1's partials, then half 0 adds
+  if (half == 1) {
+#pragma unroll
+    for (int m = 0; m < 16; ++m) other[t + 256 * m] = m2[m];
+  }
+  __syncthreads();
+  if (half == 0) {
+#pragma unroll
+    for (int m = 0; m < 16; ++m) mag2_part[(size_t)blk * n + t + 256 * m] = m2[m] + other[t + 256 * m];
+  }
+}
+
+// decomposition launch shared by the single-device and the sharded plans: the radix-16 kernel for
+// real operands at n = 4096 (APX_CIRC_R16=0 selects circ_decompose_rows_kernel)
+template <typename T>
+static int launch_decompose_rows(const T* X, int n, int cpc, const double2* roots, double2* St, double* mag2_part,
+                                 int blocks, int b_off, int j_base, int direct, cudaStream_t st) {
+  static const bool r16_off = getenv("APX_CIRC_R16") != nullptr && atoi(getenv("APX_CIRC_R16")) == 0;
+  if (std::is_same<T, double>::value && n == 4096 && direct && !r16_off) {
+    const size_t smem = (size_t)2 * kFFT16Buf * sizeof(double2);
+    APX_CUDA(cudaFuncSetAttribute(circ_decompose_r16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    circ_decompose_r16_kernel<<<blocks, 512, smem, st>>>(reinterpret_cast<const double*>(X), cpc, roots, St,
+                                                          mag2_part, b_off, j_base);
+    APX_LAUNCH_CHECK();
+    return OK;
+  }
+  const size_t smem = fft_smem_bytes(n, 1) + (size_t)n * sizeof(double);
+  auto fn = circ_decompose_rows_kernel<T>;
+  APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+  fn<<<blocks, 512, smem, st>>>(X, n, cpc, roots, St, mag2_part, b_off, j_base, direct);
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
 // mag[t] = sqrt(sum_p part[p][t]): a CTA covers 32 columns with 8 slices of the parts (slice s:
 // parts s, s+8, ...), combined in slice order -- a fixed order, 8x the loads in flight of a
 // column-per-thread loop over all parts (which was latency-bound: 33 us at n = 4096)
@@ -516,9 +622,13 @@ __global__ void __launch_bounds__(512) circ_left2_kernel(const T* __restrict__ B
 // exchanges instead of bit reversal plus four radix-8 passes). (Four columns per CTA, which would
 // halve the L_t traffic, needs 64 accumulator doubles per thread and spilled.)
 // ---------------------------------------------------------------------------------------------
+// col_base / col_end / ldm (sharded product, as circ_left2_kernel): the CTA pairs cover columns
+// [col_base, col_end) (col_base even: the full grid's pairs), written to an n x (col_end - col_base)
+// block with leading dimension ldm.
 __global__ void __launch_bounds__(512) circ_left2_r16_kernel(const double* __restrict__ B, const double2* __restrict__ L,
                                                              const int* __restrict__ sel, int k,
-                                                             const double2* __restrict__ roots, double2* __restrict__ M) {
+                                                             const double2* __restrict__ roots, double2* __restrict__ M,
+                                                             int col_base, int col_end, int64_t ldm) {
   constexpr int n = 4096;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* buf0 = reinterpret_cast<double2*>(smem_raw);
@@ -526,7 +636,7 @@ __global__ void __launch_bounds__(512) circ_left2_r16_kernel(const double* __res
   int* s_sel = reinterpret_cast<int*>(buf1 + kFFT16Buf);
   const int tid = threadIdx.x, half = tid >> 8, t = tid & 255;
   for (int q = tid; q < k; q += blockDim.x) s_sel[q] = sel[q];
-  const int c0 = 2 * blockIdx.x;
+  const int c0 = col_base + 2 * blockIdx.x;
   if (half == 0) {
     // columns c0, c0 + 1 of rows t + 256 m: one 16-byte load per row
     double2 v[16];
@@ -569,8 +679,10 @@ __global__ void __launch_bounds__(512) circ_left2_r16_kernel(const double* __res
   for (int m = 0; m < 16; ++m) v[m] = xb[t + 256 * m];
   fft4096_r16<true>(v, xb, roots, t, 1 + half);
   const int col = c0 + half;
+  if (col < col_end) {
 #pragma unroll
-  for (int m = 0; m < 16; ++m) M[(size_t)(t + 256 * m) * n + col] = v[m];
+    for (int m = 0; m < 16; ++m) M[(size_t)(t + 256 * m) * ldm + (col - col_base)] = v[m];
+  }
 }
 
 // term2 for n = 4096 on the radix-16 transform, two rows per CTA, from the precomputed conj(dA)
@@ -582,8 +694,13 @@ __global__ void __launch_bounds__(512) circ_right2_r16_kernel(const double2* __r
                                                               const double2* __restrict__ LB,
                                                               const int* __restrict__ selB, int kb,
                                                               const double2* __restrict__ roots,
-                                                              double2* __restrict__ M, double* __restrict__ msq_part) {
+                                                              double2* __restrict__ M, double* __restrict__ msq_part,
+                                                              int row_base, int row_end) {
+  // row_base / row_end (sharded product, as circ_right2_kernel): the CTA pairs cover rows
+  // [row_base, row_end) of term2; M and Xpre hold them from row row_base on
   constexpr int n = 4096;
+  M -= (size_t)row_base * n;
+  Xpre -= (size_t)row_base * n;
   extern __shared__ __align__(16) unsigned char smem_raw[];
   double2* buf0 = reinterpret_cast<double2*>(smem_raw);
   double2* buf1 = buf0 + kFFT16Buf;
@@ -591,16 +708,17 @@ __global__ void __launch_bounds__(512) circ_right2_r16_kernel(const double2* __r
   __shared__ double red[32];
   const int tid = threadIdx.x, half = tid >> 8, t = tid & 255;
   for (int q = tid; q < kb; q += blockDim.x) sB[q] = selB[q];
-  const int row = 2 * blockIdx.x + half;
+  const int row = row_base + 2 * blockIdx.x + half;
+  const bool live = row < row_end;  // an odd row count leaves the last CTA's second row empty
   double2* xb = half ? buf1 : buf0;
   // the epilogue's read-modify-write of M (term1, DRAM-resident by now): pull the row toward L2
-  if (t == 0 && ((uintptr_t)M & 15) == 0)
+  if (t == 0 && live && ((uintptr_t)(M + (size_t)row * n) & 15) == 0)
     asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(M + (size_t)row * n),
                  "r"((unsigned)(n * sizeof(double2)))
                  : "memory");
   double2 v[16];
 #pragma unroll
-  for (int m = 0; m < 16; ++m) v[m] = __ldg(Xpre + (size_t)row * n + t + 256 * m);
+  for (int m = 0; m < 16; ++m) v[m] = live ? __ldg(Xpre + (size_t)row * n + t + 256 * m) : make_double2(0.0, 0.0);
   fft4096_r16<false>(v, xb, roots, t, 1 + half);
 #pragma unroll
   for (int m = 0; m < 16; ++m) xb[t + 256 * m] = v[m];
@@ -637,12 +755,14 @@ __global__ void __launch_bounds__(512) circ_right2_r16_kernel(const double2* __r
   fft4096_r16<true>(v, xb, roots, t, 1 + half);
   double msq = 0.0;
   double2* mr = M + (size_t)row * n;
+  if (live) {
 #pragma unroll
-  for (int m = 0; m < 16; ++m) {
-    const double2 o = mr[t + 256 * m];
-    const double2 nv = make_double2(o.x + v[m].x, o.y - v[m].y);  // + conj
-    mr[t + 256 * m] = nv;
-    msq = fma(nv.x, nv.x, fma(nv.y, nv.y, msq));
+    for (int m = 0; m < 16; ++m) {
+      const double2 o = mr[t + 256 * m];
+      const double2 nv = make_double2(o.x + v[m].x, o.y - v[m].y);  // + conj
+      mr[t + 256 * m] = nv;
+      msq = fma(nv.x, nv.x, fma(nv.y, nv.y, msq));
+    }
   }
   msq = block_sum(msq, red);
   if (tid == 0 && msq_part) msq_part[blockIdx.x] = msq;
@@ -1422,10 +1542,8 @@ static int circ_decompose_run(const T* A, int n, const CircPlan& p, double2* St,
     circ_skew_kernel<T><<<dim3((unsigned)ceil_div(n, 32), (unsigned)ceil_div(n, 32)), 256, 0, st>>>(A, n, skew);
     APX_LAUNCH_CHECK();
   }
-  auto fn = circ_decompose_rows_kernel<T>;
-  APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-  fn<<<p.parts, 512, smem, st>>>(direct ? A : skew, n, p.cpc, p.roots, St, p.part, 0, 0, direct);
-  APX_LAUNCH_CHECK();
+  (void)smem;
+  APX_TRY(launch_decompose_rows<T>(direct ? A : skew, n, p.cpc, p.roots, St, p.part, p.parts, 0, 0, direct, st));
   mag_finalize_kernel<<<(unsigned)ceil_div(n, 32), 256, 0, st>>>(p.part, p.parts, n, mag);
   APX_LAUNCH_CHECK();
   return OK;
@@ -1481,7 +1599,8 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
   if (std::is_same<T, double>::value && n == 4096 && !r16_off) {
     const size_t smem2r = (size_t)2 * kFFT16Buf * sizeof(double2) + (size_t)k * sizeof(int);
     APX_CUDA(cudaFuncSetAttribute(circ_left2_r16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2r));
-    circ_left2_r16_kernel<<<n / 2, 512, smem2r, st>>>(reinterpret_cast<const double*>(B), p.L_a, sa, k, p.roots, M);
+    circ_left2_r16_kernel<<<n / 2, 512, smem2r, st>>>(reinterpret_cast<const double*>(B), p.L_a, sa, k, p.roots, M,
+                                                       0, n, (int64_t)n);
     APX_LAUNCH_CHECK();
   } else if (pairs) {
     auto fn = circ_left2_kernel<T>;
@@ -1515,7 +1634,7 @@ static int run_circulant(const T* A, const T* B, int n, int k, int order, const 
       if (Xpre != nullptr && n == 4096 && !r16_off) {
         const size_t smem2r = (size_t)2 * kFFT16Buf * sizeof(double2) + (size_t)k * sizeof(int);
         APX_CUDA(cudaFuncSetAttribute(circ_right2_r16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2r));
-        circ_right2_r16_kernel<<<n / 2, 512, smem2r, st>>>(Xpre, p.L_b, sb, k, p.roots, M, p.msq);
+        circ_right2_r16_kernel<<<n / 2, 512, smem2r, st>>>(Xpre, p.L_b, sb, k, p.roots, M, p.msq, 0, n);
       } else {
         fn<<<(unsigned)ceil_div(n, 2), 512, smem, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M, Xpre, 0,
                                                         (int)n, right2_linear(), p.msq);
@@ -1899,9 +2018,8 @@ static int run_circ_rows_phase(int phase, const T* A, const T* B, int n, int k, 
                                 st>>>(ops[o], n, (T*)p.skew, p.j_lo, p.j_hi);
           APX_LAUNCH_CHECK();
         }
-        fn<<<blk1 - blk0, 512, smem, st>>>(direct ? ops[o] : (const T*)p.skew, n, p.cpc, p.roots, Sts[o],
-                                           red_out + (size_t)o * p.parts * n, blk0, p.j_lo, direct);
-        APX_LAUNCH_CHECK();
+        APX_TRY(launch_decompose_rows<T>(direct ? ops[o] : (const T*)p.skew, n, p.cpc, p.roots, Sts[o],
+                                         red_out + (size_t)o * p.parts * n, blk1 - blk0, blk0, p.j_lo, direct, st));
       }
     }
     int parts = 0;
@@ -1945,6 +2063,16 @@ static int run_circ_rows_phase(int phase, const T* A, const T* B, int n, int k, 
       APX_LAUNCH_CHECK();
     }
     if (w > 0) {
+      static const bool r16_off = getenv("APX_CIRC_R16") != nullptr && atoi(getenv("APX_CIRC_R16")) == 0;
+      if (std::is_same<T, double>::value && n == 4096 && !r16_off) {  // the single-device kernel
+        const size_t smem2r = (size_t)2 * kFFT16Buf * sizeof(double2) + (size_t)k * sizeof(int);
+        APX_CUDA(cudaFuncSetAttribute(circ_left2_r16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2r));
+        circ_left2_r16_kernel<<<(unsigned)ceil_div(w, 2), 512, smem2r, st>>>(reinterpret_cast<const double*>(B), p.L_a,
+                                                                             sa, k, p.roots, T1, col0, col0 + w,
+                                                                             (int64_t)w);
+        APX_LAUNCH_CHECK();
+        return OK;
+      }
       auto fn = circ_left2_kernel<T>;
       APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
       const int stage_l = left2_stage_l(n, k);
@@ -1959,10 +2087,18 @@ static int run_circ_rows_phase(int phase, const T* A, const T* B, int n, int k, 
   // phase 4: term2 on this rank's rows (M_rows holds term1's rows, assembled by the caller)
   if (order == 1 && m > 0) {
     APX_TRY(launch_big_dA<T>(A, n, p.Ssel_a, sa, k, p.roots, p.Xpre, row0, row0 + m, st));
-    auto fn = circ_right2_kernel<T>;
-    APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
-    fn<<<(unsigned)ceil_div(m, 2), 512, smem2, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M_rows, p.Xpre,
-                                                     row0, row0 + m, right2_linear(), (double*)nullptr);
+    static const bool r16_off = getenv("APX_CIRC_R16") != nullptr && atoi(getenv("APX_CIRC_R16")) == 0;
+    if (p.Xpre != nullptr && n == 4096 && !r16_off) {  // the single-device kernel
+      const size_t smem2r = (size_t)2 * kFFT16Buf * sizeof(double2) + (size_t)k * sizeof(int);
+      APX_CUDA(cudaFuncSetAttribute(circ_right2_r16_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2r));
+      circ_right2_r16_kernel<<<(unsigned)ceil_div(m, 2), 512, smem2r, st>>>(p.Xpre, p.L_b, sb, k, p.roots, M_rows,
+                                                                            (double*)nullptr, row0, row0 + m);
+    } else {
+      auto fn = circ_right2_kernel<T>;
+      APX_CUDA(cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem2));
+      fn<<<(unsigned)ceil_div(m, 2), 512, smem2, st>>>(A, n, p.Ssel_a, sa, k, p.L_b, sb, k, p.roots, M_rows, p.Xpre,
+                                                       row0, row0 + m, right2_linear(), (double*)nullptr);
+    }
     APX_LAUNCH_CHECK();
   }
   int parts = 0;
