@@ -1376,14 +1376,14 @@ __global__ void __launch_bounds__(256, 2) big_dA_kernel(const T* __restrict__ A,
 // consecutive) instead of L2 loads (big_dA_kernel: 74% of its stalls waited on them). The
 // twiddle of (q, c) is loaded one term ahead. k <= kDaWinMaxK (smem).
 constexpr int kDaWinMaxK = 48;
-template <typename T>
+template <typename T, int ROWS>
 __global__ void __launch_bounds__(256, 2) big_dA_win_kernel(const T* __restrict__ A, int n,
                                                          const double2* __restrict__ Ssel,
                                                          const int* __restrict__ sel, int k,
                                                          const double2* __restrict__ roots,
                                                          double2* __restrict__ X, int row_base, int row_end) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  constexpr int W = 256 + kDaRows - 1;
+  constexpr int W = 256 + ROWS - 1;
   double2* win = reinterpret_cast<double2*>(smem_raw);  // k x W
   // twiddles w_q(c0 + l) = conj(roots[t_q (c0 + l) mod n]), factored as base_q * hi_q[l >> 4] *
   // lo_q[l & 15]: 33 table loads per term per CTA instead of one scattered load per (term, thread)
@@ -1397,7 +1397,7 @@ __global__ void __launch_bounds__(256, 2) big_dA_win_kernel(const T* __restrict_
     else if (j < 16) tw_lo[q][j] = cconj(__ldg(roots + mulmod_n(t, j % n, n)));
     else tw_hi[q][j - 16] = cconj(__ldg(roots + mulmod_n(t, (16 * (j - 16)) % n, n)));
   }
-  const int r0 = row_base + blockIdx.y * kDaRows;
+  const int r0 = row_base + blockIdx.y * ROWS;
   // window j of term q holds S_q[(r0 - c0 - 255 + j) mod n]; thread tid, row rr reads j = 255 - tid + rr
   int dbase = (r0 - c0 - 255) % n;
   if (dbase < 0) dbase += n;
@@ -1410,18 +1410,18 @@ __global__ void __launch_bounds__(256, 2) big_dA_win_kernel(const T* __restrict_
   __syncthreads();
   const int c = c0 + tid;
   if (c >= n) return;
-  double2 ah[kDaRows];
+  double2 ah[ROWS];
 #pragma unroll
-  for (int rr = 0; rr < kDaRows; ++rr) ah[rr] = make_double2(0.0, 0.0);
+  for (int rr = 0; rr < ROWS; ++rr) ah[rr] = make_double2(0.0, 0.0);
   for (int q = 0; q < k; ++q) {
     const double2 w = cmul(cmul(tw_base[q], tw_hi[q][tid >> 4]), tw_lo[q][tid & 15]);
     const double2* wq = win + (size_t)q * W + (255 - tid);
-    APX_DCHECK(255 - tid + kDaRows - 1 < W);
+    APX_DCHECK(255 - tid + ROWS - 1 < W);
 #pragma unroll
-    for (int rr = 0; rr < kDaRows; ++rr) ah[rr] = cmac(ah[rr], wq[rr], w);
+    for (int rr = 0; rr < ROWS; ++rr) ah[rr] = cmac(ah[rr], wq[rr], w);
   }
 #pragma unroll
-  for (int rr = 0; rr < kDaRows; ++rr) {
+  for (int rr = 0; rr < ROWS; ++rr) {
     const size_t r = (size_t)r0 + rr;
     if (r < (size_t)row_end) X[(r - row_base) * n + c] = cconj(csub(ld_c<T>(A, r * n + c), ah[rr]));
   }
@@ -1433,10 +1433,21 @@ template <typename T>
 static int launch_big_dA(const T* A, int n, const double2* Ssel, const int* sel, int k, const double2* roots,
                          double2* X, int row_base, int row_end, cudaStream_t st) {
   const dim3 grid((unsigned)ceil_div(n, 256), (unsigned)ceil_div(row_end - row_base, kDaRows));
+  // rows per CTA of the windowed kernel (APX_DA_ROWS=16|32, tuning knob)
+  static const int da_rows = [] {
+    const char* e = getenv("APX_DA_ROWS");
+    return (e && atoi(e) == 32) ? 32 : 16;
+  }();
   if (k <= kDaWinMaxK && n >= 256 && getenv("APX_DA_L2") == nullptr) {
-    const size_t smem = (size_t)std::max(k, 1) * (256 + kDaRows - 1) * sizeof(double2);
-    APX_CUDA(cudaFuncSetAttribute(big_dA_win_kernel<T>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    big_dA_win_kernel<T><<<grid, 256, smem, st>>>(A, n, Ssel, sel, k, roots, X, row_base, row_end);
+    auto go = [&](auto kern, int rows) -> int {
+      const size_t smem = (size_t)std::max(k, 1) * (256 + rows - 1) * sizeof(double2);
+      APX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const dim3 g((unsigned)ceil_div(n, 256), (unsigned)ceil_div(row_end - row_base, rows));
+      kern<<<g, 256, smem, st>>>(A, n, Ssel, sel, k, roots, X, row_base, row_end);
+      return OK;
+    };
+    if (da_rows == 32) APX_TRY(go(big_dA_win_kernel<T, 32>, 32));
+    else APX_TRY(go(big_dA_win_kernel<T, 16>, 16));
   } else {
     big_dA_kernel<T><<<grid, 256, 0, st>>>(A, n, Ssel, sel, k, roots, X, row_base, row_end);
   }
