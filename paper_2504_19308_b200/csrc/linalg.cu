@@ -458,13 +458,143 @@ __global__ void __launch_bounds__(256) cholinv64_kernel(const double* __restrict
   }
 }
 
+// The same elimination without a CTA barrier per pivot: every pivot row gets its own shared slot
+// (64 rows x (64 + 64) doubles = 64 KB, never reused, so no write-after-read hazard) and its own
+// mbarrier, on which the four owners of row j arrive after publishing it (release) and every thread
+// waits before reading it (acquire). A thread that is still finishing step j's update no longer
+// holds up the publication of row j + 1: the per-step chain is the owner's own update, publish and
+// arrive, instead of the slowest warp plus a barrier.
+__global__ void __launch_bounds__(256) cholinv64f_kernel(const double* __restrict__ Gin, int l,
+                                                         double* __restrict__ Xout, const int* __restrict__ gate,
+                                                         int* __restrict__ breakdown, int* __restrict__ skip_out,
+                                                         double skip_kappa) {
+  pdl_trigger();
+  pdl_wait();
+  if (*gate) return;
+  extern __shared__ __align__(16) double rows[];  // [64][128]: left block, then right block
+  __shared__ __align__(8) uint64_t rbar[64];
+  __shared__ double red[8][2];
+  const int t = threadIdx.x, r = t & 63, c0 = (t >> 6) * 16;
+  const int lane = t & 31, warp = t >> 5;
+  if (t < 64) asm volatile("mbarrier.init.shared::cta.b64 [%0], 4;" ::"r"((uint32_t)__cvta_generic_to_shared(&rbar[t])));
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  double wl[16], wr[16];
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    const int c = c0 + u;
+    wl[u] = (r < l && c < l) ? (c >= r ? Gin[r * l + c] : 0.0) : (c == r ? 1.0 : 0.0);
+    wr[u] = c == r ? 1.0 : 0.0;
+  }
+  double md = (t < 64 && r < l) ? Gin[r * l + r] : 0.0;
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
+  if (lane == 0) red[warp][0] = md;
+  __syncthreads();
+#pragma unroll
+  for (int i = 0; i < 8; ++i) md = fmax(md, red[i][0]);
+  const double tol = 4.0 * l * 2.220446049250313e-16 * md;
+  bool bad = false;
+#pragma unroll 1
+  for (int j = 0; j < l; ++j) {
+    double* bl = rows + (size_t)j * 128;
+    double* br = bl + 64;
+    const uint32_t bar = (uint32_t)__cvta_generic_to_shared(&rbar[j]);
+    if (r == j) {
+#pragma unroll
+      for (int u = 0; u < 16; u += 2) {
+        *reinterpret_cast<double2*>(&bl[c0 + u]) = make_double2(wl[u], wl[u + 1]);
+        *reinterpret_cast<double2*>(&br[c0 + u]) = make_double2(wr[u], wr[u + 1]);
+      }
+      asm volatile("mbarrier.arrive.release.cta.shared::cta.b64 _, [%0];" ::"r"(bar) : "memory");
+    }
+    asm volatile(
+        "{\n.reg .pred p;\nCW_%=:\n"
+        "mbarrier.try_wait.parity.acquire.cta.shared::cta.b64 p, [%0], 0;\n"
+        "@!p bra CW_%=;\n}\n" ::"r"(bar)
+        : "memory");
+    double p = bl[j];
+    if (!(p > tol)) bad = true;  // uniform: every thread reads the same pivot
+    if (!(p > 1e-300)) p = 1.0;  // keep the (discarded) arithmetic finite after a breakdown
+    if (r > j) {
+      const double f = bl[r] * fast_rcp(p);  // A[r][j] / p, with A[r][j] = A[j][r]
+      if (c0 + 15 > j) {
+#pragma unroll
+        for (int u = 0; u < 16; u += 2) {
+          const double2 bv = *reinterpret_cast<const double2*>(&bl[c0 + u]);
+          wl[u] = fma(-f, bv.x, wl[u]);
+          wl[u + 1] = fma(-f, bv.y, wl[u + 1]);
+        }
+      }
+      if (c0 <= j) {
+#pragma unroll
+        for (int u = 0; u < 16; u += 2) {
+          const double2 bv = *reinterpret_cast<const double2*>(&br[c0 + u]);
+          wr[u] = fma(-f, bv.x, wr[u]);
+          wr[u + 1] = fma(-f, bv.y, wr[u + 1]);
+        }
+      }
+    } else if (r == j) {
+      const double rsq = fast_rsqrt(p);
+#pragma unroll
+      for (int u = 0; u < 16; ++u) {
+        wl[u] *= rsq;
+        wr[u] *= rsq;
+      }
+    }
+  }
+  __syncthreads();
+  if (bad) {
+    if (t == 0) {
+      *breakdown = 1;
+      if (skip_out) *skip_out = 1;
+    }
+    return;
+  }
+  double r2 = 0.0, x2 = 0.0;
+  if (r < l) {
+#pragma unroll
+    for (int u = 0; u < 16; ++u) {
+      const int c = c0 + u;
+      if (c >= l) continue;
+      if (c >= r) r2 = fma(wl[u], wl[u], r2);  // R[r][c]
+      const double xv = c <= r ? wr[u] : 0.0;  // (R^{-T})[r][c] = X[c][r]
+      x2 = fma(xv, xv, x2);
+      Xout[c * l + r] = xv;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    r2 += __shfl_xor_sync(0xffffffffu, r2, o);
+    x2 += __shfl_xor_sync(0xffffffffu, x2, o);
+  }
+  if (lane == 0) {
+    red[warp][0] = r2;
+    red[warp][1] = x2;
+  }
+  __syncthreads();
+  if (t == 0 && skip_out) {
+    double sr = 0.0, sx = 0.0;
+    for (int i = 0; i < 8; ++i) {
+      sr += red[i][0];
+      sx += red[i][1];
+    }
+    *skip_out = (sqrt(sr) * sqrt(sx) <= skip_kappa) ? 1 : 0;
+  }
+}
+
 // Cholesky-inverse launch for l <= 64. (Measured alternative: the same elimination on 1024 threads,
 // 4 + 4 columns per thread, was slower -- 65 vs 55 us in the C4 chain, C1 2.19 vs 2.11 ms. The
 // step is bound by its owner warp: rows j and j+1 sit in one warp, so row j's scaling and row
 // j+1's update serialise before row j+1 can be published; tools/chol_probe2.cu, fp64_issue_probe.cu.)
 static cudaError_t launch_cholinv64(const double* G, int l, double* X, const int* gate, int* breakdown, int* skip_out,
                                    double skip_kappa, cudaStream_t st) {
-  return launch_pdl(cholinv64_kernel, dim3(1), dim3(256), 0, st, G, l, X, gate, breakdown, skip_out, skip_kappa);
+  static const bool barrier = getenv("APX_CHOL_BARRIER") != nullptr;  // A/B: one CTA barrier per pivot
+  if (barrier)
+    return launch_pdl(cholinv64_kernel, dim3(1), dim3(256), 0, st, G, l, X, gate, breakdown, skip_out, skip_kappa);
+  constexpr size_t smem = (size_t)64 * 128 * sizeof(double);
+  const cudaError_t attr = cudaFuncSetAttribute(cholinv64f_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+  if (attr != cudaSuccess) return attr;
+  return launch_pdl(cholinv64f_kernel, dim3(1), dim3(256), smem, st, G, l, X, gate, breakdown, skip_out, skip_kappa);
 }
 
 // ---- Q = Y X (X = R^{-1} upper, l <= 64) over 64-row tiles ---------------------------------
