@@ -251,9 +251,22 @@ static int mixed_gemm_splits(int n, int l) {
   return std::max(gemm_splits(n, l, n, 128, 64), gemm_splits(l, n, n, 64, 128));
 }
 
+// row groups of the residual plan's energy pass (APX_EN_GROUPS, tuning knob; 0 = one wave of
+// long-lived CTAs, the default). Short-lived CTAs (128-512 groups, several waves) let the QR's
+// single-CTA Cholesky find an SM sooner (it ends 20 us earlier) but the QR's remaining kernels then
+// overlap the pass's HBM traffic and finish no earlier (measured 1118-1142 vs 1128 products/s).
+static int resid_energy_groups(int n) {
+  static const int env = [] {
+    const char* e = getenv("APX_EN_GROUPS");
+    return e ? atoi(e) : 0;
+  }();
+  return std::min(std::max(env, 0), n);
+}
+
 static void plan_mixed(Workspace& ws, MixedPlan& p, int dtype, int n, int l, int kc) {
   const size_t e = dtype == F32 ? 4 : 8;
-  p.partial = ws.take<double>(cycle_energy_ws(n) / sizeof(double) + 1);
+  p.partial = ws.take<double>(std::max(cycle_energy_ws(n), cycle_energy_ws_groups(n, resid_energy_groups(n))) /
+                                  sizeof(double) + 1);
   p.en_b = ws.take<double>(n);
   p.nr_b = ws.take<double>(n);
   p.lam_b = ws.take<char>((size_t)pad8(kc) * n * e);
@@ -605,25 +618,33 @@ static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int
   APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, hi, y_sms));
   stage_mark(3, hi);
   APX_CUDA(cudaStreamWaitEvent(hi, ss->b_read, 0));  // lo's resets (long done)
-  if (b_after_y) {
+  // APX_B_ORDER=2: B's decomposition waits for the QR instead (its energy pass, one wave of
+  // long-lived CTAs on every SM, otherwise holds the QR's single-CTA Cholesky out of the SMs)
+  if (b_after_y == 1) {
     APX_CUDA(cudaEventRecord(ss->b_read, hi));
     APX_CUDA(cudaStreamWaitEvent(lo, ss->b_read, 0));
   }
   // ---- lo: B's cycle decomposition and the f16 lambda' table -----------------------------------
-  if (fb) {
-    APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, lo, en_cps));
-    APX_CUDA(cudaMemcpyAsync(sb, fb, kc * sizeof(int), cudaMemcpyDeviceToDevice, lo));
-    APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, lo));
-  } else {
-    APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, nullptr, p.partial, lo, en_cps));
-    APX_TRY(launch_topk(p.nr_b, n, kc, sb, lo, p.nr_b, 1.0, scal + APX_S_KEPT_B, p.en_b, scal + APX_S_FRO2_B));
-  }
   float* lb = (float*)p.lam_b;
-  APX_TRY(launch_cycle_extract<float>(B, n, sb, kc, lb, lo, /*aligned=*/true));
-  APX_TRY(zero_pad_rows<float>(lb, kc, n, lo));
-  APX_TRY(launch_lam_f16(lb, kp, n, scal + APX_S_FRO2_B, p.lamh, lo));
-  APX_CUDA(cudaEventRecord(ss->b_ready, lo));
-  stage_mark(1, lo);
+  auto b_stage = [&]() -> int {
+    if (fb) {
+      APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, lo, en_cps,
+                                           resid_energy_groups(n)));
+      APX_CUDA(cudaMemcpyAsync(sb, fb, kc * sizeof(int), cudaMemcpyDeviceToDevice, lo));
+      APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, lo));
+    } else {
+      APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, nullptr, p.partial, lo, en_cps,
+                                           resid_energy_groups(n)));
+      APX_TRY(launch_topk(p.nr_b, n, kc, sb, lo, p.nr_b, 1.0, scal + APX_S_KEPT_B, p.en_b, scal + APX_S_FRO2_B));
+    }
+    APX_TRY(launch_cycle_extract<float>(B, n, sb, kc, lb, lo, /*aligned=*/true));
+    APX_TRY(zero_pad_rows<float>(lb, kc, n, lo));
+    APX_TRY(launch_lam_f16(lb, kp, n, scal + APX_S_FRO2_B, p.lamh, lo));
+    APX_CUDA(cudaEventRecord(ss->b_ready, lo));
+    stage_mark(1, lo);
+    return OK;
+  };
+  if (b_after_y != 2) APX_TRY(b_stage());
   // ---- hi: QR, Bm (+||A||^2), dA in f16 -----------------------------------------------------------
   APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, hi, /*tf32=*/1)));
   for (int it = 0; it < q; ++it) {
@@ -633,6 +654,11 @@ static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int
     APX_TRY((qr_orthonormalize<float, float>(Y, l, 1, n, l, Q, l, 1, Qt, 1, n, p.qr_ws, p.qr_bytes, 0, hi, /*tf32=*/1)));
   }
   stage_mark(4, hi);
+  if (b_after_y == 2) {
+    APX_CUDA(cudaEventRecord(ss->b_read, hi));
+    APX_CUDA(cudaStreamWaitEvent(lo, ss->b_read, 0));
+    APX_TRY(b_stage());
+  }
   {
     // Bm = Q^T A with the A tiles rounded to TF32 (FIX 3): the rounding warps also sum the
     // squares of every A element they touch (each exactly once) -> ||A||^2 partials. Then one

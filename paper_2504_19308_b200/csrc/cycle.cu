@@ -950,6 +950,11 @@ static int energy_groups(int n, int* rows_per_chunk, int ctas_per_sm = 8) {
   return (int)ceil_div(n, *rows_per_chunk);
 }
 
+// workspace of an energy pass with `groups` row groups (launch_cycle_energies' groups_override)
+size_t cycle_energy_ws_groups(int n, int groups) {
+  return (size_t)std::max(groups, 1) * n * sizeof(double) + ceil_div(n, 256) * sizeof(unsigned) + 256;
+}
+
 size_t cycle_energy_ws(int n) {
   int rpc;
   int g = energy_groups(n, &rpc);
@@ -958,9 +963,13 @@ size_t cycle_energy_ws(int n) {
 
 template <typename T>
 int launch_cycle_energies(const T* A, int n, double* energies, double* norms, double* fro2, double* partial,
-                          cudaStream_t st, int ctas_per_sm) {
+                          cudaStream_t st, int ctas_per_sm, int groups_override) {
   int rpc;
-  const int groups = energy_groups(n, &rpc, ctas_per_sm);
+  int groups = energy_groups(n, &rpc, ctas_per_sm);
+  if (groups_override > 0) {  // many short-lived CTAs (several waves), see cycle_energy_ws_groups
+    rpc = (int)ceil_div(n, std::min(groups_override, n));
+    groups = (int)ceil_div(n, rpc);
+  }
   const unsigned cb = (unsigned)ceil_div(n, 256);
   dim3 grid(cb, (unsigned)groups);
   // separate finalize: the fused last-CTA reduce (counters != nullptr) measured 63 us vs 44 + 7
@@ -1291,7 +1300,7 @@ int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st) {
 }
 
 #define APX_INST(T)                                                                                            \
-  template int launch_cycle_energies<T>(const T*, int, double*, double*, double*, double*, cudaStream_t, int);     \
+  template int launch_cycle_energies<T>(const T*, int, double*, double*, double*, double*, cudaStream_t, int, int);     \
   template int launch_cycle_extract<T>(const T*, int, const int*, int, T*, cudaStream_t, bool);                   \
   template int launch_cycle_materialize<T>(const T*, const int*, int, int, T*, cudaStream_t);                 \
   template int launch_cycle_left_gather<T>(const T*, const T*, const int*, int, int, int, T*, cudaStream_t);  \

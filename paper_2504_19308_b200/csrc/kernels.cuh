@@ -6,6 +6,7 @@ namespace apx {
 
 // ---- cycle.cu ----
 size_t cycle_energy_ws(int n);
+size_t cycle_energy_ws_groups(int n, int groups);
 int right_gather_rows(int n, size_t elem, int k);
 // rows per block of a plain right gather (no ticket / ready flags / TF32 operands): the segmented
 // kernel's R at large n, else right_gather_rows
@@ -13,7 +14,7 @@ int right_gather_rows_plain(int n, size_t elem, int k);
 int right_gather_seg_rows(int n, size_t elem, int k);
 template <typename T>
 int launch_cycle_energies(const T* A, int n, double* energies, double* norms, double* fro2, double* partial,
-                          cudaStream_t st, int ctas_per_sm = 8);
+                          cudaStream_t st, int ctas_per_sm = 8, int groups_override = 0);
 // top-k selection (select.cuh); optionally fused: *kept = kept_scale * sum_t kept_w[sel[t]]^2 and
 // *total = sum_i tot_w[i]
 int launch_topk(const double* w, int n, int k, int* sel, cudaStream_t st, const double* kept_w = nullptr,

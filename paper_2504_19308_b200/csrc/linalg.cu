@@ -494,6 +494,7 @@ __global__ void __launch_bounds__(256) cholinv64f_kernel(const double* __restric
   for (int i = 0; i < 8; ++i) md = fmax(md, red[i][0]);
   const double tol = 4.0 * l * 2.220446049250313e-16 * md;
   bool bad = false;
+  double rs_row = 1.0;  // rows l..63 (identity padding) stay unscaled
 #pragma unroll 1
   for (int j = 0; j < l; ++j) {
     double* bl = rows + (size_t)j * 128;
@@ -533,16 +534,17 @@ __global__ void __launch_bounds__(256) cholinv64f_kernel(const double* __restric
           wr[u + 1] = fma(-f, bv.y, wr[u + 1]);
         }
       }
-    } else if (r == j) {
-      const double rsq = fast_rsqrt(p);
-#pragma unroll
-      for (int u = 0; u < 16; ++u) {
-        wl[u] *= rsq;
-        wr[u] *= rsq;
-      }
     }
+    // row j keeps its unscaled values (the published copy is what the later rows need); its
+    // 1 / sqrt(p) scaling is applied once after the loop, off the per-pivot chain
+    if (r == j) rs_row = fast_rsqrt(p);
   }
   __syncthreads();
+#pragma unroll
+  for (int u = 0; u < 16; ++u) {
+    wl[u] *= rs_row;
+    wr[u] *= rs_row;
+  }
   if (bad) {
     if (t == 0) {
       *breakdown = 1;
