@@ -93,9 +93,13 @@ int apx_cycle_first_order(int dtype, const void* A, const void* B, int64_t n, in
  * randomized_partial_svd (svd.py:83-119) with l = k_svd sketch columns, q power iterations and
  * the caller's Gaussian sketch omega (n x l, device, drawn by the host exactly as svd.py:105-106
  * does, from default_rng([seed, 0]) -- svd.py:161); B by its k_cyc dominant cycles.
- * order 1: M = Ahat.B + dA.Bhat, evaluated as Q(Q^T A . dB) + A.Bhat; order 0: M = Ahat.Bhat.
+ * order 1: M = Ahat.B + dA.Bhat. fp32 with k_svd == 64, 1 <= k_cyc <= 128 and n a multiple of
+ * 512 (up to ~13k) runs the residual plan M = Q.(Bm.B) + (A - Q.Bm).Bhat with dA and the kept
+ * diagonals in scaled f16 (FHFMA gather, fp32 accumulation; csrc/mixed_f16.cu); otherwise, or with
+ * flags bit 2, Q(Q^T A . dB) + A.Bhat with the gather over fp32 A. order 0: M = Ahat.Bhat.
  * flags bit 0: fp32 GEMMs as 3xTF32 on mma.sync; bit 1: force the mma.sync GEMMs (default: fp32
- * GEMMs on tcgen05 kind::tf32 when k_svd == 64). APX_S_KEPT_A = sum sigma^2. */
+ * GEMMs on tcgen05 kind::tf32 when k_svd == 64); bit 2: the all-fp32 plan (no f16 residual).
+ * APX_S_KEPT_A = sum sigma^2. */
 size_t apx_mixed_first_order_workspace(int dtype, int64_t n, int k_svd, int k_cyc, int order);
 int apx_mixed_first_order(int dtype, const void* A, const void* B, int64_t n, int k_svd, int k_cyc,
                           int order, int power_iterations, const void* omega,
