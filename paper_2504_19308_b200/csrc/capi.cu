@@ -285,7 +285,7 @@ static void plan_mixed(Workspace& ws, MixedPlan& p, int dtype, int n, int l, int
   p.msq = ws.take<double>((size_t)std::max<int64_t>(std::max<int64_t>(n, kNumSMs * 4), qw_ctas));
   p.asq = ws.take<double>(std::max<int>(n, kNumSMs * 4));
   p.bsq = ws.take<double>(std::max<int>(n, kNumSMs * 4));
-  p.ticket = ws.take<int>(4);
+  p.ticket = ws.take<int>(8);  // [0] gather ticket, [1] persistent Q.W ticket, [2] finalize counter, [3] use_f16
   p.ready = ws.take<int>((size_t)n + 1 + qw_ctas);  // row-block flags, then the deferred-tile list
   if (resid_shape_ok(dtype, n, l, kc)) {
     p.Q2 = ws.take<float>((size_t)n * 2 * l);
@@ -590,7 +590,7 @@ static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int
   // finalize) and `b_ready` (before the gather)
   APX_CUDA(cudaMemsetAsync(scal, 0, APX_NSCALARS * sizeof(double), ss->s));
   APX_CUDA(cudaMemsetAsync(p.ready, 0, (rblocks + 1) * sizeof(int), ss->s));
-  APX_CUDA(cudaMemsetAsync(p.ticket, 0, 4 * sizeof(int), ss->s));
+  APX_CUDA(cudaMemsetAsync(p.ticket, 0, 8 * sizeof(int), ss->s));
   APX_CUDA(cudaEventRecord(ss->b_read, ss->s));
   // The critical path is A's chain (Y -> QR -> Bm -> dA -> gather), so it runs on the
   // high-priority stream; B's decomposition and the W chain fill in on the low-priority one.
@@ -671,12 +671,20 @@ static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int
     APX_TRY(umma_tma_gemm(7 | 8 | 16, 64, A, n, Q, l, part, n, (int64_t)l * n, n, l, n, s, 0, nullptr, 0, 1, hi,
                           p.asq));
     stage_mark(16, hi);
+    // APX_RESID_F16=1 / 0 forces the f16 residual / the fp32 fallback (tests); default: decided on
+    // the device from the residual energy (bm_finalize_kernel)
+    static const int f16_mode = [] {
+      const char* e = getenv("APX_RESID_F16");
+      return e ? (atoi(e) ? 1 : 2) : 0;
+    }();
     APX_TRY(launch_bm_finalize(part, s, l, n, Bm, Q, p.Q2, p.bsq, p.asq, (int)(ceil_div(n, 128) * s),
-                               reinterpret_cast<unsigned*>(p.ticket + 2), scal + APX_S_KEPT_A, scal + APX_S_FRO2_A, hi));
+                               reinterpret_cast<unsigned*>(p.ticket + 2), scal + APX_S_KEPT_A, scal + APX_S_FRO2_A,
+                               p.ticket + 3, f16_mode, hi));
   }
   stage_mark(5, hi);
+  // dA as scaled f16 (or, in the fallback, as fp32 into M, which is free until the gather)
   APX_TRY(umma_tma_gemm(2 | 32, 128, Q, l, Bm, n, const_cast<float*>(A), n, 0, n, n, l, 1, 0, nullptr, 0, 1, hi,
-                        nullptr, nullptr, 0, nullptr, nullptr, p.dAh, scal + APX_S_FRO2_A));
+                        nullptr, nullptr, 0, nullptr, nullptr, p.dAh, scal + APX_S_FRO2_A, p.ticket + 3, M));
   stage_mark(10, hi);
   cudaEvent_t da_ready = ss->join;  // reused: recorded again at the end of lo
   APX_CUDA(cudaEventRecord(da_ready, hi));
@@ -684,7 +692,13 @@ static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int
   APX_CUDA(cudaStreamWaitEvent(hi, ss->b_ready, 0));
   stage_mark(11, hi);
   APX_TRY(launch_gather_f16(p.dAh, p.lamh, sb, kc, kp, n, n, M, scal + APX_S_FRO2_A, scal + APX_S_FRO2_B, p.ticket,
-                            p.ready, gctas, hi));
+                            p.ready, gctas, hi, nullptr, p.ticket + 3));
+  // fallback (dA too large a part of M for f16): the fp32 gather over dA, in place in M (each
+  // persistent CTA stages its whole row block before writing those rows), then all row flags;
+  // both launches return at once when the f16 gather ran
+  APX_TRY(launch_cycle_right_gather<float>(M, nullptr, 0, lb, sb, kc, n, n, 0, M, nullptr, nullptr, hi, true, gctas,
+                                           p.ticket, 1, false, nullptr, false, 0, p.ticket + 3));
+  APX_TRY(launch_fallback_flags(p.ticket + 3, p.ready, rblocks, hi));
   stage_mark(2, hi);
   APX_CUDA(cudaEventRecord(ss->hi_done, hi));
   // ---- lo: W = Bm . B at fp32 accuracy, then M += [Q|Q].[W_hi; W_lo] behind the gather's frontier --

@@ -332,7 +332,9 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
                                                           int n, int m_rows, int accumulate, T* __restrict__ M,
                                                           double* __restrict__ msq_partial,
                                                           double* __restrict__ xsq_partial, int* __restrict__ ticket,
-                                                          int* __restrict__ ready, int x_early, int row_off) {
+                                                          int* __restrict__ ready, int x_early, int row_off,
+                                                          const int* __restrict__ skip_if) {
+  if (skip_if != nullptr && *skip_if != 0) return;  // a gated-off launch (the C4 residual plan's fallback)
   constexpr int RP = gather_pitch(R, sizeof(T));
   // x_early: X (and the ticket / ready flags) predate the previous kernel of the stream, so under
   // a programmatic dependent launch the first row block is staged before waiting for that
@@ -1132,7 +1134,7 @@ template <typename T, int R>
 static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int m_rows,
                           int acc, T* M, double* msq_partial, double* xsq_partial, bool lam_padded, int max_ctas,
                           int* ticket, int col_chunks, bool trunc, int* ready, bool x_early, int row_off,
-                          cudaStream_t st) {
+                          cudaStream_t st, const int* skip_if = nullptr) {
   constexpr int U = APX_GATHER_U, CPT = APX_GATHER_CPT;
   const int kp = (int)ceil_div(std::max(k, 1), U) * U;
   const size_t smem = (size_t)gather_pitch(R, sizeof(T)) * n * sizeof(T) + (size_t)kp * sizeof(int);
@@ -1157,10 +1159,10 @@ static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const
     APX_TRY(set_smem<T>((const void*)kern, smem));
     if (x_early) {
       APX_CUDA(launch_pdl(kern, grid, dim3(threads), smem, st, X, JA, ka, lam, J, k, n, m_rows, acc, M, msq_partial,
-                          xsq_partial, ticket, ready, 1, row_off));
+                          xsq_partial, ticket, ready, 1, row_off, skip_if));
     } else {
       kern<<<grid, threads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M, msq_partial, xsq_partial, ticket,
-                                        ready, 0, row_off);
+                                        ready, 0, row_off, skip_if);
     }
     APX_LAUNCH_CHECK();
     return OK;
@@ -1232,7 +1234,7 @@ template <typename T>
 int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n,
                               int m_rows, int accumulate, T* M, double* msq_partial, double* xsq_partial,
                               cudaStream_t st, bool lam_padded, int max_ctas, int* ticket, int col_chunks,
-                              bool tf32_operands, int* ready, bool x_early, int row_off) {
+                              bool tf32_operands, int* ready, bool x_early, int row_off, const int* skip_if) {
   const int rs = right_gather_seg_rows(n, sizeof(T), k);
   if (rs > 0 && !(max_ctas > 0 && ticket) && ready == nullptr && !(tf32_operands && sizeof(T) == 4)) {
     switch (rs) {
@@ -1251,7 +1253,7 @@ int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, c
               "n=%d too large for the right gather row block", n);
 #define APX_RG(RV) \
   return right_gather_r<T, RV>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, xsq_partial, lam_padded, \
-                               max_ctas, ticket, col_chunks, tf32_operands, ready, x_early, row_off, st)
+                               max_ctas, ticket, col_chunks, tf32_operands, ready, x_early, row_off, st, skip_if)
   switch (r) {
     case 1: APX_RG(1);
     case 2: APX_RG(2);
@@ -1305,7 +1307,7 @@ int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st) {
   template int launch_cycle_materialize<T>(const T*, const int*, int, int, T*, cudaStream_t);                 \
   template int launch_cycle_left_gather<T>(const T*, const T*, const int*, int, int, int, T*, cudaStream_t);  \
   template int launch_cycle_right_gather<T>(const T*, const int*, int, const T*, const int*, int, int, int, int, T*, \
-                                            double*, double*, cudaStream_t, bool, int, int*, int, bool, int*, bool, int); \
+                                            double*, double*, cudaStream_t, bool, int, int*, int, bool, int*, bool, int, const int*); \
   template int launch_sumsq<T>(const T*, size_t, double*, int*, cudaStream_t);                               \
   template int launch_cycle_energies_rows<T>(const T*, int, int, int, double*, double*, cudaStream_t);       \
   template int launch_cycle_extract_rows<T>(const T*, int, int, int, const int*, int, T*, cudaStream_t);      \

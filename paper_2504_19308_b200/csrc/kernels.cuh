@@ -33,7 +33,7 @@ int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, c
                               int accumulate, T* M, double* msq_partial, double* xsq_partial, cudaStream_t st,
                               bool lam_padded = false, int max_ctas = 0, int* ticket = nullptr, int col_chunks = 1,
                               bool tf32_operands = false, int* ready = nullptr, bool x_early = false,
-                              int row_off = 0);
+                              int row_off = 0, const int* skip_if = nullptr);
 // ---- row-sharded cycle product (local rows [0, m) of an n x n operand = global rows row_off + r)
 template <typename T>
 int launch_cycle_energies_rows(const T* A, int m, int row_off, int n, double* energies, double* partial,
@@ -81,7 +81,8 @@ int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* 
                   int64_t ldc, int64_t c_split_stride, int M, int N, int K, int splits, int accumulate,
                   const int* mJ, int mk, int mod_n, cudaStream_t st, double* sq_partial = nullptr,
                   const int* ready = nullptr, int ready_rows = 0, const int* progress = nullptr,
-                  int* defer = nullptr, uint16_t* hout = nullptr, const double* hscale = nullptr);
+                  int* defer = nullptr, uint16_t* hout = nullptr, const double* hscale = nullptr,
+                  const int* f16_flag = nullptr, float* out32 = nullptr);
 int umma_persist_gemm(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int M, int N,
                       int K, int accumulate, cudaStream_t st, double* sq_partial = nullptr, const int* ready = nullptr,
                       int ready_rows = 0, const int* progress = nullptr, int* defer = nullptr, int ctas = 0,
@@ -98,13 +99,14 @@ int launch_dup_cols(const float* Q, int rows, int l, float* Q2, cudaStream_t st)
 int launch_round_tf32(float* X, size_t count, cudaStream_t st);
 int launch_bm_finalize(const float* part, int splits, int l, int n, float* Bm, const float* Q, float* Q2,
                        double* bsq_part, const double* asq_part, int asq_parts, unsigned* counter, double* kept_out,
-                       double* fro2_out, cudaStream_t st);
+                       double* fro2_out, int* use_f16, int f16_mode, cudaStream_t st);
+int launch_fallback_flags(const int* use_f16, int* ready, int blocks, cudaStream_t st);
 int gather_f16_threads(int n);
 size_t gather_f16_smem(int n, int kp);
 int launch_lam_f16(const float* lam, int kp, int n, const double* fro2_b, uint16_t* out, cudaStream_t st);
 int launch_gather_f16(const uint16_t* Xh, const uint16_t* lamh, const int* J, int k, int kp, int n, int m_rows, float* M,
                       const double* fro2_a, const double* fro2_b, int* ticket, int* ready, int ctas, cudaStream_t st,
-                      double* msq_partial = nullptr);
+                      double* msq_partial = nullptr, const int* gate = nullptr);
 int umma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
               int64_t c_split_stride, int M, int N, int K, int splits, int accumulate, const int* mJ, int mk,
               int mod_n, cudaStream_t st);

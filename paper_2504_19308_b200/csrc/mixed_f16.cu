@@ -63,11 +63,13 @@ __global__ void round_tf32_kernel(float* __restrict__ X, size_t count) {
 // counter, reset for the next product) sums them and the ||A||^2 partials of the GEMM in a fixed
 // order into kept_out and fro2_out.
 constexpr int kFinThreads = 256;
+constexpr double kResidF16MaxEnergy = 0.01;  // residual energy fraction up to which dA goes f16
 __global__ void __launch_bounds__(kFinThreads)
     bm_finalize_kernel(const float* __restrict__ part, int splits, int l, int n, float* __restrict__ Bm,
                        const float* __restrict__ Q, float* __restrict__ Q2, double* __restrict__ bsq_part,
                        const double* __restrict__ asq_part, int asq_parts, unsigned* __restrict__ counter,
-                       double* __restrict__ kept_out, double* __restrict__ fro2_out) {
+                       double* __restrict__ kept_out, double* __restrict__ fro2_out, int* __restrict__ use_f16,
+                       int f16_mode) {
   pdl_wait();
   __shared__ double red[32];
   __shared__ bool last;
@@ -103,6 +105,12 @@ __global__ void __launch_bounds__(kFinThreads)
     *kept_out = k;
     *fro2_out = a;
     *counter = 0u;
+    // the f16 residual is accurate enough only while dA stays a small part of the product: with
+    // f16 rounding (2^-11) on a term carrying a fraction f of ||M|| the error is ~4e-4 f, so the
+    // plan keeps it for a residual energy ||A||^2 - ||Bm||^2 <= 1% of ||A||^2 (f ~ 0.1) and falls
+    // back to the fp32 gather over dA otherwise (f16_mode 1 / 2 force either, for tests)
+    if (use_f16 != nullptr)
+      *use_f16 = f16_mode == 1 ? 1 : f16_mode == 2 ? 0 : ((a - k) <= kResidF16MaxEnergy * a ? 1 : 0);
   }
 }
 
@@ -183,7 +191,9 @@ __global__ void __launch_bounds__(NT, 1)
     cycle_gather_f16_kernel(const uint4* __restrict__ Xh, const uint32_t* __restrict__ lamh,
                             const int* __restrict__ J, int k, int kp, int n, int m_rows, float* __restrict__ M,
                             const double* __restrict__ fro2_a, const double* __restrict__ fro2_b,
-                            int* __restrict__ ticket, int* __restrict__ ready, double* __restrict__ msq_partial) {
+                            int* __restrict__ ticket, int* __restrict__ ready, double* __restrict__ msq_partial,
+                            const int* __restrict__ gate) {
+  if (gate != nullptr && *gate == 0) return;  // the plan fell back to the fp32 gather (bm_finalize)
   constexpr int LW = CPT / 2;  // lambda' words per thread per shift
   extern __shared__ __align__(16) unsigned char smem_raw[];
   uint4* Xs = reinterpret_cast<uint4*>(smem_raw);
@@ -360,10 +370,23 @@ int launch_split_tf32(const float* X, size_t count, float* X2, cudaStream_t st) 
 
 int launch_bm_finalize(const float* part, int splits, int l, int n, float* Bm, const float* Q, float* Q2,
                        double* bsq_part, const double* asq_part, int asq_parts, unsigned* counter, double* kept_out,
-                       double* fro2_out, cudaStream_t st) {
+                       double* fro2_out, int* use_f16, int f16_mode, cudaStream_t st) {
   const unsigned blocks = (unsigned)std::min<size_t>(ceil_div((size_t)l * n, (size_t)kFinThreads), (size_t)kNumSMs * 4);
   APX_CUDA(launch_pdl(bm_finalize_kernel, dim3(blocks), dim3(kFinThreads), 0, st, part, splits, l, n, Bm, Q, Q2,
-                      bsq_part, asq_part, asq_parts, counter, kept_out, fro2_out));
+                      bsq_part, asq_part, asq_parts, counter, kept_out, fro2_out, use_f16, f16_mode));
+  APX_LAUNCH_CHECK();
+  return OK;
+}
+
+// fallback of the residual plan: once the fp32 gather (which publishes no flags) is done, mark every
+// row block ready for M += Q.W; a no-op when the f16 gather ran (it published them itself)
+__global__ void fallback_flags_kernel(const int* __restrict__ use_f16, int* __restrict__ ready, int blocks) {
+  if (*use_f16 != 0) return;
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < blocks; i += gridDim.x * blockDim.x) ready[i] = 1;
+}
+
+int launch_fallback_flags(const int* use_f16, int* ready, int blocks, cudaStream_t st) {
+  fallback_flags_kernel<<<(unsigned)std::min(64, (int)ceil_div(blocks, 256)), 256, 0, st>>>(use_f16, ready, blocks);
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -399,7 +422,7 @@ int launch_lam_f16(const float* lam, int kp, int n, const double* fro2_b, uint16
 
 int launch_gather_f16(const uint16_t* Xh, const uint16_t* lamh, const int* J, int k, int kp, int n, int m_rows, float* M,
                       const double* fro2_a, const double* fro2_b, int* ticket, int* ready, int ctas, cudaStream_t st,
-                      double* msq_partial) {
+                      double* msq_partial, const int* gate) {
   const F16Cfg c = f16_cfg(n);
   APX_REQUIRE(c.nt > 0, "f16 gather: n=%d must be a multiple of 512", n);
   APX_REQUIRE(kp % (2 * kHU) == 0 && kp > 0, "f16 gather: shift count %d must be a positive multiple of 8", kp);
@@ -412,7 +435,7 @@ int launch_gather_f16(const uint16_t* Xh, const uint16_t* lamh, const int* J, in
     APX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     APX_CUDA(launch_pdl(kern, dim3(grid), dim3(c.nt), smem, st, reinterpret_cast<const uint4*>(Xh),
                         reinterpret_cast<const uint32_t*>(lamh), J, k, kp, n, m_rows, M, fro2_a, fro2_b, ticket, ready,
-                        msq_partial));
+                        msq_partial, gate));
     APX_LAUNCH_CHECK();
     return OK;
   };

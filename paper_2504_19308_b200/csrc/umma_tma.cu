@@ -117,7 +117,8 @@ __global__ void __launch_bounds__(kThreads, 1)
                     int k_per_split, int accumulate, const int* __restrict__ mJ, int mk, int mod_n,
                     double* __restrict__ sq_partial, int c_async, const int* __restrict__ ready, int ready_rows,
                     const int* __restrict__ progress, int* __restrict__ defer, unsigned long long stall_ns,
-                    uint16_t* __restrict__ hout, const double* __restrict__ hscale) {
+                    uint16_t* __restrict__ hout, const double* __restrict__ hscale,
+                    const int* __restrict__ f16_flag, float* __restrict__ out32) {
   using CF = Cfg<BN, STAGES>;
   // FIX 3: FIX 2 plus the sum of squares of the A operand (before rounding) into sq_partial.
   // FIX 4: residual epilogue -- C is an fp32 INPUT X; the CTA writes f16(2^(15-e) (X - acc)) to
@@ -327,7 +328,9 @@ __global__ void __launch_bounds__(kThreads, 1)
       }
       asm volatile("cp.async.commit_group;\ncp.async.wait_group 0;" ::: "memory");
       __syncwarp();
-      const float sc = ldexpf(1.f, 15 - f16_scale_exp(*hscale));
+      // f16_flag == 0 (the residual plan's fallback): X - acc in fp32, row-major into out32
+      const bool to_f16 = f16_flag == nullptr || *f16_flag != 0;
+      const float sc = to_f16 ? ldexpf(1.f, 15 - f16_scale_exp(*hscale)) : 1.f;
 #pragma unroll 1
       for (int j0 = 0; j0 < BN; j0 += 32) {
         float v[32];
@@ -350,8 +353,20 @@ __global__ void __launch_bounds__(kThreads, 1)
         }
       }
       __syncwarp();
+      if (!to_f16) {
+#pragma unroll 4
+        for (int r = 0; r < 32; ++r) {
+          const int rg = rbase + r;
+          if (rg >= M) break;
+#pragma unroll
+          for (int j0 = 0; j0 < BN; j0 += 32) {
+            const int c = j0 + lane;
+            if (n0 + c < N) out32[(size_t)rg * N + n0 + c] = creg[r * BN + ((((c >> 2) ^ (r & 7))) << 2) + (c & 3)];
+          }
+        }
+      }
 #pragma unroll 1
-      for (int g8 = 0; g8 < 4; ++g8) {
+      for (int g8 = 0; g8 < 4 && to_f16; ++g8) {
         const int r8 = rbase + 8 * g8;
         if (r8 >= M) break;
         uint4* dst = reinterpret_cast<uint4*>(hout) + (size_t)(r8 >> 3) * N + n0;
@@ -621,7 +636,8 @@ template <int BN, int STAGES, bool A_MN, bool B_MN, bool TRANS_OUT, int FIX>
 static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc,
                   int64_t c_split_stride, int M, int N, int K, int splits, int accumulate, const int* mJ, int mk,
                   int mod_n, double* sq_partial, const int* ready, int ready_rows, const int* progress,
-                  int* defer, uint16_t* hout, const double* hscale, cudaStream_t st) {
+                  int* defer, uint16_t* hout, const double* hscale, const int* f16_flag, float* out32,
+                  cudaStream_t st) {
   using CF = Cfg<BN, STAGES>;
   CUtensorMap ta, tb;
   // A operand: K-major stored [M][K]; MN-major stored [K][M]
@@ -634,7 +650,7 @@ static int launch(const float* A, int64_t lda, const float* B, int64_t ldb, floa
   const int c_async = ((uintptr_t)C % 16) == 0 && (ldc % 4) == 0 && (N % 4) == 0 && (c_split_stride % 4) == 0;
   APX_CUDA(launch_pdl(fn, grid, dim3(kThreads), CF::kSmem, st, ta, tb, C, ldc, c_split_stride, M, N, K, kps,
                       accumulate, mJ, mk, mod_n, sq_partial, c_async, ready, ready_rows, progress, defer, stall_ns(),
-                      hout, hscale));
+                      hout, hscale, f16_flag, out32));
   APX_LAUNCH_CHECK();
   return OK;
 }
@@ -1011,7 +1027,8 @@ int launch_qw_fixup_sum(const float* Q, int64_t ldq, const float* W, int64_t ldw
 int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* B, int64_t ldb, float* C,
                   int64_t ldc, int64_t c_split_stride, int M, int N, int K, int splits, int accumulate,
                   const int* mJ, int mk, int mod_n, cudaStream_t st, double* sq_partial, const int* ready,
-                  int ready_rows, const int* progress, int* defer, uint16_t* hout, const double* hscale) {
+                  int ready_rows, const int* progress, int* defer, uint16_t* hout, const double* hscale,
+                  const int* f16_flag, float* out32) {
   APX_REQUIRE(ready == nullptr || (accumulate && ready_rows > 0 && splits == 1 && !(layout & 4)),
               "umma_tma_gemm: ready flags need an accumulating, split-free, row-major C");
   APX_REQUIRE(defer == nullptr || (ready != nullptr && progress != nullptr && sq_partial != nullptr),
@@ -1036,7 +1053,8 @@ int umma_tma_gemm(int layout, int bn, const float* A, int64_t lda, const float* 
                                                                               c_split_stride, M, N, K, splits, \
                                                                               accumulate, mJ, mk, mod_n,       \
                                                                               sq_partial, ready, ready_rows,   \
-                                                                              progress, defer, hout, hscale, st);
+                                                                              progress, defer, hout, hscale,   \
+                                                                              f16_flag, out32, st);
   APX_TL(64, 4, 0, 0) APX_TL(64, 4, 1, 0) APX_TL(64, 4, 2, 0) APX_TL(64, 4, 3, 0)
   APX_TL(64, 4, 4, 0) APX_TL(64, 4, 5, 0) APX_TL(64, 4, 6, 0) APX_TL(64, 4, 7, 0)
   APX_TL(64, 4, 1, 1) APX_TL(64, 4, 5, 1) APX_TL(64, 4, 7, 2) APX_TL(64, 4, 7, 3) APX_TL(128, 2, 2, 4)

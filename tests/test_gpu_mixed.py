@@ -133,3 +133,50 @@ def test_mixed_pipeline_matches_single_calls(P):
         assert torch.equal(M, M1.cpu())
         assert rep.selected_b == rep1.selected_b
         assert rep.norm_da == rep1.norm_da and rep.norm_db == rep1.norm_db
+
+
+def test_mixed_resid_plan_falls_back_on_flat_spectrum(P):
+    """A with a flat spectrum (Gaussian): the rank-64 approximation leaves most of A in dA, so the
+    f16 residual would carry the product at f16 precision (~4e-4). bm_finalize sees the residual
+    energy on the device and the plan runs the fp32 gather over dA instead: parity stays < 1e-4."""
+    n, k = 1024, 64
+    rng = np.random.default_rng(17)
+    A = (rng.standard_normal((n, n)) / np.sqrt(n)).astype(np.float32)
+    B = O.gen_cycle_operand(n, k, 18).astype(np.float32)
+    Ad, Bd = torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda()
+    M, rep = P.mixed_first_order_multiply(Ad, Bd, 64, k, 1, seed=3)
+    Mo, ro = O.mixed_first_order_multiply(A.astype(np.float64), B.astype(np.float64), 64, k, 1, 3)
+    assert rep.selected_b == ro["selected_b"]
+    err = rel(M.cpu().numpy(), Mo)
+    print(f"flat spectrum, residual plan with fp32 fallback: {err:.3e}")
+    assert err < 1e-4
+
+
+FORCE_SCRIPT = r"""
+import sys, numpy as np, torch
+sys.path.insert(0, %r)
+import oracle as O
+import paper_2504_19308_b200 as P
+n = 1024
+A = O.gen_haar_spectrum(n, (np.arange(n) + 1.0) ** -1.5, 8).astype(np.float32)
+B = O.gen_cycle_operand(n, 64, 9).astype(np.float32)
+M, rep = P.mixed_first_order_multiply(torch.from_numpy(A).cuda(), torch.from_numpy(B).cuda(), 64, 64, 1, seed=4)
+Mo, _ = O.mixed_first_order_multiply(A.astype(np.float64), B.astype(np.float64), 64, 64, 1, 4)
+print(float(np.linalg.norm(M.cpu().numpy() - Mo) / np.linalg.norm(Mo)))
+"""
+
+
+@pytest.mark.parametrize("mode", ["0", "1"])
+def test_mixed_resid_plan_forced_modes(mode):
+    """APX_RESID_F16=0 forces the fp32 fallback (dA in fp32 into M, in-place fp32 gather, flags set
+    after it), =1 the f16 gather: both within tolerance on the C4-structured input."""
+    import os
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    r = subprocess.run([sys.executable, "-c", FORCE_SCRIPT % root], capture_output=True, text=True, timeout=600,
+                       env=dict(os.environ, APX_RESID_F16=mode))
+    assert r.returncode == 0, r.stderr[-2000:]
+    err = float(r.stdout.strip().splitlines()[-1])
+    print(f"APX_RESID_F16={mode}: {err:.3e}")
+    assert err < 1e-4
