@@ -1120,7 +1120,15 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
   } else if (!householder_only && l <= 64) {
     // fast path: CholeskyQR with R^{-1}; second pass only when the conditioning requires it
     int* skip2 = flag + 1;
-    const double skip_kappa = sizeof(TO) == 4 ? 3.0e4 : 0.0;
+    // one fp64 CholeskyQR pass leaves ||Q^T Q - I|| <~ u64 kappa^2: fp32 outputs tolerate kappa_F up
+    // to 3e4 (TF32-level orthogonality); fp64 outputs always take the second pass
+    // (APX_QR_KAPPA64 = a kappa_F threshold for fp64, tuning knob: at 100-300 the C1 sketches,
+    // kappa_F above that, still took both passes -- 1.31 ms either way)
+    static const double k64 = [] {
+      const char* e = getenv("APX_QR_KAPPA64");
+      return e ? atof(e) : 0.0;
+    }();
+    const double skip_kappa = sizeof(TO) == 4 ? 3.0e4 : k64;
     const int tiles = (int)ceil_div(m, 64);
     APX_TRY(launch_gram<TI>(Y, rs, cs, m, l, flag, part, G, st));
     stage_mark(12, st);  // fine-grained trace markers (bench.py C4 timeline); no-ops unless armed
