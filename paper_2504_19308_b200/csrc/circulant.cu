@@ -1398,6 +1398,14 @@ __global__ void __launch_bounds__(256, 2) big_dA_win_kernel(const T* __restrict_
     else tw_hi[q][j - 16] = cconj(__ldg(roots + mulmod_n(t, (16 * (j - 16)) % n, n)));
   }
   const int r0 = row_base + blockIdx.y * ROWS;
+  // the epilogue reads this CTA's ROWS x 256 tile of A (DRAM-resident): pull it into L2 now, one bulk
+  // prefetch per row, so the final loads (the kernel's largest stall) hit L2
+  if (tid < ROWS && r0 + tid < row_end && c0 < n) {
+    const T* rowp = A + (size_t)(r0 + tid) * n + c0;
+    const unsigned bytes = (unsigned)(min(256, n - c0) * sizeof(T)) & ~15u;
+    if (((uintptr_t)rowp & 15) == 0 && bytes > 0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rowp), "r"(bytes) : "memory");
+  }
   // window j of term q holds S_q[(r0 - c0 - 255 + j) mod n]; thread tid, row rr reads j = 255 - tid + rr
   int dbase = (r0 - c0 - 255) % n;
   if (dbase < 0) dbase += n;
