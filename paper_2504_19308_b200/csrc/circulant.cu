@@ -678,10 +678,28 @@ __global__ void __launch_bounds__(512) circ_left2_r16_kernel(const double* __res
 #pragma unroll
   for (int m = 0; m < 16; ++m) v[m] = xb[t + 256 * m];
   fft4096_r16<true>(v, xb, roots, t, 1 + half);
-  const int col = c0 + half;
-  if (col < col_end) {
+  // the two columns leave through shared memory as (row, col pair) = 32 contiguous bytes, one
+  // st.global.v4.f64 per row (a 16-byte store per column and row -- 32 scattered sectors per warp
+  // instruction -- held the kernel in LSU throttle and store drain)
+  __syncthreads();  // both halves' transforms done with buf0 / buf1
+  double2* o = buf0;  // [n][2] across buf0 and buf1 (contiguous, 2 * kFFT16Buf >= 2n)
 #pragma unroll
-    for (int m = 0; m < 16; ++m) M[(size_t)(t + 256 * m) * ldm + (col - col_base)] = v[m];
+  for (int m = 0; m < 16; ++m) o[2 * (t + 256 * m) + half] = v[m];
+  __syncthreads();
+  const bool two = c0 + 1 < col_end;
+  const bool pair_st = two && ((ldm | (c0 - col_base)) & 1) == 0 && ((uintptr_t)M & 31) == 0;
+#pragma unroll
+  for (int i = 0; i < kPP; ++i) {
+    const int p = tid + 512 * i;
+    const double2 a = o[2 * p], b = o[2 * p + 1];
+    double2* dst = M + (size_t)p * ldm + (c0 - col_base);
+    if (pair_st) {
+      asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst), "d"(a.x), "d"(a.y), "d"(b.x), "d"(b.y)
+                   : "memory");
+    } else {
+      dst[0] = a;
+      if (two) dst[1] = b;
+    }
   }
 }
 
