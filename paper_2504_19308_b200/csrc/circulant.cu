@@ -1261,6 +1261,102 @@ __global__ void __launch_bounds__(kBigThreads, 2) fft4_pass2_kernel(const double
   }
 }
 
+// Register-resident four-step passes for the lengths n1, n2 in {128, 256} (C5c: n = 32768 =
+// 128 x 256, the n = 16384 / 65536 transforms, Bluestein lengths up to 2^16). A length
+// N = R * 16 (R = 8 or 16) transform of each of the CTA's 16 sequences runs as
+//   i = j + 16 m (j < 16, m < R),  k = ka + R kb:
+//   A: thread (seq, j): DFT_R over m of x[j + 16 m] -> ka, times w_N^{j ka}, E[seq][ka][j]
+//   B: thread (seq, ka): DFT16 over j of E[seq][ka][j] -> kb: X[ka + R kb]
+// with E at seq * (16 R + 1) + ka * 16 + j (pitch = 1 mod 8 complex: every warp access hits each
+// 16-byte bank group four times, the minimum). One shared exchange per pass against log2 N
+// rounds of fft_multi's radix-2 tile passes; the global loads and stores keep the 256-byte runs of
+// the generic kernels. 256 threads; phase B uses the first 16 R.
+template <int R, bool INV>
+__device__ __forceinline__ void dft_r(double2 (&v)[R]) {
+  if constexpr (R == 8) dft8<INV>(v);
+  else dft16<INV>(v);
+}
+
+template <typename TI, int R, bool INV>
+__global__ void __launch_bounds__(256, 2) fft4_pass1_r16_kernel(const TI* in, int n2, const double2* __restrict__ roots_n,
+                                                                const double2* __restrict__ roots_n1, double2* data) {
+  constexpr int N1 = 16 * R, P = N1 + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* E = reinterpret_cast<double2*>(smem_raw);  // 16 P complex
+  const size_t n = (size_t)N1 * n2;
+  const size_t row = blockIdx.y;
+  const int i20 = blockIdx.x * 16;
+  const int t = threadIdx.x;
+  {
+    const int c = t & 15, j = t >> 4;
+    const TI* src = in + row * n + i20 + c;
+    double2 v[R];
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[m] = ld_c<TI>(src, (size_t)(j + 16 * m) * n2);
+    dft_r<R, INV>(v);
+    twiddle_powers<INV, R>(v, roots_n1, j);  // w_N1^{j ka}
+#pragma unroll
+    for (int ka = 0; ka < R; ++ka) E[c * P + ka * 16 + j] = v[ka];
+  }
+  __syncthreads();  // every load of the tile is done before any store (in-place when TI is complex)
+  if (t < 16 * R) {
+    const int c = t & 15, ka = t >> 4;
+    double2 v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = E[c * P + ka * 16 + j];
+    dft16<INV>(v);
+    // X[k1] for k1 = ka + R kb, times w_n^{i2 k1}: the first from the table, then steps w_n^{i2 R}
+    const size_t i2 = (size_t)(i20 + c);
+    double2 w = __ldg(roots_n + ((i2 * ka) & (n - 1)));
+    double2 stp = __ldg(roots_n + ((i2 * R) & (n - 1)));
+    if (INV) {
+      w.y = -w.y;
+      stp.y = -stp.y;
+    }
+    double2* dst = data + row * n + i2;
+#pragma unroll
+    for (int kb = 0; kb < 16; ++kb) {
+      dst[(size_t)(ka + R * kb) * n2] = cmul(v[kb], w);
+      w = cmul(w, stp);
+    }
+  }
+}
+
+template <int R, bool INV>
+__global__ void __launch_bounds__(256, 2) fft4_pass2_r16_kernel(const double2* __restrict__ data, int n1,
+                                                                const double2* __restrict__ roots_n2, double scale,
+                                                                double2* __restrict__ out) {
+  constexpr int N2 = 16 * R, P = N2 + 1;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  double2* E = reinterpret_cast<double2*>(smem_raw);  // 16 P complex
+  const size_t n = (size_t)n1 * N2;
+  const size_t row = blockIdx.y;
+  const int k10 = blockIdx.x * 16;
+  const int t = threadIdx.x;
+  {
+    const int s = t >> 4, j = t & 15;
+    const double2* src = data + row * n + (size_t)(k10 + s) * N2 + j;
+    double2 v[R];
+#pragma unroll
+    for (int m = 0; m < R; ++m) v[m] = __ldg(src + 16 * m);
+    dft_r<R, INV>(v);
+    twiddle_powers<INV, R>(v, roots_n2, j);  // w_N2^{j ka}
+#pragma unroll
+    for (int ka = 0; ka < R; ++ka) E[s * P + ka * 16 + j] = v[ka];
+  }
+  __syncthreads();
+  if (t < 16 * R) {
+    const int s = t & 15, ka = t >> 4;
+    double2 v[16];
+#pragma unroll
+    for (int j = 0; j < 16; ++j) v[j] = E[s * P + ka * 16 + j];
+    dft16<INV>(v);
+    double2* dst = out + row * n + k10 + s;
+#pragma unroll
+    for (int kb = 0; kb < 16; ++kb) dst[(size_t)n1 * (ka + R * kb)] = cscale(v[kb], scale);
+  }
+}
+
 // big-path helpers (all grid-stride over n x n, or tiled where a transpose is involved)
 // out[c][p] = in[p][c] (real or complex in, complex out), 32 x 32 tiles
 template <typename TI>
@@ -1807,9 +1903,55 @@ __global__ void chirp_post_kernel(const double2* __restrict__ c, int n, int L, i
 }
 
 // the four-step transform of `rows` power-of-two sequences of length f.L
+static bool r16_len(int len) { return len == 128 || len == 256; }
+static bool big_r16_enabled() {
+  static const bool on = [] {
+    const char* e = getenv("APX_BIG_R16");
+    return !(e && e[0] == '0');
+  }();
+  return on;
+}
+
+template <typename K>
+static size_t r16_smem(K kern, int len) {
+  const size_t bytes = (size_t)16 * (len + 1) * sizeof(double2);
+  cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)bytes);
+  return bytes;
+}
+
+template <typename TI, bool INV>
+static void four_step_r16_launch(const BigFFT& f, const TI* in, double2* data, double2* out, int rr, double scale,
+                                 cudaStream_t st) {
+  const dim3 g1((unsigned)(f.n2 / 16), (unsigned)rr), g2((unsigned)(f.n1 / 16), (unsigned)rr);
+  if (f.n1 == 128) {
+    auto k = fft4_pass1_r16_kernel<TI, 8, INV>;
+    k<<<g1, 256, r16_smem(k, 128), st>>>(in, f.n2, f.roots, f.roots1, data);
+  } else {
+    auto k = fft4_pass1_r16_kernel<TI, 16, INV>;
+    k<<<g1, 256, r16_smem(k, 256), st>>>(in, f.n2, f.roots, f.roots1, data);
+  }
+  if (f.n2 == 128) {
+    auto k = fft4_pass2_r16_kernel<8, INV>;
+    k<<<g2, 256, r16_smem(k, 128), st>>>(data, f.n1, f.roots2, scale, out);
+  } else {
+    auto k = fft4_pass2_r16_kernel<16, INV>;
+    k<<<g2, 256, r16_smem(k, 256), st>>>(data, f.n1, f.roots2, scale, out);
+  }
+}
+
 template <typename TI>
 static int four_step_rows(const BigFFT& f, const TI* in, double2* data, double2* out, int rows, bool inverse,
                           double scale, cudaStream_t st) {
+  if (r16_len(f.n1) && r16_len(f.n2) && big_r16_enabled()) {
+    const size_t L = (size_t)f.L;
+    for (int r0 = 0; r0 < rows; r0 += 65535) {
+      const int rr = std::min(65535, rows - r0);
+      if (inverse) four_step_r16_launch<TI, true>(f, in + r0 * L, data + r0 * L, out + r0 * L, rr, scale, st);
+      else four_step_r16_launch<TI, false>(f, in + r0 * L, data + r0 * L, out + r0 * L, rr, scale, st);
+      APX_LAUNCH_CHECK();
+    }
+    return OK;
+  }
   const size_t s1 = (size_t)kBigTile * (f.n1 + 1) * sizeof(double2), s2 = (size_t)kBigTile * (f.n2 + 1) * sizeof(double2);
   APX_CUDA(cudaFuncSetAttribute(fft4_pass1_kernel<TI>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s1));
   APX_CUDA(cudaFuncSetAttribute(fft4_pass2_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)s2));

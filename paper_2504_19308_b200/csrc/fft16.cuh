@@ -76,16 +76,38 @@ __device__ __forceinline__ void dft16(double2 (&v)[16]) {
     for (int k2 = 0; k2 < 4; ++k2) v[k1 + 4 * k2] = t[4 * k1 + k2];
 }
 
-// v[i] *= w^i, i = 0..15, w = roots[idx] (conjugated for INV)
+// 8-point DFT in place, natural order in and out (even/odd split into two 4-point DFTs)
 template <bool INV>
-__device__ __forceinline__ void twiddle_powers(double2 (&v)[16], const double2* __restrict__ roots, int idx) {
+__device__ __forceinline__ void dft8(double2 (&v)[8]) {
+  constexpr double r2 = 0.70710678118654752440;
+  constexpr double sg = INV ? 1.0 : -1.0;
+  double2 e0 = v[0], e1 = v[2], e2 = v[4], e3 = v[6], o0 = v[1], o1 = v[3], o2 = v[5], o3 = v[7];
+  dft4<INV>(e0, e1, e2, e3);
+  dft4<INV>(o0, o1, o2, o3);
+  // o_k *= w8^k: w8 = (r2, sg r2), w8^2 = (0, sg), w8^3 = (-r2, sg r2)
+  o1 = make_double2(r2 * (o1.x - sg * o1.y), r2 * (sg * o1.x + o1.y));
+  o2 = INV ? make_double2(-o2.y, o2.x) : make_double2(o2.y, -o2.x);
+  o3 = make_double2(r2 * (-o3.x - sg * o3.y), r2 * (sg * o3.x - o3.y));
+  v[0] = cadd(e0, o0);
+  v[4] = csub(e0, o0);
+  v[1] = cadd(e1, o1);
+  v[5] = csub(e1, o1);
+  v[2] = cadd(e2, o2);
+  v[6] = csub(e2, o2);
+  v[3] = cadd(e3, o3);
+  v[7] = csub(e3, o3);
+}
+
+// v[i] *= w^i, i = 0..15, w = roots[idx] (conjugated for INV)
+template <bool INV, int N = 16>
+__device__ __forceinline__ void twiddle_powers(double2 (&v)[N], const double2* __restrict__ roots, int idx) {
   double2 w = __ldg(roots + idx);
   if (INV) w.y = -w.y;
   double2 p = w;
 #pragma unroll
-  for (int i = 1; i < 16; ++i) {
+  for (int i = 1; i < N; ++i) {
     v[i] = cmul(v[i], p);
-    if (i < 15) p = cmul(p, w);
+    if (i < N - 1) p = cmul(p, w);
   }
 }
 
