@@ -366,6 +366,7 @@ struct SideStream {
   cudaStream_t s = nullptr, hi = nullptr;
   cudaEvent_t fork = nullptr, join = nullptr, b_ready = nullptr, hi_done = nullptr, b_read = nullptr;
   cudaEvent_t aux_fork = nullptr, aux_join = nullptr;  // side_fork / side_join (other products)
+  cudaEvent_t en_done = nullptr;                        // residual plan: B's energy pass done (hi)
 };
 // Keyed by the current device: one host thread may drive several GPUs (or re-target with
 // cudaSetDevice), and each device gets its own pair of streams and events.
@@ -389,6 +390,7 @@ static int get_side(SideStream** out) {
     APX_CUDA(cudaEventCreateWithFlags(&g.b_read, cudaEventDisableTiming));
     APX_CUDA(cudaEventCreateWithFlags(&g.aux_fork, cudaEventDisableTiming));
     APX_CUDA(cudaEventCreateWithFlags(&g.aux_join, cudaEventDisableTiming));
+    APX_CUDA(cudaEventCreateWithFlags(&g.en_done, cudaEventDisableTiming));
   }
   *out = &g;
   return OK;
@@ -613,6 +615,14 @@ static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int
     const char* e = getenv("APX_EN_CPS");
     return e ? std::max(1, std::min(8, atoi(e))) : 8;
   }();
+  // APX_B_ORDER=3: B's energy pass runs first, alone on hi (both it and Y are HBM streams, so the
+  // order costs nothing there), and the QR then runs without an energy pass beside it
+  if (b_after_y == 3) {
+    APX_CUDA(cudaStreamWaitEvent(hi, ss->b_read, 0));  // lo's resets
+    APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, fb ? scal + APX_S_FRO2_B : nullptr, p.partial, hi,
+                                         en_cps, resid_energy_groups(n)));
+    APX_CUDA(cudaEventRecord(ss->en_done, hi));
+  }
   stage_mark(17, hi);
   static const int y_sms = getenv("APX_Y_SMS") ? y_sm_budget() : kNumSMs;  // tuning knob
   APX_TRY(UmmaStages::a_times_x(A, Omega, Y, part, n, l, hi, y_sms));
@@ -627,14 +637,16 @@ static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int
   // ---- lo: B's cycle decomposition and the f16 lambda' table -----------------------------------
   float* lb = (float*)p.lam_b;
   auto b_stage = [&]() -> int {
+    if (b_after_y == 3) {
+      APX_CUDA(cudaStreamWaitEvent(lo, ss->en_done, 0));  // the energy pass ran on hi
+    } else {
+      APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, fb ? scal + APX_S_FRO2_B : nullptr, p.partial, lo,
+                                           en_cps, resid_energy_groups(n)));
+    }
     if (fb) {
-      APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, scal + APX_S_FRO2_B, p.partial, lo, en_cps,
-                                           resid_energy_groups(n)));
       APX_CUDA(cudaMemcpyAsync(sb, fb, kc * sizeof(int), cudaMemcpyDeviceToDevice, lo));
       APX_TRY(launch_kept_energy(p.nr_b, sb, kc, 1.0, scal + APX_S_KEPT_B, lo));
     } else {
-      APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, nullptr, p.partial, lo, en_cps,
-                                           resid_energy_groups(n)));
       APX_TRY(launch_topk(p.nr_b, n, kc, sb, lo, p.nr_b, 1.0, scal + APX_S_KEPT_B, p.en_b, scal + APX_S_FRO2_B));
     }
     APX_TRY(launch_cycle_extract<float>(B, n, sb, kc, lb, lo, /*aligned=*/true));

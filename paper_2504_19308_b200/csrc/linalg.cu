@@ -584,6 +584,254 @@ __global__ void __launch_bounds__(256) cholinv64f_kernel(const double* __restric
   }
 }
 
+// ---- blocked Cholesky inverse (l <= 64): 64 pivots on one warp, the bulk on the whole CTA -------
+// Gauss-Jordan on [G | I] by 16-column blocks. Step k (kb = 16 k):
+//   (a) warp 0 eliminates the 16 x 16 diagonal block A_kk in registers: lane i (< 16) holds row i
+//       of A_kk, lane i + 16 row i of the identity beside it; each pivot row is published in its own
+//       shared slot behind one __syncwarp, and every later row folds it in (its multiplier is
+//       a_j[i] / a_j[j]: the trailing block is symmetric, so both halves of a row read it from the
+//       published row). Rows scaled by 1 / sqrt(pivot) give Li = L_kk^{-1} (A_kk = L_kk L_kk^T).
+//   (b) the CTA: T = Li [A_k | B_k] (block row k normalised; only the left columns past the block
+//       and the right columns up to it are non-trivial: 64 columns), Mb = A_ik Li^T for the rows
+//       below, then [A_i | B_i] -= Mb T (4 x 4 register blocks) and block row k's right part := T.
+// At the end the right half is L^{-1}, X = R^{-1} = L^{-T}. The serial chain is the 64 pivots at a
+// warp's latency (one shared round trip, a reciprocal and 16 FMAs each) instead of a CTA-wide
+// publish/acquire per pivot (cholinv64f_kernel: ~1000 cycles per pivot); the O(l^3) work runs in
+// three CTA-wide phases per block. Same breakdown rule (pivot <= 4 l eps max diag G) and kappa
+// estimate: ||R||_F^2 = trace(G), so kappa_F = sqrt(trace G) ||X||_F.
+struct CholBlkSmem {
+  double S[64][130];  // [G | I] -> [.. | L^{-1}]; pitch 130 doubles
+  double T[16][66];
+  double Mb[48][17];
+  double Li[16][17];
+  double rowbuf[16][32];
+  double red[8][2];
+  double tol, trace;
+  int bad;
+  // scratch for the fused QR's Gram reduction (S is free between Cholesky runs)
+  __device__ double (*red_wide())[33] { return reinterpret_cast<double(*)[33]>(&S[0][0]); }
+};
+
+#ifndef APX_CHOL_STAMP
+#define APX_CHOL_STAMP(i)  // tools/chol_blk_probe.cu: per-phase clock stamps
+#endif
+#ifndef APX_CQR_STAMP
+#define APX_CQR_STAMP(i)  // tools/chol_blk_probe.cu: per-phase timer stamps of the fused QR (CTA 0)
+#endif
+
+__device__ __forceinline__ int cholblk_col(int q, int kb, int nr) { return q < nr ? kb + 16 + q : 64 + q - nr; }
+
+// All 256 threads. G: l x l (global or shared). Writes X = R^{-1} (zero-padded to 64 x 64) to Xs
+// (row pitch xp) and returns breakdown; *skip = (kappa_F <= skip_kappa). Ends with a CTA barrier.
+__device__ bool cholinv_blk(const double* __restrict__ G, int l, CholBlkSmem& sm, double* Xs, int xp,
+                            double skip_kappa, bool* skip) {
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  for (int e = tid; e < 64 * 64; e += 256) {
+    const int r = e >> 6, c = e & 63;
+    sm.S[r][c] = (r < l && c < l) ? G[r * l + c] : (r == c ? 1.0 : 0.0);
+    sm.S[r][64 + c] = r == c ? 1.0 : 0.0;
+  }
+  if (warp == 0) {
+    double d0 = lane < l ? G[lane * l + lane] : 0.0, d1 = lane + 32 < l ? G[(lane + 32) * l + lane + 32] : 0.0;
+    double md = fmax(d0, d1), tr = d0 + d1;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      md = fmax(md, __shfl_xor_sync(0xffffffffu, md, o));
+      tr += __shfl_xor_sync(0xffffffffu, tr, o);
+    }
+    if (lane == 0) {
+      sm.tol = 4.0 * l * 2.220446049250313e-16 * md;
+      sm.trace = tr;
+      sm.bad = 0;
+    }
+  }
+  __syncthreads();
+  APX_CHOL_STAMP(0);
+  const double tol = sm.tol;
+#pragma unroll 1
+  for (int k = 0; k < 4; ++k) {
+    const int kb = 16 * k, nr = 48 - kb;
+    // (a) the diagonal block on warp 0 by 2 x 2 block pivots: rows j, j + 1 are published together
+    //     and every later row eliminates both at once with the pivot block's inverse (one shared
+    //     round trip and one reciprocal per two pivots: tools/warp_chol_probe.cu, ~320 cycles per
+    //     single pivot); the identity half of each pivot pair is then normalised by the inverse of
+    //     the pair's 2 x 2 Cholesky factor (L^{-1} = C^{-1} E for A = (E^{-1} C)(E^{-1} C)^T).
+    if (warp == 0) {
+      const int li = lane & 15, half = lane >> 4;
+      double v[16];
+#pragma unroll
+      for (int c = 0; c < 16; ++c) v[c] = half == 0 ? sm.S[kb + li][kb + c] : (c == li ? 1.0 : 0.0);
+      bool wbad = false;
+#pragma unroll
+      for (int j = 0; j < 16; j += 2) {
+        if ((li >> 1) == (j >> 1)) {
+#pragma unroll
+          for (int c = 0; c < 16; c += 2)
+            *reinterpret_cast<double2*>(&sm.rowbuf[li][half * 16 + c]) = make_double2(v[c], v[c + 1]);
+        }
+        __syncwarp();
+        double a = sm.rowbuf[j][j], b = sm.rowbuf[j][j + 1], d = sm.rowbuf[j + 1][j + 1];
+        double det = fma(a, d, -b * b);
+        if (!(a > tol) || !(det > tol * a)) {  // pivots a and det / a (the sequential elimination's)
+          wbad = true;
+          a = 1.0;
+          b = 0.0;
+          d = 1.0;
+          det = 1.0;
+        }
+        const double idet = fast_rcp(det);
+        const double i00 = d * idet, i01 = -b * idet, i11 = a * idet;
+        if (li > j + 1) {
+          const double x0 = sm.rowbuf[j][li], x1 = sm.rowbuf[j + 1][li];  // a_ij, a_i,j+1 (symmetric)
+          const double f0 = fma(x1, i01, x0 * i00), f1 = fma(x1, i11, x0 * i01);
+          const double* p0 = &sm.rowbuf[j][half * 16];
+          const double* p1 = &sm.rowbuf[j + 1][half * 16];
+#pragma unroll
+          for (int c = 0; c < 16; c += 2) {
+            const double2 w0 = *reinterpret_cast<const double2*>(p0 + c);
+            const double2 w1 = *reinterpret_cast<const double2*>(p1 + c);
+            v[c] = fma(-f1, w1.x, fma(-f0, w0.x, v[c]));
+            v[c + 1] = fma(-f1, w1.y, fma(-f0, w0.y, v[c + 1]));
+          }
+        }
+      }
+      if (half == 1) {
+        // C = chol([[a, b], [b, d]]) = [[c00, 0], [c10, c11]]: rows j, j + 1 of Li = C^{-1} [b_j; b_j+1]
+        const int j = li & ~1;
+        const double a = sm.rowbuf[j][j], b = sm.rowbuf[j][j + 1], d = sm.rowbuf[j + 1][j + 1];
+        const double r00 = fast_rsqrt(fmax(a, 1e-300)), c10 = b * r00;
+        const double r11 = fast_rsqrt(fmax(fma(-c10, c10, d), 1e-300));
+        const double* bj = &sm.rowbuf[j][16];
+        const double* bj1 = &sm.rowbuf[j + 1][16];
+        if (li == j) {
+#pragma unroll
+          for (int c = 0; c < 16; ++c) sm.Li[li][c] = bj[c] * r00;
+        } else {
+          const double t = c10 * r00;
+#pragma unroll
+          for (int c = 0; c < 16; ++c) sm.Li[li][c] = fma(-t, bj[c], bj1[c]) * r11;
+        }
+      }
+      if (lane == 0 && wbad) sm.bad = 1;
+    }
+    __syncthreads();
+    APX_CHOL_STAMP(1 + 3 * k);
+    // (b1) T = Li [A_k | B_k] (64 columns), Mb = A_ik Li^T
+    {
+      const int mrow = tid >> 4, q0 = tid & 15;
+      double acc[4] = {0.0, 0.0, 0.0, 0.0};
+      int cols[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) cols[x] = cholblk_col(q0 + 16 * x, kb, nr);
+#pragma unroll
+      for (int s = 0; s < 16; ++s) {
+        const double w = sm.Li[mrow][s];  // zero above the diagonal
+#pragma unroll
+        for (int x = 0; x < 4; ++x) acc[x] = fma(w, sm.S[kb + s][cols[x]], acc[x]);
+      }
+#pragma unroll
+      for (int x = 0; x < 4; ++x) sm.T[mrow][q0 + 16 * x] = acc[x];
+    }
+    {
+      // up to three independent rows per thread (nr <= 48)
+      const int sc = tid & 15, ip0 = tid >> 4;
+      double a[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+      for (int s2 = 0; s2 < 16; ++s2) {
+        const double li_v = sm.Li[sc][s2];
+#pragma unroll
+        for (int x = 0; x < 3; ++x)
+          if (ip0 + 16 * x < nr) a[x] = fma(sm.S[kb + 16 + ip0 + 16 * x][kb + s2], li_v, a[x]);
+      }
+#pragma unroll
+      for (int x = 0; x < 3; ++x)
+        if (ip0 + 16 * x < nr) sm.Mb[ip0 + 16 * x][sc] = a[x];
+    }
+    __syncthreads();
+    APX_CHOL_STAMP(2 + 3 * k);
+    // (b2) the trailing update in 4 x 4 register blocks, and block row k's right part
+    if (tid < (nr / 4) * 16) {
+      const int rb = (tid >> 4) * 4, q0 = tid & 15;
+      double acc[4][4];
+      int cols[4];
+#pragma unroll
+      for (int x = 0; x < 4; ++x) cols[x] = cholblk_col(q0 + 16 * x, kb, nr);
+#pragma unroll
+      for (int y = 0; y < 4; ++y)
+#pragma unroll
+        for (int x = 0; x < 4; ++x) acc[y][x] = sm.S[kb + 16 + rb + y][cols[x]];
+#pragma unroll 4
+      for (int s = 0; s < 16; ++s) {
+        double mv[4], tv[4];
+#pragma unroll
+        for (int y = 0; y < 4; ++y) mv[y] = sm.Mb[rb + y][s];
+#pragma unroll
+        for (int x = 0; x < 4; ++x) tv[x] = sm.T[s][q0 + 16 * x];
+#pragma unroll
+        for (int y = 0; y < 4; ++y)
+#pragma unroll
+          for (int x = 0; x < 4; ++x) acc[y][x] = fma(-mv[y], tv[x], acc[y][x]);
+      }
+#pragma unroll
+      for (int y = 0; y < 4; ++y)
+#pragma unroll
+        for (int x = 0; x < 4; ++x) sm.S[kb + 16 + rb + y][cols[x]] = acc[y][x];
+    }
+    for (int e = tid; e < 16 * 64; e += 256) {
+      const int mrow = e >> 6, c = e & 63;
+      if (c <= kb + 15) sm.S[kb + mrow][64 + c] = sm.T[mrow][nr + c];
+    }
+    __syncthreads();
+    APX_CHOL_STAMP(3 + 3 * k);
+  }
+  double x2 = 0.0;
+  for (int e = tid; e < 64 * 64; e += 256) {
+    const int i = e >> 6, c = e & 63;
+    const double xv = (i < l && c < l && i <= c) ? sm.S[c][64 + i] : 0.0;  // X[i][c] = L^{-1}[c][i]
+    Xs[i * xp + c] = xv;
+    x2 = fma(xv, xv, x2);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) x2 += __shfl_xor_sync(0xffffffffu, x2, o);
+  if (lane == 0) sm.red[warp][0] = x2;
+  __syncthreads();
+  double sx = 0.0;
+#pragma unroll
+  for (int i = 0; i < 8; ++i) sx += sm.red[i][0];
+  *skip = sqrt(sm.trace) * sqrt(sx) <= skip_kappa;
+  const bool bad = sm.bad != 0;
+  __syncthreads();  // sm may be reused by the caller
+  return bad;
+}
+
+// standalone launch of cholinv_blk: same contract as cholinv64f_kernel
+__global__ void __launch_bounds__(256, 1) cholinv_blk_kernel(const double* __restrict__ Gin, int l,
+                                                             double* __restrict__ Xout, const int* __restrict__ gate,
+                                                             int* __restrict__ breakdown, int* __restrict__ skip_out,
+                                                             double skip_kappa) {
+  pdl_trigger();
+  pdl_wait();
+  if (*gate) return;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CholBlkSmem& sm = *reinterpret_cast<CholBlkSmem*>(smem_raw);
+  double* Xs = reinterpret_cast<double*>(smem_raw + sizeof(CholBlkSmem));  // 64 x 64
+  bool skip = false;
+  const bool bad = cholinv_blk(Gin, l, sm, Xs, 64, skip_kappa, &skip);
+  if (bad) {
+    if (threadIdx.x == 0) {
+      *breakdown = 1;
+      if (skip_out) *skip_out = 1;
+    }
+    return;
+  }
+  for (int e = threadIdx.x; e < l * l; e += 256) {
+    const int i = e / l, c = e - i * l;
+    Xout[e] = Xs[i * 64 + c];
+  }
+  if (threadIdx.x == 0 && skip_out) *skip_out = skip ? 1 : 0;
+}
+constexpr size_t kCholBlkSmem = sizeof(CholBlkSmem) + 64 * 64 * sizeof(double);
+
 // Cholesky-inverse launch for l <= 64. (Measured alternative: the same elimination on 1024 threads,
 // 4 + 4 columns per thread, was slower -- 65 vs 55 us in the C4 chain, C1 2.19 vs 2.11 ms. The
 // step is bound by its owner warp: rows j and j+1 sit in one warp, so row j's scaling and row
@@ -591,8 +839,16 @@ __global__ void __launch_bounds__(256) cholinv64f_kernel(const double* __restric
 static cudaError_t launch_cholinv64(const double* G, int l, double* X, const int* gate, int* breakdown, int* skip_out,
                                    double skip_kappa, cudaStream_t st) {
   static const bool barrier = getenv("APX_CHOL_BARRIER") != nullptr;  // A/B: one CTA barrier per pivot
+  static const bool flat = getenv("APX_CHOL_FLAT") != nullptr;        // A/B: unblocked, per-row mbarriers
   if (barrier)
     return launch_pdl(cholinv64_kernel, dim3(1), dim3(256), 0, st, G, l, X, gate, breakdown, skip_out, skip_kappa);
+  if (!flat) {
+    const cudaError_t a = cudaFuncSetAttribute(cholinv_blk_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)kCholBlkSmem);
+    if (a != cudaSuccess) return a;
+    return launch_pdl(cholinv_blk_kernel, dim3(1), dim3(256), kCholBlkSmem, st, G, l, X, gate, breakdown, skip_out,
+                      skip_kappa);
+  }
   constexpr size_t smem = (size_t)64 * 128 * sizeof(double);
   const cudaError_t attr = cudaFuncSetAttribute(cholinv64f_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
   if (attr != cudaSuccess) return attr;
@@ -659,6 +915,195 @@ __global__ void __launch_bounds__(256) apply_x_kernel(const TI* __restrict__ Y, 
     }
   }
 }
+
+// ---- fused CholeskyQR2 (l <= 64): one 64-row tile per CTA, every CTA resident at once --------------
+// One launch instead of the chain gram -> reduce -> cholinv -> apply (-> the same again): each CTA
+// keeps its tile of Y in shared memory (fp64) for the whole QR, writes its Gram partial, and after a
+// grid barrier reduces a slice of the entries (each entry summed over the partials in a fixed order)
+// ; after a second barrier EVERY CTA runs the same Cholesky inverse on the reduced G (cholinv_blk:
+// bitwise the same X everywhere, no third barrier and no single-CTA stage), applies it to its tile,
+// and -- when the conditioning asks for pass 2 -- repeats on the Q1 tile it still holds. Launched
+// cooperatively (the runtime checks that the grid fits co-resident); the barriers are an atomic
+// counter with a bounded wait: a barrier that does not complete within 50 ms (a co-tenant holding
+// SMs) raises the breakdown flag instead, so the Householder kernel that follows recomputes Q.
+// flag: [0] breakdown (-> Householder), [1] pass 2 skipped, [2] barrier counter (zeroed before).
+struct CqrSmem {
+  double Ys[64][kTP];  // the tile [r][i]: Y, then Q1
+  double Xs[64][kTP];  // X = R^{-1} [i][c]
+  CholBlkSmem ch;
+  int abort;
+};
+
+__device__ __forceinline__ bool cqr_grid_sync(unsigned* ctr, unsigned target, volatile int* s_abort) {
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    __threadfence();
+    atomicAdd(ctr, 1u);
+    unsigned long long t0, now;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t0));
+    while (true) {
+      unsigned v;
+      asm volatile("ld.acquire.gpu.global.u32 %0, [%1];" : "=r"(v) : "l"(ctr) : "memory");
+      if (v >= target) break;
+      asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(now));
+      if (now - t0 > 50000000ull) {
+        *s_abort = 1;
+        break;
+      }
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  return *s_abort == 0;
+}
+
+// partial Gram of the staged tile -> part (l x l)
+__device__ __forceinline__ void cqr_gram_tile(const double (*Ys)[kTP], int l, double* __restrict__ part) {
+  const int bi = (threadIdx.x >> 4) * 4, bj = (threadIdx.x & 15) * 4;
+  double acc[4][4];
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+#pragma unroll 8
+  for (int r = 0; r < 64; ++r) {
+    const double2 a01 = *reinterpret_cast<const double2*>(&Ys[r][bi]);
+    const double2 a23 = *reinterpret_cast<const double2*>(&Ys[r][bi + 2]);
+    const double2 b01 = *reinterpret_cast<const double2*>(&Ys[r][bj]);
+    const double2 b23 = *reinterpret_cast<const double2*>(&Ys[r][bj + 2]);
+    const double av[4] = {a01.x, a01.y, a23.x, a23.y}, bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+    for (int x = 0; x < 4; ++x)
+#pragma unroll
+      for (int y = 0; y < 4; ++y) acc[x][y] = fma(av[x], bv[y], acc[x][y]);
+  }
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) {
+      const int i = bi + x, j = bj + y;
+      if (i < l && j < l) part[i * l + j] = acc[x][y];
+    }
+}
+
+// this CTA's slice of G = sum_p part[p] (8 groups of 32 lanes stride the partials; fixed order)
+__device__ __forceinline__ void cqr_reduce_slice(const double* __restrict__ part, int parts, int l,
+                                                 double* __restrict__ G, double (*red)[33]) {
+  const int ll = l * l, per = (int)ceil_div(ll, (int)gridDim.x);
+  const int e0 = blockIdx.x * per, e1 = min(ll, e0 + per);
+  const int lane = threadIdx.x & 31, grp = threadIdx.x >> 5;
+  for (int eb = e0; eb < e1; eb += 32) {
+    const int e = eb + lane;
+    double s0 = 0.0, s1 = 0.0;
+    if (e < e1) {
+      int p = grp;
+      for (; p + 8 < parts; p += 16) {
+        s0 += __ldcg(part + (size_t)p * ll + e);
+        s1 += __ldcg(part + (size_t)(p + 8) * ll + e);
+      }
+      for (; p < parts; p += 8) s0 += __ldcg(part + (size_t)p * ll + e);
+    }
+    red[grp][lane] = s0 + s1;
+    __syncthreads();
+    if (grp == 0 && e < e1) {
+      double t = 0.0;
+#pragma unroll
+      for (int g = 0; g < 8; ++g) t += red[g][lane];
+      G[e] = t;
+    }
+    __syncthreads();
+  }
+}
+
+// acc = tile . X (4 x 4 per thread: rows tr.., columns tc..)
+__device__ __forceinline__ void cqr_apply_tile(const double (*Ys)[kTP], const double (*Xs)[kTP], double (&acc)[4][4]) {
+  const int tr = (threadIdx.x >> 4) * 4, tc = (threadIdx.x & 15) * 4;
+#pragma unroll
+  for (int x = 0; x < 4; ++x)
+#pragma unroll
+    for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
+#pragma unroll 8
+  for (int i = 0; i < 64; ++i) {
+    const double2 b01 = *reinterpret_cast<const double2*>(&Xs[i][tc]);
+    const double2 b23 = *reinterpret_cast<const double2*>(&Xs[i][tc + 2]);
+    const double bv[4] = {b01.x, b01.y, b23.x, b23.y};
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const double a = Ys[tr + x][i];
+#pragma unroll
+      for (int y = 0; y < 4; ++y) acc[x][y] = fma(a, bv[y], acc[x][y]);
+    }
+  }
+}
+
+template <typename TI, typename TO>
+__global__ void __launch_bounds__(256, 1) cqr2_fused_kernel(const TI* __restrict__ Y, int64_t rs, int64_t cs, int m,
+                                                            int l, double* __restrict__ part1,
+                                                            double* __restrict__ part2, double* __restrict__ G1,
+                                                            double* __restrict__ G2, int* __restrict__ flag,
+                                                            TO* __restrict__ Q, int64_t qrs, int64_t qcs,
+                                                            TO* __restrict__ Q2, int64_t q2rs, int64_t q2cs, int tf32,
+                                                            double skip_kappa) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  CqrSmem& sm = *reinterpret_cast<CqrSmem*>(smem_raw);
+  unsigned* ctr = reinterpret_cast<unsigned*>(flag + 2);
+  const unsigned nb = gridDim.x;
+  const int b = blockIdx.x, r0 = b * 64;
+  APX_CQR_STAMP(0);
+  if (threadIdx.x == 0) sm.abort = 0;
+  load_tile64<false>(Y, rs, cs, m, l, r0, sm.Ys);
+  __syncthreads();
+  APX_CQR_STAMP(1);
+  cqr_gram_tile(sm.Ys, l, part1 + (size_t)b * l * l);
+  APX_CQR_STAMP(2);
+  if (!cqr_grid_sync(ctr, nb, &sm.abort)) goto fail;
+  APX_CQR_STAMP(3);
+  cqr_reduce_slice(part1, nb, l, G1, sm.ch.red_wide());
+  APX_CQR_STAMP(4);
+  if (!cqr_grid_sync(ctr, 2 * nb, &sm.abort)) goto fail;
+  APX_CQR_STAMP(5);
+  {
+    bool skip2 = false;
+    if (cholinv_blk(G1, l, sm.ch, &sm.Xs[0][0], kTP, skip_kappa, &skip2)) goto fail;
+    APX_CQR_STAMP(6);
+    double acc[4][4];
+    cqr_apply_tile(sm.Ys, sm.Xs, acc);
+    APX_CQR_STAMP(7);
+    const int tr = (threadIdx.x >> 4) * 4, tc = (threadIdx.x & 15) * 4;
+    if (!skip2) {
+      __syncthreads();  // every read of the Y tile done
+#pragma unroll
+      for (int x = 0; x < 4; ++x)
+#pragma unroll
+        for (int y = 0; y < 4; ++y) sm.Ys[tr + x][tc + y] = (tc + y < l) ? acc[x][y] : 0.0;
+      __syncthreads();
+      cqr_gram_tile(sm.Ys, l, part2 + (size_t)b * l * l);
+      if (!cqr_grid_sync(ctr, 3 * nb, &sm.abort)) goto fail;
+      cqr_reduce_slice(part2, nb, l, G2, sm.ch.red_wide());
+      if (!cqr_grid_sync(ctr, 4 * nb, &sm.abort)) goto fail;
+      bool unused = false;
+      if (cholinv_blk(G2, l, sm.ch, &sm.Xs[0][0], kTP, 0.0, &unused)) goto fail;
+      cqr_apply_tile(sm.Ys, sm.Xs, acc);
+    }
+    if (b == 0 && threadIdx.x == 0) flag[1] = skip2 ? 1 : 0;
+#pragma unroll
+    for (int x = 0; x < 4; ++x) {
+      const int r = r0 + tr + x;
+      if (r >= m) continue;
+#pragma unroll
+      for (int y = 0; y < 4; ++y) {
+        const int c = tc + y;
+        if (c >= l) continue;
+        if (Q) Q[(size_t)r * qrs + (size_t)c * qcs] = qout<TO>(acc[x][y], tf32);
+        if (Q2) Q2[(size_t)r * q2rs + (size_t)c * q2cs] = qout<TO>(acc[x][y], tf32);
+      }
+    }
+    return;
+  }
+fail:
+  if (threadIdx.x == 0) atomicExch(flag, 1);  // breakdown or barrier timeout: the Householder kernel runs
+}
+constexpr size_t kCqrSmem = sizeof(CqrSmem);
 
 // ---- Q = Y R^{-1} by forward substitution q R = y, one warp per row ------------------------
 // Lane c owns columns c, c+32, ...; at step j the owner finalises q_j = acc_j / R_jj and every
@@ -1001,7 +1446,8 @@ __global__ void __launch_bounds__(kSmallQRThreads) qr_small_kernel(const TI* __r
 __global__ void reset_flag_kernel(int* flag, int v) {
   pdl_trigger();
   pdl_wait();
-  *flag = v;
+  flag[0] = v;
+  flag[2] = 0;  // the fused QR's barrier counter
 }
 __global__ void flag_to_double_kernel(const int* flag, double* out) { *out = (double)*flag; }
 
@@ -1083,6 +1529,17 @@ static int launch_chol(const double* G, int l, double* R, double* rdiag, int* fl
 // Q (m x l, strides qrs/qcs) = orth(Y); optional second copy Q2 (e.g. Q^T). method: 0 auto,
 // 1 force Householder. tf32: round the fp32 outputs to the nearest TF32 value (the TF32 tensor
 // core operand paths; see qout).
+// the fused CholeskyQR2 applies when its one-tile-per-CTA grid fits co-resident (one CTA per SM),
+// outside graph capture (concurrent captured products would compete for co-residency);
+// APX_QR_UNFUSED=1 selects the kernel chain (A/B)
+static bool cqr_fused_ok(int m, cudaStream_t st) {
+  static const bool off = getenv("APX_QR_UNFUSED") != nullptr;
+  if (off) return false;
+  cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
+  if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return false;
+  return ceil_div(m, 64) <= device_sms();
+}
+
 template <typename TI, typename TO>
 int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, int64_t qrs, int64_t qcs, TO* Q2,
                       int64_t q2rs, int64_t q2cs, void* wsp, size_t ws_bytes, int method, cudaStream_t st,
@@ -1117,6 +1574,26 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
     qr_small_kernel<TI, TO><<<1, kSmallQRThreads, smem, st>>>(Y, rs, cs, m, l, flag, Q, qrs, qcs, Q2, q2rs, q2cs,
                                                                tf32);
     APX_LAUNCH_CHECK();
+  } else if (!householder_only && l <= 64 && cqr_fused_ok(m, st)) {
+    // fused CholeskyQR2: one cooperative launch (cqr2_fused_kernel)
+    const double skip_kappa = sizeof(TO) == 4 ? 3.0e4 : 0.0;
+    double* part2 = W;  // m l >= parts l^2 doubles
+    APX_CUDA(cudaFuncSetAttribute(cqr2_fused_kernel<TI, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                  (int)kCqrSmem));
+    cudaLaunchConfig_t cfg = {};
+    cfg.gridDim = dim3((unsigned)parts);
+    cfg.blockDim = dim3(256);
+    cfg.dynamicSmemBytes = kCqrSmem;
+    cfg.stream = st;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeCooperative;
+    attr[0].val.cooperative = 1;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    APX_CUDA(cudaLaunchKernelEx(&cfg, cqr2_fused_kernel<TI, TO>, Y, rs, cs, m, l, part, part2, G, Rinv, flag, Q, qrs,
+                                qcs, Q2, q2rs, q2cs, tf32, skip_kappa));
+    APX_LAUNCH_CHECK();
+    for (int mk = 12; mk <= 15; ++mk) stage_mark(mk, st);
   } else if (!householder_only && l <= 64) {
     // fast path: CholeskyQR with R^{-1}; second pass only when the conditioning requires it
     int* skip2 = flag + 1;

@@ -125,19 +125,25 @@ __global__ void dup_cols_kernel(const float* __restrict__ Q, int rows, int l, fl
   }
 }
 
-// f16 lambda' table in the gather's thread order: entry (t, g * NT + tid) holds the CPT columns
-// g * CPT NT + q * NT + tid (q < CPT) of row t as CPT/2 packed f16x2 words, scaled by 2^(15 - e_B)
+constexpr int kHR = 8;  // rows per block: 8 halves = one 16-byte vector per column
+constexpr int kHU = 4;  // shifts per lambda batch
+
+// f16 lambda' table in the gather's thread order: the CPT columns g * CPT NT + q * NT + tid (q <
+// CPT) of shift t are CPT/2 packed f16x2 words, scaled by 2^(15 - e_B), at word
+//   ((g * kp / kHU + t / kHU) * NT + tid) * kHU * CPT/2 + (t % kHU) * CPT/2,
+// so one thread's batch of kHU shifts is ONE contiguous 16- or 32-byte run (a warp's batch: 512 or
+// 1024 contiguous bytes), fetched with one or two vector loads from one running pointer.
 __global__ void lam_f16_kernel(const float* __restrict__ lam, int kp, int n, int nt, int cpt,
                                const double* __restrict__ fro2_b, uint32_t* __restrict__ out) {
   const float s = ldexpf(1.f, 15 - f16_scale_exp(*fro2_b));
-  const int per_row = n / cpt;
+  const int per_row = n / cpt, lw = cpt / 2;
   const size_t count = (size_t)kp * per_row;
   for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count; i += (size_t)gridDim.x * blockDim.x) {
     const int t = (int)(i / per_row), e = (int)(i - (size_t)t * per_row);
     const int g = e / nt, tid = e - g * nt;
     const float* row = lam + (size_t)t * n + (size_t)g * cpt * nt + tid;
-    for (int w = 0; w < cpt / 2; ++w)
-      out[i * (cpt / 2) + w] = pack_half2(s * row[(2 * w) * nt], s * row[(2 * w + 1) * nt]);
+    const size_t o = (((size_t)g * (kp / kHU) + t / kHU) * nt + tid) * kHU * lw + (size_t)(t % kHU) * lw;
+    for (int w = 0; w < lw; ++w) out[o + w] = pack_half2(s * row[(2 * w) * nt], s * row[(2 * w + 1) * nt]);
   }
 }
 
@@ -149,14 +155,17 @@ __device__ __forceinline__ float fhfma(unsigned short a, unsigned short b, float
 __device__ __forceinline__ unsigned short lo16(uint32_t v) { return (unsigned short)(v & 0xffffu); }
 __device__ __forceinline__ unsigned short hi16(uint32_t v) { return (unsigned short)(v >> 16); }
 
+// one thread's lambda' batch: kHU shifts x W words, contiguous (lam_f16_kernel's layout)
 template <int W>
-__device__ __forceinline__ void ldg_nc_words(const uint32_t* p, uint32_t (&v)[W]) {
-  if constexpr (W == 1) {
-    asm volatile("ld.global.nc.u32 %0, [%1];" : "=r"(v[0]) : "l"(p));
-  } else {
-    static_assert(W == 2, "1 or 2 words");
-    asm volatile("ld.global.nc.v2.u32 {%0, %1}, [%2];" : "=r"(v[0]), "=r"(v[1]) : "l"(p));
-  }
+__device__ __forceinline__ void ldg_nc_batch(const uint32_t* p, uint32_t (&v)[kHU][W]) {
+  static_assert(kHU == 4 && (W == 1 || W == 2), "batch = 16 or 32 bytes");
+  asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+               : "=r"(v[0][0]), "=r"(v[W == 1 ? 1 : 0][W - 1]), "=r"(v[W == 1 ? 2 : 1][0]), "=r"(v[W == 1 ? 3 : 1][W - 1])
+               : "l"(p));
+  if constexpr (W == 2)
+    asm volatile("ld.global.nc.v4.u32 {%0, %1, %2, %3}, [%4];"
+                 : "=r"(v[2][0]), "=r"(v[2][1]), "=r"(v[3][0]), "=r"(v[3][1])
+                 : "l"(p + 4));
 }
 
 __device__ __forceinline__ void mbar_init(uint64_t* b, uint32_t c) {
@@ -171,8 +180,6 @@ __device__ __forceinline__ void mbar_wait(uint64_t* b, uint32_t phase) {
       : "memory");
 }
 
-constexpr int kHR = 8;  // rows per block: 8 halves = one 16-byte vector per column
-constexpr int kHU = 4;  // shifts per lambda batch
 
 // M[r0 + i, c] = 2^(e_A + e_B - 30) sum_t dAh[r0 + i, (c + J_t) mod n] * lamh_t[c], i < 8.
 // Xh: ceil(m_rows / 8) blocks of n uint4 (block b, column m = rows 8b..8b+7 of column m as f16);
@@ -186,7 +193,11 @@ constexpr int kHU = 4;  // shifts per lambda batch
 // RMW: M += (instead of =) the gather -- each column group's old M values are loaded at the
 // group's start (their latency hides under the shift loop) -- and the per-block ||M||^2 partials
 // of the final values go to msq_partial[blk] (fixed-order block sum).
-template <int NT, int CPT, bool RMW>
+// PAD: the first (CPT - 1) NT columns of the block are staged a second time behind its end (a
+// second bulk copy on the same barrier), so a thread's CPT columns for one shift are ONE wrapped base
+// plus the constant offsets q NT -- one index wrap per shift instead of one per column, and the
+// loads take their offsets as immediates.
+template <int NT, int CPT, bool RMW, bool PAD>
 __global__ void __launch_bounds__(NT, 1)
     cycle_gather_f16_kernel(const uint4* __restrict__ Xh, const uint32_t* __restrict__ lamh,
                             const int* __restrict__ J, int k, int kp, int n, int m_rows, float* __restrict__ M,
@@ -196,8 +207,9 @@ __global__ void __launch_bounds__(NT, 1)
   if (gate != nullptr && *gate == 0) return;  // the plan fell back to the fp32 gather (bm_finalize)
   constexpr int LW = CPT / 2;  // lambda' words per thread per shift
   extern __shared__ __align__(16) unsigned char smem_raw[];
+  constexpr int PADC = PAD ? (CPT - 1) * NT : 0;  // replicated columns behind the block
   uint4* Xs = reinterpret_cast<uint4*>(smem_raw);
-  int* sJ = reinterpret_cast<int*>(Xs + n);
+  int* sJ = reinterpret_cast<int*>(Xs + n + PADC);
   __shared__ __align__(8) uint64_t bar;
   __shared__ int s_blk, s_nxt;
   __shared__ double red[32];
@@ -211,7 +223,7 @@ __global__ void __launch_bounds__(NT, 1)
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
     s_nxt = -1;
   }
-  const uint32_t bytes = (uint32_t)n * 16u;
+  const uint32_t bytes = (uint32_t)n * 16u, pbytes = (uint32_t)PADC * 16u;
   const int groups = n / (CPT * NT);
   for (int it = 0;; ++it) {
     if (tid == 0) {
@@ -223,13 +235,19 @@ __global__ void __launch_bounds__(NT, 1)
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(
                          (uint32_t)__cvta_generic_to_shared(&bar)),
-                     "r"(bytes)
+                     "r"(bytes + pbytes)
                      : "memory");
         asm volatile(
             "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
                 (uint32_t)__cvta_generic_to_shared(Xs)),
             "l"(Xh + (size_t)s_blk * n), "r"(bytes), "r"((uint32_t)__cvta_generic_to_shared(&bar))
             : "memory");
+        if constexpr (PAD)
+          asm volatile(
+              "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                  (uint32_t)__cvta_generic_to_shared(Xs + n)),
+              "l"(Xh + (size_t)s_blk * n), "r"(pbytes), "r"((uint32_t)__cvta_generic_to_shared(&bar))
+              : "memory");
       }
     }
     __syncthreads();
@@ -255,8 +273,9 @@ __global__ void __launch_bounds__(NT, 1)
           for (int q = 0; q < CPT; ++q)
             mold[q][r] = r < rows ? __ldcg(M + (size_t)(r0 + r) * n + cbase + q * NT) : 0.f;
       }
-      const uint32_t* lrow = lamh + ((size_t)g * NT + tid) * LW;
-      const size_t lstride = (size_t)(n / CPT) * LW;
+      // this thread's lambda' batches for group g: one running pointer, NT kHU LW words per batch
+      const uint32_t* lp = lamh + ((size_t)g * (kp / kHU) * NT + tid) * (kHU * LW);
+      constexpr int kLStep = NT * kHU * LW;
       float acc[CPT][kHR];
 #pragma unroll
       for (int q = 0; q < CPT; ++q)
@@ -266,20 +285,26 @@ __global__ void __launch_bounds__(NT, 1)
       // (the batch's shifts ride along: their shared loads head each column's index chain)
       uint32_t lvA[kHU][LW], lvB[kHU][LW];
       int jA[kHU], jB[kHU];
+      ldg_nc_batch<LW>(lp, lvA);
 #pragma unroll
-      for (int u = 0; u < kHU; ++u) {
-        ldg_nc_words<LW>(lrow + (size_t)u * lstride, lvA[u]);
-        jA[u] = sJ[u];
-      }
+      for (int u = 0; u < kHU; ++u) jA[u] = sJ[u];
       auto compute = [&](const int (&jv)[kHU], const uint32_t (&lv)[kHU][LW]) {
 #pragma unroll
         for (int u = 0; u < kHU; ++u) {
           const int jt = jv[u];
+          unsigned m0 = (unsigned)(cbase + jt);
+          if constexpr (PAD) m0 = min(m0, m0 - (unsigned)n);
 #pragma unroll
           for (int q = 0; q < CPT; ++q) {
-            unsigned m = (unsigned)(cbase + q * NT + jt);
-            m = min(m, m - (unsigned)n);
-            APX_DCHECK(m < (unsigned)n);
+            unsigned m;
+            if constexpr (PAD) {
+              m = m0 + q * NT;
+              APX_DCHECK(m < (unsigned)(n + PADC));
+            } else {
+              m = m0 + q * NT;
+              m = min(m, m - (unsigned)n);
+              APX_DCHECK(m < (unsigned)n);
+            }
             const uint4 x = Xs[m];
             const unsigned short l = (q & 1) ? hi16(lv[u][q >> 1]) : lo16(lv[u][q >> 1]);
             acc[q][0] = fhfma(lo16(x.x), l, acc[q][0]);
@@ -295,20 +320,18 @@ __global__ void __launch_bounds__(NT, 1)
       };
       for (int t0 = 0; t0 < kp; t0 += 2 * kHU) {
         if (t0 + kHU < kp) {
+          lp += kLStep;
+          ldg_nc_batch<LW>(lp, lvB);
 #pragma unroll
-          for (int u = 0; u < kHU; ++u) {
-            ldg_nc_words<LW>(lrow + (size_t)(t0 + kHU + u) * lstride, lvB[u]);
-            jB[u] = sJ[t0 + kHU + u];
-          }
+          for (int u = 0; u < kHU; ++u) jB[u] = sJ[t0 + kHU + u];
         }
         compute(jA, lvA);
         if (t0 + kHU >= kp) break;
         if (t0 + 2 * kHU < kp) {
+          lp += kLStep;
+          ldg_nc_batch<LW>(lp, lvA);
 #pragma unroll
-          for (int u = 0; u < kHU; ++u) {
-            ldg_nc_words<LW>(lrow + (size_t)(t0 + 2 * kHU + u) * lstride, lvA[u]);
-            jA[u] = sJ[t0 + 2 * kHU + u];
-          }
+          for (int u = 0; u < kHU; ++u) jA[u] = sJ[t0 + 2 * kHU + u];
         }
         compute(jB, lvB);
       }
@@ -408,7 +431,17 @@ int launch_dup_cols(const float* Q, int rows, int l, float* Q2, cudaStream_t st)
 // threads per CTA (= column stride) of the f16 gather for n, or 0 when n does not fit its layout
 int gather_f16_threads(int n) { return f16_cfg(n).nt; }
 
-size_t gather_f16_smem(int n, int kp) { return (size_t)n * 16 + (size_t)kp * sizeof(int); }
+// the padded layout when it fits (APX_F16_PAD=0 disables it)
+static bool f16_pad(int n, int kp) {
+  static const bool off = getenv("APX_F16_PAD") != nullptr && atoi(getenv("APX_F16_PAD")) == 0;
+  const F16Cfg c = f16_cfg(n);
+  return !off && c.nt > 0 && (size_t)(n + (c.cpt - 1) * c.nt) * 16 + (size_t)kp * sizeof(int) <= 220 * 1024;
+}
+
+size_t gather_f16_smem(int n, int kp) {
+  const F16Cfg c = f16_cfg(n);
+  return (size_t)(n + (f16_pad(n, kp) ? (c.cpt - 1) * c.nt : 0)) * 16 + (size_t)kp * sizeof(int);
+}
 
 int launch_lam_f16(const float* lam, int kp, int n, const double* fro2_b, uint16_t* out, cudaStream_t st) {
   const F16Cfg c = f16_cfg(n);
@@ -439,9 +472,15 @@ int launch_gather_f16(const uint16_t* Xh, const uint16_t* lamh, const int* J, in
     APX_LAUNCH_CHECK();
     return OK;
   };
-#define APX_F16(NTV, CPTV)                                                                        \
-  if (c.nt == NTV && c.cpt == CPTV)                                                                \
-    return msq_partial ? go(cycle_gather_f16_kernel<NTV, CPTV, true>) : go(cycle_gather_f16_kernel<NTV, CPTV, false>);
+  const bool pad = f16_pad(n, kp);
+#define APX_F16(NTV, CPTV)                                                                                   \
+  if (c.nt == NTV && c.cpt == CPTV) {                                                                         \
+    if (pad)                                                                                                  \
+      return msq_partial ? go(cycle_gather_f16_kernel<NTV, CPTV, true, true>)                                 \
+                         : go(cycle_gather_f16_kernel<NTV, CPTV, false, true>);                               \
+    return msq_partial ? go(cycle_gather_f16_kernel<NTV, CPTV, true, false>)                                  \
+                       : go(cycle_gather_f16_kernel<NTV, CPTV, false, false>);                                \
+  }
   APX_F16(512, 4) APX_F16(256, 4) APX_F16(128, 4) APX_F16(1024, 2) APX_F16(512, 2) APX_F16(256, 2)
 #undef APX_F16
   set_error("f16 gather: unsupported shape %dx%d", c.nt, c.cpt);
