@@ -91,6 +91,87 @@ __global__ void __launch_bounds__(256, 8) cycle_energy_partial(const T* __restri
   if (threadIdx.x == 0) counters[blockIdx.x] = 0u;
 }
 
+// K3 (fp32, n % 4 == 0): the same energies from a row-major stream. A CTA (one per SM) walks its
+// rows, each row staged whole into shared memory by one bulk async copy into a ring of kEnRing row
+// buffers (three rows in flight behind the one being folded in: ~100 KB per SM), and accumulates
+// each element's square into a per-cycle fp32 array in shared memory (cycle of (r, c) =
+// (r - c) mod n). All threads fold one row at a time (a barrier per row), so no two threads touch a
+// cycle at once and the sums are deterministic; the array is stored permuted, q -> (q mod 4) n/4 +
+// q/4, so a warp's updates for one vector component hit consecutive words (conflict-free). Per CTA
+// <= rows_per_chunk terms per cycle in fp32; the partials go out as fp64 for
+// cycle_energy_finalize (fixed group order). (The diagonal walk of cycle_energy_partial reads one
+// 4-byte element per thread and row: 3.9 TB/s at n = 8192; a register-prefetched row stream
+// measured the same -- too few bytes in flight.)
+constexpr int kEnRing = 4;
+__global__ void __launch_bounds__(512, 1) cycle_energy_rows4_kernel(const float* __restrict__ A, int n,
+                                                                    int rows_per_chunk, double* __restrict__ partial) {
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  const int tid = threadIdx.x, nq = n >> 2;
+  float4* ring = reinterpret_cast<float4*>(smem_raw);                  // kEnRing rows of nq float4
+  float* s_en = reinterpret_cast<float*>(ring + (size_t)kEnRing * nq);  // n accumulators
+  __shared__ __align__(8) uint64_t bars[kEnRing];
+  for (int i = tid; i < n; i += 512) s_en[i] = 0.f;
+  const int r0 = blockIdx.x * rows_per_chunk, r1 = min(n, r0 + rows_per_chunk);
+  const uint32_t bytes = (uint32_t)nq * 16u;
+  auto issue = [&](int r) {  // thread 0: row r into slot (r - r0) % kEnRing
+    const int slot = (r - r0) % kEnRing;
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bars[slot]);
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(b), "r"(bytes) : "memory");
+    asm volatile("cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                     (uint32_t)__cvta_generic_to_shared(ring + (size_t)slot * nq)),
+                 "l"(A + (size_t)r * n), "r"(bytes), "r"(b)
+                 : "memory");
+  };
+  if (tid == 0) {
+    for (int i = 0; i < kEnRing; ++i)
+      asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"((uint32_t)__cvta_generic_to_shared(&bars[i])));
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    for (int r = r0; r < min(r1, r0 + kEnRing); ++r) issue(r);
+  }
+  __syncthreads();
+  for (int r = r0; r < r1; ++r) {
+    const int it = r - r0, slot = it % kEnRing;
+    const uint32_t b = (uint32_t)__cvta_generic_to_shared(&bars[slot]);
+    asm volatile(
+        "{\n.reg .pred p;\nEW_%=:\n"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n"
+        "@!p bra EW_%=;\n}\n" ::"r"(b),
+        "r"((uint32_t)((it / kEnRing) & 1))
+        : "memory");
+    const float4* row = ring + (size_t)slot * nq;
+    for (int c4 = tid; c4 < nq; c4 += 512) {
+      const float4 v4 = row[c4];
+      int q = r - 4 * c4;  // cycle of column 4 c4 (r, 4 c4 < n), minus x for component x
+      if (q < 0) q += n;
+      const float v[4] = {v4.x, v4.y, v4.z, v4.w};
+#pragma unroll
+      for (int x = 0; x < 4; ++x) {
+        int qx = q - x;
+        if (qx < 0) qx += n;
+        float* e = s_en + (qx & 3) * nq + (qx >> 2);
+        *e = fmaf(v[x], v[x], *e);
+      }
+    }
+    __syncthreads();  // the slot's reads and this row's updates done
+    if (tid == 0 && r + kEnRing < r1) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");  // generic reads before the async refill
+      issue(r + kEnRing);
+    }
+  }
+  for (int j = tid; j < n; j += 512) partial[(size_t)blockIdx.x * n + j] = (double)s_en[(j & 3) * nq + (j >> 2)];
+}
+
+static size_t rows4_smem(int n) { return (size_t)(kEnRing + 1) * n * sizeof(float); }
+static int rows4_groups(int n, int* rpc) {
+  const int want = kNumSMs;  // one CTA per SM
+  *rpc = (int)ceil_div(n, std::min(want, n));
+  return (int)ceil_div(n, *rpc);
+}
+static bool rows4_ok(int n) {
+  static const bool off = getenv("APX_EN_ROWS") != nullptr && atoi(getenv("APX_EN_ROWS")) == 0;
+  return !off && n % 4 == 0 && n >= 1024 && rows4_smem(n) <= 200 * 1024;
+}
+
 // energies[j] = sum_g partial[g][j] (fixed order, 8 loads in flight); norms[j] = sqrt(energies[j]).
 // energies[j] = sum_g partial[g][j]; norms[j] = sqrt(energies[j]). A CTA covers 32 columns with
 // 8 slices of the groups (slice s: groups s, s+8, ...), combined in slice order -- a fixed order,
@@ -960,6 +1041,7 @@ size_t cycle_energy_ws_groups(int n, int groups) {
 size_t cycle_energy_ws(int n) {
   int rpc;
   int g = energy_groups(n, &rpc);
+  if (rows4_ok(n)) g = std::max(g, rows4_groups(n, &rpc));
   return (size_t)g * n * sizeof(double) + ceil_div(n, 256) * sizeof(unsigned) + 256;
 }
 
@@ -972,11 +1054,19 @@ int launch_cycle_energies(const T* A, int n, double* energies, double* norms, do
     rpc = (int)ceil_div(n, std::min(groups_override, n));
     groups = (int)ceil_div(n, rpc);
   }
-  const unsigned cb = (unsigned)ceil_div(n, 256);
-  dim3 grid(cb, (unsigned)groups);
-  // separate finalize: the fused last-CTA reduce (counters != nullptr) measured 63 us vs 44 + 7
-  cycle_energy_partial<T><<<grid, 256, 0, st>>>(A, n, rpc, partial, nullptr, energies, norms, n, 0);
-  APX_LAUNCH_CHECK();
+  if (std::is_same<T, float>::value && rows4_ok(n) && groups_override <= 0) {
+    groups = rows4_groups(n, &rpc);
+    const size_t smem = rows4_smem(n);
+    APX_CUDA(cudaFuncSetAttribute(cycle_energy_rows4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    cycle_energy_rows4_kernel<<<(unsigned)groups, 512, smem, st>>>(reinterpret_cast<const float*>(A), n, rpc, partial);
+    APX_LAUNCH_CHECK();
+  } else {
+    const unsigned cb = (unsigned)ceil_div(n, 256);
+    dim3 grid(cb, (unsigned)groups);
+    // separate finalize: the fused last-CTA reduce (counters != nullptr) measured 63 us vs 44 + 7
+    cycle_energy_partial<T><<<grid, 256, 0, st>>>(A, n, rpc, partial, nullptr, energies, norms, n, 0);
+    APX_LAUNCH_CHECK();
+  }
   APX_CUDA(launch_pdl(cycle_energy_finalize, dim3((unsigned)ceil_div(n, 32)), dim3(256), 0, st, partial, n, groups,
                       energies, norms));
   APX_LAUNCH_CHECK();
