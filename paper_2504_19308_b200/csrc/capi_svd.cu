@@ -61,14 +61,18 @@ void plan_side(Workspace& ws, Side& s, int m, int n, int l) {
 // Q (m x l) orthonormal basis of range(A Omega) after q power iterations; Qt = Q^T.
 int range_finder(const double* A, int m, int n, int l, int q, const double* Om, const Side& s, const Dgemm& g,
                  cudaStream_t st) {
+  // the QRs inside the power iteration only carry the subspace to the next product (method 2: one
+  // CholeskyQR pass when the sketch is well conditioned); the last one is the full QR
   APX_TRY(g(A, n, Om, l, s.Y, l, m, l, n, 0, st));
-  APX_TRY((qr_orthonormalize<double, double>(s.Y, l, 1, m, l, s.Q, l, 1, s.Qt, 1, m, s.qr, s.qr_bytes, 0, st)));
+  APX_TRY((qr_orthonormalize<double, double>(s.Y, l, 1, m, l, s.Q, l, 1, s.Qt, 1, m, s.qr, s.qr_bytes, q > 0 ? 2 : 0,
+                                             st)));
   for (int it = 0; it < q; ++it) {
     APX_TRY(g(s.Qt, m, A, n, s.Pt, n, l, n, m, 0, st));  // Pt = Q^T A  (= (A^T Q)^T)
     APX_TRY((qr_orthonormalize<double, double>(s.Pt, 1, n, n, l, s.P, l, 1, (double*)nullptr, 0, 0, s.qr, s.qr_bytes,
-                                               0, st)));
+                                               2, st)));
     APX_TRY(g(A, n, s.P, l, s.Y, l, m, l, n, 0, st));
-    APX_TRY((qr_orthonormalize<double, double>(s.Y, l, 1, m, l, s.Q, l, 1, s.Qt, 1, m, s.qr, s.qr_bytes, 0, st)));
+    APX_TRY((qr_orthonormalize<double, double>(s.Y, l, 1, m, l, s.Q, l, 1, s.Qt, 1, m, s.qr, s.qr_bytes,
+                                               it + 1 < q ? 2 : 0, st)));
   }
   return OK;
 }

@@ -648,8 +648,9 @@ __device__ bool cholinv_blk(const double* __restrict__ G, int l, CholBlkSmem& sm
   __syncthreads();
   APX_CHOL_STAMP(0);
   const double tol = sm.tol;
+  const int nblk = (l + 15) >> 4;  // blocks past l are identity: nothing to eliminate
 #pragma unroll 1
-  for (int k = 0; k < 4; ++k) {
+  for (int k = 0; k < nblk; ++k) {
     const int kb = 16 * k, nr = 48 - kb;
     // (a) the diagonal block on warp 0 by 2 x 2 block pivots: rows j, j + 1 are published together
     //     and every later row eliminates both at once with the pivot block's inverse (one shared
@@ -1575,8 +1576,8 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
                                                                tf32);
     APX_LAUNCH_CHECK();
   } else if (!householder_only && l <= 64 && cqr_fused_ok(m, st)) {
-    // fused CholeskyQR2: one cooperative launch (cqr2_fused_kernel)
-    const double skip_kappa = sizeof(TO) == 4 ? 3.0e4 : 0.0;
+    // fused CholeskyQR2: one cooperative launch (cqr2_fused_kernel); pass-2 rule as below
+    const double skip_kappa = sizeof(TO) == 4 ? 3.0e4 : (method == 2 ? 1.0e4 : 0.0);
     double* part2 = W;  // m l >= parts l^2 doubles
     APX_CUDA(cudaFuncSetAttribute(cqr2_fused_kernel<TI, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                   (int)kCqrSmem));
@@ -1605,7 +1606,10 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
       const char* e = getenv("APX_QR_KAPPA64");
       return e ? atof(e) : 0.0;
     }();
-    const double skip_kappa = sizeof(TO) == 4 ? 3.0e4 : k64;
+    // method 2 (an intermediate QR of a power iteration: only the spanned subspace matters, and a
+    // one-pass Q with ||Q^T Q - I|| ~ u kappa^2 spans it as well as a two-pass one): fp64 outputs
+    // skip pass 2 up to kappa_F = 1e4 too
+    const double skip_kappa = sizeof(TO) == 4 ? 3.0e4 : (method == 2 ? 1.0e4 : k64);
     const int tiles = (int)ceil_div(m, 64);
     APX_TRY(launch_gram<TI>(Y, rs, cs, m, l, flag, part, G, st));
     stage_mark(12, st);  // fine-grained trace markers (bench.py C4 timeline); no-ops unless armed
