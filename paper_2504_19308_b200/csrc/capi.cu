@@ -255,6 +255,12 @@ static int mixed_gemm_splits(int n, int l) {
 // long-lived CTAs, the default). Short-lived CTAs (128-512 groups, several waves) let the QR's
 // single-CTA Cholesky find an SM sooner (it ends 20 us earlier) but the QR's remaining kernels then
 // overlap the pass's HBM traffic and finish no earlier (measured 1118-1142 vs 1128 products/s).
+// CTAs of B's energy pass in the residual plan (row-stream kernel): the SMs the fused QR leaves
+// (qr_sm_footprint), so neither waits for the other's CTAs to drain
+static int resid_energy_ctas(int n) {
+  return std::max(16, device_sms() - qr_sm_footprint(n, 64));
+}
+
 static int resid_energy_groups(int n) {
   static const int env = [] {
     const char* e = getenv("APX_EN_GROUPS");
@@ -640,8 +646,9 @@ static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int
     if (b_after_y == 3) {
       APX_CUDA(cudaStreamWaitEvent(lo, ss->en_done, 0));  // the energy pass ran on hi
     } else {
+      // on the SMs the QR (64 CTAs of two row tiles each at n = 8192) leaves: the two run side by side
       APX_TRY(launch_cycle_energies<float>(B, n, p.en_b, p.nr_b, fb ? scal + APX_S_FRO2_B : nullptr, p.partial, lo,
-                                           en_cps, resid_energy_groups(n)));
+                                           en_cps, resid_energy_groups(n), resid_energy_ctas(n)));
     }
     if (fb) {
       APX_CUDA(cudaMemcpyAsync(sb, fb, kc * sizeof(int), cudaMemcpyDeviceToDevice, lo));

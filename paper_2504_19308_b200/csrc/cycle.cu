@@ -103,14 +103,15 @@ __global__ void __launch_bounds__(256, 8) cycle_energy_partial(const T* __restri
 // 4-byte element per thread and row: 3.9 TB/s at n = 8192; a register-prefetched row stream
 // measured the same -- too few bytes in flight.)
 constexpr int kEnRing = 4;
-__global__ void __launch_bounds__(512, 1) cycle_energy_rows4_kernel(const float* __restrict__ A, int n,
+constexpr int kEnThreads = 512;
+__global__ void __launch_bounds__(kEnThreads, 1) cycle_energy_rows4_kernel(const float* __restrict__ A, int n,
                                                                     int rows_per_chunk, double* __restrict__ partial) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
   const int tid = threadIdx.x, nq = n >> 2;
   float4* ring = reinterpret_cast<float4*>(smem_raw);                  // kEnRing rows of nq float4
   float* s_en = reinterpret_cast<float*>(ring + (size_t)kEnRing * nq);  // n accumulators
   __shared__ __align__(8) uint64_t bars[kEnRing];
-  for (int i = tid; i < n; i += 512) s_en[i] = 0.f;
+  for (int i = tid; i < n; i += kEnThreads) s_en[i] = 0.f;
   const int r0 = blockIdx.x * rows_per_chunk, r1 = min(n, r0 + rows_per_chunk);
   const uint32_t bytes = (uint32_t)nq * 16u;
   auto issue = [&](int r) {  // thread 0: row r into slot (r - r0) % kEnRing
@@ -139,7 +140,7 @@ __global__ void __launch_bounds__(512, 1) cycle_energy_rows4_kernel(const float*
         "r"((uint32_t)((it / kEnRing) & 1))
         : "memory");
     const float4* row = ring + (size_t)slot * nq;
-    for (int c4 = tid; c4 < nq; c4 += 512) {
+    for (int c4 = tid; c4 < nq; c4 += kEnThreads) {
       const float4 v4 = row[c4];
       int q = r - 4 * c4;  // cycle of column 4 c4 (r, 4 c4 < n), minus x for component x
       if (q < 0) q += n;
@@ -158,12 +159,14 @@ __global__ void __launch_bounds__(512, 1) cycle_energy_rows4_kernel(const float*
       issue(r + kEnRing);
     }
   }
-  for (int j = tid; j < n; j += 512) partial[(size_t)blockIdx.x * n + j] = (double)s_en[(j & 3) * nq + (j >> 2)];
+  for (int j = tid; j < n; j += kEnThreads) partial[(size_t)blockIdx.x * n + j] = (double)s_en[(j & 3) * nq + (j >> 2)];
 }
 
 static size_t rows4_smem(int n) { return (size_t)(kEnRing + 1) * n * sizeof(float); }
-static int rows4_groups(int n, int* rpc) {
-  const int want = kNumSMs;  // one CTA per SM
+static int rows4_groups(int n, int* rpc, int ctas = 0) {
+  static const int env = getenv("APX_EN_CTAS") ? atoi(getenv("APX_EN_CTAS")) : 0;  // tuning knob
+  if (env > 0) ctas = env;
+  const int want = ctas > 0 ? std::min(ctas, kNumSMs) : kNumSMs;  // one CTA per SM
   *rpc = (int)ceil_div(n, std::min(want, n));
   return (int)ceil_div(n, *rpc);
 }
@@ -1047,7 +1050,7 @@ size_t cycle_energy_ws(int n) {
 
 template <typename T>
 int launch_cycle_energies(const T* A, int n, double* energies, double* norms, double* fro2, double* partial,
-                          cudaStream_t st, int ctas_per_sm, int groups_override) {
+                          cudaStream_t st, int ctas_per_sm, int groups_override, int rows4_ctas) {
   int rpc;
   int groups = energy_groups(n, &rpc, ctas_per_sm);
   if (groups_override > 0) {  // many short-lived CTAs (several waves), see cycle_energy_ws_groups
@@ -1055,10 +1058,10 @@ int launch_cycle_energies(const T* A, int n, double* energies, double* norms, do
     groups = (int)ceil_div(n, rpc);
   }
   if (std::is_same<T, float>::value && rows4_ok(n) && groups_override <= 0) {
-    groups = rows4_groups(n, &rpc);
+    groups = rows4_groups(n, &rpc, rows4_ctas);
     const size_t smem = rows4_smem(n);
     APX_CUDA(cudaFuncSetAttribute(cycle_energy_rows4_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    cycle_energy_rows4_kernel<<<(unsigned)groups, 512, smem, st>>>(reinterpret_cast<const float*>(A), n, rpc, partial);
+    cycle_energy_rows4_kernel<<<(unsigned)groups, kEnThreads, smem, st>>>(reinterpret_cast<const float*>(A), n, rpc, partial);
     APX_LAUNCH_CHECK();
   } else {
     const unsigned cb = (unsigned)ceil_div(n, 256);
@@ -1392,7 +1395,7 @@ int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st) {
 }
 
 #define APX_INST(T)                                                                                            \
-  template int launch_cycle_energies<T>(const T*, int, double*, double*, double*, double*, cudaStream_t, int, int);     \
+  template int launch_cycle_energies<T>(const T*, int, double*, double*, double*, double*, cudaStream_t, int, int, int);     \
   template int launch_cycle_extract<T>(const T*, int, const int*, int, T*, cudaStream_t, bool);                   \
   template int launch_cycle_materialize<T>(const T*, const int*, int, int, T*, cudaStream_t);                 \
   template int launch_cycle_left_gather<T>(const T*, const T*, const int*, int, int, int, T*, cudaStream_t);  \

@@ -14,9 +14,10 @@ int right_gather_rows_plain(int n, size_t elem, int k);
 int right_gather_seg_rows(int n, size_t elem, int k);
 template <typename T>
 int launch_cycle_energies(const T* A, int n, double* energies, double* norms, double* fro2, double* partial,
-                          cudaStream_t st, int ctas_per_sm = 8, int groups_override = 0);
+                          cudaStream_t st, int ctas_per_sm = 8, int groups_override = 0, int rows4_ctas = 0);
 // top-k selection (select.cuh); optionally fused: *kept = kept_scale * sum_t kept_w[sel[t]]^2 and
 // *total = sum_i tot_w[i]
+int qr_sm_footprint(int m, int l);  // linalg.cu: SMs of the fused CholeskyQR2
 int launch_topk(const double* w, int n, int k, int* sel, cudaStream_t st, const double* kept_w = nullptr,
                 double kept_scale = 1.0, double* kept = nullptr, const double* tot_w = nullptr,
                 double* total = nullptr);

@@ -928,10 +928,15 @@ __global__ void __launch_bounds__(256) apply_x_kernel(const TI* __restrict__ Y, 
 // counter with a bounded wait: a barrier that does not complete within 50 ms (a co-tenant holding
 // SMs) raises the breakdown flag instead, so the Householder kernel that follows recomputes Q.
 // flag: [0] breakdown (-> Householder), [1] pass 2 skipped, [2] barrier counter (zeroed before).
+// X = R^{-1} is written into the Cholesky buffer's left half (dead once the elimination is done),
+// which keeps the CTA at ~121 KB of shared memory: a CTA of B's energy pass (96 KB) fits beside it on
+// the same SM, so the QR and the energy pass that runs concurrently in the C4 plan do not exclude
+// each other's CTAs
+constexpr int kCqrXP = 130;  // = CholBlkSmem::S row pitch
+template <int TPC>
 struct CqrSmem {
-  double Ys[64][kTP];  // the tile [r][i]: Y, then Q1
-  double Xs[64][kTP];  // X = R^{-1} [i][c]
-  CholBlkSmem ch;
+  double Ys[TPC][64][kTP];  // the CTA's tiles [r][i]: Y, then Q1
+  CholBlkSmem ch;           // ch.S[i][0..63] holds X[i][c] after each Cholesky inverse
   int abort;
 };
 
@@ -958,8 +963,9 @@ __device__ __forceinline__ bool cqr_grid_sync(unsigned* ctr, unsigned target, vo
   return *s_abort == 0;
 }
 
-// partial Gram of the staged tile -> part (l x l)
-__device__ __forceinline__ void cqr_gram_tile(const double (*Ys)[kTP], int l, double* __restrict__ part) {
+// partial Gram of the staged tiles -> part (l x l)
+template <int TPC>
+__device__ __forceinline__ void cqr_gram_tile(const double (*Yt)[64][kTP], int l, double* __restrict__ part) {
   const int bi = (threadIdx.x >> 4) * 4, bj = (threadIdx.x & 15) * 4;
   double acc[4][4];
 #pragma unroll
@@ -967,7 +973,9 @@ __device__ __forceinline__ void cqr_gram_tile(const double (*Ys)[kTP], int l, do
 #pragma unroll
     for (int y = 0; y < 4; ++y) acc[x][y] = 0.0;
 #pragma unroll 8
-  for (int r = 0; r < 64; ++r) {
+  for (int rr = 0; rr < 64 * TPC; ++rr) {
+    const double(*Ys)[kTP] = Yt[rr >> 6];
+    const int r = rr & 63;
     const double2 a01 = *reinterpret_cast<const double2*>(&Ys[r][bi]);
     const double2 a23 = *reinterpret_cast<const double2*>(&Ys[r][bi + 2]);
     const double2 b01 = *reinterpret_cast<const double2*>(&Ys[r][bj]);
@@ -1016,8 +1024,8 @@ __device__ __forceinline__ void cqr_reduce_slice(const double* __restrict__ part
   }
 }
 
-// acc = tile . X (4 x 4 per thread: rows tr.., columns tc..)
-__device__ __forceinline__ void cqr_apply_tile(const double (*Ys)[kTP], const double (*Xs)[kTP], double (&acc)[4][4]) {
+// acc = tile . X (4 x 4 per thread: rows tr.., columns tc..); X rows at pitch kCqrXP
+__device__ __forceinline__ void cqr_apply_tile(const double (*Ys)[kTP], const double (*Xs)[kCqrXP], double (&acc)[4][4]) {
   const int tr = (threadIdx.x >> 4) * 4, tc = (threadIdx.x & 15) * 4;
 #pragma unroll
   for (int x = 0; x < 4; ++x)
@@ -1037,7 +1045,7 @@ __device__ __forceinline__ void cqr_apply_tile(const double (*Ys)[kTP], const do
   }
 }
 
-template <typename TI, typename TO>
+template <typename TI, typename TO, int TPC>
 __global__ void __launch_bounds__(256, 1) cqr2_fused_kernel(const TI* __restrict__ Y, int64_t rs, int64_t cs, int m,
                                                             int l, double* __restrict__ part1,
                                                             double* __restrict__ part2, double* __restrict__ G1,
@@ -1046,16 +1054,18 @@ __global__ void __launch_bounds__(256, 1) cqr2_fused_kernel(const TI* __restrict
                                                             TO* __restrict__ Q2, int64_t q2rs, int64_t q2cs, int tf32,
                                                             double skip_kappa) {
   extern __shared__ __align__(16) unsigned char smem_raw[];
-  CqrSmem& sm = *reinterpret_cast<CqrSmem*>(smem_raw);
+  CqrSmem<TPC>& sm = *reinterpret_cast<CqrSmem<TPC>*>(smem_raw);
   unsigned* ctr = reinterpret_cast<unsigned*>(flag + 2);
   const unsigned nb = gridDim.x;
-  const int b = blockIdx.x, r0 = b * 64;
+  const int b = blockIdx.x;
+  const int tr = (threadIdx.x >> 4) * 4, tc = (threadIdx.x & 15) * 4;
   APX_CQR_STAMP(0);
   if (threadIdx.x == 0) sm.abort = 0;
-  load_tile64<false>(Y, rs, cs, m, l, r0, sm.Ys);
+#pragma unroll
+  for (int t = 0; t < TPC; ++t) load_tile64<false>(Y, rs, cs, m, l, (b * TPC + t) * 64, sm.Ys[t]);
   __syncthreads();
   APX_CQR_STAMP(1);
-  cqr_gram_tile(sm.Ys, l, part1 + (size_t)b * l * l);
+  cqr_gram_tile<TPC>(sm.Ys, l, part1 + (size_t)b * l * l);
   APX_CQR_STAMP(2);
   if (!cqr_grid_sync(ctr, nb, &sm.abort)) goto fail;
   APX_CQR_STAMP(3);
@@ -1065,38 +1075,45 @@ __global__ void __launch_bounds__(256, 1) cqr2_fused_kernel(const TI* __restrict
   APX_CQR_STAMP(5);
   {
     bool skip2 = false;
-    if (cholinv_blk(G1, l, sm.ch, &sm.Xs[0][0], kTP, skip_kappa, &skip2)) goto fail;
+    if (cholinv_blk(G1, l, sm.ch, &sm.ch.S[0][0], kCqrXP, skip_kappa, &skip2)) goto fail;
     APX_CQR_STAMP(6);
     double acc[4][4];
-    cqr_apply_tile(sm.Ys, sm.Xs, acc);
-    APX_CQR_STAMP(7);
-    const int tr = (threadIdx.x >> 4) * 4, tc = (threadIdx.x & 15) * 4;
     if (!skip2) {
-      __syncthreads();  // every read of the Y tile done
+      // Q1 = Y X, tile by tile, in place; then pass 2 on the Q1 tiles
 #pragma unroll
-      for (int x = 0; x < 4; ++x)
+      for (int t = 0; t < TPC; ++t) {
+        cqr_apply_tile(sm.Ys[t], sm.ch.S, acc);
+        __syncthreads();  // every read of the tile done
 #pragma unroll
-        for (int y = 0; y < 4; ++y) sm.Ys[tr + x][tc + y] = (tc + y < l) ? acc[x][y] : 0.0;
+        for (int x = 0; x < 4; ++x)
+#pragma unroll
+          for (int y = 0; y < 4; ++y) sm.Ys[t][tr + x][tc + y] = (tc + y < l) ? acc[x][y] : 0.0;
+      }
       __syncthreads();
-      cqr_gram_tile(sm.Ys, l, part2 + (size_t)b * l * l);
+      cqr_gram_tile<TPC>(sm.Ys, l, part2 + (size_t)b * l * l);
       if (!cqr_grid_sync(ctr, 3 * nb, &sm.abort)) goto fail;
       cqr_reduce_slice(part2, nb, l, G2, sm.ch.red_wide());
       if (!cqr_grid_sync(ctr, 4 * nb, &sm.abort)) goto fail;
       bool unused = false;
-      if (cholinv_blk(G2, l, sm.ch, &sm.Xs[0][0], kTP, 0.0, &unused)) goto fail;
-      cqr_apply_tile(sm.Ys, sm.Xs, acc);
+      if (cholinv_blk(G2, l, sm.ch, &sm.ch.S[0][0], kCqrXP, 0.0, &unused)) goto fail;
     }
+    APX_CQR_STAMP(7);
     if (b == 0 && threadIdx.x == 0) flag[1] = skip2 ? 1 : 0;
 #pragma unroll
-    for (int x = 0; x < 4; ++x) {
-      const int r = r0 + tr + x;
-      if (r >= m) continue;
+    for (int t = 0; t < TPC; ++t) {
+      cqr_apply_tile(sm.Ys[t], sm.ch.S, acc);
+      const int r0 = (b * TPC + t) * 64;
 #pragma unroll
-      for (int y = 0; y < 4; ++y) {
-        const int c = tc + y;
-        if (c >= l) continue;
-        if (Q) Q[(size_t)r * qrs + (size_t)c * qcs] = qout<TO>(acc[x][y], tf32);
-        if (Q2) Q2[(size_t)r * q2rs + (size_t)c * q2cs] = qout<TO>(acc[x][y], tf32);
+      for (int x = 0; x < 4; ++x) {
+        const int r = r0 + tr + x;
+        if (r >= m) continue;
+#pragma unroll
+        for (int y = 0; y < 4; ++y) {
+          const int c = tc + y;
+          if (c >= l) continue;
+          if (Q) Q[(size_t)r * qrs + (size_t)c * qcs] = qout<TO>(acc[x][y], tf32);
+          if (Q2) Q2[(size_t)r * q2rs + (size_t)c * q2cs] = qout<TO>(acc[x][y], tf32);
+        }
       }
     }
     return;
@@ -1104,7 +1121,13 @@ __global__ void __launch_bounds__(256, 1) cqr2_fused_kernel(const TI* __restrict
 fail:
   if (threadIdx.x == 0) atomicExch(flag, 1);  // breakdown or barrier timeout: the Householder kernel runs
 }
-constexpr size_t kCqrSmem = sizeof(CqrSmem);
+// tiles per CTA: 2 when the sketch has many row tiles (C4: 64 CTAs instead of 128, so B's concurrent
+// energy pass keeps the other SMs), else 1; APX_QR_TPC overrides
+static int cqr_tpc(int tiles) {
+  static const int env = getenv("APX_QR_TPC") ? atoi(getenv("APX_QR_TPC")) : 0;
+  if (env == 1 || env == 2) return env;
+  return tiles > 96 ? 2 : 1;
+}
 
 // ---- Q = Y R^{-1} by forward substitution q R = y, one warp per row ------------------------
 // Lane c owns columns c, c+32, ...; at step j the owner finalises q_j = acc_j / R_jj and every
@@ -1538,7 +1561,15 @@ static bool cqr_fused_ok(int m, cudaStream_t st) {
   if (off) return false;
   cudaStreamCaptureStatus cap = cudaStreamCaptureStatusNone;
   if (cudaStreamIsCapturing(st, &cap) != cudaSuccess || cap != cudaStreamCaptureStatusNone) return false;
-  return ceil_div(m, 64) <= device_sms();
+  const int tiles = (int)ceil_div(m, 64);
+  return ceil_div(tiles, cqr_tpc(tiles)) <= device_sms();
+}
+
+// SMs the fused QR of an m x l sketch occupies (0 when it takes the unfused chain)
+int qr_sm_footprint(int m, int l) {
+  if (l > 64 || getenv("APX_QR_UNFUSED") != nullptr) return 0;
+  const int tiles = (int)ceil_div(m, 64);
+  return (int)ceil_div(tiles, cqr_tpc(tiles));
 }
 
 template <typename TI, typename TO>
@@ -1579,21 +1610,26 @@ int qr_orthonormalize(const TI* Y, int64_t rs, int64_t cs, int m, int l, TO* Q, 
     // fused CholeskyQR2: one cooperative launch (cqr2_fused_kernel); pass-2 rule as below
     const double skip_kappa = sizeof(TO) == 4 ? 3.0e4 : (method == 2 ? 1.0e4 : 0.0);
     double* part2 = W;  // m l >= parts l^2 doubles
-    APX_CUDA(cudaFuncSetAttribute(cqr2_fused_kernel<TI, TO>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                  (int)kCqrSmem));
-    cudaLaunchConfig_t cfg = {};
-    cfg.gridDim = dim3((unsigned)parts);
-    cfg.blockDim = dim3(256);
-    cfg.dynamicSmemBytes = kCqrSmem;
-    cfg.stream = st;
-    cudaLaunchAttribute attr[1];
-    attr[0].id = cudaLaunchAttributeCooperative;
-    attr[0].val.cooperative = 1;
-    cfg.attrs = attr;
-    cfg.numAttrs = 1;
-    APX_CUDA(cudaLaunchKernelEx(&cfg, cqr2_fused_kernel<TI, TO>, Y, rs, cs, m, l, part, part2, G, Rinv, flag, Q, qrs,
-                                qcs, Q2, q2rs, q2cs, tf32, skip_kappa));
-    APX_LAUNCH_CHECK();
+    const int tpc = cqr_tpc(parts);
+    auto go = [&](auto kern, size_t smem) -> int {
+      APX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = dim3((unsigned)ceil_div(parts, tpc));
+      cfg.blockDim = dim3(256);
+      cfg.dynamicSmemBytes = smem;
+      cfg.stream = st;
+      cudaLaunchAttribute attr[1];
+      attr[0].id = cudaLaunchAttributeCooperative;
+      attr[0].val.cooperative = 1;
+      cfg.attrs = attr;
+      cfg.numAttrs = 1;
+      APX_CUDA(cudaLaunchKernelEx(&cfg, kern, Y, rs, cs, m, l, part, part2, G, Rinv, flag, Q, qrs, qcs, Q2, q2rs, q2cs,
+                                  tf32, skip_kappa));
+      APX_LAUNCH_CHECK();
+      return OK;
+    };
+    if (tpc == 2) APX_TRY(go(cqr2_fused_kernel<TI, TO, 2>, sizeof(CqrSmem<2>)));
+    else APX_TRY(go(cqr2_fused_kernel<TI, TO, 1>, sizeof(CqrSmem<1>)));
     for (int mk = 12; mk <= 15; ++mk) stage_mark(mk, st);
   } else if (!householder_only && l <= 64) {
     // fast path: CholeskyQR with R^{-1}; second pass only when the conditioning requires it

@@ -89,12 +89,12 @@ int main() {
     cudaMalloc(&g2, sizeof(double) * ll * ll);
     cudaMalloc(&fl, 16);
     cudaMemcpy(Yd, hY, sizeof(float) * m * ll, cudaMemcpyHostToDevice);
-    cudaFuncSetAttribute(cqr2_fused_kernel<float, float>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)kCqrSmem);
+    cudaFuncSetAttribute(cqr2_fused_kernel<float, float, 1>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sizeof(CqrSmem<1>));
     float best = 1e9;
     for (int it = 0; it < 10; ++it) {
       cudaMemset(fl, 0, 16);
       cudaEventRecord(a);
-      cqr2_fused_kernel<float, float><<<parts, 256, kCqrSmem>>>(Yd, ll, 1, m, ll, p1, p2, g1, g2, fl, Qd, ll, 1,
+      cqr2_fused_kernel<float, float, 1><<<parts, 256, sizeof(CqrSmem<1>)>>>(Yd, ll, 1, m, ll, p1, p2, g1, g2, fl, Qd, ll, 1,
                                                                 (float*)nullptr, 0, 0, 1, 3e4);
       cudaEventRecord(b);
       cudaEventSynchronize(b);
