@@ -1549,8 +1549,178 @@ __global__ void __launch_bounds__(256, 2) big_dA_win_kernel(const T* __restrict_
   }
 }
 
-// conj(dA) rows [row_base, row_end) into X (rows from row_base on): the windowed kernel when the
-// k windows fit shared memory, else the L2 kernel
+// Same result as big_dA_win_kernel by register blocks: a thread forms an 8-row x 4-column tile
+// (rows r0 + 8 rg + a, columns c0 + 4 cg + b) and the CTA a 32 x 4 kCG tile. Over the thread's tile
+// d = r - c takes only 11 distinct values (a - b in [-3, 7]), so one term costs 11 window loads and
+// 2 twiddle loads (LDS.128) for 32 complex MACs -- the per-column kernel spends 16 + 3 on 16 -- and
+// the column twiddles w_q(c + b) come from w_q(c) by the recurrence w *= w_q(1). The window of term
+// q (W = 32 + 4 kCG - 1 consecutive cyclic indices of S_q) is stored split by j mod 4 at position
+// j >> 2: for a fixed m the lanes' reads j = 4 (2 rg - cg + kCG - 1) + m are consecutive positions of
+// one class, i.e. conflict-free. Terms are staged kKC at a time into two buffers by cp.async (the
+// next chunk lands while this one is multiplied), so any k runs. NW warps per CTA: 4 row groups x
+// NW/4 column halves of 32 column groups; the default NW = 4 (128 x 32 tile, 194 registers) keeps
+// two CTAs per SM so one CTA's staging and epilogue overlap the other's multiplies.
+template <int NW>
+struct DaBlk {
+  static constexpr int kThreads = 32 * NW, kR = 32, kCG = 8 * NW, kC = 4 * kCG, kKC = 8;
+  static constexpr int kW = kR + kC - 1, kP = (kW + 3) / 4;
+  static constexpr size_t kWinBytes = sizeof(double2) * kKC * 4 * kP;
+  static constexpr size_t kTwBytes = sizeof(double2) * kKC * (kCG + 1);
+  static constexpr size_t kSmem = 2 * (kWinBytes + kTwBytes);
+  static constexpr size_t kATile = sizeof(double) * kR * kC;  // real operands: A's tile for the epilogue
+};
+__device__ __forceinline__ void da_cp16(void* dst, const void* src) {
+  asm volatile("cp.async.cg.shared.global [%0], [%1], 16;\n" ::"r"((unsigned)__cvta_generic_to_shared(dst)),
+               "l"(src)
+               : "memory");
+}
+template <typename T, int NW>
+__global__ void __launch_bounds__(32 * NW, 8 / NW) big_dA_blk_kernel(const T* __restrict__ A, int n,
+                                                                  const double2* __restrict__ Ssel,
+                                                                  const int* __restrict__ sel, int k,
+                                                                  const double2* __restrict__ roots,
+                                                                  double2* __restrict__ X, int row_base,
+                                                                  int row_end) {
+  using G = DaBlk<NW>;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  using Win = double2[G::kKC][4][G::kP];
+  using Tw = double2[G::kKC][G::kCG + 1];  // [q][column group g] = w_q(c0 + 4 g); [q][kCG] = w_q(1)
+  Win* win = reinterpret_cast<Win*>(smem_raw);
+  Tw* tw = reinterpret_cast<Tw*>(smem_raw + 2 * G::kWinBytes);
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  const int cg = (warp >> 2) * 32 + lane, rg = warp & 3;
+  const int c0 = blockIdx.x * G::kC, r0 = row_base + blockIdx.y * G::kR;
+  // window entry j of every term is S_q[(r0 - c0 - (kC - 1) + j) mod n]
+  int dbase = (int)(((long long)r0 - c0 - (G::kC - 1)) % n);
+  if (dbase < 0) dbase += n;
+  // the epilogue reads the CTA's tile of A: real operands stage it into shared memory by cp.async
+  // with the first chunk (it lands under the multiplies), complex ones pull it into L2
+  constexpr bool kStageA = std::is_same<T, double>::value;
+  double* As = reinterpret_cast<double*>(smem_raw + G::kSmem);  // [kR][kC] when kStageA
+  if constexpr (kStageA) {
+    const int cols = min(G::kC, n - c0);
+    if ((n & 1) == 0) {
+      for (int e = tid; e < G::kR * (G::kC / 2); e += G::kThreads) {
+        const int rr = e / (G::kC / 2), cc = 2 * (e - rr * (G::kC / 2));
+        if (r0 + rr < row_end && cc < cols) da_cp16(As + rr * G::kC + cc, A + (size_t)(r0 + rr) * n + c0 + cc);
+      }
+    } else {
+      for (int e = tid; e < G::kR * G::kC; e += G::kThreads) {
+        const int rr = e / G::kC, cc = e - rr * G::kC;
+        if (r0 + rr < row_end && cc < cols)
+          asm volatile("cp.async.ca.shared.global [%0], [%1], 8;\n" ::"r"(
+                           (unsigned)__cvta_generic_to_shared(As + rr * G::kC + cc)),
+                       "l"(A + (size_t)(r0 + rr) * n + c0 + cc)
+                       : "memory");
+      }
+    }
+  } else if (tid < G::kR && r0 + tid < row_end) {
+    const T* rowp = A + (size_t)(r0 + tid) * n + c0;
+    const unsigned bytes = (unsigned)(min(G::kC, n - c0) * sizeof(T)) & ~15u;
+    if (((uintptr_t)rowp & 15) == 0 && bytes > 0)
+      asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(rowp), "r"(bytes) : "memory");
+  }
+  // the staging is all cp.async (windows and twiddle-table entries; conj applied at use), indices
+  // wrapped by one conditional subtract when n >= W (a 64-bit modulo per entry was 11% of the stalls)
+  auto stage = [&](int q0, int buf) {
+    const int kc = min(G::kKC, k - q0);
+    if (n >= G::kW) {
+      for (int q = 0; q < kc; ++q) {
+        const double2* Sq = Ssel + (size_t)(q0 + q) * n;
+        for (int j = tid; j < G::kW; j += G::kThreads) {
+          const int d = dbase + j;
+          da_cp16(&win[buf][q][j & 3][j >> 2], Sq + (d >= n ? d - n : d));
+        }
+      }
+    } else {
+      for (int e = tid; e < kc * G::kW; e += G::kThreads) {
+        const int q = e / G::kW, j = e - q * G::kW;
+        da_cp16(&win[buf][q][j & 3][j >> 2], Ssel + (size_t)(q0 + q) * n + (dbase + j) % n);
+      }
+    }
+    for (int e = tid; e < kc * (G::kCG + 1); e += G::kThreads) {
+      const int q = e / (G::kCG + 1), g = e - q * (G::kCG + 1);
+      int c = g < G::kCG ? c0 + 4 * g : 1;
+      if (c >= n) c %= n;
+      da_cp16(&tw[buf][q][g], roots + mulmod_n(__ldg(sel + q0 + q), c, n));  // conj: exp(+2 pi i t c / n)
+    }
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+  };
+  double2 ah[8][4];
+#pragma unroll
+  for (int a = 0; a < 8; ++a)
+#pragma unroll
+    for (int b = 0; b < 4; ++b) ah[a][b] = make_double2(0.0, 0.0);
+  // j(a, b) = 8 rg + a - 4 cg - b + kC - 1 = 4 pbase + (a - b + 3)
+  const int pbase = 2 * rg + G::kCG - 1 - cg;
+  if (k > 0) stage(0, 0);
+  for (int q0 = 0, it = 0; q0 < k; q0 += G::kKC, ++it) {
+    const int buf = it & 1;
+    if (q0 + G::kKC < k) {
+      stage(q0 + G::kKC, buf ^ 1);
+      asm volatile("cp.async.wait_group 1;\n" ::: "memory");
+    } else {
+      asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    }
+    __syncthreads();
+    const int kc = min(G::kKC, k - q0);
+    for (int q = 0; q < kc; ++q) {
+      double2 v[11];
+#pragma unroll
+      for (int m = 0; m < 11; ++m) v[m] = win[buf][q][m & 3][pbase + (m >> 2)];
+      double2 w[4];
+      w[0] = cconj(tw[buf][q][cg]);
+      const double2 w1 = cconj(tw[buf][q][G::kCG]);
+#pragma unroll
+      for (int b = 1; b < 4; ++b) w[b] = cmul(w[b - 1], w1);
+#pragma unroll
+      for (int a = 0; a < 8; ++a)
+#pragma unroll
+        for (int b = 0; b < 4; ++b) ah[a][b] = cmac(ah[a][b], v[a - b + 3], w[b]);
+    }
+    __syncthreads();  // buffer buf is restaged two chunks on
+  }
+  if (k <= 0) {  // nothing staged a window: the A tile's copies still need their wait
+    asm volatile("cp.async.commit_group;\n" ::: "memory");
+    asm volatile("cp.async.wait_group 0;\n" ::: "memory");
+    __syncthreads();
+  }
+  // epilogue: all of the tile's A loads first (the stores' asm would otherwise order each row's
+  // loads behind the previous row's stores), then conj(A - Ahat) out as 32-byte stores
+  const int cb = c0 + 4 * cg;
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int r = r0 + 8 * rg + a;
+#pragma unroll
+    for (int b = 0; b < 4; ++b)
+      if (r < row_end && cb + b < n) {
+        double2 x;
+        if constexpr (kStageA) x = make_double2(As[(8 * rg + a) * G::kC + 4 * cg + b], 0.0);
+        else x = ld_c<T>(A, (size_t)r * n + cb + b);
+        ah[a][b] = cconj(csub(x, ah[a][b]));
+      }
+  }
+#pragma unroll
+  for (int a = 0; a < 8; ++a) {
+    const int r = r0 + 8 * rg + a;
+    if (r >= row_end) continue;
+    double2* dst = X + (size_t)(r - row_base) * n + cb;
+    if (cb + 3 < n && (((uintptr_t)dst) & 31) == 0) {
+#pragma unroll
+      for (int h = 0; h < 2; ++h)
+        asm volatile("st.global.v4.f64 [%0], {%1, %2, %3, %4};" ::"l"(dst + 2 * h), "d"(ah[a][2 * h].x),
+                     "d"(ah[a][2 * h].y), "d"(ah[a][2 * h + 1].x), "d"(ah[a][2 * h + 1].y)
+                     : "memory");
+    } else {
+#pragma unroll
+      for (int b = 0; b < 4; ++b)
+        if (cb + b < n) dst[b] = ah[a][b];
+    }
+  }
+}
+
+// conj(dA) rows [row_base, row_end) into X (rows from row_base on): the register-blocked kernel
+// (any k); APX_DA_KERNEL=win|l2 selects the earlier per-column kernels for A/B timing
 template <typename T>
 static int launch_big_dA(const T* A, int n, const double2* Ssel, const int* sel, int k, const double2* roots,
                          double2* X, int row_base, int row_end, cudaStream_t st) {
@@ -1560,7 +1730,24 @@ static int launch_big_dA(const T* A, int n, const double2* Ssel, const int* sel,
     const char* e = getenv("APX_DA_ROWS");
     return (e && atoi(e) == 32) ? 32 : 16;
   }();
-  if (k <= kDaWinMaxK && n >= 256 && getenv("APX_DA_L2") == nullptr) {
+  static const int da_kind = [] {
+    const char* e = getenv("APX_DA_KERNEL");
+    if (getenv("APX_DA_L2")) return 2;
+    return !e ? 0 : (strcmp(e, "win") == 0 ? 1 : strcmp(e, "l2") == 0 ? 2 : 0);
+  }();
+  if (da_kind == 0) {
+    auto go = [&](auto kern, auto geom) -> int {
+      using G = decltype(geom);
+      const size_t smem = G::kSmem + (std::is_same<T, double>::value ? G::kATile : 0);
+      APX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+      const dim3 g((unsigned)ceil_div(n, G::kC), (unsigned)ceil_div(row_end - row_base, G::kR));
+      kern<<<g, G::kThreads, smem, st>>>(A, n, Ssel, sel, k, roots, X, row_base, row_end);
+      return OK;
+    };
+    static const bool wide = getenv("APX_DA_WIDE") != nullptr;  // 256-thread CTAs (one per SM)
+    if (wide) APX_TRY(go(big_dA_blk_kernel<T, 8>, DaBlk<8>{}));
+    else APX_TRY(go(big_dA_blk_kernel<T, 4>, DaBlk<4>{}));
+  } else if (da_kind == 1 && k <= kDaWinMaxK && n >= 256) {
     auto go = [&](auto kern, int rows) -> int {
       const size_t smem = (size_t)std::max(k, 1) * (256 + rows - 1) * sizeof(double2);
       APX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
