@@ -89,8 +89,12 @@ __global__ void __launch_bounds__(GLOBAL ? 1024 : 512)
         // circle method: position 0 fixed, others rotate
         int a = 0, b = 1;
         if (active) {
-          a = (pr == 0) ? 0 : 1 + (pr - 1 + round) % (le - 1);
-          b = 1 + (le - 2 - pr + round) % (le - 1);
+          // (x) mod (le - 1) for 0 <= x < 2 (le - 1): one conditional subtract instead of a division
+          int xa = pr - 1 + round, xb = le - 2 - pr + round;
+          if (xa >= le - 1) xa -= le - 1;
+          if (xb >= le - 1) xb -= le - 1;
+          a = (pr == 0) ? 0 : 1 + xa;
+          b = 1 + xb;
           if (a > b) { const int t = a; a = b; b = t; }
         }
         double* wa = Wc + (size_t)a * l;
@@ -102,6 +106,8 @@ __global__ void __launch_bounds__(GLOBAL ? 1024 : 512)
         constexpr int kR = GLOBAL ? 1 : KR;
         double xw[kR], yw[kR], xv[kR], yv[kR];
         double ga = 0.0;
+        // the pair's carried squared norms: loaded ahead of the dot product's reduction
+        const double al = active ? nrm2[a] : 0.0, be = active ? nrm2[b] : 0.0;
         if (GLOBAL) {
           if (active)
             for (int i = hl; i < l; i += 16) ga = fma(wa[i], wb[i], ga);
@@ -118,11 +124,14 @@ __global__ void __launch_bounds__(GLOBAL ? 1024 : 512)
         }
 #pragma unroll
         for (int o = 8; o > 0; o >>= 1) ga += __shfl_xor_sync(0xffffffffu, ga, o);
-        const double al = active ? nrm2[a] : 0.0, be = active ? nrm2[b] : 0.0;
         if (active && ga != 0.0 && ga * ga > tol2 * al * be) {
-          const double zeta = (be - al) * svd_rcp(2.0 * fabs(ga)) * (ga > 0.0 ? 1.0 : -1.0);
-          const double z2 = fma(zeta, zeta, 1.0);
-          const double t = (zeta >= 0.0 ? 1.0 : -1.0) * svd_rcp(fabs(zeta) + z2 * svd_rsqrt(z2));
+          // t = tan(theta) = sign(zeta) / (|zeta| + sqrt(1 + zeta^2)), zeta = (be - al) / (2 ga),
+          // written as sign(d) g2 / (|d| + hypot(d, g2)) with d = be - al, g2 = 2 ga: three
+          // dependent rcp/rsqrt chains instead of four (the rotation is every round's critical path)
+          const double d = be - al, g2 = 2.0 * ga;
+          const double h2 = fma(d, d, g2 * g2);
+          const double hyp = h2 > 1e-290 ? h2 * svd_rsqrt(h2) : hypot(d, g2);  // (squares underflow)
+          const double t = (d >= 0.0 ? g2 : -g2) * svd_rcp(fabs(d) + hyp);
           const double c = svd_rsqrt(fma(t, t, 1.0)), sn = c * t;
           if (GLOBAL) {
             for (int i = hl; i < l; i += 16) {
@@ -239,7 +248,10 @@ int launch_small_svd(const double* W, int l, double* U, double* S, double* V, do
   const size_t smem = ((size_t)le * l + (size_t)le * le) * sizeof(double);
   auto go = [&](auto kern) -> int {
     APX_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<1, 512, smem, st>>>(W, l, U, S, V, VT, nullptr);
+    // one half-warp per column pair of a round: ceil(le / 4) warps (a 40-wide sketch: 10 warps, no
+    // idle warps in the per-round barrier)
+    const int threads = std::min(512, std::max(64, 32 * ((le / 2 + 1) / 2)));
+    kern<<<1, threads, smem, st>>>(W, l, U, S, V, VT, nullptr);
     APX_LAUNCH_CHECK();
     return OK;
   };
