@@ -727,10 +727,12 @@ static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int
   const int wchunks = std::max(1, std::min(8, (int)ceil_div(5 * free_sms, wblocks)));
   APX_TRY(UmmaStages::bm_times_db(B, Bm, W, part, n, l, nullptr, 0, lo, free_sms));
   stage_mark(9, lo);
-  APX_TRY(launch_cycle_right_gather<float>(Bm, nullptr, 0, lb, sb, kc, n, l, -1, W, nullptr, nullptr, lo, true, 0,
-                                           nullptr, wchunks, /*tf32_operands=*/true));
+  // W0 - Bm.Bhat_tf32 + Bm.Bhat as ONE gather over lambda - tf32(lambda): Bm is TF32-exact (the
+  // finalize rounded it), so the TF32 and fp32 gathers differ only in lambda's truncated bits (two
+  // gathers, each a few waves of 192 KB CTAs on the SMs the f16 gather leaves, were 163 us of the
+  // low-priority chain, which sets the product's end)
   APX_TRY(launch_cycle_right_gather<float>(Bm, nullptr, 0, lb, sb, kc, n, l, 1, W, nullptr, nullptr, lo, true, 0,
-                                           nullptr, wchunks, /*tf32_operands=*/false));
+                                           nullptr, wchunks, /*tf32_operands=*/2));
   APX_TRY(launch_split_tf32(W, (size_t)l * n, p.W2, lo));
   stage_mark(6, lo);
   // one tile per CTA (3 CTAs per SM on the SMs the gather leaves free). APX_QW_PERSIST=1: the

@@ -406,11 +406,13 @@ constexpr int kGatherThreads = APX_GATHER_THREADS;
 
 // TRUNC (fp32 only): operands truncated to TF32 (low 13 mantissa bits cleared) exactly as the
 // tcgen05 kind::tf32 datapath reads them, so subtracting this gather from a TF32 GEMM over the
-// same operands cancels the kept part exactly (up to fp32 summation order).
+// same operands cancels the kept part exactly (up to fp32 summation order). TM = 2 (DELTA): lambda
+// replaced by lambda - tf32(lambda), X as is -- for a TF32-exact X (the residual plan's Bm) this is
+// the difference of the plain and the TRUNC gathers in one pass.
 __device__ __forceinline__ float tf32_trunc(float x) { return __uint_as_float(__float_as_uint(x) & 0xffffe000u); }
 __device__ __forceinline__ double tf32_trunc(double x) { return x; }
 
-template <typename T, int R, bool FAST, bool TRUNC = false>
+template <typename T, int R, bool FAST, int TM = 0>
 __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T* __restrict__ X, const int* __restrict__ JA, int ka,
                                                           const T* __restrict__ lam, const int* __restrict__ J, int k,
                                                           int n, int m_rows, int accumulate, T* __restrict__ M,
@@ -418,6 +420,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
                                                           double* __restrict__ xsq_partial, int* __restrict__ ticket,
                                                           int* __restrict__ ready, int x_early, int row_off,
                                                           const int* __restrict__ skip_if) {
+  constexpr bool TRUNC = TM == 1, DELTA = TM == 2 && sizeof(T) == 4;
   if (skip_if != nullptr && *skip_if != 0) return;  // a gated-off launch (the C4 residual plan's fallback)
   constexpr int RP = gather_pitch(R, sizeof(T));
   // x_early: X (and the ticket / ready flags) predate the previous kernel of the stream, so under
@@ -575,6 +578,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
               mm[u][q] = (int)m;
               lv[u][q] = ldg_nc_ordered(lrow + c);
               if constexpr (TRUNC) lv[u][q] = tf32_trunc(lv[u][q]);
+              if constexpr (DELTA) lv[u][q] = lv[u][q] - tf32_trunc(lv[u][q]);
             } else {
               int m = c + jt;
               m = m >= n ? m - n : m;
@@ -582,6 +586,7 @@ __global__ void __launch_bounds__(kGatherThreads, 1) cycle_right_gather(const T*
               mm[u][q] = ok ? m * RP : 0;
               lv[u][q] = ok ? __ldg(lrow + c) : T(0);
               if constexpr (TRUNC) lv[u][q] = tf32_trunc(lv[u][q]);
+              if constexpr (DELTA) lv[u][q] = lv[u][q] - tf32_trunc(lv[u][q]);
             }
           }
         }
@@ -1226,7 +1231,7 @@ int launch_cycle_left_gather_rows(const T* X, const T* lam, const int* J, int k,
 template <typename T, int R>
 static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int m_rows,
                           int acc, T* M, double* msq_partial, double* xsq_partial, bool lam_padded, int max_ctas,
-                          int* ticket, int col_chunks, bool trunc, int* ready, bool x_early, int row_off,
+                          int* ticket, int col_chunks, int trunc, int* ready, bool x_early, int row_off,
                           cudaStream_t st, const int* skip_if = nullptr) {
   constexpr int U = APX_GATHER_U, CPT = APX_GATHER_CPT;
   const int kp = (int)ceil_div(std::max(k, 1), U) * U;
@@ -1261,10 +1266,12 @@ static int right_gather_r(const T* X, const int* JA, int ka, const T* lam, const
     return OK;
   };
   if (fast) {
-    if (trunc && sizeof(T) == 4) return go(cycle_right_gather<T, R, true, true>);
+    if (trunc == 1 && sizeof(T) == 4) return go(cycle_right_gather<T, R, true, 1>);
+    if (trunc == 2 && sizeof(T) == 4) return go(cycle_right_gather<T, R, true, 2>);
     return go(cycle_right_gather<T, R, true>);
   }
-  if (trunc && sizeof(T) == 4) return go(cycle_right_gather<T, R, false, true>);
+  if (trunc == 1 && sizeof(T) == 4) return go(cycle_right_gather<T, R, false, 1>);
+  if (trunc == 2 && sizeof(T) == 4) return go(cycle_right_gather<T, R, false, 2>);
   return go(cycle_right_gather<T, R, false>);
 }
 
@@ -1322,12 +1329,13 @@ static int right_gather_seg_r(const T* X, const int* JA, int ka, const T* lam, c
 // lam: the column-aligned table (cycle_extract<T, true>), k x n, or (lam_padded) ceil(k/8)*8 x n
 // with zero rows past k -- enables the fast path. accumulate: 0 M = X.Bhat, 1 M += X.Bhat,
 // -1 M -= X.Bhat. max_ctas + ticket: persistent grid; col_chunks: split the columns over CTAs;
-// tf32_operands (fp32 fast path): X and lambda truncated to TF32 (see cycle_right_gather).
+// tf32_operands (fp32): 1 = X and lambda truncated to TF32, 2 = lambda - tf32(lambda) (see
+// cycle_right_gather).
 template <typename T>
 int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n,
                               int m_rows, int accumulate, T* M, double* msq_partial, double* xsq_partial,
                               cudaStream_t st, bool lam_padded, int max_ctas, int* ticket, int col_chunks,
-                              bool tf32_operands, int* ready, bool x_early, int row_off, const int* skip_if) {
+                              int tf32_operands, int* ready, bool x_early, int row_off, const int* skip_if) {
   const int rs = right_gather_seg_rows(n, sizeof(T), k);
   if (rs > 0 && !(max_ctas > 0 && ticket) && ready == nullptr && !(tf32_operands && sizeof(T) == 4)) {
     switch (rs) {
@@ -1400,7 +1408,7 @@ int launch_sum_vector(const double* v, int n, double* out, cudaStream_t st) {
   template int launch_cycle_materialize<T>(const T*, const int*, int, int, T*, cudaStream_t);                 \
   template int launch_cycle_left_gather<T>(const T*, const T*, const int*, int, int, int, T*, cudaStream_t);  \
   template int launch_cycle_right_gather<T>(const T*, const int*, int, const T*, const int*, int, int, int, int, T*, \
-                                            double*, double*, cudaStream_t, bool, int, int*, int, bool, int*, bool, int, const int*); \
+                                            double*, double*, cudaStream_t, bool, int, int*, int, int, int*, bool, int, const int*); \
   template int launch_sumsq<T>(const T*, size_t, double*, int*, cudaStream_t);                               \
   template int launch_cycle_energies_rows<T>(const T*, int, int, int, double*, double*, cudaStream_t);       \
   template int launch_cycle_extract_rows<T>(const T*, int, int, int, const int*, int, T*, cudaStream_t);      \

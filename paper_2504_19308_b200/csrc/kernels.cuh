@@ -33,7 +33,7 @@ template <typename T>
 int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n, int m_rows,
                               int accumulate, T* M, double* msq_partial, double* xsq_partial, cudaStream_t st,
                               bool lam_padded = false, int max_ctas = 0, int* ticket = nullptr, int col_chunks = 1,
-                              bool tf32_operands = false, int* ready = nullptr, bool x_early = false,
+                              int tf32_operands = 0, int* ready = nullptr, bool x_early = false,
                               int row_off = 0, const int* skip_if = nullptr);
 // ---- row-sharded cycle product (local rows [0, m) of an n x n operand = global rows row_off + r)
 template <typename T>
