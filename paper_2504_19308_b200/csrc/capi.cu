@@ -57,6 +57,7 @@ struct CyclePlan {
   bool left_t;       // A_hat . X evaluated as (X^T A_hat^T)^T with the right gather
   double* msq;       // ||M||^2 partials
   int n_msq;
+  unsigned short* lam_h;  // f16 lambda' table of the f16-staged residual gather (fp32, large n)
 };
 
 static void plan_cycle(Workspace& ws, CyclePlan& p, int dtype, int n, int ka, int kb, int order) {
@@ -75,6 +76,9 @@ static void plan_cycle(Workspace& ws, CyclePlan& p, int dtype, int n, int ka, in
   p.jneg = ws.take<int>((size_t)pad8(ka));
   p.n_msq = std::max<int>((int)ceil_div(n, 1), kNumSMs * 4);
   p.msq = ws.take<double>(p.n_msq);
+  p.lam_h = (dtype == F32 && order == 1 && ka > 0 && right_gather_seg_rows(n, 4, kb) > 0)
+                ? (unsigned short*)ws.take<char>(right_gather_seg_f16_ws(n, kb))
+                : nullptr;
 }
 
 template <typename T>
@@ -114,7 +118,13 @@ static int run_cycle(const T* A, const T* B, int n, int ka, int kb, int order, c
     APX_TRY(left_product(B, M));
     stage_mark(2, st);
     // M += dA . Bhat (right gather over row blocks of A, masked to dA on load) + ||M||^2
-    APX_TRY(launch_cycle_right_gather<T>(A, sa, ka, lb, sb, kb, n, n, 1, M, p.msq, nullptr, st, true));
+    // (large fp32 n: staged as scaled f16 when dA is a small residual -- cycle.cu K11h)
+    if (p.lam_h != nullptr && right_gather_seg_f16_ok(n, sizeof(T), kb))
+      APX_TRY(launch_cycle_right_gather_seg_f16((const float*)A, sa, ka, (const float*)lb, sb, kb, n, n, 1, (float*)M,
+                                                p.msq, st, 0, p.lam_h, scal + APX_S_FRO2_A, scal + APX_S_KEPT_A,
+                                                scal + APX_S_FRO2_B));
+    else
+      APX_TRY(launch_cycle_right_gather<T>(A, sa, ka, lb, sb, kb, n, n, 1, M, p.msq, nullptr, st, true));
     stage_mark(3, st);
     const int rblocks = (int)ceil_div(n, right_gather_rows_plain(n, sizeof(T), kb));
     APX_TRY(launch_sum_vector(p.msq, rblocks, scal + APX_S_FRO2_M, st));
@@ -142,6 +152,7 @@ struct CycleRowsPlan {
   void *lam_a, *lam_b, *bhat, *xt, *tt;
   int *jneg;
   bool left_t;
+  unsigned short* lam_h;
 };
 
 static void plan_cycle_rows(Workspace& ws, CycleRowsPlan& p, int dtype, int n, int m, int ka, int kb, int order) {
@@ -158,6 +169,9 @@ static void plan_cycle_rows(Workspace& ws, CycleRowsPlan& p, int dtype, int n, i
   p.xt = p.left_t ? (void*)ws.take<char>((size_t)n * n * e) : nullptr;
   p.tt = p.left_t ? (void*)ws.take<char>((size_t)n * m * e) : nullptr;
   p.jneg = ws.take<int>((size_t)pad8(ka));
+  p.lam_h = (dtype == F32 && order == 1 && ka > 0 && right_gather_seg_rows(n, 4, kb) > 0)
+                ? (unsigned short*)ws.take<char>(right_gather_seg_f16_ws(n, kb))
+                : nullptr;
 }
 
 __global__ void sqrt_vector_kernel(const double* __restrict__ e, int n, double* __restrict__ out) {
@@ -201,8 +215,13 @@ static int run_cycle_rows(int phase, const T* A, int m, int r0, const T* B, int 
   }
   if (order == 1) {
     // M_rows += dA_rows . Bhat (A's kept cycles masked on load, global row r0 + r) + ||M_g||^2
-    APX_TRY(launch_cycle_right_gather<T>(A, sa, ka, lb, sb, kb, n, m, 1, M, p.msq, nullptr, st, true, 0, nullptr, 1,
-                                         false, nullptr, false, r0));
+    if (p.lam_h != nullptr && right_gather_seg_f16_ok(n, sizeof(T), kb))
+      APX_TRY(launch_cycle_right_gather_seg_f16((const float*)A, sa, ka, (const float*)lb, sb, kb, n, m, 1, (float*)M,
+                                                p.msq, st, r0, p.lam_h, scal + APX_S_FRO2_A, scal + APX_S_KEPT_A,
+                                                scal + APX_S_FRO2_B));
+    else
+      APX_TRY(launch_cycle_right_gather<T>(A, sa, ka, lb, sb, kb, n, m, 1, M, p.msq, nullptr, st, true, 0, nullptr, 1,
+                                           false, nullptr, false, r0));
     const int rblocks = (int)ceil_div(m, right_gather_rows_plain(n, sizeof(T), kb));
     APX_TRY(launch_sum_vector(p.msq, rblocks, red_out, st));
   } else {

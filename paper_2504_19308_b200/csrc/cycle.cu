@@ -744,12 +744,50 @@ __device__ __forceinline__ int lower_index(const int2* tab, int k, int v, int fr
   return a;
 }
 
-template <typename T, int R>
+// residual-energy rule of the f16 plans (mixed_f16.cu kResidF16MaxEnergy): the masked operand
+// X - Xhat carries at most 1% of ||X||^2, so f16 rounding of it (2^-11 relative) stays below
+// ~4e-5 of the product
+__device__ __forceinline__ bool resid_small(const double* fro2, const double* kept) {
+  const double f = *fro2, kp = *kept;
+  return f > 0.0 && f < 1e300 && (f - kp) <= 0.01 * f;
+}
+
+// lower_index for a converged warp and a short table: every lane counts its entries below v
+// (independent loads) and one warp reduction adds them -- ~60 cycles instead of log2(k)
+// dependent shared-memory round trips (16% of the f16 segmented gather's stall samples)
+__device__ __forceinline__ int count_below(const int2* tab, int k, int v) {
+  int c = 0;
+  for (int i = threadIdx.x & 31; i < k; i += 32) c += tab[i].x < v ? 1 : 0;
+  return __reduce_add_sync(0xffffffffu, c);
+}
+__device__ __forceinline__ void red_add(float* a, float v) {
+  asm volatile("red.relaxed.gpu.global.add.f32 [%0], %1;" ::"l"(a), "f"(v) : "memory");
+}
+__device__ __forceinline__ void red_add(double* a, double v) {
+  asm volatile("red.relaxed.gpu.global.add.f64 [%0], %1;" ::"l"(a), "d"(v) : "memory");
+}
+__device__ __forceinline__ float ld_relaxed_f32(const float* a) {
+  float v;
+  asm volatile("ld.relaxed.gpu.global.f32 %0, [%1];" : "=f"(v) : "l"(a) : "memory");
+  return v;
+}
+__device__ __forceinline__ float ld_relaxed(const float* a) { return ld_relaxed_f32(a); }
+__device__ __forceinline__ double ld_relaxed(const double* a) {
+  double v;
+  asm volatile("ld.relaxed.gpu.global.f64 %0, [%1];" : "=d"(v) : "l"(a) : "memory");
+  return v;
+}
+
+template <typename T, int R, int TUNE>
 __global__ void __launch_bounds__(kSegThreads, 1)
     cycle_right_gather_seg(const T* __restrict__ X, const int* __restrict__ JA, int ka, const T* __restrict__ lam,
                            const int* __restrict__ J, int k, int n, int m_rows, int accumulate, T* __restrict__ M,
                            double* __restrict__ msq_partial, double* __restrict__ xsq_partial, int SW, int row_off,
-                           int c_lo, int c_hi, int lam_ld, int out_ld) {
+                           int c_lo, int c_hi, int lam_ld, int out_ld, const double* __restrict__ g_fro2,
+                           const double* __restrict__ g_kept) {
+  // the f16-staged variant (cycle_right_gather_seg_h) takes the product when the masked operand is
+  // a small residual; this kernel is then its no-op twin (same device-side decision, no host sync)
+  if (g_fro2 != nullptr && resid_small(g_fro2, g_kept)) return;
   constexpr int RP = gather_pitch(R, sizeof(T));
   constexpr int CPT = seg_cpt<T>();
   constexpr int NP = (sizeof(T) == 4) ? R / 2 : 0;
@@ -828,15 +866,16 @@ __global__ void __launch_bounds__(kSegThreads, 1)
       //  boundary: the window straddles a segment end (m0 in [s0 - CW + 1, s0) or
       //            (s0 + sw - CW, s0 + sw)): per-lane checks, ~2 such shifts per chunk over the sweep.
       // Each is a cyclic interval of J values, i.e. a cyclic run of the sorted table.
+      auto lower = [&](int v) -> int { return (k <= 256 && (TUNE & 2)) ? count_below(sJT, k, v) : lower_index(sJT, k, v, 0); };
       auto run = [&](int v, int len, int& first) -> int {  // J in [v, v + len) mod n, len < n
         v %= n;
         if (v < 0) v += n;
-        first = lower_index(sJT, k, v, 0);
+        first = lower(v);
         int cnt;
         if (v + len <= n) {
-          cnt = lower_index(sJT, k, v + len, first) - first;
+          cnt = lower(v + len) - first;
         } else {
-          cnt = (k - first) + min(lower_index(sJT, k, v + len - n, 0), first);
+          cnt = (k - first) + min(lower(v + len - n), first);
         }
         if (first >= k) first -= k;  // every shift is below v: the run starts at index 0
         return cnt;
@@ -845,8 +884,14 @@ __global__ void __launch_bounds__(kSegThreads, 1)
       const int c_int = run(s0 - cw, sw - CW + 1, f_int);
       const int n_blo = run(s0 - CW + 1 - cw, CW - 1, f_lo);
       const int n_bhi = nseg > 1 ? run(s0 + sw - CW + 1 - cw, CW - 1, f_hi) : 0;
-      // the chunk's M lines toward L2 (read back by the epilogue)
-      if (s > 0 || accumulate != 0) {
+      // A segment that is neither the first of an overwriting pass nor the last adds its partial
+      // sums with fire-and-forget reductions at L2 (red.add: no old value to wait for -- the
+      // epilogue's load stalls were ~17% of the samples); the last segment needs the final values
+      // for ||M||^2 and reads them back (relaxed loads: program order behind this thread's own
+      // reductions on the same addresses). Otherwise: the chunk's M lines toward L2.
+      const bool rmw = s > 0 || accumulate != 0;
+      const bool red = rmw && !last && (TUNE & 1);
+      if (rmw && !red) {
 #pragma unroll
         for (int q = 0; q < CPT; ++q)
 #pragma unroll
@@ -942,8 +987,8 @@ __global__ void __launch_bounds__(kSegThreads, 1)
       for (int q = 0; q < CPT; ++q)
 #pragma unroll
         for (int rr = 0; rr < R; ++rr)
-          old[q][rr] = (rr < rows && (s > 0 || accumulate != 0))
-                           ? ldg_hint(M + (size_t)(r0 + rr) * out_ld + (cw - c_lo) + 32 * q + lane, pol_stream)
+          old[q][rr] = (rr < rows && rmw && !red)
+                           ? ld_relaxed(M + (size_t)(r0 + rr) * out_ld + (cw - c_lo) + 32 * q + lane)
                            : T(0);
 #pragma unroll
       for (int q = 0; q < CPT; ++q)
@@ -961,9 +1006,14 @@ __global__ void __launch_bounds__(kSegThreads, 1)
             a = accs[q][rr];
           }
           if (rr < rows) {
-            const T v = accumulate < 0 ? old[q][rr] - a : old[q][rr] + a;
-            stg_hint(M + (size_t)(r0 + rr) * out_ld + (cw - c_lo) + 32 * q + lane, v, pol_stream);
-            if (last) msq += (double)v * (double)v;
+            T* mp = M + (size_t)(r0 + rr) * out_ld + (cw - c_lo) + 32 * q + lane;
+            if (red) {
+              red_add(mp, accumulate < 0 ? -a : a);
+            } else {
+              const T v = accumulate < 0 ? old[q][rr] - a : old[q][rr] + a;
+              stg_hint(mp, v, pol_stream);
+              if (last) msq += (double)v * (double)v;
+            }
           }
         }
     }
@@ -971,6 +1021,269 @@ __global__ void __launch_bounds__(kSegThreads, 1)
   if (xsq_partial != nullptr) {
     const double t = block_sum(xs, red);
     if (threadIdx.x == 0) xsq_partial[blockIdx.x] = t;
+  }
+  if (msq_partial != nullptr) {
+    const double t = block_sum(msq, red);
+    if (threadIdx.x == 0) msq_partial[blockIdx.x] = t;
+  }
+}
+
+// ------------------------------------------------------------------------------------------
+// K11h: the segmented gather over a small masked residual, staged as scaled f16 (fp32 only).
+// The order-1 cycle product's second term dX . Bhat (dX = X with its kept cycles masked on load)
+// is a small part of M whenever the kept cycles carry the operand (C5: 1.6% of ||A||_F), so --
+// as in the C4 residual plan (mixed_f16.cu) -- dX is staged as 2^(15 - e_X) dX in f16 (e_X from
+// ||X||_F: no entry can overflow, masked or not) and the kept diagonals of B as 2^(15 - e_B)
+// lambda' in f16 (a k x n table made once per product); products are f16 x f16 with fp32
+// accumulation (fma.rn.f32.f16), rescaled by 2^(e_X + e_B - 30) once per output and segment.
+// Shared memory holds 8 rows x SW columns as one 16-byte vector per column: a warp's load of 32
+// columns is 4 wavefronts for 256 FMAs (the fp32 kernel at R = 6: 6 for 192), plus one 64-byte
+// lambda' wavefront per 16 loads (thread-order f16 table, 8 bytes per shift); the segment is twice as wide, so M is read-modified-written
+// 3 times instead of 5 at n = 32768. Runs only when resid_small() holds (device-side decision;
+// cycle_right_gather_seg is launched behind it as the fallback and returns at once otherwise).
+// Accumulation order per output: segments ascending, in a segment the sorted interior run and
+// then the two boundary runs -- independent of the row blocking, so row-sharded runs reproduce
+// the single-device bits.
+// ------------------------------------------------------------------------------------------
+constexpr int kSegHR = 8;
+
+__device__ __forceinline__ float fhfma_seg(unsigned short a, unsigned short b, float c) {
+  float d;
+  asm("fma.rn.f32.f16 %0, %1, %2, %3;" : "=f"(d) : "h"(a), "h"(b), "f"(c));
+  return d;
+}
+
+// f16 lambda' table in the gather's thread order: within each 128-column chunk the four columns
+// lane + 32 q (q < 4) of one lane sit together, lamh[t][chunk * 128 + lane * 4 + q] =
+// f16(2^(15 - e_B) lam[t][chunk * 128 + 32 q + lane]), so a thread's four columns of one shift are
+// ONE 8-byte load (a warp: 256 contiguous bytes) instead of four 2-byte loads.
+__global__ void lam_seg_f16_kernel(const float* __restrict__ lam, size_t count, const double* __restrict__ fro2_b,
+                                   unsigned short* __restrict__ out, const double* __restrict__ g_fro2,
+                                   const double* __restrict__ g_kept) {
+  if (g_fro2 != nullptr && !resid_small(g_fro2, g_kept)) return;
+  const float s = ldexpf(1.f, 15 - f16_scale_exp(*fro2_b));
+  const size_t nth = (size_t)gridDim.x * blockDim.x;
+  for (size_t i = blockIdx.x * (size_t)blockDim.x + threadIdx.x; i < count / 4; i += nth) {
+    const size_t chunk = i >> 5, lane = i & 31;  // chunks run through the rows (n % 128 == 0)
+    const float* src = lam + chunk * 128 + lane;
+    uint2 o;
+    o.x = pack_half2(s * src[0], s * src[32]);
+    o.y = pack_half2(s * src[64], s * src[96]);
+    *reinterpret_cast<uint2*>(out + chunk * 128 + lane * 4) = o;
+  }
+}
+__device__ __forceinline__ uint2 ldg_nc_hint_u64(const unsigned short* a, unsigned long long pol) {
+  uint2 v;
+  asm volatile("ld.global.nc.L2::cache_hint.v2.u32 {%0, %1}, [%2], %3;" : "=r"(v.x), "=r"(v.y) : "l"(a), "l"(pol));
+  return v;
+}
+
+template <int TUNE>
+__global__ void __launch_bounds__(kSegThreads, 1)
+    cycle_right_gather_seg_h(const float* __restrict__ X, const int* __restrict__ JA, int ka,
+                             const unsigned short* __restrict__ lamh, const int* __restrict__ J, int k, int n,
+                             int m_rows, int accumulate, float* __restrict__ M, double* __restrict__ msq_partial,
+                             int SW, int row_off, int lam_ld, const double* __restrict__ g_fro2,
+                             const double* __restrict__ g_kept, const double* __restrict__ fro2_b, int force) {
+  if (!force && !resid_small(g_fro2, g_kept)) return;
+  constexpr int R = kSegHR, CPT = 4;
+  extern __shared__ __align__(16) unsigned char smem_raw[];
+  uint4* Xs = reinterpret_cast<uint4*>(smem_raw);  // column m of the segment: rows r0..r0+7 as f16
+  int2* sJT = reinterpret_cast<int2*>(Xs + SW);   // (shift, lambda row), ascending shift
+  __shared__ double red[32];
+  const unsigned long long pol_keep = l2_policy_evict_last(), pol_stream = l2_policy_evict_first();
+  const int e_x = f16_scale_exp(*g_fro2), e_b = f16_scale_exp(*fro2_b);
+  const float sx = ldexpf(1.f, 15 - e_x), inv = ldexpf(1.f, e_x + e_b - 30);
+  for (int t = threadIdx.x; t < k; t += blockDim.x) {
+    const int j = J[t];
+    int rank = 0;
+    for (int u = 0; u < k; ++u) rank += J[u] < j;
+    sJT[rank] = make_int2(j, t);
+  }
+  const int r0 = blockIdx.x * R;
+  const int rows = min(R, m_rows - r0);
+  const int nseg = (int)ceil_div(n, SW);
+  double msq = 0.0;
+  for (int s = 0; s < nseg; ++s) {
+    const int s0 = s * SW, sw = min(SW, n - s0);
+    __syncthreads();  // the previous segment's readers are done (and the sort is visible)
+    // fill: coalesced 16-byte reads of 8 rows, 4 columns per thread step, scaled and packed
+    for (int iv = threadIdx.x; iv < sw / 4; iv += blockDim.x) {
+      float4 buf[R];
+#pragma unroll
+      for (int rr = 0; rr < R; ++rr)
+        buf[rr] = rr < rows ? __ldg(reinterpret_cast<const float4*>(X + (size_t)(r0 + rr) * n + s0) + iv)
+                            : float4{0.f, 0.f, 0.f, 0.f};
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        float e[R];
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) e[rr] = sx * reinterpret_cast<const float*>(&buf[rr])[q];
+        uint4 o;
+        o.x = pack_half2(e[0], e[1]);
+        o.y = pack_half2(e[2], e[3]);
+        o.z = pack_half2(e[4], e[5]);
+        o.w = pack_half2(e[6], e[7]);
+        Xs[iv * 4 + q] = o;
+      }
+    }
+    if (JA != nullptr) {
+      __syncthreads();
+      unsigned short* Xh = reinterpret_cast<unsigned short*>(Xs);
+      for (int e = threadIdx.x; e < rows * ka; e += blockDim.x) {
+        const int rr = e / ka, t = e - rr * ka;
+        int m = (r0 + rr + row_off - JA[t]) % n;
+        if (m < 0) m += n;
+        if (m >= s0 && m < s0 + sw) Xh[(size_t)(m - s0) * R + rr] = 0;
+      }
+    }
+    __syncthreads();
+    const bool last = s == nseg - 1;
+    if (threadIdx.x == 0 && s + 1 < nseg) {  // next segment's rows toward L2 while this one runs
+      const int n1 = min(SW, n - (s0 + SW));
+      for (int rr = 0; rr < rows; ++rr)
+        asm volatile("cp.async.bulk.prefetch.L2.global [%0], %1;" ::"l"(X + (size_t)(r0 + rr) * n + s0 + SW),
+                     "r"((unsigned)(n1 * sizeof(float)))
+                     : "memory");
+    }
+    const int lane = threadIdx.x & 31;
+    constexpr int CW = 32 * CPT;
+    const uint4* xlane = Xs + lane;
+    for (int cw = (threadIdx.x >> 5) * CW; cw < n; cw += (blockDim.x >> 5) * CW) {
+      // interior / boundary runs of the sorted shift table, as in cycle_right_gather_seg
+      auto lower = [&](int v) -> int { return (k <= 256 && (TUNE & 2)) ? count_below(sJT, k, v) : lower_index(sJT, k, v, 0); };
+      auto run = [&](int v, int len, int& first) -> int {
+        v %= n;
+        if (v < 0) v += n;
+        first = lower(v);
+        int cnt;
+        if (v + len <= n) {
+          cnt = lower(v + len) - first;
+        } else {
+          cnt = (k - first) + min(lower(v + len - n), first);
+        }
+        if (first >= k) first -= k;
+        return cnt;
+      };
+      int f_int, f_lo, f_hi;
+      const int c_int = run(s0 - cw, sw - CW + 1, f_int);
+      const int n_blo = run(s0 - CW + 1 - cw, CW - 1, f_lo);
+      const int n_bhi = nseg > 1 ? run(s0 + sw - CW + 1 - cw, CW - 1, f_hi) : 0;
+      // red: a segment that is neither the first of an overwriting pass nor the last adds its
+      // partial sums with fire-and-forget reductions at L2 (no old-value load to wait for); the
+      // last segment needs the final values (||M||^2), so it reads them back (relaxed, from L2:
+      // program order after this thread's own reductions on the same addresses)
+      const bool rmw = s > 0 || accumulate != 0;
+      const bool red = rmw && !last && (TUNE & 1);
+      if (rmw && !red) {
+#pragma unroll
+        for (int q = 0; q < CPT; ++q)
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr)
+            if (rr < rows) asm volatile("prefetch.global.L2 [%0];" ::"l"(M + (size_t)(r0 + rr) * n + cw + 32 * q + lane));
+      }
+      float acc[CPT][R];
+#pragma unroll
+      for (int q = 0; q < CPT; ++q)
+#pragma unroll
+        for (int rr = 0; rr < R; ++rr) acc[q][rr] = 0.f;
+      auto fma_rows = [&](int q, const uint4 x, unsigned short l) {
+        acc[q][0] = fhfma_seg((unsigned short)(x.x & 0xffffu), l, acc[q][0]);
+        acc[q][1] = fhfma_seg((unsigned short)(x.x >> 16), l, acc[q][1]);
+        acc[q][2] = fhfma_seg((unsigned short)(x.y & 0xffffu), l, acc[q][2]);
+        acc[q][3] = fhfma_seg((unsigned short)(x.y >> 16), l, acc[q][3]);
+        acc[q][4] = fhfma_seg((unsigned short)(x.z & 0xffffu), l, acc[q][4]);
+        acc[q][5] = fhfma_seg((unsigned short)(x.z >> 16), l, acc[q][5]);
+        acc[q][6] = fhfma_seg((unsigned short)(x.w & 0xffffu), l, acc[q][6]);
+        acc[q][7] = fhfma_seg((unsigned short)(x.w >> 16), l, acc[q][7]);
+      };
+      auto load_batch = [&](int i0, int (&off)[kSegU], uint2 (&lv)[kSegU]) {
+#pragma unroll
+        for (int u = 0; u < kSegU; ++u) {
+          int i = f_int + i0 + u;
+          i = i >= k ? i - k : i;
+          const bool in = i0 + u < c_int;
+          const int2 jt = sJT[in ? i : f_int];  // broadcast
+          unsigned m = (unsigned)(cw + jt.x);
+          m = min(m, m - (unsigned)n);  // (cw + J) mod n
+          off[u] = in ? (int)(m - (unsigned)s0) : 0;
+          lv[u] = in ? ldg_nc_hint_u64(lamh + (size_t)jt.y * lam_ld + cw + lane * 4, pol_keep) : uint2{0u, 0u};
+        }
+      };
+      auto compute_batch = [&](const int (&off)[kSegU], const uint2 (&lv)[kSegU]) {
+#pragma unroll
+        for (int u = 0; u < kSegU; ++u) {
+          fma_rows(0, xlane[off[u]], (unsigned short)(lv[u].x & 0xffffu));
+          fma_rows(1, xlane[off[u] + 32], (unsigned short)(lv[u].x >> 16));
+          fma_rows(2, xlane[off[u] + 64], (unsigned short)(lv[u].y & 0xffffu));
+          fma_rows(3, xlane[off[u] + 96], (unsigned short)(lv[u].y >> 16));
+        }
+      };
+      {
+        int oA[kSegU], oB[kSegU];
+        uint2 lvA[kSegU], lvB[kSegU];
+        if (c_int > 0) load_batch(0, oA, lvA);
+        for (int i0 = 0; i0 < c_int; i0 += 2 * kSegU) {
+          if (i0 + kSegU < c_int) load_batch(i0 + kSegU, oB, lvB);
+          compute_batch(oA, lvA);
+          if (i0 + kSegU >= c_int) break;
+          if (i0 + 2 * kSegU < c_int) load_batch(i0 + 2 * kSegU, oA, lvA);
+          compute_batch(oB, lvB);
+        }
+      }
+      auto boundary = [&](int first, int cnt) {
+        for (int e = 0; e < cnt; ++e) {
+          int i = first + e;
+          i = i >= k ? i - k : i;
+          const int2 jt = sJT[i];
+          const unsigned short* lrow = lamh + (size_t)jt.y * lam_ld;
+          unsigned short lv[CPT];
+          unsigned l[CPT];
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) {
+            const int c = cw + 32 * q + lane;
+            unsigned m = (unsigned)(c + jt.x);
+            m = min(m, m - (unsigned)n);
+            const unsigned d = m - (unsigned)s0;
+            const bool ok = d < (unsigned)sw;
+            l[q] = ok ? d : 0u;
+            lv[q] = ok ? __ldg(lrow + cw + lane * 4 + q) : (unsigned short)0;
+          }
+#pragma unroll
+          for (int q = 0; q < CPT; ++q) fma_rows(q, Xs[l[q]], lv[q]);
+        }
+      };
+      boundary(f_lo, n_blo);
+      boundary(f_hi, n_bhi);
+      // M (+)= the segment's partial sums, one column of the chunk at a time (8 old values in
+      // flight per thread; the lines were prefetched into L2 at the chunk's start)
+      if (red) {
+#pragma unroll
+        for (int q = 0; q < CPT; ++q)
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr)
+            if (rr < rows) {
+              const float a = acc[q][rr] * inv;
+              red_add(M + (size_t)(r0 + rr) * n + cw + 32 * q + lane, accumulate < 0 ? -a : a);
+            }
+      } else {
+#pragma unroll
+        for (int q = 0; q < CPT; ++q) {
+          float old[R];
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr)
+            old[rr] = (rmw && rr < rows) ? ld_relaxed_f32(M + (size_t)(r0 + rr) * n + cw + 32 * q + lane) : 0.f;
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr)
+            if (rr < rows) {
+              const float a = acc[q][rr] * inv;
+              const float v = (accumulate < 0) ? old[rr] - a : old[rr] + a;
+              stg_hint(M + (size_t)(r0 + rr) * n + cw + 32 * q + lane, v, pol_stream);
+              if (last) msq += (double)v * (double)v;
+            }
+        }
+      }
+    }
   }
   if (msq_partial != nullptr) {
     const double t = block_sum(msq, red);
@@ -1309,21 +1622,85 @@ int right_gather_rows_plain(int n, size_t elem, int k) {
   return r > 0 ? r : right_gather_rows(n, elem, k);
 }
 
+// epilogue / search variant of the segmented gathers (TUNE = 3: red.add epilogue on the middle
+// segments + lane-parallel shift search; 0: read-modify-write everywhere + binary search);
+// APX_SEG_TUNE (fp32/fp64 kernel) and APX_SEGH_TUNE (f16-staged kernel) = 0 / 1 pick one for A/B
+static int seg_tune(int fp32_kernel) {
+  const char* e = getenv(fp32_kernel ? "APX_SEG_TUNE" : "APX_SEGH_TUNE");
+  if (e) return atoi(e) != 0;
+  // same-box A/B at C5 (n = 32768, k = 128): fp32 kernel 60.68 ms (0) vs 60.85 (3) per product --
+  // it sits at 78% of the L1 data pipe either way; f16-staged kernel 52.5 (0) vs 50.1 (3)
+  return fp32_kernel ? 0 : 1;
+}
+
 template <typename T, int R>
 static int right_gather_seg_r(const T* X, const int* JA, int ka, const T* lam, const int* J, int k, int n,
                               int m_rows, int acc, T* M, double* msq_partial, double* xsq_partial, cudaStream_t st,
-                              int row_off = 0, int c_lo = 0, int c_hi = -1, int lam_ld = -1, int out_ld = -1) {
+                              int row_off = 0, int c_lo = 0, int c_hi = -1, int lam_ld = -1, int out_ld = -1,
+                              const double* g_fro2 = nullptr, const double* g_kept = nullptr) {
   if (c_hi < 0) c_hi = n;
   if (lam_ld < 0) lam_ld = n;
   if (out_ld < 0) out_ld = n;
   const int SW = seg_width(n, sizeof(T), k, R);
   const size_t smem = (size_t)gather_pitch(R, sizeof(T)) * SW * sizeof(T) + (size_t)2 * k * sizeof(int);
-  auto kern = cycle_right_gather_seg<T, R>;
+  auto kern = seg_tune(1) ? cycle_right_gather_seg<T, R, 3> : cycle_right_gather_seg<T, R, 0>;
   APX_TRY(set_smem<T>((const void*)kern, smem));
   kern<<<(unsigned)ceil_div(m_rows, R), kSegThreads, smem, st>>>(X, JA, ka, lam, J, k, n, m_rows, acc, M, msq_partial,
-                                                                 xsq_partial, SW, row_off, c_lo, c_hi, lam_ld, out_ld);
+                                                                 xsq_partial, SW, row_off, c_lo, c_hi, lam_ld, out_ld, g_fro2, g_kept);
   APX_LAUNCH_CHECK();
   return OK;
+}
+
+// ---- f16-staged residual gather (K11h) ----
+// APX_SEG_F16: 0 = never (fp32 segmented gather only), 1 = device-side rule (default), 2 = always
+static int seg_f16_mode() {
+  const char* e = getenv("APX_SEG_F16");
+  const int v = e ? atoi(e) : 1;
+  return v < 0 || v > 2 ? 1 : v;
+}
+bool right_gather_seg_f16_ok(int n, size_t elem, int k) {
+  return elem == 4 && seg_f16_mode() != 0 && right_gather_seg_rows(n, elem, k) > 0 && n % (32 * 4) == 0;
+}
+size_t right_gather_seg_f16_ws(int n, int k) { return (size_t)std::max(k, 1) * n * sizeof(unsigned short) + 16; }
+
+// M (+)= (X masked by JA) . Bhat over the segmented path, f16-staged when the residual is small
+// (decided on the device from *fro2_x and *kept_x), else the fp32 segmented gather. msq_partial
+// gets one partial per fp32 row block (right_gather_rows_plain rows); the f16 kernel fills the
+// first ceil(m_rows / 8) of them and the rest stay zero.
+int launch_cycle_right_gather_seg_f16(const float* X, const int* JA, int ka, const float* lam, const int* J, int k,
+                                      int n, int m_rows, int accumulate, float* M, double* msq_partial,
+                                      cudaStream_t st, int row_off, unsigned short* lamh, const double* fro2_x,
+                                      const double* kept_x, const double* fro2_b) {
+  const int mode = seg_f16_mode();
+  APX_REQUIRE(right_gather_seg_f16_ok(n, 4, k) && JA != nullptr && lamh != nullptr, "seg f16 gather: bad call");
+  const int R32 = right_gather_seg_rows(n, 4, k);
+  if (msq_partial) APX_CUDA(cudaMemsetAsync(msq_partial, 0, ceil_div(m_rows, R32) * sizeof(double), st));
+  const size_t cnt = (size_t)k * n;
+  lam_seg_f16_kernel<<<(unsigned)std::min<size_t>(ceil_div(cnt / 4, (size_t)256), (size_t)kNumSMs * 8), 256, 0, st>>>(
+      lam, cnt, fro2_b, lamh, mode == 2 ? nullptr : fro2_x, kept_x);
+  APX_LAUNCH_CHECK();
+  const size_t budget = 216 * 1024 - (size_t)std::max(k, 1) * sizeof(int2);
+  const int64_t maxw = (int64_t)(budget / 16) & ~int64_t(127);
+  const int64_t nseg = ceil_div(n, maxw);
+  const int SW = (int)(ceil_div(ceil_div(n, nseg), 128) * 128);
+  const size_t smem = (size_t)SW * 16 + (size_t)k * sizeof(int2);
+  auto kern = seg_tune(0) ? cycle_right_gather_seg_h<3> : cycle_right_gather_seg_h<0>;
+  APX_TRY(set_smem<float>((const void*)kern, smem));
+  kern<<<(unsigned)ceil_div(m_rows, kSegHR), kSegThreads, smem, st>>>(
+      X, JA, ka, lamh, J, k, n, m_rows, accumulate, M, msq_partial, SW, row_off, n, fro2_x, kept_x, fro2_b,
+      mode == 2 ? 1 : 0);
+  APX_LAUNCH_CHECK();
+  if (mode == 2) return OK;
+#define APX_SEGF(RV)                                                                                               \
+  return right_gather_seg_r<float, RV>(X, JA, ka, lam, J, k, n, m_rows, accumulate, M, msq_partial, nullptr, st, \
+                                       row_off, 0, -1, -1, -1, fro2_x, kept_x)
+  switch (R32) {
+    case 2: APX_SEGF(2);
+    case 4: APX_SEGF(4);
+    case 6: APX_SEGF(6);
+    default: APX_SEGF(8);
+  }
+#undef APX_SEGF
 }
 
 // lam: the column-aligned table (cycle_extract<T, true>), k x n, or (lam_padded) ceil(k/8)*8 x n

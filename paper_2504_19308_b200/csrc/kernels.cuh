@@ -35,6 +35,13 @@ int launch_cycle_right_gather(const T* X, const int* JA, int ka, const T* lam, c
                               bool lam_padded = false, int max_ctas = 0, int* ticket = nullptr, int col_chunks = 1,
                               int tf32_operands = 0, int* ready = nullptr, bool x_early = false,
                               int row_off = 0, const int* skip_if = nullptr);
+// f16-staged segmented gather of a small masked residual (cycle.cu K11h; fp32, large n)
+bool right_gather_seg_f16_ok(int n, size_t elem, int k);
+size_t right_gather_seg_f16_ws(int n, int k);
+int launch_cycle_right_gather_seg_f16(const float* X, const int* JA, int ka, const float* lam, const int* J, int k,
+                                      int n, int m_rows, int accumulate, float* M, double* msq_partial,
+                                      cudaStream_t st, int row_off, unsigned short* lamh, const double* fro2_x,
+                                      const double* kept_x, const double* fro2_b);
 // ---- row-sharded cycle product (local rows [0, m) of an n x n operand = global rows row_off + r)
 template <typename T>
 int launch_cycle_energies_rows(const T* A, int m, int row_off, int n, double* energies, double* partial,

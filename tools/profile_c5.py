@@ -11,8 +11,9 @@ import paper_2504_19308_b200 as P  # noqa: E402
 from devgen import c5_operand  # noqa: E402
 
 n = int(os.environ.get("C5_N", 32768))
-A, _ = c5_operand(n, 128, 32, seed=5, operand=0)
-B, _ = c5_operand(n, 128, 32, seed=5, operand=1)
+r = int(os.environ.get("C5_R", 32))  # circulant terms; 0 = cycle-dominated operands (f16 residual gather)
+A, _ = c5_operand(n, 128, r, seed=5, operand=0)
+B, _ = c5_operand(n, 128, r, seed=5, operand=1)
 torch.cuda.synchronize()
 P.cycle_product_device(A, B, 128, 128, 1)
 torch.cuda.synchronize()
