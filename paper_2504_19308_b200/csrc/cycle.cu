@@ -1134,6 +1134,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
         const int rr = e / ka, t = e - rr * ka;
         int m = (r0 + rr + row_off - JA[t]) % n;
         if (m < 0) m += n;
+        APX_DCHECK(m >= 0 && m < n);
         if (m >= s0 && m < s0 + sw) Xh[(size_t)(m - s0) * R + rr] = 0;
       }
     }
@@ -1213,6 +1214,7 @@ __global__ void __launch_bounds__(kSegThreads, 1)
       auto compute_batch = [&](const int (&off)[kSegU], const uint2 (&lv)[kSegU]) {
 #pragma unroll
         for (int u = 0; u < kSegU; ++u) {
+          APX_DCHECK(off[u] >= 0 && off[u] + 96 + lane < sw);
           fma_rows(0, xlane[off[u]], (unsigned short)(lv[u].x & 0xffffu));
           fma_rows(1, xlane[off[u] + 32], (unsigned short)(lv[u].x >> 16));
           fma_rows(2, xlane[off[u] + 64], (unsigned short)(lv[u].y & 0xffffu));
@@ -1250,7 +1252,10 @@ __global__ void __launch_bounds__(kSegThreads, 1)
             lv[q] = ok ? __ldg(lrow + cw + lane * 4 + q) : (unsigned short)0;
           }
 #pragma unroll
-          for (int q = 0; q < CPT; ++q) fma_rows(q, Xs[l[q]], lv[q]);
+          for (int q = 0; q < CPT; ++q) {
+            APX_DCHECK(l[q] < (unsigned)sw);
+            fma_rows(q, Xs[l[q]], lv[q]);
+          }
         }
       };
       boundary(f_lo, n_blo);

@@ -23,6 +23,19 @@ def case(name, fn):
     print("ok", name, flush=True)
 
 
+if os.environ.get("SAN_SEG"):
+    # large-n segmented gathers only (fp32 n = 13312 > 12800: K11s, and its f16-staged variant K11h
+    # forced and under the device-side rule); a separate, slower run: SAN_SEG=1
+    n = 13312
+    As, _ = G.cycle_operand(n, 8, 1, dev, torch.float32)
+    Bs, _ = G.cycle_operand(n, 8, 2, dev, torch.float32)
+    for mode in ("0", "2", "1"):
+        os.environ["APX_SEG_F16"] = mode
+        case(f"segmented cycle product fp32 n={n} k=8 APX_SEG_F16={mode}",
+             lambda: P.cycle.cycle_product_device(As, Bs, 8, 8, 1))
+    print("all cases ok")
+    sys.exit(0)
+
 A, _ = G.cycle_operand(256, 20, 1, dev)
 B, _ = G.cycle_operand(256, 20, 2, dev)
 for order in (0, 1):
