@@ -720,12 +720,17 @@ static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int
                                p.ticket + 3, f16_mode, hi));
   }
   stage_mark(5, hi);
+  // APX_W0_EARLY=1: the low-priority chain (W0 = Bm.B ...) starts once Bm exists, beside the dA
+  // pass, instead of behind it (tuning knob; APX_W0_SMS: the SM budget W0's K split is sized for)
+  static const int w0_early = getenv("APX_W0_EARLY") ? atoi(getenv("APX_W0_EARLY")) : 0;
+  static const int w0_sms = getenv("APX_W0_SMS") ? atoi(getenv("APX_W0_SMS")) : 0;
+  cudaEvent_t da_ready = ss->join;  // reused: recorded again at the end of lo
+  if (w0_early) APX_CUDA(cudaEventRecord(da_ready, hi));
   // dA as scaled f16 (or, in the fallback, as fp32 into M, which is free until the gather)
   APX_TRY(umma_tma_gemm(2 | 32, 128, Q, l, Bm, n, const_cast<float*>(A), n, 0, n, n, l, 1, 0, nullptr, 0, 1, hi,
                         nullptr, nullptr, 0, nullptr, nullptr, p.dAh, scal + APX_S_FRO2_A, p.ticket + 3, M));
   stage_mark(10, hi);
-  cudaEvent_t da_ready = ss->join;  // reused: recorded again at the end of lo
-  APX_CUDA(cudaEventRecord(da_ready, hi));
+  if (!w0_early) APX_CUDA(cudaEventRecord(da_ready, hi));
   // ---- hi: the f16 gather M = dA . Bhat -------------------------------------------------------------
   APX_CUDA(cudaStreamWaitEvent(hi, ss->b_ready, 0));
   stage_mark(11, hi);
@@ -744,7 +749,7 @@ static int run_mixed_f32_resid(const float* A, const float* B, int n, int l, int
   APX_CUDA(cudaStreamWaitEvent(lo, da_ready, 0));
   const int wblocks = (int)ceil_div(l, right_gather_rows(n, sizeof(float), kc));
   const int wchunks = std::max(1, std::min(8, (int)ceil_div(5 * free_sms, wblocks)));
-  APX_TRY(UmmaStages::bm_times_db(B, Bm, W, part, n, l, nullptr, 0, lo, free_sms));
+  APX_TRY(UmmaStages::bm_times_db(B, Bm, W, part, n, l, nullptr, 0, lo, w0_sms > 0 ? w0_sms : free_sms));
   stage_mark(9, lo);
   // W0 - Bm.Bhat_tf32 + Bm.Bhat as ONE gather over lambda - tf32(lambda): Bm is TF32-exact (the
   // finalize rounded it), so the TF32 and fp32 gathers differ only in lambda's truncated bits (two
