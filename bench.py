@@ -793,7 +793,10 @@ def run_c5_rows(args, rank, world, local_rank):
     ms_max = max_over_ranks(ms, world, dev)
     sel = res["r"]["sel_a"].to(torch.int64)
     sels = [torch.empty_like(sel) for _ in range(world)]
-    dist.all_gather(sels, sel)
+    if world > 1:
+        dist.all_gather(sels, sel)
+    else:
+        sels = [sel]
     if rank == 0:
         pk = pipe_peaks()
         t_step = ms_max / args.steps * 1e-3

@@ -156,7 +156,8 @@ def ordered_sum(t, group=None):
     NCCL groups gather into one buffer (ncclAllGather); other backends (gloo) gather a list."""
     import torch.distributed as dist
 
-    world = dist.get_world_size(group)
+    # no process group: a single-process run is a world of one (bench.py --gpus 1 --shard rows)
+    world = dist.get_world_size(group) if dist.is_initialized() else 1
     if world == 1:
         return t
     flat = t.contiguous().view(-1)
@@ -312,7 +313,9 @@ def _a2a_rows(T1, M_rows, plan, rank, group=None):
     in_splits = [(b - a) * w for (a, b), _ in plan]
     out_splits = [m * (d - c) for _, (c, d) in plan]
     recv = torch.empty(sum(out_splits), dtype=T1.dtype, device=T1.device)
-    if dist.get_backend(group) == "nccl":
+    if not dist.is_initialized():  # a world of one: the piece stays
+        recv.copy_(send)
+    elif dist.get_backend(group) == "nccl":
         dist.all_to_all_single(torch.view_as_real(recv).view(-1), torch.view_as_real(send).view(-1),
                                [2 * x for x in out_splits], [2 * x for x in in_splits], group=group)
     else:  # gloo has no alltoall: pairwise point-to-point exchanges (the grouped send/recv form)
@@ -337,7 +340,7 @@ def circulant_product_rows(A, B, k: int, order: int, group=None, out=None):
     """This rank's rows of the circulant product (the exchanges over torch.distributed)."""
     import torch.distributed as dist
 
-    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    world, rank = (dist.get_world_size(group), dist.get_rank(group)) if dist.is_initialized() else (1, 0)
     gen = circulant_rows_steps(A, B, k, order, world, rank, out)
     try:
         req = next(gen)

@@ -368,3 +368,17 @@ def test_row_sharded_sfft_protocol_gloo():
     assert fro2 == pytest.approx(float(np.sum(A ** 2)), rel=1e-12)
     assert res2 == pytest.approx(rep["norm_da"] ** 2, rel=1e-12)
     assert m2 == pytest.approx(float(np.sum(np.abs(M) ** 2)), rel=1e-12)
+
+
+def test_ordered_sum_without_process_group_is_identity():
+    """A single-process run (no torch.distributed group) is a world of one: ordered_sum returns its
+    argument untouched instead of raising (bench.py --gpus 1 --shard rows)."""
+    import torch
+    import torch.distributed as dist
+    from paper_2504_19308_b200 import sharded as S
+
+    assert not dist.is_initialized()
+    t = torch.arange(6, dtype=torch.float64).reshape(2, 3)
+    ref = t.clone()
+    assert S.ordered_sum(t) is t
+    assert torch.equal(t, ref)
