@@ -131,6 +131,43 @@ def gather_capture():
             "l1_datapath_frac_active_sms": pipe * 148.0 / min(148.0, grid)}
 
 
+# committed `ncu --set full` summaries of each config's dominant kernels (tools/ncu_summary.py format)
+NCU_FILES = {
+    "c1": ["profiles/r02c_cqr2_c1_ncu.txt"],
+    "c2": ["profiles/r02e_c2_cycle_right_gather_ncu.txt", "profiles/r02e_c2_cycle_left_gather_ncu.txt"],
+    "c3": ["profiles/r02e_c3_circ_left2_r16_ncu.txt", "profiles/r02e_c3_circ_right2_r16_ncu.txt",
+           "profiles/r02e_c3_circ_decompose_r16_ncu.txt"],
+    "c5": ["profiles/r01_seg_gather_ncu.txt"],
+    "c5c": ["profiles/r02c_fft4_pass1_r16_ncu.txt", "profiles/r02c_fft4_pass2_r16_ncu.txt"],
+}
+
+
+def ncu_limiters(cfg):
+    """Per dominant kernel of `cfg`: which unit the committed ncu capture shows it bound by (L1
+    data pipe, DRAM, FP64 / FMA pipe utilisation as fractions of their peaks). Static evidence
+    read from profiles/, not a measurement of this run."""
+    out = []
+    for rel_path in NCU_FILES.get(cfg, []):
+        path = os.path.join(ROOT, rel_path)
+        if not os.path.exists(path):
+            continue
+        vals, name = {}, None
+        for line in open(path):
+            if line.startswith("Kernel Name"):
+                name = line[len("Kernel Name"):].strip().split("(")[0].replace("void ", "")
+            m = re.match(r"(\S+)\s+([0-9.]+)\s*(\S*)", line)
+            if m:
+                vals[m.group(1)] = float(m.group(2))
+        pct = lambda k: (vals[k] / 100.0) if k in vals else None  # noqa: E731
+        out.append({"kernel": name,
+                    "l1_data_pipe_frac": pct("l1tex__data_pipe_lsu_wavefronts.avg.pct_of_peak_sustained_elapsed"),
+                    "dram_frac": pct("gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed"),
+                    "fp64_pipe_frac": pct("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
+                    "fma_pipe_frac": pct("sm__pipe_fma_cycles_active.avg.pct_of_peak_sustained_active"),
+                    "source": rel_path})
+    return out or None
+
+
 def host_info():
     """CPU model, core count and BLAS threading of the host the CPU leg runs on."""
     model = None
@@ -731,6 +768,7 @@ def run_secondary(args, rank, world, local_rank):
         ach = st["bytes"] / t_step / 1e9
         roof = {"bound": "hbm", "kernel": "whole product", "achieved": ach, "peak": hbm, "unit": "GB/s",
                 "frac": ach / hbm, "traffic": None, "peak_kind": hbm_kind, "alg_bytes_per_step": st["bytes"]}
+    roof["ncu_limiters"] = ncu_limiters(cfg)
     line = {"metric": METRIC, "value": job_throughput(args.steps * st["units"], world, ms_max * 1e-3),
             "unit": "products/s", "n_gpus": world, "steps": args.steps, "warmup": args.warmup,
             "ms_per_step": ms_max / args.steps, "higher_is_better": True, "scaling": "weak",
