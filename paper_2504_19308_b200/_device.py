@@ -7,6 +7,8 @@ used by bench.py and by callers that keep data resident in HBM).
 
 from __future__ import annotations
 
+import os
+
 import numpy as np
 import torch
 
@@ -132,8 +134,8 @@ def to_user(t: torch.Tensor, host, out=None):
         out.copy_(t, non_blocking=True)
         torch.cuda.current_stream().synchronize()
         return out
-    if t.numel() * t.element_size() < _PIN_MIN_BYTES:
-        return t.cpu().numpy()
+    if t.numel() * t.element_size() < _PIN_MIN_BYTES or os.environ.get("APX_PINNED_RESULTS", "1") == "0":
+        return t.cpu().numpy()  # (APX_PINNED_RESULTS=0: callers that hoard results keep them pageable)
     # large results land in a pinned buffer (async DMA at PCIe rate instead of a pageable copy);
     # the numpy array returned is a view that keeps it alive and hands it back to torch's pinned
     # cache when the caller drops it
